@@ -1,0 +1,163 @@
+/*
+ * pmg.h -- C ABI of libpmg.so, the B200 (sm_100a) implementation of the
+ * pressure-correction solve path of arXiv:1307.2036 (reference package
+ * `panelmg`, /root/reference/pkg/src/panelmg).
+ *
+ * Every entry point takes plain pointers and sizes; device pointers are
+ * CUDA global-memory addresses, `stream` is a cudaStream_t passed as
+ * void* (NULL = legacy default stream).  Every call returns 0 on success
+ * or a negative status; pmg_last_error() returns the message of the most
+ * recent failure on the calling thread.  Calls are stream-ordered and
+ * never synchronise the host, except where a scalar is returned to a
+ * HOST pointer (documented per call).
+ *
+ * Field layout on the device (one "part" = the columns one worker owns):
+ * red/black split, horizontal index fastest.  Cell (i, j, k) of a part
+ * with local i in [-1, nx], j in [-1, ny] (-1 and nx/ny are halo) lives at
+ *
+ *   field[c * cstride + k * plane + (j + 1) * pitch + PMG_OFF + (i >> 1)]
+ *   with colour c = (i + j + parity) & 1, parity = (i0 + j0) & 1,
+ *
+ * i.e. red cells ((i+j) even in GLOBAL indices, reference smoother.py:66)
+ * and black cells are two separate [nz][ny+2][pitch] arrays.  Use
+ * pmg_level_layout() for pitch/plane/cstride and pmg_level_field_doubles()
+ * for the allocation size.
+ */
+#ifndef PMG_H
+#define PMG_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMG_OK 0
+#define PMG_ERR_VALUE -1    /* maps to ValueError (shape / layout / config)     */
+#define PMG_ERR_CUDA -2     /* CUDA runtime failure -> RuntimeError              */
+#define PMG_ERR_PIVOT -3    /* zero pivot -> ZeroPivotError (tridiag.py:20)      */
+#define PMG_ERR_INTERNAL -4
+
+#define PMG_OFF 4           /* offset (doubles) of h = 0 inside a row            */
+
+typedef struct pmg_level pmg_level;   /* opaque */
+
+/*
+ * One grid level of one part.  Replaces the coefficient set-up of
+ * PanelOperator.__init__ (stencil.py:90-114), GridFactors/build_factors
+ * (geometry.py:141-240) and the pivot factorisation of _Block
+ * (smoother.py:89-99).  2-D factor arrays are HOST pointers covering the
+ * part's owned columns, stored with j (y) slowest:
+ *   wx   [ny][nx+1]   wx[j][i]  = face between local columns i-1 and i
+ *   wy   [ny+1][nx]   wy[j][i]  = face between local rows j-1 and j
+ *   av, vh, sumw [ny][nx]
+ * 1-D arrays: dr[nz], vprof[nz+1], volprof[nz].  Arrays are copied; if
+ * every 2-D array is constant the level runs the uniform-coefficient
+ * kernels (1-D diagonal / pivot tables, reference arithmetic order).
+ */
+typedef struct pmg_level_desc {
+    int nx, ny, nz;            /* owned columns of this part, vertical cells   */
+    int i0, j0;                /* global origin of the part                    */
+    double omega2;             /* omega^2                  (stencil.py:101)   */
+    double vcoef;              /* omega^2 * lambda^2       (stencil.py:102)   */
+    const double *dr, *vprof, *volprof;
+    const double *wx, *wy, *av, *vh, *sumw;
+} pmg_level_desc;
+
+int pmg_version(void);
+const char *pmg_last_error(void);
+int pmg_device_sm_count(int device, int *out);
+
+int pmg_level_create(const pmg_level_desc *desc, pmg_level **out);
+int pmg_level_destroy(pmg_level *lvl);
+long long pmg_level_field_doubles(const pmg_level *lvl);
+int pmg_level_layout(const pmg_level *lvl, int *pitch, long long *plane,
+                     long long *cstride, int *parity, int *uniform);
+/* copy of the 1-D tables the uniform kernels use (diag[nz], band[nz+1],
+ * invd[nz]); fails with PMG_ERR_VALUE on a variable-coefficient level. */
+int pmg_level_tables(const pmg_level *lvl, double *diag, double *band, double *invd);
+/* pivot table of a variable-coefficient level: computes the per-column
+ * invd of smoother.py:93-99 into the level (device, field layout).
+ * Called automatically on first use; exposed for set-up timing. */
+int pmg_level_prepare(pmg_level *lvl, void *stream);
+
+/* ---- layout conversion: reference (nx, ny, nz) C-order, k fastest
+ *      (field.py:3-10 owned block) <-> device split layout -------------- */
+int pmg_from_ref_layout(const pmg_level *lvl, const double *src_dev, double *field,
+                        void *stream);
+int pmg_to_ref_layout(const pmg_level *lvl, const double *field, double *dst_dev,
+                      void *stream);
+
+/* ---- operator: PanelOperator.apply / residual (stencil.py:127-165) --- */
+/* out = A u on owned cells; u halo must be current. */
+int pmg_apply(const pmg_level *lvl, const double *u, double *out, void *stream);
+/* r = f - A u.  r may be NULL (norm only).  If norm2_dev != NULL,
+ * norm2_dev[0] = sum of r^2 over owned cells (fixed reduction order;
+ * scratch holds pmg_partials_size() doubles). */
+int pmg_residual(const pmg_level *lvl, const double *f, const double *u, double *r,
+                 double *scratch, double *norm2_dev, void *stream);
+/* q = A p and dot_dev[0] = p.q over owned cells (CG, krylov.py:139-140). */
+int pmg_apply_dot(const pmg_level *lvl, const double *p, double *q, double *scratch,
+                  double *dot_dev, void *stream);
+/* residual fused with the children-sum restriction (multigrid.py:278-282):
+ * coarse_f = R (f - A u), r never stored. */
+int pmg_residual_restrict(const pmg_level *fine, const pmg_level *coarse,
+                          const double *f, const double *u, double *coarse_f,
+                          void *stream);
+
+/* ---- line smoother: LineSmoother.half_sweep (smoother.py:122-182) ---- */
+int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
+                   double rho, int zero_start, int neighbors_zero, double post_scale,
+                   void *stream);
+
+/* ---- transfers (multigrid.py:209-268) ------------------------------- */
+/* coarse = weight * sum of the 4 children (weight 1: V-cycle, 0.25: mean) */
+int pmg_restrict(const pmg_level *fine, const pmg_level *coarse, const double *fine_f,
+                 double *coarse_f, double weight, void *stream);
+/* fine (+)= P coarse (9-3-3-1 bilinear); coarse halo incl. corners current.
+ * add = 0: overwrite owned cells, add = 1: u += P e (multigrid.py:287-290). */
+int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
+                double *fine_u, int add, void *stream);
+
+/* ---- halos (partition.py:158-191) ----------------------------------- */
+/* Fill the whole halo ring of a part that is its own neighbour (one worker
+ * per direction): periodic_x/y wrap, otherwise mirror the adjacent owned
+ * value.  Two-phase semantics incl. corners. */
+int pmg_halo_self(const pmg_level *lvl, double *field, int periodic_x, int periodic_y,
+                  void *stream);
+/* Pack / unpack one face strip (both colours, all k) for an exchange with
+ * another part.  face: 0 = -x (i = 0), 1 = +x (i = nx-1), 2 = -y (j = 0),
+ * 3 = +y (j = ny-1).  x faces span j in [0, ny); y faces span i in
+ * [-1, nx] (extended range: corners, phase 2 of partition.py:181-190).
+ * Buffer length: pmg_face_doubles(). unpack writes the halo strip on the
+ * same side (face 0 -> i = -1, ...); mirror = 1 copies the part's own
+ * adjacent owned strip instead of buf (physical boundary). */
+long long pmg_face_doubles(const pmg_level *lvl, int face);
+int pmg_pack_face(const pmg_level *lvl, const double *field, int face, double *buf,
+                  void *stream);
+int pmg_unpack_face(const pmg_level *lvl, double *field, int face, const double *buf,
+                    int mirror, void *stream);
+
+/* ---- reductions and vector updates (partition.py:138-155, 267-286) -- */
+/* scratch size (doubles) every reduction entry point may use */
+long long pmg_partials_size(void);
+/* out_dev[0] = a.b over owned cells (deterministic order) */
+int pmg_dot(const pmg_level *lvl, const double *a, const double *b, double *scratch,
+            double *out_dev, void *stream);
+/* full-allocation BLAS-1 (halo included, like DistField.add_scaled):
+ * y = y + a x ; y = x + b y */
+int pmg_axpy(long long n, double a, const double *x, double *y, void *stream);
+int pmg_xpby(long long n, const double *x, double b, double *y, void *stream);
+/* CG update (krylov.py:143-146) fused: u += alpha p; r -= alpha q
+ * (full allocation) and rr_dev[0] = ||r||^2 over owned cells.  alpha is
+ * read from DEVICE memory as alpha_num[0] / alpha_den[0] so the step
+ * needs no host round trip. */
+int pmg_cg_update(const pmg_level *lvl, const double *alpha_num, const double *alpha_den,
+                  const double *p, const double *q, double *u, double *r,
+                  double *scratch, double *rr_dev, void *stream);
+/* p = z + (beta_num[0]/beta_den[0]) p over the full allocation. */
+int pmg_cg_direction(long long n, const double *beta_num, const double *beta_den,
+                     const double *z, double *p, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMG_H */

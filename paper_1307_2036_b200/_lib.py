@@ -1,0 +1,113 @@
+"""ctypes binding of libpmg.so (include/pmg.h).
+
+There is no CPU fallback: importing the solver modules without the
+built library, or calling a kernel without a CUDA device, raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("PMG_LIB", os.path.join(_HERE, "libpmg.so"))
+
+PMG_OK = 0
+PMG_ERR_VALUE = -1
+PMG_ERR_CUDA = -2
+PMG_ERR_PIVOT = -3
+OFF = 4
+
+
+class LevelDesc(C.Structure):
+    _fields_ = [
+        ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+        ("i0", C.c_int), ("j0", C.c_int),
+        ("omega2", C.c_double), ("vcoef", C.c_double),
+        ("dr", C.c_void_p), ("vprof", C.c_void_p), ("volprof", C.c_void_p),
+        ("wx", C.c_void_p), ("wy", C.c_void_p), ("av", C.c_void_p),
+        ("vh", C.c_void_p), ("sumw", C.c_void_p),
+    ]
+
+
+_P = C.c_void_p
+_D = C.c_double
+_I = C.c_int
+_LL = C.c_longlong
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "pmg_version": (_I, []),
+    "pmg_last_error": (C.c_char_p, []),
+    "pmg_device_sm_count": (_I, [_I, C.POINTER(_I)]),
+    "pmg_level_create": (_I, [C.POINTER(LevelDesc), C.POINTER(_P)]),
+    "pmg_level_destroy": (_I, [_P]),
+    "pmg_level_field_doubles": (_LL, [_P]),
+    "pmg_level_layout": (_I, [_P, C.POINTER(_I), C.POINTER(_LL), C.POINTER(_LL),
+                              C.POINTER(_I), C.POINTER(_I)]),
+    "pmg_level_tables": (_I, [_P, _P, _P, _P]),
+    "pmg_level_prepare": (_I, [_P, _P]),
+    "pmg_from_ref_layout": (_I, [_P, _P, _P, _P]),
+    "pmg_to_ref_layout": (_I, [_P, _P, _P, _P]),
+    "pmg_apply": (_I, [_P, _P, _P, _P]),
+    "pmg_residual": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "pmg_apply_dot": (_I, [_P, _P, _P, _P, _P, _P]),
+    "pmg_residual_restrict": (_I, [_P, _P, _P, _P, _P, _P]),
+    "pmg_half_sweep": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _P]),
+    "pmg_restrict": (_I, [_P, _P, _P, _P, _D, _P]),
+    "pmg_prolong": (_I, [_P, _P, _P, _P, _I, _P]),
+    "pmg_halo_self": (_I, [_P, _P, _I, _I, _P]),
+    "pmg_face_doubles": (_LL, [_P, _I]),
+    "pmg_pack_face": (_I, [_P, _P, _I, _P, _P]),
+    "pmg_unpack_face": (_I, [_P, _P, _I, _P, _I, _P]),
+    "pmg_partials_size": (_LL, []),
+    "pmg_dot": (_I, [_P, _P, _P, _P, _P, _P]),
+    "pmg_axpy": (_I, [_LL, _D, _P, _P, _P]),
+    "pmg_xpby": (_I, [_LL, _P, _D, _P, _P]),
+    "pmg_cg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "pmg_cg_direction": (_I, [_LL, _P, _P, _P, _P, _P]),
+}
+
+
+class PivotError(ArithmeticError):
+    pass
+
+
+_lib = None
+
+
+def load():
+    """Load libpmg.so (built by ``__graft_entry__.build()``); raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"libpmg.so not found at {LIB_PATH}: build it with "
+            "`python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str = ""):
+    if rc == PMG_OK:
+        return
+    msg = load().pmg_last_error().decode(errors="replace")
+    if rc == PMG_ERR_VALUE:
+        raise ValueError(f"{what}: {msg}")
+    if rc == PMG_ERR_PIVOT:
+        from .tridiag import ZeroPivotError
+        raise ZeroPivotError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg}")
+
+
+def call(name: str, *args):
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+    return rc

@@ -1,0 +1,388 @@
+// libpmg C ABI (include/pmg.h): level set-up and the extern "C" entry points.
+//
+// Host-side coefficient tables are computed here in the reference's
+// expression order (stencil.py:105-109, smoother.py:93-99); the host code is
+// compiled with -ffp-contract=off so no FMA contraction changes a rounding.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pmg_common.cuh"
+
+namespace pmg {
+cudaError_t launch_apply(const Lvl &, const double *, const double *, double *, int, double *,
+                         int *, cudaStream_t);
+cudaError_t launch_finalize(const double *, int, double *, cudaStream_t);
+cudaError_t launch_residual_restrict(const Lvl &, const Lvl &, const double *, const double *,
+                                     double *, cudaStream_t);
+cudaError_t launch_half_sweep(const Lvl &, double *, const double *, int, double, int, int,
+                              double, cudaStream_t);
+cudaError_t launch_invd(const Lvl &, double *, cudaStream_t);
+cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, double,
+                            cudaStream_t);
+cudaError_t launch_prolong(const Lvl &, const Lvl &, const double *, double *, int, cudaStream_t);
+cudaError_t launch_halo_self(const Lvl &, double *, int, int, cudaStream_t);
+int face_len(const Lvl &, int);
+cudaError_t launch_pack(const Lvl &, const double *, int, double *, cudaStream_t);
+cudaError_t launch_unpack(const Lvl &, double *, int, const double *, int, cudaStream_t);
+cudaError_t launch_dot(const Lvl &, const double *, const double *, double *, int *, cudaStream_t);
+cudaError_t launch_axpy(long long, double, const double *, double *, cudaStream_t);
+cudaError_t launch_xpby(long long, const double *, double, double *, cudaStream_t);
+cudaError_t launch_cg_direction(long long, const double *, const double *, const double *,
+                                double *, cudaStream_t);
+cudaError_t launch_cg_update(const Lvl &, const double *, const double *, const double *,
+                             const double *, double *, double *, double *, int *, cudaStream_t);
+cudaError_t launch_from_ref(const Lvl &, const double *, double *, cudaStream_t);
+cudaError_t launch_to_ref(const Lvl &, const double *, double *, cudaStream_t);
+}  // namespace pmg
+
+using namespace pmg;
+
+struct pmg_level {
+    Lvl L;
+    int i0, j0;
+    std::vector<double> h_diag, h_band, h_invd;   // uniform tables (host copy)
+    std::vector<void *> owned;                    // device allocations to free
+    double *invd_field = nullptr;                 // variable: per-cell pivots
+    bool prepared = false;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+static int cuda_fail(cudaError_t e, const char *where) {
+    return fail(PMG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define PMG_CHECK_LVL(l)                                                     \
+    do {                                                                     \
+        if (!(l)) return fail(PMG_ERR_VALUE, "null level handle");           \
+    } while (0)
+
+#define PMG_CUDA(call, where)                                                \
+    do {                                                                     \
+        cudaError_t e_ = (call);                                             \
+        if (e_ != cudaSuccess) return cuda_fail(e_, where);                  \
+    } while (0)
+
+static cudaError_t upload(pmg_level *lv, const double *h, size_t n, const double **dst) {
+    void *d = nullptr;
+    cudaError_t e = cudaMalloc(&d, n * sizeof(double) + 8);
+    if (e != cudaSuccess) return e;
+    lv->owned.push_back(d);
+    e = cudaMemcpy(d, h, n * sizeof(double), cudaMemcpyHostToDevice);
+    *dst = (const double *)d;
+    return e;
+}
+
+static bool all_equal(const double *a, size_t n) {
+    for (size_t t = 1; t < n; ++t)
+        if (a[t] != a[0]) return false;
+    return true;
+}
+
+extern "C" {
+
+int pmg_version(void) { return 1; }
+
+const char *pmg_last_error(void) { return g_err.c_str(); }
+
+int pmg_device_sm_count(int device, int *out) {
+    PMG_CUDA(cudaDeviceGetAttribute(out, cudaDevAttrMultiProcessorCount, device), "sm count");
+    return PMG_OK;
+}
+
+int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
+    if (!d || !out) return fail(PMG_ERR_VALUE, "null argument");
+    if (d->nx < 1 || d->ny < 1 || d->nz < 1)
+        return fail(PMG_ERR_VALUE, "level needs nx, ny, nz >= 1");
+    if (!d->dr || !d->vprof || !d->volprof || !d->wx || !d->wy || !d->av || !d->vh || !d->sumw)
+        return fail(PMG_ERR_VALUE, "missing factor array");
+    const int nx = d->nx, ny = d->ny, nz = d->nz;
+    auto *lv = new pmg_level();
+    Lvl &L = lv->L;
+    std::memset(&L, 0, sizeof(L));
+    L.nx = nx;
+    L.ny = ny;
+    L.nz = nz;
+    // row: h in [-1, nx>>1] at OFF-1 .. OFF+(nx>>1); pitch multiple of 8 doubles
+    const int need = OFF + (nx >> 1) + 1;
+    L.pitch = (need + 7) / 8 * 8;
+    L.plane = (long long)(ny + 2) * L.pitch;
+    L.cstride = (long long)nz * L.plane;
+    L.par = (d->i0 + d->j0) & 1;
+    L.omega2 = d->omega2;
+    L.vcoef = d->vcoef;
+    lv->i0 = d->i0;
+    lv->j0 = d->j0;
+
+    const size_t n2 = (size_t)nx * ny;
+    const bool uni = all_equal(d->wx, (size_t)ny * (nx + 1)) &&
+                     all_equal(d->wy, (size_t)(ny + 1) * nx) && all_equal(d->av, n2) &&
+                     all_equal(d->vh, n2) && all_equal(d->sumw, n2);
+    L.uniform = uni ? 1 : 0;
+    std::vector<double> drw(nz);
+    for (int k = 0; k < nz; ++k) drw[k] = d->omega2 * d->dr[k];   // stencil.py:103
+    cudaError_t e;
+    if ((e = upload(lv, drw.data(), nz, &L.drw)) != cudaSuccess ||
+        (e = upload(lv, d->vprof, nz + 1, &L.vprof)) != cudaSuccess ||
+        (e = upload(lv, d->volprof, nz, &L.volprof)) != cudaSuccess ||
+        (e = upload(lv, d->dr, nz, &L.dr)) != cudaSuccess) {
+        pmg_level_destroy(lv);
+        return cuda_fail(e, "level upload");
+    }
+    if (uni) {
+        const double wx0 = d->wx[0], wy0 = d->wy[0], av0 = d->av[0], vh0 = d->vh[0],
+                     sw0 = d->sumw[0];
+        L.wx0 = wx0;
+        L.wy0 = wy0;
+        L.csub0 = d->vcoef * av0;                                   // smoother.py:88
+        lv->h_diag.resize(nz);
+        lv->h_band.assign(nz + 1, 0.0);
+        lv->h_invd.resize(nz);
+        const double osw = d->omega2 * sw0;
+        const double cv = d->vcoef * av0;
+        for (int k = 0; k < nz; ++k) {                              // stencil.py:105-109
+            const double t1 = vh0 * d->volprof[k];
+            const double t2 = osw * d->dr[k];
+            const double t3 = cv * (d->vprof[k] + d->vprof[k + 1]);
+            lv->h_diag[k] = (t1 + t2) + t3;
+        }
+        for (int k = 0; k <= nz; ++k) lv->h_band[k] = cv * d->vprof[k];   // stencil.py:79-81
+        lv->h_invd[0] = 1.0 / lv->h_diag[0];                        // smoother.py:93-99
+        for (int k = 1; k < nz; ++k) {
+            const double sk = d->vprof[k] * L.csub0;
+            const double ss = sk * sk;
+            const double m = ss * lv->h_invd[k - 1];
+            lv->h_invd[k] = 1.0 / (lv->h_diag[k] - m);
+        }
+        for (int k = 0; k < nz; ++k)
+            if (!std::isfinite(lv->h_invd[k]) || std::fabs(lv->h_diag[k]) < 1e-300) {
+                pmg_level_destroy(lv);
+                return fail(PMG_ERR_PIVOT, "zero pivot in the column factorisation");
+            }
+        if ((e = upload(lv, lv->h_diag.data(), nz, &L.diag1)) != cudaSuccess ||
+            (e = upload(lv, lv->h_band.data(), nz + 1, &L.band1)) != cudaSuccess ||
+            (e = upload(lv, lv->h_invd.data(), nz, &L.invd1)) != cudaSuccess) {
+            pmg_level_destroy(lv);
+            return cuda_fail(e, "level tables");
+        }
+    } else {
+        if ((e = upload(lv, d->wx, (size_t)ny * (nx + 1), &L.wx)) != cudaSuccess ||
+            (e = upload(lv, d->wy, (size_t)(ny + 1) * nx, &L.wy)) != cudaSuccess ||
+            (e = upload(lv, d->av, n2, &L.av)) != cudaSuccess ||
+            (e = upload(lv, d->vh, n2, &L.vh)) != cudaSuccess ||
+            (e = upload(lv, d->sumw, n2, &L.sumw)) != cudaSuccess) {
+            pmg_level_destroy(lv);
+            return cuda_fail(e, "level factors");
+        }
+        void *p = nullptr;
+        if ((e = cudaMalloc(&p, 2 * L.cstride * sizeof(double))) != cudaSuccess) {
+            pmg_level_destroy(lv);
+            return cuda_fail(e, "pivot table");
+        }
+        lv->owned.push_back(p);
+        lv->invd_field = (double *)p;
+        L.invd = lv->invd_field;
+    }
+    *out = lv;
+    return PMG_OK;
+}
+
+int pmg_level_destroy(pmg_level *lv) {
+    if (!lv) return PMG_OK;
+    for (void *p : lv->owned) cudaFree(p);
+    delete lv;
+    return PMG_OK;
+}
+
+long long pmg_level_field_doubles(const pmg_level *lv) {
+    if (!lv) return -1;
+    return 2 * lv->L.cstride;
+}
+
+int pmg_level_layout(const pmg_level *lv, int *pitch, long long *plane, long long *cstride,
+                     int *parity, int *uniform) {
+    PMG_CHECK_LVL(lv);
+    if (pitch) *pitch = lv->L.pitch;
+    if (plane) *plane = lv->L.plane;
+    if (cstride) *cstride = lv->L.cstride;
+    if (parity) *parity = lv->L.par;
+    if (uniform) *uniform = lv->L.uniform;
+    return PMG_OK;
+}
+
+int pmg_level_tables(const pmg_level *lv, double *diag, double *band, double *invd) {
+    PMG_CHECK_LVL(lv);
+    if (!lv->L.uniform) return fail(PMG_ERR_VALUE, "level has variable coefficients");
+    const int nz = lv->L.nz;
+    if (diag) std::memcpy(diag, lv->h_diag.data(), nz * sizeof(double));
+    if (band) std::memcpy(band, lv->h_band.data(), (nz + 1) * sizeof(double));
+    if (invd) std::memcpy(invd, lv->h_invd.data(), nz * sizeof(double));
+    return PMG_OK;
+}
+
+int pmg_level_prepare(pmg_level *lv, void *stream) {
+    PMG_CHECK_LVL(lv);
+    if (lv->L.uniform || lv->prepared) return PMG_OK;
+    PMG_CUDA(launch_invd(lv->L, lv->invd_field, (cudaStream_t)stream), "invd");
+    lv->prepared = true;
+    return PMG_OK;
+}
+
+int pmg_from_ref_layout(const pmg_level *lv, const double *src, double *field, void *st) {
+    PMG_CHECK_LVL(lv);
+    PMG_CUDA(launch_from_ref(lv->L, src, field, (cudaStream_t)st), "from_ref_layout");
+    return PMG_OK;
+}
+
+int pmg_to_ref_layout(const pmg_level *lv, const double *field, double *dst, void *st) {
+    PMG_CHECK_LVL(lv);
+    PMG_CUDA(launch_to_ref(lv->L, field, dst, (cudaStream_t)st), "to_ref_layout");
+    return PMG_OK;
+}
+
+int pmg_apply(const pmg_level *lv, const double *u, double *out, void *st) {
+    PMG_CHECK_LVL(lv);
+    int np = 0;
+    PMG_CUDA(launch_apply(lv->L, u, nullptr, out, 0, nullptr, &np, (cudaStream_t)st), "apply");
+    return PMG_OK;
+}
+
+int pmg_residual(const pmg_level *lv, const double *f, const double *u, double *r,
+                 double *scratch, double *norm2, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (norm2 && !scratch) return fail(PMG_ERR_VALUE, "norm needs a scratch buffer");
+    int np = 0;
+    PMG_CUDA(launch_apply(lv->L, u, f, r, 1, norm2 ? scratch : nullptr, &np, (cudaStream_t)st),
+             "residual");
+    if (norm2) PMG_CUDA(launch_finalize(scratch, np, norm2, (cudaStream_t)st), "residual norm");
+    return PMG_OK;
+}
+
+int pmg_apply_dot(const pmg_level *lv, const double *p, double *q, double *scratch, double *dot,
+                  void *st) {
+    PMG_CHECK_LVL(lv);
+    if (!scratch || !dot) return fail(PMG_ERR_VALUE, "apply_dot needs scratch and output");
+    int np = 0;
+    PMG_CUDA(launch_apply(lv->L, p, nullptr, q, 2, scratch, &np, (cudaStream_t)st), "apply_dot");
+    PMG_CUDA(launch_finalize(scratch, np, dot, (cudaStream_t)st), "apply_dot reduce");
+    return PMG_OK;
+}
+
+static int check_pair(const pmg_level *f, const pmg_level *c) {
+    if (!f || !c) return fail(PMG_ERR_VALUE, "null level handle");
+    if (c->L.nx * 2 != f->L.nx || c->L.ny * 2 != f->L.ny || c->L.nz != f->L.nz)
+        return fail(PMG_ERR_VALUE, "coarse level must halve nx and ny at equal nz");
+    return PMG_OK;
+}
+
+int pmg_residual_restrict(const pmg_level *fine, const pmg_level *coarse, const double *f,
+                          const double *u, double *cf, void *st) {
+    int rc = check_pair(fine, coarse);
+    if (rc) return rc;
+    PMG_CUDA(launch_residual_restrict(fine->L, coarse->L, u, f, cf, (cudaStream_t)st),
+             "residual_restrict");
+    return PMG_OK;
+}
+
+int pmg_half_sweep(const pmg_level *lv, double *u, const double *f, int color, double rho,
+                   int zero_start, int neighbors_zero, double post_scale, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
+    if (!lv->L.uniform && !lv->prepared) {
+        int rc = pmg_level_prepare(const_cast<pmg_level *>(lv), st);
+        if (rc) return rc;
+    }
+    PMG_CUDA(launch_half_sweep(lv->L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
+                               (cudaStream_t)st),
+             "half_sweep");
+    return PMG_OK;
+}
+
+int pmg_restrict(const pmg_level *fine, const pmg_level *coarse, const double *ff, double *cf,
+                 double weight, void *st) {
+    int rc = check_pair(fine, coarse);
+    if (rc) return rc;
+    PMG_CUDA(launch_restrict(fine->L, coarse->L, ff, cf, weight, (cudaStream_t)st), "restrict");
+    return PMG_OK;
+}
+
+int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *cu, double *fu,
+                int add, void *st) {
+    int rc = check_pair(fine, coarse);
+    if (rc) return rc;
+    PMG_CUDA(launch_prolong(fine->L, coarse->L, cu, fu, add, (cudaStream_t)st), "prolong");
+    return PMG_OK;
+}
+
+int pmg_halo_self(const pmg_level *lv, double *field, int px, int py, void *st) {
+    PMG_CHECK_LVL(lv);
+    PMG_CUDA(launch_halo_self(lv->L, field, px, py, (cudaStream_t)st), "halo_self");
+    return PMG_OK;
+}
+
+long long pmg_face_doubles(const pmg_level *lv, int face) {
+    if (!lv || face < 0 || face > 3) return -1;
+    return (long long)face_len(lv->L, face) * lv->L.nz;
+}
+
+int pmg_pack_face(const pmg_level *lv, const double *field, int face, double *buf, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (face < 0 || face > 3) return fail(PMG_ERR_VALUE, "face must be 0..3");
+    PMG_CUDA(launch_pack(lv->L, field, face, buf, (cudaStream_t)st), "pack_face");
+    return PMG_OK;
+}
+
+int pmg_unpack_face(const pmg_level *lv, double *field, int face, const double *buf, int mirror,
+                    void *st) {
+    PMG_CHECK_LVL(lv);
+    if (face < 0 || face > 3) return fail(PMG_ERR_VALUE, "face must be 0..3");
+    PMG_CUDA(launch_unpack(lv->L, field, face, buf, mirror, (cudaStream_t)st), "unpack_face");
+    return PMG_OK;
+}
+
+long long pmg_partials_size(void) { return PARTIALS; }
+
+int pmg_dot(const pmg_level *lv, const double *a, const double *b, double *scratch, double *out,
+            void *st) {
+    PMG_CHECK_LVL(lv);
+    int np = 0;
+    PMG_CUDA(launch_dot(lv->L, a, b, scratch, &np, (cudaStream_t)st), "dot");
+    PMG_CUDA(launch_finalize(scratch, np, out, (cudaStream_t)st), "dot reduce");
+    return PMG_OK;
+}
+
+int pmg_axpy(long long n, double a, const double *x, double *y, void *st) {
+    PMG_CUDA(launch_axpy(n, a, x, y, (cudaStream_t)st), "axpy");
+    return PMG_OK;
+}
+
+int pmg_xpby(long long n, const double *x, double b, double *y, void *st) {
+    PMG_CUDA(launch_xpby(n, x, b, y, (cudaStream_t)st), "xpby");
+    return PMG_OK;
+}
+
+int pmg_cg_update(const pmg_level *lv, const double *num, const double *den, const double *p,
+                  const double *q, double *u, double *r, double *scratch, double *rr, void *st) {
+    PMG_CHECK_LVL(lv);
+    int np = 0;
+    PMG_CUDA(launch_cg_update(lv->L, num, den, p, q, u, r, scratch, &np, (cudaStream_t)st),
+             "cg_update");
+    PMG_CUDA(launch_finalize(scratch, np, rr, (cudaStream_t)st), "cg_update reduce");
+    return PMG_OK;
+}
+
+int pmg_cg_direction(long long n, const double *num, const double *den, const double *z,
+                     double *p, void *st) {
+    PMG_CUDA(launch_cg_direction(n, num, den, z, p, (cudaStream_t)st), "cg_direction");
+    return PMG_OK;
+}
+
+}  // extern "C"

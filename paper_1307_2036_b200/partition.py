@@ -1,0 +1,506 @@
+"""Horizontal domain decomposition, device fields, halo exchange, reductions.
+
+Mirrors the reference communication layer (``partition.py``) with real
+devices behind it:
+
+* a worker ("part") owns an ``mx x my`` block of whole vertical columns
+  (``PAPER.md:527``); its field lives in HBM in the red/black split,
+  horizontal-fastest layout of ``include/pmg.h``;
+* with ``torch.distributed`` initialised and ``world_size > 1`` every rank
+  owns exactly one part and halos / reductions go over NCCL (or gloo);
+  otherwise all parts live on the current device in one process, which
+  is how the reference's simulated workers (``partition.py:1-19``) and
+  its partition-invariance tests are reproduced on one GPU;
+* one part that is its own neighbour in both directions refreshes its
+  halo ring with a single kernel (``pmg_halo_self``).
+
+The decomposition is a px x py grid of parts (the reference's 4^p square
+tilings are the special case px = py = 2^p).  Coarse levels keep every
+worker active (no folding): build hierarchies with at least one column
+per part on the coarsest level.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import LevelDesc, call
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        _LIB = _lib.load()
+    return _LIB
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dist():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        return dist
+    return None
+
+
+def _split_workers(workers: int):
+    """px x py for a worker count: 4^p -> square (reference), 2 -> 2x1,
+    8 -> 4x2 (BASELINE configs[3])."""
+    if workers < 1 or workers & (workers - 1):
+        raise ValueError(f"worker count must be a power of two (got {workers})")
+    a = workers.bit_length() - 1
+    px = 1 << ((a + 1) // 2)
+    return px, workers // px
+
+
+class Decomposition:
+    """Static px x py tiling of the finest level (reference
+    ``Decomposition``, partition.py:45-68)."""
+
+    def __init__(self, nx: int, workers: int = 1, ny: int | None = None, px: int | None = None,
+                 py: int | None = None, periodic: bool | None = None):
+        ny = nx if ny is None else ny
+        if px is None or py is None:
+            px, py = _split_workers(workers)
+        if px * py != workers:
+            raise ValueError(f"{px} x {py} process grid does not hold {workers} workers")
+        if nx % px or ny % py:
+            raise ValueError(f"grid {nx} x {ny} not divisible by the {px} x {py} worker grid")
+        self.nx, self.ny = nx, ny
+        self.workers = workers
+        self.px, self.py = px, py
+        self.pside = px if px == py else None
+        self.periodic = periodic
+        self.collect_calls = 0
+        self.distribute_calls = 0
+        self._layouts = {}
+
+    def layout(self, nx_level: int, pside: int | None = None) -> "LevelLayout":
+        ny_level = nx_level * self.ny // self.nx
+        key = (nx_level, ny_level)
+        if key not in self._layouts:
+            self._layouts[key] = LevelLayout(self, nx_level, ny_level)
+        return self._layouts[key]
+
+    def bind_periodic(self, periodic: bool) -> None:
+        if self.periodic is None:
+            self.periodic = bool(periodic)
+        elif self.periodic != bool(periodic):
+            raise ValueError("decomposition already bound to the other boundary type")
+
+
+def decompose(nx: int, workers: int) -> Decomposition:
+    return Decomposition(nx, workers)
+
+
+class LevelLayout:
+    """Owned rectangles of one grid level (reference ``LevelLayout``,
+    partition.py:76-118).  Worker id = ai * py + aj."""
+
+    def __init__(self, decomp: Decomposition, nx: int, ny: int):
+        if nx % decomp.px or ny % decomp.py:
+            raise ValueError(
+                f"level {nx} x {ny} has fewer columns than the {decomp.px} x {decomp.py} "
+                "worker grid (coarse-level folding is not supported; use fewer levels)")
+        self.decomp = decomp
+        self.nx, self.ny = nx, ny
+        self.px, self.py = decomp.px, decomp.py
+        self.mx, self.my = nx // decomp.px, ny // decomp.py
+        self.pside = decomp.pside
+        self.mloc = self.mx
+        self.group = 1
+        self.workers = [ai * self.py + aj for ai in range(self.px) for aj in range(self.py)]
+        self.halo_count = 0
+        self._geom = {}
+        d = _dist()
+        if d is not None:
+            if d.get_world_size() != decomp.workers:
+                raise ValueError("one worker per rank: world size must equal the worker count")
+            self.local_workers = [d.get_rank()]
+        else:
+            self.local_workers = list(self.workers)
+
+    @property
+    def periodic(self) -> bool:
+        return bool(self.decomp.periodic)
+
+    def coords(self, worker: int):
+        return divmod(worker, self.py)
+
+    def worker_at(self, ai: int, aj: int) -> int:
+        return ai * self.py + aj
+
+    def origin(self, worker: int):
+        ai, aj = self.coords(worker)
+        return ai * self.mx, aj * self.my
+
+    def neighbor(self, worker: int, di: int, dj: int):
+        ai, aj = self.coords(worker)
+        ni, nj = ai + di, aj + dj
+        if self.periodic:
+            return self.worker_at(ni % self.px, nj % self.py)
+        if 0 <= ni < self.px and 0 <= nj < self.py:
+            return self.worker_at(ni, nj)
+        return None
+
+    def geometry(self, worker: int, nz: int) -> "LevelHandle":
+        """Layout-only level handle of one part (unit factors)."""
+        key = (worker, nz)
+        h = self._geom.get(key)
+        if h is None:
+            i0, j0 = self.origin(worker)
+            h = LevelHandle.unit(self.mx, self.my, nz, i0, j0)
+            self._geom[key] = h
+        return h
+
+
+class LevelHandle:
+    """Owner of one ``pmg_level`` (coefficients + layout of one part)."""
+
+    def __init__(self, mx, my, nz, i0, j0, omega2, vcoef, dr, vprof, volprof,
+                 wx, wy, av, vh, sumw):
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64)
+                      for a in (dr, vprof, volprof, wx, wy, av, vh, sumw)]
+        ptr = [a.ctypes.data_as(C.c_void_p) for a in self._keep]
+        desc = LevelDesc(mx, my, nz, i0, j0, float(omega2), float(vcoef), *ptr)
+        h = C.c_void_p()
+        call("pmg_level_create", C.byref(desc), C.byref(h))
+        self.h = h
+        self.mx, self.my, self.nz = mx, my, nz
+        self.i0, self.j0 = i0, j0
+        self.ndoubles = int(lib().pmg_level_field_doubles(h))
+        pitch, plane, cstr = C.c_int(), C.c_longlong(), C.c_longlong()
+        par, uni = C.c_int(), C.c_int()
+        call("pmg_level_layout", h, C.byref(pitch), C.byref(plane), C.byref(cstr),
+             C.byref(par), C.byref(uni))
+        self.pitch, self.plane, self.cstride = pitch.value, plane.value, cstr.value
+        self.parity, self.uniform = par.value, bool(uni.value)
+        self._keep = None
+
+    @classmethod
+    def unit(cls, mx, my, nz, i0, j0):
+        one = np.ones(1)
+        return cls(mx, my, nz, i0, j0, 0.0, 0.0, np.ones(nz), np.ones(nz + 1), np.ones(nz),
+                   np.broadcast_to(one, (my, mx + 1)), np.broadcast_to(one, (my + 1, mx)),
+                   np.broadcast_to(one, (my, mx)), np.broadcast_to(one, (my, mx)),
+                   np.broadcast_to(one, (my, mx)))
+
+    def tables(self):
+        nz = self.nz
+        d, b, v = np.empty(nz), np.empty(nz + 1), np.empty(nz)
+        call("pmg_level_tables", self.h, d.ctypes.data_as(C.c_void_p),
+             b.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p))
+        return d, b, v
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().pmg_level_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+class DevField:
+    """One part of a field in HBM (flat float64 tensor, split layout)."""
+
+    __slots__ = ("geom", "data")
+
+    def __init__(self, geom: LevelHandle, data: torch.Tensor | None = None):
+        self.geom = geom
+        if data is None:
+            data = torch.zeros(geom.ndoubles, dtype=torch.float64, device="cuda")
+        self.data = data
+
+    @property
+    def ptr(self):
+        return C.c_void_p(self.data.data_ptr())
+
+    @property
+    def m(self):
+        return self.geom.mx
+
+    @property
+    def nz(self):
+        return self.geom.nz
+
+    def copy(self) -> "DevField":
+        return DevField(self.geom, self.data.clone())
+
+    def fill(self, value: float) -> None:
+        self.data.fill_(value)
+
+    def owned_array(self) -> np.ndarray:
+        """(mx, my, nz) host copy of the owned cells (reference layout)."""
+        g = self.geom
+        buf = torch.empty(g.mx * g.my * g.nz, dtype=torch.float64, device=self.data.device)
+        call("pmg_to_ref_layout", g.h, self.ptr, C.c_void_p(buf.data_ptr()), _stream())
+        return buf.cpu().numpy().reshape(g.mx, g.my, g.nz)
+
+    def load_owned(self, arr) -> None:
+        """Write an (mx, my, nz) block (numpy or torch, host or device)."""
+        g = self.geom
+        if isinstance(arr, np.ndarray):
+            t = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float64))
+        else:
+            t = arr.contiguous()
+        if t.numel() != g.mx * g.my * g.nz:
+            raise ValueError("block does not match the part size")
+        if t.device.type != "cuda":
+            dev = torch.empty(t.numel(), dtype=torch.float64, device=self.data.device)
+            dev.copy_(t.reshape(-1), non_blocking=t.is_pinned())
+            t = dev
+        call("pmg_from_ref_layout", g.h, C.c_void_p(t.data_ptr()), self.ptr, _stream())
+
+
+class DistField:
+    """A field split over the parts of one layout (reference ``DistField``,
+    partition.py:121-155).  ``parts`` holds the parts hosted here."""
+
+    __slots__ = ("layout", "parts")
+
+    def __init__(self, layout: LevelLayout, parts: dict):
+        self.layout = layout
+        self.parts = parts
+
+    @classmethod
+    def zeros(cls, layout: LevelLayout, nz: int) -> "DistField":
+        return cls(layout, {w: DevField(layout.geometry(w, nz)) for w in layout.local_workers})
+
+    @property
+    def nz(self) -> int:
+        return next(iter(self.parts.values())).nz
+
+    def copy(self) -> "DistField":
+        return DistField(self.layout, {w: f.copy() for w, f in self.parts.items()})
+
+    def copy_from(self, other: "DistField") -> None:
+        for w, f in self.parts.items():
+            f.data.copy_(other.parts[w].data)
+
+    def fill(self, value: float) -> None:
+        for f in self.parts.values():
+            f.fill(value)
+
+    def add_scaled(self, alpha: float, other: "DistField") -> None:
+        """self += alpha * other over the full arrays, halo included
+        (partition.py:145-148)."""
+        for w, f in self.parts.items():
+            call("pmg_axpy", f.geom.ndoubles, float(alpha), other.parts[w].ptr, f.ptr,
+                 _stream())
+
+    def scale_plus(self, beta: float, other: "DistField") -> None:
+        """self = other + beta * self over the full arrays (partition.py:150-155)."""
+        for w, f in self.parts.items():
+            call("pmg_xpby", f.geom.ndoubles, other.parts[w].ptr, float(beta), f.ptr,
+                 _stream())
+
+
+# ---------------------------------------------------------------------------
+# halo exchange (partition.py:158-191)
+# ---------------------------------------------------------------------------
+_OPP = {0: 1, 1: 0, 2: 3, 3: 2}
+_DIR = {0: (-1, 0), 1: (1, 0), 2: (0, -1), 3: (0, 1)}
+
+
+class _FaceBuffers:
+    cache = {}
+
+    @classmethod
+    def get(cls, geom: LevelHandle, tag: str, face: int) -> torch.Tensor:
+        key = (geom.mx, geom.my, geom.nz, tag, face)
+        t = cls.cache.get(key)
+        if t is None:
+            n = int(lib().pmg_face_doubles(geom.h, face))
+            t = torch.empty(n, dtype=torch.float64, device="cuda")
+            cls.cache[key] = t
+        return t
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def halo_exchange(df: DistField) -> None:
+    """Refresh every halo cell: x strips first, then y strips over the
+    extended range (corners), periodic wrap or mirror at physical
+    boundaries.  Counted once per call on the layout."""
+    lay = df.layout
+    st = _stream()
+    if lay.px == 1 and lay.py == 1:
+        f = df.parts[lay.workers[0]]
+        call("pmg_halo_self", f.geom.h, f.ptr, int(lay.periodic), int(lay.periodic), st)
+        lay.halo_count += 1
+        return
+    d = _dist()
+    for faces in ((0, 1), (2, 3)):
+        if d is None:
+            _phase_local(df, faces, st)
+        else:
+            _phase_dist(df, faces, st, d)
+    lay.halo_count += 1
+
+
+def _phase_local(df: DistField, faces, st) -> None:
+    lay = df.layout
+    for w, f in df.parts.items():
+        for face in faces:
+            nb = lay.neighbor(w, *_DIR[face])
+            if nb is None:
+                call("pmg_unpack_face", f.geom.h, f.ptr, face, None, 1, st)
+                continue
+            src = df.parts[nb]
+            buf = _FaceBuffers.get(f.geom, "local", face)
+            call("pmg_pack_face", src.geom.h, src.ptr, _OPP[face], _ptr(buf), st)
+            call("pmg_unpack_face", f.geom.h, f.ptr, face, _ptr(buf), 0, st)
+
+
+def exchange_plan(lay: LevelLayout, w: int, faces):
+    """Message plan of one part for one phase: [(send_face, peer_send,
+    recv_face, peer_recv)], ordered [send f0, recv h1, send f1, recv h0]
+    so that two faces exchanged with the same peer (2 ranks along a
+    periodic axis) pair up correctly under NCCL's in-order matching; gloo
+    matches them by tag (= the sender's face index)."""
+    a, b = faces
+    return [(sf, lay.neighbor(w, *_DIR[sf]), rf, lay.neighbor(w, *_DIR[rf]))
+            for sf, rf in ((a, b), (b, a))]
+
+
+def exchange_messages(dist, w: int, plan, sendbufs: dict, recvbufs: dict) -> dict:
+    """Post the plan's sends/receives (device-agnostic: NCCL with CUDA
+    tensors, gloo with CPU tensors) and wait.  Returns recv_face ->
+    "buf" (recvbufs[face] holds the neighbour strip), "mirror"
+    (physical boundary) or "self" (own neighbour: copied locally)."""
+    ops, how = [], {}
+    for sf, ps, rf, pr in plan:
+        if ps == w and pr == w:
+            recvbufs[rf].copy_(sendbufs[sf])
+            how[rf] = "self"
+            continue
+        if ps is not None:
+            ops.append(dist.P2POp(dist.isend, sendbufs[sf], ps, tag=sf))
+        if pr is not None:
+            ops.append(dist.P2POp(dist.irecv, recvbufs[rf], pr, tag=sf))
+            how[rf] = "buf"
+        else:
+            how[rf] = "mirror"
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return how
+
+
+def _phase_dist(df: DistField, faces, st, dist) -> None:
+    """One rank = one part: pack own faces, exchange, unpack halos."""
+    lay = df.layout
+    (w, f), = df.parts.items()
+    plan = exchange_plan(lay, w, faces)
+    sendbufs, recvbufs = {}, {}
+    for sf, ps, rf, pr in plan:
+        sendbufs[sf] = _FaceBuffers.get(f.geom, "send", sf)
+        recvbufs[rf] = _FaceBuffers.get(f.geom, "recv", rf)
+        if ps is not None:
+            call("pmg_pack_face", f.geom.h, f.ptr, sf, _ptr(sendbufs[sf]), st)
+    how = exchange_messages(dist, w, plan, sendbufs, recvbufs)
+    for face, kind in how.items():
+        if kind == "mirror":
+            call("pmg_unpack_face", f.geom.h, f.ptr, face, None, 1, st)
+        else:
+            call("pmg_unpack_face", f.geom.h, f.ptr, face, _ptr(recvbufs[face]), 0, st)
+
+
+# ---------------------------------------------------------------------------
+# global <-> parts (partition.py:243-264)
+# ---------------------------------------------------------------------------
+def scatter_owned(arr, layout: LevelLayout) -> DistField:
+    """Split a global (nx, ny, nz) array (numpy, or torch on host/device)
+    over the layout's local parts; halos start at zero."""
+    if arr.shape[0] != layout.nx or arr.shape[1] != layout.ny:
+        raise ValueError("array does not match the layout size")
+    nz = int(arr.shape[2])
+    df = DistField.zeros(layout, nz)
+    for w, f in df.parts.items():
+        i0, j0 = layout.origin(w)
+        if layout.px == 1 and layout.py == 1:
+            f.load_owned(arr)
+        else:
+            f.load_owned(arr[i0:i0 + layout.mx, j0:j0 + layout.my, :])
+    return df
+
+
+def gather_owned(df: DistField) -> np.ndarray:
+    """Assemble the global (nx, ny, nz) host array of owned values (on every
+    rank when distributed)."""
+    lay = df.layout
+    out = np.empty((lay.nx, lay.ny, df.nz))
+    d = _dist()
+    if d is None:
+        for w, f in df.parts.items():
+            i0, j0 = lay.origin(w)
+            out[i0:i0 + lay.mx, j0:j0 + lay.my, :] = f.owned_array()
+        return out
+    (w, f), = df.parts.items()
+    mine = torch.from_numpy(f.owned_array())
+    dev = "cuda" if d.get_backend() == "nccl" else "cpu"
+    mine = mine.to(dev)
+    allp = [torch.empty_like(mine) for _ in range(d.get_world_size())]
+    d.all_gather(allp, mine)
+    for wk, blk in enumerate(allp):
+        i0, j0 = lay.origin(wk)
+        out[i0:i0 + lay.mx, j0:j0 + lay.my, :] = blk.cpu().numpy()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# reductions (partition.py:267-286)
+# ---------------------------------------------------------------------------
+class _Scratch:
+    t = None
+    res = None
+
+    @classmethod
+    def get(cls):
+        if cls.t is None:
+            cls.t = torch.empty(int(lib().pmg_partials_size()), dtype=torch.float64, device="cuda")
+            cls.res = torch.zeros(64, dtype=torch.float64, device="cuda")
+        return cls.t, cls.res
+
+
+def reduce_parts(vals: torch.Tensor) -> float:
+    """Sum per-part device scalars in part order, then over ranks."""
+    tot = vals.sum() if vals.numel() > 1 else vals[0]
+    d = _dist()
+    if d is not None:
+        t = tot.reshape(1).clone()
+        if d.get_backend() != "nccl":
+            t = t.cpu()
+        d.all_reduce(t)
+        return float(t.item())
+    return float(tot.item())
+
+
+def dist_dot(a: DistField, b: DistField, deterministic: bool = False) -> float:
+    """Owned-cell inner product over all parts (fixed per-part reduction
+    order; part results summed in worker order, then across ranks)."""
+    scratch, res = _Scratch.get()
+    st = _stream()
+    ws = list(a.parts.keys())
+    out = torch.empty(len(ws), dtype=torch.float64, device="cuda")
+    for n, w in enumerate(ws):
+        fa, fb = a.parts[w], b.parts[w]
+        call("pmg_dot", fa.geom.h, fa.ptr, fb.ptr, _ptr(scratch),
+             C.c_void_p(out.data_ptr() + 8 * n), st)
+    return reduce_parts(out)
+
+
+def dist_norm(a: DistField, deterministic: bool = False) -> float:
+    return math.sqrt(dist_dot(a, a, deterministic))

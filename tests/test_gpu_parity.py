@@ -1,0 +1,303 @@
+"""CUDA path vs the oracle / reference goldens (needs a B200).
+
+Operator, smoother and transfers are compiled without FMA contraction and
+in the reference's expression order, so they must match the reference
+BIT FOR BIT (tolerance 0).  Solver histories involve reductions whose
+order differs (block trees vs numpy pairwise): 1e-8 relative per
+north_star, with equal iteration counts; in practice ~1e-14.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def uni(shape, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=shape)
+
+
+@pytest.fixture(scope="module")
+def pmg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1307_2036_b200 as m
+    return m
+
+
+def grid_of(pmg, g, nx=None):
+    nx = int(g["nx"]) if nx is None else nx
+    nz = int(g["nz"])
+    lv = g["levels"]
+    depth = float(lv[-1] - 1.0)
+    if bool(g["periodic"]):
+        shape = pmg.geometry.omega_shape_config4 if bool(g["variable"]) else None
+        return pmg.periodic_box(nx, nz, depth, lv, omega_shape=shape)
+    return pmg.panel_grid(nx, nz, depth=depth, flat_mode=True, levels=lv)
+
+
+def setup(pmg, name, workers=1):
+    g = load(name)
+    grid = grid_of(pmg, g)
+    params = pmg.toy_parameters(grid.nx, grid.nz, float(g["omega2"]), float(g["lambda2"]))
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=int(g["nlev"]), eps=1e-5)
+    dec = pmg.Decomposition(grid.nx, workers)
+    hier = pmg.build_hierarchy(grid, params, cfg, dec)
+    return g, grid, params, cfg, hier
+
+
+def field(pmg, arr, layout):
+    d = pmg.scatter_owned(arr, layout)
+    pmg.halo_exchange(d)
+    return d
+
+
+OPS = ["ops_periodic", "ops_neumann", "ops_variable", "ops_config"]
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+@pytest.mark.parametrize("name", OPS)
+def test_ops_bitwise(pmg, name, workers):
+    g, grid, params, cfg, hier = setup(pmg, name, workers)
+    nx, nz = grid.nx, grid.nz
+    fine, coarse = hier.levels[0], hier.levels[1]
+    op, lay = fine.op, fine.layout
+    ug, fg = uni((nx, nx, nz), 1), uni((nx, nx, nz), 2)
+    u, f = field(pmg, ug, lay), field(pmg, fg, lay)
+    G = pmg.gather_owned
+    assert np.array_equal(G(op.apply(u)), g["apply"])
+    assert np.array_equal(G(op.residual(f, u)), g["residual"])
+    sm = fine.smoother
+    for rho in (1.0, 1.4):
+        uu = field(pmg, ug, lay)
+        sm.half_sweep(uu, f, 0, rho)
+        assert np.array_equal(G(uu), g[f"half_red_rho{rho}"])
+        pmg.halo_exchange(uu)
+        sm.half_sweep(uu, f, 1, rho)
+        assert np.array_equal(G(uu), g[f"half_black_rho{rho}"])
+    uu = field(pmg, ug, lay)
+    sm.sweep(uu, f, nsweeps=2, rho=1.0)
+    assert np.array_equal(G(uu), g["sweep2"])
+    for rho in (1.0, 1.3):
+        assert np.array_equal(G(sm.ssor_apply(f, rho)), g[f"ssor_rho{rho}"])
+    assert np.array_equal(G(pmg.restrict(u, fine, coarse)), g["restrict_mean"])
+    cd = field(pmg, uni((nx // 2, nx // 2, nz), 3), coarse.layout)
+    assert np.array_equal(G(pmg.prolong(cd, coarse, fine)), g["prolong"])
+    # one V-cycle from zero, unfused and fused (same arithmetic)
+    for fused in (False, True):
+        c2 = pmg.MGConfig(policy="explicit", explicit_levels=int(g["nlev"]), fused=fused)
+        scratch = hier.make_scratch()
+        scratch[0].f.copy_from(f)
+        pmg.v_cycle(hier, c2, scratch)
+        assert np.array_equal(G(scratch[0].u), g["vcycle1"])
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("name", OPS)
+def test_solvers_vs_reference(pmg, name, graph):
+    g, grid, params, cfg, hier = setup(pmg, name)
+    nx, nz = grid.nx, grid.nz
+    fg = uni((nx, nx, nz), 2)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=int(g["nlev"]), eps=1e-5,
+                       graph=graph)
+    f = pmg.scatter_owned(fg, hier.fine.layout)
+    u, rep = pmg.mg_solve(f, hier, cfg)
+    ref = g["mg_history"]
+    assert rep.iterations == len(ref) - 1
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-12
+    got = pmg.gather_owned(u)
+    assert np.max(np.abs(got - g["mg_u"])) <= 1e-12 * np.max(np.abs(g["mg_u"]))
+    op = hier.fine.op
+    pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+    uc, rc = pmg.pcg_solve(f, op, pre, eps=1e-8, maxiter=200)
+    ref = g["cg_history"]
+    assert rc.iterations == len(ref) - 1
+    assert np.max(np.abs(np.array(rc.residual_history) - ref) / ref) <= 1e-10
+    got = pmg.gather_owned(uc)
+    assert np.max(np.abs(got - g["cg_u"])) <= 1e-10 * np.max(np.abs(g["cg_u"]))
+
+
+@pytest.mark.parametrize("solver", ["mg", "cg"])
+def test_config0_vs_reference(pmg, solver):
+    from paper_1307_2036_b200 import configs
+    g = load(f"config0_{solver}")
+    prob = configs.config(0)
+    fg = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
+    grid, params = prob.grid(), prob.params()
+    if solver == "mg":
+        cfg = prob.mg_config()
+        hier = pmg.build_hierarchy(grid, params, cfg)
+        u, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
+    else:
+        op = pmg.PanelOperator(grid, params)
+        pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+        u, rep = pmg.pcg_solve(pmg.scatter_owned(fg, op.layout), op, pre, eps=1e-5,
+                               maxiter=2000)
+    ref = g["history"]
+    assert rep.iterations == int(g["iterations"])
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-8
+    got = pmg.gather_owned(u)
+    assert np.max(np.abs(got - g["u"])) <= 1e-8 * np.max(np.abs(g["u"]))
+
+
+@pytest.mark.parametrize("w", ["0.0001", "0.001", "0.01", "0.1"])
+@pytest.mark.parametrize("solver", ["mg", "cg"])
+def test_omega_sweep_small(pmg, w, solver):
+    from paper_1307_2036_b200 import configs
+    g = load(f"sweep128_{solver}_w{w}")
+    prob = configs.Problem(128, 128, 64, float(w), 1.0, 4)
+    fg = configs.rhs(128, 128, 64, 0)
+    grid, params = prob.grid(), prob.params()
+    if solver == "mg":
+        cfg = prob.mg_config()
+        hier = pmg.build_hierarchy(grid, params, cfg)
+        _, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
+    else:
+        op = pmg.PanelOperator(grid, params)
+        pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+        _, rep = pmg.pcg_solve(pmg.scatter_owned(fg, op.layout), op, pre, eps=1e-5,
+                               maxiter=2000)
+    ref = g["history"]
+    assert rep.iterations == int(g["iterations"])
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-8
+
+
+@pytest.mark.parametrize("name,nx,nlev", [("config4_like_mg", 64, 4),
+                                          ("config4_like256_mg", 256, 5)])
+def test_config4_like(pmg, name, nx, nlev):
+    from paper_1307_2036_b200 import configs
+    g = load(name)
+    prob = configs.Problem(nx, nx, 128, 1e-3, 1.0, nlev, stretch=1.05, variable_omega=True)
+    fg = configs.rhs(nx, nx, 128, 0)
+    cfg = prob.mg_config()
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
+    assert not hier.fine.op.uniform
+    u, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
+    ref = g["history"]
+    assert rep.iterations == int(g["iterations"])
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-8
+    ug = pmg.gather_owned(u)
+    idx = g["sample_idx"]
+    got = ug[idx[:, 0], idx[:, 1], idx[:, 2]]
+    assert np.max(np.abs(got - g["sample_u"])) <= 1e-8 * float(g["u_absmax"])
+
+
+@pytest.mark.parametrize("workers", [2, 4, 8, 16])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_partition_invariance(pmg, workers, periodic):
+    """tests/test_partition.py:122-154 on the device: parts emulated on one
+    GPU exchange halos through the pack/unpack kernels."""
+    nx, nz = 32, 8
+    if periodic:
+        grid = pmg.periodic_box(nx, nz, 0.01)
+    else:
+        grid = pmg.panel_grid(nx, nz, flat_mode=True)
+    params = pmg.toy_parameters(nx, nz, 6.7e-4 if not periodic else 1e-3, 3.3e-2)
+    fg = uni((nx, nx, nz), 3)
+    hist = {}
+    cg = {}
+    for p in (1, workers):
+        cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, graph=False)
+        hier = pmg.build_hierarchy(grid, params, cfg, pmg.Decomposition(nx, p))
+        f = pmg.scatter_owned(fg, hier.fine.layout)
+        _, rep = pmg.mg_solve(f, hier, cfg)
+        hist[p] = np.array(rep.residual_history)
+        op = hier.fine.op
+        pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+        _, rc = pmg.pcg_solve(f, op, pre, eps=1e-5, maxiter=100)
+        cg[p] = np.array(rc.residual_history)
+    for h in (hist, cg):
+        assert len(h[1]) == len(h[workers])
+        assert np.max(np.abs(h[workers] - h[1]) / h[1]) <= 1e-10
+
+
+def test_exchange_counts(pmg):
+    """1 + 2(nu_pre + nu_post) exchanges per level per cycle, 2 per coarse
+    sweep (tests/test_multigrid.py:165-177)."""
+    grid = pmg.periodic_box(32, 4, 0.01)
+    params = pmg.toy_parameters(32, 4, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, graph=False, maxiter=1, eps=0.5)
+    hier = pmg.build_hierarchy(grid, params, cfg, pmg.Decomposition(32, 4))
+    f = pmg.scatter_owned(uni((32, 32, 4), 0), hier.fine.layout)
+    scratch = hier.make_scratch()
+    scratch[0].f.copy_from(f)
+    hier.reset_counters()
+    pmg.v_cycle(hier, cfg, scratch)
+    counts = [lev.layout.halo_count for lev in hier.levels]
+    assert counts[:-1] == [5, 5] and counts[-1] == 2
+
+
+def test_layout_round_trip(pmg):
+    for nx, ny, nz, p in ((16, 16, 4, 1), (32, 16, 3, 2), (8, 8, 5, 4)):
+        grid = pmg.periodic_box(nx, nz, 0.01, ny=ny)
+        dec = pmg.Decomposition(nx, p, ny=ny, periodic=True)
+        lay = dec.layout(nx)
+        a = uni((nx, ny, nz), 7)
+        assert np.array_equal(pmg.gather_owned(pmg.scatter_owned(a, lay)), a)
+
+
+def test_rectangular_periodic_vs_oracle(pmg):
+    """nx != ny periodic grids (the 2- and 8-GPU global grids of configs[3])."""
+    from oracle import port
+    nx, ny, nz = 32, 16, 8
+    lv = port.uniform_levels(nz, 0.01)
+    fg = uni((nx, ny, nz), 5)
+    h = port.Hierarchy(nx, ny, 3, lambda a, b: port.config_factors(a, b, lv), 1e-3, 1.0)
+    ou, orep = port.mg_solve(h, fg)
+    grid = pmg.periodic_box(nx, nz, 0.01, ny=ny)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    for p in (1, 2, 8):
+        cfg = pmg.MGConfig(policy="explicit", explicit_levels=3)
+        dec = pmg.Decomposition(nx, p, ny=ny)
+        hier = pmg.build_hierarchy(grid, params, cfg, dec)
+        u, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
+        assert rep.iterations == orep.iterations
+        oh = np.array(orep.residual_history)
+        assert np.max(np.abs(np.array(rep.residual_history) - oh) / oh) <= 1e-10
+        ug = pmg.gather_owned(u)
+        assert np.max(np.abs(ug - ou[1:-1, 1:-1, :])) <= 1e-10 * np.max(np.abs(ug))
+
+
+def test_zero_rhs_and_breakdown(pmg):
+    grid = pmg.periodic_box(16, 4, 0.01)
+    params = pmg.toy_parameters(16, 4, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=2)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    f = pmg.scatter_owned(np.zeros((16, 16, 4)), hier.fine.layout)
+    u, rep = pmg.mg_solve(f, hier, cfg)
+    assert rep.iterations == 0 and rep.converged and rep.residual_history == [0.0]
+    u, rep = pmg.pcg_solve(f, hier.fine.op)
+    assert rep.iterations == 0 and rep.converged
+
+
+@pytest.mark.slow
+def test_config1_full_size(pmg):
+    """BASELINE configs[1] at full size (1024^2 x 128, 7 levels) against the
+    reference's own history (tests/golden/config1_mg.npz)."""
+    path = os.path.join(GOLD, "config1_mg.npz")
+    if not os.path.exists(path):
+        pytest.skip("config1 golden not generated")
+    from paper_1307_2036_b200 import configs
+    g = load("config1_mg")
+    prob = configs.config(1)
+    fg = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
+    cfg = prob.mg_config()
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
+    u, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
+    ref = g["history"]
+    assert rep.iterations == int(g["iterations"])
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-8
+    ug = pmg.gather_owned(u)
+    idx = g["sample_idx"]
+    got = ug[idx[:, 0], idx[:, 1], idx[:, 2]]
+    assert np.max(np.abs(got - g["sample_u"])) <= 1e-8 * float(g["u_absmax"])
+    assert abs(ug.sum() - float(g["u_sum"])) <= 1e-8 * float(g["u_absmax"]) * ug.size ** 0.5
