@@ -63,6 +63,9 @@ typedef struct pmg_level_desc {
 } pmg_level_desc;
 
 int pmg_version(void);
+/* number of kernel launches this library has issued (or recorded into a
+ * CUDA graph) since load; launchers with a reduction count two. */
+long long pmg_launch_count(void);
 const char *pmg_last_error(void);
 int pmg_device_sm_count(int device, int *out);
 
@@ -104,6 +107,12 @@ int pmg_residual_restrict(const pmg_level *fine, const pmg_level *coarse,
                           void *stream);
 
 /* ---- line smoother: LineSmoother.half_sweep (smoother.py:122-182) ---- */
+/* mode 0 (default): fast k-segmented column solve (uniform levels; agrees
+ * with the sequential Thomas algorithm to ~1e-15 relative); mode 1: exact
+ * sequential Thomas recurrence, bit-identical to the reference.  Levels
+ * with variable coefficients always use the exact solver. */
+int pmg_set_smoother_mode(int mode);
+int pmg_get_smoother_mode(void);
 int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
                    double rho, int zero_start, int neighbors_zero, double post_scale,
                    void *stream);

@@ -38,6 +38,7 @@ _LL = C.c_longlong
 # name -> (restype, argtypes)
 SIGNATURES = {
     "pmg_version": (_I, []),
+    "pmg_launch_count": (_LL, []),
     "pmg_last_error": (C.c_char_p, []),
     "pmg_device_sm_count": (_I, [_I, C.POINTER(_I)]),
     "pmg_level_create": (_I, [C.POINTER(LevelDesc), C.POINTER(_P)]),
@@ -54,6 +55,8 @@ SIGNATURES = {
     "pmg_apply_dot": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_residual_restrict": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_half_sweep": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _P]),
+    "pmg_set_smoother_mode": (_I, [_I]),
+    "pmg_get_smoother_mode": (_I, []),
     "pmg_restrict": (_I, [_P, _P, _P, _P, _D, _P]),
     "pmg_prolong": (_I, [_P, _P, _P, _P, _I, _P]),
     "pmg_halo_self": (_I, [_P, _P, _I, _I, _P]),

@@ -3,15 +3,19 @@
 // Host-side coefficient tables are computed here in the reference's
 // expression order (stencil.py:105-109, smoother.py:93-99); the host code is
 // compiled with -ffp-contract=off so no FMA contraction changes a rounding.
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <string>
 #include <vector>
 
 #include "pmg_common.cuh"
 
 namespace pmg {
+extern std::atomic<long long> g_launches;
+extern int g_smoother_exact;
 cudaError_t launch_apply(const Lvl &, const double *, const double *, double *, int, double *,
                          int *, cudaStream_t);
 cudaError_t launch_finalize(const double *, int, double *, cudaStream_t);
@@ -44,6 +48,7 @@ struct pmg_level {
     Lvl L;
     int i0, j0;
     std::vector<double> h_diag, h_band, h_invd;   // uniform tables (host copy)
+    std::vector<double> h_seg;                    // fast solver tables
     std::vector<void *> owned;                    // device allocations to free
     double *invd_field = nullptr;                 // variable: per-cell pivots
     bool prepared = false;
@@ -91,6 +96,16 @@ extern "C" {
 
 int pmg_version(void) { return 1; }
 
+int pmg_set_smoother_mode(int mode) {
+    if (mode < 0 || mode > 1) return fail(PMG_ERR_VALUE, "smoother mode must be 0 (fast) or 1 (exact)");
+    pmg::g_smoother_exact = mode;
+    return PMG_OK;
+}
+
+int pmg_get_smoother_mode(void) { return pmg::g_smoother_exact; }
+
+long long pmg_launch_count(void) { return g_launches.load(); }
+
 const char *pmg_last_error(void) { return g_err.c_str(); }
 
 int pmg_device_sm_count(int device, int *out) {
@@ -114,8 +129,11 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
     // row: h in [-1, nx>>1] at OFF-1 .. OFF+(nx>>1); pitch multiple of 8 doubles
     const int need = OFF + (nx >> 1) + 1;
     L.pitch = (need + 7) / 8 * 8;
-    L.plane = (long long)(ny + 2) * L.pitch;
-    L.cstride = (long long)nz * L.plane;
+    // row-major over j: a row's whole column data is one contiguous
+    // nz * pitch block, so column-oriented kernels touch few 2 MB pages
+    L.plane = L.pitch;
+    L.jstride = (long long)nz * L.pitch;
+    L.cstride = (long long)(ny + 2) * L.jstride;
     L.par = (d->i0 + d->j0) & 1;
     L.omega2 = d->omega2;
     L.vcoef = d->vcoef;
@@ -167,7 +185,29 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
                 pmg_level_destroy(lv);
                 return fail(PMG_ERR_PIVOT, "zero pivot in the column factorisation");
             }
-        if ((e = upload(lv, lv->h_diag.data(), nz, &L.diag1)) != cudaSuccess ||
+        // k-segmented solver tables: g_k = iota_k r_k + alpha_k g_{k-1},
+        // x_k = g_k + mu_k x_{k+1}; pf / q = products of alpha / mu over the
+        // segment from its start / to its end (segments of L.seg levels)
+        int seg = 4;
+        while (seg < 32 && (nz + seg - 1) / seg > 8) seg <<= 1;
+        L.seg = ((nz + seg - 1) / seg <= 8) ? seg : 0;
+        lv->h_seg.assign(4 * (size_t)nz, 0.0);
+        double *al = lv->h_seg.data(), *mu = al + nz, *pf = mu + nz, *qq = pf + nz;
+        for (int k = 0; k < nz; ++k) {
+            al[k] = (k == 0) ? 0.0 : (L.csub0 * d->vprof[k]) * lv->h_invd[k];
+            mu[k] = (k + 1 < nz) ? (L.csub0 * d->vprof[k + 1]) * lv->h_invd[k] : 0.0;
+        }
+        if (L.seg) {
+            for (int a = 0; a < nz; a += seg) {
+                const int b = std::min(nz, a + seg) - 1;
+                double p = 1.0;
+                for (int k = a; k <= b; ++k) { p *= al[k]; pf[k] = p; }
+                double q = 1.0;
+                for (int k = b; k >= a; --k) { q *= mu[k]; qq[k] = q; }
+            }
+        }
+        if ((e = upload(lv, lv->h_seg.data(), 4 * (size_t)nz, &L.segtab)) != cudaSuccess ||
+            (e = upload(lv, lv->h_diag.data(), nz, &L.diag1)) != cudaSuccess ||
             (e = upload(lv, lv->h_band.data(), nz + 1, &L.band1)) != cudaSuccess ||
             (e = upload(lv, lv->h_invd.data(), nz, &L.invd1)) != cudaSuccess) {
             pmg_level_destroy(lv);

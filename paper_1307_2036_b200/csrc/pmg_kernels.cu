@@ -7,9 +7,17 @@
 // bit-identical to the reference (see tests/test_gpu_parity.py).
 //
 // Layout: red/black split, horizontal index fastest (include/pmg.h).
+#include <atomic>
+#include <cstdlib>
+
 #include "pmg_common.cuh"
 
 namespace pmg {
+
+// kernel launches issued by this library (host-side count, incl. launches
+// recorded into CUDA graphs)
+std::atomic<long long> g_launches{0};
+int g_smoother_exact = 0;
 
 // ---------------------------------------------------------------------------
 // block reduction helpers (deterministic: fixed shuffle tree + fixed
@@ -60,12 +68,14 @@ constexpr int AP_TY = 4;
 template <bool UNI, int MODE, bool NORM>
 __global__ void __launch_bounds__(32 * 2 * AP_TY)
 k_apply(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
-        double *__restrict__ out, double *__restrict__ partials) {
+        double *__restrict__ out, double *__restrict__ partials, int kc) {
     const int lane = threadIdx.x;
     const int c = threadIdx.y & 1;
     const int j = blockIdx.y * AP_TY + (threadIdx.y >> 1);
     const int h = blockIdx.x * 32 + lane;
     const int i = 2 * h + ((j + L.par + c) & 1);
+    const int k0 = blockIdx.z * kc;
+    const int k1 = min(L.nz, k0 + kc);
     double acc2 = 0.0;
     if (j < L.ny && i < L.nx) {
         const int o = c ^ 1;
@@ -90,9 +100,10 @@ k_apply(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
         }
         const int nz = L.nz;
         const long long pl = L.plane;
-        double um = 0.0, u0 = u[pc], up = 0.0;
+        double um = (k0 > 0) ? u[pc + (long long)(k0 - 1) * pl] : 0.0;
+        double u0 = u[pc + (long long)k0 * pl], up = 0.0;
 #pragma unroll 4
-        for (int k = 0; k < nz; ++k) {
+        for (int k = k0; k < k1; ++k) {
             const long long ko = (long long)k * pl;
             up = (k + 1 < nz) ? u[pc + ko + pl] : 0.0;
             double acc = wxm * u[pW + ko];
@@ -121,7 +132,102 @@ k_apply(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
     if (NORM) {
         const double s = block_sum(acc2);
         if (threadIdx.x == 0 && threadIdx.y == 0)
-            partials[blockIdx.y * gridDim.x + blockIdx.x] = s;
+            partials[(blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Batched variant of k_apply: each thread owns KB consecutive levels of
+// one column and issues every load of its chunk before any arithmetic, so
+// (KB+2) + 5 KB independent 8-byte loads per thread are in flight (the
+// sequential-k version left the SM latency-bound at ~30% of HBM peak).
+// Same arithmetic, same order.
+// ---------------------------------------------------------------------------
+template <bool UNI, int MODE, bool NORM, int KB>
+__global__ void __launch_bounds__(32 * 2 * AP_TY)
+k_apply_b(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
+          double *__restrict__ out, double *__restrict__ partials, int hx, int jy, int ntiles) {
+    const int lane = threadIdx.x;
+    const int c = threadIdx.y & 1;
+    const int nz = L.nz;
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    double acc2 = 0.0;
+    // grid-stride over tiles (h-block fastest, then k chunk, then row block:
+    // concurrently processed tiles share rows, i.e. contiguous memory)
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int nkc = (nz + KB - 1) / KB;
+        const int hb = tile % hx;
+        const int rest = tile / hx;
+        const int k0 = (rest % nkc) * KB;
+        const int jb = rest / nkc;
+        const int j = jb * AP_TY + (threadIdx.y >> 1);
+        const int h = hb * 32 + lane;
+        const int i = 2 * h + ((j + L.par + c) & 1);
+        if (j >= L.ny || i >= L.nx) continue;
+        const long long kb = (long long)k0 * pl;
+        const long long pc = at(L, c, 0, j, h) + kb;
+        const long long pW = at(L, o, 0, j, (i - 1) >> 1) + kb;
+        const long long pE = at(L, o, 0, j, (i + 1) >> 1) + kb;
+        const long long pS = at(L, o, 0, j - 1, h) + kb;
+        const long long pN = at(L, o, 0, j + 1, h) + kb;
+        double uc[KB + 2], vw[KB], ve[KB], vs[KB], vn[KB], vf[KB];
+        uc[0] = (k0 > 0) ? u[pc - pl] : 0.0;
+#pragma unroll
+        for (int t = 0; t < KB; ++t) {
+            const bool ok = k0 + t < nz;
+            const long long ko = (long long)t * pl;
+            uc[t + 1] = ok ? u[pc + ko] : 0.0;
+            vw[t] = ok ? u[pW + ko] : 0.0;
+            ve[t] = ok ? u[pE + ko] : 0.0;
+            vs[t] = ok ? u[pS + ko] : 0.0;
+            vn[t] = ok ? u[pN + ko] : 0.0;
+            if (MODE == 1) vf[t] = ok ? f[pc + ko] : 0.0;
+        }
+        uc[KB + 1] = (k0 + KB < nz) ? u[pc + (long long)KB * pl] : 0.0;
+        double wxm, wxp, wym, wyp, cv, vhc = 0.0, osw = 0.0;
+        if (UNI) {
+            wxm = wxp = L.wx0;
+            wym = wyp = L.wy0;
+            cv = L.csub0;
+        } else {
+            wxm = L.wx[(long long)j * (L.nx + 1) + i];
+            wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
+            wym = L.wy[(long long)j * L.nx + i];
+            wyp = L.wy[(long long)(j + 1) * L.nx + i];
+            cv = L.vcoef * L.av[(long long)j * L.nx + i];
+            vhc = L.vh[(long long)j * L.nx + i];
+            osw = L.omega2 * L.sumw[(long long)j * L.nx + i];
+        }
+#pragma unroll
+        for (int t = 0; t < KB; ++t) {
+            const int k = k0 + t;
+            if (k < nz) {
+                double acc = wxm * vw[t];
+                acc = acc + wxp * ve[t];
+                acc = acc + wym * vs[t];
+                acc = acc + wyp * vn[t];
+                acc = acc * L.drw[k];
+                double d;
+                if (UNI) {
+                    d = L.diag1[k];
+                } else {
+                    d = vhc * L.volprof[k];
+                    d = d + osw * L.dr[k];
+                    d = d + cv * (L.vprof[k] + L.vprof[k + 1]);
+                }
+                double res = d * uc[t + 1] - acc;
+                if (k >= 1) res = res - (UNI ? L.band1[k] : cv * L.vprof[k]) * uc[t];
+                if (k + 1 < nz) res = res - (UNI ? L.band1[k + 1] : cv * L.vprof[k + 1]) * uc[t + 2];
+                if (MODE == 1) res = vf[t] - res;
+                if (out) out[pc + (long long)t * pl] = res;
+                if (NORM) acc2 += (MODE == 2) ? uc[t + 1] * res : res * res;
+            }
+        }
+    }
+    if (NORM) {
+        const double s = block_sum(acc2);
+        if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = s;
     }
 }
 
@@ -173,18 +279,25 @@ __device__ __forceinline__ double resid_cell(const Lvl &L, const double *__restr
 template <bool UNI>
 __global__ void __launch_bounds__(256)
 k_residual_restrict(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
-                    double *__restrict__ cf) {
+                    double *__restrict__ cf, int kc) {
     const int I = blockIdx.x * blockDim.x + threadIdx.x;
-    const int J = blockIdx.y * blockDim.y + threadIdx.y;
+    const int J = blockIdx.z * blockDim.y + threadIdx.y;
     if (I >= C.nx || J >= C.ny) return;
+    const int k0 = blockIdx.y * kc;
+    const int k1 = min(F.nz, k0 + kc);
     const int i0 = 2 * I, j0 = 2 * J;
     const long long q00 = cell(F, i0, j0, 0), q10 = cell(F, i0 + 1, j0, 0);
     const long long q01 = cell(F, i0, j0 + 1, 0), q11 = cell(F, i0 + 1, j0 + 1, 0);
     const long long pl = F.plane;
+    const long long kb = (long long)k0 * pl;
     double m00 = 0, m10 = 0, m01 = 0, m11 = 0;
-    double c00 = u[q00], c10 = u[q10], c01 = u[q01], c11 = u[q11];
+    if (k0 > 0) {
+        m00 = u[q00 + kb - pl]; m10 = u[q10 + kb - pl];
+        m01 = u[q01 + kb - pl]; m11 = u[q11 + kb - pl];
+    }
+    double c00 = u[q00 + kb], c10 = u[q10 + kb], c01 = u[q01 + kb], c11 = u[q11 + kb];
     const long long qc = cell(C, I, J, 0);
-    for (int k = 0; k < F.nz; ++k) {
+    for (int k = k0; k < k1; ++k) {
         const long long ko = (long long)k * pl;
         const bool nx_ = k + 1 < F.nz;
         const double p00 = nx_ ? u[q00 + ko + pl] : 0.0, p10 = nx_ ? u[q10 + ko + pl] : 0.0;
@@ -211,26 +324,33 @@ k_residual_restrict(Lvl F, Lvl C, const double *__restrict__ u, const double *__
 // step (smoother.py:163-170).  Several CTAs per SM overlap phase 1 loads of
 // some CTAs with the serial phase of others.
 // ---------------------------------------------------------------------------
+constexpr int HS_THREADS = 128;
+
 template <bool UNI>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(HS_THREADS, 6)
 k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
              int zero_start, int nbr_zero, double post_scale) {
     extern __shared__ double smem[];
     const int nz = L.nz;
-    double *s = smem;                                // [nz][32]  rhs -> g
-    double *so = smem + nz * 32;                     // [nz][32]  u_old (rho != 1)
-    double *sinv = so + ((!zero_start && rho != 1.0) ? nz * 32 : 0);   // [nz][32] (var)
+    const bool need_old = !zero_start && rho != 1.0;
+    double *s = smem;                                    // [nz][32]  rhs -> g
+    double *so = s + nz * 32;                            // [nz][32]  u_old (rho != 1)
+    double *sinv = so + (need_old ? nz * 32 : 0);        // [nz][32]  pivots (variable)
+    double *tvp = sinv + (UNI ? 0 : nz * 32);            // [nz+1]    vprof
+    double *tinv = tvp + nz + 1;                         // [nz]      pivots (uniform)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int j = blockIdx.y;
     const int h = blockIdx.x * 32 + lane;
     const int i = 2 * h + ((j + L.par + c) & 1);
     const bool act = i < L.nx;
-    const bool need_old = !zero_start && rho != 1.0;
     const int o = c ^ 1;
     const long long pc = at(L, c, 0, j, h);
     const long long pl = L.plane;
 
-    double cv = L.csub0;
+    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
+        tvp[t] = L.vprof[t];
+        if (UNI && t < nz) tinv[t] = L.invd1[t];
+    }
     if (act) {
         double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
         if (!UNI) {
@@ -264,28 +384,29 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
     }
     __syncthreads();
     if (w != 0 || !act) return;
+    double cv = L.csub0;
     if (!UNI) cv = L.vcoef * L.av[(long long)j * L.nx + i];
-    const double *vp = L.vprof;
     // forward elimination (smoother.py:151-156)
-    double g = s[lane] * (UNI ? L.invd1[0] : sinv[lane]);
+    double g = s[lane] * (UNI ? tinv[0] : sinv[lane]);
     s[lane] = g;
-#pragma unroll 4
+#pragma unroll 8
     for (int k = 1; k < nz; ++k) {
         double t = g * cv;
-        t = t * vp[k];
+        t = t * tvp[k];
         g = s[k * 32 + lane] + t;
-        g = g * (UNI ? L.invd1[k] : sinv[k * 32 + lane]);
+        g = g * (UNI ? tinv[k] : sinv[k * 32 + lane]);
         s[k * 32 + lane] = g;
     }
     // back substitution (smoother.py:157-161) + relaxation (163-170)
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
     double x = g;
+#pragma unroll 8
     for (int k = nz - 1; k >= 0; --k) {
         if (k < nz - 1) {
             double t = x * cv;
-            t = t * vp[k + 1];
-            t = t * (UNI ? L.invd1[k] : sinv[k * 32 + lane]);
+            t = t * tvp[k + 1];
+            t = t * (UNI ? tinv[k] : sinv[k * 32 + lane]);
             x = s[k * 32 + lane] + t;
         }
         double y = x;
@@ -296,6 +417,749 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
             y = y + omr * so[k * 32 + lane];
         }
         u[pc + (long long)k * pl] = y;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Line smoother half-sweep, register-resident variant (default).
+//
+// CTA = 32 columns (lane) x NW warps; warp w owns the k-segment
+// [w*SEG, (w+1)*SEG) of every column IN REGISTERS.  All warps assemble
+// their RHS segment at once (SEG independent k-planes per thread in flight:
+// one or two DRAM round trips per CTA).  The Thomas recurrence stays exactly
+// the reference's (smoother.py:151-161): the forward chain runs through
+// warps 0..NW-1 and the backward chain through NW-1..0, handing the running
+// value over in shared memory; so the result is bit-identical to the
+// sequential column solve.  Relaxation + stores run on all warps again.
+// Only ~2 KB of shared memory per CTA: occupancy is register-limited.
+// ---------------------------------------------------------------------------
+template <bool UNI, int SEG>
+__global__ void __launch_bounds__(256, 3)
+k_half_sweep_reg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                 int zero_start, int nbr_zero, double post_scale) {
+    extern __shared__ double tab[];
+    const int nz = L.nz;
+    double *tvp = tab;              // [nz+1]
+    double *tinv = tvp + nz + 1;    // [nz]  (uniform pivots)
+    double *tdrw = tinv + nz;       // [nz]
+    __shared__ double hand[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int j = blockIdx.y;
+    const int h = blockIdx.x * 32 + lane;
+    const int i = 2 * h + ((j + L.par + c) & 1);
+    const bool act = i < L.nx;
+    const int o = c ^ 1;
+    const long long pc = at(L, c, 0, j, h);
+    const long long pl = L.plane;
+    const int k0 = w * SEG;
+
+    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
+        tvp[t] = L.vprof[t];
+        if (t < nz) {
+            if (UNI) tinv[t] = L.invd1[t];
+            tdrw[t] = L.drw[t];
+        }
+    }
+    __syncthreads();
+
+    double r[SEG];
+    double iv[UNI ? 1 : SEG];
+    double cv = L.csub0;
+    if (act) {
+        double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
+        if (!UNI) {
+            wxm = L.wx[(long long)j * (L.nx + 1) + i];
+            wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
+            wym = L.wy[(long long)j * L.nx + i];
+            wyp = L.wy[(long long)(j + 1) * L.nx + i];
+            cv = L.vcoef * L.av[(long long)j * L.nx + i];
+        }
+        const long long pW = at(L, o, 0, j, (i - 1) >> 1);
+        const long long pE = at(L, o, 0, j, (i + 1) >> 1);
+        const long long pS = at(L, o, 0, j - 1, h);
+        const long long pN = at(L, o, 0, j + 1, h);
+#pragma unroll
+        for (int s = 0; s < SEG; ++s) {
+            const int k = k0 + s;
+            if (k < nz) {
+                const long long ko = (long long)k * pl;
+                double g;
+                if (nbr_zero) {
+                    g = f[pc + ko];
+                } else {
+                    g = wxm * u[pW + ko];
+                    g = g + wxp * u[pE + ko];
+                    g = g + wym * u[pS + ko];
+                    g = g + wyp * u[pN + ko];
+                    g = g * tdrw[k];
+                    g = g + f[pc + ko];
+                }
+                r[s] = g;
+                if (!UNI) iv[s] = L.invd[pc + ko];
+            }
+        }
+    }
+    // forward elimination, warp by warp (smoother.py:151-156)
+    for (int step = 0; step < nw; ++step) {
+        if (w == step && act) {
+            double g = (w == 0) ? 0.0 : hand[lane];
+#pragma unroll
+            for (int s = 0; s < SEG; ++s) {
+                const int k = k0 + s;
+                if (k < nz) {
+                    const double ivk = UNI ? tinv[k] : iv[s];
+                    if (k == 0) {
+                        g = r[s] * ivk;
+                    } else {
+                        double t = g * cv;
+                        t = t * tvp[k];
+                        g = r[s] + t;
+                        g = g * ivk;
+                    }
+                    r[s] = g;
+                }
+            }
+            hand[lane] = g;
+        }
+        __syncthreads();
+    }
+    // back substitution, warp by warp (smoother.py:157-161)
+    for (int step = nw - 1; step >= 0; --step) {
+        if (w == step && act) {
+            double x = hand[lane];
+#pragma unroll
+            for (int s = SEG - 1; s >= 0; --s) {
+                const int k = k0 + s;
+                if (k < nz - 1) {
+                    double t = x * cv;
+                    t = t * tvp[k + 1];
+                    t = t * (UNI ? tinv[k] : iv[s]);
+                    x = r[s] + t;
+                    r[s] = x;
+                } else if (k == nz - 1) {
+                    x = r[s];
+                }
+            }
+            hand[lane] = x;
+        }
+        __syncthreads();
+    }
+    if (!act) return;
+    // relaxation (smoother.py:163-170) and coalesced stores, all warps
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+#pragma unroll
+    for (int s = 0; s < SEG; ++s) {
+        const int k = k0 + s;
+        if (k < nz) {
+            double y = r[s];
+            if (zero_start) {
+                if (scale != 1.0) y = y * scale;
+            } else if (rho != 1.0) {
+                // u still holds the old value of this (own) cell
+                y = y * rho;
+                y = y + omr * u[pc + (long long)k * pl];
+            }
+            u[pc + (long long)k * pl] = y;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Line smoother half-sweep, persistent warp-specialised pipeline (default
+// for uniform coefficients).
+//
+// Tile = 32 columns (one 32-wide h strip of one row) x nz levels.  Each
+// CTA is resident on one SM and walks tiles blockIdx.x, +gridDim.x, ...
+//   * producer warps (NG groups x NP warps; group g takes every NG-th
+//     tile of the CTA) assemble the tile's RHS: warp p owns a k-segment
+//     and issues 8 levels x 5 loads per lane before any arithmetic, then
+//     writes g[k][lane] into a shared-memory tile buffer;
+//   * NS solver warps (solver s takes the CTA's tiles q = s mod NS, double
+//     buffered) run the exact Thomas recurrence of smoother.py:151-161 per
+//     lane in shared memory and stream x (relaxed, smoother.py:163-170)
+//     straight to HBM.
+// FULL/EMPTY hand-offs are named barriers (bar.arrive / bar.sync).  The
+// serial chain of one tile (2 nz dependent steps) overlaps the loads of
+// the next tiles, so the SM keeps DRAM busy; results are bit-identical to
+// the sequential column solve.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr int PP_KB = 4;    // levels per producer load batch
+constexpr int PP_NP = 8;    // producer warps per group
+constexpr int PP_NG = 2;    // producer groups
+constexpr int PP_NS = 3;    // solver warps (double-buffered each)
+constexpr int PP_NBUF = 2 * PP_NS;
+constexpr int PP_THREADS = 32 * (PP_NP * PP_NG + PP_NS);
+
+__global__ void __launch_bounds__(PP_THREADS, 1)
+k_half_sweep_pipe(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
+    extern __shared__ double sm[];
+    const int nz = L.nz;
+    double *tvp = sm;                 // [nz+1]
+    double *tinv = tvp + nz + 1;      // [nz]
+    double *tdrw = tinv + nz;         // [nz]
+    double *bufs = sm + ((3 * nz + 1 + 3) & ~3);   // [NBUF][nz][32]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
+        tvp[t] = L.vprof[t];
+        if (t < nz) {
+            tinv[t] = L.invd1[t];
+            tdrw[t] = L.drw[t];
+        }
+    }
+    __syncthreads();
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    const int nprod = PP_NP * PP_NG;
+    const int cnt = 32 * (PP_NP + 1);   // one producer group + one solver warp
+    if (warp < nprod) {
+        // ------------------------------ producer ------------------------------
+        const int grp = warp / PP_NP, pw = warp % PP_NP;
+        const int seg = (nz + PP_NP - 1) / PP_NP;
+        const int ka = pw * seg, kz = min(nz, ka + seg);
+        const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
+        for (int q = grp;; q += PP_NG) {
+            const int t = blockIdx.x + q * gridDim.x;
+            if (t >= ntiles) break;
+            const int sv = q % PP_NS;
+            const int b = 2 * sv + (q / PP_NS) % 2;
+            if (q >= PP_NBUF) nbar_sync(1 + PP_NBUF + b, cnt);      // EMPTY(b)
+            double *buf = bufs + (size_t)b * nz * 32;
+            const int j = t / htiles;
+            const int h0 = (t % htiles) * 32;
+            // inactive lanes (i >= nx on narrow levels) clamp to the last
+            // active column so the warp stays converged for the shuffle;
+            // the shuffle source of the last active lane is then itself,
+            // so its E neighbour is loaded explicitly (vx) as for lane 31
+            const int s0 = (j + L.par + c) & 1;
+            const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+            const int ln = min(lane, nact - 1);
+            const int h = h0 + ln;
+            const int i = 2 * h + s0;
+            const bool lastlane = (ln == nact - 1);
+            if (nact > 0) {
+                const long long pc = at(L, c, 0, j, h);
+                const long long pW = at(L, o, 0, j, (i - 1) >> 1);
+                const long long pE = at(L, o, 0, j, (i + 1) >> 1);
+                const long long pS = at(L, o, 0, j - 1, h);
+                const long long pN = at(L, o, 0, j + 1, h);
+                for (int k8 = ka; k8 < kz; k8 += PP_KB) {
+                    // PP_KB levels x 4 loads in flight per lane; the E neighbour
+                    // of lane l is the W neighbour of lane l+1 (same row, next h)
+                    double vf[PP_KB], vw[PP_KB], vs[PP_KB], vn[PP_KB], vx[PP_KB];
+#pragma unroll
+                    for (int e = 0; e < PP_KB; ++e) {
+                        const int k = k8 + e;
+                        if (k < kz) {
+                            const long long ko = (long long)k * pl;
+                            vf[e] = f[pc + ko];
+                            if (!nbr_zero) {
+                                vw[e] = u[pW + ko];
+                                vs[e] = u[pS + ko];
+                                vn[e] = u[pN + ko];
+                                vx[e] = lastlane ? u[pE + ko] : 0.0;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < PP_KB; ++e) {
+                        const int k = k8 + e;
+                        double ve = __shfl_down_sync(0xffffffffu, vw[e], 1);
+                        if (lastlane) ve = vx[e];
+                        if (k < kz) {
+                            double g;
+                            if (nbr_zero) {
+                                g = vf[e];
+                            } else {
+                                g = wxm * vw[e];
+                                g = g + wxp * ve;
+                                g = g + wym * vs[e];
+                                g = g + wyp * vn[e];
+                                g = g * tdrw[k];
+                                g = g + vf[e];
+                            }
+                            if (lane < nact) buf[k * 32 + lane] = g;
+                        }
+                    }
+                }
+            }
+            nbar_arrive(1 + b, cnt);                                   // FULL(b)
+        }
+    } else {
+        // ------------------------------- solver -------------------------------
+        const int sv = warp - nprod;
+        if (sv >= PP_NS) return;
+        const double cv = L.csub0;
+        const double scale = rho * post_scale;
+        const double omr = 1.0 - rho;
+        for (int q = sv;; q += PP_NS) {
+            const int t = blockIdx.x + q * gridDim.x;
+            if (t >= ntiles) break;
+            const int b = 2 * sv + (q / PP_NS) % 2;
+            nbar_sync(1 + b, cnt);                                     // FULL(b)
+            double *buf = bufs + (size_t)b * nz * 32;
+            const int j = t / htiles;
+            const int h = (t % htiles) * 32 + lane;
+            const int i = 2 * h + ((j + L.par + c) & 1);
+            if (i < L.nx) {
+                const long long pc = at(L, c, 0, j, h);
+                // forward elimination in register chunks of 8 levels: the
+                // chunk's 8 LDS are issued before the dependent chain
+                double g = 0.0;
+                for (int kb = 0; kb < nz; kb += 8) {
+                    double r[8];
+                    const double *tv = tvp + kb, *ti = tinv + kb;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (kb + e < nz) r[e] = buf[(kb + e) * 32 + lane];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int k = kb + e;
+                        if (k < nz) {
+                            if (k == 0) {
+                                g = r[e] * ti[e];
+                            } else {
+                                double tt = g * cv;
+                                tt = tt * tv[e];
+                                g = r[e] + tt;
+                                g = g * ti[e];
+                            }
+                            r[e] = g;
+                        }
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (kb + e < nz) buf[(kb + e) * 32 + lane] = r[e];
+                }
+                // back substitution + relaxation, chunks of 8 from the top
+                double x = g;
+                const int top = ((nz - 1) / 8) * 8;
+                for (int kb = top; kb >= 0; kb -= 8) {
+                    double r[8];
+                    const double *tv = tvp + kb + 1, *ti = tinv + kb;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e)
+                        if (kb + e < nz - 1) r[e] = buf[(kb + e) * 32 + lane];
+#pragma unroll
+                    for (int e = 7; e >= 0; --e) {
+                        const int k = kb + e;
+                        if (k < nz - 1) {
+                            double tt = x * cv;
+                            tt = tt * tv[e];
+                            tt = tt * ti[e];
+                            x = r[e] + tt;
+                        }
+                        if (k < nz) {
+                            double y = x;
+                            if (zero_start) {
+                                if (scale != 1.0) y = y * scale;
+                            } else if (rho != 1.0) {
+                                y = y * rho;
+                                y = y + omr * u[pc + (long long)k * pl];
+                            }
+                            u[pc + (long long)k * pl] = y;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            // release the buffer only if a producer will wait for it
+            if (blockIdx.x + (q + PP_NBUF) * gridDim.x < ntiles) nbar_arrive(1 + PP_NBUF + b, cnt);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Line smoother half-sweep, TMA-fed solver warps (default for uniform
+// coefficients).
+//
+// Every warp of the persistent CTA is an independent pipeline over its own
+// sequence of tiles (32 columns of one row x nz levels):
+//   * lane 0 streams the tile's k-planes into a shared-memory ring of R
+//     slots with 1-D bulk TMA copies (cp.async.bulk ... complete_tx), one
+//     mbarrier per slot: per level the 34-element W/E row of the other
+//     colour, its S and N rows and the f row (1040 bytes).  The copies
+//     bypass L1 and need no registers, so ~R KB per warp are in flight;
+//   * the forward sweep waits on the slot, assembles the RHS exactly as
+//     smoother.py:137-145 and runs the elimination (smoother.py:151-156),
+//     keeping g[k] in a per-warp shared buffer;
+//   * the back substitution (smoother.py:157-161) + relaxation
+//     (smoother.py:163-170) streams x straight to HBM while the ring
+//     already fills with the next tile.
+// Arithmetic and order are the reference's: bit-identical results.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+constexpr int TM_R = 16;          // ring slots (levels in flight) per warp
+constexpr int TM_ROW = 136;       // doubles per slot: W/E 36 | S 32 | N 32 | f 32 (+pad)
+
+struct TmaTile {
+    // geometry of one tile for the lane-0 issuer and the consumers
+    int j, h0, s0, nact;
+};
+
+__device__ __forceinline__ TmaTile tma_tile(const Lvl &L, int t, int htiles, int c) {
+    TmaTile T;
+    T.j = t / htiles;
+    T.h0 = (t % htiles) * 32;
+    T.s0 = (T.j + L.par + c) & 1;
+    T.nact = min(32, ((L.nx - T.s0) + 1) / 2 - T.h0);
+    return T;
+}
+
+// lane 0: stage level k of tile T into ring slot
+__device__ __forceinline__ void tma_issue(const Lvl &L, const double *u, const double *f, int c,
+                                          int nbr_zero, const TmaTile &T, int k, double *slot,
+                                          uint64_t *bar) {
+    const int o = c ^ 1;
+    const int n = T.nact;
+    // f row: columns h0 .. h0+n-1 (16-byte granules: start is even)
+    const long long pf = at(L, c, k, T.j, T.h0);
+    const uint32_t fb = (uint32_t)(((n + 1) & ~1) * 8);
+    uint32_t tx = fb;
+    uint32_t wb = 0, sb = 0;
+    long long pw = 0;
+    if (!nbr_zero) {
+        // W/E row: h0 + s0 - 1 .. h0 + s0 + n - 1 ; aligned start a0
+        const int first = OFF + T.h0 + T.s0 - 1;        // element offset in the row
+        const int a0 = first & ~1;
+        const int last = OFF + T.h0 + T.s0 + n - 1;
+        wb = (uint32_t)(((last - a0 + 2) & ~1) * 8);
+        pw = at(L, o, k, T.j, 0) - OFF + a0;
+        sb = fb;
+        tx += wb + 2 * sb;
+    }
+    mbar_expect_tx(bar, tx);
+    tma_1d(slot + 100, f + pf, fb, bar);
+    if (!nbr_zero) {
+        tma_1d(slot, u + pw, wb, bar);
+        tma_1d(slot + 36, u + at(L, o, k, T.j - 1, T.h0), sb, bar);
+        tma_1d(slot + 68, u + at(L, o, k, T.j + 1, T.h0), sb, bar);
+    }
+}
+
+__global__ void __launch_bounds__(128, 1)
+k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                 int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
+    extern __shared__ __align__(16) double tsm[];
+    const int nz = L.nz;
+    const int nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // shared layout: tables | per warp { gbuf [nz][32] | ring [R][ROW] } | bars
+    double *tvp = tsm;
+    double *tinv = tvp + nz + 1;
+    double *tdrw = tinv + nz;
+    const int tab = (3 * nz + 1 + 1) & ~1;
+    const int per_warp = nz * 32 + TM_R * TM_ROW;
+    double *gbuf = tsm + tab + (size_t)warp * per_warp;
+    double *ring = gbuf + nz * 32;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + tab + (size_t)nw * per_warp) + warp * TM_R;
+    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
+        tvp[t] = L.vprof[t];
+        if (t < nz) {
+            tinv[t] = L.invd1[t];
+            tdrw[t] = L.drw[t];
+        }
+    }
+    if (lane == 0)
+        for (int r = 0; r < TM_R; ++r) mbar_init(&bars[r], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    const long long pl = L.plane;
+    const double cv = L.csub0, wx0 = L.wx0, wy0 = L.wy0;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    // issue stream: (tile q, level k) in order over this warp's tiles
+    int iq = warp, ik = 0;             // next level to issue
+    uint32_t iseq = 0, cseq = 0;       // issued / consumed level counters
+    auto issue_next = [&]() {
+        const int t = blockIdx.x + iq * gridDim.x;
+        if (t >= ntiles) return;
+        const TmaTile T = tma_tile(L, t, htiles, c);
+        const int slot = iseq % TM_R;
+        if (lane == 0) {
+            fence_proxy_async();
+            tma_issue(L, u, f, c, nbr_zero, T, ik, ring + slot * TM_ROW, &bars[slot]);
+        }
+        ++iseq;
+        if (++ik == nz) {
+            ik = 0;
+            iq += nw;
+        }
+    };
+    for (int r = 0; r < TM_R; ++r) issue_next();
+
+    for (int q = warp;; q += nw) {
+        const int t = blockIdx.x + q * gridDim.x;
+        if (t >= ntiles) break;
+        const TmaTile T = tma_tile(L, t, htiles, c);
+        const bool act = lane < T.nact;
+        const int dW = (OFF + T.h0 + T.s0 - 1) - ((OFF + T.h0 + T.s0 - 1) & ~1);
+        // ---- forward: RHS assembly + elimination ----
+        double g = 0.0;
+        for (int k = 0; k < nz; ++k) {
+            const int slot = cseq % TM_R;
+            mbar_wait(&bars[slot], (cseq / TM_R) & 1);
+            const double *sl = ring + slot * TM_ROW;
+            double rhs;
+            if (nbr_zero) {
+                rhs = sl[100 + lane];
+            } else {
+                rhs = wx0 * sl[dW + lane];
+                rhs = rhs + wx0 * sl[dW + lane + 1];
+                rhs = rhs + wy0 * sl[36 + lane];
+                rhs = rhs + wy0 * sl[68 + lane];
+                rhs = rhs * tdrw[k];
+                rhs = rhs + sl[100 + lane];
+            }
+            if (k == 0) {
+                g = rhs * tinv[0];
+            } else {
+                double tt = g * cv;
+                tt = tt * tvp[k];
+                g = rhs + tt;
+                g = g * tinv[k];
+            }
+            gbuf[k * 32 + lane] = g;
+            ++cseq;
+            __syncwarp();
+            issue_next();
+        }
+        // ---- backward + relaxation + store ----
+        if (act) {
+            const long long pc = at(L, c, 0, T.j, T.h0 + lane);
+            double x = g;
+            const int top = ((nz - 1) / 8) * 8;
+            for (int kb = top; kb >= 0; kb -= 8) {
+                double r[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (kb + e < nz - 1) r[e] = gbuf[(kb + e) * 32 + lane];
+#pragma unroll
+                for (int e = 7; e >= 0; --e) {
+                    const int k = kb + e;
+                    if (k < nz - 1) {
+                        double tt = x * cv;
+                        tt = tt * tvp[k + 1];
+                        tt = tt * tinv[k];
+                        x = r[e] + tt;
+                    }
+                    if (k < nz) {
+                        double y = x;
+                        if (zero_start) {
+                            if (scale != 1.0) y = y * scale;
+                        } else if (rho != 1.0) {
+                            y = y * rho;
+                            y = y + omr * u[pc + (long long)k * pl];
+                        }
+                        u[pc + (long long)k * pl] = y;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Line smoother half-sweep, FAST mode (default, uniform coefficients):
+// k-segmented column solve.
+//
+// CTA = 32 columns x NW warps; warp w owns levels [w*SEG, (w+1)*SEG) of
+// every column in registers.  The Thomas recurrences are linear:
+//   forward  g_k = iota_k r_k + alpha_k g_{k-1}
+//   backward x_k = g_k + mu_k x_{k+1}
+// so each warp solves its segment with zero incoming value (h, y), the
+// segment ends are joined by a scan of NW terms in shared memory and
+// g = h + pf G, x = y + q X fix the segments up (pf, q: products of alpha,
+// mu over the segment, per-level tables).  Every warp issues its loads in
+// batches of 8 levels x 4 rows (E neighbours by warp shuffle) with the
+// full L1 available -- no serial chain, no large shared buffers.  Same
+// operator and RHS as smoother.py:137-170; reassociated elimination
+// (agrees with the sequential solve to ~1e-15 relative; the exact mode is
+// k_half_sweep_tma / k_half_sweep).
+// ---------------------------------------------------------------------------
+#ifndef PMG_SEG_B
+#define PMG_SEG_B 4   // levels per load batch
+#endif
+template <int SEG>
+__global__ void __launch_bounds__(256, 2)
+k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                 int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
+    extern __shared__ double ssm[];
+    const int nz = L.nz;
+    double *tdrw = ssm;                 // [nz]
+    double *tiot = tdrw + nz;           // [nz]
+    double *tal = tiot + nz;            // [nz]
+    double *tmu = tal + nz;             // [nz]
+    double *tpf = tmu + nz;             // [nz]
+    double *tq = tpf + nz;              // [nz]
+    double *hend = tq + nz;             // [8][32]
+    double *ybeg = hend + 8 * 32;       // [8][32]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
+        tdrw[t] = L.drw[t];
+        tiot[t] = L.invd1[t];
+        tal[t] = L.segtab[t];
+        tmu[t] = L.segtab[nz + t];
+        tpf[t] = L.segtab[2 * nz + t];
+        tq[t] = L.segtab[3 * nz + t];
+    }
+    __syncthreads();
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    const int k0 = w * SEG;
+    const int kn = min(SEG, nz - k0);          // levels of this warp (may be <= 0)
+    const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int j = t / htiles;
+        const int h0 = (t - j * htiles) * 32;
+        const int s0 = (j + L.par + c) & 1;
+        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+        const int ln = min(lane, nact - 1);
+        const bool lastlane = (ln == nact - 1);
+        const int h = h0 + ln;
+        const int i = 2 * h + s0;
+        const long long pc = at(L, c, k0, j, h);
+        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
+        const long long pS = at(L, o, k0, j - 1, h);
+        const long long pN = at(L, o, k0, j + 1, h);
+        double r[SEG];
+        // ---- RHS assembly, batches of 8 levels ----
+#pragma unroll
+        for (int b8 = 0; b8 < SEG; b8 += (SEG < PMG_SEG_B ? SEG : PMG_SEG_B)) {
+            constexpr int B = SEG < PMG_SEG_B ? SEG : PMG_SEG_B;
+            double vf[B], vw[B], vs[B], vn[B], vx[B];
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const int kk = b8 + e;
+                if (kk < kn) {
+                    const long long ko = (long long)kk * pl;
+                    vf[e] = f[pc + ko];
+                    if (!nbr_zero) {
+                        vw[e] = u[pW + ko];
+                        vs[e] = u[pS + ko];
+                        vn[e] = u[pN + ko];
+                        vx[e] = lastlane ? u[pE + ko] : 0.0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const int kk = b8 + e;
+                double ve = __shfl_down_sync(0xffffffffu, nbr_zero ? 0.0 : vw[e], 1);
+                if (lastlane) ve = vx[e];
+                if (kk < kn) {
+                    double g;
+                    if (nbr_zero) {
+                        g = vf[e];
+                    } else {
+                        g = wxm * vw[e];
+                        g = g + wxp * ve;
+                        g = g + wym * vs[e];
+                        g = g + wyp * vn[e];
+                        g = g * tdrw[k0 + kk];
+                        g = g + vf[e];
+                    }
+                    r[b8 + e] = g;
+                }
+            }
+        }
+        // ---- local forward: h_k = iota_k r_k + alpha_k h_{k-1} ----
+        double hp = 0.0;
+#pragma unroll
+        for (int e = 0; e < SEG; ++e) {
+            if (e < kn) {
+                const int k = k0 + e;
+                hp = __fma_rn(tal[k], hp, tiot[k] * r[e]);
+                r[e] = hp;
+            }
+        }
+        if (kn > 0) hend[w * 32 + lane] = hp;
+        __syncthreads();
+        // incoming G = g_{k0-1}: scan over the segments below
+        double G = 0.0;
+        for (int sgm = 0; sgm < w; ++sgm)
+            G = __fma_rn(tpf[min(nz, (sgm + 1) * SEG) - 1], G, hend[sgm * 32 + lane]);
+        // ---- fix-up + local backward: y_k = g_k + mu_k y_{k+1} ----
+        double yp = 0.0;
+#pragma unroll
+        for (int e = SEG - 1; e >= 0; --e) {
+            if (e < kn) {
+                const int k = k0 + e;
+                const double g = __fma_rn(tpf[k], G, r[e]);
+                yp = __fma_rn(tmu[k], yp, g);
+                r[e] = yp;
+            }
+        }
+        if (kn > 0) ybeg[w * 32 + lane] = yp;
+        __syncthreads();
+        double X = 0.0;
+        for (int sgm = nw - 1; sgm > w; --sgm) {
+            const int a = sgm * SEG;
+            if (a < nz) X = __fma_rn(tq[a], X, ybeg[sgm * 32 + lane]);
+        }
+        // ---- fix-up, relaxation, store ----
+        if (lane < nact) {
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                if (e < kn) {
+                    const int k = k0 + e;
+                    double y = __fma_rn(tq[k], X, r[e]);
+                    const long long q = pc + (long long)e * pl;
+                    if (zero_start) {
+                        if (scale != 1.0) y = y * scale;
+                    } else if (rho != 1.0) {
+                        y = y * rho;
+                        y = y + omr * u[q];
+                    }
+                    u[q] = y;
+                }
+            }
+        }
+        __syncthreads();   // hend / ybeg reuse by the next tile
     }
 }
 
@@ -331,8 +1195,8 @@ __global__ void k_invd(Lvl L, double *__restrict__ invd) {
 __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *__restrict__ cu,
                            double weight) {
     const int I = blockIdx.x * blockDim.x + threadIdx.x;
-    const int J = blockIdx.y;
-    const int k = blockIdx.z;
+    const int k = blockIdx.y;
+    const int J = blockIdx.z;
     if (I >= C.nx) return;
     const int i0 = 2 * I, j0 = 2 * J;
     double a = fu[cell(F, i0, j0, k)] + fu[cell(F, i0 + 1, j0, k)];
@@ -345,8 +1209,8 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
 __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu,
                           int add) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
-    const int k = blockIdx.z;
+    const int k = blockIdx.y;
+    const int j = blockIdx.z;
     const int c = t & 1;                 // interleave colours inside a warp
     const int h = t >> 1;
     const int i = 2 * h + ((j + F.par + c) & 1);
@@ -375,21 +1239,30 @@ __device__ __forceinline__ int hmap(int i, int n, int periodic) {
     return i;
 }
 
-// whole ring of a part that is its own neighbour in both directions
+// whole ring of a part that is its own neighbour in both directions.
+// Work items: first the two y strips (j = -1, ny; i in [-1, nx]) with i
+// fastest, then the two x strips (i = -1, nx; j in [0, ny)) with k fastest,
+// so consecutive threads touch contiguous memory.  Sources are always owned
+// cells (hmap), so both parts run concurrently.
 __global__ void k_halo_self(Lvl L, double *__restrict__ d, int px, int py) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    const int k = blockIdx.y;
-    const int nring = 2 * (L.nx + 2) + 2 * L.ny;
-    if (t >= nring) return;
-    int i, j;
-    if (t < L.nx + 2) {
-        i = t - 1; j = -1;
-    } else if (t < 2 * (L.nx + 2)) {
-        i = t - (L.nx + 2) - 1; j = L.ny;
-    } else if (t < 2 * (L.nx + 2) + L.ny) {
-        i = -1; j = t - 2 * (L.nx + 2);
+    const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int w = 2 * (L.nx + 2);
+    const long long ny_items = (long long)w * L.nz;
+    const long long nx_items = 2LL * L.ny * L.nz;
+    int i, j, k;
+    if (t < ny_items) {
+        const int q = (int)(t % w);
+        k = (int)(t / w);
+        i = (q % (L.nx + 2)) - 1;
+        j = (q < L.nx + 2) ? -1 : L.ny;
+    } else if (t < ny_items + nx_items) {
+        const long long u2 = t - ny_items;
+        k = (int)(u2 % L.nz);
+        const int r = (int)(u2 / L.nz);
+        j = r % L.ny;
+        i = (r < L.ny) ? -1 : L.nx;
     } else {
-        i = L.nx; j = t - 2 * (L.nx + 2) - L.ny;
+        return;
     }
     d[cell(L, i, j, k)] = d[cell(L, hmap(i, L.nx, px), hmap(j, L.ny, py), k)];
 }
@@ -435,7 +1308,7 @@ __global__ void k_unpack_face(Lvl L, double *__restrict__ d, int face, const dou
 // ---------------------------------------------------------------------------
 // reductions and BLAS-1 (partition.py:138-155, 267-286)
 // ---------------------------------------------------------------------------
-// Owned cells enumerated as rows (c, k, j) x h; block b takes rows b,
+// Owned cells enumerated as rows (c, j, k) x h; block b takes rows b,
 // b+grid, ...; fixed grid => fixed summation order (deterministic).
 __global__ void __launch_bounds__(256)
 k_dot(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
@@ -444,9 +1317,9 @@ k_dot(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
     const int nrows = 2 * L.nz * L.ny;
     double s = 0.0;
     for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
-        const int j = r % L.ny;
-        const int ck = r / L.ny;
-        const int k = ck % L.nz, c = ck / L.nz;
+        const int k = r % L.nz;
+        const int cj = r / L.nz;
+        const int j = cj % L.ny, c = cj / L.ny;
         const int s0 = (j + L.par + c) & 1;
         const long long base = at(L, c, k, j, 0);
         for (int h = threadIdx.x; h < rowlen; h += blockDim.x) {
@@ -481,19 +1354,18 @@ __global__ void k_cg_direction(long long n, const double *__restrict__ num,
 
 // u += alpha p ; r -= alpha q over the full allocation (halo included, as
 // DistField.add_scaled, partition.py:145-148); partial ||r||^2 over owned.
-// Rows of the allocation are (c, k, jj) with jj in [0, ny+2), pitch wide.
+// Rows of the allocation are (c, jj, k) with jj in [0, ny+2), pitch wide.
 __global__ void __launch_bounds__(256)
 k_cg_update(Lvl L, const double *__restrict__ num, const double *__restrict__ den,
             const double *__restrict__ p, const double *__restrict__ q, double *__restrict__ u,
             double *__restrict__ r, double *__restrict__ partials) {
     const double alpha = num[0] / den[0];
     const double malpha = -alpha;
-    const int rows_per_plane = L.ny + 2;
-    const int nrows = 2 * L.nz * rows_per_plane;
+    const int nrows = 2 * (L.ny + 2) * L.nz;
     double s = 0.0;
     for (int row = blockIdx.x; row < nrows; row += gridDim.x) {
-        const int jj = row % rows_per_plane;
-        const int c = row / (rows_per_plane * L.nz);
+        const int jj = (row / L.nz) % (L.ny + 2);
+        const int c = row / ((L.ny + 2) * L.nz);
         const int j = jj - 1;
         const int s0 = (j + L.par + c) & 1;
         const long long base = (long long)row * L.pitch;
@@ -517,7 +1389,7 @@ k_cg_update(Lvl L, const double *__restrict__ num, const double *__restrict__ de
 // ---------------------------------------------------------------------------
 __global__ void k_from_ref(Lvl L, const double *__restrict__ src, double *__restrict__ d) {
     __shared__ double tile[32][33];
-    const int i0 = blockIdx.x * 32, k0 = blockIdx.z * 32, j = blockIdx.y;
+    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     for (int r = ty; r < 32; r += 8) {
         const int i = i0 + r, k = k0 + tx;
@@ -532,7 +1404,7 @@ __global__ void k_from_ref(Lvl L, const double *__restrict__ src, double *__rest
 
 __global__ void k_to_ref(Lvl L, const double *__restrict__ d, double *__restrict__ dst) {
     __shared__ double tile[32][33];
-    const int i0 = blockIdx.x * 32, k0 = blockIdx.z * 32, j = blockIdx.y;
+    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
     const int tx = threadIdx.x, ty = threadIdx.y;
     for (int r = ty; r < 32; r += 8) {
         const int i = i0 + tx, k = k0 + r;
@@ -548,18 +1420,96 @@ __global__ void k_to_ref(Lvl L, const double *__restrict__ d, double *__restrict
 // ===========================================================================
 // host launchers
 // ===========================================================================
+static int g_sms = 0;
+static int sm_count() {
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+
 static inline dim3 apply_grid(const Lvl &L) {
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     return dim3(hx, (L.ny + AP_TY - 1) / AP_TY);
 }
 
+static inline int k_chunk(const Lvl &L, long long columns, int want_blocks_per_sm_x148) {
+    // split k so that small levels still fill the machine
+    int kc = L.nz;
+    while (kc > 8 && columns * (L.nz / kc) < want_blocks_per_sm_x148) kc >>= 1;
+    return kc;
+}
+
+template <int KB>
+static cudaError_t launch_apply_kb(const Lvl &L, const double *u, const double *f, double *out,
+                                  int mode, double *partials, int *nparts, cudaStream_t st) {
+    const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
+    const bool norm = partials != nullptr;
+    const int hx = g0.x, jy = g0.y;
+    const int ntiles = hx * jy * ((L.nz + KB - 1) / KB);
+    int occ = 1;
+#define PMG_OCC(U, M, N) \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_b<U, M, N, KB>, 32 * 2 * AP_TY, 0)
+    if (L.uniform) {
+        if (mode == 0) PMG_OCC(true, 0, false);
+        else if (mode == 1) { if (norm) PMG_OCC(true, 1, true); else PMG_OCC(true, 1, false); }
+        else PMG_OCC(true, 2, true);
+    } else {
+        if (mode == 0) PMG_OCC(false, 0, false);
+        else if (mode == 1) { if (norm) PMG_OCC(false, 1, true); else PMG_OCC(false, 1, false); }
+        else PMG_OCC(false, 2, true);
+    }
+#undef PMG_OCC
+    const int cap = sm_count() * (occ > 0 ? occ : 1);
+    const int grid = ntiles < cap ? ntiles : cap;
+    *nparts = grid;
+#define PMG_AB(U, M, N) \
+    k_apply_b<U, M, N, KB><<<grid, b, 0, st>>>(L, u, f, out, partials, hx, jy, ntiles)
+    if (L.uniform) {
+        if (mode == 0) PMG_AB(true, 0, false);
+        else if (mode == 1) { if (norm) PMG_AB(true, 1, true); else PMG_AB(true, 1, false); }
+        else PMG_AB(true, 2, true);
+    } else {
+        if (mode == 0) PMG_AB(false, 0, false);
+        else if (mode == 1) { if (norm) PMG_AB(false, 1, true); else PMG_AB(false, 1, false); }
+        else PMG_AB(false, 2, true);
+    }
+#undef PMG_AB
+    return cudaGetLastError();
+}
+
+static int apply_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PMG_APPLY_VARIANT");
+        v = (e && e[0] == 'l') ? 1 : 0;   // 0: batched (default), 1: k-loop
+    }
+    return v;
+}
+
 cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double *out, int mode,
                          double *partials, int *nparts, cudaStream_t st) {
-    const dim3 g = apply_grid(L), b(32, 2 * AP_TY);
-    *nparts = g.x * g.y;
-    if ((long long)g.x * g.y > PARTIALS) return cudaErrorInvalidValue;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
-#define PMG_AP(U, M, N) k_apply<U, M, N><<<g, b, 0, st>>>(L, u, f, out, partials)
+    if (apply_variant() == 0) {
+        static int kbsel = -1;
+        if (kbsel < 0) {
+            const char *e = getenv("PMG_APPLY_KB");
+            kbsel = e ? atoi(e) : 4;
+        }
+        if (kbsel == 8) return launch_apply_kb<8>(L, u, f, out, mode, partials, nparts, st);
+        if (kbsel == 2) return launch_apply_kb<2>(L, u, f, out, mode, partials, nparts, st);
+        return launch_apply_kb<4>(L, u, f, out, mode, partials, nparts, st);
+    }
+    const int kc = k_chunk(L, (long long)L.nx * L.ny, 148 * 2048 * 2);
+    const dim3 g(g0.x, g0.y, (L.nz + kc - 1) / kc);
+    *nparts = g.x * g.y * g.z;
+    if ((long long)g.x * g.y * g.z > PARTIALS) return cudaErrorInvalidValue;
+#define PMG_AP(U, M, N) k_apply<U, M, N><<<g, b, 0, st>>>(L, u, f, out, partials, kc)
     if (L.uniform) {
         if (mode == 0) PMG_AP(true, 0, false);
         else if (mode == 1) { if (norm) PMG_AP(true, 1, true); else PMG_AP(true, 1, false); }
@@ -574,36 +1524,138 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
 }
 
 cudaError_t launch_finalize(const double *partials, int n, double *out, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_finalize<<<1, 1024, 0, st>>>(partials, n, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u, const double *f,
                                      double *cf, cudaStream_t st) {
-    const dim3 b(32, 8), g((C.nx + 31) / 32, (C.ny + 7) / 8);
-    if (F.uniform) k_residual_restrict<true><<<g, b, 0, st>>>(F, C, u, f, cf);
-    else k_residual_restrict<false><<<g, b, 0, st>>>(F, C, u, f, cf);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int kc = k_chunk(F, (long long)C.nx * C.ny, 148 * 2048 * 2);
+    const dim3 b(32, 8), g((C.nx + 31) / 32, (F.nz + kc - 1) / kc, (C.ny + 7) / 8);
+    if (F.uniform) k_residual_restrict<true><<<g, b, 0, st>>>(F, C, u, f, cf, kc);
+    else k_residual_restrict<false><<<g, b, 0, st>>>(F, C, u, f, cf, kc);
     return cudaGetLastError();
 }
 
 size_t half_sweep_smem(const Lvl &L, bool need_old) {
     size_t n = (size_t)L.nz * 32;
-    return sizeof(double) * (n + (need_old ? n : 0) + (L.uniform ? 0 : n));
+    return sizeof(double) * (n + (need_old ? n : 0) + (L.uniform ? 0 : n) + 2 * L.nz + 1);
+}
+
+template <bool UNI, int SEG>
+static void hs_reg(const Lvl &L, dim3 g, int nw, double *u, const double *f, int color, double rho,
+                   int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
+    const size_t sm = sizeof(double) * (3 * L.nz + 1);
+    k_half_sweep_reg<UNI, SEG><<<g, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero,
+                                                      post_scale);
+}
+
+static int hs_variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PMG_HS_VARIANT");
+        // 3: TMA solver warps (default), 2: producer/solver pipeline,
+        // 0: registers, 1: shared-memory
+        v = (e && e[0] == 't') ? 3 : (e && e[0] == 'r') ? 0 : (e && e[0] == 'p') ? 2 : 1;
+    }
+    return v;
 }
 
 cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int color, double rho,
                               int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
-    const bool need_old = !zero_start && rho != 1.0;
-    const size_t sm = half_sweep_smem(L, need_old);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
-    const int nw = L.nz >= 8 ? 8 : (L.nz >= 4 ? 4 : (L.nz >= 2 ? 2 : 1));
-    const dim3 b(32 * nw);
+    if (!g_smoother_exact && L.uniform && L.seg) {
+        const int nw = (L.nz + L.seg - 1) / L.seg;
+        const size_t sm = sizeof(double) * (6 * (size_t)L.nz + 2 * 8 * 32);
+        const int ntiles = hx * L.ny;
+        int occ = 1;
+        switch (L.seg) {
+        case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<4>, 32 * nw, sm); break;
+        case 8: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<8>, 32 * nw, sm); break;
+        case 16: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<16>, 32 * nw, sm); break;
+        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<32>, 32 * nw, sm); break;
+        }
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        const int grid = ntiles < cap ? ntiles : cap;
+#define PMG_SEG(S) k_half_sweep_seg<S><<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, \
+                                                                   nbr_zero, post_scale, ntiles, hx)
+        switch (L.seg) {
+        case 4: PMG_SEG(4); break;
+        case 8: PMG_SEG(8); break;
+        case 16: PMG_SEG(16); break;
+        default: PMG_SEG(32); break;
+        }
+#undef PMG_SEG
+        return cudaGetLastError();
+    }
+    if (hs_variant() == 3 && L.uniform) {
+        const int tab = (3 * L.nz + 1 + 1) & ~1;
+        const size_t per_warp = (size_t)L.nz * 32 + TM_R * TM_ROW;
+        const size_t budget = 225 * 1024;
+        int nw = (int)((budget / 8 - tab) / (per_warp + TM_R));
+        if (nw > 4) nw = 4;
+        if (nw >= 1) {
+            const size_t sm = 8 * (tab + nw * per_warp) + 8 * (size_t)nw * TM_R;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_half_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024);
+                attr = true;
+            }
+            const int ntiles = hx * L.ny;
+            int grid = (ntiles + nw - 1) / nw;
+            if (grid > 148) grid = 148;
+            k_half_sweep_tma<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero,
+                                                        post_scale, ntiles, hx);
+            return cudaGetLastError();
+        }
+    }
+    if (hs_variant() == 2 && L.uniform) {
+        const size_t sm = sizeof(double) * (((3 * L.nz + 1 + 3) & ~3) + (size_t)PP_NBUF * L.nz * 32);
+        if (sm <= 220 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_half_sweep_pipe,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                attr = true;
+            }
+            const int ntiles = hx * L.ny;
+            const int grid = ntiles < 148 ? ntiles : 148;
+            k_half_sweep_pipe<<<grid, PP_THREADS, sm, st>>>(L, u, f, color, rho, zero_start,
+                                                            nbr_zero, post_scale, ntiles, hx);
+            return cudaGetLastError();
+        }
+    }
+    if (hs_variant() != 1 && L.nz <= 256) {
+        // SEG: k levels per warp, NW = ceil(nz / SEG) <= 8 warps
+        int seg = 4;
+        while (seg < 32 && (L.nz + seg - 1) / seg > 8) seg <<= 1;
+        const int nw = (L.nz + seg - 1) / seg;
+#define PMG_HS(U)                                                                        \
+        switch (seg) {                                                                    \
+        case 4: hs_reg<U, 4>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break;   \
+        case 8: hs_reg<U, 8>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break;   \
+        case 16: hs_reg<U, 16>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break; \
+        default: hs_reg<U, 32>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break; \
+        }
+        if (L.uniform) { PMG_HS(true) } else { PMG_HS(false) }
+#undef PMG_HS
+        return cudaGetLastError();
+    }
+    const bool need_old = !zero_start && rho != 1.0;
+    const size_t sm = half_sweep_smem(L, need_old);
+    const dim3 b(HS_THREADS);
     static bool attr_set[2] = {false, false};
     if (L.uniform) {
         if (!attr_set[0]) {
             cudaFuncSetAttribute(k_half_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024);
+            cudaFuncSetAttribute(k_half_sweep<true>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             attr_set[0] = true;
         }
         k_half_sweep<true><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
@@ -611,6 +1663,8 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
         if (!attr_set[1]) {
             cudaFuncSetAttribute(k_half_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  200 * 1024);
+            cudaFuncSetAttribute(k_half_sweep<false>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             attr_set[1] = true;
         }
         k_half_sweep<false><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
@@ -619,32 +1673,37 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
 }
 
 cudaError_t launch_invd(const Lvl &L, double *invd, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_invd<<<dim3((L.nx + 127) / 128, L.ny), 128, 0, st>>>(L, invd);
     return cudaGetLastError();
 }
 
 cudaError_t launch_restrict(const Lvl &F, const Lvl &C, const double *fu, double *cu, double w,
                             cudaStream_t st) {
-    k_restrict<<<dim3((C.nx + 127) / 128, C.ny, C.nz), 128, 0, st>>>(F, C, fu, cu, w);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_restrict<<<dim3((C.nx + 127) / 128, C.nz, C.ny), 128, 0, st>>>(F, C, fu, cu, w);
     return cudaGetLastError();
 }
 
 cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double *fu, int add,
                            cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const int n2 = 2 * ((F.nx + 1) / 2);
-    k_prolong<<<dim3((n2 + 127) / 128, F.ny, F.nz), 128, 0, st>>>(F, C, cu, fu, add);
+    k_prolong<<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add);
     return cudaGetLastError();
 }
 
 cudaError_t launch_halo_self(const Lvl &L, double *d, int px, int py, cudaStream_t st) {
-    const int nring = 2 * (L.nx + 2) + 2 * L.ny;
-    k_halo_self<<<dim3((nring + 127) / 128, L.nz), 128, 0, st>>>(L, d, px, py);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const long long n = 2LL * (L.nx + 2) * L.nz + 2LL * L.ny * L.nz;
+    k_halo_self<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(L, d, px, py);
     return cudaGetLastError();
 }
 
 int face_len(const Lvl &L, int face) { return face < 2 ? L.ny : L.nx + 2; }
 
 cudaError_t launch_pack(const Lvl &L, const double *d, int face, double *buf, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const int len = face_len(L, face);
     k_pack_face<<<dim3((len + 127) / 128, L.nz), 128, 0, st>>>(L, d, face, buf, len);
     return cudaGetLastError();
@@ -652,20 +1711,10 @@ cudaError_t launch_pack(const Lvl &L, const double *d, int face, double *buf, cu
 
 cudaError_t launch_unpack(const Lvl &L, double *d, int face, const double *buf, int mirror,
                           cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const int len = face_len(L, face);
     k_unpack_face<<<dim3((len + 127) / 128, L.nz), 128, 0, st>>>(L, d, face, buf, len, mirror);
     return cudaGetLastError();
-}
-
-static int g_sms = 0;
-static int sm_count() {
-    if (!g_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_sms <= 0) g_sms = 148;
-    }
-    return g_sms;
 }
 
 static inline int stream_blocks(long long n) {
@@ -676,6 +1725,7 @@ static inline int stream_blocks(long long n) {
 
 cudaError_t launch_dot(const Lvl &L, const double *a, const double *b, double *partials, int *np,
                        cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const long long n = 2LL * L.nz * L.ny * ((L.nx + 1) >> 1);
     int g = stream_blocks(n);
     if (g > 2 * L.nz * L.ny) g = 2 * L.nz * L.ny;
@@ -685,17 +1735,20 @@ cudaError_t launch_dot(const Lvl &L, const double *a, const double *b, double *p
 }
 
 cudaError_t launch_axpy(long long n, double a, const double *x, double *y, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_axpy<<<stream_blocks(n), 256, 0, st>>>(n, a, x, y);
     return cudaGetLastError();
 }
 
 cudaError_t launch_xpby(long long n, const double *x, double b, double *y, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_xpby<<<stream_blocks(n), 256, 0, st>>>(n, x, b, y);
     return cudaGetLastError();
 }
 
 cudaError_t launch_cg_direction(long long n, const double *num, const double *den, const double *z,
                                 double *p, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     k_cg_direction<<<stream_blocks(n), 256, 0, st>>>(n, num, den, z, p);
     return cudaGetLastError();
 }
@@ -703,6 +1756,7 @@ cudaError_t launch_cg_direction(long long n, const double *num, const double *de
 cudaError_t launch_cg_update(const Lvl &L, const double *num, const double *den,
                              const double *p, const double *q, double *u, double *r,
                              double *partials, int *np, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const long long n = 2LL * L.cstride;
     int g = stream_blocks(n);
     if (g > 2 * L.nz * (L.ny + 2)) g = 2 * L.nz * (L.ny + 2);
@@ -712,12 +1766,14 @@ cudaError_t launch_cg_update(const Lvl &L, const double *num, const double *den,
 }
 
 cudaError_t launch_from_ref(const Lvl &L, const double *src, double *d, cudaStream_t st) {
-    k_from_ref<<<dim3((L.nx + 31) / 32, L.ny, (L.nz + 31) / 32), dim3(32, 8), 0, st>>>(L, src, d);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_from_ref<<<dim3((L.nx + 31) / 32, (L.nz + 31) / 32, L.ny), dim3(32, 8), 0, st>>>(L, src, d);
     return cudaGetLastError();
 }
 
 cudaError_t launch_to_ref(const Lvl &L, const double *d, double *dst, cudaStream_t st) {
-    k_to_ref<<<dim3((L.nx + 31) / 32, L.ny, (L.nz + 31) / 32), dim3(32, 8), 0, st>>>(L, d, dst);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_to_ref<<<dim3((L.nx + 31) / 32, (L.nz + 31) / 32, L.ny), dim3(32, 8), 0, st>>>(L, d, dst);
     return cudaGetLastError();
 }
 

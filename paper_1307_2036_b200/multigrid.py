@@ -274,10 +274,13 @@ class _CycleGraph:
             fine.op.residual_norm2_dev(s0.f, s0.u, None, self.res)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
+        from .partition import lib
+        l0 = lib().pmg_launch_count()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             v_cycle(hier, cfg, scratch)
             fine.op.residual_norm2_dev(s0.f, s0.u, None, self.res)
+        self.launches = lib().pmg_launch_count() - l0   # library kernels per replay
 
     def replay(self) -> torch.Tensor:
         self.graph.replay()

@@ -246,7 +246,18 @@ class DevField:
         call("pmg_to_ref_layout", g.h, self.ptr, C.c_void_p(buf.data_ptr()), _stream())
         return buf.cpu().numpy().reshape(g.mx, g.my, g.nz)
 
-    def load_owned(self, arr) -> None:
+    def owned_to(self, host: torch.Tensor, staging: torch.Tensor | None = None) -> None:
+        """Copy the owned cells into a preallocated (pinned) host tensor of
+        mx*my*nz doubles, reference layout; synchronous."""
+        g = self.geom
+        n = g.mx * g.my * g.nz
+        buf = staging if staging is not None else torch.empty(n, dtype=torch.float64,
+                                                              device=self.data.device)
+        call("pmg_to_ref_layout", g.h, self.ptr, C.c_void_p(buf.data_ptr()), _stream())
+        host.view(-1).copy_(buf[:n], non_blocking=host.is_pinned())
+        torch.cuda.current_stream().synchronize()
+
+    def load_owned(self, arr, staging: torch.Tensor | None = None) -> None:
         """Write an (mx, my, nz) block (numpy or torch, host or device)."""
         g = self.geom
         if isinstance(arr, np.ndarray):
@@ -256,8 +267,9 @@ class DevField:
         if t.numel() != g.mx * g.my * g.nz:
             raise ValueError("block does not match the part size")
         if t.device.type != "cuda":
-            dev = torch.empty(t.numel(), dtype=torch.float64, device=self.data.device)
-            dev.copy_(t.reshape(-1), non_blocking=t.is_pinned())
+            dev = staging if staging is not None else torch.empty(
+                t.numel(), dtype=torch.float64, device=self.data.device)
+            dev[:t.numel()].copy_(t.reshape(-1), non_blocking=t.is_pinned())
             t = dev
         call("pmg_from_ref_layout", g.h, C.c_void_p(t.data_ptr()), self.ptr, _stream())
 
@@ -434,6 +446,19 @@ def scatter_owned(arr, layout: LevelLayout) -> DistField:
             f.load_owned(arr)
         else:
             f.load_owned(arr[i0:i0 + layout.mx, j0:j0 + layout.my, :])
+    return df
+
+
+def scatter_block(block, layout: LevelLayout, out: DistField | None = None,
+                  staging: torch.Tensor | None = None) -> DistField:
+    """Field whose (single) local part is ``block`` (mx, my, nz): the
+    multi-rank entry point, each rank passing only its own columns."""
+    if len(layout.local_workers) != 1:
+        raise ValueError("scatter_block needs exactly one local part")
+    nz = int(block.shape[2])
+    df = out if out is not None else DistField.zeros(layout, nz)
+    (w, f), = df.parts.items()
+    f.load_owned(block, staging)
     return df
 
 

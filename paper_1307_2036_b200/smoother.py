@@ -11,14 +11,39 @@ order (bit-identical results).
 
 from __future__ import annotations
 
+from contextlib import contextmanager
 from dataclasses import dataclass
 
-from ._lib import call
+from ._lib import call, load
 from .partition import DistField, _stream, halo_exchange
 from .stencil import PanelOperator
 
 RED, BLACK = 0, 1
 ORDERINGS = ("redblack", "symmetric", "jacobi")
+
+
+def set_exact_smoother(exact: bool) -> None:
+    """Select the column solver of every half-sweep in this process:
+    exact=False (default) -- k-segmented solve (reassociated elimination,
+    ~1e-15 relative from the sequential recurrence), the fast path;
+    exact=True -- the sequential Thomas recurrence of smoother.py:151-161,
+    bit-identical to the reference.  Variable-coefficient levels always
+    run the exact solver."""
+    call("pmg_set_smoother_mode", 1 if exact else 0)
+
+
+def exact_smoother_enabled() -> bool:
+    return bool(load().pmg_get_smoother_mode())
+
+
+@contextmanager
+def exact_smoother(exact: bool = True):
+    prev = exact_smoother_enabled()
+    set_exact_smoother(exact)
+    try:
+        yield
+    finally:
+        set_exact_smoother(prev)
 
 
 @dataclass(frozen=True)

@@ -26,6 +26,13 @@ def uni(shape, seed):
     return np.random.default_rng(seed).uniform(-1.0, 1.0, size=shape)
 
 
+def hist_err(h, ref):
+    """Max relative history deviation; entries near the rounding floor of
+    the residual evaluation (~1e-13 ||r0||) are compared absolutely."""
+    h, ref = np.asarray(h, dtype=float), np.asarray(ref, dtype=float)
+    return float(np.max(np.abs(h - ref) / (ref + 1e-13 * ref[0])))
+
+
 @pytest.fixture(scope="module")
 def pmg():
     if not torch.cuda.is_available():
@@ -67,6 +74,29 @@ OPS = ["ops_periodic", "ops_neumann", "ops_variable", "ops_config"]
 @pytest.mark.parametrize("workers", [1, 4])
 @pytest.mark.parametrize("name", OPS)
 def test_ops_bitwise(pmg, name, workers):
+    """Exact smoother mode: every operator / smoother / transfer output is
+    bit-identical to the reference."""
+    with pmg.exact_smoother():
+        _ops_check(pmg, name, workers, 0.0)
+
+
+@pytest.mark.parametrize("workers", [1, 4])
+@pytest.mark.parametrize("name", OPS)
+def test_ops_fast_smoother(pmg, name, workers):
+    """Default (fast, k-segmented) smoother: the reference's own half-sweep
+    tolerance (tests/test_smoother.py:48 uses 1e-12 against a column-wise
+    Thomas solve); operator and transfers stay bit-identical."""
+    with pmg.exact_smoother(False):
+        _ops_check(pmg, name, workers, 1e-12)
+
+
+def _close(got, ref, tol):
+    if tol == 0.0:
+        return np.array_equal(got, ref)
+    return np.max(np.abs(got - ref)) <= tol * max(1.0, np.max(np.abs(ref)))
+
+
+def _ops_check(pmg, name, workers, tol):
     g, grid, params, cfg, hier = setup(pmg, name, workers)
     nx, nz = grid.nx, grid.nz
     fine, coarse = hier.levels[0], hier.levels[1]
@@ -80,15 +110,15 @@ def test_ops_bitwise(pmg, name, workers):
     for rho in (1.0, 1.4):
         uu = field(pmg, ug, lay)
         sm.half_sweep(uu, f, 0, rho)
-        assert np.array_equal(G(uu), g[f"half_red_rho{rho}"])
+        assert _close(G(uu), g[f"half_red_rho{rho}"], tol)
         pmg.halo_exchange(uu)
         sm.half_sweep(uu, f, 1, rho)
-        assert np.array_equal(G(uu), g[f"half_black_rho{rho}"])
+        assert _close(G(uu), g[f"half_black_rho{rho}"], tol)
     uu = field(pmg, ug, lay)
     sm.sweep(uu, f, nsweeps=2, rho=1.0)
-    assert np.array_equal(G(uu), g["sweep2"])
+    assert _close(G(uu), g["sweep2"], tol)
     for rho in (1.0, 1.3):
-        assert np.array_equal(G(sm.ssor_apply(f, rho)), g[f"ssor_rho{rho}"])
+        assert _close(G(sm.ssor_apply(f, rho)), g[f"ssor_rho{rho}"], tol)
     assert np.array_equal(G(pmg.restrict(u, fine, coarse)), g["restrict_mean"])
     cd = field(pmg, uni((nx // 2, nx // 2, nz), 3), coarse.layout)
     assert np.array_equal(G(pmg.prolong(cd, coarse, fine)), g["prolong"])
@@ -98,7 +128,22 @@ def test_ops_bitwise(pmg, name, workers):
         scratch = hier.make_scratch()
         scratch[0].f.copy_from(f)
         pmg.v_cycle(hier, c2, scratch)
-        assert np.array_equal(G(scratch[0].u), g["vcycle1"])
+        assert _close(G(scratch[0].u), g["vcycle1"], tol)
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_solvers_exact_mode_vs_reference(pmg, name):
+    """Exact smoother: MG histories agree to reduction-order rounding."""
+    g, grid, params, cfg, hier = setup(pmg, name)
+    nx, nz = grid.nx, grid.nz
+    with pmg.exact_smoother():
+        u, rep = pmg.mg_solve(pmg.scatter_owned(uni((nx, nx, nz), 2), hier.fine.layout),
+                              hier, cfg)
+    ref = g["mg_history"]
+    assert rep.iterations == len(ref) - 1
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-12
+    got = pmg.gather_owned(u)
+    assert np.max(np.abs(got - g["mg_u"])) <= 1e-12 * np.max(np.abs(g["mg_u"]))
 
 
 @pytest.mark.parametrize("graph", [False, True])
@@ -111,11 +156,13 @@ def test_solvers_vs_reference(pmg, name, graph):
                        graph=graph)
     f = pmg.scatter_owned(fg, hier.fine.layout)
     u, rep = pmg.mg_solve(f, hier, cfg)
+    # fast (k-segmented) smoother: reassociated elimination -> ~1e-12;
+    # north_star bar is 1e-8
     ref = g["mg_history"]
     assert rep.iterations == len(ref) - 1
-    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-12
+    assert np.max(np.abs(np.array(rep.residual_history) - ref) / ref) <= 1e-10
     got = pmg.gather_owned(u)
-    assert np.max(np.abs(got - g["mg_u"])) <= 1e-12 * np.max(np.abs(g["mg_u"]))
+    assert np.max(np.abs(got - g["mg_u"])) <= 1e-10 * np.max(np.abs(g["mg_u"]))
     op = hier.fine.op
     pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
     uc, rc = pmg.pcg_solve(f, op, pre, eps=1e-8, maxiter=200)
@@ -246,25 +293,27 @@ def test_layout_round_trip(pmg):
 
 
 def test_rectangular_periodic_vs_oracle(pmg):
-    """nx != ny periodic grids (the 2- and 8-GPU global grids of configs[3])."""
+    """nx != ny periodic grids (the 2- and 8-GPU global grids of configs[3]),
+    split into 1, 2 and 8 parts, against the oracle on the same grid."""
     from oracle import port
     nx, ny, nz = 32, 16, 8
-    lv = port.uniform_levels(nz, 0.01)
+    lv = port.uniform_levels(nz, 1.0)
     fg = uni((nx, ny, nz), 5)
-    h = port.Hierarchy(nx, ny, 3, lambda a, b: port.config_factors(a, b, lv), 1e-3, 1.0)
+    h = port.Hierarchy(nx, ny, 3, lambda a, b: port.config_factors(a, b, lv), 0.7, 1.3)
     ou, orep = port.mg_solve(h, fg)
-    grid = pmg.periodic_box(nx, nz, 0.01, ny=ny)
-    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
-    for p in (1, 2, 8):
-        cfg = pmg.MGConfig(policy="explicit", explicit_levels=3)
-        dec = pmg.Decomposition(nx, p, ny=ny)
-        hier = pmg.build_hierarchy(grid, params, cfg, dec)
-        u, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
-        assert rep.iterations == orep.iterations
-        oh = np.array(orep.residual_history)
-        assert np.max(np.abs(np.array(rep.residual_history) - oh) / oh) <= 1e-10
-        ug = pmg.gather_owned(u)
-        assert np.max(np.abs(ug - ou[1:-1, 1:-1, :])) <= 1e-10 * np.max(np.abs(ug))
+    grid = pmg.periodic_box(nx, nz, 1.0, lv, ny=ny)
+    params = pmg.toy_parameters(nx, nz, 0.7, 1.3)
+    for exact, tol in ((True, 1e-10), (False, 1e-8)):
+        for p in (1, 2, 8):
+            cfg = pmg.MGConfig(policy="explicit", explicit_levels=3)
+            dec = pmg.Decomposition(nx, p, ny=ny)
+            hier = pmg.build_hierarchy(grid, params, cfg, dec)
+            with pmg.exact_smoother(exact):
+                u, rep = pmg.mg_solve(pmg.scatter_owned(fg, hier.fine.layout), hier, cfg)
+            assert rep.iterations == orep.iterations > 3
+            assert hist_err(rep.residual_history, orep.residual_history) <= tol
+            ug = pmg.gather_owned(u)
+            assert np.max(np.abs(ug - ou[1:-1, 1:-1, :])) <= tol * np.max(np.abs(ug))
 
 
 def test_zero_rhs_and_breakdown(pmg):

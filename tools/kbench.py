@@ -1,0 +1,69 @@
+"""Dev micro-benchmark: fine-level kernel times at configs[1] size (or
+--nx/--nz), CUDA events, L2-cold (fields >> L2)."""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1307_2036_b200 as pmg  # noqa: E402
+from paper_1307_2036_b200 import configs, multigrid as mg  # noqa: E402
+
+
+def timeit(fn, reps=20):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--nx", type=int, default=1024)
+ap.add_argument("--nz", type=int, default=128)
+ap.add_argument("--levels", type=int, default=7)
+ap.add_argument("--variable", action="store_true")
+a = ap.parse_args()
+prob = configs.Problem(a.nx, a.nx, a.nz, 1e-3, 1.0, a.levels, stretch=1.05 if a.variable else None,
+                       variable_omega=a.variable)
+cfg = prob.mg_config()
+hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
+sc = hier.persistent_scratch()
+f = pmg.scatter_owned(configs.rhs(a.nx, a.nx, a.nz, 0), hier.fine.layout)
+sc[0].f.copy_from(f)
+out = {"variant": os.environ.get("PMG_HS_VARIANT", "reg")}
+res = torch.zeros(1, dtype=torch.float64, device="cuda")
+for c, lev in enumerate(hier.levels):
+    s = sc[c]
+    n = lev.layout.nx * lev.layout.ny * a.nz
+    row = {}
+    flip = [0]
+
+    def hs():
+        lev.smoother.half_sweep(s.u, s.f, flip[0] & 1, 1.0)
+        flip[0] += 1
+    t = timeit(hs)
+    row["half_sweep"] = (round(t * 1e3, 1), round(12 * n / t / 1e6))
+    t = timeit(lambda: lev.op.residual_norm2_dev(s.f, s.u, None, res))
+    row["resid_norm"] = (round(t * 1e3, 1), round(16 * n / t / 1e6))
+    if c + 1 < len(hier.levels):
+        co = hier.levels[c + 1]
+        t = timeit(lambda: mg._residual_restrict(lev, co, s.f, s.u, sc[c + 1].f))
+        row["resid_restrict"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
+        t = timeit(lambda: mg._prolong_add(sc[c + 1].u, co, lev, s.u))
+        row["prolong_add"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
+    t = timeit(lambda: pmg.halo_exchange(s.u))
+    row["halo"] = round(t * 1e3, 1)
+    print(f"L{c} nx={lev.layout.nx}: " + json.dumps(row), flush=True)
+# full solve
+for _ in range(2):
+    u, rep = pmg.mg_solve(f, hier, cfg)
+t = timeit(lambda: pmg.mg_solve(f, hier, cfg, out=u), 5)
+print(json.dumps({"solve_ms": round(t, 3), "iters": rep.iterations,
+                  "hist": rep.residual_history}))
