@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -190,7 +191,11 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
         // segment from its start / to its end (segments of L.seg levels)
         int seg = 4;
         while (seg < 32 && (nz + seg - 1) / seg > 8) seg <<= 1;
-        L.seg = ((nz + seg - 1) / seg <= 8) ? seg : 0;
+        if (const char *es = getenv("PMG_SEG")) {   // tuning override
+            const int v = atoi(es);
+            if (v == 4 || v == 8 || v == 16 || v == 32) seg = v;
+        }
+        L.seg = ((nz + seg - 1) / seg <= 16) ? seg : 0;
         lv->h_seg.assign(4 * (size_t)nz, 0.0);
         double *al = lv->h_seg.data(), *mu = al + nz, *pf = mu + nz, *qq = pf + nz;
         for (int k = 0; k < nz; ++k) {

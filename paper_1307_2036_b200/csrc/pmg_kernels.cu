@@ -143,91 +143,217 @@ k_apply(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
 // sequential-k version left the SM latency-bound at ~30% of HBM peak).
 // Same arithmetic, same order.
 // ---------------------------------------------------------------------------
+// Column walker shared by the batched stencil kernels: residual / A u of
+// KB consecutive levels of one column, every load of the batch issued
+// before any arithmetic.  Tables (drw, diag, band) come from shared memory.
+template <bool UNI, int MODE, int KB>
+__device__ __forceinline__ void stencil_batch(
+    const Lvl &L, const double *__restrict__ u, const double *__restrict__ f, int k0,
+    long long pc, long long pW, long long pE, long long pS, long long pN, double wxm,
+    double wxp, double wym, double wyp, double cv, double vhc, double osw,
+    const double *tdrw, const double *tdiag, const double *tband, double (&res)[KB],
+    double (&uown)[KB]) {
+    const int nz = L.nz;
+    const long long pl = L.plane;
+    double uc[KB + 2], vw[KB], ve[KB], vs[KB], vn[KB], vf[KB];
+    uc[0] = (k0 > 0) ? u[pc - pl] : 0.0;
+#pragma unroll
+    for (int t = 0; t < KB; ++t) {
+        const bool ok = k0 + t < nz;
+        const long long ko = (long long)t * pl;
+        uc[t + 1] = ok ? u[pc + ko] : 0.0;
+        vw[t] = ok ? u[pW + ko] : 0.0;
+        ve[t] = ok ? u[pE + ko] : 0.0;
+        vs[t] = ok ? u[pS + ko] : 0.0;
+        vn[t] = ok ? u[pN + ko] : 0.0;
+        if (MODE == 1) vf[t] = ok ? f[pc + ko] : 0.0;
+    }
+    uc[KB + 1] = (k0 + KB < nz) ? u[pc + (long long)KB * pl] : 0.0;
+#pragma unroll
+    for (int t = 0; t < KB; ++t) {
+        const int k = k0 + t;
+        uown[t] = uc[t + 1];
+        if (k < nz) {
+            double acc = wxm * vw[t];
+            acc = acc + wxp * ve[t];
+            acc = acc + wym * vs[t];
+            acc = acc + wyp * vn[t];
+            acc = acc * tdrw[k];
+            double d;
+            if (UNI) {
+                d = tdiag[k];
+            } else {
+                d = vhc * L.volprof[k];
+                d = d + osw * L.dr[k];
+                d = d + cv * (L.vprof[k] + L.vprof[k + 1]);
+            }
+            double r = d * uc[t + 1] - acc;
+            if (k >= 1) r = r - (UNI ? tband[k] : cv * L.vprof[k]) * uc[t];
+            if (k + 1 < nz) r = r - (UNI ? tband[k + 1] : cv * L.vprof[k + 1]) * uc[t + 2];
+            if (MODE == 1) r = vf[t] - r;
+            res[t] = r;
+        } else {
+            res[t] = 0.0;
+        }
+    }
+}
+
+__device__ __forceinline__ void load_stencil_tables(const Lvl &L, double *tdrw, double *tdiag,
+                                                    double *tband) {
+    for (int t = threadIdx.x + blockDim.x * threadIdx.y; t <= L.nz;
+         t += blockDim.x * blockDim.y) {
+        if (t < L.nz) tdrw[t] = L.drw[t];
+        if (L.uniform) {
+            if (t < L.nz) tdiag[t] = L.diag1[t];
+            tband[t] = L.band1[t];
+        }
+    }
+}
+
+template <bool UNI>
+__device__ __forceinline__ void column_coeffs(const Lvl &L, int i, int j, double &wxm, double &wxp,
+                                              double &wym, double &wyp, double &cv, double &vhc,
+                                              double &osw) {
+    if (UNI) {
+        wxm = wxp = L.wx0;
+        wym = wyp = L.wy0;
+        cv = L.csub0;
+        vhc = osw = 0.0;
+    } else {
+        wxm = L.wx[(long long)j * (L.nx + 1) + i];
+        wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
+        wym = L.wy[(long long)j * L.nx + i];
+        wyp = L.wy[(long long)(j + 1) * L.nx + i];
+        cv = L.vcoef * L.av[(long long)j * L.nx + i];
+        vhc = L.vh[(long long)j * L.nx + i];
+        osw = L.omega2 * L.sumw[(long long)j * L.nx + i];
+    }
+}
+
+// Persistent batched apply / residual: tile = 32 columns x AP_TY rows x 2
+// colours; each thread walks its whole column in batches of KB levels.
 template <bool UNI, int MODE, bool NORM, int KB>
-__global__ void __launch_bounds__(32 * 2 * AP_TY)
+__global__ void __launch_bounds__(32 * 2 * AP_TY, 3)
 k_apply_b(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
-          double *__restrict__ out, double *__restrict__ partials, int hx, int jy, int ntiles) {
+          double *__restrict__ out, double *__restrict__ partials, int hx, int jy, int ntiles,
+          int kcs) {
+    __shared__ double tdrw[256], tdiag[256], tband[257];
+    load_stencil_tables(L, tdrw, tdiag, tband);
+    __syncthreads();
     const int lane = threadIdx.x;
     const int c = threadIdx.y & 1;
     const int nz = L.nz;
     const int o = c ^ 1;
     const long long pl = L.plane;
     double acc2 = 0.0;
-    // grid-stride over tiles (h-block fastest, then k chunk, then row block:
-    // concurrently processed tiles share rows, i.e. contiguous memory)
+    // tile = (h block, row block, k chunk of kcs levels); kcs = nz on big
+    // levels (one walk per column), smaller on coarse levels to fill the GPU
+    const int nkc = (nz + kcs - 1) / kcs;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int nkc = (nz + KB - 1) / KB;
-        const int hb = tile % hx;
-        const int rest = tile / hx;
-        const int k0 = (rest % nkc) * KB;
-        const int jb = rest / nkc;
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int jb = t2 / hx;
+        const int hb = t2 - jb * hx;
         const int j = jb * AP_TY + (threadIdx.y >> 1);
         const int h = hb * 32 + lane;
         const int i = 2 * h + ((j + L.par + c) & 1);
         if (j >= L.ny || i >= L.nx) continue;
-        const long long kb = (long long)k0 * pl;
-        const long long pc = at(L, c, 0, j, h) + kb;
-        const long long pW = at(L, o, 0, j, (i - 1) >> 1) + kb;
-        const long long pE = at(L, o, 0, j, (i + 1) >> 1) + kb;
-        const long long pS = at(L, o, 0, j - 1, h) + kb;
-        const long long pN = at(L, o, 0, j + 1, h) + kb;
-        double uc[KB + 2], vw[KB], ve[KB], vs[KB], vn[KB], vf[KB];
-        uc[0] = (k0 > 0) ? u[pc - pl] : 0.0;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        long long pc = at(L, c, kbeg, j, h);
+        long long pW = at(L, o, kbeg, j, (i - 1) >> 1);
+        long long pE = at(L, o, kbeg, j, (i + 1) >> 1);
+        long long pS = at(L, o, kbeg, j - 1, h);
+        long long pN = at(L, o, kbeg, j + 1, h);
+        double wxm, wxp, wym, wyp, cv, vhc, osw;
+        column_coeffs<UNI>(L, i, j, wxm, wxp, wym, wyp, cv, vhc, osw);
+        for (int k0 = kbeg; k0 < kend; k0 += KB) {
+            double res[KB], uown[KB];
+            stencil_batch<UNI, MODE, KB>(L, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp, cv,
+                                         vhc, osw, tdrw, tdiag, tband, res, uown);
 #pragma unroll
-        for (int t = 0; t < KB; ++t) {
-            const bool ok = k0 + t < nz;
-            const long long ko = (long long)t * pl;
-            uc[t + 1] = ok ? u[pc + ko] : 0.0;
-            vw[t] = ok ? u[pW + ko] : 0.0;
-            ve[t] = ok ? u[pE + ko] : 0.0;
-            vs[t] = ok ? u[pS + ko] : 0.0;
-            vn[t] = ok ? u[pN + ko] : 0.0;
-            if (MODE == 1) vf[t] = ok ? f[pc + ko] : 0.0;
-        }
-        uc[KB + 1] = (k0 + KB < nz) ? u[pc + (long long)KB * pl] : 0.0;
-        double wxm, wxp, wym, wyp, cv, vhc = 0.0, osw = 0.0;
-        if (UNI) {
-            wxm = wxp = L.wx0;
-            wym = wyp = L.wy0;
-            cv = L.csub0;
-        } else {
-            wxm = L.wx[(long long)j * (L.nx + 1) + i];
-            wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
-            wym = L.wy[(long long)j * L.nx + i];
-            wyp = L.wy[(long long)(j + 1) * L.nx + i];
-            cv = L.vcoef * L.av[(long long)j * L.nx + i];
-            vhc = L.vh[(long long)j * L.nx + i];
-            osw = L.omega2 * L.sumw[(long long)j * L.nx + i];
-        }
-#pragma unroll
-        for (int t = 0; t < KB; ++t) {
-            const int k = k0 + t;
-            if (k < nz) {
-                double acc = wxm * vw[t];
-                acc = acc + wxp * ve[t];
-                acc = acc + wym * vs[t];
-                acc = acc + wyp * vn[t];
-                acc = acc * L.drw[k];
-                double d;
-                if (UNI) {
-                    d = L.diag1[k];
-                } else {
-                    d = vhc * L.volprof[k];
-                    d = d + osw * L.dr[k];
-                    d = d + cv * (L.vprof[k] + L.vprof[k + 1]);
+            for (int t = 0; t < KB; ++t) {
+                if (k0 + t < kend) {
+                    if (out) out[pc + (long long)t * pl] = res[t];
+                    if (NORM) acc2 += (MODE == 2) ? uown[t] * res[t] : res[t] * res[t];
                 }
-                double res = d * uc[t + 1] - acc;
-                if (k >= 1) res = res - (UNI ? L.band1[k] : cv * L.vprof[k]) * uc[t];
-                if (k + 1 < nz) res = res - (UNI ? L.band1[k + 1] : cv * L.vprof[k + 1]) * uc[t + 2];
-                if (MODE == 1) res = vf[t] - res;
-                if (out) out[pc + (long long)t * pl] = res;
-                if (NORM) acc2 += (MODE == 2) ? uc[t + 1] * res : res * res;
             }
+            const long long step = (long long)KB * pl;
+            pc += step; pW += step; pE += step; pS += step; pN += step;
         }
     }
     if (NORM) {
         const double s = block_sum(acc2);
         if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = s;
+    }
+}
+
+// Persistent batched residual + children-sum restriction: tile = 32 h x
+// fine rows (2J, 2J+1) x 2 colours = the 4 children of 32 coarse columns
+// (coarse I = h).  Fine residuals go through shared memory, are summed in
+// the reference order ((r(2I,2J) + r(2I+1,2J)) + r(2I,2J+1)) + r(2I+1,2J+1)
+// (multigrid.py:210-212) and written to the coarse f; r never hits HBM.
+template <bool UNI, int KB>
+__global__ void __launch_bounds__(128)
+k_residual_restrict_b(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
+                      double *__restrict__ cf, int hx, int ntiles, int kcs) {
+    __shared__ double tdrw[256], tdiag[256], tband[257];
+    __shared__ double rs[4][KB][33];
+    load_stencil_tables(F, tdrw, tdiag, tband);
+    __syncthreads();
+    const int lane = threadIdx.x;
+    const int ty = threadIdx.y;          // 2 * row + colour
+    const int c = ty & 1, rr = ty >> 1;
+    const int nz = F.nz;
+    const int o = c ^ 1;
+    const long long pl = F.plane;
+    const int nkc = (nz + kcs - 1) / kcs;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int J = t2 / hx;
+        const int hb = t2 - J * hx;
+        const int j = 2 * J + rr;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const int h = hb * 32 + lane;             // fine h == coarse I
+        const int i = 2 * h + ((j + F.par + c) & 1);
+        const bool act = h < C.nx;
+        long long pc = 0, pW = 0, pE = 0, pS = 0, pN = 0;
+        double wxm = 0, wxp = 0, wym = 0, wyp = 0, cv = 0, vhc = 0, osw = 0;
+        if (act) {
+            pc = at(F, c, kbeg, j, h);
+            pW = at(F, o, kbeg, j, (i - 1) >> 1);
+            pE = at(F, o, kbeg, j, (i + 1) >> 1);
+            pS = at(F, o, kbeg, j - 1, h);
+            pN = at(F, o, kbeg, j + 1, h);
+            column_coeffs<UNI>(F, i, j, wxm, wxp, wym, wyp, cv, vhc, osw);
+        }
+        // slot of each child in rs[]: child (a, b) = (i - 2I, j - 2J) -> 2b + a
+        const int slot = 2 * rr + (i & 1);
+        const int I = h;
+        const int cc = (I + J + C.par) & 1;
+        const long long pcoarse = act ? at(C, cc, 0, J, I >> 1) : 0;
+        for (int k0 = kbeg; k0 < kend; k0 += KB) {
+            double res[KB], uown[KB];
+            if (act)
+                stencil_batch<UNI, 1, KB>(F, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp, cv,
+                                          vhc, osw, tdrw, tdiag, tband, res, uown);
+#pragma unroll
+            for (int t = 0; t < KB; ++t) rs[slot][t][lane] = act ? res[t] : 0.0;
+            __syncthreads();
+            // thread (lane, ty) sums level t = ty, ty + 4, ... of coarse column lane
+            for (int t = ty; t < KB; t += 4) {
+                const int k = k0 + t;
+                if (act && k < kend) {
+                    double sm = rs[0][t][lane] + rs[1][t][lane];
+                    sm = sm + rs[2][t][lane];
+                    sm = sm + rs[3][t][lane];
+                    cf[pcoarse + (long long)k * C.plane] = sm;
+                }
+            }
+            __syncthreads();
+            const long long step = (long long)KB * pl;
+            pc += step; pW += step; pE += step; pS += step; pN += step;
+        }
     }
 }
 
@@ -1022,7 +1148,7 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 #define PMG_SEG_B 4   // levels per load batch
 #endif
 template <int SEG>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(512, 1)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
     extern __shared__ double ssm[];
@@ -1033,8 +1159,8 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     double *tmu = tal + nz;             // [nz]
     double *tpf = tmu + nz;             // [nz]
     double *tq = tpf + nz;              // [nz]
-    double *hend = tq + nz;             // [8][32]
-    double *ybeg = hend + 8 * 32;       // [8][32]
+    double *hend = tq + nz;             // [16][32]
+    double *ybeg = hend + 16 * 32;      // [16][32]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int t = threadIdx.x; t < nz; t += blockDim.x) {
         tdrw[t] = L.drw[t];
@@ -1228,6 +1354,63 @@ __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *_
     e = e * 0.0625;
     const long long q = at(F, c, k, j, h);
     fu[q] = add ? fu[q] + e : e;
+}
+
+// Persistent batched prolongation + add: thread = one fine column (h, row,
+// colour), walks k in batches of PB levels with all 4 coarse + 1 fine loads
+// of the batch in flight; the coarse values are shared by the 4 children
+// through L1.  Same arithmetic as k_prolong.
+template <int PB>
+__global__ void __launch_bounds__(256)
+k_prolong_b(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
+            int hx, int ntiles, int kcs) {
+    const int lane = threadIdx.x & 31;
+    const int ty = threadIdx.x >> 5;               // 8 warps: 4 rows x 2 colours
+    const int c = ty & 1;
+    const int nz = F.nz;
+    const int nkc = (nz + kcs - 1) / kcs;
+    const long long pl = F.plane, cpl = C.plane;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int jb = t2 / hx;
+        const int hb = t2 - jb * hx;
+        const int j = jb * 4 + (ty >> 1);
+        const int h = hb * 32 + lane;
+        const int i = 2 * h + ((j + F.par + c) & 1);
+        if (j >= F.ny || i >= F.nx) continue;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const int I = i >> 1, J = j >> 1;
+        const int dI = (i & 1) ? 1 : -1, dJ = (j & 1) ? 1 : -1;
+        const long long qc = cell(C, I, J, kbeg), qx = cell(C, I + dI, J, kbeg);
+        const long long qy = cell(C, I, J + dJ, kbeg), qd = cell(C, I + dI, J + dJ, kbeg);
+        const long long q = at(F, c, kbeg, j, h);
+        for (int k0 = kbeg; k0 < kend; k0 += PB) {
+            double vc[PB], vx[PB], vy[PB], vd[PB], vu[PB];
+#pragma unroll
+            for (int t = 0; t < PB; ++t) {
+                if (k0 + t < kend) {
+                    const long long co = (long long)(k0 - kbeg + t) * cpl;
+                    vc[t] = cu[qc + co];
+                    vx[t] = cu[qx + co];
+                    vy[t] = cu[qy + co];
+                    vd[t] = cu[qd + co];
+                    if (add) vu[t] = fu[q + (long long)(k0 - kbeg + t) * pl];
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < PB; ++t) {
+                if (k0 + t < kend) {
+                    double e = 9.0 * vc[t];
+                    e = e + 3.0 * vx[t];
+                    e = e + 3.0 * vy[t];
+                    e = e + vd[t];
+                    e = e * 0.0625;
+                    fu[q + (long long)(k0 - kbeg + t) * pl] = add ? vu[t] + e : e;
+                }
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1449,7 +1632,6 @@ static cudaError_t launch_apply_kb(const Lvl &L, const double *u, const double *
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
     const int hx = g0.x, jy = g0.y;
-    const int ntiles = hx * jy * ((L.nz + KB - 1) / KB);
     int occ = 1;
 #define PMG_OCC(U, M, N) \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_b<U, M, N, KB>, 32 * 2 * AP_TY, 0)
@@ -1464,10 +1646,15 @@ static cudaError_t launch_apply_kb(const Lvl &L, const double *u, const double *
     }
 #undef PMG_OCC
     const int cap = sm_count() * (occ > 0 ? occ : 1);
+    // split k on small levels until there are >= 2 tiles per resident CTA
+    int kcs = L.nz;
+    while (kcs > 2 * KB && (long long)hx * jy * ((L.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
+    kcs = (kcs + KB - 1) / KB * KB;
+    const int ntiles = hx * jy * ((L.nz + kcs - 1) / kcs);
     const int grid = ntiles < cap ? ntiles : cap;
     *nparts = grid;
 #define PMG_AB(U, M, N) \
-    k_apply_b<U, M, N, KB><<<grid, b, 0, st>>>(L, u, f, out, partials, hx, jy, ntiles)
+    k_apply_b<U, M, N, KB><<<grid, b, 0, st>>>(L, u, f, out, partials, hx, jy, ntiles, kcs)
     if (L.uniform) {
         if (mode == 0) PMG_AB(true, 0, false);
         else if (mode == 1) { if (norm) PMG_AB(true, 1, true); else PMG_AB(true, 1, false); }
@@ -1495,7 +1682,7 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
-    if (apply_variant() == 0) {
+    if (apply_variant() == 0 && L.nz <= 256) {
         static int kbsel = -1;
         if (kbsel < 0) {
             const char *e = getenv("PMG_APPLY_KB");
@@ -1532,6 +1719,26 @@ cudaError_t launch_finalize(const double *partials, int n, double *out, cudaStre
 cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u, const double *f,
                                      double *cf, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (F.nz <= 256 && getenv("PMG_RR_OLD") == nullptr) {
+        constexpr int KB = 4;
+        const int hx = (C.nx + 31) / 32;
+        int occ = 1;
+        if (F.uniform)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_b<true, KB>, 128, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_b<false, KB>, 128, 0);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        int kcs = F.nz;
+        while (kcs > 2 * KB && (long long)hx * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
+        kcs = (kcs + KB - 1) / KB * KB;
+        const int ntiles = hx * C.ny * ((F.nz + kcs - 1) / kcs);
+        const int grid = ntiles < cap ? ntiles : cap;
+        if (F.uniform)
+            k_residual_restrict_b<true, KB><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
+        else
+            k_residual_restrict_b<false, KB><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
+        return cudaGetLastError();
+    }
     const int kc = k_chunk(F, (long long)C.nx * C.ny, 148 * 2048 * 2);
     const dim3 b(32, 8), g((C.nx + 31) / 32, (F.nz + kc - 1) / kc, (C.ny + 7) / 8);
     if (F.uniform) k_residual_restrict<true><<<g, b, 0, st>>>(F, C, u, f, cf, kc);
@@ -1570,7 +1777,7 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
     const dim3 g(hx, L.ny);
     if (!g_smoother_exact && L.uniform && L.seg) {
         const int nw = (L.nz + L.seg - 1) / L.seg;
-        const size_t sm = sizeof(double) * (6 * (size_t)L.nz + 2 * 8 * 32);
+        const size_t sm = sizeof(double) * (6 * (size_t)L.nz + 2 * 16 * 32);
         const int ntiles = hx * L.ny;
         int occ = 1;
         switch (L.seg) {
@@ -1688,6 +1895,20 @@ cudaError_t launch_restrict(const Lvl &F, const Lvl &C, const double *fu, double
 cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double *fu, int add,
                            cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (getenv("PMG_PROLONG_B") != nullptr) {   // column walker (slower on B200)
+        constexpr int PB = 4;
+        const int hx = ((F.nx + 1) / 2 + 31) / 32, jy = (F.ny + 3) / 4;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_prolong_b<PB>, 256, 0);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        int kcs = F.nz;
+        while (kcs > 2 * PB && (long long)hx * jy * ((F.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
+        kcs = (kcs + PB - 1) / PB * PB;
+        const int ntiles = hx * jy * ((F.nz + kcs - 1) / kcs);
+        const int grid = ntiles < cap ? ntiles : cap;
+        k_prolong_b<PB><<<grid, 256, 0, st>>>(F, C, cu, fu, add, hx, ntiles, kcs);
+        return cudaGetLastError();
+    }
     const int n2 = 2 * ((F.nx + 1) / 2);
     k_prolong<<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add);
     return cudaGetLastError();
