@@ -196,8 +196,9 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
             if (v == 4 || v == 8 || v == 16 || v == 32) seg = v;
         }
         L.seg = ((nz + seg - 1) / seg <= 16) ? seg : 0;
-        lv->h_seg.assign(4 * (size_t)nz, 0.0);
+        lv->h_seg.assign(5 * (size_t)nz, 0.0);
         double *al = lv->h_seg.data(), *mu = al + nz, *pf = mu + nz, *qq = pf + nz;
+        double *ag = qq + nz;
         for (int k = 0; k < nz; ++k) {
             al[k] = (k == 0) ? 0.0 : (L.csub0 * d->vprof[k]) * lv->h_invd[k];
             mu[k] = (k + 1 < nz) ? (L.csub0 * d->vprof[k + 1]) * lv->h_invd[k] : 0.0;
@@ -209,9 +210,12 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
                 for (int k = a; k <= b; ++k) { p *= al[k]; pf[k] = p; }
                 double q = 1.0;
                 for (int k = b; k >= a; --k) { q *= mu[k]; qq[k] = q; }
+                // ag[k] = d y_k / d G for the zero-boundary backward sweep
+                double gg = 0.0;
+                for (int k = b; k >= a; --k) { gg = pf[k] + mu[k] * gg; ag[k] = gg; }
             }
         }
-        if ((e = upload(lv, lv->h_seg.data(), 4 * (size_t)nz, &L.segtab)) != cudaSuccess ||
+        if ((e = upload(lv, lv->h_seg.data(), 5 * (size_t)nz, &L.segtab)) != cudaSuccess ||
             (e = upload(lv, lv->h_diag.data(), nz, &L.diag1)) != cudaSuccess ||
             (e = upload(lv, lv->h_band.data(), nz + 1, &L.band1)) != cudaSuccess ||
             (e = upload(lv, lv->h_invd.data(), nz, &L.invd1)) != cudaSuccess) {

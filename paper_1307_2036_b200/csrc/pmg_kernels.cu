@@ -156,19 +156,21 @@ __device__ __forceinline__ void stencil_batch(
     const int nz = L.nz;
     const long long pl = L.plane;
     double uc[KB + 2], vw[KB], ve[KB], vs[KB], vn[KB], vf[KB];
-    uc[0] = (k0 > 0) ? u[pc - pl] : 0.0;
+    // every load unpredicated: levels beyond the column are clamped to a
+    // valid address and their values never used (predicated loads split the
+    // batch into separately waited groups)
+    uc[0] = u[pc - ((k0 > 0) ? pl : 0)];
 #pragma unroll
     for (int t = 0; t < KB; ++t) {
-        const bool ok = k0 + t < nz;
-        const long long ko = (long long)t * pl;
-        uc[t + 1] = ok ? u[pc + ko] : 0.0;
-        vw[t] = ok ? u[pW + ko] : 0.0;
-        ve[t] = ok ? u[pE + ko] : 0.0;
-        vs[t] = ok ? u[pS + ko] : 0.0;
-        vn[t] = ok ? u[pN + ko] : 0.0;
-        if (MODE == 1) vf[t] = ok ? f[pc + ko] : 0.0;
+        const long long ko = (long long)min(t, nz - 1 - k0) * pl;
+        uc[t + 1] = u[pc + ko];
+        vw[t] = u[pW + ko];
+        ve[t] = u[pE + ko];
+        vs[t] = u[pS + ko];
+        vn[t] = u[pN + ko];
+        if (MODE == 1) vf[t] = f[pc + ko];
     }
-    uc[KB + 1] = (k0 + KB < nz) ? u[pc + (long long)KB * pl] : 0.0;
+    uc[KB + 1] = u[pc + (long long)min(KB, nz - 1 - k0) * pl];
 #pragma unroll
     for (int t = 0; t < KB; ++t) {
         const int k = k0 + t;
@@ -287,6 +289,288 @@ k_apply_b(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
     }
 }
 
+// Tile-walk apply / residual: tile = one row j x 32 columns x both
+// colours; warp w = (colour w & 1, k-segment w >> 1) of SEGA levels, so
+// each warp walks only SEGA/KB batches per tile and consecutive tiles of
+// the machine touch the same rows (the layout's contiguous row blocks).
+template <bool UNI, int MODE, bool NORM, int KB, int SEGA>
+__global__ void __launch_bounds__(512, 1)
+k_apply_t(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
+          double *__restrict__ out, double *__restrict__ partials, int hx, int ntiles) {
+    __shared__ double tdrw[256], tdiag[256], tband[257];
+    load_stencil_tables(L, tdrw, tdiag, tband);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int c = w & 1;
+    const int kseg = (w >> 1) * SEGA;
+    const int nz = L.nz;
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    double acc2 = 0.0;
+    if (kseg < nz) {
+        const int kend = min(nz, kseg + SEGA);
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int j = tile / hx;
+            const int hb = tile - j * hx;
+            const int s0 = (j + L.par + c) & 1;
+            const int hmax = ((L.nx - s0) + 1) / 2 - 1;          // last valid h of this row/colour
+            const bool act = hb * 32 + lane <= hmax;
+            const int h = act ? hb * 32 + lane : hmax;
+            const int i = 2 * h + s0;
+            long long pc = at(L, c, kseg, j, h);
+            long long pW = at(L, o, kseg, j, (i - 1) >> 1);
+            long long pE = at(L, o, kseg, j, (i + 1) >> 1);
+            long long pS = at(L, o, kseg, j - 1, h);
+            long long pN = at(L, o, kseg, j + 1, h);
+            double wxm, wxp, wym, wyp, cv, vhc, osw;
+            column_coeffs<UNI>(L, i, j, wxm, wxp, wym, wyp, cv, vhc, osw);
+            for (int k0 = kseg; k0 < kend; k0 += KB) {
+                double res[KB], uown[KB];
+                stencil_batch<UNI, MODE, KB>(L, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp,
+                                             cv, vhc, osw, tdrw, tdiag, tband, res, uown);
+                if (act) {
+#pragma unroll
+                    for (int t = 0; t < KB; ++t) {
+                        if (k0 + t < kend) {
+                            if (out) out[pc + (long long)t * pl] = res[t];
+                            if (NORM) acc2 += (MODE == 2) ? uown[t] * res[t] : res[t] * res[t];
+                        }
+                    }
+                }
+                const long long step = (long long)KB * pl;
+                pc += step; pW += step; pE += step; pS += step; pN += step;
+            }
+        }
+    }
+    if (NORM) {
+        const double s = block_sum(acc2);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Vectorised column-pair stencil (uniform coefficients): a thread owns the
+// adjacent same-colour columns h = 2m, 2m+1 of one row; every row segment it
+// needs is one 16-byte load (own u, f, S, N rows) and the W/E neighbours of
+// both columns come from the other colour's pair o[2m..2m+1] plus ONE scalar
+// (o[2m+2] if the row's shift s = 1, else o[2m-1]).  Same arithmetic and
+// order per cell as stencil.py:140-164.
+// ---------------------------------------------------------------------------
+struct D2 { double x, y; };
+
+__device__ __forceinline__ D2 ld2(const double *p) {
+    const double2 v = *reinterpret_cast<const double2 *>(p);
+    return D2{v.x, v.y};
+}
+
+template <int MODE, int KB>
+__device__ __forceinline__ void stencil_batch2(
+    const Lvl &L, const double *__restrict__ u, const double *__restrict__ f, int k0, int s,
+    long long pc, long long po, long long pS, long long pN, long long px, const double *tdrw,
+    const double *tdiag, const double *tband, double (&r0)[KB], double (&r1)[KB],
+    double (&u0)[KB], double (&u1)[KB]) {
+    const int nz = L.nz;
+    const long long pl = L.plane;
+    D2 uc[KB + 2], vo[KB], vs[KB], vn[KB], vf[KB];
+    double vx[KB];
+    uc[0] = ld2(u + pc - ((k0 > 0) ? pl : 0));
+#pragma unroll
+    for (int t = 0; t < KB; ++t) {
+        const long long ko = (long long)min(t, nz - 1 - k0) * pl;
+        uc[t + 1] = ld2(u + pc + ko);
+        vo[t] = ld2(u + po + ko);
+        vx[t] = u[px + ko];
+        vs[t] = ld2(u + pS + ko);
+        vn[t] = ld2(u + pN + ko);
+        if (MODE == 1) vf[t] = ld2(f + pc + ko);
+    }
+    uc[KB + 1] = ld2(u + pc + (long long)min(KB, nz - 1 - k0) * pl);
+    const double w0 = L.wx0, w1 = L.wy0;
+#pragma unroll
+    for (int t = 0; t < KB; ++t) {
+        const int k = k0 + t;
+        // W/E of column 2m (a) and 2m+1 (b)
+        const double wa = s ? vo[t].x : vx[t];
+        const double ea = s ? vo[t].y : vo[t].x;
+        const double wb = ea;
+        const double eb = s ? vx[t] : vo[t].y;
+        u0[t] = uc[t + 1].x;
+        u1[t] = uc[t + 1].y;
+        double acc = w0 * wa;
+        acc = acc + w0 * ea;
+        acc = acc + w1 * vs[t].x;
+        acc = acc + w1 * vn[t].x;
+        acc = acc * tdrw[min(k, nz - 1)];
+        double bcc = w0 * wb;
+        bcc = bcc + w0 * eb;
+        bcc = bcc + w1 * vs[t].y;
+        bcc = bcc + w1 * vn[t].y;
+        bcc = bcc * tdrw[min(k, nz - 1)];
+        const double d = tdiag[min(k, nz - 1)];
+        double ra = d * uc[t + 1].x - acc;
+        double rb = d * uc[t + 1].y - bcc;
+        if (k >= 1) {
+            const double bl = tband[min(k, nz)];
+            ra = ra - bl * uc[t].x;
+            rb = rb - bl * uc[t].y;
+        }
+        if (k + 1 < nz) {
+            const double bu = tband[k + 1];
+            ra = ra - bu * uc[t + 2].x;
+            rb = rb - bu * uc[t + 2].y;
+        }
+        if (MODE == 1) {
+            ra = vf[t].x - ra;
+            rb = vf[t].y - rb;
+        }
+        r0[t] = ra;
+        r1[t] = rb;
+    }
+}
+
+// tile = 64 columns x AP_TY rows x 2 colours, column-pair threads walk k
+template <int MODE, bool NORM, int KB>
+__global__ void __launch_bounds__(32 * 2 * AP_TY, 2)
+k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
+          double *__restrict__ out, double *__restrict__ partials, int hx, int jy, int ntiles,
+          int kcs) {
+    __shared__ double tdrw[256], tdiag[256], tband[257];
+    load_stencil_tables(L, tdrw, tdiag, tband);
+    __syncthreads();
+    const int lane = threadIdx.x;
+    const int c = threadIdx.y & 1;
+    const int nz = L.nz;
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    const int nkc = (nz + kcs - 1) / kcs;
+    double acc2 = 0.0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int jb = t2 / hx;
+        const int hb = t2 - jb * hx;
+        const int j = jb * AP_TY + (threadIdx.y >> 1);
+        if (j >= L.ny) continue;
+        const int s = (j + L.par + c) & 1;
+        const int ncol = ((L.nx - s) + 1) / 2;          // columns of this colour in row j
+        const int m = hb * 32 + lane;
+        const bool act = 2 * m < ncol;
+        const int mm = act ? m : (ncol - 1) / 2;
+        const int h = 2 * mm;
+        const bool two = act && (h + 1 < ncol);
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        long long pc = at(L, c, kbeg, j, h);
+        long long po = at(L, o, kbeg, j, h);
+        long long pS = at(L, o, kbeg, j - 1, h);
+        long long pN = at(L, o, kbeg, j + 1, h);
+        long long px = at(L, o, kbeg, j, s ? h + 2 : h - 1);
+        for (int k0 = kbeg; k0 < kend; k0 += KB) {
+            double r0[KB], r1[KB], u0[KB], u1[KB];
+            stencil_batch2<MODE, KB>(L, u, f, k0, s, pc, po, pS, pN, px, tdrw, tdiag, tband, r0,
+                                     r1, u0, u1);
+            if (act) {
+#pragma unroll
+                for (int t = 0; t < KB; ++t) {
+                    if (k0 + t < kend) {
+                        const long long q = pc + (long long)t * pl;
+                        if (out) {
+                            if (two) {
+                                *reinterpret_cast<double2 *>(out + q) = make_double2(r0[t], r1[t]);
+                            } else {
+                                out[q] = r0[t];
+                            }
+                        }
+                        if (NORM) {
+                            acc2 += (MODE == 2) ? u0[t] * r0[t] : r0[t] * r0[t];
+                            if (two) acc2 += (MODE == 2) ? u1[t] * r1[t] : r1[t] * r1[t];
+                        }
+                    }
+                }
+            }
+            const long long step = (long long)KB * pl;
+            pc += step; po += step; pS += step; pN += step; px += step;
+        }
+    }
+    if (NORM) {
+        const double s2 = block_sum(acc2);
+        if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = s2;
+    }
+}
+
+// Vectorised residual + children-sum restriction (uniform): tile = 64
+// coarse columns I (= fine h) of coarse row J; warp (row rr, colour c)
+// computes the residual of fine columns h = 2m, 2m+1 in fine row 2J + rr;
+// children are combined in shared memory in the reference order and each
+// thread writes coarse I = 2m and 2m+1 (one per colour array, coalesced).
+template <int KB>
+__global__ void __launch_bounds__(128, 4)
+k_residual_restrict_v(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
+                      double *__restrict__ cf, int hx, int ntiles, int kcs) {
+    __shared__ double tdrw[256], tdiag[256], tband[257];
+    __shared__ double rs[4][KB][65];
+    load_stencil_tables(F, tdrw, tdiag, tband);
+    __syncthreads();
+    const int lane = threadIdx.x;
+    const int ty = threadIdx.y;              // 2 * rr + c
+    const int c = ty & 1, rr = ty >> 1;
+    const int nz = F.nz;
+    const int o = c ^ 1;
+    const long long pl = F.plane;
+    const int nkc = (nz + kcs - 1) / kcs;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int J = t2 / hx;
+        const int hb = t2 - J * hx;
+        const int j = 2 * J + rr;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const int s = (j + F.par + c) & 1;
+        const int m = hb * 32 + lane;                  // coarse I = 2m, 2m+1
+        const bool act = 2 * m < C.nx;
+        const int h = act ? 2 * m : 2 * ((C.nx - 1) / 2);
+        long long pc = at(F, c, kbeg, j, h);
+        long long po = at(F, o, kbeg, j, h);
+        long long pS = at(F, o, kbeg, j - 1, h);
+        long long pN = at(F, o, kbeg, j + 1, h);
+        long long px = at(F, o, kbeg, j, s ? h + 2 : h - 1);
+        const int slot = 2 * rr + s;
+        const int cc0 = (2 * m + J + C.par) & 1;       // colour of coarse I = 2m
+        const long long q0 = act ? at(C, cc0, kbeg, J, m) : 0;
+        const long long q1 = act ? at(C, cc0 ^ 1, kbeg, J, m) : 0;
+        const bool two = act && (2 * m + 1 < C.nx);
+        for (int k0 = kbeg; k0 < kend; k0 += KB) {
+            double r0[KB], r1[KB], u0[KB], u1[KB];
+            stencil_batch2<1, KB>(F, u, f, k0, s, pc, po, pS, pN, px, tdrw, tdiag, tband, r0, r1,
+                                  u0, u1);
+#pragma unroll
+            for (int t = 0; t < KB; ++t) {
+                rs[slot][t][2 * lane] = r0[t];
+                rs[slot][t][2 * lane + 1] = r1[t];
+            }
+            __syncthreads();
+            for (int t = ty; t < KB; t += 4) {
+                const int k = k0 + t;
+                if (act && k < kend) {
+                    const long long ko = (long long)(k - kbeg) * C.plane;
+                    double a = rs[0][t][2 * lane] + rs[1][t][2 * lane];
+                    a = a + rs[2][t][2 * lane];
+                    a = a + rs[3][t][2 * lane];
+                    cf[q0 + ko] = a;
+                    if (two) {
+                        double b = rs[0][t][2 * lane + 1] + rs[1][t][2 * lane + 1];
+                        b = b + rs[2][t][2 * lane + 1];
+                        b = b + rs[3][t][2 * lane + 1];
+                        cf[q1 + ko] = b;
+                    }
+                }
+            }
+            __syncthreads();
+            const long long step = (long long)KB * pl;
+            pc += step; po += step; pS += step; pN += step; px += step;
+        }
+    }
+}
+
 // Persistent batched residual + children-sum restriction: tile = 32 h x
 // fine rows (2J, 2J+1) x 2 colours = the 4 children of 32 coarse columns
 // (coarse I = h).  Fine residuals go through shared memory, are summed in
@@ -314,12 +598,12 @@ k_residual_restrict_b(Lvl F, Lvl C, const double *__restrict__ u, const double *
         const int hb = t2 - J * hx;
         const int j = 2 * J + rr;
         const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
-        const int h = hb * 32 + lane;             // fine h == coarse I
+        const bool act = hb * 32 + lane < C.nx;
+        const int h = act ? hb * 32 + lane : C.nx - 1;   // fine h == coarse I (clamped)
         const int i = 2 * h + ((j + F.par + c) & 1);
-        const bool act = h < C.nx;
         long long pc = 0, pW = 0, pE = 0, pS = 0, pN = 0;
         double wxm = 0, wxp = 0, wym = 0, wyp = 0, cv = 0, vhc = 0, osw = 0;
-        if (act) {
+        {
             pc = at(F, c, kbeg, j, h);
             pW = at(F, o, kbeg, j, (i - 1) >> 1);
             pE = at(F, o, kbeg, j, (i + 1) >> 1);
@@ -334,9 +618,8 @@ k_residual_restrict_b(Lvl F, Lvl C, const double *__restrict__ u, const double *
         const long long pcoarse = act ? at(C, cc, 0, J, I >> 1) : 0;
         for (int k0 = kbeg; k0 < kend; k0 += KB) {
             double res[KB], uown[KB];
-            if (act)
-                stencil_batch<UNI, 1, KB>(F, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp, cv,
-                                          vhc, osw, tdrw, tdiag, tband, res, uown);
+            stencil_batch<UNI, 1, KB>(F, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp, cv,
+                                      vhc, osw, tdrw, tdiag, tband, res, uown);
 #pragma unroll
             for (int t = 0; t < KB; ++t) rs[slot][t][lane] = act ? res[t] : 0.0;
             __syncthreads();
@@ -1144,13 +1427,13 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // (agrees with the sequential solve to ~1e-15 relative; the exact mode is
 // k_half_sweep_tma / k_half_sweep).
 // ---------------------------------------------------------------------------
-#ifndef PMG_SEG_B
-#define PMG_SEG_B 4   // levels per load batch
-#endif
-template <int SEG>
-__global__ void __launch_bounds__(512, 1)
+template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false>
+__global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                 int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
+                 int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles) {
+    // NBZ = 0/1: neighbours-zero mode fixed at compile time; FULL: every warp
+    // owns exactly SEG levels (nz % SEG == 0) -- no per-level predicates
+    const int nbr_zero = (NBZ >= 0) ? NBZ : nbr_zero_rt;
     extern __shared__ double ssm[];
     const int nz = L.nz;
     double *tdrw = ssm;                 // [nz]
@@ -1174,7 +1457,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     const int o = c ^ 1;
     const long long pl = L.plane;
     const int k0 = w * SEG;
-    const int kn = min(SEG, nz - k0);          // levels of this warp (may be <= 0)
+    const int kn = FULL ? SEG : min(SEG, nz - k0);   // levels of this warp (may be <= 0)
     const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
@@ -1286,6 +1569,294 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
             }
         }
         __syncthreads();   // hend / ybeg reuse by the next tile
+    }
+}
+
+// Same k-segmented solve with the segment values kept in shared memory
+// (tile [nz][32]) instead of registers: registers then only carry the
+// in-flight load batch, so more warps fit per SM.
+template <int SEG, int B, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_half_sweep_segs(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
+    extern __shared__ double ssm[];
+    const int nz = L.nz;
+    double *tdrw = ssm;                 // [nz]
+    double *tiot = tdrw + nz;           // [nz]
+    double *tal = tiot + nz;            // [nz]
+    double *tmu = tal + nz;             // [nz]
+    double *tpf = tmu + nz;             // [nz]
+    double *tq = tpf + nz;              // [nz]
+    double *hend = tq + nz;             // [8][32]
+    double *ybeg = hend + 8 * 32;       // [8][32]
+    double *sv = ybeg + 8 * 32;         // [nz][32]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
+        tdrw[t] = L.drw[t];
+        tiot[t] = L.invd1[t];
+        tal[t] = L.segtab[t];
+        tmu[t] = L.segtab[nz + t];
+        tpf[t] = L.segtab[2 * nz + t];
+        tq[t] = L.segtab[3 * nz + t];
+    }
+    __syncthreads();
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    const int k0 = w * SEG;
+    const int kn = min(SEG, nz - k0);
+    const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int j = t / htiles;
+        const int h0 = (t - j * htiles) * 32;
+        const int s0 = (j + L.par + c) & 1;
+        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+        const int ln = min(lane, nact - 1);
+        const bool lastlane = (ln == nact - 1);
+        const int h = h0 + ln;
+        const int i = 2 * h + s0;
+        const long long pc = at(L, c, k0, j, h);
+        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
+        const long long pS = at(L, o, k0, j - 1, h);
+        const long long pN = at(L, o, k0, j + 1, h);
+        // ---- RHS + local forward h_k = iota r_k + alpha h_{k-1}, batch by batch ----
+        double hp = 0.0;
+        for (int b8 = 0; b8 < kn; b8 += B) {
+            double vf[B], vw[B], vs[B], vn[B], vx[B];
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const int kk = b8 + e;
+                if (kk < kn) {
+                    const long long ko = (long long)kk * pl;
+                    vf[e] = f[pc + ko];
+                    if (!nbr_zero) {
+                        vw[e] = u[pW + ko];
+                        vs[e] = u[pS + ko];
+                        vn[e] = u[pN + ko];
+                        vx[e] = lastlane ? u[pE + ko] : 0.0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const int kk = b8 + e;
+                double ve = __shfl_down_sync(0xffffffffu, nbr_zero ? 0.0 : vw[e], 1);
+                if (lastlane) ve = vx[e];
+                if (kk < kn) {
+                    const int k = k0 + kk;
+                    double g;
+                    if (nbr_zero) {
+                        g = vf[e];
+                    } else {
+                        g = wxm * vw[e];
+                        g = g + wxp * ve;
+                        g = g + wym * vs[e];
+                        g = g + wyp * vn[e];
+                        g = g * tdrw[k];
+                        g = g + vf[e];
+                    }
+                    hp = __fma_rn(tal[k], hp, tiot[k] * g);
+                    sv[k * 32 + lane] = hp;
+                }
+            }
+        }
+        if (kn > 0) hend[w * 32 + lane] = hp;
+        __syncthreads();
+        double G = 0.0;
+        for (int sgm = 0; sgm < w; ++sgm)
+            G = __fma_rn(tpf[min(nz, (sgm + 1) * SEG) - 1], G, hend[sgm * 32 + lane]);
+        double yp = 0.0;
+        for (int e = kn - 1; e >= 0; --e) {
+            const int k = k0 + e;
+            const double g = __fma_rn(tpf[k], G, sv[k * 32 + lane]);
+            yp = __fma_rn(tmu[k], yp, g);
+            sv[k * 32 + lane] = yp;
+        }
+        if (kn > 0) ybeg[w * 32 + lane] = yp;
+        __syncthreads();
+        double X = 0.0;
+        for (int sgm = nw - 1; sgm > w; --sgm) {
+            const int a = sgm * SEG;
+            if (a < nz) X = __fma_rn(tq[a], X, ybeg[sgm * 32 + lane]);
+        }
+        if (lane < nact) {
+            for (int e = 0; e < kn; ++e) {
+                const int k = k0 + e;
+                double y = __fma_rn(tq[k], X, sv[k * 32 + lane]);
+                const long long q = pc + (long long)e * pl;
+                if (zero_start) {
+                    if (scale != 1.0) y = y * scale;
+                } else if (rho != 1.0) {
+                    y = y * rho;
+                    y = y + omr * u[q];
+                }
+                u[q] = y;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// One-barrier k-segmented solve.  Each warp runs the forward AND the
+// backward sweep of its segment with zero boundary values (h, y0) and
+// publishes h at its top and y0 at its bottom; the backward solution is
+// affine in the incoming forward value G and the incoming backward value X:
+//   x_k = y0_k + ag_k G + q_k X,
+// so after ONE barrier every warp solves the 2 x NW reduced system for its
+// own (G, X) from the published values.  The exchange arrays are double
+// buffered by tile parity (warps are never more than one tile apart), so
+// there is no end-of-tile barrier.
+template <int SEG, int B, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+k_half_sweep_seg1(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
+    extern __shared__ double ssm[];
+    const int nz = L.nz;
+    double *tdrw = ssm;                 // [nz]
+    double *tiot = tdrw + nz;           // [nz]
+    double *tal = tiot + nz;            // [nz]
+    double *tmu = tal + nz;             // [nz]
+    double *tpf = tmu + nz;             // [nz]
+    double *tq = tpf + nz;              // [nz]
+    double *tag = tq + nz;              // [nz]
+    double *xch = tag + nz;             // [2 parity][2 (hend, y0beg)][8][32]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
+        tdrw[t] = L.drw[t];
+        tiot[t] = L.invd1[t];
+        tal[t] = L.segtab[t];
+        tmu[t] = L.segtab[nz + t];
+        tpf[t] = L.segtab[2 * nz + t];
+        tq[t] = L.segtab[3 * nz + t];
+        tag[t] = L.segtab[4 * nz + t];
+    }
+    __syncthreads();
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    const int k0 = w * SEG;
+    const int kn = min(SEG, nz - k0);
+    const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    int par = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
+        const int j = t / htiles;
+        const int h0 = (t - j * htiles) * 32;
+        const int s0 = (j + L.par + c) & 1;
+        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+        const int ln = min(lane, nact - 1);
+        const bool lastlane = (ln == nact - 1);
+        const int h = h0 + ln;
+        const int i = 2 * h + s0;
+        const long long pc = at(L, c, k0, j, h);
+        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
+        const long long pS = at(L, o, k0, j - 1, h);
+        const long long pN = at(L, o, k0, j + 1, h);
+        double r[SEG];
+#pragma unroll
+        for (int b8 = 0; b8 < SEG; b8 += B) {
+            double vf[B], vw[B], vs[B], vn[B], vx[B];
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const int kk = b8 + e;
+                if (kk < kn) {
+                    const long long ko = (long long)kk * pl;
+                    vf[e] = f[pc + ko];
+                    if (!nbr_zero) {
+                        vw[e] = u[pW + ko];
+                        vs[e] = u[pS + ko];
+                        vn[e] = u[pN + ko];
+                        vx[e] = lastlane ? u[pE + ko] : 0.0;
+                    }
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const int kk = b8 + e;
+                double ve = __shfl_down_sync(0xffffffffu, nbr_zero ? 0.0 : vw[e], 1);
+                if (lastlane) ve = vx[e];
+                if (kk < kn) {
+                    double g;
+                    if (nbr_zero) {
+                        g = vf[e];
+                    } else {
+                        g = wxm * vw[e];
+                        g = g + wxp * ve;
+                        g = g + wym * vs[e];
+                        g = g + wyp * vn[e];
+                        g = g * tdrw[k0 + kk];
+                        g = g + vf[e];
+                    }
+                    r[b8 + e] = g;
+                }
+            }
+        }
+        // zero-boundary forward (h) and backward (y0) sweeps of the segment
+        double hp = 0.0;
+#pragma unroll
+        for (int e = 0; e < SEG; ++e)
+            if (e < kn) {
+                const int k = k0 + e;
+                hp = __fma_rn(tal[k], hp, tiot[k] * r[e]);
+                r[e] = hp;
+            }
+        double yp = 0.0;
+#pragma unroll
+        for (int e = SEG - 1; e >= 0; --e)
+            if (e < kn) {
+                const int k = k0 + e;
+                yp = __fma_rn(tmu[k], yp, r[e]);
+                r[e] = yp;
+            }
+        double *xh = xch + par * 2 * 8 * 32;
+        double *xy = xh + 8 * 32;
+        if (kn > 0) {
+            xh[w * 32 + lane] = hp;
+            xy[w * 32 + lane] = yp;
+        }
+        __syncthreads();
+        // reduced system: G_s = hend_{s-1} + pf_end(s-1) G_{s-1};
+        // X_s = y0beg_{s+1} + ag_{a(s+1)} G_{s+1} + q_{a(s+1)} X_{s+1}
+        double Gs[8];
+        double G = 0.0;
+#pragma unroll
+        for (int sg = 0; sg < 8; ++sg) {
+            Gs[sg] = G;
+            if (sg < nw) {
+                const int b = min(nz, (sg + 1) * SEG) - 1;
+                G = __fma_rn(tpf[b], G, xh[sg * 32 + lane]);
+            }
+        }
+        double X = 0.0, Gw = 0.0;
+#pragma unroll
+        for (int sg = 7; sg >= 0; --sg) {
+            const int a = sg * SEG;
+            if (sg > w && sg < nw && a < nz) {
+                const double v = __fma_rn(tag[a], Gs[sg], xy[sg * 32 + lane]);
+                X = __fma_rn(tq[a], X, v);
+            }
+            if (sg == w) Gw = Gs[sg];
+        }
+        if (lane < nact) {
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                if (e < kn) {
+                    const int k = k0 + e;
+                    double y = __fma_rn(tag[k], Gw, __fma_rn(tq[k], X, r[e]));
+                    const long long q = pc + (long long)e * pl;
+                    if (zero_start) {
+                        if (scale != 1.0) y = y * scale;
+                    } else if (rho != 1.0) {
+                        y = y * rho;
+                        y = y + omr * u[q];
+                    }
+                    u[q] = y;
+                }
+            }
+        }
     }
 }
 
@@ -1682,6 +2253,62 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
+    if (apply_variant() == 0 && L.uniform && L.nz <= 256 && getenv("PMG_APPLY_V0") == nullptr) {
+        // vectorised column pairs
+        constexpr int KB = 4;
+        const int hx = ((L.nx + 1) / 2 + 63) / 64, jy = (L.ny + AP_TY - 1) / AP_TY;
+        const bool norm = partials != nullptr;
+        auto go = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * 2 * AP_TY, 0);
+            const int cap = sm_count() * (occ > 0 ? occ : 1);
+            int kcs = L.nz;
+            while (kcs > 2 * KB && (long long)hx * jy * ((L.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
+            kcs = (kcs + KB - 1) / KB * KB;
+            const int ntiles = hx * jy * ((L.nz + kcs - 1) / kcs);
+            const int grid = ntiles < cap ? ntiles : cap;
+            *nparts = grid;
+            kern<<<grid, dim3(32, 2 * AP_TY), 0, st>>>(L, u, f, out, partials, hx, jy, ntiles, kcs);
+        };
+        if (mode == 0) go(k_apply_v<0, false, KB>);
+        else if (mode == 1) { if (norm) go(k_apply_v<1, true, KB>); else go(k_apply_v<1, false, KB>); }
+        else go(k_apply_v<2, true, KB>);
+        return cudaGetLastError();
+    }
+    if (apply_variant() == 0 && L.nz <= 256 && L.nz >= 16 && getenv("PMG_APPLY_T") != nullptr) {
+        // tile walk: 16 warps = 2 colours x 8 k-segments
+        constexpr int KB = 4;
+        const int sega = ((L.nz + 7) / 8 + KB - 1) / KB * KB;
+        const int hx = ((L.nx + 1) / 2 + 31) / 32;
+        const int ntiles = hx * L.ny;
+        const bool norm = partials != nullptr;
+        auto go = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, 0);
+            const int cap = sm_count() * (occ > 0 ? occ : 1);
+            const int grid = ntiles < cap ? ntiles : cap;
+            *nparts = grid;
+            kern<<<grid, 512, 0, st>>>(L, u, f, out, partials, hx, ntiles);
+        };
+#define PMG_AT(U, M, N)                                                          \
+    do {                                                                         \
+        if (sega <= 4) go(k_apply_t<U, M, N, KB, 4>);                            \
+        else if (sega <= 8) go(k_apply_t<U, M, N, KB, 8>);                       \
+        else if (sega <= 16) go(k_apply_t<U, M, N, KB, 16>);                     \
+        else go(k_apply_t<U, M, N, KB, 32>);                                     \
+    } while (0)
+        if (L.uniform) {
+            if (mode == 0) PMG_AT(true, 0, false);
+            else if (mode == 1) { if (norm) PMG_AT(true, 1, true); else PMG_AT(true, 1, false); }
+            else PMG_AT(true, 2, true);
+        } else {
+            if (mode == 0) PMG_AT(false, 0, false);
+            else if (mode == 1) { if (norm) PMG_AT(false, 1, true); else PMG_AT(false, 1, false); }
+            else PMG_AT(false, 2, true);
+        }
+#undef PMG_AT
+        return cudaGetLastError();
+    }
     if (apply_variant() == 0 && L.nz <= 256) {
         static int kbsel = -1;
         if (kbsel < 0) {
@@ -1719,6 +2346,20 @@ cudaError_t launch_finalize(const double *partials, int n, double *out, cudaStre
 cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u, const double *f,
                                      double *cf, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (F.uniform && F.nz <= 256 && getenv("PMG_RR_V0") == nullptr) {
+        constexpr int KB = 4;
+        const int hx = (C.nx + 63) / 64;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_v<KB>, 128, 0);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        int kcs = F.nz;
+        while (kcs > 2 * KB && (long long)hx * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
+        kcs = (kcs + KB - 1) / KB * KB;
+        const int ntiles = hx * C.ny * ((F.nz + kcs - 1) / kcs);
+        const int grid = ntiles < cap ? ntiles : cap;
+        k_residual_restrict_v<KB><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
+        return cudaGetLastError();
+    }
     if (F.nz <= 256 && getenv("PMG_RR_OLD") == nullptr) {
         constexpr int KB = 4;
         const int hx = (C.nx + 31) / 32;
@@ -1775,28 +2416,100 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
-    if (!g_smoother_exact && L.uniform && L.seg) {
+    if (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) {
         const int nw = (L.nz + L.seg - 1) / L.seg;
         const size_t sm = sizeof(double) * (6 * (size_t)L.nz + 2 * 16 * 32);
+        const size_t sm1 = sizeof(double) * (7 * (size_t)L.nz + 2 * 2 * 8 * 32);
         const int ntiles = hx * L.ny;
-        int occ = 1;
-        switch (L.seg) {
-        case 4: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<4>, 32 * nw, sm); break;
-        case 8: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<8>, 32 * nw, sm); break;
-        case 16: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<16>, 32 * nw, sm); break;
-        default: cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_half_sweep_seg<32>, 32 * nw, sm); break;
+        static int var = -1;
+        if (var < 0) {
+            const char *e = getenv("PMG_SEG_VARIANT");
+            var = e ? atoi(e) : 0;
         }
-        const int cap = sm_count() * (occ > 0 ? occ : 1);
-        const int grid = ntiles < cap ? ntiles : cap;
-#define PMG_SEG(S) k_half_sweep_seg<S><<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, \
-                                                                   nbr_zero, post_scale, ntiles, hx)
-        switch (L.seg) {
-        case 4: PMG_SEG(4); break;
-        case 8: PMG_SEG(8); break;
-        case 16: PMG_SEG(16); break;
-        default: PMG_SEG(32); break;
+        auto run = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+            const int cap = sm_count() * (occ > 0 ? occ : 1);
+            const int grid = ntiles < cap ? ntiles : cap;
+            kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
+                                            ntiles, hx);
+        };
+        const size_t sms = sm + sizeof(double) * (size_t)L.nz * 32 - sizeof(double) * 16 * 32;
+        auto runs = [&](auto kern) {
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+                attr = true;
+            }
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sms);
+            const int cap = sm_count() * (occ > 0 ? occ : 1);
+            const int grid = ntiles < cap ? ntiles : cap;
+            kern<<<grid, 32 * nw, sms, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
+                                             ntiles, hx);
+        };
+        auto run1 = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm1);
+            const int cap = sm_count() * (occ > 0 ? occ : 1);
+            const int grid = ntiles < cap ? ntiles : cap;
+            kern<<<grid, 32 * nw, sm1, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
+                                             ntiles, hx);
+        };
+        if (var == 0) {
+            // default: compile-time neighbour mode, predicate-free when the
+            // segments tile nz exactly (all BASELINE configs)
+            const bool full = (L.nz % L.seg) == 0;
+#define PMG_SEGF(S)                                                                   \
+    do {                                                                              \
+        if (full) {                                                                   \
+            if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true>);                    \
+            else run(k_half_sweep_seg<S, 4, 2, 0, true>);                             \
+        } else {                                                                      \
+            run(k_half_sweep_seg<S, 4, 2>);                                           \
+        }                                                                             \
+    } while (0)
+            switch (L.seg) {
+            case 4: PMG_SEGF(4); break;
+            case 8: PMG_SEGF(8); break;
+            case 16: PMG_SEGF(16); break;
+            default: run(k_half_sweep_seg<32, 4, 1>); break;
+            }
+#undef PMG_SEGF
+            return cudaGetLastError();
         }
-#undef PMG_SEG
+        if (var == 12) {
+            switch (L.seg) {
+            case 4: run1(k_half_sweep_seg1<4, 4, 2>); break;
+            case 8: run1(k_half_sweep_seg1<8, 4, 2>); break;
+            case 16: run1(k_half_sweep_seg1<16, 4, 2>); break;
+            default: run1(k_half_sweep_seg1<32, 4, 1>); break;
+            }
+            return cudaGetLastError();
+        }
+        switch (L.seg) {
+        case 4: run(k_half_sweep_seg<4, 4, 2>); break;
+        case 8: run(k_half_sweep_seg<8, 4, 2>); break;
+        case 16:
+            if (var == 10) {
+                if (L.nz % 16 == 0) {
+                    if (nbr_zero) run(k_half_sweep_seg<16, 4, 2, 1, true>);
+                    else run(k_half_sweep_seg<16, 4, 2, 0, true>);
+                } else {
+                    run(k_half_sweep_seg<16, 4, 2>);
+                }
+            } else if (var == 11) {
+                if (nbr_zero) run(k_half_sweep_seg<16, 8, 1, 1, true>);
+                else run(k_half_sweep_seg<16, 8, 1, 0, true>);
+            } else if (var == 1) run(k_half_sweep_seg<16, 8, 1>);
+            else if (var == 4) runs(k_half_sweep_segs<16, 4, 3>);
+            else if (var == 5) runs(k_half_sweep_segs<16, 8, 2>);
+            else if (var == 6) runs(k_half_sweep_segs<16, 4, 4>);
+            else if (var == 7) run1(k_half_sweep_seg1<16, 4, 3>);
+            else run(k_half_sweep_seg<16, 4, 2>);
+            break;
+        default: run(k_half_sweep_seg<32, 4, 1>); break;
+        }
         return cudaGetLastError();
     }
     if (hs_variant() == 3 && L.uniform) {
