@@ -125,6 +125,11 @@ int pmg_restrict(const pmg_level *fine, const pmg_level *coarse, const double *f
  * add = 0: overwrite owned cells, add = 1: u += P e (multigrid.py:287-290). */
 int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
                 double *fine_u, int add, void *stream);
+/* same, restricted to the colours in color_mask (1 red, 2 black, 3 both):
+ * with rho = 1 the post-smoothing red half-sweep overwrites every red cell
+ * without reading it, so the V-cycle prolongs into black cells only. */
+int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
+                       double *fine_u, int add, int color_mask, void *stream);
 
 /* ---- halos (partition.py:158-191) ----------------------------------- */
 /* Fill the whole halo ring of a part that is its own neighbour (one worker

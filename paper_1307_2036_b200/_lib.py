@@ -59,6 +59,7 @@ SIGNATURES = {
     "pmg_get_smoother_mode": (_I, []),
     "pmg_restrict": (_I, [_P, _P, _P, _P, _D, _P]),
     "pmg_prolong": (_I, [_P, _P, _P, _P, _I, _P]),
+    "pmg_prolong_colors": (_I, [_P, _P, _P, _P, _I, _I, _P]),
     "pmg_halo_self": (_I, [_P, _P, _I, _I, _P]),
     "pmg_face_doubles": (_LL, [_P, _I]),
     "pmg_pack_face": (_I, [_P, _P, _I, _P, _P]),

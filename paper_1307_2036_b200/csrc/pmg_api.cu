@@ -27,7 +27,8 @@ cudaError_t launch_half_sweep(const Lvl &, double *, const double *, int, double
 cudaError_t launch_invd(const Lvl &, double *, cudaStream_t);
 cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, double,
                             cudaStream_t);
-cudaError_t launch_prolong(const Lvl &, const Lvl &, const double *, double *, int, cudaStream_t);
+cudaError_t launch_prolong(const Lvl &, const Lvl &, const double *, double *, int, int,
+                           cudaStream_t);
 cudaError_t launch_halo_self(const Lvl &, double *, int, int, cudaStream_t);
 int face_len(const Lvl &, int);
 cudaError_t launch_pack(const Lvl &, const double *, int, double *, cudaStream_t);
@@ -367,7 +368,17 @@ int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *cu
                 int add, void *st) {
     int rc = check_pair(fine, coarse);
     if (rc) return rc;
-    PMG_CUDA(launch_prolong(fine->L, coarse->L, cu, fu, add, (cudaStream_t)st), "prolong");
+    PMG_CUDA(launch_prolong(fine->L, coarse->L, cu, fu, add, 3, (cudaStream_t)st), "prolong");
+    return PMG_OK;
+}
+
+int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *cu, double *fu,
+                       int add, int color_mask, void *st) {
+    int rc = check_pair(fine, coarse);
+    if (rc) return rc;
+    if (color_mask < 1 || color_mask > 3) return fail(PMG_ERR_VALUE, "color_mask must be 1, 2 or 3");
+    PMG_CUDA(launch_prolong(fine->L, coarse->L, cu, fu, add, color_mask, (cudaStream_t)st),
+             "prolong_colors");
     return PMG_OK;
 }
 

@@ -1904,12 +1904,13 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
 }
 
 __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu,
-                          int add) {
+                          int add, int cmask) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int k = blockIdx.y;
     const int j = blockIdx.z;
-    const int c = t & 1;                 // interleave colours inside a warp
-    const int h = t >> 1;
+    // cmask 3: both colours interleaved in a warp; 1 / 2: red / black only
+    const int c = (cmask == 3) ? (t & 1) : (cmask >> 1);
+    const int h = (cmask == 3) ? (t >> 1) : t;
     const int i = 2 * h + ((j + F.par + c) & 1);
     if (i >= F.nx) return;
     const int I = i >> 1, J = j >> 1;
@@ -2606,9 +2607,9 @@ cudaError_t launch_restrict(const Lvl &F, const Lvl &C, const double *fu, double
 }
 
 cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double *fu, int add,
-                           cudaStream_t st) {
+                           int cmask, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (getenv("PMG_PROLONG_B") != nullptr) {   // column walker (slower on B200)
+    if (getenv("PMG_PROLONG_B") != nullptr && cmask == 3) {   // column walker (slower on B200)
         constexpr int PB = 4;
         const int hx = ((F.nx + 1) / 2 + 31) / 32, jy = (F.ny + 3) / 4;
         int occ = 1;
@@ -2622,8 +2623,8 @@ cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double 
         k_prolong_b<PB><<<grid, 256, 0, st>>>(F, C, cu, fu, add, hx, ntiles, kcs);
         return cudaGetLastError();
     }
-    const int n2 = 2 * ((F.nx + 1) / 2);
-    k_prolong<<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add);
+    const int n2 = (cmask == 3 ? 2 : 1) * ((F.nx + 1) / 2);
+    k_prolong<<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
     return cudaGetLastError();
 }
 

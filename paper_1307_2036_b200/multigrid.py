@@ -203,11 +203,12 @@ def prolong(df: DistField, coarse: Level, fine: Level, out: DistField | None = N
     return out
 
 
-def _prolong_add(cu: DistField, coarse: Level, fine: Level, u: DistField) -> None:
+def _prolong_add(cu: DistField, coarse: Level, fine: Level, u: DistField,
+                 black_only: bool = False) -> None:
     st = _stream()
     for w, cf in cu.parts.items():
-        call("pmg_prolong", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
-             u.parts[w].ptr, 1, st)
+        call("pmg_prolong_colors", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
+             u.parts[w].ptr, 1, 2 if black_only else 3, st)
 
 
 def _residual_restrict(lev: Level, coarse: Level, f: DistField, u: DistField,
@@ -219,28 +220,48 @@ def _residual_restrict(lev: Level, coarse: Level, f: DistField, u: DistField,
 
 
 def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0) -> None:
-    """One V-cycle on ``scratch[c].u`` (halo-consistent on entry), Alg. 1."""
+    """One V-cycle on ``scratch[c].u`` (halo-consistent on entry), Alg. 1.
+
+    With ``cfg.fused`` and rho = 1 two pieces of provably dead work are
+    skipped (bit-identical result): the zero fill of the coarse iterate (its
+    first red half-sweep runs with neighbours_zero, rhs = f exactly as
+    f + drw*0, and the black half-sweep never reads old black values) and the
+    prolongation into red cells (the post-smoothing red half-sweep overwrites
+    them without reading them).
+    """
     lev = hier.levels[c]
     s = scratch[c]
+    lean = cfg.fused and cfg.rho == 1.0
     if c + 1 < len(hier.levels):
-        lev.smoother.sweep(s.u, s.f, cfg.nu_pre, cfg.rho)
+        _pre_smooth(lev, s, cfg.nu_pre, cfg.rho, lean and c > 0)
         coarse = hier.levels[c + 1]
         if cfg.fused:
             _residual_restrict(lev, coarse, s.f, s.u, scratch[c + 1].f)
         else:
             lev.op.residual(s.f, s.u, out=s.r)
             _restrict_into(s.r, lev, coarse, scratch[c + 1].f, 1.0)
-        scratch[c + 1].u.fill(0.0)
+        if not (lean and (cfg.nu_pre >= 1 or c + 2 == len(hier.levels))):
+            scratch[c + 1].u.fill(0.0)
         v_cycle(hier, cfg, scratch, c + 1)
         if cfg.fused:
-            _prolong_add(scratch[c + 1].u, coarse, lev, s.u)
+            _prolong_add(scratch[c + 1].u, coarse, lev, s.u, black_only=lean and cfg.nu_post >= 1)
         else:
             corr = prolong(scratch[c + 1].u, coarse, lev, out=s.r)
             _add_owned(s.u, corr)
         halo_exchange(s.u)
         lev.smoother.sweep(s.u, s.f, cfg.nu_post, cfg.rho)
     else:
-        lev.smoother.sweep(s.u, s.f, cfg.resolved_coarse_sweeps(), cfg.rho)
+        _pre_smooth(lev, s, cfg.resolved_coarse_sweeps(), cfg.rho, lean and c > 0)
+
+
+def _pre_smooth(lev: Level, s: _Scratch, nsweeps: int, rho: float, from_zero: bool) -> None:
+    """``nsweeps`` red-black sweeps; ``from_zero``: the iterate is zero on
+    entry but was not filled, so the first red half-sweep ignores u."""
+    for n in range(nsweeps):
+        lev.smoother.half_sweep(s.u, s.f, RED, rho, neighbors_zero=(from_zero and n == 0))
+        halo_exchange(s.u)
+        lev.smoother.half_sweep(s.u, s.f, BLACK, rho)
+        halo_exchange(s.u)
 
 
 def _add_owned(u: DistField, e: DistField) -> None:
