@@ -571,6 +571,77 @@ k_residual_restrict_v(Lvl F, Lvl C, const double *__restrict__ u, const double *
     }
 }
 
+// Warp-level residual + restriction (uniform): no CTA barriers.  A warp
+// owns 16 coarse columns of coarse row J: lane = q*8 + m, quarter q = (fine
+// row offset rr, colour c), m = column pair.  The four children of a coarse
+// cell live in the four quarters of the same m, so they are combined with
+// warp shuffles in the reference order ((s0 + s1) + s2) + s3.
+template <int KB>
+__global__ void __launch_bounds__(256, 2)
+k_residual_restrict_w(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
+                      double *__restrict__ cf, int hb16, int ntiles, int kcs) {
+    __shared__ double tdrw[256], tdiag[256], tband[257];
+    load_stencil_tables(F, tdrw, tdiag, tband);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int q = lane >> 3, m = lane & 7;
+    const int rr = q >> 1, c = q & 1;
+    const int nz = F.nz;
+    const int o = c ^ 1;
+    const long long pl = F.plane;
+    const int nkc = (nz + kcs - 1) / kcs;
+    // children slot -> quarter (depends only on the fine parity)
+    const int pf = F.par;
+    const int qa = pf ? 1 : 0, qb = pf ? 0 : 1, qc = pf ? 2 : 3, qd = pf ? 3 : 2;
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles;
+         tile += nwarps) {
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int J = t2 / hb16;
+        const int b = t2 - J * hb16;
+        const int j = 2 * J + rr;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const int s = (j + F.par + c) & 1;
+        const int hh = 16 * b + 2 * m;
+        const bool act = hh < C.nx;
+        const int h = act ? hh : 2 * ((C.nx - 1) / 2);
+        long long pc = at(F, c, kbeg, j, h);
+        long long po = at(F, o, kbeg, j, h);
+        long long pS = at(F, o, kbeg, j - 1, h);
+        long long pN = at(F, o, kbeg, j + 1, h);
+        long long px = at(F, o, kbeg, j, s ? h + 2 : h - 1);
+        const int cc0 = (h + J + C.par) & 1;
+        const long long q0 = at(C, cc0, kbeg, J, h >> 1);
+        const long long q1 = at(C, cc0 ^ 1, kbeg, J, h >> 1);
+        const bool two = act && (h + 1 < C.nx);
+        for (int k0 = kbeg; k0 < kend; k0 += KB) {
+            double r0[KB], r1[KB], u0[KB], u1[KB];
+            stencil_batch2<1, KB>(F, u, f, k0, s, pc, po, pS, pN, px, tdrw, tdiag, tband, r0, r1,
+                                  u0, u1);
+#pragma unroll
+            for (int t = 0; t < KB; ++t) {
+                double a = __shfl_sync(0xffffffffu, r0[t], qa * 8 + m) +
+                           __shfl_sync(0xffffffffu, r0[t], qb * 8 + m);
+                a = a + __shfl_sync(0xffffffffu, r0[t], qc * 8 + m);
+                a = a + __shfl_sync(0xffffffffu, r0[t], qd * 8 + m);
+                double bsum = __shfl_sync(0xffffffffu, r1[t], qa * 8 + m) +
+                              __shfl_sync(0xffffffffu, r1[t], qb * 8 + m);
+                bsum = bsum + __shfl_sync(0xffffffffu, r1[t], qc * 8 + m);
+                bsum = bsum + __shfl_sync(0xffffffffu, r1[t], qd * 8 + m);
+                const int k = k0 + t;
+                if ((t & 3) == q && act && k < kend) {
+                    const long long ko = (long long)(k - kbeg) * C.plane;
+                    cf[q0 + ko] = a;
+                    if (two) cf[q1 + ko] = bsum;
+                }
+            }
+            const long long step = (long long)KB * pl;
+            pc += step; po += step; pS += step; pN += step; px += step;
+        }
+    }
+}
+
 // Persistent batched residual + children-sum restriction: tile = 32 h x
 // fine rows (2J, 2J+1) x 2 colours = the 4 children of 32 coarse columns
 // (coarse I = h).  Fine residuals go through shared memory, are summed in
@@ -2347,6 +2418,21 @@ cudaError_t launch_finalize(const double *partials, int n, double *out, cudaStre
 cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u, const double *f,
                                      double *cf, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (F.uniform && F.nz <= 256 && getenv("PMG_RR_W") != nullptr) {   // warp-shuffle variant
+        constexpr int KB = 4;
+        const int hb16 = (C.nx + 15) / 16;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_w<KB>, 256, 0);
+        const int capw = sm_count() * (occ > 0 ? occ : 1) * 8;
+        int kcs = F.nz;
+        while (kcs > 2 * KB && (long long)hb16 * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * capw) kcs >>= 1;
+        kcs = (kcs + KB - 1) / KB * KB;
+        const int ntiles = hb16 * C.ny * ((F.nz + kcs - 1) / kcs);
+        int grid = (ntiles + 7) / 8;
+        if (grid > capw / 8) grid = capw / 8;
+        k_residual_restrict_w<KB><<<grid, 256, 0, st>>>(F, C, u, f, cf, hb16, ntiles, kcs);
+        return cudaGetLastError();
+    }
     if (F.uniform && F.nz <= 256 && getenv("PMG_RR_V0") == nullptr) {
         constexpr int KB = 4;
         const int hx = (C.nx + 63) / 64;

@@ -350,3 +350,44 @@ def test_config1_full_size(pmg):
     got = ug[idx[:, 0], idx[:, 1], idx[:, 2]]
     assert np.max(np.abs(got - g["sample_u"])) <= 1e-8 * float(g["u_absmax"])
     assert abs(ug.sum() - float(g["u_sum"])) <= 1e-8 * float(g["u_absmax"]) * ug.size ** 0.5
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("w", ["0.0001", "0.001", "0.01", "0.1"])
+def test_config2_cg_full_size(pmg, w):
+    """BASELINE configs[2]: CG + line SSOR at 1024^2 x 128 for the omega^2
+    sweep, against the reference's own full histories (make_golden.py big)."""
+    path = os.path.join(GOLD, f"config2_cg_w{w}.npz")
+    if not os.path.exists(path):
+        pytest.skip("config2 golden not generated")
+    from paper_1307_2036_b200 import configs
+    g = load(f"config2_cg_w{w}")
+    prob = configs.config(2, omega2=float(w))
+    op = pmg.PanelOperator(prob.grid(), prob.params())
+    pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+    f = pmg.scatter_owned(configs.rhs(prob.nx, prob.ny, prob.nz, 0), op.layout)
+    u, rep = pmg.pcg_solve(f, op, pre, eps=1e-5, maxiter=2000)
+    assert rep.iterations == int(g["iterations"])
+    assert hist_err(rep.residual_history, g["history"]) <= 1e-8
+    ug = pmg.gather_owned(u)
+    idx = g["sample_idx"]
+    got = ug[idx[:, 0], idx[:, 1], idx[:, 2]]
+    assert np.max(np.abs(got - g["sample_u"])) <= 1e-8 * float(g["u_absmax"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("w", ["0.0001", "0.01", "0.1"])
+def test_config2_mg_full_size(pmg, w):
+    """configs[2] companion: MG iteration counts stay flat across omega^2."""
+    path = os.path.join(GOLD, f"config2_mg_w{w}.npz")
+    if not os.path.exists(path):
+        pytest.skip("config2 MG golden not generated")
+    from paper_1307_2036_b200 import configs
+    g = load(f"config2_mg_w{w}")
+    prob = configs.config(2, omega2=float(w))
+    cfg = prob.mg_config()
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
+    f = pmg.scatter_owned(configs.rhs(prob.nx, prob.ny, prob.nz, 0), hier.fine.layout)
+    u, rep = pmg.mg_solve(f, hier, cfg)
+    assert rep.iterations == int(g["iterations"])
+    assert hist_err(rep.residual_history, g["history"]) <= 1e-8
