@@ -112,6 +112,13 @@ int pmg_residual_restrict(const pmg_level *fine, const pmg_level *coarse,
  * sequential Thomas recurrence, bit-identical to the reference.  Levels
  * with variable coefficients always use the exact solver. */
 int pmg_set_smoother_mode(int mode);
+/* half sweep of a part that is its own neighbour in both directions, with
+ * the halo ring refresh fused into the kernel (halo_flags: bit0 = on,
+ * bit1 = periodic x, bit2 = periodic y; mirror otherwise): equivalent to
+ * pmg_half_sweep + pmg_halo_self without the extra launch and pass. */
+int pmg_half_sweep_halo(const pmg_level *lvl, double *u, const double *f, int color,
+                        double rho, int zero_start, int neighbors_zero, double post_scale,
+                        int halo_flags, void *stream);
 int pmg_get_smoother_mode(void);
 int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
                    double rho, int zero_start, int neighbors_zero, double post_scale,
@@ -130,6 +137,10 @@ int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *co
  * without reading it, so the V-cycle prolongs into black cells only. */
 int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
                        double *fine_u, int add, int color_mask, void *stream);
+/* ... with the fused self-halo refresh of pmg_half_sweep_halo */
+int pmg_prolong_colors_halo(const pmg_level *fine, const pmg_level *coarse,
+                            const double *coarse_u, double *fine_u, int add, int color_mask,
+                            int halo_flags, void *stream);
 
 /* ---- halos (partition.py:158-191) ----------------------------------- */
 /* Fill the whole halo ring of a part that is its own neighbour (one worker

@@ -356,6 +356,23 @@ int pmg_half_sweep(const pmg_level *lv, double *u, const double *f, int color, d
     return PMG_OK;
 }
 
+int pmg_half_sweep_halo(const pmg_level *lv, double *u, const double *f, int color, double rho,
+                        int zero_start, int neighbors_zero, double post_scale, int halo_flags,
+                        void *st) {
+    PMG_CHECK_LVL(lv);
+    if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
+    if (!lv->L.uniform && !lv->prepared) {
+        int rc = pmg_level_prepare(const_cast<pmg_level *>(lv), st);
+        if (rc) return rc;
+    }
+    Lvl L = lv->L;
+    L.hflags = halo_flags & 7;
+    PMG_CUDA(launch_half_sweep(L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
+                               (cudaStream_t)st),
+             "half_sweep_halo");
+    return PMG_OK;
+}
+
 int pmg_restrict(const pmg_level *fine, const pmg_level *coarse, const double *ff, double *cf,
                  double weight, void *st) {
     int rc = check_pair(fine, coarse);
@@ -374,10 +391,17 @@ int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *cu
 
 int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *cu, double *fu,
                        int add, int color_mask, void *st) {
+    return pmg_prolong_colors_halo(fine, coarse, cu, fu, add, color_mask, 0, st);
+}
+
+int pmg_prolong_colors_halo(const pmg_level *fine, const pmg_level *coarse, const double *cu,
+                            double *fu, int add, int color_mask, int halo_flags, void *st) {
     int rc = check_pair(fine, coarse);
     if (rc) return rc;
     if (color_mask < 1 || color_mask > 3) return fail(PMG_ERR_VALUE, "color_mask must be 1, 2 or 3");
-    PMG_CUDA(launch_prolong(fine->L, coarse->L, cu, fu, add, color_mask, (cudaStream_t)st),
+    Lvl F = fine->L;
+    F.hflags = halo_flags & 7;
+    PMG_CUDA(launch_prolong(F, coarse->L, cu, fu, add, color_mask, (cudaStream_t)st),
              "prolong_colors");
     return PMG_OK;
 }

@@ -897,6 +897,7 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
             y = y + omr * so[k * 32 + lane];
         }
         u[pc + (long long)k * pl] = y;
+        halo_copies(L, u, i, j, k, y);
     }
 }
 
@@ -1498,7 +1499,7 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // (agrees with the sequential solve to ~1e-15 relative; the exact mode is
 // k_half_sweep_tma / k_half_sweep).
 // ---------------------------------------------------------------------------
-template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false>
+template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false>
 __global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                  int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles) {
@@ -1636,7 +1637,16 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                         y = y + omr * u[q];
                     }
                     u[q] = y;
+                    if (HALO) r[e] = y;
                 }
+            }
+        }
+        // fused self-halo: only tiles touching the part boundary (warp-uniform)
+        if (HALO && (j == 0 || j == L.ny - 1 || h0 == 0 || h0 + 32 >= ((L.nx - s0) + 1) / 2)) {
+            if (lane < nact) {
+#pragma unroll
+                for (int e = 0; e < SEG; ++e)
+                    if (e < kn) halo_copies(L, u, i, j, k0 + e, r[e]);
             }
         }
         __syncthreads();   // hend / ybeg reuse by the next tile
@@ -1974,6 +1984,7 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
     cu[cell(C, I, J, k)] = a;
 }
 
+template <bool HALO>
 __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu,
                           int add, int cmask) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1996,7 +2007,9 @@ __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *_
     e = e + cd;
     e = e * 0.0625;
     const long long q = at(F, c, k, j, h);
-    fu[q] = add ? fu[q] + e : e;
+    const double v = add ? fu[q] + e : e;
+    fu[q] = v;
+    if (HALO) halo_copies(F, fu, i, j, k, v);
 }
 
 // Persistent batched prolongation + add: thread = one fine column (h, row,
@@ -2498,9 +2511,28 @@ static int hs_variant() {
     return v;
 }
 
-cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int color, double rho,
+static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
+                                       double rho, int zero_start, int nbr_zero,
+                                       double post_scale, cudaStream_t st, bool *fused);
+
+cudaError_t launch_halo_self(const Lvl &L, double *d, int px, int py, cudaStream_t st);
+
+cudaError_t launch_half_sweep(const Lvl &L0, double *u, const double *f, int color, double rho,
                               int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    bool fused = false;
+    cudaError_t e = launch_half_sweep_k(L0, u, f, color, rho, zero_start, nbr_zero, post_scale,
+                                        st, &fused);
+    if (e == cudaSuccess && (L0.hflags & 1) && !fused) {
+        // this variant does not write halo copies itself
+        e = launch_halo_self(L0, u, (L0.hflags >> 1) & 1, (L0.hflags >> 2) & 1, st);
+    }
+    return e;
+}
+
+static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
+                                       double rho, int zero_start, int nbr_zero,
+                                       double post_scale, cudaStream_t st, bool *fused) {
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
     if (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) {
@@ -2549,9 +2581,14 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
             const bool full = (L.nz % L.seg) == 0;
 #define PMG_SEGF(S)                                                                   \
     do {                                                                              \
-        if (full) {                                                                   \
+        if (full && (L.hflags & 1)) {                                                 \
+            if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true, true>);              \
+            else run(k_half_sweep_seg<S, 4, 2, 0, true, true>);                       \
+        } else if (full) {                                                            \
             if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true>);                    \
             else run(k_half_sweep_seg<S, 4, 2, 0, true>);                             \
+        } else if (L.hflags & 1) {                                                    \
+            run(k_half_sweep_seg<S, 4, 2, -1, false, true>);                          \
         } else {                                                                      \
             run(k_half_sweep_seg<S, 4, 2>);                                           \
         }                                                                             \
@@ -2563,6 +2600,7 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
             default: run(k_half_sweep_seg<32, 4, 1>); break;
             }
 #undef PMG_SEGF
+            *fused = true;
             return cudaGetLastError();
         }
         if (var == 12) {
@@ -2666,6 +2704,7 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
             attr_set[0] = true;
         }
         k_half_sweep<true><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
+        *fused = true;
     } else {
         if (!attr_set[1]) {
             cudaFuncSetAttribute(k_half_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2675,6 +2714,7 @@ cudaError_t launch_half_sweep(const Lvl &L, double *u, const double *f, int colo
             attr_set[1] = true;
         }
         k_half_sweep<false><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
+        *fused = true;
     }
     return cudaGetLastError();
 }
@@ -2710,7 +2750,10 @@ cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double 
         return cudaGetLastError();
     }
     const int n2 = (cmask == 3 ? 2 : 1) * ((F.nx + 1) / 2);
-    k_prolong<<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+    if (F.hflags & 1)
+        k_prolong<true><<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+    else
+        k_prolong<false><<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
     return cudaGetLastError();
 }
 

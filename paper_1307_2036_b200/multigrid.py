@@ -27,7 +27,7 @@ from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
 from .partition import (Decomposition, DistField, LevelLayout, _dist, _stream, dist_norm,
-                        halo_exchange, reduce_parts)
+                        halo_exchange, reduce_parts, self_halo_flags)
 from .smoother import BLACK, RED, LineSmoother
 from .stencil import PanelOperator
 
@@ -204,11 +204,19 @@ def prolong(df: DistField, coarse: Level, fine: Level, out: DistField | None = N
 
 
 def _prolong_add(cu: DistField, coarse: Level, fine: Level, u: DistField,
-                 black_only: bool = False) -> None:
+                 black_only: bool = False, exchange: bool = False) -> None:
+    """u += P e (into black cells only if ``black_only``); ``exchange``
+    also refreshes u's halo (fused into the kernel on a single part)."""
     st = _stream()
+    hf = self_halo_flags(u.layout) if exchange else 0
     for w, cf in cu.parts.items():
-        call("pmg_prolong_colors", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
-             u.parts[w].ptr, 1, 2 if black_only else 3, st)
+        call("pmg_prolong_colors_halo", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
+             u.parts[w].ptr, 1, 2 if black_only else 3, hf, st)
+    if exchange:
+        if hf:
+            u.layout.halo_count += 1
+        else:
+            halo_exchange(u)
 
 
 def _residual_restrict(lev: Level, coarse: Level, f: DistField, u: DistField,
@@ -244,11 +252,12 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0) -> None:
             scratch[c + 1].u.fill(0.0)
         v_cycle(hier, cfg, scratch, c + 1)
         if cfg.fused:
-            _prolong_add(scratch[c + 1].u, coarse, lev, s.u, black_only=lean and cfg.nu_post >= 1)
+            _prolong_add(scratch[c + 1].u, coarse, lev, s.u, black_only=lean and cfg.nu_post >= 1,
+                         exchange=True)
         else:
             corr = prolong(scratch[c + 1].u, coarse, lev, out=s.r)
             _add_owned(s.u, corr)
-        halo_exchange(s.u)
+            halo_exchange(s.u)
         lev.smoother.sweep(s.u, s.f, cfg.nu_post, cfg.rho)
     else:
         _pre_smooth(lev, s, cfg.resolved_coarse_sweeps(), cfg.rho, lean and c > 0)
@@ -258,10 +267,8 @@ def _pre_smooth(lev: Level, s: _Scratch, nsweeps: int, rho: float, from_zero: bo
     """``nsweeps`` red-black sweeps; ``from_zero``: the iterate is zero on
     entry but was not filled, so the first red half-sweep ignores u."""
     for n in range(nsweeps):
-        lev.smoother.half_sweep(s.u, s.f, RED, rho, neighbors_zero=(from_zero and n == 0))
-        halo_exchange(s.u)
-        lev.smoother.half_sweep(s.u, s.f, BLACK, rho)
-        halo_exchange(s.u)
+        lev.smoother.half_sweep_exchange(s.u, s.f, RED, rho, neighbors_zero=(from_zero and n == 0))
+        lev.smoother.half_sweep_exchange(s.u, s.f, BLACK, rho)
 
 
 def _add_owned(u: DistField, e: DistField) -> None:

@@ -342,6 +342,20 @@ def _ptr(t: torch.Tensor):
     return C.c_void_p(t.data_ptr())
 
 
+def self_halo_flags(lay: "LevelLayout") -> int:
+    """halo_flags for kernels that refresh the halo ring themselves: nonzero
+    only for a single-part layout (its own neighbour in both directions)."""
+    if lay.px == 1 and lay.py == 1 and _FUSED_HALO:
+        return 1 | (2 if lay.periodic else 0) | (4 if lay.periodic else 0)
+    return 0
+
+
+import os as _os
+# fused halos measured slower on B200 for configs[1] (boundary-tile epilogue
+# imbalances the persistent smoother grid): opt-in
+_FUSED_HALO = bool(_os.environ.get("PMG_FUSED_HALO"))
+
+
 def halo_exchange(df: DistField) -> None:
     """Refresh every halo cell: x strips first, then y strips over the
     extended range (corners), periodic wrap or mirror at physical
