@@ -308,9 +308,9 @@ def main():
                       "GB_s": b * n_fine / tt / 1e9}
     peak, peak_src = measured_peak()
     ach = 12 * n_fine / t_hs / 1e9
-    traffic = ncu_traffic("k_half_sweep")
+    traffic = ncu_traffic("k_half_sweep_seg")
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": traffic, "kernel": "k_half_sweep (fine level)",
+                "frac": ach / peak, "traffic": traffic, "kernel": "k_half_sweep_seg (fine level, fast line solver)",
                 "alg_bytes_per_launch": 12 * n_fine, "launch_ms": t_hs * 1e3,
                 "peak_source": peak_src}
 

@@ -356,6 +356,14 @@ import os as _os
 _FUSED_HALO = bool(_os.environ.get("PMG_FUSED_HALO"))
 
 
+def set_fused_halo(on: bool) -> bool:
+    """Enable the in-kernel halo refresh for single-part layouts; returns the
+    previous setting."""
+    global _FUSED_HALO
+    prev, _FUSED_HALO = _FUSED_HALO, bool(on)
+    return prev
+
+
 def halo_exchange(df: DistField) -> None:
     """Refresh every halo cell: x strips first, then y strips over the
     extended range (corners), periodic wrap or mirror at physical

@@ -391,3 +391,25 @@ def test_config2_mg_full_size(pmg, w):
     u, rep = pmg.mg_solve(f, hier, cfg)
     assert rep.iterations == int(g["iterations"])
     assert hist_err(rep.residual_history, g["history"]) <= 1e-8
+
+
+@pytest.mark.parametrize("name", OPS)
+def test_fused_halo_path(pmg, name):
+    """In-kernel halo refresh (opt-in) gives the same V-cycle and solve."""
+    from paper_1307_2036_b200 import partition
+    g, grid, params, cfg, hier = setup(pmg, name)
+    nx, nz = grid.nx, grid.nz
+    prev = partition.set_fused_halo(True)
+    try:
+        with pmg.exact_smoother():
+            scratch = hier.make_scratch()
+            scratch[0].f.copy_from(field(pmg, uni((nx, nx, nz), 2), hier.fine.layout))
+            pmg.v_cycle(hier, cfg, scratch)
+            assert np.array_equal(pmg.gather_owned(scratch[0].u), g["vcycle1"])
+        cfg2 = pmg.MGConfig(policy="explicit", explicit_levels=int(g["nlev"]), graph=False)
+        u, rep = pmg.mg_solve(pmg.scatter_owned(uni((nx, nx, nz), 2), hier.fine.layout), hier,
+                              cfg2)
+        assert rep.iterations == len(g["mg_history"]) - 1
+        assert hist_err(rep.residual_history, g["mg_history"]) <= 1e-10
+    finally:
+        partition.set_fused_halo(prev)

@@ -52,9 +52,12 @@ if os.path.exists(p):
     lines.append("")
 
 # ---- full capture of fine-level kernels ----
-p = os.path.join(GO, "prof_fine.ncu-rep")
 traffic = {}
-if os.path.exists(p):
+import glob
+CURRENT = ["k_half_sweep_seg", "k_apply_v", "k_residual_restrict_v", "k_prolong"]
+for p in [os.path.join(GO, f"prof_{k}.ncu-rep") for k in CURRENT]:
+    if not os.path.exists(p):
+        continue
     raw = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
@@ -64,7 +67,7 @@ if os.path.exists(p):
             "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
             "launch__grid_size", "launch__block_size"]
-    lines.append("# ncu --set full, fine level (1024^2 x 128) kernels")
+    lines.append(f"# ncu --set full, fine level (1024^2 x 128): {os.path.basename(p)}")
     for r in rows[2:]:
         name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "")
         vals = {}

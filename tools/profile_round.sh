@@ -12,8 +12,9 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     -c 4000 --csv --log-file gpurun_out/launches.csv python bench.py $ARGS > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launch rc=$?"
 # fine-level kernels: the first launches of each in a solve are the finest level
-python tools/kbench.py --levels 2 > gpurun_out/kb.log 2>&1 && \
-ncu --set full --clock-control none --import-source on \
-    -k regex:"k_half_sweep_seg|k_apply_b|k_residual_restrict_b|k_prolong" -c 4 \
-    -o gpurun_out/prof_fine python tools/kbench.py --levels 2 > gpurun_out/ncu_full.log 2>&1
-echo "ncu full rc=$?"
+python tools/kbench.py --levels 2 > gpurun_out/kb.log 2>&1
+for k in k_half_sweep_seg k_apply_v k_residual_restrict_v k_prolong; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
+      -o gpurun_out/prof_$k python tools/kbench.py --levels 2 > gpurun_out/ncu_$k.log 2>&1
+  echo "ncu full $k rc=$?"
+done
