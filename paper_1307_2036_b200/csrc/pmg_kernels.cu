@@ -363,12 +363,87 @@ __device__ __forceinline__ D2 ld2(const double *p) {
     return D2{v.x, v.y};
 }
 
-template <int MODE, int KB>
+// per-column coefficients of a column pair (variable levels; uniform levels
+// use the level scalars)
+struct Col2 {
+    double wxm, wxp, wym, wyp, cv, vh, osw;
+};
+
+template <bool UNI>
+__device__ __forceinline__ Col2 col2_coeffs(const Lvl &L, int i, int j) {
+    Col2 C;
+    if (UNI) {
+        C.wxm = C.wxp = L.wx0;
+        C.wym = C.wyp = L.wy0;
+        C.cv = L.csub0;
+        C.vh = C.osw = 0.0;
+    } else {
+        C.wxm = L.wx[(long long)j * (L.nx + 1) + i];
+        C.wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
+        C.wym = L.wy[(long long)j * L.nx + i];
+        C.wyp = L.wy[(long long)(j + 1) * L.nx + i];
+        C.cv = L.vcoef * L.av[(long long)j * L.nx + i];
+        C.vh = L.vh[(long long)j * L.nx + i];
+        C.osw = L.omega2 * L.sumw[(long long)j * L.nx + i];
+    }
+    return C;
+}
+
+// shared 1-D tables of a level: uniform -> drw, diag, band; variable ->
+// drw, volprof, dr, vprof
+struct Tabs {
+    double *drw, *diag, *band, *vol, *dr, *vp;
+};
+
+__device__ __forceinline__ void load_tabs(const Lvl &L, const Tabs &T) {
+    const int nthr = blockDim.x * blockDim.y;
+    for (int t = threadIdx.x + blockDim.x * threadIdx.y; t <= L.nz; t += nthr) {
+        if (t < L.nz) T.drw[t] = L.drw[t];
+        if (L.uniform) {
+            if (t < L.nz) T.diag[t] = L.diag1[t];
+            T.band[t] = L.band1[t];
+        } else {
+            if (t < L.nz) {
+                T.vol[t] = L.volprof[t];
+                T.dr[t] = L.dr[t];
+            }
+            T.vp[t] = L.vprof[t];
+        }
+    }
+}
+
+template <int MODE, int KB, bool UNI>
+__device__ __forceinline__ double cell_res(const Lvl &L, const Tabs &T, const Col2 &C, int k,
+                                           double w, double e, double sn, double nn, double um,
+                                           double u0, double up, double fv) {
+    const int nz = L.nz;
+    const int kk = min(k, nz - 1);
+    double acc = C.wxm * w;
+    acc = acc + C.wxp * e;
+    acc = acc + C.wym * sn;
+    acc = acc + C.wyp * nn;
+    acc = acc * T.drw[kk];
+    double d;
+    if (UNI) {
+        d = T.diag[kk];
+    } else {
+        d = C.vh * T.vol[kk];
+        d = d + C.osw * T.dr[kk];
+        d = d + C.cv * (T.vp[kk] + T.vp[kk + 1]);
+    }
+    double r = d * u0 - acc;
+    if (k >= 1) r = r - (UNI ? T.band[min(k, nz)] : C.cv * T.vp[min(k, nz)]) * um;
+    if (k + 1 < nz) r = r - (UNI ? T.band[k + 1] : C.cv * T.vp[k + 1]) * up;
+    if (MODE == 1) r = fv - r;
+    return r;
+}
+
+template <int MODE, int KB, bool UNI = true>
 __device__ __forceinline__ void stencil_batch2(
     const Lvl &L, const double *__restrict__ u, const double *__restrict__ f, int k0, int s,
-    long long pc, long long po, long long pS, long long pN, long long px, const double *tdrw,
-    const double *tdiag, const double *tband, double (&r0)[KB], double (&r1)[KB],
-    double (&u0)[KB], double (&u1)[KB]) {
+    long long pc, long long po, long long pS, long long pN, long long px, const Tabs &T,
+    const Col2 &A, const Col2 &B, double (&r0)[KB], double (&r1)[KB], double (&u0)[KB],
+    double (&u1)[KB]) {
     const int nz = L.nz;
     const long long pl = L.plane;
     D2 uc[KB + 2], vo[KB], vs[KB], vn[KB], vf[KB];
@@ -385,7 +460,6 @@ __device__ __forceinline__ void stencil_batch2(
         if (MODE == 1) vf[t] = ld2(f + pc + ko);
     }
     uc[KB + 1] = ld2(u + pc + (long long)min(KB, nz - 1 - k0) * pl);
-    const double w0 = L.wx0, w1 = L.wy0;
 #pragma unroll
     for (int t = 0; t < KB; ++t) {
         const int k = k0 + t;
@@ -396,46 +470,22 @@ __device__ __forceinline__ void stencil_batch2(
         const double eb = s ? vx[t] : vo[t].y;
         u0[t] = uc[t + 1].x;
         u1[t] = uc[t + 1].y;
-        double acc = w0 * wa;
-        acc = acc + w0 * ea;
-        acc = acc + w1 * vs[t].x;
-        acc = acc + w1 * vn[t].x;
-        acc = acc * tdrw[min(k, nz - 1)];
-        double bcc = w0 * wb;
-        bcc = bcc + w0 * eb;
-        bcc = bcc + w1 * vs[t].y;
-        bcc = bcc + w1 * vn[t].y;
-        bcc = bcc * tdrw[min(k, nz - 1)];
-        const double d = tdiag[min(k, nz - 1)];
-        double ra = d * uc[t + 1].x - acc;
-        double rb = d * uc[t + 1].y - bcc;
-        if (k >= 1) {
-            const double bl = tband[min(k, nz)];
-            ra = ra - bl * uc[t].x;
-            rb = rb - bl * uc[t].y;
-        }
-        if (k + 1 < nz) {
-            const double bu = tband[k + 1];
-            ra = ra - bu * uc[t + 2].x;
-            rb = rb - bu * uc[t + 2].y;
-        }
-        if (MODE == 1) {
-            ra = vf[t].x - ra;
-            rb = vf[t].y - rb;
-        }
-        r0[t] = ra;
-        r1[t] = rb;
+        r0[t] = cell_res<MODE, KB, UNI>(L, T, A, k, wa, ea, vs[t].x, vn[t].x, uc[t].x,
+                                        uc[t + 1].x, uc[t + 2].x, MODE == 1 ? vf[t].x : 0.0);
+        r1[t] = cell_res<MODE, KB, UNI>(L, T, B, k, wb, eb, vs[t].y, vn[t].y, uc[t].y,
+                                        uc[t + 1].y, uc[t + 2].y, MODE == 1 ? vf[t].y : 0.0);
     }
 }
 
 // tile = 64 columns x AP_TY rows x 2 colours, column-pair threads walk k
-template <int MODE, bool NORM, int KB>
+template <int MODE, bool NORM, int KB, bool UNI = true>
 __global__ void __launch_bounds__(32 * 2 * AP_TY, 2)
 k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
           double *__restrict__ out, double *__restrict__ partials, int hx, int jy, int ntiles,
           int kcs) {
-    __shared__ double tdrw[256], tdiag[256], tband[257];
-    load_stencil_tables(L, tdrw, tdiag, tband);
+    __shared__ double s_drw[256], s_a[257], s_b[257], s_c[257];
+    const Tabs T{s_drw, s_a, s_b, s_a, s_b, s_c};
+    load_tabs(L, T);
     __syncthreads();
     const int lane = threadIdx.x;
     const int c = threadIdx.y & 1;
@@ -459,6 +509,8 @@ k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
         const int h = 2 * mm;
         const bool two = act && (h + 1 < ncol);
         const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const Col2 A = col2_coeffs<UNI>(L, 2 * h + s, j);
+        const Col2 B = col2_coeffs<UNI>(L, min(2 * h + 2 + s, L.nx - 1), j);
         long long pc = at(L, c, kbeg, j, h);
         long long po = at(L, o, kbeg, j, h);
         long long pS = at(L, o, kbeg, j - 1, h);
@@ -466,8 +518,8 @@ k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
         long long px = at(L, o, kbeg, j, s ? h + 2 : h - 1);
         for (int k0 = kbeg; k0 < kend; k0 += KB) {
             double r0[KB], r1[KB], u0[KB], u1[KB];
-            stencil_batch2<MODE, KB>(L, u, f, k0, s, pc, po, pS, pN, px, tdrw, tdiag, tband, r0,
-                                     r1, u0, u1);
+            stencil_batch2<MODE, KB, UNI>(L, u, f, k0, s, pc, po, pS, pN, px, T, A, B, r0, r1,
+                                          u0, u1);
             if (act) {
 #pragma unroll
                 for (int t = 0; t < KB; ++t) {
@@ -502,13 +554,14 @@ k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
 // computes the residual of fine columns h = 2m, 2m+1 in fine row 2J + rr;
 // children are combined in shared memory in the reference order and each
 // thread writes coarse I = 2m and 2m+1 (one per colour array, coalesced).
-template <int KB>
+template <int KB, bool UNI = true>
 __global__ void __launch_bounds__(128, 4)
 k_residual_restrict_v(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
                       double *__restrict__ cf, int hx, int ntiles, int kcs) {
-    __shared__ double tdrw[256], tdiag[256], tband[257];
+    __shared__ double s_drw[256], s_a[257], s_b[257], s_c[257];
     __shared__ double rs[4][KB][65];
-    load_stencil_tables(F, tdrw, tdiag, tband);
+    const Tabs T{s_drw, s_a, s_b, s_a, s_b, s_c};
+    load_tabs(F, T);
     __syncthreads();
     const int lane = threadIdx.x;
     const int ty = threadIdx.y;              // 2 * rr + c
@@ -534,14 +587,16 @@ k_residual_restrict_v(Lvl F, Lvl C, const double *__restrict__ u, const double *
         long long pN = at(F, o, kbeg, j + 1, h);
         long long px = at(F, o, kbeg, j, s ? h + 2 : h - 1);
         const int slot = 2 * rr + s;
+        const Col2 A = col2_coeffs<UNI>(F, 2 * h + s, j);
+        const Col2 B = col2_coeffs<UNI>(F, min(2 * h + 2 + s, F.nx - 1), j);
         const int cc0 = (2 * m + J + C.par) & 1;       // colour of coarse I = 2m
         const long long q0 = act ? at(C, cc0, kbeg, J, m) : 0;
         const long long q1 = act ? at(C, cc0 ^ 1, kbeg, J, m) : 0;
         const bool two = act && (2 * m + 1 < C.nx);
         for (int k0 = kbeg; k0 < kend; k0 += KB) {
             double r0[KB], r1[KB], u0[KB], u1[KB];
-            stencil_batch2<1, KB>(F, u, f, k0, s, pc, po, pS, pN, px, tdrw, tdiag, tband, r0, r1,
-                                  u0, u1);
+            stencil_batch2<1, KB, UNI>(F, u, f, k0, s, pc, po, pS, pN, px, T, A, B, r0, r1,
+                                       u0, u1);
 #pragma unroll
             for (int t = 0; t < KB; ++t) {
                 rs[slot][t][2 * lane] = r0[t];
@@ -617,8 +672,12 @@ k_residual_restrict_w(Lvl F, Lvl C, const double *__restrict__ u, const double *
         const bool two = act && (h + 1 < C.nx);
         for (int k0 = kbeg; k0 < kend; k0 += KB) {
             double r0[KB], r1[KB], u0[KB], u1[KB];
-            stencil_batch2<1, KB>(F, u, f, k0, s, pc, po, pS, pN, px, tdrw, tdiag, tband, r0, r1,
-                                  u0, u1);
+            {
+                const Tabs T{tdrw, tdiag, tband, nullptr, nullptr, nullptr};
+                const Col2 A = col2_coeffs<true>(F, 0, 0);
+                stencil_batch2<1, KB, true>(F, u, f, k0, s, pc, po, pS, pN, px, T, A, A, r0, r1,
+                                            u0, u1);
+            }
 #pragma unroll
             for (int t = 0; t < KB; ++t) {
                 double a = __shfl_sync(0xffffffffu, r0[t], qa * 8 + m) +
@@ -1941,6 +2000,145 @@ k_half_sweep_seg1(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
     }
 }
 
+// ---------------------------------------------------------------------------
+// FAST half-sweep for VARIABLE coefficients (configs[4]): the k-segmented
+// solve of k_half_sweep_seg with per-column weights / vertical coupling and
+// the per-cell pivots of the level (L.invd, smoother.py:93-99) loaded with
+// the RHS batch; the segment products (pf, q) are formed on the fly and
+// published with the boundary values.  nz must be a multiple of SEG.
+// ---------------------------------------------------------------------------
+template <int SEG, int NBZ>
+__global__ void __launch_bounds__(512, 1)
+k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
+                  int zero_start, int post_scale_unused, double post_scale, int ntiles,
+                  int htiles) {
+    extern __shared__ double vsm[];
+    const int nz = L.nz;
+    double *tdrw = vsm;                  // [nz]
+    double *tvp = tdrw + nz;             // [nz+1]
+    double *xh = tvp + ((nz + 2) & ~1);  // [16][32] segment end h
+    double *xp = xh + 16 * 32;           // [16][32] segment product of alpha
+    double *xy = xp + 16 * 32;           // [16][32] segment start y
+    double *xq = xy + 16 * 32;           // [16][32] segment product of mu
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
+        if (t < nz) tdrw[t] = L.drw[t];
+        tvp[t] = L.vprof[t];
+    }
+    __syncthreads();
+    const int o = c ^ 1;
+    const long long pl = L.plane;
+    const int k0 = w * SEG;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int j = t / htiles;
+        const int h0 = (t - j * htiles) * 32;
+        const int s0 = (j + L.par + c) & 1;
+        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+        const int ln = min(lane, nact - 1);
+        const bool lastlane = (ln == nact - 1);
+        const int h = h0 + ln;
+        const int i = 2 * h + s0;
+        const long long pc = at(L, c, k0, j, h);
+        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
+        const long long pS = at(L, o, k0, j - 1, h);
+        const long long pN = at(L, o, k0, j + 1, h);
+        const long long q2 = (long long)j * L.nx + i;
+        const double wxm = L.wx[(long long)j * (L.nx + 1) + i];
+        const double wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
+        const double wym = L.wy[q2];
+        const double wyp = L.wy[(long long)(j + 1) * L.nx + i];
+        const double cv = L.vcoef * L.av[q2];
+        double r[SEG], vi[SEG], pq[SEG];
+#pragma unroll
+        constexpr int B = SEG < 4 ? SEG : 4;
+#pragma unroll
+        for (int b8 = 0; b8 < SEG; b8 += B) {
+            double vf[B], vw[B], vs[B], vn[B], vx[B], vv[B];
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                const long long ko = (long long)(b8 + e) * pl;
+                vf[e] = f[pc + ko];
+                vv[e] = L.invd[pc + ko];
+                if (!NBZ) {
+                    vw[e] = u[pW + ko];
+                    vs[e] = u[pS + ko];
+                    vn[e] = u[pN + ko];
+                    vx[e] = lastlane ? u[pE + ko] : 0.0;
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < B; ++e) {
+                double g;
+                if (NBZ) {
+                    g = vf[e];
+                } else {
+                    double ve = __shfl_down_sync(0xffffffffu, vw[e], 1);
+                    if (lastlane) ve = vx[e];
+                    g = wxm * vw[e];
+                    g = g + wxp * ve;
+                    g = g + wym * vs[e];
+                    g = g + wyp * vn[e];
+                    g = g * tdrw[k0 + b8 + e];
+                    g = g + vf[e];
+                }
+                r[b8 + e] = g;
+                vi[b8 + e] = vv[e];
+            }
+        }
+        // local forward h_k = iota_k r_k + alpha_k h_{k-1}, alpha_k = (cv vp_k) iota_k
+        double hp = 0.0, pf = 1.0;
+#pragma unroll
+        for (int e = 0; e < SEG; ++e) {
+            const int k = k0 + e;
+            const double al = (k == 0) ? 0.0 : (cv * tvp[k]) * vi[e];
+            pf *= al;
+            pq[e] = pf;
+            hp = __fma_rn(al, hp, vi[e] * r[e]);
+            r[e] = hp;
+        }
+        xh[w * 32 + lane] = hp;
+        xp[w * 32 + lane] = pf;
+        __syncthreads();
+        double G = 0.0;
+        for (int sg = 0; sg < w; ++sg) G = __fma_rn(xp[sg * 32 + lane], G, xh[sg * 32 + lane]);
+        // fix-up g = h + pf G, local backward y_k = g_k + mu_k y_{k+1}
+        double yp = 0.0, qq = 1.0;
+#pragma unroll
+        for (int e = SEG - 1; e >= 0; --e) {
+            const int k = k0 + e;
+            const double mu = (k + 1 < nz) ? (cv * tvp[k + 1]) * vi[e] : 0.0;
+            const double g = __fma_rn(pq[e], G, r[e]);
+            qq *= mu;
+            pq[e] = qq;
+            yp = __fma_rn(mu, yp, g);
+            r[e] = yp;
+        }
+        xy[w * 32 + lane] = yp;
+        xq[w * 32 + lane] = qq;
+        __syncthreads();
+        double X = 0.0;
+        for (int sg = nw - 1; sg > w; --sg) X = __fma_rn(xq[sg * 32 + lane], X, xy[sg * 32 + lane]);
+        if (lane < nact) {
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                double y = __fma_rn(pq[e], X, r[e]);
+                const long long q = pc + (long long)e * pl;
+                if (zero_start) {
+                    if (scale != 1.0) y = y * scale;
+                } else if (rho != 1.0) {
+                    y = y * rho;
+                    y = y + omr * u[q];
+                }
+                u[q] = y;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // per-column pivots of a variable-coefficient level (smoother.py:93-99)
 __global__ void k_invd(Lvl L, double *__restrict__ invd) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2338,7 +2536,7 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
-    if (apply_variant() == 0 && L.uniform && L.nz <= 256 && getenv("PMG_APPLY_V0") == nullptr) {
+    if (apply_variant() == 0 && L.nz <= 256 && getenv("PMG_APPLY_V0") == nullptr) {
         // vectorised column pairs
         constexpr int KB = 4;
         const int hx = ((L.nx + 1) / 2 + 63) / 64, jy = (L.ny + AP_TY - 1) / AP_TY;
@@ -2355,9 +2553,15 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
             *nparts = grid;
             kern<<<grid, dim3(32, 2 * AP_TY), 0, st>>>(L, u, f, out, partials, hx, jy, ntiles, kcs);
         };
-        if (mode == 0) go(k_apply_v<0, false, KB>);
-        else if (mode == 1) { if (norm) go(k_apply_v<1, true, KB>); else go(k_apply_v<1, false, KB>); }
-        else go(k_apply_v<2, true, KB>);
+        if (L.uniform) {
+            if (mode == 0) go(k_apply_v<0, false, KB, true>);
+            else if (mode == 1) { if (norm) go(k_apply_v<1, true, KB, true>); else go(k_apply_v<1, false, KB, true>); }
+            else go(k_apply_v<2, true, KB, true>);
+        } else {
+            if (mode == 0) go(k_apply_v<0, false, KB, false>);
+            else if (mode == 1) { if (norm) go(k_apply_v<1, true, KB, false>); else go(k_apply_v<1, false, KB, false>); }
+            else go(k_apply_v<2, true, KB, false>);
+        }
         return cudaGetLastError();
     }
     if (apply_variant() == 0 && L.nz <= 256 && L.nz >= 16 && getenv("PMG_APPLY_T") != nullptr) {
@@ -2446,18 +2650,24 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
         k_residual_restrict_w<KB><<<grid, 256, 0, st>>>(F, C, u, f, cf, hb16, ntiles, kcs);
         return cudaGetLastError();
     }
-    if (F.uniform && F.nz <= 256 && getenv("PMG_RR_V0") == nullptr) {
+    if (F.nz <= 256 && getenv("PMG_RR_V0") == nullptr) {
         constexpr int KB = 4;
         const int hx = (C.nx + 63) / 64;
         int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_v<KB>, 128, 0);
+        if (F.uniform)
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_v<KB, true>, 128, 0);
+        else
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_v<KB, false>, 128, 0);
         const int cap = sm_count() * (occ > 0 ? occ : 1);
         int kcs = F.nz;
         while (kcs > 2 * KB && (long long)hx * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
         kcs = (kcs + KB - 1) / KB * KB;
         const int ntiles = hx * C.ny * ((F.nz + kcs - 1) / kcs);
         const int grid = ntiles < cap ? ntiles : cap;
-        k_residual_restrict_v<KB><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
+        if (F.uniform)
+            k_residual_restrict_v<KB, true><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
+        else
+            k_residual_restrict_v<KB, false><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
         return cudaGetLastError();
     }
     if (F.nz <= 256 && getenv("PMG_RR_OLD") == nullptr) {
@@ -2535,6 +2745,34 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
                                        double post_scale, cudaStream_t st, bool *fused) {
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
+    if (!g_smoother_exact && !L.uniform && L.nz <= 256 && getenv("PMG_VAR_EXACT") == nullptr) {
+        // variable coefficients: 16 warps, SEG = nz / 16 (must divide)
+        int seg = 0;
+        if (L.nz % 16 == 0 && L.nz / 16 <= 16) seg = L.nz / 16;
+        if (seg == 1 || seg == 2 || seg == 4 || seg == 8 || seg == 16) {
+            const int nw = L.nz / seg;
+            const size_t sm = sizeof(double) * (L.nz + ((L.nz + 2) & ~1) + 4 * 16 * 32);
+            const int ntiles = hx * L.ny;
+            auto runv = [&](auto kern) {
+                int occ = 1;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+                const int cap = sm_count() * (occ > 0 ? occ : 1);
+                const int grid = ntiles < cap ? ntiles : cap;
+                kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, 0, post_scale,
+                                                ntiles, hx);
+            };
+#define PMG_SEGV(S) do { if (nbr_zero) runv(k_half_sweep_segv<S, 1>); else runv(k_half_sweep_segv<S, 0>); } while (0)
+            switch (seg) {
+            case 1: PMG_SEGV(1); break;
+            case 2: PMG_SEGV(2); break;
+            case 4: PMG_SEGV(4); break;
+            case 8: PMG_SEGV(8); break;
+            default: PMG_SEGV(16); break;
+            }
+#undef PMG_SEGV
+            return cudaGetLastError();
+        }
+    }
     if (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) {
         const int nw = (L.nz + L.seg - 1) / L.seg;
         const size_t sm = sizeof(double) * (6 * (size_t)L.nz + 2 * 16 * 32);
