@@ -171,13 +171,19 @@ int pmg_dot(const pmg_level *lvl, const double *a, const double *b, double *scra
  * y = y + a x ; y = x + b y */
 int pmg_axpy(long long n, double a, const double *x, double *y, void *stream);
 int pmg_xpby(long long n, const double *x, double b, double *y, void *stream);
-/* CG update (krylov.py:143-146) fused: u += alpha p; r -= alpha q
- * (full allocation) and rr_dev[0] = ||r||^2 over owned cells.  alpha is
+/* CG update (krylov.py:143-146) fused: u += alpha p (skipped if u is NULL);
+ * r -= alpha q (full allocation) and rr_dev[0] = ||r||^2 over owned cells.  alpha is
  * read from DEVICE memory as alpha_num[0] / alpha_den[0] so the step
  * needs no host round trip. */
 int pmg_cg_update(const pmg_level *lvl, const double *alpha_num, const double *alpha_den,
                   const double *p, const double *q, double *u, double *r,
                   double *scratch, double *rr_dev, void *stream);
+/* u += (alpha_num/alpha_den) p; p = z + (beta_num/beta_den) p in one pass
+ * (full allocation): the iterate update of CG iteration k deferred into the
+ * direction update of iteration k+1.  z = NULL: only u += alpha p. */
+int pmg_cg_step(long long n, const double *alpha_num, const double *alpha_den,
+                const double *beta_num, const double *beta_den, const double *z, double *p,
+                double *u, void *stream);
 /* p = z + (beta_num[0]/beta_den[0]) p over the full allocation. */
 int pmg_cg_direction(long long n, const double *beta_num, const double *beta_den,
                      const double *z, double *p, void *stream);

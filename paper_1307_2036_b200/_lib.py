@@ -72,6 +72,7 @@ SIGNATURES = {
     "pmg_xpby": (_I, [_LL, _P, _D, _P, _P]),
     "pmg_cg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pmg_cg_direction": (_I, [_LL, _P, _P, _P, _P, _P]),
+    "pmg_cg_step": (_I, [_LL, _P, _P, _P, _P, _P, _P, _P, _P]),
 }
 
 

@@ -41,6 +41,8 @@ cudaError_t launch_cg_direction(long long, const double *, const double *, const
 cudaError_t launch_cg_update(const Lvl &, const double *, const double *, const double *,
                              const double *, double *, double *, double *, int *, cudaStream_t);
 cudaError_t launch_from_ref(const Lvl &, const double *, double *, cudaStream_t);
+cudaError_t launch_cg_up(long long, const double *, const double *, const double *, const double *,
+                         const double *, double *, double *, cudaStream_t);
 cudaError_t launch_to_ref(const Lvl &, const double *, double *, cudaStream_t);
 }  // namespace pmg
 
@@ -460,6 +462,14 @@ int pmg_cg_update(const pmg_level *lv, const double *num, const double *den, con
     PMG_CUDA(launch_cg_update(lv->L, num, den, p, q, u, r, scratch, &np, (cudaStream_t)st),
              "cg_update");
     PMG_CUDA(launch_finalize(scratch, np, rr, (cudaStream_t)st), "cg_update reduce");
+    return PMG_OK;
+}
+
+int pmg_cg_step(long long n, const double *alpha_num, const double *alpha_den,
+                const double *beta_num, const double *beta_den, const double *z, double *p,
+                double *u, void *st) {
+    PMG_CUDA(launch_cg_up(n, alpha_num, alpha_den, beta_num, beta_den, z, p, u, (cudaStream_t)st),
+             "cg_step");
     return PMG_OK;
 }
 

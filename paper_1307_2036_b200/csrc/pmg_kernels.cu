@@ -2389,6 +2389,29 @@ __global__ void k_cg_direction(long long n, const double *__restrict__ num,
         p[e] = b * p[e] + z[e];
 }
 
+// u += (an/ad) p ; p = z + (bn/bd) p over the full allocation: the CG
+// iterate update of iteration k (krylov.py:143) deferred into the direction
+// update of iteration k+1 (krylov.py:157), which reads p_k anyway.
+__global__ void k_cg_up(long long n, const double *__restrict__ an, const double *__restrict__ ad,
+                        const double *__restrict__ bn, const double *__restrict__ bd,
+                        const double *__restrict__ z, double *__restrict__ p,
+                        double *__restrict__ u) {
+    const double a = an[0] / ad[0];
+    if (z == nullptr) {   // final iterate update only
+        for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+             e += (long long)gridDim.x * blockDim.x)
+            u[e] = u[e] + a * p[e];
+        return;
+    }
+    const double b = bn[0] / bd[0];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x) {
+        const double pv = p[e];
+        u[e] = u[e] + a * pv;
+        p[e] = b * pv + z[e];
+    }
+}
+
 // u += alpha p ; r -= alpha q over the full allocation (halo included, as
 // DistField.add_scaled, partition.py:145-148); partial ||r||^2 over owned.
 // Rows of the allocation are (c, jj, k) with jj in [0, ny+2), pitch wide.
@@ -2409,7 +2432,7 @@ k_cg_update(Lvl L, const double *__restrict__ num, const double *__restrict__ de
         const bool owned_row = (j >= 0 && j < L.ny);
         for (int t = threadIdx.x; t < L.pitch; t += blockDim.x) {
             const long long e = base + t;
-            u[e] = u[e] + alpha * p[e];
+            if (u != nullptr) u[e] = u[e] + alpha * p[e];
             const double rv = r[e] + malpha * q[e];
             r[e] = rv;
             const int h = t - OFF;
@@ -3052,6 +3075,13 @@ cudaError_t launch_cg_direction(long long n, const double *num, const double *de
                                 double *p, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     k_cg_direction<<<stream_blocks(n), 256, 0, st>>>(n, num, den, z, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cg_up(long long n, const double *an, const double *ad, const double *bn,
+                         const double *bd, const double *z, double *p, double *u, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_cg_up<<<stream_blocks(n), 256, 0, st>>>(n, an, ad, bn, bd, z, p, u);
     return cudaGetLastError();
 }
 

@@ -136,11 +136,10 @@ class LineSmoother:
         """z = M^{-1} r, symmetric red-black block SSOR from zero
         (smoother.py:224-244): red (zero start, no neighbours), black (zero
         start, x (2 - rho)), red; three exchanges."""
-        if out is None:
-            z = DistField.zeros(self.op.layout, self.op.nz)
-        else:
-            z = out
-            z.fill(0.0)
+        # the reference zero-fills z first (smoother.py:235-238); that fill is
+        # dead work here: the first red half-sweep ignores z (neighbours zero,
+        # zero start), the black one reads only the fresh red values
+        z = DistField.zeros(self.op.layout, self.op.nz) if out is None else out
         self.half_sweep_exchange(z, r, RED, rho, zero_start=True, neighbors_zero=True)
         self.half_sweep_exchange(z, r, BLACK, rho, zero_start=True, post_scale=2.0 - rho)
         self.half_sweep_exchange(z, r, RED, rho)
