@@ -328,8 +328,8 @@ class _FaceBuffers:
     cache = {}
 
     @classmethod
-    def get(cls, geom: LevelHandle, tag: str, face: int) -> torch.Tensor:
-        key = (geom.mx, geom.my, geom.nz, tag, face)
+    def get(cls, geom: LevelHandle, tag: str, face: int, owner: int = -1) -> torch.Tensor:
+        key = (geom.mx, geom.my, geom.nz, tag, face, owner)
         t = cls.cache.get(key)
         if t is None:
             n = int(lib().pmg_face_doubles(geom.h, face))
@@ -440,8 +440,8 @@ def _phase_dist(df: DistField, faces, st, dist) -> None:
     plan = exchange_plan(lay, w, faces)
     sendbufs, recvbufs = {}, {}
     for sf, ps, rf, pr in plan:
-        sendbufs[sf] = _FaceBuffers.get(f.geom, "send", sf)
-        recvbufs[rf] = _FaceBuffers.get(f.geom, "recv", rf)
+        sendbufs[sf] = _FaceBuffers.get(f.geom, "send", sf, w)
+        recvbufs[rf] = _FaceBuffers.get(f.geom, "recv", rf, w)
         if ps is not None:
             call("pmg_pack_face", f.geom.h, f.ptr, sf, _ptr(sendbufs[sf]), st)
     how = exchange_messages(dist, w, plan, sendbufs, recvbufs)

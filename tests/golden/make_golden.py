@@ -197,6 +197,33 @@ def config_solve(name, nx, nz, omega2, lambda2, nlev, solver, variable=False,
         uninject()
 
 
+def native_fixture(name, nx, nz, dt, flat, policy="standard"):
+    """The reference's OWN problem family, unmodified: cubed-sphere panel (or
+    its flat box), zero-flux boundaries, graded levels, derived parameters
+    (tests/test_partition.py:122-136 setup)."""
+    uninject()
+    from panelmg import derive_parameters
+    grid = panel_grid(nx, nz, flat_mode=flat)
+    prm = derive_parameters(nx, nz, dt)
+    fg = np.random.default_rng(3).uniform(-1, 1, (nx, nx, nz))
+    cfg = MGConfig(policy=policy)
+    hier = build_hierarchy(grid, prm, cfg, Decomposition(nx, 1))
+    ud, rep = mg_solve(scatter_owned(fg, hier.fine.layout), hier, cfg)
+    op = hier.fine.op
+    pre = SSORPreconditioner(LineSmoother(op))
+    uc, rc = pcg_solve(scatter_owned(fg, op.layout), op, pre, eps=1e-5, maxiter=500)
+    u = scatter_owned(np.random.default_rng(4).uniform(-1, 1, (nx, nx, nz)), op.layout)
+    halo_exchange(u)
+    out = {"nx": nx, "nz": nz, "dt": dt, "flat": flat, "policy": policy,
+           "omega2": prm.omega2, "lambda2": prm.lambda2,
+           "apply": gather_owned(op.apply(u)),
+           "mg_history": np.array(rep.residual_history), "mg_u": gather_owned(ud),
+           "cg_history": np.array(rc.residual_history), "cg_u": gather_owned(uc),
+           "levels": hier.level_sizes()}
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name, "mg", rep.iterations, "cg", rc.iterations)
+
+
 def main(which):
     if which in ("small", "all"):
         # per-op fixtures: periodic config factors, the reference's own
@@ -219,6 +246,10 @@ def main(which):
                      variable=True, stretch=1.05)
         config_solve("config4_like256_mg", 256, 128, 1e-3, 1.0, 5, "mg",
                      variable=True, stretch=1.05)
+    if which in ("native", "small", "all"):
+        native_fixture("native_panel32", 32, 8, 4800.0, flat=False)
+        native_fixture("native_flat32", 32, 8, 4800.0, flat=True)
+        native_fixture("native_panel64_shallow", 64, 16, 2400.0, flat=False, policy="very_shallow")
     if which in ("big", "all"):
         config_solve("config1_mg", 1024, 128, 1e-3, 1.0, 7, "mg")
         for w in (1e-4, 1e-3, 1e-2, 1e-1):
