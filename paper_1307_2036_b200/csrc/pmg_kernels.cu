@@ -2367,6 +2367,48 @@ k_dot(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// Vectorised owned-cell dot / norm: owned rows (c, j, k) are contiguous
+// [OFF, OFF + nh) segments; a thread covers one double2 of RPB rows at once
+// (all loads in flight before the accumulation), grid-stride over row
+// blocks in a fixed order (deterministic).  SAME: a == b, loaded once.
+template <int RPB, bool SAME>
+__global__ void __launch_bounds__(256)
+k_dot2(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
+       double *__restrict__ partials, int nch) {
+    // items = (owned row (c, j, k), chunk of 2 * blockDim elements)
+    const int nrows = 2 * L.nz * L.ny;
+    const int nitems = nrows * nch;
+    const int span = 2 * blockDim.x;
+    double s = 0.0;
+    for (int i0 = blockIdx.x * RPB; i0 < nitems; i0 += gridDim.x * RPB) {
+        double2 va[RPB], vb[RPB];
+        int lim[RPB];
+#pragma unroll
+        for (int q = 0; q < RPB; ++q) {
+            const int it = min(i0 + q, nitems - 1);
+            const int r = it / nch, ch = it - r * nch;
+            const int k = r % L.nz;
+            const int cj = r / L.nz;
+            const int j = cj % L.ny, c = cj / L.ny;
+            const int s0 = (j + L.par + c) & 1;
+            const int nh = ((L.nx - s0) + 1) / 2;
+            const int e0 = ch * span + 2 * threadIdx.x;
+            lim[q] = (i0 + q < nitems) ? nh - e0 : 0;        // valid elements from e0
+            const int e = min(e0, max(nh - 2, 0));
+            const long long base = at(L, c, k, j, 0);
+            va[q] = *reinterpret_cast<const double2 *>(a + base + e);
+            vb[q] = SAME ? va[q] : *reinterpret_cast<const double2 *>(b + base + e);
+        }
+#pragma unroll
+        for (int q = 0; q < RPB; ++q) {
+            if (lim[q] > 0) s += va[q].x * vb[q].x;
+            if (lim[q] > 1) s += va[q].y * vb[q].y;
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
 __global__ void k_axpy(long long n, double a, const double *__restrict__ x, double *__restrict__ y) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
          e += (long long)gridDim.x * blockDim.x)
@@ -3051,11 +3093,20 @@ static inline int stream_blocks(long long n) {
 cudaError_t launch_dot(const Lvl &L, const double *a, const double *b, double *partials, int *np,
                        cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    const long long n = 2LL * L.nz * L.ny * ((L.nx + 1) >> 1);
-    int g = stream_blocks(n);
-    if (g > 2 * L.nz * L.ny) g = 2 * L.nz * L.ny;
+    constexpr int RPB = 4;
+    const int nh = (L.nx + 1) / 2;
+    int bs = (nh / 2 + 31) / 32 * 32;
+    bs = bs < 32 ? 32 : (bs > 256 ? 256 : bs);
+    const int nch = (nh + 2 * bs - 1) / (2 * bs);
+    const int nitems = 2 * L.nz * L.ny * nch;
+    int g = (nitems + RPB - 1) / RPB;
+    const int cap = 8 * sm_count();
+    if (g > cap) g = cap;
     *np = g;
-    k_dot<<<g, 256, 0, st>>>(L, a, b, partials);
+    if (a == b)
+        k_dot2<RPB, true><<<g, bs, 0, st>>>(L, a, b, partials, nch);
+    else
+        k_dot2<RPB, false><<<g, bs, 0, st>>>(L, a, b, partials, nch);
     return cudaGetLastError();
 }
 

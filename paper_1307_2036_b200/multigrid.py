@@ -227,7 +227,8 @@ def _residual_restrict(lev: Level, coarse: Level, f: DistField, u: DistField,
              f.parts[w].ptr, uf.ptr, cf.parts[w].ptr, st)
 
 
-def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0) -> None:
+def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
+            first: bool = False) -> None:
     """One V-cycle on ``scratch[c].u`` (halo-consistent on entry), Alg. 1.
 
     With ``cfg.fused`` and rho = 1 two pieces of provably dead work are
@@ -241,7 +242,8 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0) -> None:
     s = scratch[c]
     lean = cfg.fused and cfg.rho == 1.0
     if c + 1 < len(hier.levels):
-        _pre_smooth(lev, s, cfg.nu_pre, cfg.rho, lean and c > 0)
+        # ``first``: the finest iterate is zero on entry but was not filled
+        _pre_smooth(lev, s, cfg.nu_pre, cfg.rho, lean and (c > 0 or first))
         coarse = hier.levels[c + 1]
         if cfg.fused:
             _residual_restrict(lev, coarse, s.f, s.u, scratch[c + 1].f)
@@ -287,18 +289,20 @@ def _echo(hier: LevelHierarchy, cfg: MGConfig) -> dict:
 
 
 class _CycleGraph:
-    """CUDA graph of one V-cycle + fine residual norm on persistent scratch."""
+    """CUDA graph of one V-cycle + fine residual norm over ``scratch``
+    (whose level-0 entries may be the caller's f and iterate)."""
 
-    def __init__(self, hier: LevelHierarchy, cfg: MGConfig, scratch):
+    def __init__(self, hier: LevelHierarchy, cfg: MGConfig, scratch, first: bool):
         self.res = torch.zeros(len(scratch[0].u.parts), dtype=torch.float64, device="cuda")
         s0 = scratch[0]
         fine = hier.fine
-        # warm-up outside capture (allocations, kernel attributes); the
-        # iterate is reset by every solve, so running it on scratch is harmless
+        # warm-up outside capture (allocations, kernel attributes); it runs
+        # on the solve's own buffers before the iteration starts, and the
+        # first cycle never reads the iterate's initial contents
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            v_cycle(hier, cfg, scratch)
+            v_cycle(hier, cfg, scratch, first=first)
             fine.op.residual_norm2_dev(s0.f, s0.u, None, self.res)
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
@@ -306,7 +310,7 @@ class _CycleGraph:
         l0 = lib().pmg_launch_count()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            v_cycle(hier, cfg, scratch)
+            v_cycle(hier, cfg, scratch, first=first)
             fine.op.residual_norm2_dev(s0.f, s0.u, None, self.res)
         self.launches = lib().pmg_launch_count() - l0   # library kernels per replay
 
@@ -315,42 +319,61 @@ class _CycleGraph:
         return self.res
 
 
+def _ptrs(df: DistField):
+    return tuple(p.data.data_ptr() for p in df.parts.values())
+
+
 def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField | None = None):
     """Repeat V-cycles from u = 0 until ||r|| / ||r0|| < eps (multigrid.py:297-330).
 
-    Non-convergence within ``maxiter`` is reported, not raised.  With
-    ``cfg.graph`` the iterate lives in hierarchy-owned scratch and the
-    returned field is a copy (or ``out``).
+    Non-convergence within ``maxiter`` is reported, not raised.
+
+    B200 execution: ``f`` is read in place (never copied) and, if ``out`` is
+    given, the iterate lives in ``out`` -- the V-cycle graphs are captured
+    over those buffers and cached per buffer identity, so repeated solves
+    copy nothing.  Without ``out`` a fresh field is returned.  With rho = 1
+    the first cycle starts from zero without a fill (its first red
+    half-sweep ignores u, exactly as f + drw*0 = f).
     """
     use_graph = cfg.graph and _dist() is None
-    scratch = hier.persistent_scratch() if use_graph else hier.make_scratch()
-    s0 = scratch[0]
-    s0.f.copy_from(f)
-    s0.u.fill(0.0)
-    u = s0.u
-    r0 = dist_norm(s0.f, cfg.deterministic)
+    coarse = hier.persistent_scratch() if use_graph else hier.make_scratch()
+    # iterate: the caller's ``out``; else the hierarchy's level-0 scratch
+    # (graph reuse across calls), copied out at the end
+    u = out if out is not None else coarse[0].u
+    scratch = [_Scratch(u, f, coarse[0].r)] + coarse[1:]
+    r0 = dist_norm(f, cfg.deterministic)
     history = [r0]
     echo = _echo(hier, cfg)
     if r0 == 0.0:
-        return (u.copy() if use_graph else u), SolveReport(0, history, True, 0.0, echo)
-    graph = None
+        u.fill(0.0)
+        return (u if out is not None else u.copy()), SolveReport(0, history, True, 0.0, echo)
+    lean_first = (cfg.fused and cfg.rho == 1.0 and cfg.nu_pre >= 1 and len(hier.levels) > 1)
+    graphs = {}
     if use_graph:
-        key = (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused)
-        graph = hier._graphs.get(key)
-        if graph is None:
-            graph = _CycleGraph(hier, cfg, scratch)
-            hier._graphs[key] = graph
-            s0.u.fill(0.0)
-    res = torch.zeros(len(s0.u.parts), dtype=torch.float64, device="cuda")
+        base = (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
+                _ptrs(f), _ptrs(u))
+        for first in ((True, False) if lean_first else (False,)):
+            key = base + (first,)
+            g = hier._graphs.get(key)
+            if g is None:
+                if len(hier._graphs) > 16:          # bound the cache
+                    hier._graphs.clear()
+                g = _CycleGraph(hier, cfg, scratch, first)
+                hier._graphs[key] = g
+            graphs[first] = g
+    if not lean_first:
+        u.fill(0.0)
+    res = torch.zeros(len(u.parts), dtype=torch.float64, device="cuda")
     converged = False
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for _ in range(cfg.maxiter):
-        if graph is not None:
-            rr = graph.replay()
+    for it in range(cfg.maxiter):
+        first = lean_first and it == 0
+        if use_graph:
+            rr = graphs[first].replay()
         else:
-            v_cycle(hier, cfg, scratch)
-            hier.fine.op.residual_norm2_dev(s0.f, u, None, res)
+            v_cycle(hier, cfg, scratch, first=first)
+            hier.fine.op.residual_norm2_dev(f, u, None, res)
             rr = res
         rnorm = math.sqrt(reduce_parts(rr))
         history.append(rnorm)
@@ -358,10 +381,6 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
             converged = True
             break
     wall = time.perf_counter() - t0
-    if use_graph:
-        if out is None:
-            out = u.copy()
-        else:
-            out.copy_from(u)
-        u = out
+    if out is None:
+        u = u.copy()
     return u, SolveReport(len(history) - 1, history, converged, wall, echo)
