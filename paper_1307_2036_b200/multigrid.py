@@ -27,7 +27,7 @@ from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
 from .partition import (Decomposition, DistField, LevelLayout, _dist, _stream, dist_norm,
-                        halo_exchange, reduce_parts, self_halo_flags)
+                        halo_exchange, reduce_parts, scalar_buffer, self_halo_flags)
 from .smoother import BLACK, RED, LineSmoother
 from .stencil import PanelOperator
 
@@ -293,7 +293,7 @@ class _CycleGraph:
     (whose level-0 entries may be the caller's f and iterate)."""
 
     def __init__(self, hier: LevelHierarchy, cfg: MGConfig, scratch, first: bool):
-        self.res = torch.zeros(len(scratch[0].u.parts), dtype=torch.float64, device="cuda")
+        self.res = scalar_buffer(len(scratch[0].u.parts))
         s0 = scratch[0]
         fine = hier.fine
         # warm-up outside capture (allocations, kernel attributes); it runs
@@ -363,9 +363,9 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
             graphs[first] = g
     if not lean_first:
         u.fill(0.0)
-    res = torch.zeros(len(u.parts), dtype=torch.float64, device="cuda")
+    res = scalar_buffer(len(u.parts))
     converged = False
-    torch.cuda.synchronize()
+    torch.cuda.current_stream().synchronize()
     t0 = time.perf_counter()
     for it in range(cfg.maxiter):
         first = lean_first and it == 0

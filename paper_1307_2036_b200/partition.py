@@ -522,8 +522,22 @@ class _Scratch:
         return cls.t, cls.res
 
 
+def scalar_buffer(n: int) -> torch.Tensor:
+    """Per-part reduction results.  Single process: pinned, device-mapped
+    host memory (UVA) -- the finalize kernel stores the scalar straight into
+    host memory, so reading it needs a stream sync but no copy-engine
+    transfer (a tiny D2H copy would queue behind bulk downloads of a
+    pipelined solve).  Distributed: device memory for the NCCL all-reduce."""
+    if _dist() is None:
+        return torch.zeros(n, dtype=torch.float64, pin_memory=True)
+    return torch.zeros(n, dtype=torch.float64, device="cuda")
+
+
 def reduce_parts(vals: torch.Tensor) -> float:
-    """Sum per-part device scalars in part order, then over ranks."""
+    """Sum per-part scalars in part order, then over ranks."""
+    if not vals.is_cuda and _dist() is None:   # host-mapped results
+        torch.cuda.current_stream().synchronize()
+        return float(sum(vals.tolist()))
     tot = vals.sum() if vals.numel() > 1 else vals[0]
     d = _dist()
     if d is not None:
@@ -541,7 +555,7 @@ def dist_dot(a: DistField, b: DistField, deterministic: bool = False) -> float:
     scratch, res = _Scratch.get()
     st = _stream()
     ws = list(a.parts.keys())
-    out = torch.empty(len(ws), dtype=torch.float64, device="cuda")
+    out = scalar_buffer(len(ws))
     for n, w in enumerate(ws):
         fa, fb = a.parts[w], b.parts[w]
         call("pmg_dot", fa.geom.h, fa.ptr, fb.ptr, _ptr(scratch),

@@ -118,7 +118,8 @@ class PanelOperator:
                  C.c_void_p(res.data_ptr() + 8 * n), st)
 
     def residual_norm(self, f: DistField, u: DistField, out: DistField | None = None) -> float:
-        res = torch.empty(len(u.parts), dtype=torch.float64, device="cuda")
+        from .partition import scalar_buffer
+        res = scalar_buffer(len(u.parts))
         self.residual_norm2_dev(f, u, out, res)
         return float(np.sqrt(reduce_parts(res)))
 
