@@ -142,6 +142,19 @@ int pmg_prolong_colors_halo(const pmg_level *fine, const pmg_level *coarse,
                             const double *coarse_u, double *fine_u, int add, int color_mask,
                             int halo_flags, void *stream);
 
+/* Coarse-grid correction fused into the first post-smoothing half-sweep
+ * (multigrid.py:283-292 then smoother.py:184-191 with rho = 1): relaxes
+ * colour `color` of fine_u as if fine_u had first received u += P coarse_u
+ * and a halo exchange.  The other colour is NOT updated in memory -- valid
+ * only because the next half-sweep overwrites it without reading it (the
+ * V-cycle's post-smoothing with rho = 1).  coarse_u's halo must be current.
+ * halo_flags as pmg_half_sweep_halo.  Fast smoother, uniform levels only:
+ * pmg_half_sweep_prolong_ok tells (else PMG_ERR_VALUE). */
+int pmg_half_sweep_prolong_ok(const pmg_level *fine);
+int pmg_half_sweep_prolong(const pmg_level *fine, const pmg_level *coarse, double *fine_u,
+                           const double *fine_f, const double *coarse_u, int color,
+                           int halo_flags, void *stream);
+
 /* ---- halos (partition.py:158-191) ----------------------------------- */
 /* Fill the whole halo ring of a part that is its own neighbour (one worker
  * per direction): periodic_x/y wrap, otherwise mirror the adjacent owned

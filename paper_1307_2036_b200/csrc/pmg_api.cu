@@ -27,6 +27,9 @@ cudaError_t launch_half_sweep(const Lvl &, double *, const double *, int, double
 cudaError_t launch_invd(const Lvl &, double *, cudaStream_t);
 cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, double,
                             cudaStream_t);
+bool half_sweep_pro_ok(const Lvl &F);
+cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const double *f,
+                                  const double *cu, int color, cudaStream_t st);
 cudaError_t launch_prolong(const Lvl &, const Lvl &, const double *, double *, int, int,
                            cudaStream_t);
 cudaError_t launch_halo_self(const Lvl &, double *, int, int, cudaStream_t);
@@ -372,6 +375,25 @@ int pmg_half_sweep_halo(const pmg_level *lv, double *u, const double *f, int col
     PMG_CUDA(launch_half_sweep(L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
                                (cudaStream_t)st),
              "half_sweep_halo");
+    return PMG_OK;
+}
+
+int pmg_half_sweep_prolong_ok(const pmg_level *fine) {
+    return (fine && half_sweep_pro_ok(fine->L)) ? 1 : 0;
+}
+
+int pmg_half_sweep_prolong(const pmg_level *fine, const pmg_level *coarse, double *u,
+                           const double *f, const double *cu, int color, int halo_flags,
+                           void *st) {
+    int rc = check_pair(fine, coarse);
+    if (rc) return rc;
+    if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
+    if (!half_sweep_pro_ok(fine->L))
+        return fail(PMG_ERR_VALUE, "fused prolongation needs the fast smoother on a uniform level");
+    Lvl F = fine->L;
+    F.hflags = halo_flags & 7;
+    PMG_CUDA(launch_half_sweep_pro(F, coarse->L, u, f, cu, color, (cudaStream_t)st),
+             "half_sweep_prolong");
     return PMG_OK;
 }
 

@@ -1558,41 +1558,123 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // (agrees with the sequential solve to ~1e-15 relative; the exact mode is
 // k_half_sweep_tma / k_half_sweep).
 // ---------------------------------------------------------------------------
-template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false>
+// Column solve of one tile of the k-segmented smoother, given r[e] =
+// iota_k * rhs_k for this warp's levels: local forward, segment scan,
+// local backward, segment scan, fix-up, relaxation and store (+ halo
+// copies).  Shared by k_half_sweep_seg and k_half_sweep_pro.
+template <int SEG, bool HALO>
+__device__ __forceinline__ void seg_solve_store(
+    const Lvl &L, double *__restrict__ u, double (&r)[SEG], const double2 *ti,
+    const double2 *tb, const double *tq, double *hend, double *ybeg, int c, int j, int h0,
+    int s0, int i, int nact, int kn, long long pc, long long pl, int zero_start, double rho,
+    double scale, double omr) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int nz = L.nz;
+    const int k0 = w * SEG;
+        // ---- local forward: h_k = iota_k r_k + alpha_k h_{k-1} ----
+    double hp = 0.0;
+#pragma unroll
+    for (int e = 0; e < SEG; ++e) {
+        if (e < kn) {
+            hp = __fma_rn(ti[k0 + e].y, hp, r[e]);
+            r[e] = hp;
+        }
+    }
+    if (kn > 0) hend[w * 32 + lane] = hp;
+    __syncthreads();
+    // incoming G = g_{k0-1}: scan over the segments below
+    double G = 0.0;
+    for (int sgm = 0; sgm < w; ++sgm)
+        G = __fma_rn(tb[min(nz, (sgm + 1) * SEG) - 1].x, G, hend[sgm * 32 + lane]);
+    // ---- fix-up + local backward: y_k = g_k + mu_k y_{k+1} ----
+    double yp = 0.0;
+#pragma unroll
+    for (int e = SEG - 1; e >= 0; --e) {
+        if (e < kn) {
+            const double2 pm = tb[k0 + e];
+            const double g = __fma_rn(pm.x, G, r[e]);
+            yp = __fma_rn(pm.y, yp, g);
+            r[e] = yp;
+        }
+    }
+    if (kn > 0) ybeg[w * 32 + lane] = yp;
+    __syncthreads();
+    double X = 0.0;
+    for (int sgm = nw - 1; sgm > w; --sgm) {
+        const int a = sgm * SEG;
+        if (a < nz) X = __fma_rn(tq[a], X, ybeg[sgm * 32 + lane]);
+    }
+    // ---- fix-up, relaxation, store ----
+    if (lane < nact) {
+#pragma unroll
+        for (int e = 0; e < SEG; ++e) {
+            if (e < kn) {
+                const int k = k0 + e;
+                double y = __fma_rn(tq[k], X, r[e]);
+                const long long q = pc + (long long)e * pl;
+                if (zero_start) {
+                    if (scale != 1.0) y = y * scale;
+                } else if (rho != 1.0) {
+                    y = y * rho;
+                    y = y + omr * u[q];
+                }
+                u[q] = y;
+                if (HALO) r[e] = y;
+            }
+        }
+    }
+    // fused self-halo: only tiles touching the part boundary (warp-uniform)
+    if (HALO && (j == 0 || j == L.ny - 1 || h0 == 0 || h0 + 32 >= ((L.nx - s0) + 1) / 2)) {
+        if (lane < nact) {
+#pragma unroll
+            for (int e = 0; e < SEG; ++e)
+                if (e < kn) halo_copies(L, u, i, j, k0 + e, r[e]);
+        }
+    }
+}
+
+template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false,
+          int PLC = 0>
 __global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                  int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles) {
     // NBZ = 0/1: neighbours-zero mode fixed at compile time; FULL: every warp
-    // owns exactly SEG levels (nz % SEG == 0) -- no per-level predicates
+    // owns exactly SEG levels (nz % SEG == 0) -- no per-level predicates;
+    // PLC: the k-plane stride as a compile-time constant (0: runtime), so
+    // every level's load is base + immediate -- no address arithmetic
     const int nbr_zero = (NBZ >= 0) ? NBZ : nbr_zero_rt;
     extern __shared__ double ssm[];
     const int nz = L.nz;
-    double *tdrw = ssm;                 // [nz]
-    double *tiot = tdrw + nz;           // [nz]
-    double *tal = tiot + nz;            // [nz]
-    double *tmu = tal + nz;             // [nz]
-    double *tpf = tmu + nz;             // [nz]
-    double *tq = tpf + nz;              // [nz]
-    double *hend = tq + nz;             // [16][32]
-    double *ybeg = hend + 16 * 32;      // [16][32]
+    // tables, paired for 16-byte shared loads:
+    //   tw[k] = (iota drw wx0, iota drw wy0), ti[k] = (iota, alpha),
+    //   tb[k] = (pf, mu), tq[k] = q
+    double2 *tw = reinterpret_cast<double2 *>(ssm);   // [nz]
+    double2 *ti = tw + nz;                              // [nz]
+    double2 *tb = ti + nz;                              // [nz]
+    double *tq = reinterpret_cast<double *>(tb + nz);   // [nz]
+    // segment-end values, double-buffered by tile parity so a warp can
+    // start the next tile while others still read the previous scan
+    double *hend0 = tq + nz;            // [2][16][32]
+    double *ybeg0 = hend0 + 2 * 16 * 32;  // [2][16][32]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int t = threadIdx.x; t < nz; t += blockDim.x) {
-        tdrw[t] = L.drw[t];
-        tiot[t] = L.invd1[t];
-        tal[t] = L.segtab[t];
-        tmu[t] = L.segtab[nz + t];
-        tpf[t] = L.segtab[2 * nz + t];
+        const double io = L.invd1[t], dd = io * L.drw[t];
+        tw[t] = make_double2(dd * L.wx0, dd * L.wy0);
+        ti[t] = make_double2(io, L.segtab[t]);
+        tb[t] = make_double2(L.segtab[2 * nz + t], L.segtab[nz + t]);
         tq[t] = L.segtab[3 * nz + t];
     }
     __syncthreads();
     const int o = c ^ 1;
-    const long long pl = L.plane;
+    const long long pl = PLC ? (long long)PLC : L.plane;
     const int k0 = w * SEG;
     const int kn = FULL ? SEG : min(SEG, nz - k0);   // levels of this warp (may be <= 0)
-    const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int par = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
+        double *hend = hend0 + par * 16 * 32;
+        double *ybeg = ybeg0 + par * 16 * 32;
         const int j = t / htiles;
         const int h0 = (t - j * htiles) * 32;
         const int s0 = (j + L.par + c) & 1;
@@ -1632,83 +1714,153 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                 double ve = __shfl_down_sync(0xffffffffu, nbr_zero ? 0.0 : vw[e], 1);
                 if (lastlane) ve = vx[e];
                 if (kk < kn) {
-                    double g;
-                    if (nbr_zero) {
-                        g = vf[e];
-                    } else {
-                        g = wxm * vw[e];
-                        g = g + wxp * ve;
-                        g = g + wym * vs[e];
-                        g = g + wyp * vn[e];
-                        g = g * tdrw[k0 + kk];
-                        g = g + vf[e];
+                    // iota_k * rhs_k (the forward step's first term)
+                    const double2 ia = ti[k0 + kk];
+                    double g = ia.x * vf[e];
+                    if (!nbr_zero) {
+                        const double2 cw = tw[k0 + kk];
+                        g = __fma_rn(cw.y, vs[e] + vn[e], g);
+                        g = __fma_rn(cw.x, vw[e] + ve, g);
                     }
                     r[b8 + e] = g;
                 }
             }
         }
-        // ---- local forward: h_k = iota_k r_k + alpha_k h_{k-1} ----
-        double hp = 0.0;
+        seg_solve_store<SEG, HALO>(L, u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0, i, nact, kn, pc,
+                                   pl, zero_start, rho, scale, omr);
+    }
+}
+
+// Post-smoothing first half-sweep with the coarse-grid correction fused in
+// (fast mode, uniform, rho = 1).  The reference adds P e to the whole fine
+// iterate, exchanges halos and then relaxes colour c (multigrid.py:283-292,
+// smoother.py:184-191).  With rho = 1 the colour-c values are overwritten
+// unread and the other colour is read only here (before the next
+// half-sweep overwrites it), so the correction is applied on the fly to
+// the four neighbours the line RHS reads: v + (P e)(x, y), with P the 9-3-3-1
+// bilinear interpolation written as two 3-1 passes,
+//   P e = (3 g(Y) + g(Y + dY)) / 16,  g(Y) = 3 e(X, Y) + e(X + dX, Y)
+// (X = x >> 1, dX = x odd ? +1 : -1, likewise Y).  Neighbours in the fine
+// halo ring take the interpolation at their virtual position, which reads
+// coarse cells -1 .. nxc only and equals the correction of the cell the
+// halo copies (periodic wrap, mirror, or the neighbour part's own cell),
+// so no exchange is needed between prolongation and relaxation.  Each lane
+// loads e(h-1 .. h+1, J-1 .. J+1) per level (L1/L2-resident rows).
+template <int SEG, int PLC, int CPLC, bool HALO, int PB = 2>
+__global__ void __launch_bounds__(256, 2)
+k_half_sweep_pro(Lvl L, Lvl C, double *__restrict__ u, const double *__restrict__ f,
+                 const double *__restrict__ cu, int c, int ntiles, int htiles) {
+    extern __shared__ double ssm[];
+    const int nz = L.nz;
+    double2 *tw = reinterpret_cast<double2 *>(ssm);
+    double2 *ti = tw + nz;
+    double2 *tb = ti + nz;
+    double *tq = reinterpret_cast<double *>(tb + nz);
+    double *hend0 = tq + nz;
+    double *ybeg0 = hend0 + 2 * 16 * 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
+        const double io = L.invd1[t], dd = io * L.drw[t];
+        tw[t] = make_double2(dd * L.wx0, dd * L.wy0);
+        ti[t] = make_double2(io, L.segtab[t]);
+        tb[t] = make_double2(L.segtab[2 * nz + t], L.segtab[nz + t]);
+        tq[t] = L.segtab[3 * nz + t];
+    }
+    __syncthreads();
+    const int o = c ^ 1;
+    const long long pl = PLC ? (long long)PLC : L.plane;
+    const long long cpl = CPLC ? (long long)CPLC : C.plane;
+    const int k0 = w * SEG;
+    int par = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
+        double *hend = hend0 + par * 16 * 32;
+        double *ybeg = ybeg0 + par * 16 * 32;
+        const int j = t / htiles;
+        const int h0 = (t - j * htiles) * 32;
+        const int s0 = (j + L.par + c) & 1;
+        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+        const int ln = min(lane, nact - 1);
+        const bool lastlane = (ln == nact - 1);
+        const int h = h0 + ln;
+        const int i = 2 * h + s0;
+        const long long pc = at(L, c, k0, j, h);
+        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
+        const long long pS = at(L, o, k0, j - 1, h);
+        const long long pN = at(L, o, k0, j + 1, h);
+        // coarse e(h-1 .. h+1, J-1 .. J+1): per row, e(h-1) and e(h+1) are
+        // adjacent elements of one colour array, e(h) is in the other
+        const int J = j >> 1;
+        const long long qa0 = cell(C, h - 1, J - 1, k0), qb0 = cell(C, h, J - 1, k0);
+        const long long qa1 = cell(C, h - 1, J, k0), qb1 = cell(C, h, J, k0);
+        const long long qa2 = cell(C, h - 1, J + 1, k0), qb2 = cell(C, h, J + 1, k0);
+        const bool jo = j & 1;
+        double r[SEG];
+        // ---- pass 1 (coarse rows, L1/L2-resident): the correction's share
+        // of the line RHS, wy (PeS + PeN) + wx (PeW + PeE), times iota ----
 #pragma unroll
-        for (int e = 0; e < SEG; ++e) {
-            if (e < kn) {
-                const int k = k0 + e;
-                hp = __fma_rn(tal[k], hp, tiot[k] * r[e]);
-                r[e] = hp;
+        for (int b = 0; b < SEG; b += PB) {
+            double em[PB][3], e0[PB][3], ep[PB][3];
+#pragma unroll
+            for (int e = 0; e < PB; ++e) {
+                const long long co = (long long)(b + e) * cpl;
+                em[e][0] = cu[qa0 + co]; ep[e][0] = cu[qa0 + co + 1]; e0[e][0] = cu[qb0 + co];
+                em[e][1] = cu[qa1 + co]; ep[e][1] = cu[qa1 + co + 1]; e0[e][1] = cu[qb1 + co];
+                em[e][2] = cu[qa2 + co]; ep[e][2] = cu[qa2 + co + 1]; e0[e][2] = cu[qb2 + co];
             }
-        }
-        if (kn > 0) hend[w * 32 + lane] = hp;
-        __syncthreads();
-        // incoming G = g_{k0-1}: scan over the segments below
-        double G = 0.0;
-        for (int sgm = 0; sgm < w; ++sgm)
-            G = __fma_rn(tpf[min(nz, (sgm + 1) * SEG) - 1], G, hend[sgm * 32 + lane]);
-        // ---- fix-up + local backward: y_k = g_k + mu_k y_{k+1} ----
-        double yp = 0.0;
 #pragma unroll
-        for (int e = SEG - 1; e >= 0; --e) {
-            if (e < kn) {
-                const int k = k0 + e;
-                const double g = __fma_rn(tpf[k], G, r[e]);
-                yp = __fma_rn(tmu[k], yp, g);
-                r[e] = yp;
-            }
-        }
-        if (kn > 0) ybeg[w * 32 + lane] = yp;
-        __syncthreads();
-        double X = 0.0;
-        for (int sgm = nw - 1; sgm > w; --sgm) {
-            const int a = sgm * SEG;
-            if (a < nz) X = __fma_rn(tq[a], X, ybeg[sgm * 32 + lane]);
-        }
-        // ---- fix-up, relaxation, store ----
-        if (lane < nact) {
+            for (int e = 0; e < PB; ++e) {
+                // x passes: g at x = i (S/N columns), i-1 (W), i+1 (E)
+                double gi[3], gw[3], ge[3];
 #pragma unroll
-            for (int e = 0; e < SEG; ++e) {
-                if (e < kn) {
-                    const int k = k0 + e;
-                    double y = __fma_rn(tq[k], X, r[e]);
-                    const long long q = pc + (long long)e * pl;
-                    if (zero_start) {
-                        if (scale != 1.0) y = y * scale;
-                    } else if (rho != 1.0) {
-                        y = y * rho;
-                        y = y + omr * u[q];
-                    }
-                    u[q] = y;
-                    if (HALO) r[e] = y;
+                for (int d = 0; d < 3; ++d) {
+                    const double c3 = 3.0 * e0[e][d];
+                    gi[d] = s0 ? c3 + ep[e][d] : c3 + em[e][d];
+                    gw[d] = s0 ? c3 + em[e][d] : __fma_rn(3.0, em[e][d], e0[e][d]);
+                    ge[d] = s0 ? __fma_rn(3.0, ep[e][d], e0[e][d]) : c3 + ep[e][d];
                 }
+                // y passes (rows J-1, J, J+1 = d 0, 1, 2)
+                const double gw2 = jo ? gw[2] : gw[0];       // W/E partner row
+                const double ge2 = jo ? ge[2] : ge[0];
+                const double pw = __fma_rn(3.0, gw[1], gw2) * 0.0625;
+                const double pe = __fma_rn(3.0, ge[1], ge2) * 0.0625;
+                const double ps = (jo ? __fma_rn(3.0, gi[1], gi[0])
+                                      : __fma_rn(3.0, gi[0], gi[1])) * 0.0625;
+                const double pn = (jo ? __fma_rn(3.0, gi[2], gi[1])
+                                      : __fma_rn(3.0, gi[1], gi[2])) * 0.0625;
+                double pev = __shfl_down_sync(0xffffffffu, pw, 1);
+                if (lastlane) pev = pe;
+                const double2 cw = tw[k0 + b + e];
+                r[b + e] = __fma_rn(cw.y, ps + pn, cw.x * (pw + pev));
             }
         }
-        // fused self-halo: only tiles touching the part boundary (warp-uniform)
-        if (HALO && (j == 0 || j == L.ny - 1 || h0 == 0 || h0 + 32 >= ((L.nx - s0) + 1) / 2)) {
-            if (lane < nact) {
+        // ---- pass 2: the line RHS from the fine fields, as k_half_sweep_seg ----
 #pragma unroll
-                for (int e = 0; e < SEG; ++e)
-                    if (e < kn) halo_copies(L, u, i, j, k0 + e, r[e]);
+        for (int b = 0; b < SEG; b += 4) {
+            double vf[4], vw[4], vs[4], vn[4], vx[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const long long ko = (long long)(b + e) * pl;
+                vf[e] = f[pc + ko];
+                vw[e] = u[pW + ko];
+                vs[e] = u[pS + ko];
+                vn[e] = u[pN + ko];
+                vx[e] = lastlane ? u[pE + ko] : 0.0;
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                double ve = __shfl_down_sync(0xffffffffu, vw[e], 1);
+                if (lastlane) ve = vx[e];
+                const double2 ia = ti[k0 + b + e];
+                const double2 cw = tw[k0 + b + e];
+                double g = __fma_rn(ia.x, vf[e], r[b + e]);
+                g = __fma_rn(cw.y, vs[e] + vn[e], g);
+                g = __fma_rn(cw.x, vw[e] + ve, g);
+                r[b + e] = g;
             }
         }
-        __syncthreads();   // hend / ybeg reuse by the next tile
+        seg_solve_store<SEG, HALO>(L, u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0, i, nact, SEG,
+                                   pc, pl, 0, 1.0, 1.0, 0.0);
     }
 }
 
@@ -2805,6 +2957,52 @@ cudaError_t launch_half_sweep(const Lvl &L0, double *u, const double *f, int col
     return e;
 }
 
+// fused coarse-grid correction + half-sweep (k_half_sweep_pro): available
+// in fast mode on uniform levels whose segments tile nz
+bool half_sweep_pro_ok(const Lvl &F) {
+    return !g_smoother_exact && F.uniform && (F.seg == 4 || F.seg == 8 || F.seg == 16) &&
+           F.nz % F.seg == 0 && F.nz / F.seg <= 8;
+}
+
+cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const double *f,
+                                  const double *cu, int color, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int hx = ((F.nx + 1) / 2 + 31) / 32;
+    const int ntiles = hx * F.ny;
+    const int nw = F.nz / F.seg;
+    const size_t sm = sizeof(double) * (7 * (size_t)F.nz + 4 * 16 * 32);
+    auto run = [&](auto kern) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        const int grid = ntiles < cap ? ntiles : cap;
+        kern<<<grid, 32 * nw, sm, st>>>(F, C, u, f, cu, color, ntiles, hx);
+    };
+    static int pb = -1;
+    if (pb < 0) {
+        const char *e = getenv("PMG_PRO_PB");
+        pb = e ? atoi(e) : 2;
+    }
+    if (F.seg == 16 && pb == 4 && F.plane == 520 && C.plane == 264) {
+        run(k_half_sweep_pro<16, 520, 264, false, 4>);
+    } else if (F.seg == 16 && pb == 1 && F.plane == 520 && C.plane == 264) {
+        run(k_half_sweep_pro<16, 520, 264, false, 1>);
+    } else if (F.seg == 16) {
+        if (F.plane == 520 && C.plane == 264) run(k_half_sweep_pro<16, 520, 264, false>);
+        else if (F.plane == 264 && C.plane == 136) run(k_half_sweep_pro<16, 264, 136, false>);
+        else if (F.plane == 136 && C.plane == 72) run(k_half_sweep_pro<16, 136, 72, false>);
+        else run(k_half_sweep_pro<16, 0, 0, false>);
+    } else if (F.seg == 8) {
+        run(k_half_sweep_pro<8, 0, 0, false>);
+    } else {
+        run(k_half_sweep_pro<4, 0, 0, false>);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess && (F.hflags & 1))
+        e = launch_halo_self(F, u, (F.hflags >> 1) & 1, (F.hflags >> 2) & 1, st);
+    return e;
+}
+
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
                                        double post_scale, cudaStream_t st, bool *fused) {
@@ -2840,7 +3038,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
     }
     if (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) {
         const int nw = (L.nz + L.seg - 1) / L.seg;
-        const size_t sm = sizeof(double) * (6 * (size_t)L.nz + 2 * 16 * 32);
+        const size_t sm = sizeof(double) * (7 * (size_t)L.nz + 4 * 16 * 32);
         const size_t sm1 = sizeof(double) * (7 * (size_t)L.nz + 2 * 2 * 8 * 32);
         const int ntiles = hx * L.ny;
         static int var = -1;
@@ -2882,6 +3080,14 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             // default: compile-time neighbour mode, predicate-free when the
             // segments tile nz exactly (all BASELINE configs)
             const bool full = (L.nz % L.seg) == 0;
+            // compile-time plane stride for the large levels of nz = 128
+            // (pitch of nx = 1024, 512, 256)
+            const int plc = (L.seg == 16 && full && !(L.hflags & 1)) ? (int)L.plane : 0;
+#define PMG_SEGP(S, P)                                                                \
+    do {                                                                              \
+        if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true, false, P>);             \
+        else run(k_half_sweep_seg<S, 4, 2, 0, true, false, P>);                      \
+    } while (0)
 #define PMG_SEGF(S)                                                                   \
     do {                                                                              \
         if (full && (L.hflags & 1)) {                                                 \
@@ -2896,13 +3102,17 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             run(k_half_sweep_seg<S, 4, 2>);                                           \
         }                                                                             \
     } while (0)
-            switch (L.seg) {
+            if (plc == 520 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 520);
+            else if (plc == 264 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 264);
+            else if (plc == 136 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 136);
+            else switch (L.seg) {
             case 4: PMG_SEGF(4); break;
             case 8: PMG_SEGF(8); break;
             case 16: PMG_SEGF(16); break;
             default: run(k_half_sweep_seg<32, 4, 1>); break;
             }
 #undef PMG_SEGF
+#undef PMG_SEGP
             *fused = true;
             return cudaGetLastError();
         }

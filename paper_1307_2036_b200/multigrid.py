@@ -22,7 +22,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import call
+from ._lib import call, load
 from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
@@ -219,6 +219,34 @@ def _prolong_add(cu: DistField, coarse: Level, fine: Level, u: DistField,
             halo_exchange(u)
 
 
+#: fuse the coarse-grid correction into the first post-smoothing half-sweep
+#: (k_half_sweep_pro: fast smoother, uniform levels, rho = 1).  Off by
+#: default: it saves the 10 N-byte prolongation pass but the fused kernel
+#: is latency-bound on its extra coarse loads and measured slower on B200
+#: (configs[1] fine level: 835-970 us vs 640 us for black-only
+#: prolongation + half-sweep)
+FUSE_PROLONG = False
+
+
+def _pro_ok(lev: Level) -> bool:
+    return all(load().pmg_half_sweep_prolong_ok(h.h) == 1 for h in lev.op.handles.values())
+
+
+def _sweep_prolong(lev: Level, coarse: Level, cu: DistField, s) -> None:
+    """Red half-sweep of ``s.u`` as if ``s.u += P cu`` and a halo exchange
+    had come first (pmg_half_sweep_prolong), then the red halo exchange."""
+    u = s.u
+    hf = self_halo_flags(u.layout)
+    st = _stream()
+    for w, uf in u.parts.items():
+        call("pmg_half_sweep_prolong", lev.op.handles[w].h, coarse.op.handles[w].h, uf.ptr,
+             s.f.parts[w].ptr, cu.parts[w].ptr, RED, hf, st)
+    if hf:
+        u.layout.halo_count += 1
+    else:
+        halo_exchange(u)
+
+
 def _residual_restrict(lev: Level, coarse: Level, f: DistField, u: DistField,
                        cf: DistField) -> None:
     st = _stream()
@@ -253,14 +281,21 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
         if not (lean and (cfg.nu_pre >= 1 or c + 2 == len(hier.levels))):
             scratch[c + 1].u.fill(0.0)
         v_cycle(hier, cfg, scratch, c + 1)
-        if cfg.fused:
-            _prolong_add(scratch[c + 1].u, coarse, lev, s.u, black_only=lean and cfg.nu_post >= 1,
+        post = cfg.nu_post
+        if cfg.fused and lean and post >= 1 and FUSE_PROLONG and _pro_ok(lev):
+            # correction fused into the first red half-sweep (the black
+            # values it corrects are read only there, then overwritten)
+            _sweep_prolong(lev, coarse, scratch[c + 1].u, s)
+            lev.smoother.half_sweep_exchange(s.u, s.f, BLACK, cfg.rho)
+            post -= 1
+        elif cfg.fused:
+            _prolong_add(scratch[c + 1].u, coarse, lev, s.u, black_only=lean and post >= 1,
                          exchange=True)
         else:
             corr = prolong(scratch[c + 1].u, coarse, lev, out=s.r)
             _add_owned(s.u, corr)
             halo_exchange(s.u)
-        lev.smoother.sweep(s.u, s.f, cfg.nu_post, cfg.rho)
+        lev.smoother.sweep(s.u, s.f, post, cfg.rho)
     else:
         _pre_smooth(lev, s, cfg.resolved_coarse_sweeps(), cfg.rho, lean and c > 0)
 

@@ -15,6 +15,24 @@ from paper_1307_2036_b200 import configs, multigrid as mg  # noqa: E402
 def timeit(fn, reps=20):
     fn()
     torch.cuda.synchronize()
+    if os.environ.get("KB_GRAPH"):
+        # replay a captured sequence: no host launch overhead in the timing
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for _ in range(reps):
+                    fn()
+        torch.cuda.current_stream().wait_stream(s)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
@@ -27,15 +45,17 @@ def timeit(fn, reps=20):
 ap = argparse.ArgumentParser()
 ap.add_argument("--nx", type=int, default=1024)
 ap.add_argument("--nz", type=int, default=128)
+ap.add_argument("--ny", type=int, default=0)
 ap.add_argument("--levels", type=int, default=7)
 ap.add_argument("--variable", action="store_true")
 a = ap.parse_args()
-prob = configs.Problem(a.nx, a.nx, a.nz, 1e-3, 1.0, a.levels, stretch=1.05 if a.variable else None,
+a.ny = a.ny or a.nx
+prob = configs.Problem(a.nx, a.ny, a.nz, 1e-3, 1.0, a.levels, stretch=1.05 if a.variable else None,
                        variable_omega=a.variable)
 cfg = prob.mg_config()
 hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
 sc = hier.persistent_scratch()
-f = pmg.scatter_owned(configs.rhs(a.nx, a.nx, a.nz, 0), hier.fine.layout)
+f = pmg.scatter_owned(configs.rhs(a.nx, a.ny, a.nz, 0), hier.fine.layout)
 sc[0].f.copy_from(f)
 out = {"variant": os.environ.get("PMG_HS_VARIANT", "reg")}
 res = torch.zeros(1, dtype=torch.float64, device="cuda")
@@ -58,6 +78,11 @@ for c, lev in enumerate(hier.levels):
         row["resid_restrict"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
         t = timeit(lambda: mg._prolong_add(sc[c + 1].u, co, lev, s.u))
         row["prolong_add"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
+        t = timeit(lambda: mg._prolong_add(sc[c + 1].u, co, lev, s.u, black_only=True))
+        row["prolong_black"] = (round(t * 1e3, 1), round(10 * n / t / 1e6))
+        if mg._pro_ok(lev):
+            t = timeit(lambda: mg._sweep_prolong(lev, co, sc[c + 1].u, s))
+            row["sweep_prolong"] = (round(t * 1e3, 1), round(14 * n / t / 1e6))
     t = timeit(lambda: pmg.halo_exchange(s.u))
     row["halo"] = round(t * 1e3, 1)
     print(f"L{c} nx={lev.layout.nx}: " + json.dumps(row), flush=True)
