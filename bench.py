@@ -274,17 +274,25 @@ def main():
     t = max_over_ranks(t_local, world)
     launches_lib = lib.pmg_launch_count() - l0
     # kernels replayed from the captured V-cycle graphs (first cycle + the rest)
-    from paper_1307_2036_b200.multigrid import _ptrs
-    gkey = (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
-            _ptrs(f), _ptrs(u))
-    g_first = hier._graphs.get(gkey + (True,))
-    g_rest = hier._graphs.get(gkey + (False,))
+    from paper_1307_2036_b200 import multigrid as mgm
     gpu_launches = launches_lib
-    for n_it in iters:
-        if g_first is not None:
-            gpu_launches += g_first.launches + (n_it - 1) * g_rest.launches
-        elif g_rest is not None:
-            gpu_launches += n_it * g_rest.launches
+    if lay.px == 1 and lay.py == 1 and mgm.USE_NATIVE:
+        # single part: the C++ driver's graphs (pmg_mg_solve)
+        nh = hier.native(cfg)
+        fp, up = f.parts[w].ptr, u.parts[w].ptr
+        l_first, l_rest = nh.graph_launches(fp, up, True), nh.graph_launches(fp, up, False)
+        for n_it in iters:
+            gpu_launches += (l_first + (n_it - 1) * l_rest) if l_first >= 0 else n_it * l_rest
+    else:
+        gkey = (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
+                mgm._ptrs(f), mgm._ptrs(u))
+        g_first = hier._graphs.get(gkey + (True,))
+        g_rest = hier._graphs.get(gkey + (False,))
+        for n_it in iters:
+            if g_first is not None:
+                gpu_launches += g_first.launches + (n_it - 1) * g_rest.launches
+            elif g_rest is not None:
+                gpu_launches += n_it * g_rest.launches
     value = dof * args.steps / t
 
     # ---- dominant kernel: fine-level half-sweep (12 B per fine cell) ---------

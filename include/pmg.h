@@ -15,13 +15,15 @@
  * red/black split, horizontal index fastest.  Cell (i, j, k) of a part
  * with local i in [-1, nx], j in [-1, ny] (-1 and nx/ny are halo) lives at
  *
- *   field[c * cstride + k * plane + (j + 1) * pitch + PMG_OFF + (i >> 1)]
+ *   field[c * cstride + (j + 1) * nz * plane + k * plane + PMG_OFF + (i >> 1)]
  *   with colour c = (i + j + parity) & 1, parity = (i0 + j0) & 1,
+ *   plane = pitch = roundup(PMG_OFF + nx/2 + 1, 8), cstride = (ny+2)*nz*plane,
  *
  * i.e. red cells ((i+j) even in GLOBAL indices, reference smoother.py:66)
- * and black cells are two separate [nz][ny+2][pitch] arrays.  Use
+ * and black cells are two separate [ny+2][nz][pitch] arrays (rows j
+ * slowest, then vertical levels k, then the horizontal index).  Use
  * pmg_level_layout() for pitch/plane/cstride and pmg_level_field_doubles()
- * for the allocation size.
+ * (= 2 * cstride) for the allocation size.
  */
 #ifndef PMG_H
 #define PMG_H
@@ -35,6 +37,7 @@ extern "C" {
 #define PMG_ERR_CUDA -2     /* CUDA runtime failure -> RuntimeError              */
 #define PMG_ERR_PIVOT -3    /* zero pivot -> ZeroPivotError (tridiag.py:20)      */
 #define PMG_ERR_INTERNAL -4
+#define PMG_ERR_BREAKDOWN -5 /* CG breakdown -> BreakdownError (krylov.py:29)    */
 
 #define PMG_OFF 4           /* offset (doubles) of h = 0 inside a row            */
 
@@ -70,6 +73,8 @@ const char *pmg_last_error(void);
 int pmg_device_sm_count(int device, int *out);
 
 int pmg_level_create(const pmg_level_desc *desc, pmg_level **out);
+/* owned columns and vertical cells of a level */
+int pmg_level_dims(const pmg_level *lvl, int *nx, int *ny, int *nz);
 int pmg_level_destroy(pmg_level *lvl);
 long long pmg_level_field_doubles(const pmg_level *lvl);
 int pmg_level_layout(const pmg_level *lvl, int *pitch, long long *plane,
@@ -88,6 +93,19 @@ int pmg_from_ref_layout(const pmg_level *lvl, const double *src_dev, double *fie
                         void *stream);
 int pmg_to_ref_layout(const pmg_level *lvl, const double *field, double *dst_dev,
                       void *stream);
+
+/* host (nx, ny, nz) reference-layout block <-> device field through a
+ * device staging buffer of nx*ny*nz doubles (Field upload / download of
+ * SURVEY 8b; scatter_owned / gather_owned per part, partition.py:243-264).
+ * Stream-ordered; the host buffer should be pinned for asynchrony. */
+int pmg_field_upload(const pmg_level *lvl, const double *host, double *field,
+                     double *staging_dev, void *stream);
+int pmg_field_download(const pmg_level *lvl, const double *field, double *host,
+                       double *staging_dev, void *stream);
+/* whole allocation (halo included): fill with a value / copy
+ * (DistField.fill / copy, partition.py:128-137) */
+int pmg_fill(const pmg_level *lvl, double *field, double value, void *stream);
+int pmg_copy(const pmg_level *lvl, double *dst, const double *src, void *stream);
 
 /* ---- operator: PanelOperator.apply / residual (stencil.py:127-165) --- */
 /* out = A u on owned cells; u halo must be current. */
@@ -122,6 +140,15 @@ int pmg_half_sweep_halo(const pmg_level *lvl, double *u, const double *f, int co
 int pmg_get_smoother_mode(void);
 int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
                    double rho, int zero_start, int neighbors_zero, double post_scale,
+                   void *stream);
+
+/* z = M^-1 r, symmetric red-black block SSOR from zero for a part that is
+ * its own neighbour (LineSmoother.ssor_apply, smoother.py:224-244): red
+ * (zero start, no neighbours), black (zero start, x (2 - rho)), red, each
+ * followed by pmg_halo_self.  If rz_dev != NULL also rz_dev[0] = <r, z>
+ * (scratch: pmg_partials_size() doubles). */
+int pmg_ssor_apply(const pmg_level *lvl, const double *r, double *z, double rho,
+                   int periodic_x, int periodic_y, double *scratch, double *rz_dev,
                    void *stream);
 
 /* ---- transfers (multigrid.py:209-268) ------------------------------- */
@@ -177,6 +204,9 @@ int pmg_unpack_face(const pmg_level *lvl, double *field, int face, const double 
 /* ---- reductions and vector updates (partition.py:138-155, 267-286) -- */
 /* scratch size (doubles) every reduction entry point may use */
 long long pmg_partials_size(void);
+/* out_dev[0] = ||a||^2 over owned cells (pmg_dot(a, a)) */
+int pmg_norm2(const pmg_level *lvl, const double *a, double *scratch, double *out_dev,
+              void *stream);
 /* out_dev[0] = a.b over owned cells (deterministic order) */
 int pmg_dot(const pmg_level *lvl, const double *a, const double *b, double *scratch,
             double *out_dev, void *stream);
@@ -200,6 +230,45 @@ int pmg_cg_step(long long n, const double *alpha_num, const double *alpha_den,
 /* p = z + (beta_num[0]/beta_den[0]) p over the full allocation. */
 int pmg_cg_direction(long long n, const double *beta_num, const double *beta_den,
                      const double *z, double *p, void *stream);
+
+/* ---- device-resident drivers (multigrid.py:271-330, krylov.py:88-167) --
+ * For one part that is its own neighbour in both directions (one GPU per
+ * process; halos periodic or mirror per axis).  The hierarchy keeps the
+ * level handles (not owned; they must outlive it) and allocates the coarse
+ * iterates / right-hand sides and reduction scratch.  Same operation
+ * sequence as the Python drivers (bit-identical results). */
+typedef struct pmg_hier pmg_hier;     /* opaque */
+typedef struct pmg_mg_desc {
+    int nu_pre, nu_post;       /* V(nu_pre, nu_post)           (multigrid.py:54-84) */
+    int coarse_sweeps;         /* red-black sweeps on the coarsest level             */
+    double rho;                /* overrelaxation weight, (0, 2)                      */
+    int periodic_x, periodic_y;
+} pmg_mg_desc;
+/* levels[0] finest ... levels[nlev-1] coarsest, each halving nx and ny */
+int pmg_hier_create(const pmg_level *const *levels, int nlev, const pmg_mg_desc *desc,
+                    pmg_hier **out);
+int pmg_hier_destroy(pmg_hier *hier);
+/* one V-cycle on u (halo current) for right-hand side f (multigrid.py:271-294);
+ * first = 1: u is zero on entry but unfilled (rho = 1, nu_pre >= 1) */
+int pmg_vcycle(pmg_hier *hier, double *u, const double *f, int first, void *stream);
+/* u = 0; V-cycles until ||f - A u|| / ||f|| < eps or maxiter (multigrid.py:297-330).
+ * hist[0..iters] (HOST, maxiter + 1 doubles) receives the residual norms;
+ * non-convergence is reported in *converged, not as an error.  Synchronises
+ * the stream once per cycle; the cycle + norm replays as a CUDA graph. */
+int pmg_mg_solve(pmg_hier *hier, const double *f, double *u, double eps, int maxiter,
+                 double *hist, int *iters, int *converged, void *stream);
+/* kernels per replay of the cycle graph captured for (f, u, first); -1 if
+ * none (launch accounting: graph replays issue no host-side launches) */
+long long pmg_hier_graph_launches(const pmg_hier *hier, const double *f, const double *u,
+                                  int first);
+/* preconditioned CG from u = 0 (krylov.py:88-167): precond 1 = SSOR(rho),
+ * 0 = identity; tau as the reference (tiny-residual cut-off).  work: device
+ * buffer of pmg_pcg_work_doubles() doubles; hist as pmg_mg_solve.
+ * PMG_ERR_BREAKDOWN on <p, A p> <= 0 or <r, z> <= 0. */
+long long pmg_pcg_work_doubles(const pmg_level *lvl);
+int pmg_pcg_solve(const pmg_level *lvl, const double *f, double *u, double eps, int maxiter,
+                  double tau, int precond, double rho, int periodic_x, int periodic_y,
+                  double *work, double *hist, int *iters, int *converged, void *stream);
 
 #ifdef __cplusplus
 }

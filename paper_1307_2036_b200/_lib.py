@@ -16,7 +16,15 @@ PMG_OK = 0
 PMG_ERR_VALUE = -1
 PMG_ERR_CUDA = -2
 PMG_ERR_PIVOT = -3
+PMG_ERR_BREAKDOWN = -5
 OFF = 4
+
+
+class MGDesc(C.Structure):
+    _fields_ = [
+        ("nu_pre", C.c_int), ("nu_post", C.c_int), ("coarse_sweeps", C.c_int),
+        ("rho", C.c_double), ("periodic_x", C.c_int), ("periodic_y", C.c_int),
+    ]
 
 
 class LevelDesc(C.Structure):
@@ -48,6 +56,21 @@ SIGNATURES = {
                               C.POINTER(_I), C.POINTER(_I)]),
     "pmg_level_tables": (_I, [_P, _P, _P, _P]),
     "pmg_level_prepare": (_I, [_P, _P]),
+    "pmg_level_dims": (_I, [_P, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
+    "pmg_field_upload": (_I, [_P, _P, _P, _P, _P]),
+    "pmg_field_download": (_I, [_P, _P, _P, _P, _P]),
+    "pmg_fill": (_I, [_P, _P, _D, _P]),
+    "pmg_copy": (_I, [_P, _P, _P, _P]),
+    "pmg_norm2": (_I, [_P, _P, _P, _P, _P]),
+    "pmg_ssor_apply": (_I, [_P, _P, _P, _D, _I, _I, _P, _P, _P]),
+    "pmg_hier_create": (_I, [C.POINTER(_P), _I, C.POINTER(MGDesc), C.POINTER(_P)]),
+    "pmg_hier_destroy": (_I, [_P]),
+    "pmg_hier_graph_launches": (_LL, [_P, _P, _P, _I]),
+    "pmg_vcycle": (_I, [_P, _P, _P, _I, _P]),
+    "pmg_mg_solve": (_I, [_P, _P, _P, _D, _I, _P, C.POINTER(_I), C.POINTER(_I), _P]),
+    "pmg_pcg_work_doubles": (_LL, [_P]),
+    "pmg_pcg_solve": (_I, [_P, _P, _P, _D, _I, _D, _I, _D, _I, _I, _P, _P, C.POINTER(_I),
+                           C.POINTER(_I), _P]),
     "pmg_from_ref_layout": (_I, [_P, _P, _P, _P]),
     "pmg_to_ref_layout": (_I, [_P, _P, _P, _P]),
     "pmg_apply": (_I, [_P, _P, _P, _P]),
@@ -113,6 +136,9 @@ def check(rc: int, what: str = ""):
     if rc == PMG_ERR_PIVOT:
         from .tridiag import ZeroPivotError
         raise ZeroPivotError(f"{what}: {msg}")
+    if rc == PMG_ERR_BREAKDOWN:
+        from .krylov import BreakdownError
+        raise BreakdownError(msg)
     raise RuntimeError(f"{what}: {msg}")
 
 

@@ -38,6 +38,7 @@ cudaError_t launch_pack(const Lvl &, const double *, int, double *, cudaStream_t
 cudaError_t launch_unpack(const Lvl &, double *, int, const double *, int, cudaStream_t);
 cudaError_t launch_dot(const Lvl &, const double *, const double *, double *, int *, cudaStream_t);
 cudaError_t launch_axpy(long long, double, const double *, double *, cudaStream_t);
+cudaError_t launch_fill(long long, double, double *, cudaStream_t);
 cudaError_t launch_xpby(long long, const double *, double, double *, cudaStream_t);
 cudaError_t launch_cg_direction(long long, const double *, const double *, const double *,
                                 double *, cudaStream_t);
@@ -66,6 +67,11 @@ static thread_local std::string g_err;
 static int fail(int code, const std::string &msg) {
     g_err = msg;
     return code;
+}
+
+namespace pmg {
+// error reporting for the other translation units of the library
+int set_error(int code, const char *msg) { return fail(code, msg); }
 }
 
 static int cuda_fail(cudaError_t e, const char *where) {
@@ -273,6 +279,14 @@ int pmg_level_layout(const pmg_level *lv, int *pitch, long long *plane, long lon
     return PMG_OK;
 }
 
+int pmg_level_dims(const pmg_level *lv, int *nx, int *ny, int *nz) {
+    PMG_CHECK_LVL(lv);
+    if (nx) *nx = lv->L.nx;
+    if (ny) *ny = lv->L.ny;
+    if (nz) *nz = lv->L.nz;
+    return PMG_OK;
+}
+
 int pmg_level_tables(const pmg_level *lv, double *diag, double *band, double *invd) {
     PMG_CHECK_LVL(lv);
     if (!lv->L.uniform) return fail(PMG_ERR_VALUE, "level has variable coefficients");
@@ -464,6 +478,68 @@ int pmg_dot(const pmg_level *lv, const double *a, const double *b, double *scrat
     int np = 0;
     PMG_CUDA(launch_dot(lv->L, a, b, scratch, &np, (cudaStream_t)st), "dot");
     PMG_CUDA(launch_finalize(scratch, np, out, (cudaStream_t)st), "dot reduce");
+    return PMG_OK;
+}
+
+int pmg_norm2(const pmg_level *lv, const double *a, double *scratch, double *out, void *st) {
+    return pmg_dot(lv, a, a, scratch, out, st);
+}
+
+int pmg_fill(const pmg_level *lv, double *field, double value, void *st) {
+    PMG_CHECK_LVL(lv);
+    const long long n = lv->L.cstride * 2;
+    if (value == 0.0 && !std::signbit(value)) {
+        PMG_CUDA(cudaMemsetAsync(field, 0, sizeof(double) * n, (cudaStream_t)st), "fill");
+    } else {
+        PMG_CUDA(launch_fill(n, value, field, (cudaStream_t)st), "fill");
+    }
+    return PMG_OK;
+}
+
+int pmg_copy(const pmg_level *lv, double *dst, const double *src, void *st) {
+    PMG_CHECK_LVL(lv);
+    PMG_CUDA(cudaMemcpyAsync(dst, src, sizeof(double) * lv->L.cstride * 2,
+                             cudaMemcpyDeviceToDevice, (cudaStream_t)st), "copy");
+    return PMG_OK;
+}
+
+int pmg_field_upload(const pmg_level *lv, const double *host, double *field, double *staging,
+                     void *st) {
+    PMG_CHECK_LVL(lv);
+    if (!host || !field || !staging) return fail(PMG_ERR_VALUE, "null buffer");
+    const size_t n = (size_t)lv->L.nx * lv->L.ny * lv->L.nz;
+    PMG_CUDA(cudaMemcpyAsync(staging, host, n * sizeof(double), cudaMemcpyHostToDevice,
+                             (cudaStream_t)st), "field upload");
+    PMG_CUDA(launch_from_ref(lv->L, staging, field, (cudaStream_t)st), "field upload layout");
+    return PMG_OK;
+}
+
+int pmg_field_download(const pmg_level *lv, const double *field, double *host, double *staging,
+                       void *st) {
+    PMG_CHECK_LVL(lv);
+    if (!host || !field || !staging) return fail(PMG_ERR_VALUE, "null buffer");
+    const size_t n = (size_t)lv->L.nx * lv->L.ny * lv->L.nz;
+    PMG_CUDA(launch_to_ref(lv->L, field, staging, (cudaStream_t)st), "field download layout");
+    PMG_CUDA(cudaMemcpyAsync(host, staging, n * sizeof(double), cudaMemcpyDeviceToHost,
+                             (cudaStream_t)st), "field download");
+    return PMG_OK;
+}
+
+int pmg_ssor_apply(const pmg_level *lv, const double *r, double *z, double rho, int periodic_x,
+                   int periodic_y, double *scratch, double *rz_dev, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (!(rho > 0.0 && rho < 2.0)) return fail(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
+    if (rz_dev && !scratch) return fail(PMG_ERR_VALUE, "the <r, z> product needs a scratch buffer");
+    int rc;
+    // smoother.py:224-244: red from zero without neighbours, black from zero
+    // scaled by (2 - rho), red; a halo refresh after each
+    if ((rc = pmg_half_sweep(lv, z, r, 0, rho, 1, 1, 1.0, st))) return rc;
+    if ((rc = pmg_halo_self(lv, z, periodic_x, periodic_y, st))) return rc;
+    if ((rc = pmg_half_sweep(lv, z, r, 1, rho, 1, 0, 2.0 - rho, st))) return rc;
+    if ((rc = pmg_halo_self(lv, z, periodic_x, periodic_y, st))) return rc;
+    if ((rc = pmg_half_sweep(lv, z, r, 0, rho, 0, 0, 1.0, st))) return rc;
+    if ((rc = pmg_halo_self(lv, z, periodic_x, periodic_y, st))) return rc;
+    if (rz_dev) return pmg_dot(lv, r, z, scratch, rz_dev, st);
     return PMG_OK;
 }
 

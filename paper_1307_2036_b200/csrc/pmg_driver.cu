@@ -1,0 +1,372 @@
+// Native solve drivers of libpmg (include/pmg.h, "drivers" section):
+// the V-cycle / mg_solve of multigrid.py:271-330 and the preconditioned CG of
+// krylov.py:88-167 for one part that is its own neighbour (one GPU per
+// process, periodic or mirror halos), written over the level entry points
+// of pmg_api.cu.  The V-cycle + convergence norm is captured once per
+// (f, u, first-cycle, stream) into a CUDA graph and replayed; the host reads
+// one scalar per cycle (CG: three per iteration) from host-mapped memory.
+//
+// Operation sequence = the Python drivers' fused path (multigrid.v_cycle
+// with cfg.fused, krylov.pcg_solve), so both give bit-identical results.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/pmg.h"
+
+namespace pmg {
+int set_error(int code, const char *msg);
+}
+
+namespace {
+
+int err(int code, const std::string &m) { return pmg::set_error(code, m.c_str()); }
+
+int cuda_err(cudaError_t e, const char *where) {
+    return err(PMG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TRY(x)                         \
+    do {                               \
+        int rc_ = (x);                 \
+        if (rc_) return rc_;           \
+    } while (0)
+#define TRYC(x, where)                            \
+    do {                                          \
+        cudaError_t e_ = (x);                     \
+        if (e_ != cudaSuccess) return cuda_err(e_, where); \
+    } while (0)
+
+struct Graph {
+    const double *f;
+    double *u;
+    int first;
+    cudaStream_t st;
+    cudaGraphExec_t exec;
+    long long launches;   // library kernels recorded in the graph
+};
+
+}  // namespace
+
+struct pmg_hier {
+    std::vector<const pmg_level *> lv;
+    std::vector<long long> nd;       // field doubles per level
+    pmg_mg_desc d;
+    std::vector<double *> u, f;      // coarse-level iterates / right-hand sides (index >= 1)
+    double *scratch = nullptr;       // reduction partials
+    double *res_h = nullptr;         // host-mapped scalars [8]
+    double *res_d = nullptr;
+    std::vector<Graph> graphs;
+    // the legacy default stream cannot be captured: solves issued on it run
+    // on this stream, ordered after / before the caller's work by events
+    cudaStream_t own = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+};
+
+namespace {
+
+void free_hier(pmg_hier *h) {
+    for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+    for (size_t c = 1; c < h->u.size(); ++c) {
+        cudaFree(h->u[c]);
+        cudaFree(h->f[c]);
+    }
+    if (h->scratch) cudaFree(h->scratch);
+    if (h->res_h) cudaFreeHost(h->res_h);
+    if (h->own) cudaStreamDestroy(h->own);
+    if (h->ev_in) cudaEventDestroy(h->ev_in);
+    if (h->ev_out) cudaEventDestroy(h->ev_out);
+    delete h;
+}
+
+int halo(const pmg_hier *h, int c, double *x, cudaStream_t st) {
+    return pmg_halo_self(h->lv[c], x, h->d.periodic_x, h->d.periodic_y, st);
+}
+
+// red-black sweeps with a halo refresh after each half (smoother.py:184-191);
+// from_zero: the iterate is zero on entry but unfilled, the first red
+// half-sweep ignores it (neighbours zero; rhs = f exactly)
+int sweeps(const pmg_hier *h, int c, double *u, const double *f, int n, bool from_zero,
+           cudaStream_t st) {
+    for (int s = 0; s < n; ++s) {
+        TRY(pmg_half_sweep(h->lv[c], u, f, 0, h->d.rho, 0, (from_zero && s == 0) ? 1 : 0, 1.0, st));
+        TRY(halo(h, c, u, st));
+        TRY(pmg_half_sweep(h->lv[c], u, f, 1, h->d.rho, 0, 0, 1.0, st));
+        TRY(halo(h, c, u, st));
+    }
+    return PMG_OK;
+}
+
+// Alg. 1 (multigrid.py:271-294); level 0 works on the caller's u0 / f0
+int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStream_t st) {
+    const int L = (int)h->lv.size();
+    double *u = c ? h->u[c] : u0;
+    const double *f = c ? h->f[c] : f0;
+    const bool lean = h->d.rho == 1.0;
+    if (c + 1 < L) {
+        TRY(sweeps(h, c, u, f, h->d.nu_pre, lean && (c > 0 || first), st));
+        TRY(pmg_residual_restrict(h->lv[c], h->lv[c + 1], f, u, h->f[c + 1], st));
+        // the coarse iterate starts from zero: skip the fill when its first
+        // red half-sweep ignores it anyway
+        const int first_sweeps = (c + 2 == L) ? h->d.coarse_sweeps : h->d.nu_pre;
+        if (!(lean && first_sweeps >= 1))
+            TRYC(cudaMemsetAsync(h->u[c + 1], 0, sizeof(double) * h->nd[c + 1], st), "coarse fill");
+        TRY(vcycle(h, c + 1, u0, f0, false, st));
+        // u += P e (black cells only when the red half-sweep overwrites red)
+        TRY(pmg_prolong_colors(h->lv[c], h->lv[c + 1], h->u[c + 1], u, 1,
+                               (lean && h->d.nu_post >= 1) ? 2 : 3, st));
+        TRY(halo(h, c, u, st));
+        TRY(sweeps(h, c, u, f, h->d.nu_post, false, st));
+    } else {
+        TRY(sweeps(h, c, u, f, h->d.coarse_sweeps, lean && c > 0, st));
+    }
+    return PMG_OK;
+}
+
+int cycle_and_norm(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st) {
+    TRY(vcycle(h, 0, u, f, first, st));
+    return pmg_residual(h->lv[0], f, u, nullptr, h->scratch, h->res_d, st);
+}
+
+int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st) {
+    if (!st) return cycle_and_norm(h, u, f, first, st);   // legacy stream: no capture
+    for (auto &g : h->graphs)
+        if (g.f == f && g.u == u && g.first == (int)first && g.st == st) {
+            TRYC(cudaGraphLaunch(g.exec, st), "graph launch");
+            return PMG_OK;
+        }
+    if (h->graphs.size() >= 8) {
+        cudaGraphExecDestroy(h->graphs.front().exec);
+        h->graphs.erase(h->graphs.begin());
+    }
+    cudaGraph_t graph;
+    const long long l0 = pmg_launch_count();
+    TRYC(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
+    int rc = cycle_and_norm(h, u, f, first, st);
+    cudaError_t e = cudaStreamEndCapture(st, &graph);
+    if (rc) {
+        if (e == cudaSuccess) cudaGraphDestroy(graph);
+        return rc;
+    }
+    TRYC(e, "capture end");
+    Graph g{f, u, (int)first, st, nullptr, pmg_launch_count() - l0};
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    TRYC(e, "graph instantiate");
+    h->graphs.push_back(g);
+    TRYC(cudaGraphLaunch(g.exec, st), "graph launch");
+    return PMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmg_hier_create(const pmg_level *const *levels, int nlev, const pmg_mg_desc *desc,
+                    pmg_hier **out) {
+    if (!levels || !desc || !out || nlev < 1) return err(PMG_ERR_VALUE, "bad hierarchy arguments");
+    if (desc->nu_pre < 0 || desc->nu_post < 0 || desc->coarse_sweeps < 0)
+        return err(PMG_ERR_VALUE, "sweep counts must be non-negative");
+    if (!(desc->rho > 0.0 && desc->rho < 2.0))
+        return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
+    int nx0 = 0, ny0 = 0, nz0 = 0;
+    for (int c = 0; c < nlev; ++c) {
+        int nx, ny, nz;
+        TRY(pmg_level_dims(levels[c], &nx, &ny, &nz));
+        if (c == 0) {
+            nx0 = nx, ny0 = ny, nz0 = nz;
+        } else if (nx != (nx0 >> c) || ny != (ny0 >> c) || nz != nz0 || (nx << c) != nx0 ||
+                   (ny << c) != ny0) {
+            return err(PMG_ERR_VALUE, "each level must halve nx and ny at equal nz");
+        }
+    }
+    pmg_hier *h = new pmg_hier();
+    h->d = *desc;
+    h->lv.assign(levels, levels + nlev);
+    h->u.assign(nlev, nullptr);
+    h->f.assign(nlev, nullptr);
+    for (int c = 0; c < nlev; ++c) h->nd.push_back(pmg_level_field_doubles(levels[c]));
+    cudaError_t e = cudaSuccess;
+    for (int c = 1; c < nlev && e == cudaSuccess; ++c) {
+        e = cudaMalloc(&h->u[c], sizeof(double) * h->nd[c]);
+        if (e == cudaSuccess) e = cudaMalloc(&h->f[c], sizeof(double) * h->nd[c]);
+        // halos of a fresh coarse iterate must be finite
+        if (e == cudaSuccess) e = cudaMemset(h->u[c], 0, sizeof(double) * h->nd[c]);
+    }
+    if (e == cudaSuccess) e = cudaMalloc(&h->scratch, sizeof(double) * pmg_partials_size());
+    if (e == cudaSuccess) e = cudaHostAlloc(&h->res_h, 8 * sizeof(double), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&h->res_d, h->res_h, 0);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_out, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        free_hier(h);
+        return cuda_err(e, "hierarchy allocation");
+    }
+    *out = h;
+    return PMG_OK;
+}
+
+int pmg_hier_destroy(pmg_hier *h) {
+    if (h) free_hier(h);
+    return PMG_OK;
+}
+
+long long pmg_hier_graph_launches(const pmg_hier *h, const double *f, const double *u,
+                                  int first) {
+    if (!h) return -1;
+    for (auto &g : h->graphs)
+        if (g.f == f && g.u == u && g.first == first) return g.launches;
+    return -1;
+}
+
+int pmg_vcycle(pmg_hier *h, double *u, const double *f, int first, void *stream) {
+    if (!h || !u || !f) return err(PMG_ERR_VALUE, "null argument");
+    if (first && !(h->d.rho == 1.0 && h->lv.size() > 1 && h->d.nu_pre >= 1))
+        return err(PMG_ERR_VALUE, "first = 1 needs rho = 1, nu_pre >= 1 and two levels");
+    return vcycle(h, 0, u, f, first != 0, (cudaStream_t)stream);
+}
+
+static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int maxiter,
+                       double *hist, int *iters, int *converged, cudaStream_t st) {
+    const pmg_level *l0 = h->lv[0];
+    // r0 = ||f|| (multigrid.py:307-309)
+    TRY(pmg_dot(l0, f, f, h->scratch, h->res_d, st));
+    TRYC(cudaStreamSynchronize(st), "sync");
+    const double r0 = std::sqrt(h->res_h[0]);
+    hist[0] = r0;
+    *iters = 0;
+    *converged = 0;
+    if (r0 == 0.0) {
+        TRY(pmg_fill(l0, u, 0.0, st));
+        *converged = 1;
+        return PMG_OK;
+    }
+    // rho = 1: the first cycle starts from zero without filling u
+    const bool lean_first = h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->lv.size() > 1;
+    if (!lean_first) TRY(pmg_fill(l0, u, 0.0, st));
+    for (int it = 0; it < maxiter; ++it) {
+        TRY(replay(h, u, f, lean_first && it == 0, st));
+        TRYC(cudaStreamSynchronize(st), "sync");
+        const double rn = std::sqrt(h->res_h[0]);
+        hist[it + 1] = rn;
+        *iters = it + 1;
+        if (rn / r0 < eps) {
+            *converged = 1;
+            break;
+        }
+    }
+    return PMG_OK;
+}
+
+int pmg_mg_solve(pmg_hier *h, const double *f, double *u, double eps, int maxiter, double *hist,
+                 int *iters, int *converged, void *stream) {
+    if (!h || !f || !u || !hist || !iters || !converged) return err(PMG_ERR_VALUE, "null argument");
+    if (maxiter < 0 || !(eps > 0.0)) return err(PMG_ERR_VALUE, "need eps > 0 and maxiter >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (st) return mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, st);
+    // legacy stream: run on the hierarchy's stream, ordered by events
+    TRYC(cudaEventRecord(h->ev_in, 0), "event");
+    TRYC(cudaStreamWaitEvent(h->own, h->ev_in, 0), "event wait");
+    const int rc = mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, h->own);
+    TRYC(cudaEventRecord(h->ev_out, h->own), "event");
+    TRYC(cudaStreamWaitEvent(0, h->ev_out, 0), "event wait");
+    return rc;
+}
+
+// Alg. 2 (krylov.py:88-167, the Python pcg_solve's sequence without a
+// callback): SSOR (precond = 1) or identity (precond = 0) preconditioner;
+// alpha and beta stay on the device and the host reads <p,q>, ||r||^2 and
+// the <r,z> of the step once per iteration.  The iterate update of
+// iteration k is deferred into the direction update of iteration k+1
+// (pmg_cg_step) and flushed at exit.  PMG_ERR_BREAKDOWN on <p,q> <= 0 or
+// <r,z> <= 0.  work: pmg_pcg_work_doubles() device doubles.
+int pmg_pcg_solve(const pmg_level *lv, const double *f, double *u, double eps, int maxiter,
+                  double tau, int precond, double rho, int periodic_x, int periodic_y,
+                  double *work, double *hist, int *iters, int *converged, void *stream) {
+    if (!lv || !f || !u || !work || !hist || !iters || !converged)
+        return err(PMG_ERR_VALUE, "null argument");
+    if (!(eps > 0.0 && eps < 1.0)) return err(PMG_ERR_VALUE, "relative tolerance must lie in (0, 1)");
+    if (precond && !(rho > 0.0 && rho < 2.0))
+        return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long n = pmg_level_field_doubles(lv);
+    double *r = work, *z = work + n, *p = work + 2 * n, *q = work + 3 * n;
+    double *scratch = work + 4 * n;
+    double *kap = scratch + pmg_partials_size();   // device scalars: kappa, pq, rr, kappa_new
+    double *pq = kap + 1, *rr = kap + 2, *kapn = kap + 3;
+    double *res_h = nullptr, *res_d = nullptr;
+    TRYC(cudaHostAlloc(&res_h, 4 * sizeof(double), cudaHostAllocMapped), "pinned scalars");
+    struct Free {
+        double *p;
+        ~Free() { cudaFreeHost(p); }
+    } guard{res_h};
+    TRYC(cudaHostGetDevicePointer((void **)&res_d, res_h, 0), "pinned scalars");
+    auto precondition = [&](void) -> int {
+        if (precond)
+            return pmg_ssor_apply(lv, r, z, rho, periodic_x, periodic_y, nullptr, nullptr, stream);
+        TRY(pmg_copy(lv, z, r, stream));
+        return pmg_halo_self(lv, z, periodic_x, periodic_y, stream);
+    };
+    auto read = [&](const double *dev, int k) -> int {
+        TRYC(cudaMemcpyAsync(res_d, dev, k * sizeof(double), cudaMemcpyDeviceToDevice, st),
+             "scalar read");
+        TRYC(cudaStreamSynchronize(st), "sync");
+        return PMG_OK;
+    };
+    // u = 0, r = f (full allocation), r0 = ||r||
+    TRY(pmg_fill(lv, u, 0.0, stream));
+    TRY(pmg_copy(lv, r, f, stream));
+    TRY(pmg_dot(lv, r, r, scratch, res_d, stream));
+    TRYC(cudaStreamSynchronize(st), "sync");
+    const double r0 = std::sqrt(res_h[0]);
+    hist[0] = r0;
+    *iters = 0;
+    *converged = 0;
+    if (r0 == 0.0 || r0 < tau) {
+        *converged = 1;
+        return PMG_OK;
+    }
+    TRY(precondition());
+    TRY(pmg_copy(lv, p, z, stream));
+    TRY(pmg_dot(lv, r, z, scratch, kap, stream));
+    TRY(read(kap, 1));
+    if (!(res_h[0] > 0.0)) return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
+    bool pending = false;
+    for (int it = 1; it <= maxiter; ++it) {
+        TRY(pmg_apply_dot(lv, p, q, scratch, pq, stream));
+        TRY(pmg_cg_update(lv, kap, pq, p, q, nullptr, r, scratch, rr, stream));
+        pending = true;
+        TRY(read(kap, 3));                        // kappa, pq, rr
+        if (!(res_h[0] > 0.0)) return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
+        if (!(res_h[1] > 0.0)) return err(PMG_ERR_BREAKDOWN, "<p, A p> <= 0: operator is not positive definite");
+        const double rn = std::sqrt(res_h[2]);
+        hist[it] = rn;
+        *iters = it;
+        if (rn / r0 < eps || rn < tau) {
+            *converged = 1;
+            break;
+        }
+        TRY(precondition());
+        TRY(pmg_dot(lv, r, z, scratch, kapn, stream));
+        // u += (kappa / pq) p ; p = z + (kappa_new / kappa) p
+        TRY(pmg_cg_step(n, kap, pq, kapn, kap, z, p, u, stream));
+        pending = false;
+        TRYC(cudaMemcpyAsync(kap, kapn, sizeof(double), cudaMemcpyDeviceToDevice, st), "kappa");
+    }
+    if (pending) TRY(pmg_cg_step(n, kap, pq, kap, kap, nullptr, p, u, stream));
+    TRY(read(kap, 1));
+    if (!*converged && !(res_h[0] > 0.0))
+        return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
+    return PMG_OK;
+}
+
+long long pmg_pcg_work_doubles(const pmg_level *lv) {
+    if (!lv) return -1;
+    return 4 * pmg_level_field_doubles(lv) + pmg_partials_size() + 8;
+}
+
+}  // extern "C"

@@ -2561,6 +2561,12 @@ k_dot2(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+__global__ void k_fill(long long n, double v, double *__restrict__ y) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+         e += (long long)gridDim.x * blockDim.x)
+        y[e] = v;
+}
+
 __global__ void k_axpy(long long n, double a, const double *__restrict__ x, double *__restrict__ y) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
          e += (long long)gridDim.x * blockDim.x)
@@ -3317,6 +3323,12 @@ cudaError_t launch_dot(const Lvl &L, const double *a, const double *b, double *p
         k_dot2<RPB, true><<<g, bs, 0, st>>>(L, a, b, partials, nch);
     else
         k_dot2<RPB, false><<<g, bs, 0, st>>>(L, a, b, partials, nch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(long long n, double v, double *y, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k_fill<<<stream_blocks(n), 256, 0, st>>>(n, v, y);
     return cudaGetLastError();
 }
 

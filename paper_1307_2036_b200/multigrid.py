@@ -16,13 +16,15 @@ stopping rule (``multigrid.py:297-330``).  B200-specific execution:
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import time
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
-from ._lib import call, load
+from ._lib import MGDesc, call, load
 from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
@@ -107,6 +109,7 @@ class LevelHierarchy:
         self.params = params
         self._persist = None
         self._graphs = {}
+        self._native = {}
 
     def __len__(self) -> int:
         return len(self.levels)
@@ -136,6 +139,44 @@ class LevelHierarchy:
         if self._persist is None:
             self._persist = self.make_scratch()
         return self._persist
+
+    def native(self, cfg: "MGConfig") -> "NativeHierarchy":
+        """The device-resident driver (pmg_hier) of this single-part
+        hierarchy for ``cfg``'s cycle shape (cached)."""
+        key = (cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), cfg.rho)
+        h = self._native.get(key)
+        if h is None:
+            h = NativeHierarchy(self, cfg)
+            self._native[key] = h
+        return h
+
+
+class NativeHierarchy:
+    """Owner of a ``pmg_hier``: the C++ V-cycle / mg_solve driver over this
+    hierarchy's level handles (include/pmg.h, drivers section)."""
+
+    def __init__(self, hier: LevelHierarchy, cfg: "MGConfig"):
+        lay = hier.fine.layout
+        if len(lay.local_workers) != 1 or lay.px != 1 or lay.py != 1:
+            raise ValueError("the native driver runs single-part hierarchies")
+        w = lay.local_workers[0]
+        self._levels = [lev.op.handles[w] for lev in hier.levels]   # keep alive
+        arr = (C.c_void_p * len(self._levels))(*[h.h.value for h in self._levels])
+        per = int(bool(lay.periodic))
+        d = MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), float(cfg.rho), per,
+                   per)
+        h = C.c_void_p()
+        call("pmg_hier_create", arr, len(self._levels), C.byref(d), C.byref(h))
+        self.h = h
+        self._lib = load()
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            self._lib.pmg_hier_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def graph_launches(self, f_ptr: int, u_ptr: int, first: bool) -> int:
+        return int(self._lib.pmg_hier_graph_launches(self.h, f_ptr, u_ptr, int(first)))
 
 
 def _level_count(nx: int, pside: int, cfg: MGConfig) -> int:
@@ -354,6 +395,35 @@ class _CycleGraph:
         return self.res
 
 
+#: single-part graph solves run the C++ driver (pmg_mg_solve); False keeps
+#: the Python V-cycle (same kernels, same order: bit-identical results)
+USE_NATIVE = True
+
+
+def _mg_solve_native(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out):
+    """mg_solve through pmg_mg_solve: the V-cycle sequence of ``v_cycle``
+    (fused path) captured once per buffer pair into a CUDA graph by the
+    library, one 8-byte host read per cycle."""
+    nh = hier.native(cfg)
+    if out is None:
+        u = hier.persistent_scratch()[0].u
+    else:
+        u = out
+    (w, uf), = u.parts.items()
+    fp = f.parts[w]
+    hist = np.zeros(cfg.maxiter + 1)
+    iters, conv = C.c_int(), C.c_int()
+    torch.cuda.current_stream().synchronize()
+    t0 = time.perf_counter()
+    call("pmg_mg_solve", nh.h, fp.ptr, uf.ptr, float(cfg.eps), int(cfg.maxiter),
+         hist.ctypes.data_as(C.c_void_p), C.byref(iters), C.byref(conv), _stream())
+    wall = time.perf_counter() - t0
+    history = hist[:iters.value + 1].tolist()
+    if out is None:
+        u = u.copy()
+    return u, SolveReport(iters.value, history, bool(conv.value), wall, _echo(hier, cfg))
+
+
 def _ptrs(df: DistField):
     return tuple(p.data.data_ptr() for p in df.parts.values())
 
@@ -371,6 +441,9 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
     half-sweep ignores u, exactly as f + drw*0 = f).
     """
     use_graph = cfg.graph and _dist() is None
+    if (use_graph and cfg.fused and USE_NATIVE and not FUSE_PROLONG
+            and hier.fine.layout.px == 1 and hier.fine.layout.py == 1):
+        return _mg_solve_native(f, hier, cfg, out)
     coarse = hier.persistent_scratch() if use_graph else hier.make_scratch()
     # iterate: the caller's ``out``; else the hierarchy's level-0 scratch
     # (graph reuse across calls), copied out at the end

@@ -562,3 +562,69 @@ def test_fused_prolongation(pmg, workers, periodic, graph):
     assert len(h0) == len(h1)
     assert np.max(np.abs(h1 - h0) / h0) <= 1e-9
     assert np.max(np.abs(u1 - u0)) <= 1e-11 * np.max(np.abs(u0))
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+def test_native_drivers_match_python(pmg, periodic):
+    """pmg_mg_solve / pmg_pcg_solve (C++ drivers, CUDA-graph replay) against
+    the Python drivers over the same kernels: bit-identical histories and
+    iterates, on the legacy stream and on a side stream."""
+    from paper_1307_2036_b200 import krylov as kr
+    from paper_1307_2036_b200 import multigrid as mgm
+    nx, nz = 32, 8
+    grid = pmg.periodic_box(nx, nz, 0.01) if periodic else pmg.panel_grid(nx, nz, flat_mode=True)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 3.3e-2)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, eps=1e-9)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    f = pmg.scatter_owned(uni((nx, nx, nz), 5), hier.fine.layout)
+    res = {}
+    for native in (False, True):
+        mgm.USE_NATIVE = kr.USE_NATIVE = native
+        try:
+            u, rep = pmg.mg_solve(f, hier, cfg)
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                u2, rep2 = pmg.mg_solve(f, hier, cfg)
+            torch.cuda.current_stream().wait_stream(side)
+            op = hier.fine.op
+            cg = {}
+            for name, pre in (("ssor", pmg.SSORPreconditioner(pmg.LineSmoother(op))),
+                              ("ssor13", pmg.SSORPreconditioner(pmg.LineSmoother(op), 1.3)),
+                              ("id", pmg.IdentityPreconditioner())):
+                uc, rc = pmg.pcg_solve(f, op, pre, eps=1e-8, maxiter=200)
+                cg[name] = (rc.residual_history, pmg.gather_owned(uc), rc.converged)
+            res[native] = (rep.residual_history, pmg.gather_owned(u), rep2.residual_history,
+                           pmg.gather_owned(u2), cg)
+        finally:
+            mgm.USE_NATIVE = kr.USE_NATIVE = True
+    a, b = res[False], res[True]
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
+    assert b[2] == b[0] and np.array_equal(b[3], b[1])
+    for name in a[4]:
+        assert a[4][name][0] == b[4][name][0], name
+        assert np.array_equal(a[4][name][1], b[4][name][1]), name
+        assert a[4][name][2] and b[4][name][2]
+
+
+def test_native_hierarchy_errors(pmg):
+    from paper_1307_2036_b200 import _lib
+    lib = _lib.load()
+    grid = pmg.periodic_box(16, 4, 0.01)
+    params = pmg.toy_parameters(16, 4, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=2)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    w = hier.fine.layout.local_workers[0]
+    hs = [hier.levels[1].op.handles[w].h.value, hier.levels[0].op.handles[w].h.value]
+    import ctypes as C
+    arr = (C.c_void_p * 2)(*hs)
+    d = _lib.MGDesc(1, 1, 1, 1.0, 1, 1)
+    out = C.c_void_p()
+    assert lib.pmg_hier_create(arr, 2, C.byref(d), C.byref(out)) == _lib.PMG_ERR_VALUE
+    d = _lib.MGDesc(1, 1, 1, 2.5, 1, 1)
+    arr = (C.c_void_p * 2)(*hs[::-1])
+    assert lib.pmg_hier_create(arr, 2, C.byref(d), C.byref(out)) == _lib.PMG_ERR_VALUE
+    # breakdown maps to BreakdownError: an indefinite "preconditioner" is not
+    # reachable through the API, so check the status mapping directly
+    with pytest.raises(pmg.BreakdownError):
+        _lib.check(_lib.PMG_ERR_BREAKDOWN, "pmg_pcg_solve")
