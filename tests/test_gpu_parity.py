@@ -628,3 +628,63 @@ def test_native_hierarchy_errors(pmg):
     # reachable through the API, so check the status mapping directly
     with pytest.raises(pmg.BreakdownError):
         _lib.check(_lib.PMG_ERR_BREAKDOWN, "pmg_pcg_solve")
+
+
+@pytest.mark.parametrize("solver", ["mg", "cg"])
+def test_c_host_program(pmg, tmp_path, solver):
+    """examples/c_solve.c: a plain C program builds the levels, uploads f,
+    solves and downloads u through include/pmg.h alone; its history and
+    solution equal the Python drop-in's bit for bit (same kernels)."""
+    import shutil
+    import subprocess
+    from paper_1307_2036_b200 import _lib, configs
+    from paper_1307_2036_b200.geometry import build_factors
+    from paper_1307_2036_b200.stencil import _part_factors
+    if shutil.which("gcc") is None:
+        pytest.skip("no C compiler")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "c_solve"
+    cuda = "/usr/local/cuda"
+    libdir = os.path.dirname(_lib.LIB_PATH)
+    subprocess.run(["gcc", "-O2", "-o", str(exe), os.path.join(root, "examples", "c_solve.c"),
+                    "-I", os.path.join(root, "include"), "-I", f"{cuda}/include",
+                    "-L", libdir, "-lpmg", "-L", f"{cuda}/lib64", "-lcudart",
+                    f"-Wl,-rpath,{libdir}:{cuda}/lib64"], check=True)
+    prob = configs.config(0)
+    cfg = prob.mg_config()
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
+    fg = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
+    maxiter = 50
+    with open(tmp_path / "in.bin", "wb") as fp:
+        np.array([prob.nx, prob.ny, prob.nz, len(hier.levels), 1, maxiter,
+                  0 if solver == "mg" else 1], dtype=np.int32).tofile(fp)
+        op0 = hier.fine.op
+        np.array([1e-5, op0.omega2, op0.vcoef]).tofile(fp)
+        for lev in hier.levels:
+            fac = build_factors(lev.grid)
+            for a in (fac.dr, fac.vprof, fac.volprof,
+                      *_part_factors(fac, 0, 0, lev.grid.nx, lev.grid.ny)):
+                np.ascontiguousarray(a, dtype=np.float64).tofile(fp)
+        fg.tofile(fp)
+    run = subprocess.run([str(exe), str(tmp_path / "in.bin"), str(tmp_path / "out.bin")],
+                         capture_output=True, text=True)
+    assert run.returncode == 0, run.stderr
+    raw = open(tmp_path / "out.bin", "rb").read()
+    iters, conv = np.frombuffer(raw[:8], dtype=np.int32)
+    hist = np.frombuffer(raw[8:8 + 8 * (iters + 1)])
+    u_c = np.frombuffer(raw[8 + 8 * (iters + 1):]).reshape(prob.nx, prob.ny, prob.nz)
+    f = pmg.scatter_owned(fg, hier.fine.layout)
+    if solver == "mg":
+        u, rep = pmg.mg_solve(f, hier, cfg)
+    else:
+        op = hier.fine.op
+        u, rep = pmg.pcg_solve(f, op, pmg.SSORPreconditioner(pmg.LineSmoother(op)), eps=1e-5,
+                               maxiter=maxiter)
+    assert conv == 1 and iters == rep.iterations
+    assert list(hist) == rep.residual_history
+    assert np.array_equal(u_c, pmg.gather_owned(u))
+    if solver == "mg":                    # and the reference's own history
+        g = load("config0_mg")
+        ref = np.asarray(g["history"])
+        assert len(ref) == len(hist)
+        assert np.max(np.abs(hist - ref) / ref[0]) <= 1e-10
