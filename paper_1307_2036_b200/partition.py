@@ -99,6 +99,14 @@ class Decomposition:
 
 
 def decompose(nx: int, workers: int) -> Decomposition:
+    """The reference's validating constructor (partition.py:71-73): a square
+    tiling of 4^p workers.  ``Decomposition`` itself also takes the 2 x 1 and
+    4 x 2 grids of BASELINE configs[3]."""
+    side = math.isqrt(workers) if workers >= 1 else 0
+    if side * side != workers or side & (side - 1):
+        raise ValueError(f"worker count must be 4^p (got {workers})")
+    if nx % side:
+        raise ValueError(f"nx={nx} not divisible by sqrt(workers)={side}")
     return Decomposition(nx, workers)
 
 
