@@ -106,6 +106,12 @@ int pmg_field_download(const pmg_level *lvl, const double *field, double *host,
  * (DistField.fill / copy, partition.py:128-137) */
 int pmg_fill(const pmg_level *lvl, double *field, double value, void *stream);
 int pmg_copy(const pmg_level *lvl, double *dst, const double *src, void *stream);
+/* copy a w x h block of columns (all k) between two parts, e.g. the
+ * coarse-level folding of collect / distribute (partition.py:194-240):
+ * dst (di + i, dj + j, k) = src (si + i, sj + j, k), local indices, the halo
+ * ring (-1, nx / ny) included; colours follow each part's global parity. */
+int pmg_copy_block(const pmg_level *src_lvl, const double *src, const pmg_level *dst_lvl,
+                   double *dst, int si, int sj, int di, int dj, int w, int h, void *stream);
 
 /* ---- operator: PanelOperator.apply / residual (stencil.py:127-165) --- */
 /* out = A u on owned cells; u halo must be current. */

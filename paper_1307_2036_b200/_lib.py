@@ -61,6 +61,7 @@ SIGNATURES = {
     "pmg_field_download": (_I, [_P, _P, _P, _P, _P]),
     "pmg_fill": (_I, [_P, _P, _D, _P]),
     "pmg_copy": (_I, [_P, _P, _P, _P]),
+    "pmg_copy_block": (_I, [_P, _P, _P, _P, _I, _I, _I, _I, _I, _I, _P]),
     "pmg_norm2": (_I, [_P, _P, _P, _P, _P]),
     "pmg_ssor_apply": (_I, [_P, _P, _P, _D, _I, _I, _P, _P, _P]),
     "pmg_hier_create": (_I, [C.POINTER(_P), _I, C.POINTER(MGDesc), C.POINTER(_P)]),

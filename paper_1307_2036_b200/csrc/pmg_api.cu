@@ -39,6 +39,8 @@ cudaError_t launch_unpack(const Lvl &, double *, int, const double *, int, cudaS
 cudaError_t launch_dot(const Lvl &, const double *, const double *, double *, int *, cudaStream_t);
 cudaError_t launch_axpy(long long, double, const double *, double *, cudaStream_t);
 cudaError_t launch_fill(long long, double, double *, cudaStream_t);
+cudaError_t launch_copy_block(const Lvl &, const double *, const Lvl &, double *, int, int, int, int,
+                              int, int, cudaStream_t);
 cudaError_t launch_xpby(long long, const double *, double, double *, cudaStream_t);
 cudaError_t launch_cg_direction(long long, const double *, const double *, const double *,
                                 double *, cudaStream_t);
@@ -493,6 +495,19 @@ int pmg_fill(const pmg_level *lv, double *field, double value, void *st) {
     } else {
         PMG_CUDA(launch_fill(n, value, field, (cudaStream_t)st), "fill");
     }
+    return PMG_OK;
+}
+
+int pmg_copy_block(const pmg_level *src_lvl, const double *src, const pmg_level *dst_lvl,
+                   double *dst, int si, int sj, int di, int dj, int w, int h, void *st) {
+    if (!src_lvl || !dst_lvl) return fail(PMG_ERR_VALUE, "null level handle");
+    const Lvl &S = src_lvl->L, &D = dst_lvl->L;
+    if (S.nz != D.nz) return fail(PMG_ERR_VALUE, "levels differ in nz");
+    if (w < 0 || h < 0 || si < -1 || sj < -1 || di < -1 || dj < -1 || si + w > S.nx + 1 ||
+        sj + h > S.ny + 1 || di + w > D.nx + 1 || dj + h > D.ny + 1)
+        return fail(PMG_ERR_VALUE, "block outside the parts (halo ring included)");
+    PMG_CUDA(launch_copy_block(S, src, D, dst, si, sj, di, dj, w, h, (cudaStream_t)st),
+             "copy_block");
     return PMG_OK;
 }
 

@@ -2561,6 +2561,21 @@ k_dot2(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// block copy between two parts' layouts (coarse-level folding,
+// partition.py:194-240): dst cell (di + i, dj + j, k) = src cell
+// (si + i, sj + j, k) for i < w, j < h, all k; halo indices allowed
+__global__ void k_copy_block(Lvl S, const double *__restrict__ src, Lvl D, double *__restrict__ dst,
+                             int si, int sj, int di, int dj, int w, int h) {
+    const long long n = (long long)w * h * S.nz;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(t % w);
+        const int j = (int)((t / w) % h);
+        const int k = (int)(t / ((long long)w * h));
+        dst[cell(D, di + i, dj + j, k)] = src[cell(S, si + i, sj + j, k)];
+    }
+}
+
 __global__ void k_fill(long long n, double v, double *__restrict__ y) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
          e += (long long)gridDim.x * blockDim.x)
@@ -3323,6 +3338,15 @@ cudaError_t launch_dot(const Lvl &L, const double *a, const double *b, double *p
         k_dot2<RPB, true><<<g, bs, 0, st>>>(L, a, b, partials, nch);
     else
         k_dot2<RPB, false><<<g, bs, 0, st>>>(L, a, b, partials, nch);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_copy_block(const Lvl &S, const double *src, const Lvl &D, double *dst, int si,
+                              int sj, int di, int dj, int w, int h, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const long long n = (long long)w * h * S.nz;
+    if (n <= 0) return cudaSuccess;
+    k_copy_block<<<stream_blocks(n), 256, 0, st>>>(S, src, D, dst, si, sj, di, dj, w, h);
     return cudaGetLastError();
 }
 

@@ -28,8 +28,9 @@ from ._lib import MGDesc, call, load
 from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
-from .partition import (Decomposition, DistField, LevelLayout, _dist, _stream, dist_norm,
-                        halo_exchange, reduce_parts, scalar_buffer, self_halo_flags)
+from .partition import (Decomposition, DistField, LevelLayout, _dist, _stream, collect,
+                        distribute, dist_norm, halo_exchange, reduce_parts, scalar_buffer,
+                        self_halo_flags)
 from .smoother import BLACK, RED, LineSmoother
 from .stencil import PanelOperator
 
@@ -122,6 +123,11 @@ class LevelHierarchy:
         return [lev.nx for lev in self.levels]
 
     def first_fold_level(self):
+        """Level number (finest = len(self)) below which workers fold
+        (multigrid.py:135-140)."""
+        for c, lev in enumerate(self.levels):
+            if lev.fold_layout is not None:
+                return len(self.levels) - c - 1
         return None
 
     def make_scratch(self):
@@ -207,12 +213,28 @@ def build_hierarchy(grid: PanelGrid, params: ModelParameters, cfg: MGConfig,
         raise ValueError(f"l_split must lie in [1, {nlev}]")
     levels = []
     g = grid
+    apx, apy = decomp.px, decomp.py
     for c in range(nlev):
-        layout = decomp.layout(g.nx)
+        # active workers: as many per direction as the level has columns,
+        # fewer below l_split (reference multigrid.py:188-199)
+        wx, wy = apx, apy
+        paper_level = nlev - c
+        if cfg.l_split is not None and paper_level <= cfg.l_split:
+            folds = cfg.l_split - paper_level + 1
+            wx, wy = max(1, decomp.px >> folds), max(1, decomp.py >> folds)
+        apx, apy = min(apx, wx, g.nx), min(apy, wy, g.ny)
+        layout = decomp.layout(g.nx, active=(apx, apy))
         op = PanelOperator(g, params, layout)
         levels.append(Level(g, layout, op, LineSmoother(op)))
         if c + 1 < nlev:
             g = g.coarsen()
+    for c in range(nlev - 1):
+        fine, coarse = levels[c], levels[c + 1]
+        fl, cl = fine.layout, coarse.layout
+        if (cl.px, cl.py) != (fl.px, fl.py):
+            if fl.px not in (cl.px, 2 * cl.px) or fl.py not in (cl.py, 2 * cl.py):
+                raise ValueError("worker folding must at most halve the active grid per level")
+            fine.fold_layout = decomp.layout(fine.nx, active=(cl.px, cl.py))
     return LevelHierarchy(levels, decomp, params)
 
 
@@ -225,22 +247,32 @@ def restrict(df: DistField, fine: Level, coarse: Level) -> DistField:
 
 def _restrict_into(df: DistField, fine: Level, coarse: Level, out: DistField,
                    weight: float) -> DistField:
+    """coarse f = weight x children sum; a folding level first collects the
+    fine parts onto the coarse level's workers (multigrid.py:216-223)."""
+    if fine.fold_layout is not None:
+        df = collect(df, fine.fold_layout)
     st = _stream()
     for w, ff in df.parts.items():
-        call("pmg_restrict", fine.op.handles[w].h, coarse.op.handles[w].h, ff.ptr,
-             out.parts[w].ptr, float(weight), st)
+        call("pmg_restrict", ff.geom.h, out.parts[w].geom.h, ff.ptr, out.parts[w].ptr,
+             float(weight), st)
     return out
 
 
 def prolong(df: DistField, coarse: Level, fine: Level, out: DistField | None = None) -> DistField:
     """Bilinear cell-centre interpolation (multigrid.py:249-268); the
-    coarse halo (incl. corners) must be current."""
+    coarse halo (incl. corners) must be current.  Across a fold the result
+    is staged on the folded workers and distributed."""
+    st = _stream()
+    if fine.fold_layout is not None:
+        staged = DistField.zeros(fine.fold_layout, df.nz)
+        for w, cf in df.parts.items():
+            call("pmg_prolong", staged.parts[w].geom.h, cf.geom.h, cf.ptr,
+                 staged.parts[w].ptr, 0, st)
+        return distribute(staged, fine.layout, out=out)
     if out is None:
         out = DistField.zeros(fine.layout, df.nz)
-    st = _stream()
     for w, cf in df.parts.items():
-        call("pmg_prolong", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
-             out.parts[w].ptr, 0, st)
+        call("pmg_prolong", out.parts[w].geom.h, cf.geom.h, cf.ptr, out.parts[w].ptr, 0, st)
     return out
 
 
@@ -314,7 +346,8 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
         # ``first``: the finest iterate is zero on entry but was not filled
         _pre_smooth(lev, s, cfg.nu_pre, cfg.rho, lean and (c > 0 or first))
         coarse = hier.levels[c + 1]
-        if cfg.fused:
+        fold = lev.fold_layout is not None
+        if cfg.fused and not fold:
             _residual_restrict(lev, coarse, s.f, s.u, scratch[c + 1].f)
         else:
             lev.op.residual(s.f, s.u, out=s.r)
@@ -323,7 +356,11 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
             scratch[c + 1].u.fill(0.0)
         v_cycle(hier, cfg, scratch, c + 1)
         post = cfg.nu_post
-        if cfg.fused and lean and post >= 1 and FUSE_PROLONG and _pro_ok(lev):
+        if fold:
+            corr = prolong(scratch[c + 1].u, coarse, lev, out=s.r)
+            _add_owned(s.u, corr)
+            halo_exchange(s.u)
+        elif cfg.fused and lean and post >= 1 and FUSE_PROLONG and _pro_ok(lev):
             # correction fused into the first red half-sweep (the black
             # values it corrects are read only there, then overwritten)
             _sweep_prolong(lev, coarse, scratch[c + 1].u, s)

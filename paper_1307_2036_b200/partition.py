@@ -84,11 +84,22 @@ class Decomposition:
         self.distribute_calls = 0
         self._layouts = {}
 
-    def layout(self, nx_level: int, pside: int | None = None) -> "LevelLayout":
+    def layout(self, nx_level: int, pside: int | None = None, active=None) -> "LevelLayout":
+        """Layout of a level with ``nx_level`` columns (and the decomposition's
+        aspect ratio).  By default as many workers stay active per direction
+        as the level has columns (reference partition.py:60-68); ``pside``
+        (square, reference API) or ``active`` = (apx, apy) choose fewer: the
+        coarse-level folding of the standard policy."""
         ny_level = nx_level * self.ny // self.nx
-        key = (nx_level, ny_level)
+        if active is None:
+            if pside is not None:
+                active = (pside, pside)
+            else:
+                active = (min(self.px, nx_level), min(self.py, ny_level))
+        apx, apy = active
+        key = (nx_level, ny_level, apx, apy)
         if key not in self._layouts:
-            self._layouts[key] = LevelLayout(self, nx_level, ny_level)
+            self._layouts[key] = LevelLayout(self, nx_level, ny_level, apx, apy)
         return self._layouts[key]
 
     def bind_periodic(self, periodic: bool) -> None:
@@ -112,27 +123,39 @@ def decompose(nx: int, workers: int) -> Decomposition:
 
 class LevelLayout:
     """Owned rectangles of one grid level (reference ``LevelLayout``,
-    partition.py:76-118).  Worker id = ai * py + aj."""
+    partition.py:76-118).  Worker ids index the full px x py grid
+    (id = wi * py + wj); on a folded level only an apx x apy sub-grid is
+    active, every (px / apx) x (py / apy) group represented by its
+    lowest-indexed worker."""
 
-    def __init__(self, decomp: Decomposition, nx: int, ny: int):
-        if nx % decomp.px or ny % decomp.py:
-            raise ValueError(
-                f"level {nx} x {ny} has fewer columns than the {decomp.px} x {decomp.py} "
-                "worker grid (coarse-level folding is not supported; use fewer levels)")
+    def __init__(self, decomp: Decomposition, nx: int, ny: int, apx: int | None = None,
+                 apy: int | None = None):
+        apx = decomp.px if apx is None else apx
+        apy = decomp.py if apy is None else apy
+        for a, p in ((apx, decomp.px), (apy, decomp.py)):
+            if a < 1 or a & (a - 1) or p % a:
+                raise ValueError("active side must be a power of two dividing the worker grid")
+        if nx % apx or ny % apy:
+            raise ValueError(f"level {nx} x {ny} not divisible by the {apx} x {apy} active "
+                             "worker grid")
         self.decomp = decomp
         self.nx, self.ny = nx, ny
-        self.px, self.py = decomp.px, decomp.py
-        self.mx, self.my = nx // decomp.px, ny // decomp.py
-        self.pside = decomp.pside
+        self.px, self.py = apx, apy
+        self.gx, self.gy = decomp.px // apx, decomp.py // apy
+        self.mx, self.my = nx // apx, ny // apy
+        self.pside = apx if apx == apy else None
         self.mloc = self.mx
-        self.group = 1
-        self.workers = [ai * self.py + aj for ai in range(self.px) for aj in range(self.py)]
+        self.group = self.gx
+        self.workers = [self.worker_at(ai, aj) for ai in range(apx) for aj in range(apy)]
         self.halo_count = 0
         self._geom = {}
         d = _dist()
         if d is not None:
             if d.get_world_size() != decomp.workers:
                 raise ValueError("one worker per rank: world size must equal the worker count")
+            if len(self.workers) != decomp.workers:
+                raise ValueError("coarse-level folding across ranks is not supported "
+                                 "(use the shallow policy or fewer levels)")
             self.local_workers = [d.get_rank()]
         else:
             self.local_workers = list(self.workers)
@@ -142,10 +165,13 @@ class LevelLayout:
         return bool(self.decomp.periodic)
 
     def coords(self, worker: int):
-        return divmod(worker, self.py)
+        wi, wj = divmod(worker, self.decomp.py)
+        if wi % self.gx or wj % self.gy:
+            raise ValueError(f"worker {worker} not active on this layout")
+        return wi // self.gx, wj // self.gy
 
     def worker_at(self, ai: int, aj: int) -> int:
-        return ai * self.py + aj
+        return (ai * self.gx) * self.decomp.py + aj * self.gy
 
     def origin(self, worker: int):
         ai, aj = self.coords(worker)
@@ -463,6 +489,50 @@ def _phase_dist(df: DistField, faces, st, dist) -> None:
 # ---------------------------------------------------------------------------
 # global <-> parts (partition.py:243-264)
 # ---------------------------------------------------------------------------
+def collect(df: DistField, to_layout: LevelLayout) -> DistField:
+    """Fold each group of parts onto its lowest-indexed worker (reference
+    partition.py:194-218): the owned blocks are copied into one part of
+    ``to_layout`` (same nx, fewer active workers); halos are left zero."""
+    lay = df.layout
+    fx, fy = lay.px // to_layout.px, lay.py // to_layout.py
+    if (to_layout.nx != lay.nx or to_layout.ny != lay.ny or fx * to_layout.px != lay.px
+            or fy * to_layout.py != lay.py or fx * fy < 2):
+        raise ValueError("collect target must fold the active grid at the same level size")
+    out = DistField.zeros(to_layout, df.nz)
+    st = _stream()
+    for pw, big in out.parts.items():
+        ai, aj = to_layout.coords(pw)
+        for di in range(fx):
+            for dj in range(fy):
+                ch = df.parts[lay.worker_at(fx * ai + di, fy * aj + dj)]
+                call("pmg_copy_block", ch.geom.h, ch.ptr, big.geom.h, big.ptr, 0, 0,
+                     di * lay.mx, dj * lay.my, lay.mx, lay.my, st)
+    lay.decomp.collect_calls += 1
+    return out
+
+
+def distribute(df: DistField, to_layout: LevelLayout, out: DistField | None = None) -> DistField:
+    """Inverse of ``collect`` (reference partition.py:221-240): every part
+    of ``to_layout`` receives its owned block plus the surrounding one-cell
+    ring from the folded part."""
+    lay = df.layout
+    fx, fy = to_layout.px // lay.px, to_layout.py // lay.py
+    if (to_layout.nx != lay.nx or to_layout.ny != lay.ny or fx * lay.px != to_layout.px
+            or fy * lay.py != to_layout.py or fx * fy < 2):
+        raise ValueError("distribute target must unfold the active grid at the same level size")
+    if out is None:
+        out = DistField.zeros(to_layout, df.nz)
+    st = _stream()
+    m, n = to_layout.mx, to_layout.my
+    for cw, ch in out.parts.items():
+        ai, aj = to_layout.coords(cw)
+        big = df.parts[lay.worker_at(ai // fx, aj // fy)]
+        call("pmg_copy_block", big.geom.h, big.ptr, ch.geom.h, ch.ptr, (ai % fx) * m - 1,
+             (aj % fy) * n - 1, -1, -1, m + 2, n + 2, st)
+    lay.decomp.distribute_calls += 1
+    return out
+
+
 def scatter_owned(arr, layout: LevelLayout) -> DistField:
     """Split a global (nx, ny, nz) array (numpy, or torch on host/device)
     over the layout's local parts; halos start at zero."""

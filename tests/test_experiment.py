@@ -123,13 +123,13 @@ def test_tables_equal_reference(gold, tmp_path):
 
 @pytest.mark.gpu
 def test_manufactured_solution_is_discrete_exact():
-    """tests/test_bench_cli.py:23-35 on the device (standard policy: down
-    to one column)."""
+    """tests/test_bench_cli.py:23-47 on the device (standard policy: down to
+    one column; with 4 parts the coarse levels fold onto one worker)."""
     import paper_1307_2036_b200 as pmg
     params = pmg.derive_parameters(64, 16, 2400.0)
     grid = pmg.panel_grid(64, 16)
     f, uex = pmg.manufactured_rhs(grid, params)
-    for workers in (1,):
+    for workers in (1, 4):
         cfg = pmg.MGConfig(eps=1e-10, maxiter=50, deterministic=workers > 1)
         hier = pmg.build_hierarchy(grid, params, cfg, pmg.Decomposition(64, workers))
         u, rep = pmg.mg_solve(pmg.scatter_owned(f.owned, hier.fine.layout), hier, cfg)

@@ -688,3 +688,47 @@ def test_c_host_program(pmg, tmp_path, solver):
         ref = np.asarray(g["history"])
         assert len(ref) == len(hist)
         assert np.max(np.abs(hist - ref) / ref[0]) <= 1e-10
+
+
+@pytest.mark.parametrize("workers", [4, 16])
+@pytest.mark.parametrize("l_split", [None, 3])
+def test_folding_partition_invariance(pmg, workers, l_split):
+    """Standard policy (down to one global column) on P parts: the coarse
+    levels fold onto fewer workers through collect / distribute
+    (partition.py:194-240); histories equal P = 1 to 1e-10
+    (tests/test_partition.py:122-154), fold counters as the reference."""
+    nx, nz = 32, 8
+    grid = pmg.panel_grid(nx, nz, flat_mode=True)
+    params = pmg.toy_parameters(nx, nz, 6.7e-4, 3.3e-2)
+    fg = uni((nx, nx, nz), 9)
+    hist = {}
+    for p in (1, workers):
+        cfg = pmg.MGConfig(policy="standard", l_split=l_split, graph=False)
+        hier = pmg.build_hierarchy(grid, params, cfg, pmg.Decomposition(nx, p))
+        if p > 1:
+            assert hier.first_fold_level() is not None
+        f = pmg.scatter_owned(fg, hier.fine.layout)
+        hier.reset_counters()
+        _, rep = pmg.mg_solve(f, hier, cfg)
+        hist[p] = np.array(rep.residual_history)
+        if p > 1:
+            folds = sum(lev.fold_layout is not None for lev in hier.levels)
+            assert hier.decomp.collect_calls == folds * rep.iterations
+            assert hier.decomp.distribute_calls == folds * rep.iterations
+    assert len(hist[1]) == len(hist[workers])
+    assert np.max(np.abs(hist[workers] - hist[1]) / hist[1][0]) <= 1e-10
+
+
+def test_collect_distribute_round_trip(pmg):
+    nx, nz = 16, 3
+    dec = pmg.Decomposition(nx, 16)
+    lay = dec.layout(nx)
+    fold = dec.layout(nx, active=(2, 2))
+    a = uni((nx, nx, nz), 4)
+    df = pmg.scatter_owned(a, lay)
+    pmg.halo_exchange(df)
+    from paper_1307_2036_b200.partition import collect, distribute
+    big = collect(df, fold)
+    assert np.array_equal(pmg.gather_owned(big), a)
+    back = distribute(big, lay)
+    assert np.array_equal(pmg.gather_owned(back), a)
