@@ -28,6 +28,7 @@ cudaError_t launch_invd(const Lvl &, double *, cudaStream_t);
 cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, double,
                             cudaStream_t);
 bool half_sweep_pro_ok(const Lvl &F);
+void setup_kernel_attributes();
 cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const double *f,
                                   const double *cu, int color, cudaStream_t st);
 cudaError_t launch_prolong(const Lvl &, const Lvl &, const double *, double *, int, int,
@@ -134,6 +135,7 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
         return fail(PMG_ERR_VALUE, "level needs nx, ny, nz >= 1");
     if (!d->dr || !d->vprof || !d->volprof || !d->wx || !d->wy || !d->av || !d->vh || !d->sumw)
         return fail(PMG_ERR_VALUE, "missing factor array");
+    setup_kernel_attributes();
     const int nx = d->nx, ny = d->ny, nz = d->nz;
     auto *lv = new pmg_level();
     Lvl &L = lv->L;

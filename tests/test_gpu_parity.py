@@ -732,3 +732,35 @@ def test_collect_distribute_round_trip(pmg):
     assert np.array_equal(pmg.gather_owned(big), a)
     back = distribute(big, lay)
     assert np.array_equal(pmg.gather_owned(back), a)
+
+
+@pytest.mark.parametrize("nx,nz,workers", [(32, 32, 1), (64, 64, 1), (64, 128, 1),
+                                           (128, 128, 4), (256, 32, 1)])
+def test_staged_smoother_vs_exact(pmg, nx, nz, workers):
+    """The fast half-sweep at nz multiples of 16 and parts of >= 32 columns
+    (k_half_sweep_seg with compile-time plane strides; k_half_sweep_cp when
+    PMG_CP=1) against the exact sequential solver, every mode of
+    LineSmoother.half_sweep (rho, zero start, no neighbours, post scale) and
+    ssor_apply: 1e-12 (tests/test_smoother.py:48)."""
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    op = pmg.PanelOperator(grid, params, pmg.Decomposition(nx, workers).layout(nx))
+    sm = pmg.LineSmoother(op)
+    ug, fg = uni((nx, nx, nz), 21), uni((nx, nx, nz), 22)
+    f = pmg.scatter_owned(fg, op.layout)
+    G = pmg.gather_owned
+    runs = {}
+    for exact in (True, False):
+        with pmg.exact_smoother(exact):
+            out = []
+            for color, rho, zs, nb, ps in ((0, 1.0, False, False, 1.0), (1, 1.0, False, False, 1.0),
+                                           (0, 1.4, False, False, 1.0), (0, 1.0, True, True, 1.0),
+                                           (1, 1.3, True, False, 0.7)):
+                u = pmg.scatter_owned(ug, op.layout)
+                pmg.halo_exchange(u)
+                sm.half_sweep(u, f, color, rho, zs, nb, ps)
+                out.append(G(u))
+            out.append(G(sm.ssor_apply(f, 1.0)))
+            runs[exact] = out
+    for a, b in zip(runs[True], runs[False]):
+        assert _close(b, a, 1e-12)
