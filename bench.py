@@ -121,11 +121,19 @@ def dist_setup(n):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n:
         raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    # PMG_DIST_BACKEND=gloo PMG_DIST_DEVICE=0: every rank on one device with
+    # host-staged halos -- a functional check of the multi-rank path on a
+    # one-GPU box (no kernel waits on another rank); timings meaningless
+    dev = int(os.environ.get("PMG_DIST_DEVICE", local))
+    backend = os.environ.get("PMG_DIST_BACKEND", "nccl")
     if torch.cuda.is_available():
-        torch.cuda.set_device(local)
+        torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    return world, rank, local
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    return world, rank, dev
 
 
 def barrier(world):
@@ -139,7 +147,8 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -478,7 +478,18 @@ def _phase_dist(df: DistField, faces, st, dist) -> None:
         recvbufs[rf] = _FaceBuffers.get(f.geom, "recv", rf, w)
         if ps is not None:
             call("pmg_pack_face", f.geom.h, f.ptr, sf, _ptr(sendbufs[sf]), st)
-    how = exchange_messages(dist, w, plan, sendbufs, recvbufs)
+    if dist.get_backend() == "nccl" or not f.data.is_cuda:
+        how = exchange_messages(dist, w, plan, sendbufs, recvbufs)
+    else:
+        # host-staged exchange for CPU backends (gloo): device faces -> host,
+        # send/recv, host -> device (the NCCL path moves device buffers)
+        torch.cuda.current_stream().synchronize()
+        hs = {k: v.cpu() for k, v in sendbufs.items()}
+        hr = {k: torch.empty(v.shape, dtype=v.dtype) for k, v in recvbufs.items()}
+        how = exchange_messages(dist, w, plan, hs, hr)
+        for k, v in hr.items():
+            if how.get(k) in ("buf", "self"):
+                recvbufs[k].copy_(v)
     for face, kind in how.items():
         if kind == "mirror":
             call("pmg_unpack_face", f.geom.h, f.ptr, face, None, 1, st)
