@@ -626,6 +626,118 @@ k_residual_restrict_v(Lvl F, Lvl C, const double *__restrict__ u, const double *
     }
 }
 
+// Residual + children-sum restriction, one thread per coarse column pair
+// (uniform coefficients, fine nx a multiple of 4).  Thread (J, m) owns the
+// fine window i = 4m .. 4m+3 of rows 2J, 2J+1: per level it loads both
+// colours of the two centre rows as double2 (each colour's pair is the
+// other colour's W/E neighbours) plus the two outer W/E scalars, both
+// colours of rows 2J-1 and 2J+2 (S/N) and f: 12 double2 + 4 scalars for 8
+// residuals, no shared-memory reduction, no barriers.  Vertical
+// neighbours slide through registers.  Same cell arithmetic (cell_res,
+// stencil.py:140-164) and children order (multigrid.py:210-212) as
+// k_residual_restrict_v: bit-identical results.
+template <int MINB = 2, bool NORM = false>
+__global__ void __launch_bounds__(128, MINB)
+k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
+                      double *__restrict__ cf, int mb32, int ntiles, int kcs,
+                      double *__restrict__ partials) {
+    // NORM: the convergence residual ||f - A u||^2 instead of the
+    // restriction (C describes the row-pair / column-quad grid only)
+    double acc2 = 0.0;
+    __shared__ double s_drw[256], s_a[257], s_b[257], s_c[257];
+    const Tabs T{s_drw, s_a, s_b, s_a, s_b, s_c};
+    load_tabs(F, T);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int nwarp = gridDim.x * (blockDim.x >> 5);
+    const int nz = F.nz;
+    const long long pl = F.plane;
+    const int nkc = (nz + kcs - 1) / kcs;
+    const int npair = C.nx >> 1;
+    const Col2 W = col2_coeffs<true>(F, 0, 0);
+    for (int wt = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wt < ntiles; wt += nwarp) {
+        const int kcI = wt % nkc;
+        const int t2 = wt / nkc;
+        const int J = t2 / mb32;
+        const int m0 = (t2 - J * mb32) * 32;
+        const bool act = m0 + lane < npair;
+        const int m = act ? m0 + lane : npair - 1;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const int ja = 2 * J, jb = ja + 1;
+        const int cAa = (ja + F.par) & 1, cAb = cAa ^ 1;     // colour at even i, rows ja / jb
+        // row bases at level 0 (colour at even i first, then odd i)
+        const long long a_e = at(F, cAa, 0, ja, 2 * m), a_o = at(F, cAa ^ 1, 0, ja, 2 * m);
+        const long long b_e = at(F, cAb, 0, jb, 2 * m), b_o = at(F, cAb ^ 1, 0, jb, 2 * m);
+        const long long al = at(F, cAa ^ 1, 0, ja, 2 * m - 1), ar = at(F, cAa, 0, ja, 2 * m + 2);
+        const long long bl = at(F, cAb ^ 1, 0, jb, 2 * m - 1), br = at(F, cAb, 0, jb, 2 * m + 2);
+        // row ja-1: even-i colour = cAb (parity flips with j); row jb+1: cAa
+        const long long s_e = at(F, cAb, 0, ja - 1, 2 * m), s_o = at(F, cAa, 0, ja - 1, 2 * m);
+        const long long n_e = at(F, cAa, 0, jb + 1, 2 * m), n_o = at(F, cAb, 0, jb + 1, 2 * m);
+        const int cc0 = (2 * m + J + C.par) & 1;
+        const long long q0 = at(C, cc0, 0, J, m), q1 = at(C, cc0 ^ 1, 0, J, m);
+        // vertical window of the centre values: [0] k-1, [1] k, [2] k+1
+        D2 ce[3], co[3], de[3], dd[3];   // row ja even / odd i, row jb even / odd i
+        {
+            const long long km = (long long)max(kbeg - 1, 0) * pl, k0 = (long long)kbeg * pl;
+            ce[0] = ld2(u + a_e + km); co[0] = ld2(u + a_o + km);
+            de[0] = ld2(u + b_e + km); dd[0] = ld2(u + b_o + km);
+            ce[1] = ld2(u + a_e + k0); co[1] = ld2(u + a_o + k0);
+            de[1] = ld2(u + b_e + k0); dd[1] = ld2(u + b_o + k0);
+        }
+        for (int k = kbeg; k < kend; ++k) {
+            const long long ko = (long long)k * pl;
+            const long long kp = (long long)min(k + 1, nz - 1) * pl;
+            ce[2] = ld2(u + a_e + kp); co[2] = ld2(u + a_o + kp);
+            de[2] = ld2(u + b_e + kp); dd[2] = ld2(u + b_o + kp);
+            const double xal = u[al + ko], xar = u[ar + ko], xbl = u[bl + ko], xbr = u[br + ko];
+            const D2 se = ld2(u + s_e + ko), so = ld2(u + s_o + ko);
+            const D2 ne = ld2(u + n_e + ko), no = ld2(u + n_o + ko);
+            const D2 fae = ld2(f + a_e + ko), fao = ld2(f + a_o + ko);
+            const D2 fbe = ld2(f + b_e + ko), fbo = ld2(f + b_o + ko);
+            // row ja: cells 4m (ce.x), 4m+1 (co.x), 4m+2 (ce.y), 4m+3 (co.y)
+            const double ra0 = cell_res<1, 1, true>(F, T, W, k, xal, co[1].x, se.x, de[1].x,
+                                                    ce[0].x, ce[1].x, ce[2].x, fae.x);
+            const double ra1 = cell_res<1, 1, true>(F, T, W, k, ce[1].x, ce[1].y, so.x, dd[1].x,
+                                                    co[0].x, co[1].x, co[2].x, fao.x);
+            const double ra2 = cell_res<1, 1, true>(F, T, W, k, co[1].x, co[1].y, se.y, de[1].y,
+                                                    ce[0].y, ce[1].y, ce[2].y, fae.y);
+            const double ra3 = cell_res<1, 1, true>(F, T, W, k, ce[1].y, xar, so.y, dd[1].y,
+                                                    co[0].y, co[1].y, co[2].y, fao.y);
+            // row jb: S neighbours are row ja, N neighbours row jb+1
+            const double rb0 = cell_res<1, 1, true>(F, T, W, k, xbl, dd[1].x, ce[1].x, ne.x,
+                                                    de[0].x, de[1].x, de[2].x, fbe.x);
+            const double rb1 = cell_res<1, 1, true>(F, T, W, k, de[1].x, de[1].y, co[1].x, no.x,
+                                                    dd[0].x, dd[1].x, dd[2].x, fbo.x);
+            const double rb2 = cell_res<1, 1, true>(F, T, W, k, dd[1].x, dd[1].y, ce[1].y, ne.y,
+                                                    de[0].y, de[1].y, de[2].y, fbe.y);
+            const double rb3 = cell_res<1, 1, true>(F, T, W, k, de[1].y, xbr, co[1].y, no.y,
+                                                    dd[0].y, dd[1].y, dd[2].y, fbo.y);
+            if (NORM) {
+                if (act) {
+                    acc2 += ra0 * ra0; acc2 += ra1 * ra1; acc2 += ra2 * ra2; acc2 += ra3 * ra3;
+                    acc2 += rb0 * rb0; acc2 += rb1 * rb1; acc2 += rb2 * rb2; acc2 += rb3 * rb3;
+                }
+            } else if (act) {
+                const long long cko = (long long)k * C.plane;
+                double a = ra0 + ra1;
+                a = a + rb0;
+                a = a + rb1;
+                double b = ra2 + ra3;
+                b = b + rb2;
+                b = b + rb3;
+                cf[q0 + cko] = a;
+                cf[q1 + cko] = b;
+            }
+            ce[0] = ce[1]; co[0] = co[1]; de[0] = de[1]; dd[0] = dd[1];
+            ce[1] = ce[2]; co[1] = co[2]; de[1] = de[2]; dd[1] = dd[2];
+        }
+    }
+    if (NORM) {
+        const double s2 = block_sum(acc2);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s2;
+    }
+}
+
 // Warp-level residual + restriction (uniform): no CTA barriers.  A warp
 // owns 16 coarse columns of coarse row J: lane = q*8 + m, quarter q = (fine
 // row offset rr, colour c), m = column pair.  The four children of a coarse
@@ -2386,7 +2498,6 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
         const double wyp = L.wy[(long long)(j + 1) * L.nx + i];
         const double cv = L.vcoef * L.av[q2];
         double r[SEG], vi[SEG], pq[SEG];
-#pragma unroll
         constexpr int B = SEG < 4 ? SEG : 4;
 #pragma unroll
         for (int b8 = 0; b8 < SEG; b8 += B) {
@@ -2953,6 +3064,29 @@ static int apply_variant() {
 
 cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double *out, int mode,
                          double *partials, int *nparts, cudaStream_t st) {
+    if (mode == 1 && partials && !out && L.uniform && L.nz <= 256 && L.nx % 4 == 0 &&
+        L.ny % 2 == 0 && L.nx >= 4 && getenv("PMG_NORM_Q")) {
+        // norm-only residual with the column-quad kernel (k_residual_restrict_q):
+        // opt-in, measured 444 vs 428 us (k_apply_v) at configs[1]'s fine level
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        Lvl Cq = L;                         // the row-pair / quad grid: nx/2 x ny/2
+        Cq.nx = L.nx / 2;
+        Cq.ny = L.ny / 2;
+        Cq.par = 0;
+        const int mb32 = ((Cq.nx >> 1) + 31) / 32;
+        auto kern = k_residual_restrict_q<2, true>;
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
+        const int capw = sm_count() * (occ > 0 ? occ : 1) * 4;
+        int kcs = L.nz;
+        while (kcs > 8 && (long long)mb32 * Cq.ny * ((L.nz + kcs - 1) / kcs) < 2LL * capw) kcs >>= 1;
+        const int ntiles = mb32 * Cq.ny * ((L.nz + kcs - 1) / kcs);
+        int grid = (ntiles + 3) / 4;
+        if (grid > capw / 4) grid = capw / 4;
+        *nparts = grid;
+        kern<<<grid, 128, 0, st>>>(L, Cq, u, f, nullptr, mb32, ntiles, kcs, partials);
+        return cudaGetLastError();
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
@@ -3068,6 +3202,23 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
         int grid = (ntiles + 7) / 8;
         if (grid > capw / 8) grid = capw / 8;
         k_residual_restrict_w<KB><<<grid, 256, 0, st>>>(F, C, u, f, cf, hb16, ntiles, kcs);
+        return cudaGetLastError();
+    }
+    if (F.uniform && F.nz <= 256 && F.nx % 4 == 0 && C.nx >= 2 && !getenv("PMG_RR_NOQ")) {
+        const int mb32 = ((C.nx >> 1) + 31) / 32;
+        auto runq = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
+            const int capw = sm_count() * (occ > 0 ? occ : 1) * 4;
+            int kcs = F.nz;
+            while (kcs > 8 && (long long)mb32 * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * capw)
+                kcs >>= 1;
+            const int ntiles = mb32 * C.ny * ((F.nz + kcs - 1) / kcs);
+            int grid = (ntiles + 3) / 4;
+            if (grid > capw / 4) grid = capw / 4;
+            kern<<<grid, 128, 0, st>>>(F, C, u, f, cf, mb32, ntiles, kcs, nullptr);
+        };
+        runq(k_residual_restrict_q<2>);
         return cudaGetLastError();
     }
     if (F.nz <= 256 && getenv("PMG_RR_V0") == nullptr) {

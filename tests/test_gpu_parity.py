@@ -468,6 +468,9 @@ class _FakeDist:
         self.local = threading.local()
         self.isend, self.irecv = "send", "recv"
 
+    def get_backend(self):          # device buffers move directly, as with NCCL
+        return "nccl"
+
     class P2POp:
         def __init__(self, op, tensor, peer, tag=0):
             self.op, self.tensor, self.peer, self.tag = op, tensor, peer, tag
