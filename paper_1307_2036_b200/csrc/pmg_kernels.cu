@@ -136,217 +136,6 @@ k_apply(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Batched variant of k_apply: each thread owns KB consecutive levels of
-// one column and issues every load of its chunk before any arithmetic, so
-// (KB+2) + 5 KB independent 8-byte loads per thread are in flight (the
-// sequential-k version left the SM latency-bound at ~30% of HBM peak).
-// Same arithmetic, same order.
-// ---------------------------------------------------------------------------
-// Column walker shared by the batched stencil kernels: residual / A u of
-// KB consecutive levels of one column, every load of the batch issued
-// before any arithmetic.  Tables (drw, diag, band) come from shared memory.
-template <bool UNI, int MODE, int KB>
-__device__ __forceinline__ void stencil_batch(
-    const Lvl &L, const double *__restrict__ u, const double *__restrict__ f, int k0,
-    long long pc, long long pW, long long pE, long long pS, long long pN, double wxm,
-    double wxp, double wym, double wyp, double cv, double vhc, double osw,
-    const double *tdrw, const double *tdiag, const double *tband, double (&res)[KB],
-    double (&uown)[KB]) {
-    const int nz = L.nz;
-    const long long pl = L.plane;
-    double uc[KB + 2], vw[KB], ve[KB], vs[KB], vn[KB], vf[KB];
-    // every load unpredicated: levels beyond the column are clamped to a
-    // valid address and their values never used (predicated loads split the
-    // batch into separately waited groups)
-    uc[0] = u[pc - ((k0 > 0) ? pl : 0)];
-#pragma unroll
-    for (int t = 0; t < KB; ++t) {
-        const long long ko = (long long)min(t, nz - 1 - k0) * pl;
-        uc[t + 1] = u[pc + ko];
-        vw[t] = u[pW + ko];
-        ve[t] = u[pE + ko];
-        vs[t] = u[pS + ko];
-        vn[t] = u[pN + ko];
-        if (MODE == 1) vf[t] = f[pc + ko];
-    }
-    uc[KB + 1] = u[pc + (long long)min(KB, nz - 1 - k0) * pl];
-#pragma unroll
-    for (int t = 0; t < KB; ++t) {
-        const int k = k0 + t;
-        uown[t] = uc[t + 1];
-        if (k < nz) {
-            double acc = wxm * vw[t];
-            acc = acc + wxp * ve[t];
-            acc = acc + wym * vs[t];
-            acc = acc + wyp * vn[t];
-            acc = acc * tdrw[k];
-            double d;
-            if (UNI) {
-                d = tdiag[k];
-            } else {
-                d = vhc * L.volprof[k];
-                d = d + osw * L.dr[k];
-                d = d + cv * (L.vprof[k] + L.vprof[k + 1]);
-            }
-            double r = d * uc[t + 1] - acc;
-            if (k >= 1) r = r - (UNI ? tband[k] : cv * L.vprof[k]) * uc[t];
-            if (k + 1 < nz) r = r - (UNI ? tband[k + 1] : cv * L.vprof[k + 1]) * uc[t + 2];
-            if (MODE == 1) r = vf[t] - r;
-            res[t] = r;
-        } else {
-            res[t] = 0.0;
-        }
-    }
-}
-
-__device__ __forceinline__ void load_stencil_tables(const Lvl &L, double *tdrw, double *tdiag,
-                                                    double *tband) {
-    for (int t = threadIdx.x + blockDim.x * threadIdx.y; t <= L.nz;
-         t += blockDim.x * blockDim.y) {
-        if (t < L.nz) tdrw[t] = L.drw[t];
-        if (L.uniform) {
-            if (t < L.nz) tdiag[t] = L.diag1[t];
-            tband[t] = L.band1[t];
-        }
-    }
-}
-
-template <bool UNI>
-__device__ __forceinline__ void column_coeffs(const Lvl &L, int i, int j, double &wxm, double &wxp,
-                                              double &wym, double &wyp, double &cv, double &vhc,
-                                              double &osw) {
-    if (UNI) {
-        wxm = wxp = L.wx0;
-        wym = wyp = L.wy0;
-        cv = L.csub0;
-        vhc = osw = 0.0;
-    } else {
-        wxm = L.wx[(long long)j * (L.nx + 1) + i];
-        wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
-        wym = L.wy[(long long)j * L.nx + i];
-        wyp = L.wy[(long long)(j + 1) * L.nx + i];
-        cv = L.vcoef * L.av[(long long)j * L.nx + i];
-        vhc = L.vh[(long long)j * L.nx + i];
-        osw = L.omega2 * L.sumw[(long long)j * L.nx + i];
-    }
-}
-
-// Persistent batched apply / residual: tile = 32 columns x AP_TY rows x 2
-// colours; each thread walks its whole column in batches of KB levels.
-template <bool UNI, int MODE, bool NORM, int KB>
-__global__ void __launch_bounds__(32 * 2 * AP_TY, 3)
-k_apply_b(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
-          double *__restrict__ out, double *__restrict__ partials, int hx, int jy, int ntiles,
-          int kcs) {
-    __shared__ double tdrw[256], tdiag[256], tband[257];
-    load_stencil_tables(L, tdrw, tdiag, tband);
-    __syncthreads();
-    const int lane = threadIdx.x;
-    const int c = threadIdx.y & 1;
-    const int nz = L.nz;
-    const int o = c ^ 1;
-    const long long pl = L.plane;
-    double acc2 = 0.0;
-    // tile = (h block, row block, k chunk of kcs levels); kcs = nz on big
-    // levels (one walk per column), smaller on coarse levels to fill the GPU
-    const int nkc = (nz + kcs - 1) / kcs;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int kcI = tile % nkc;
-        const int t2 = tile / nkc;
-        const int jb = t2 / hx;
-        const int hb = t2 - jb * hx;
-        const int j = jb * AP_TY + (threadIdx.y >> 1);
-        const int h = hb * 32 + lane;
-        const int i = 2 * h + ((j + L.par + c) & 1);
-        if (j >= L.ny || i >= L.nx) continue;
-        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
-        long long pc = at(L, c, kbeg, j, h);
-        long long pW = at(L, o, kbeg, j, (i - 1) >> 1);
-        long long pE = at(L, o, kbeg, j, (i + 1) >> 1);
-        long long pS = at(L, o, kbeg, j - 1, h);
-        long long pN = at(L, o, kbeg, j + 1, h);
-        double wxm, wxp, wym, wyp, cv, vhc, osw;
-        column_coeffs<UNI>(L, i, j, wxm, wxp, wym, wyp, cv, vhc, osw);
-        for (int k0 = kbeg; k0 < kend; k0 += KB) {
-            double res[KB], uown[KB];
-            stencil_batch<UNI, MODE, KB>(L, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp, cv,
-                                         vhc, osw, tdrw, tdiag, tband, res, uown);
-#pragma unroll
-            for (int t = 0; t < KB; ++t) {
-                if (k0 + t < kend) {
-                    if (out) out[pc + (long long)t * pl] = res[t];
-                    if (NORM) acc2 += (MODE == 2) ? uown[t] * res[t] : res[t] * res[t];
-                }
-            }
-            const long long step = (long long)KB * pl;
-            pc += step; pW += step; pE += step; pS += step; pN += step;
-        }
-    }
-    if (NORM) {
-        const double s = block_sum(acc2);
-        if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = s;
-    }
-}
-
-// Tile-walk apply / residual: tile = one row j x 32 columns x both
-// colours; warp w = (colour w & 1, k-segment w >> 1) of SEGA levels, so
-// each warp walks only SEGA/KB batches per tile and consecutive tiles of
-// the machine touch the same rows (the layout's contiguous row blocks).
-template <bool UNI, int MODE, bool NORM, int KB, int SEGA>
-__global__ void __launch_bounds__(512, 1)
-k_apply_t(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
-          double *__restrict__ out, double *__restrict__ partials, int hx, int ntiles) {
-    __shared__ double tdrw[256], tdiag[256], tband[257];
-    load_stencil_tables(L, tdrw, tdiag, tband);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int c = w & 1;
-    const int kseg = (w >> 1) * SEGA;
-    const int nz = L.nz;
-    const int o = c ^ 1;
-    const long long pl = L.plane;
-    double acc2 = 0.0;
-    if (kseg < nz) {
-        const int kend = min(nz, kseg + SEGA);
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int j = tile / hx;
-            const int hb = tile - j * hx;
-            const int s0 = (j + L.par + c) & 1;
-            const int hmax = ((L.nx - s0) + 1) / 2 - 1;          // last valid h of this row/colour
-            const bool act = hb * 32 + lane <= hmax;
-            const int h = act ? hb * 32 + lane : hmax;
-            const int i = 2 * h + s0;
-            long long pc = at(L, c, kseg, j, h);
-            long long pW = at(L, o, kseg, j, (i - 1) >> 1);
-            long long pE = at(L, o, kseg, j, (i + 1) >> 1);
-            long long pS = at(L, o, kseg, j - 1, h);
-            long long pN = at(L, o, kseg, j + 1, h);
-            double wxm, wxp, wym, wyp, cv, vhc, osw;
-            column_coeffs<UNI>(L, i, j, wxm, wxp, wym, wyp, cv, vhc, osw);
-            for (int k0 = kseg; k0 < kend; k0 += KB) {
-                double res[KB], uown[KB];
-                stencil_batch<UNI, MODE, KB>(L, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp,
-                                             cv, vhc, osw, tdrw, tdiag, tband, res, uown);
-                if (act) {
-#pragma unroll
-                    for (int t = 0; t < KB; ++t) {
-                        if (k0 + t < kend) {
-                            if (out) out[pc + (long long)t * pl] = res[t];
-                            if (NORM) acc2 += (MODE == 2) ? uown[t] * res[t] : res[t] * res[t];
-                        }
-                    }
-                }
-                const long long step = (long long)KB * pl;
-                pc += step; pW += step; pE += step; pS += step; pN += step;
-            }
-        }
-    }
-    if (NORM) {
-        const double s = block_sum(acc2);
-        if (threadIdx.x == 0) partials[blockIdx.x] = s;
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Vectorised column-pair stencil (uniform coefficients): a thread owns the
@@ -738,149 +527,6 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
     }
 }
 
-// Warp-level residual + restriction (uniform): no CTA barriers.  A warp
-// owns 16 coarse columns of coarse row J: lane = q*8 + m, quarter q = (fine
-// row offset rr, colour c), m = column pair.  The four children of a coarse
-// cell live in the four quarters of the same m, so they are combined with
-// warp shuffles in the reference order ((s0 + s1) + s2) + s3.
-template <int KB>
-__global__ void __launch_bounds__(256, 2)
-k_residual_restrict_w(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
-                      double *__restrict__ cf, int hb16, int ntiles, int kcs) {
-    __shared__ double tdrw[256], tdiag[256], tband[257];
-    load_stencil_tables(F, tdrw, tdiag, tband);
-    __syncthreads();
-    const int lane = threadIdx.x & 31;
-    const int q = lane >> 3, m = lane & 7;
-    const int rr = q >> 1, c = q & 1;
-    const int nz = F.nz;
-    const int o = c ^ 1;
-    const long long pl = F.plane;
-    const int nkc = (nz + kcs - 1) / kcs;
-    // children slot -> quarter (depends only on the fine parity)
-    const int pf = F.par;
-    const int qa = pf ? 1 : 0, qb = pf ? 0 : 1, qc = pf ? 2 : 3, qd = pf ? 3 : 2;
-    const int nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int tile = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); tile < ntiles;
-         tile += nwarps) {
-        const int kcI = tile % nkc;
-        const int t2 = tile / nkc;
-        const int J = t2 / hb16;
-        const int b = t2 - J * hb16;
-        const int j = 2 * J + rr;
-        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
-        const int s = (j + F.par + c) & 1;
-        const int hh = 16 * b + 2 * m;
-        const bool act = hh < C.nx;
-        const int h = act ? hh : 2 * ((C.nx - 1) / 2);
-        long long pc = at(F, c, kbeg, j, h);
-        long long po = at(F, o, kbeg, j, h);
-        long long pS = at(F, o, kbeg, j - 1, h);
-        long long pN = at(F, o, kbeg, j + 1, h);
-        long long px = at(F, o, kbeg, j, s ? h + 2 : h - 1);
-        const int cc0 = (h + J + C.par) & 1;
-        const long long q0 = at(C, cc0, kbeg, J, h >> 1);
-        const long long q1 = at(C, cc0 ^ 1, kbeg, J, h >> 1);
-        const bool two = act && (h + 1 < C.nx);
-        for (int k0 = kbeg; k0 < kend; k0 += KB) {
-            double r0[KB], r1[KB], u0[KB], u1[KB];
-            {
-                const Tabs T{tdrw, tdiag, tband, nullptr, nullptr, nullptr};
-                const Col2 A = col2_coeffs<true>(F, 0, 0);
-                stencil_batch2<1, KB, true>(F, u, f, k0, s, pc, po, pS, pN, px, T, A, A, r0, r1,
-                                            u0, u1);
-            }
-#pragma unroll
-            for (int t = 0; t < KB; ++t) {
-                double a = __shfl_sync(0xffffffffu, r0[t], qa * 8 + m) +
-                           __shfl_sync(0xffffffffu, r0[t], qb * 8 + m);
-                a = a + __shfl_sync(0xffffffffu, r0[t], qc * 8 + m);
-                a = a + __shfl_sync(0xffffffffu, r0[t], qd * 8 + m);
-                double bsum = __shfl_sync(0xffffffffu, r1[t], qa * 8 + m) +
-                              __shfl_sync(0xffffffffu, r1[t], qb * 8 + m);
-                bsum = bsum + __shfl_sync(0xffffffffu, r1[t], qc * 8 + m);
-                bsum = bsum + __shfl_sync(0xffffffffu, r1[t], qd * 8 + m);
-                const int k = k0 + t;
-                if ((t & 3) == q && act && k < kend) {
-                    const long long ko = (long long)(k - kbeg) * C.plane;
-                    cf[q0 + ko] = a;
-                    if (two) cf[q1 + ko] = bsum;
-                }
-            }
-            const long long step = (long long)KB * pl;
-            pc += step; po += step; pS += step; pN += step; px += step;
-        }
-    }
-}
-
-// Persistent batched residual + children-sum restriction: tile = 32 h x
-// fine rows (2J, 2J+1) x 2 colours = the 4 children of 32 coarse columns
-// (coarse I = h).  Fine residuals go through shared memory, are summed in
-// the reference order ((r(2I,2J) + r(2I+1,2J)) + r(2I,2J+1)) + r(2I+1,2J+1)
-// (multigrid.py:210-212) and written to the coarse f; r never hits HBM.
-template <bool UNI, int KB>
-__global__ void __launch_bounds__(128)
-k_residual_restrict_b(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
-                      double *__restrict__ cf, int hx, int ntiles, int kcs) {
-    __shared__ double tdrw[256], tdiag[256], tband[257];
-    __shared__ double rs[4][KB][33];
-    load_stencil_tables(F, tdrw, tdiag, tband);
-    __syncthreads();
-    const int lane = threadIdx.x;
-    const int ty = threadIdx.y;          // 2 * row + colour
-    const int c = ty & 1, rr = ty >> 1;
-    const int nz = F.nz;
-    const int o = c ^ 1;
-    const long long pl = F.plane;
-    const int nkc = (nz + kcs - 1) / kcs;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int kcI = tile % nkc;
-        const int t2 = tile / nkc;
-        const int J = t2 / hx;
-        const int hb = t2 - J * hx;
-        const int j = 2 * J + rr;
-        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
-        const bool act = hb * 32 + lane < C.nx;
-        const int h = act ? hb * 32 + lane : C.nx - 1;   // fine h == coarse I (clamped)
-        const int i = 2 * h + ((j + F.par + c) & 1);
-        long long pc = 0, pW = 0, pE = 0, pS = 0, pN = 0;
-        double wxm = 0, wxp = 0, wym = 0, wyp = 0, cv = 0, vhc = 0, osw = 0;
-        {
-            pc = at(F, c, kbeg, j, h);
-            pW = at(F, o, kbeg, j, (i - 1) >> 1);
-            pE = at(F, o, kbeg, j, (i + 1) >> 1);
-            pS = at(F, o, kbeg, j - 1, h);
-            pN = at(F, o, kbeg, j + 1, h);
-            column_coeffs<UNI>(F, i, j, wxm, wxp, wym, wyp, cv, vhc, osw);
-        }
-        // slot of each child in rs[]: child (a, b) = (i - 2I, j - 2J) -> 2b + a
-        const int slot = 2 * rr + (i & 1);
-        const int I = h;
-        const int cc = (I + J + C.par) & 1;
-        const long long pcoarse = act ? at(C, cc, 0, J, I >> 1) : 0;
-        for (int k0 = kbeg; k0 < kend; k0 += KB) {
-            double res[KB], uown[KB];
-            stencil_batch<UNI, 1, KB>(F, u, f, k0, pc, pW, pE, pS, pN, wxm, wxp, wym, wyp, cv,
-                                      vhc, osw, tdrw, tdiag, tband, res, uown);
-#pragma unroll
-            for (int t = 0; t < KB; ++t) rs[slot][t][lane] = act ? res[t] : 0.0;
-            __syncthreads();
-            // thread (lane, ty) sums level t = ty, ty + 4, ... of coarse column lane
-            for (int t = ty; t < KB; t += 4) {
-                const int k = k0 + t;
-                if (act && k < kend) {
-                    double sm = rs[0][t][lane] + rs[1][t][lane];
-                    sm = sm + rs[2][t][lane];
-                    sm = sm + rs[3][t][lane];
-                    cf[pcoarse + (long long)k * C.plane] = sm;
-                }
-            }
-            __syncthreads();
-            const long long step = (long long)KB * pl;
-            pc += step; pW += step; pE += step; pS += step; pN += step;
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // residual fused with children-sum restriction (multigrid.py:278-282):
@@ -1072,366 +718,10 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Line smoother half-sweep, register-resident variant (default).
-//
-// CTA = 32 columns (lane) x NW warps; warp w owns the k-segment
-// [w*SEG, (w+1)*SEG) of every column IN REGISTERS.  All warps assemble
-// their RHS segment at once (SEG independent k-planes per thread in flight:
-// one or two DRAM round trips per CTA).  The Thomas recurrence stays exactly
-// the reference's (smoother.py:151-161): the forward chain runs through
-// warps 0..NW-1 and the backward chain through NW-1..0, handing the running
-// value over in shared memory; so the result is bit-identical to the
-// sequential column solve.  Relaxation + stores run on all warps again.
-// Only ~2 KB of shared memory per CTA: occupancy is register-limited.
-// ---------------------------------------------------------------------------
-template <bool UNI, int SEG>
-__global__ void __launch_bounds__(256, 3)
-k_half_sweep_reg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                 int zero_start, int nbr_zero, double post_scale) {
-    extern __shared__ double tab[];
-    const int nz = L.nz;
-    double *tvp = tab;              // [nz+1]
-    double *tinv = tvp + nz + 1;    // [nz]  (uniform pivots)
-    double *tdrw = tinv + nz;       // [nz]
-    __shared__ double hand[32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int j = blockIdx.y;
-    const int h = blockIdx.x * 32 + lane;
-    const int i = 2 * h + ((j + L.par + c) & 1);
-    const bool act = i < L.nx;
-    const int o = c ^ 1;
-    const long long pc = at(L, c, 0, j, h);
-    const long long pl = L.plane;
-    const int k0 = w * SEG;
-
-    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
-        tvp[t] = L.vprof[t];
-        if (t < nz) {
-            if (UNI) tinv[t] = L.invd1[t];
-            tdrw[t] = L.drw[t];
-        }
-    }
-    __syncthreads();
-
-    double r[SEG];
-    double iv[UNI ? 1 : SEG];
-    double cv = L.csub0;
-    if (act) {
-        double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
-        if (!UNI) {
-            wxm = L.wx[(long long)j * (L.nx + 1) + i];
-            wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
-            wym = L.wy[(long long)j * L.nx + i];
-            wyp = L.wy[(long long)(j + 1) * L.nx + i];
-            cv = L.vcoef * L.av[(long long)j * L.nx + i];
-        }
-        const long long pW = at(L, o, 0, j, (i - 1) >> 1);
-        const long long pE = at(L, o, 0, j, (i + 1) >> 1);
-        const long long pS = at(L, o, 0, j - 1, h);
-        const long long pN = at(L, o, 0, j + 1, h);
-#pragma unroll
-        for (int s = 0; s < SEG; ++s) {
-            const int k = k0 + s;
-            if (k < nz) {
-                const long long ko = (long long)k * pl;
-                double g;
-                if (nbr_zero) {
-                    g = f[pc + ko];
-                } else {
-                    g = wxm * u[pW + ko];
-                    g = g + wxp * u[pE + ko];
-                    g = g + wym * u[pS + ko];
-                    g = g + wyp * u[pN + ko];
-                    g = g * tdrw[k];
-                    g = g + f[pc + ko];
-                }
-                r[s] = g;
-                if (!UNI) iv[s] = L.invd[pc + ko];
-            }
-        }
-    }
-    // forward elimination, warp by warp (smoother.py:151-156)
-    for (int step = 0; step < nw; ++step) {
-        if (w == step && act) {
-            double g = (w == 0) ? 0.0 : hand[lane];
-#pragma unroll
-            for (int s = 0; s < SEG; ++s) {
-                const int k = k0 + s;
-                if (k < nz) {
-                    const double ivk = UNI ? tinv[k] : iv[s];
-                    if (k == 0) {
-                        g = r[s] * ivk;
-                    } else {
-                        double t = g * cv;
-                        t = t * tvp[k];
-                        g = r[s] + t;
-                        g = g * ivk;
-                    }
-                    r[s] = g;
-                }
-            }
-            hand[lane] = g;
-        }
-        __syncthreads();
-    }
-    // back substitution, warp by warp (smoother.py:157-161)
-    for (int step = nw - 1; step >= 0; --step) {
-        if (w == step && act) {
-            double x = hand[lane];
-#pragma unroll
-            for (int s = SEG - 1; s >= 0; --s) {
-                const int k = k0 + s;
-                if (k < nz - 1) {
-                    double t = x * cv;
-                    t = t * tvp[k + 1];
-                    t = t * (UNI ? tinv[k] : iv[s]);
-                    x = r[s] + t;
-                    r[s] = x;
-                } else if (k == nz - 1) {
-                    x = r[s];
-                }
-            }
-            hand[lane] = x;
-        }
-        __syncthreads();
-    }
-    if (!act) return;
-    // relaxation (smoother.py:163-170) and coalesced stores, all warps
-    const double scale = rho * post_scale;
-    const double omr = 1.0 - rho;
-#pragma unroll
-    for (int s = 0; s < SEG; ++s) {
-        const int k = k0 + s;
-        if (k < nz) {
-            double y = r[s];
-            if (zero_start) {
-                if (scale != 1.0) y = y * scale;
-            } else if (rho != 1.0) {
-                // u still holds the old value of this (own) cell
-                y = y * rho;
-                y = y + omr * u[pc + (long long)k * pl];
-            }
-            u[pc + (long long)k * pl] = y;
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
-// Line smoother half-sweep, persistent warp-specialised pipeline (default
-// for uniform coefficients).
-//
-// Tile = 32 columns (one 32-wide h strip of one row) x nz levels.  Each
-// CTA is resident on one SM and walks tiles blockIdx.x, +gridDim.x, ...
-//   * producer warps (NG groups x NP warps; group g takes every NG-th
-//     tile of the CTA) assemble the tile's RHS: warp p owns a k-segment
-//     and issues 8 levels x 5 loads per lane before any arithmetic, then
-//     writes g[k][lane] into a shared-memory tile buffer;
-//   * NS solver warps (solver s takes the CTA's tiles q = s mod NS, double
-//     buffered) run the exact Thomas recurrence of smoother.py:151-161 per
-//     lane in shared memory and stream x (relaxed, smoother.py:163-170)
-//     straight to HBM.
-// FULL/EMPTY hand-offs are named barriers (bar.arrive / bar.sync).  The
-// serial chain of one tile (2 nz dependent steps) overlaps the loads of
-// the next tiles, so the SM keeps DRAM busy; results are bit-identical to
-// the sequential column solve.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void nbar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int n) {
-    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-constexpr int PP_KB = 4;    // levels per producer load batch
-constexpr int PP_NP = 8;    // producer warps per group
-constexpr int PP_NG = 2;    // producer groups
-constexpr int PP_NS = 3;    // solver warps (double-buffered each)
-constexpr int PP_NBUF = 2 * PP_NS;
-constexpr int PP_THREADS = 32 * (PP_NP * PP_NG + PP_NS);
-
-__global__ void __launch_bounds__(PP_THREADS, 1)
-k_half_sweep_pipe(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
-    extern __shared__ double sm[];
-    const int nz = L.nz;
-    double *tvp = sm;                 // [nz+1]
-    double *tinv = tvp + nz + 1;      // [nz]
-    double *tdrw = tinv + nz;         // [nz]
-    double *bufs = sm + ((3 * nz + 1 + 3) & ~3);   // [NBUF][nz][32]
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
-        tvp[t] = L.vprof[t];
-        if (t < nz) {
-            tinv[t] = L.invd1[t];
-            tdrw[t] = L.drw[t];
-        }
-    }
-    __syncthreads();
-    const int o = c ^ 1;
-    const long long pl = L.plane;
-    const int nprod = PP_NP * PP_NG;
-    const int cnt = 32 * (PP_NP + 1);   // one producer group + one solver warp
-    if (warp < nprod) {
-        // ------------------------------ producer ------------------------------
-        const int grp = warp / PP_NP, pw = warp % PP_NP;
-        const int seg = (nz + PP_NP - 1) / PP_NP;
-        const int ka = pw * seg, kz = min(nz, ka + seg);
-        const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
-        for (int q = grp;; q += PP_NG) {
-            const int t = blockIdx.x + q * gridDim.x;
-            if (t >= ntiles) break;
-            const int sv = q % PP_NS;
-            const int b = 2 * sv + (q / PP_NS) % 2;
-            if (q >= PP_NBUF) nbar_sync(1 + PP_NBUF + b, cnt);      // EMPTY(b)
-            double *buf = bufs + (size_t)b * nz * 32;
-            const int j = t / htiles;
-            const int h0 = (t % htiles) * 32;
-            // inactive lanes (i >= nx on narrow levels) clamp to the last
-            // active column so the warp stays converged for the shuffle;
-            // the shuffle source of the last active lane is then itself,
-            // so its E neighbour is loaded explicitly (vx) as for lane 31
-            const int s0 = (j + L.par + c) & 1;
-            const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
-            const int ln = min(lane, nact - 1);
-            const int h = h0 + ln;
-            const int i = 2 * h + s0;
-            const bool lastlane = (ln == nact - 1);
-            if (nact > 0) {
-                const long long pc = at(L, c, 0, j, h);
-                const long long pW = at(L, o, 0, j, (i - 1) >> 1);
-                const long long pE = at(L, o, 0, j, (i + 1) >> 1);
-                const long long pS = at(L, o, 0, j - 1, h);
-                const long long pN = at(L, o, 0, j + 1, h);
-                for (int k8 = ka; k8 < kz; k8 += PP_KB) {
-                    // PP_KB levels x 4 loads in flight per lane; the E neighbour
-                    // of lane l is the W neighbour of lane l+1 (same row, next h)
-                    double vf[PP_KB], vw[PP_KB], vs[PP_KB], vn[PP_KB], vx[PP_KB];
-#pragma unroll
-                    for (int e = 0; e < PP_KB; ++e) {
-                        const int k = k8 + e;
-                        if (k < kz) {
-                            const long long ko = (long long)k * pl;
-                            vf[e] = f[pc + ko];
-                            if (!nbr_zero) {
-                                vw[e] = u[pW + ko];
-                                vs[e] = u[pS + ko];
-                                vn[e] = u[pN + ko];
-                                vx[e] = lastlane ? u[pE + ko] : 0.0;
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int e = 0; e < PP_KB; ++e) {
-                        const int k = k8 + e;
-                        double ve = __shfl_down_sync(0xffffffffu, vw[e], 1);
-                        if (lastlane) ve = vx[e];
-                        if (k < kz) {
-                            double g;
-                            if (nbr_zero) {
-                                g = vf[e];
-                            } else {
-                                g = wxm * vw[e];
-                                g = g + wxp * ve;
-                                g = g + wym * vs[e];
-                                g = g + wyp * vn[e];
-                                g = g * tdrw[k];
-                                g = g + vf[e];
-                            }
-                            if (lane < nact) buf[k * 32 + lane] = g;
-                        }
-                    }
-                }
-            }
-            nbar_arrive(1 + b, cnt);                                   // FULL(b)
-        }
-    } else {
-        // ------------------------------- solver -------------------------------
-        const int sv = warp - nprod;
-        if (sv >= PP_NS) return;
-        const double cv = L.csub0;
-        const double scale = rho * post_scale;
-        const double omr = 1.0 - rho;
-        for (int q = sv;; q += PP_NS) {
-            const int t = blockIdx.x + q * gridDim.x;
-            if (t >= ntiles) break;
-            const int b = 2 * sv + (q / PP_NS) % 2;
-            nbar_sync(1 + b, cnt);                                     // FULL(b)
-            double *buf = bufs + (size_t)b * nz * 32;
-            const int j = t / htiles;
-            const int h = (t % htiles) * 32 + lane;
-            const int i = 2 * h + ((j + L.par + c) & 1);
-            if (i < L.nx) {
-                const long long pc = at(L, c, 0, j, h);
-                // forward elimination in register chunks of 8 levels: the
-                // chunk's 8 LDS are issued before the dependent chain
-                double g = 0.0;
-                for (int kb = 0; kb < nz; kb += 8) {
-                    double r[8];
-                    const double *tv = tvp + kb, *ti = tinv + kb;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if (kb + e < nz) r[e] = buf[(kb + e) * 32 + lane];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        const int k = kb + e;
-                        if (k < nz) {
-                            if (k == 0) {
-                                g = r[e] * ti[e];
-                            } else {
-                                double tt = g * cv;
-                                tt = tt * tv[e];
-                                g = r[e] + tt;
-                                g = g * ti[e];
-                            }
-                            r[e] = g;
-                        }
-                    }
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if (kb + e < nz) buf[(kb + e) * 32 + lane] = r[e];
-                }
-                // back substitution + relaxation, chunks of 8 from the top
-                double x = g;
-                const int top = ((nz - 1) / 8) * 8;
-                for (int kb = top; kb >= 0; kb -= 8) {
-                    double r[8];
-                    const double *tv = tvp + kb + 1, *ti = tinv + kb;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e)
-                        if (kb + e < nz - 1) r[e] = buf[(kb + e) * 32 + lane];
-#pragma unroll
-                    for (int e = 7; e >= 0; --e) {
-                        const int k = kb + e;
-                        if (k < nz - 1) {
-                            double tt = x * cv;
-                            tt = tt * tv[e];
-                            tt = tt * ti[e];
-                            x = r[e] + tt;
-                        }
-                        if (k < nz) {
-                            double y = x;
-                            if (zero_start) {
-                                if (scale != 1.0) y = y * scale;
-                            } else if (rho != 1.0) {
-                                y = y * rho;
-                                y = y + omr * u[pc + (long long)k * pl];
-                            }
-                            u[pc + (long long)k * pl] = y;
-                        }
-                    }
-                }
-            }
-            __syncwarp();
-            // release the buffer only if a producer will wait for it
-            if (blockIdx.x + (q + PP_NBUF) * gridDim.x < ntiles) nbar_arrive(1 + PP_NBUF + b, cnt);
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Line smoother half-sweep, TMA-fed solver warps (default for uniform
-// coefficients).
+// Line smoother half-sweep, TMA-fed solver warps (exact mode, opt-in:
+// PMG_HS_VARIANT=t).
 //
 // Every warp of the persistent CTA is an independent pipeline over its own
 // sequence of tiles (32 columns of one row x nz levels):
@@ -2158,293 +1448,6 @@ k_half_sweep_cp(Lvl L, double *__restrict__ u, const double *__restrict__ f, int
     cp_wait<0>();
 }
 
-// Same k-segmented solve with the segment values kept in shared memory
-// (tile [nz][32]) instead of registers: registers then only carry the
-// in-flight load batch, so more warps fit per SM.
-template <int SEG, int B, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-k_half_sweep_segs(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
-    extern __shared__ double ssm[];
-    const int nz = L.nz;
-    double *tdrw = ssm;                 // [nz]
-    double *tiot = tdrw + nz;           // [nz]
-    double *tal = tiot + nz;            // [nz]
-    double *tmu = tal + nz;             // [nz]
-    double *tpf = tmu + nz;             // [nz]
-    double *tq = tpf + nz;              // [nz]
-    double *hend = tq + nz;             // [8][32]
-    double *ybeg = hend + 8 * 32;       // [8][32]
-    double *sv = ybeg + 8 * 32;         // [nz][32]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
-        tdrw[t] = L.drw[t];
-        tiot[t] = L.invd1[t];
-        tal[t] = L.segtab[t];
-        tmu[t] = L.segtab[nz + t];
-        tpf[t] = L.segtab[2 * nz + t];
-        tq[t] = L.segtab[3 * nz + t];
-    }
-    __syncthreads();
-    const int o = c ^ 1;
-    const long long pl = L.plane;
-    const int k0 = w * SEG;
-    const int kn = min(SEG, nz - k0);
-    const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
-    const double scale = rho * post_scale;
-    const double omr = 1.0 - rho;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int j = t / htiles;
-        const int h0 = (t - j * htiles) * 32;
-        const int s0 = (j + L.par + c) & 1;
-        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
-        const int ln = min(lane, nact - 1);
-        const bool lastlane = (ln == nact - 1);
-        const int h = h0 + ln;
-        const int i = 2 * h + s0;
-        const long long pc = at(L, c, k0, j, h);
-        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
-        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
-        const long long pS = at(L, o, k0, j - 1, h);
-        const long long pN = at(L, o, k0, j + 1, h);
-        // ---- RHS + local forward h_k = iota r_k + alpha h_{k-1}, batch by batch ----
-        double hp = 0.0;
-        for (int b8 = 0; b8 < kn; b8 += B) {
-            double vf[B], vw[B], vs[B], vn[B], vx[B];
-#pragma unroll
-            for (int e = 0; e < B; ++e) {
-                const int kk = b8 + e;
-                if (kk < kn) {
-                    const long long ko = (long long)kk * pl;
-                    vf[e] = f[pc + ko];
-                    if (!nbr_zero) {
-                        vw[e] = u[pW + ko];
-                        vs[e] = u[pS + ko];
-                        vn[e] = u[pN + ko];
-                        vx[e] = lastlane ? u[pE + ko] : 0.0;
-                    }
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < B; ++e) {
-                const int kk = b8 + e;
-                double ve = __shfl_down_sync(0xffffffffu, nbr_zero ? 0.0 : vw[e], 1);
-                if (lastlane) ve = vx[e];
-                if (kk < kn) {
-                    const int k = k0 + kk;
-                    double g;
-                    if (nbr_zero) {
-                        g = vf[e];
-                    } else {
-                        g = wxm * vw[e];
-                        g = g + wxp * ve;
-                        g = g + wym * vs[e];
-                        g = g + wyp * vn[e];
-                        g = g * tdrw[k];
-                        g = g + vf[e];
-                    }
-                    hp = __fma_rn(tal[k], hp, tiot[k] * g);
-                    sv[k * 32 + lane] = hp;
-                }
-            }
-        }
-        if (kn > 0) hend[w * 32 + lane] = hp;
-        __syncthreads();
-        double G = 0.0;
-        for (int sgm = 0; sgm < w; ++sgm)
-            G = __fma_rn(tpf[min(nz, (sgm + 1) * SEG) - 1], G, hend[sgm * 32 + lane]);
-        double yp = 0.0;
-        for (int e = kn - 1; e >= 0; --e) {
-            const int k = k0 + e;
-            const double g = __fma_rn(tpf[k], G, sv[k * 32 + lane]);
-            yp = __fma_rn(tmu[k], yp, g);
-            sv[k * 32 + lane] = yp;
-        }
-        if (kn > 0) ybeg[w * 32 + lane] = yp;
-        __syncthreads();
-        double X = 0.0;
-        for (int sgm = nw - 1; sgm > w; --sgm) {
-            const int a = sgm * SEG;
-            if (a < nz) X = __fma_rn(tq[a], X, ybeg[sgm * 32 + lane]);
-        }
-        if (lane < nact) {
-            for (int e = 0; e < kn; ++e) {
-                const int k = k0 + e;
-                double y = __fma_rn(tq[k], X, sv[k * 32 + lane]);
-                const long long q = pc + (long long)e * pl;
-                if (zero_start) {
-                    if (scale != 1.0) y = y * scale;
-                } else if (rho != 1.0) {
-                    y = y * rho;
-                    y = y + omr * u[q];
-                }
-                u[q] = y;
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// One-barrier k-segmented solve.  Each warp runs the forward AND the
-// backward sweep of its segment with zero boundary values (h, y0) and
-// publishes h at its top and y0 at its bottom; the backward solution is
-// affine in the incoming forward value G and the incoming backward value X:
-//   x_k = y0_k + ag_k G + q_k X,
-// so after ONE barrier every warp solves the 2 x NW reduced system for its
-// own (G, X) from the published values.  The exchange arrays are double
-// buffered by tile parity (warps are never more than one tile apart), so
-// there is no end-of-tile barrier.
-template <int SEG, int B, int MINB>
-__global__ void __launch_bounds__(256, MINB)
-k_half_sweep_seg1(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                  int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
-    extern __shared__ double ssm[];
-    const int nz = L.nz;
-    double *tdrw = ssm;                 // [nz]
-    double *tiot = tdrw + nz;           // [nz]
-    double *tal = tiot + nz;            // [nz]
-    double *tmu = tal + nz;             // [nz]
-    double *tpf = tmu + nz;             // [nz]
-    double *tq = tpf + nz;              // [nz]
-    double *tag = tq + nz;              // [nz]
-    double *xch = tag + nz;             // [2 parity][2 (hend, y0beg)][8][32]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
-        tdrw[t] = L.drw[t];
-        tiot[t] = L.invd1[t];
-        tal[t] = L.segtab[t];
-        tmu[t] = L.segtab[nz + t];
-        tpf[t] = L.segtab[2 * nz + t];
-        tq[t] = L.segtab[3 * nz + t];
-        tag[t] = L.segtab[4 * nz + t];
-    }
-    __syncthreads();
-    const int o = c ^ 1;
-    const long long pl = L.plane;
-    const int k0 = w * SEG;
-    const int kn = min(SEG, nz - k0);
-    const double wxm = L.wx0, wxp = L.wx0, wym = L.wy0, wyp = L.wy0;
-    const double scale = rho * post_scale;
-    const double omr = 1.0 - rho;
-    int par = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
-        const int j = t / htiles;
-        const int h0 = (t - j * htiles) * 32;
-        const int s0 = (j + L.par + c) & 1;
-        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
-        const int ln = min(lane, nact - 1);
-        const bool lastlane = (ln == nact - 1);
-        const int h = h0 + ln;
-        const int i = 2 * h + s0;
-        const long long pc = at(L, c, k0, j, h);
-        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
-        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
-        const long long pS = at(L, o, k0, j - 1, h);
-        const long long pN = at(L, o, k0, j + 1, h);
-        double r[SEG];
-#pragma unroll
-        for (int b8 = 0; b8 < SEG; b8 += B) {
-            double vf[B], vw[B], vs[B], vn[B], vx[B];
-#pragma unroll
-            for (int e = 0; e < B; ++e) {
-                const int kk = b8 + e;
-                if (kk < kn) {
-                    const long long ko = (long long)kk * pl;
-                    vf[e] = f[pc + ko];
-                    if (!nbr_zero) {
-                        vw[e] = u[pW + ko];
-                        vs[e] = u[pS + ko];
-                        vn[e] = u[pN + ko];
-                        vx[e] = lastlane ? u[pE + ko] : 0.0;
-                    }
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < B; ++e) {
-                const int kk = b8 + e;
-                double ve = __shfl_down_sync(0xffffffffu, nbr_zero ? 0.0 : vw[e], 1);
-                if (lastlane) ve = vx[e];
-                if (kk < kn) {
-                    double g;
-                    if (nbr_zero) {
-                        g = vf[e];
-                    } else {
-                        g = wxm * vw[e];
-                        g = g + wxp * ve;
-                        g = g + wym * vs[e];
-                        g = g + wyp * vn[e];
-                        g = g * tdrw[k0 + kk];
-                        g = g + vf[e];
-                    }
-                    r[b8 + e] = g;
-                }
-            }
-        }
-        // zero-boundary forward (h) and backward (y0) sweeps of the segment
-        double hp = 0.0;
-#pragma unroll
-        for (int e = 0; e < SEG; ++e)
-            if (e < kn) {
-                const int k = k0 + e;
-                hp = __fma_rn(tal[k], hp, tiot[k] * r[e]);
-                r[e] = hp;
-            }
-        double yp = 0.0;
-#pragma unroll
-        for (int e = SEG - 1; e >= 0; --e)
-            if (e < kn) {
-                const int k = k0 + e;
-                yp = __fma_rn(tmu[k], yp, r[e]);
-                r[e] = yp;
-            }
-        double *xh = xch + par * 2 * 8 * 32;
-        double *xy = xh + 8 * 32;
-        if (kn > 0) {
-            xh[w * 32 + lane] = hp;
-            xy[w * 32 + lane] = yp;
-        }
-        __syncthreads();
-        // reduced system: G_s = hend_{s-1} + pf_end(s-1) G_{s-1};
-        // X_s = y0beg_{s+1} + ag_{a(s+1)} G_{s+1} + q_{a(s+1)} X_{s+1}
-        double Gs[8];
-        double G = 0.0;
-#pragma unroll
-        for (int sg = 0; sg < 8; ++sg) {
-            Gs[sg] = G;
-            if (sg < nw) {
-                const int b = min(nz, (sg + 1) * SEG) - 1;
-                G = __fma_rn(tpf[b], G, xh[sg * 32 + lane]);
-            }
-        }
-        double X = 0.0, Gw = 0.0;
-#pragma unroll
-        for (int sg = 7; sg >= 0; --sg) {
-            const int a = sg * SEG;
-            if (sg > w && sg < nw && a < nz) {
-                const double v = __fma_rn(tag[a], Gs[sg], xy[sg * 32 + lane]);
-                X = __fma_rn(tq[a], X, v);
-            }
-            if (sg == w) Gw = Gs[sg];
-        }
-        if (lane < nact) {
-#pragma unroll
-            for (int e = 0; e < SEG; ++e) {
-                if (e < kn) {
-                    const int k = k0 + e;
-                    double y = __fma_rn(tag[k], Gw, __fma_rn(tq[k], X, r[e]));
-                    const long long q = pc + (long long)e * pl;
-                    if (zero_start) {
-                        if (scale != 1.0) y = y * scale;
-                    } else if (rho != 1.0) {
-                        y = y * rho;
-                        y = y + omr * u[q];
-                    }
-                    u[q] = y;
-                }
-            }
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // FAST half-sweep for VARIABLE coefficients (configs[4]): the k-segmented
@@ -2655,62 +1658,6 @@ __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *_
     if (HALO) halo_copies(F, fu, i, j, k, v);
 }
 
-// Persistent batched prolongation + add: thread = one fine column (h, row,
-// colour), walks k in batches of PB levels with all 4 coarse + 1 fine loads
-// of the batch in flight; the coarse values are shared by the 4 children
-// through L1.  Same arithmetic as k_prolong.
-template <int PB>
-__global__ void __launch_bounds__(256)
-k_prolong_b(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
-            int hx, int ntiles, int kcs) {
-    const int lane = threadIdx.x & 31;
-    const int ty = threadIdx.x >> 5;               // 8 warps: 4 rows x 2 colours
-    const int c = ty & 1;
-    const int nz = F.nz;
-    const int nkc = (nz + kcs - 1) / kcs;
-    const long long pl = F.plane, cpl = C.plane;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int kcI = tile % nkc;
-        const int t2 = tile / nkc;
-        const int jb = t2 / hx;
-        const int hb = t2 - jb * hx;
-        const int j = jb * 4 + (ty >> 1);
-        const int h = hb * 32 + lane;
-        const int i = 2 * h + ((j + F.par + c) & 1);
-        if (j >= F.ny || i >= F.nx) continue;
-        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
-        const int I = i >> 1, J = j >> 1;
-        const int dI = (i & 1) ? 1 : -1, dJ = (j & 1) ? 1 : -1;
-        const long long qc = cell(C, I, J, kbeg), qx = cell(C, I + dI, J, kbeg);
-        const long long qy = cell(C, I, J + dJ, kbeg), qd = cell(C, I + dI, J + dJ, kbeg);
-        const long long q = at(F, c, kbeg, j, h);
-        for (int k0 = kbeg; k0 < kend; k0 += PB) {
-            double vc[PB], vx[PB], vy[PB], vd[PB], vu[PB];
-#pragma unroll
-            for (int t = 0; t < PB; ++t) {
-                if (k0 + t < kend) {
-                    const long long co = (long long)(k0 - kbeg + t) * cpl;
-                    vc[t] = cu[qc + co];
-                    vx[t] = cu[qx + co];
-                    vy[t] = cu[qy + co];
-                    vd[t] = cu[qd + co];
-                    if (add) vu[t] = fu[q + (long long)(k0 - kbeg + t) * pl];
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < PB; ++t) {
-                if (k0 + t < kend) {
-                    double e = 9.0 * vc[t];
-                    e = e + 3.0 * vx[t];
-                    e = e + 3.0 * vy[t];
-                    e = e + vd[t];
-                    e = e * 0.0625;
-                    fu[q + (long long)(k0 - kbeg + t) * pl] = add ? vu[t] + e : e;
-                }
-            }
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // halos (partition.py:158-191)
@@ -2787,30 +1734,6 @@ __global__ void k_unpack_face(Lvl L, double *__restrict__ d, int face, const dou
     d[cell(L, i, j, k)] = v;
 }
 
-// ---------------------------------------------------------------------------
-// reductions and BLAS-1 (partition.py:138-155, 267-286)
-// ---------------------------------------------------------------------------
-// Owned cells enumerated as rows (c, j, k) x h; block b takes rows b,
-// b+grid, ...; fixed grid => fixed summation order (deterministic).
-__global__ void __launch_bounds__(256)
-k_dot(Lvl L, const double *__restrict__ a, const double *__restrict__ b,
-      double *__restrict__ partials) {
-    const int rowlen = (L.nx + 1) >> 1;
-    const int nrows = 2 * L.nz * L.ny;
-    double s = 0.0;
-    for (int r = blockIdx.x; r < nrows; r += gridDim.x) {
-        const int k = r % L.nz;
-        const int cj = r / L.nz;
-        const int j = cj % L.ny, c = cj / L.ny;
-        const int s0 = (j + L.par + c) & 1;
-        const long long base = at(L, c, k, j, 0);
-        for (int h = threadIdx.x; h < rowlen; h += blockDim.x) {
-            if (2 * h + s0 < L.nx) s += a[base + h] * b[base + h];
-        }
-    }
-    s = block_sum(s);
-    if (threadIdx.x == 0) partials[blockIdx.x] = s;
-}
 
 // Vectorised owned-cell dot / norm: owned rows (c, j, k) are contiguous
 // [OFF, OFF + nh) segments; a thread covers one double2 of RPB rows at once
@@ -3011,47 +1934,6 @@ static inline int k_chunk(const Lvl &L, long long columns, int want_blocks_per_s
     return kc;
 }
 
-template <int KB>
-static cudaError_t launch_apply_kb(const Lvl &L, const double *u, const double *f, double *out,
-                                  int mode, double *partials, int *nparts, cudaStream_t st) {
-    const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
-    const bool norm = partials != nullptr;
-    const int hx = g0.x, jy = g0.y;
-    int occ = 1;
-#define PMG_OCC(U, M, N) \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply_b<U, M, N, KB>, 32 * 2 * AP_TY, 0)
-    if (L.uniform) {
-        if (mode == 0) PMG_OCC(true, 0, false);
-        else if (mode == 1) { if (norm) PMG_OCC(true, 1, true); else PMG_OCC(true, 1, false); }
-        else PMG_OCC(true, 2, true);
-    } else {
-        if (mode == 0) PMG_OCC(false, 0, false);
-        else if (mode == 1) { if (norm) PMG_OCC(false, 1, true); else PMG_OCC(false, 1, false); }
-        else PMG_OCC(false, 2, true);
-    }
-#undef PMG_OCC
-    const int cap = sm_count() * (occ > 0 ? occ : 1);
-    // split k on small levels until there are >= 2 tiles per resident CTA
-    int kcs = L.nz;
-    while (kcs > 2 * KB && (long long)hx * jy * ((L.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
-    kcs = (kcs + KB - 1) / KB * KB;
-    const int ntiles = hx * jy * ((L.nz + kcs - 1) / kcs);
-    const int grid = ntiles < cap ? ntiles : cap;
-    *nparts = grid;
-#define PMG_AB(U, M, N) \
-    k_apply_b<U, M, N, KB><<<grid, b, 0, st>>>(L, u, f, out, partials, hx, jy, ntiles, kcs)
-    if (L.uniform) {
-        if (mode == 0) PMG_AB(true, 0, false);
-        else if (mode == 1) { if (norm) PMG_AB(true, 1, true); else PMG_AB(true, 1, false); }
-        else PMG_AB(true, 2, true);
-    } else {
-        if (mode == 0) PMG_AB(false, 0, false);
-        else if (mode == 1) { if (norm) PMG_AB(false, 1, true); else PMG_AB(false, 1, false); }
-        else PMG_AB(false, 2, true);
-    }
-#undef PMG_AB
-    return cudaGetLastError();
-}
 
 static int apply_variant() {
     static int v = -1;
@@ -3118,50 +2000,6 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
         }
         return cudaGetLastError();
     }
-    if (apply_variant() == 0 && L.nz <= 256 && L.nz >= 16 && getenv("PMG_APPLY_T") != nullptr) {
-        // tile walk: 16 warps = 2 colours x 8 k-segments
-        constexpr int KB = 4;
-        const int sega = ((L.nz + 7) / 8 + KB - 1) / KB * KB;
-        const int hx = ((L.nx + 1) / 2 + 31) / 32;
-        const int ntiles = hx * L.ny;
-        const bool norm = partials != nullptr;
-        auto go = [&](auto kern) {
-            int occ = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 512, 0);
-            const int cap = sm_count() * (occ > 0 ? occ : 1);
-            const int grid = ntiles < cap ? ntiles : cap;
-            *nparts = grid;
-            kern<<<grid, 512, 0, st>>>(L, u, f, out, partials, hx, ntiles);
-        };
-#define PMG_AT(U, M, N)                                                          \
-    do {                                                                         \
-        if (sega <= 4) go(k_apply_t<U, M, N, KB, 4>);                            \
-        else if (sega <= 8) go(k_apply_t<U, M, N, KB, 8>);                       \
-        else if (sega <= 16) go(k_apply_t<U, M, N, KB, 16>);                     \
-        else go(k_apply_t<U, M, N, KB, 32>);                                     \
-    } while (0)
-        if (L.uniform) {
-            if (mode == 0) PMG_AT(true, 0, false);
-            else if (mode == 1) { if (norm) PMG_AT(true, 1, true); else PMG_AT(true, 1, false); }
-            else PMG_AT(true, 2, true);
-        } else {
-            if (mode == 0) PMG_AT(false, 0, false);
-            else if (mode == 1) { if (norm) PMG_AT(false, 1, true); else PMG_AT(false, 1, false); }
-            else PMG_AT(false, 2, true);
-        }
-#undef PMG_AT
-        return cudaGetLastError();
-    }
-    if (apply_variant() == 0 && L.nz <= 256) {
-        static int kbsel = -1;
-        if (kbsel < 0) {
-            const char *e = getenv("PMG_APPLY_KB");
-            kbsel = e ? atoi(e) : 4;
-        }
-        if (kbsel == 8) return launch_apply_kb<8>(L, u, f, out, mode, partials, nparts, st);
-        if (kbsel == 2) return launch_apply_kb<2>(L, u, f, out, mode, partials, nparts, st);
-        return launch_apply_kb<4>(L, u, f, out, mode, partials, nparts, st);
-    }
     const int kc = k_chunk(L, (long long)L.nx * L.ny, 148 * 2048 * 2);
     const dim3 g(g0.x, g0.y, (L.nz + kc - 1) / kc);
     *nparts = g.x * g.y * g.z;
@@ -3189,21 +2027,6 @@ cudaError_t launch_finalize(const double *partials, int n, double *out, cudaStre
 cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u, const double *f,
                                      double *cf, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (F.uniform && F.nz <= 256 && getenv("PMG_RR_W") != nullptr) {   // warp-shuffle variant
-        constexpr int KB = 4;
-        const int hb16 = (C.nx + 15) / 16;
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_w<KB>, 256, 0);
-        const int capw = sm_count() * (occ > 0 ? occ : 1) * 8;
-        int kcs = F.nz;
-        while (kcs > 2 * KB && (long long)hb16 * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * capw) kcs >>= 1;
-        kcs = (kcs + KB - 1) / KB * KB;
-        const int ntiles = hb16 * C.ny * ((F.nz + kcs - 1) / kcs);
-        int grid = (ntiles + 7) / 8;
-        if (grid > capw / 8) grid = capw / 8;
-        k_residual_restrict_w<KB><<<grid, 256, 0, st>>>(F, C, u, f, cf, hb16, ntiles, kcs);
-        return cudaGetLastError();
-    }
     if (F.uniform && F.nz <= 256 && F.nx % 4 == 0 && C.nx >= 2 && !getenv("PMG_RR_NOQ")) {
         const int mb32 = ((C.nx >> 1) + 31) / 32;
         auto runq = [&](auto kern) {
@@ -3221,7 +2044,7 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
         runq(k_residual_restrict_q<2>);
         return cudaGetLastError();
     }
-    if (F.nz <= 256 && getenv("PMG_RR_V0") == nullptr) {
+    if (F.nz <= 256) {
         constexpr int KB = 4;
         const int hx = (C.nx + 63) / 64;
         int occ = 1;
@@ -3241,26 +2064,6 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
             k_residual_restrict_v<KB, false><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
         return cudaGetLastError();
     }
-    if (F.nz <= 256 && getenv("PMG_RR_OLD") == nullptr) {
-        constexpr int KB = 4;
-        const int hx = (C.nx + 31) / 32;
-        int occ = 1;
-        if (F.uniform)
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_b<true, KB>, 128, 0);
-        else
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_residual_restrict_b<false, KB>, 128, 0);
-        const int cap = sm_count() * (occ > 0 ? occ : 1);
-        int kcs = F.nz;
-        while (kcs > 2 * KB && (long long)hx * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
-        kcs = (kcs + KB - 1) / KB * KB;
-        const int ntiles = hx * C.ny * ((F.nz + kcs - 1) / kcs);
-        const int grid = ntiles < cap ? ntiles : cap;
-        if (F.uniform)
-            k_residual_restrict_b<true, KB><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
-        else
-            k_residual_restrict_b<false, KB><<<grid, dim3(32, 4), 0, st>>>(F, C, u, f, cf, hx, ntiles, kcs);
-        return cudaGetLastError();
-    }
     const int kc = k_chunk(F, (long long)C.nx * C.ny, 148 * 2048 * 2);
     const dim3 b(32, 8), g((C.nx + 31) / 32, (F.nz + kc - 1) / kc, (C.ny + 7) / 8);
     if (F.uniform) k_residual_restrict<true><<<g, b, 0, st>>>(F, C, u, f, cf, kc);
@@ -3273,21 +2076,14 @@ size_t half_sweep_smem(const Lvl &L, bool need_old) {
     return sizeof(double) * (n + (need_old ? n : 0) + (L.uniform ? 0 : n) + 2 * L.nz + 1);
 }
 
-template <bool UNI, int SEG>
-static void hs_reg(const Lvl &L, dim3 g, int nw, double *u, const double *f, int color, double rho,
-                   int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
-    const size_t sm = sizeof(double) * (3 * L.nz + 1);
-    k_half_sweep_reg<UNI, SEG><<<g, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero,
-                                                      post_scale);
-}
 
 static int hs_variant() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("PMG_HS_VARIANT");
-        // 3: TMA solver warps (default), 2: producer/solver pipeline,
-        // 0: registers, 1: shared-memory
-        v = (e && e[0] == 't') ? 3 : (e && e[0] == 'r') ? 0 : (e && e[0] == 'p') ? 2 : 1;
+        // exact mode: 1 shared-memory RHS + lane-sequential Thomas (default),
+        // 3: TMA-fed solver warps
+        v = (e && e[0] == 't') ? 3 : 1;
     }
     return v;
 }
@@ -3423,13 +2219,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
     if (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) {
         const int nw = (L.nz + L.seg - 1) / L.seg;
         const size_t sm = sizeof(double) * (7 * (size_t)L.nz + 4 * 16 * 32);
-        const size_t sm1 = sizeof(double) * (7 * (size_t)L.nz + 2 * 2 * 8 * 32);
         const int ntiles = hx * L.ny;
-        static int var = -1;
-        if (var < 0) {
-            const char *e = getenv("PMG_SEG_VARIANT");
-            var = e ? atoi(e) : 0;
-        }
         auto run = [&](auto kern) {
             int occ = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
@@ -3438,29 +2228,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
                                             ntiles, hx);
         };
-        const size_t sms = sm + sizeof(double) * (size_t)L.nz * 32 - sizeof(double) * 16 * 32;
-        auto runs = [&](auto kern) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-                attr = true;
-            }
-            int occ = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sms);
-            const int cap = sm_count() * (occ > 0 ? occ : 1);
-            const int grid = ntiles < cap ? ntiles : cap;
-            kern<<<grid, 32 * nw, sms, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                             ntiles, hx);
-        };
-        auto run1 = [&](auto kern) {
-            int occ = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm1);
-            const int cap = sm_count() * (occ > 0 ? occ : 1);
-            const int grid = ntiles < cap ? ntiles : cap;
-            kern<<<grid, 32 * nw, sm1, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                             ntiles, hx);
-        };
-        if (var == 0 && cp_eligible(L) && !(L.hflags & 1)) {
+        if (cp_eligible(L) && !(L.hflags & 1)) {
             const int ht = ((L.nx + 1) / 2) / CP_TW;
             const int nt = ht * L.ny;
             const size_t smc = sizeof(double) * (3 * (size_t)L.nz * CP_ROW + 7 * (size_t)L.nz +
@@ -3476,9 +2244,9 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             }
             return cudaGetLastError();
         }
-        if (var == 0) {
-            // default: compile-time neighbour mode, predicate-free when the
-            // segments tile nz exactly (all BASELINE configs)
+        {
+            // compile-time neighbour mode, predicate-free when the segments
+            // tile nz exactly (all BASELINE configs)
             const bool full = (L.nz % L.seg) == 0;
             // compile-time plane stride for the large levels of nz = 128
             // (pitch of nx = 1024, 512, 256)
@@ -3516,39 +2284,6 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             *fused = true;
             return cudaGetLastError();
         }
-        if (var == 12) {
-            switch (L.seg) {
-            case 4: run1(k_half_sweep_seg1<4, 4, 2>); break;
-            case 8: run1(k_half_sweep_seg1<8, 4, 2>); break;
-            case 16: run1(k_half_sweep_seg1<16, 4, 2>); break;
-            default: run1(k_half_sweep_seg1<32, 4, 1>); break;
-            }
-            return cudaGetLastError();
-        }
-        switch (L.seg) {
-        case 4: run(k_half_sweep_seg<4, 4, 2>); break;
-        case 8: run(k_half_sweep_seg<8, 4, 2>); break;
-        case 16:
-            if (var == 10) {
-                if (L.nz % 16 == 0) {
-                    if (nbr_zero) run(k_half_sweep_seg<16, 4, 2, 1, true>);
-                    else run(k_half_sweep_seg<16, 4, 2, 0, true>);
-                } else {
-                    run(k_half_sweep_seg<16, 4, 2>);
-                }
-            } else if (var == 11) {
-                if (nbr_zero) run(k_half_sweep_seg<16, 8, 1, 1, true>);
-                else run(k_half_sweep_seg<16, 8, 1, 0, true>);
-            } else if (var == 1) run(k_half_sweep_seg<16, 8, 1>);
-            else if (var == 4) runs(k_half_sweep_segs<16, 4, 3>);
-            else if (var == 5) runs(k_half_sweep_segs<16, 8, 2>);
-            else if (var == 6) runs(k_half_sweep_segs<16, 4, 4>);
-            else if (var == 7) run1(k_half_sweep_seg1<16, 4, 3>);
-            else run(k_half_sweep_seg<16, 4, 2>);
-            break;
-        default: run(k_half_sweep_seg<32, 4, 1>); break;
-        }
-        return cudaGetLastError();
     }
     if (hs_variant() == 3 && L.uniform) {
         const int tab = (3 * L.nz + 1 + 1) & ~1;
@@ -3571,38 +2306,6 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
                                                         post_scale, ntiles, hx);
             return cudaGetLastError();
         }
-    }
-    if (hs_variant() == 2 && L.uniform) {
-        const size_t sm = sizeof(double) * (((3 * L.nz + 1 + 3) & ~3) + (size_t)PP_NBUF * L.nz * 32);
-        if (sm <= 220 * 1024) {
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_half_sweep_pipe,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-                attr = true;
-            }
-            const int ntiles = hx * L.ny;
-            const int grid = ntiles < 148 ? ntiles : 148;
-            k_half_sweep_pipe<<<grid, PP_THREADS, sm, st>>>(L, u, f, color, rho, zero_start,
-                                                            nbr_zero, post_scale, ntiles, hx);
-            return cudaGetLastError();
-        }
-    }
-    if (hs_variant() != 1 && L.nz <= 256) {
-        // SEG: k levels per warp, NW = ceil(nz / SEG) <= 8 warps
-        int seg = 4;
-        while (seg < 32 && (L.nz + seg - 1) / seg > 8) seg <<= 1;
-        const int nw = (L.nz + seg - 1) / seg;
-#define PMG_HS(U)                                                                        \
-        switch (seg) {                                                                    \
-        case 4: hs_reg<U, 4>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break;   \
-        case 8: hs_reg<U, 8>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break;   \
-        case 16: hs_reg<U, 16>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break; \
-        default: hs_reg<U, 32>(L, g, nw, u, f, color, rho, zero_start, nbr_zero, post_scale, st); break; \
-        }
-        if (L.uniform) { PMG_HS(true) } else { PMG_HS(false) }
-#undef PMG_HS
-        return cudaGetLastError();
     }
     const bool need_old = !zero_start && rho != 1.0;
     const size_t sm = half_sweep_smem(L, need_old);
@@ -3648,20 +2351,6 @@ cudaError_t launch_restrict(const Lvl &F, const Lvl &C, const double *fu, double
 cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double *fu, int add,
                            int cmask, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (getenv("PMG_PROLONG_B") != nullptr && cmask == 3) {   // column walker (slower on B200)
-        constexpr int PB = 4;
-        const int hx = ((F.nx + 1) / 2 + 31) / 32, jy = (F.ny + 3) / 4;
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_prolong_b<PB>, 256, 0);
-        const int cap = sm_count() * (occ > 0 ? occ : 1);
-        int kcs = F.nz;
-        while (kcs > 2 * PB && (long long)hx * jy * ((F.nz + kcs - 1) / kcs) < 2LL * cap) kcs >>= 1;
-        kcs = (kcs + PB - 1) / PB * PB;
-        const int ntiles = hx * jy * ((F.nz + kcs - 1) / kcs);
-        const int grid = ntiles < cap ? ntiles : cap;
-        k_prolong_b<PB><<<grid, 256, 0, st>>>(F, C, cu, fu, add, hx, ntiles, kcs);
-        return cudaGetLastError();
-    }
     const int n2 = (cmask == 3 ? 2 : 1) * ((F.nx + 1) / 2);
     if (F.hflags & 1)
         k_prolong<true><<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
