@@ -1630,6 +1630,73 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
     cu[cell(C, I, J, k)] = a;
 }
 
+// Prolongation + add, one thread per coarse column pair (fine nx a
+// multiple of 4): the fine 4 x 2 window of coarse cells (2m, J), (2m+1, J).
+// Per level and coarse row J-1 .. J+1 each lane loads e(2m) and e(2m+1)
+// (one element of each colour array, coalesced across lanes) and takes
+// e(2m-1), e(2m+2) from its neighbour lanes; the fine cells of the colours
+// in cmask are read and written as double2.  Same 9-3-3-1 arithmetic and
+// order as k_prolong (multigrid.py:233-245): bit-identical.
+__global__ void __launch_bounds__(128)
+k_prolong_q(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
+            int cmask) {
+    const int lane = threadIdx.x & 31;
+    const int npair = C.nx >> 1;
+    const int m0 = blockIdx.x * 128 + (threadIdx.x & ~31);   // first pair of this warp
+    if (m0 >= npair) return;
+    const int k = blockIdx.y, J = blockIdx.z;
+    const int nact = min(32, npair - m0);
+    const bool act = lane < nact;
+    const int m = m0 + (act ? lane : nact - 1);
+    const bool first = lane == 0, last = lane == nact - 1;
+    // coarse rows J-1, J, J+1: e(2m), e(2m+1) and the window edges e(2m-1), e(2m+2)
+    double e0[3], e1[3], el[3], er[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const int Y = J - 1 + d;
+        e0[d] = cu[cell(C, 2 * m, Y, k)];
+        e1[d] = cu[cell(C, 2 * m + 1, Y, k)];
+        const double xl = first ? cu[cell(C, 2 * m - 1, Y, k)] : 0.0;
+        const double xr = last ? cu[cell(C, 2 * m + 2, Y, k)] : 0.0;
+        el[d] = __shfl_up_sync(0xffffffffu, e1[d], 1);
+        er[d] = __shfl_down_sync(0xffffffffu, e0[d], 1);
+        if (first) el[d] = xl;
+        if (last) er[d] = xr;
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {           // fine rows 2J (dJ = -1), 2J+1 (dJ = +1)
+        const int j = 2 * J + r;
+        const int yn = r ? 2 : 0;           // coarse row J + dJ (J itself is index 1)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            if (!(cmask >> c & 1)) continue;
+            const int sc = (j + F.par + c) & 1;   // colour c at i = 4m + sc, 4m + 2 + sc
+            double v[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                // fine i - 4m = 2q + sc: I = 2m + q, I + dI by the parity sc
+                const double cc1 = q ? e1[1] : e0[1], ccn = q ? e1[yn] : e0[yn];
+                const double xc1 = sc ? (q ? er[1] : e1[1]) : (q ? e0[1] : el[1]);
+                const double xcn = sc ? (q ? er[yn] : e1[yn]) : (q ? e0[yn] : el[yn]);
+                double e = 9.0 * cc1;
+                e = e + 3.0 * xc1;
+                e = e + 3.0 * ccn;
+                e = e + xcn;
+                v[q] = e * 0.0625;
+            }
+            if (act) {
+                const long long qf = at(F, c, k, j, 2 * m);
+                if (add) {
+                    const D2 old = ld2(fu + qf);
+                    v[0] = old.x + v[0];
+                    v[1] = old.y + v[1];
+                }
+                *reinterpret_cast<double2 *>(fu + qf) = make_double2(v[0], v[1]);
+            }
+        }
+    }
+}
+
 template <bool HALO>
 __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu,
                           int add, int cmask) {
@@ -2351,6 +2418,12 @@ cudaError_t launch_restrict(const Lvl &F, const Lvl &C, const double *fu, double
 cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double *fu, int add,
                            int cmask, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!(F.hflags & 1) && F.nx % 4 == 0 && C.nx >= 2 && !getenv("PMG_PROLONG_NOQ")) {
+        const int npair = C.nx >> 1;
+        k_prolong_q<<<dim3((npair + 127) / 128, F.nz, C.ny), 128, 0, st>>>(F, C, cu, fu, add,
+                                                                           cmask);
+        return cudaGetLastError();
+    }
     const int n2 = (cmask == 3 ? 2 : 1) * ((F.nx + 1) / 2);
     if (F.hflags & 1)
         k_prolong<true><<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
