@@ -28,6 +28,10 @@ cudaError_t launch_invd(const Lvl &, double *, cudaStream_t);
 cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, double,
                             cudaStream_t);
 bool half_sweep_pro_ok(const Lvl &F);
+bool half_sweep_dot_ok(const Lvl &L);
+cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
+                                  int zero_start, int nbr_zero, double post_scale,
+                                  double *partials, int *np, cudaStream_t st);
 void setup_kernel_attributes();
 cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const double *f,
                                   const double *cu, int color, cudaStream_t st);
@@ -548,6 +552,22 @@ int pmg_ssor_apply(const pmg_level *lv, const double *r, double *z, double rho, 
     if (!(rho > 0.0 && rho < 2.0)) return fail(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
     if (rz_dev && !scratch) return fail(PMG_ERR_VALUE, "the <r, z> product needs a scratch buffer");
     int rc;
+    if (rz_dev && half_sweep_dot_ok(lv->L)) {
+        // <r, z> fused into the two half-sweeps that produce final values:
+        // black (final after the black sweep) and the last red sweep
+        cudaStream_t cs = (cudaStream_t)st;
+        int n1 = 0, n2 = 0;
+        if ((rc = pmg_half_sweep(lv, z, r, 0, rho, 1, 1, 1.0, st))) return rc;
+        if ((rc = pmg_halo_self(lv, z, periodic_x, periodic_y, st))) return rc;
+        PMG_CUDA(launch_half_sweep_dot(lv->L, z, r, 1, rho, 1, 0, 2.0 - rho, scratch, &n1, cs),
+                 "ssor black");
+        if ((rc = pmg_halo_self(lv, z, periodic_x, periodic_y, st))) return rc;
+        PMG_CUDA(launch_half_sweep_dot(lv->L, z, r, 0, rho, 0, 0, 1.0, scratch + n1, &n2, cs),
+                 "ssor red");
+        if ((rc = pmg_halo_self(lv, z, periodic_x, periodic_y, st))) return rc;
+        PMG_CUDA(launch_finalize(scratch, n1 + n2, rz_dev, cs), "ssor <r, z>");
+        return PMG_OK;
+    }
     // smoother.py:224-244: red from zero without neighbours, black from zero
     // scaled by (2 - rho), red; a halo refresh after each
     if ((rc = pmg_half_sweep(lv, z, r, 0, rho, 1, 1, 1.0, st))) return rc;

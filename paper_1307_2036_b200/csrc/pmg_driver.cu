@@ -305,11 +305,13 @@ int pmg_pcg_solve(const pmg_level *lv, const double *f, double *u, double eps, i
         ~Free() { cudaFreeHost(p); }
     } guard{res_h};
     TRYC(cudaHostGetDevicePointer((void **)&res_d, res_h, 0), "pinned scalars");
-    auto precondition = [&](void) -> int {
+    // z = M r and rz_dev[0] = <r, z> (fused into the SSOR half-sweeps)
+    auto precondition = [&](double *rz_dev) -> int {
         if (precond)
-            return pmg_ssor_apply(lv, r, z, rho, periodic_x, periodic_y, nullptr, nullptr, stream);
+            return pmg_ssor_apply(lv, r, z, rho, periodic_x, periodic_y, scratch, rz_dev, stream);
         TRY(pmg_copy(lv, z, r, stream));
-        return pmg_halo_self(lv, z, periodic_x, periodic_y, stream);
+        TRY(pmg_halo_self(lv, z, periodic_x, periodic_y, stream));
+        return pmg_dot(lv, r, z, scratch, rz_dev, stream);
     };
     auto read = [&](const double *dev, int k) -> int {
         TRYC(cudaMemcpyAsync(res_d, dev, k * sizeof(double), cudaMemcpyDeviceToDevice, st),
@@ -330,9 +332,8 @@ int pmg_pcg_solve(const pmg_level *lv, const double *f, double *u, double eps, i
         *converged = 1;
         return PMG_OK;
     }
-    TRY(precondition());
+    TRY(precondition(kap));
     TRY(pmg_copy(lv, p, z, stream));
-    TRY(pmg_dot(lv, r, z, scratch, kap, stream));
     TRY(read(kap, 1));
     if (!(res_h[0] > 0.0)) return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
     bool pending = false;
@@ -350,8 +351,7 @@ int pmg_pcg_solve(const pmg_level *lv, const double *f, double *u, double eps, i
             *converged = 1;
             break;
         }
-        TRY(precondition());
-        TRY(pmg_dot(lv, r, z, scratch, kapn, stream));
+        TRY(precondition(kapn));
         // u += (kappa / pq) p ; p = z + (kappa_new / kappa) p
         TRY(pmg_cg_step(n, kap, pq, kapn, kap, z, p, u, stream));
         pending = false;

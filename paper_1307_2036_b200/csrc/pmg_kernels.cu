@@ -964,12 +964,12 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // iota_k * rhs_k for this warp's levels: local forward, segment scan,
 // local backward, segment scan, fix-up, relaxation and store (+ halo
 // copies).  Shared by k_half_sweep_seg and k_half_sweep_pro.
-template <int SEG, bool HALO>
+template <int SEG, bool HALO, bool DOT = false>
 __device__ __forceinline__ void seg_solve_store(
     const Lvl &L, double *__restrict__ u, double (&r)[SEG], const double2 *ti,
     const double2 *tb, const double *tq, double *hend, double *ybeg, int c, int j, int h0,
     int s0, int i, int nact, int kn, long long pc, long long pl, int zero_start, double rho,
-    double scale, double omr) {
+    double scale, double omr, const double *__restrict__ f = nullptr, double *dacc = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int nz = L.nz;
     const int k0 = w * SEG;
@@ -1022,6 +1022,7 @@ __device__ __forceinline__ void seg_solve_store(
                 }
                 u[q] = y;
                 if (HALO) r[e] = y;
+                if (DOT) *dacc += f[q] * y;       // <rhs, new value> (CG's <r, z>)
             }
         }
     }
@@ -1036,10 +1037,13 @@ __device__ __forceinline__ void seg_solve_store(
 }
 
 template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false,
-          int PLC = 0>
+          int PLC = 0, bool DOT = false>
 __global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                 int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles) {
+                 int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles,
+                 double *__restrict__ dotp) {
+    // DOT: also dotp[blockIdx.x] = sum over this CTA's cells of f * (new u),
+    // fixed order (CG's <r, z> fused into the SSOR half-sweeps)
     // NBZ = 0/1: neighbours-zero mode fixed at compile time; FULL: every warp
     // owns exactly SEG levels (nz % SEG == 0) -- no per-level predicates;
     // PLC: the k-plane stride as a compile-time constant (0: runtime), so
@@ -1073,6 +1077,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     const int kn = FULL ? SEG : min(SEG, nz - k0);   // levels of this warp (may be <= 0)
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
+    double dacc = 0.0;
     int par = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
         double *hend = hend0 + par * 16 * 32;
@@ -1128,8 +1133,12 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                 }
             }
         }
-        seg_solve_store<SEG, HALO>(L, u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0, i, nact, kn, pc,
-                                   pl, zero_start, rho, scale, omr);
+        seg_solve_store<SEG, HALO, DOT>(L, u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0, i, nact,
+                                        kn, pc, pl, zero_start, rho, scale, omr, f, &dacc);
+    }
+    if (DOT) {
+        const double s2 = block_sum(dacc);
+        if (threadIdx.x == 0) dotp[blockIdx.x] = s2;
     }
 }
 
@@ -2174,6 +2183,41 @@ cudaError_t launch_half_sweep(const Lvl &L0, double *u, const double *f, int col
     return e;
 }
 
+// fast half-sweep with the fused <f, new u> partial sums (CG's <r, z>):
+// available for uniform levels whose 16-level segments tile nz (no fused
+// halo); partials[0 .. *np) receive per-CTA sums in a fixed order.
+bool half_sweep_dot_ok(const Lvl &L) {
+    return !g_smoother_exact && L.uniform && L.seg == 16 && L.nz % 16 == 0 && L.nz / 16 <= 8 &&
+           !(L.hflags & 1);
+}
+
+cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
+                                  int zero_start, int nbr_zero, double post_scale,
+                                  double *partials, int *np, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int hx = ((L.nx + 1) / 2 + 31) / 32;
+    const int nw = L.nz / 16;
+    const size_t sm = sizeof(double) * (7 * (size_t)L.nz + 4 * 16 * 32);
+    const int ntiles = hx * L.ny;
+    auto run = [&](auto kern) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        const int grid = ntiles < cap ? ntiles : cap;
+        *np = grid;
+        kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
+                                        ntiles, hx, partials);
+    };
+    if (nbr_zero) {
+        if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 1, true, false, 520, true>);
+        else run(k_half_sweep_seg<16, 4, 2, 1, true, false, 0, true>);
+    } else {
+        if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, true>);
+        else run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, true>);
+    }
+    return cudaGetLastError();
+}
+
 // fused coarse-grid correction + half-sweep (k_half_sweep_pro): available
 // in fast mode on uniform levels whose segments tile nz
 bool half_sweep_pro_ok(const Lvl &F) {
@@ -2293,7 +2337,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             const int cap = sm_count() * (occ > 0 ? occ : 1);
             const int grid = ntiles < cap ? ntiles : cap;
             kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                            ntiles, hx);
+                                            ntiles, hx, nullptr);
         };
         if (cp_eligible(L) && !(L.hflags & 1)) {
             const int ht = ((L.nx + 1) / 2) / CP_TW;
