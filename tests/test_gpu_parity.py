@@ -767,3 +767,38 @@ def test_staged_smoother_vs_exact(pmg, nx, nz, workers):
             runs[exact] = out
     for a, b in zip(runs[True], runs[False]):
         assert _close(b, a, 1e-12)
+
+
+@pytest.mark.parametrize("nx,nz", [(4, 1), (8, 2), (8, 3), (16, 5), (32, 17), (16, 33),
+                                   (32, 100), (8, 255), (8, 256), (8, 257), (8, 300)])
+def test_shapes_vs_oracle(pmg, nx, nz):
+    """Ragged and extreme vertical sizes (single level, odd nz, non-multiples
+    of the segment length, the 256-level limits of the batched kernels and
+    beyond): MG and SSOR-CG against the oracle, both smoother modes."""
+    from oracle import port
+    lv = port.uniform_levels(nz, 0.01)
+    nlev = min(3, int(np.log2(nx)) + 1)
+    fg = uni((nx, nx, nz), nz)
+    h = port.Hierarchy(nx, nx, nlev, lambda a, b: port.config_factors(a, b, lv), 1e-3, 1.0)
+    ou, orep = port.mg_solve(h, fg, eps=1e-6)
+    oc, crep = port.pcg_solve(h.levels[0], fg, eps=1e-6, maxiter=300)
+    grid = pmg.periodic_box(nx, nz, 0.01, lv)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    for exact, tol in ((True, 1e-10), (False, 1e-8)):
+        cfg = pmg.MGConfig(policy="explicit", explicit_levels=nlev, eps=1e-6)
+        hier = pmg.build_hierarchy(grid, params, cfg)
+        f = pmg.scatter_owned(fg, hier.fine.layout)
+        with pmg.exact_smoother(exact):
+            u, rep = pmg.mg_solve(f, hier, cfg)
+            op = hier.fine.op
+            uc, rc = pmg.pcg_solve(f, op, pmg.SSORPreconditioner(pmg.LineSmoother(op)),
+                                   eps=1e-6, maxiter=300)
+        assert rep.iterations == orep.iterations, exact
+        # relative agreement down to the residual evaluation's rounding floor
+        # (~1e-15 ||r0|| for the reassociated fast solver)
+        h, ref = np.array(rep.residual_history), np.array(orep.residual_history)
+        assert np.all(np.abs(h - ref) <= tol * ref + 1e-13 * ref[0]), (exact, h, ref)
+        ug = pmg.gather_owned(u)
+        assert np.max(np.abs(ug - ou[1:-1, 1:-1, :])) <= tol * max(1.0, np.max(np.abs(ug)))
+        assert abs(rc.iterations - crep.iterations) <= (0 if exact else 1)
+        assert rc.converged
