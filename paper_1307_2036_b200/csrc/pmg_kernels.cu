@@ -10,6 +10,8 @@
 #include <atomic>
 #include <cstdlib>
 
+#include <cudaTypedefs.h>
+
 #include "pmg_common.cuh"
 
 namespace pmg {
@@ -719,25 +721,7 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
 }
 
 
-// ---------------------------------------------------------------------------
-// Line smoother half-sweep, TMA-fed solver warps (exact mode, opt-in:
-// PMG_HS_VARIANT=t).
-//
-// Every warp of the persistent CTA is an independent pipeline over its own
-// sequence of tiles (32 columns of one row x nz levels):
-//   * lane 0 streams the tile's k-planes into a shared-memory ring of R
-//     slots with 1-D bulk TMA copies (cp.async.bulk ... complete_tx), one
-//     mbarrier per slot: per level the 34-element W/E row of the other
-//     colour, its S and N rows and the f row (1040 bytes).  The copies
-//     bypass L1 and need no registers, so ~R KB per warp are in flight;
-//   * the forward sweep waits on the slot, assembles the RHS exactly as
-//     smoother.py:137-145 and runs the elimination (smoother.py:151-156),
-//     keeping g[k] in a per-warp shared buffer;
-//   * the back substitution (smoother.py:157-161) + relaxation
-//     (smoother.py:163-170) streams x straight to HBM while the ring
-//     already fills with the next tile.
-// Arithmetic and order are the reference's: bit-identical results.
-// ---------------------------------------------------------------------------
+// shared-memory address and mbarrier helpers (TMA-fed kernels)
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -749,13 +733,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
-}
-__device__ __forceinline__ void tma_1d(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile(
@@ -770,70 +747,58 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-constexpr int TM_R = 16;          // ring slots (levels in flight) per warp
-constexpr int TM_ROW = 136;       // doubles per slot: W/E 36 | S 32 | N 32 | f 32 (+pad)
 
-struct TmaTile {
-    // geometry of one tile for the lane-0 issuer and the consumers
-    int j, h0, s0, nact;
+// ---------------------------------------------------------------------------
+// Line smoother half-sweep, EXACT arithmetic, fed by tensor-map TMA
+// (uniform coefficients).
+//
+// Every warp of the persistent CTA is an independent pipeline over its own
+// tiles (32 columns of one row x nz levels, lane = column): lane 0 streams
+// chunks of KC levels of the tile's four rows -- f, the other colour's W/E
+// row (36 wide), S and N -- into a ring of R shared-memory slots with one
+// 3-D cp.async.bulk.tensor box per row and chunk (mbarrier complete_tx),
+// R chunks ahead, across tile boundaries; the lanes run the reference's
+// sequential Thomas recurrence (smoother.py:137-170, same operation order as
+// k_half_sweep: bit-identical) and keep g in a per-warp [nz][32] buffer for
+// the back substitution, which streams x to HBM while the ring already
+// fills with the next tile.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *map, int x, int y, int z,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int KC>
+struct TxSlot {                  // doubles per ring slot: W [KC][36] S [KC][32] N [KC][32] F [KC][32]
+    static constexpr int W = 0, S = KC * 36, N = S + KC * 32, F = N + KC * 32, SIZE = F + KC * 32;
 };
 
-__device__ __forceinline__ TmaTile tma_tile(const Lvl &L, int t, int htiles, int c) {
-    TmaTile T;
-    T.j = t / htiles;
-    T.h0 = (t % htiles) * 32;
-    T.s0 = (T.j + L.par + c) & 1;
-    T.nact = min(32, ((L.nx - T.s0) + 1) / 2 - T.h0);
-    return T;
-}
-
-// lane 0: stage level k of tile T into ring slot
-__device__ __forceinline__ void tma_issue(const Lvl &L, const double *u, const double *f, int c,
-                                          int nbr_zero, const TmaTile &T, int k, double *slot,
-                                          uint64_t *bar) {
-    const int o = c ^ 1;
-    const int n = T.nact;
-    // f row: columns h0 .. h0+n-1 (16-byte granules: start is even)
-    const long long pf = at(L, c, k, T.j, T.h0);
-    const uint32_t fb = (uint32_t)(((n + 1) & ~1) * 8);
-    uint32_t tx = fb;
-    uint32_t wb = 0, sb = 0;
-    long long pw = 0;
-    if (!nbr_zero) {
-        // W/E row: h0 + s0 - 1 .. h0 + s0 + n - 1 ; aligned start a0
-        const int first = OFF + T.h0 + T.s0 - 1;        // element offset in the row
-        const int a0 = first & ~1;
-        const int last = OFF + T.h0 + T.s0 + n - 1;
-        wb = (uint32_t)(((last - a0 + 2) & ~1) * 8);
-        pw = at(L, o, k, T.j, 0) - OFF + a0;
-        sb = fb;
-        tx += wb + 2 * sb;
-    }
-    mbar_expect_tx(bar, tx);
-    tma_1d(slot + 100, f + pf, fb, bar);
-    if (!nbr_zero) {
-        tma_1d(slot, u + pw, wb, bar);
-        tma_1d(slot + 36, u + at(L, o, k, T.j - 1, T.h0), sb, bar);
-        tma_1d(slot + 68, u + at(L, o, k, T.j + 1, T.h0), sb, bar);
-    }
-}
-
+template <int KC, int R>
 __global__ void __launch_bounds__(128, 1)
-k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                 int zero_start, int nbr_zero, double post_scale, int ntiles, int htiles) {
-    extern __shared__ __align__(16) double tsm[];
+k_half_sweep_tx(Lvl L, double *__restrict__ u, int c, double rho, int zero_start, int nbr_zero,
+                double post_scale, int ntiles, int htiles,
+                const __grid_constant__ CUtensorMap mF, const __grid_constant__ CUtensorMap mW,
+                const __grid_constant__ CUtensorMap mSN) {
+    extern __shared__ __align__(128) double xsm_raw[];
+    // TMA destinations must be 128-byte aligned
+    double *xsm = xsm_raw + (((128u - (smem_u32(xsm_raw) & 127u)) & 127u) >> 3);
+    using SL = TxSlot<KC>;
     const int nz = L.nz;
     const int nw = blockDim.x >> 5;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // shared layout: tables | per warp { gbuf [nz][32] | ring [R][ROW] } | bars
-    double *tvp = tsm;
+    const int nch = nz / KC;                          // chunks per tile (KC divides nz)
+    // shared layout: per warp { ring [R][SL::SIZE] | gbuf [nz][32] } | tables | bars
+    const int per_warp = R * SL::SIZE + nz * 32;
+    double *ring = xsm + (size_t)warp * per_warp;
+    double *gbuf = ring + R * SL::SIZE;
+    double *tvp = xsm + (size_t)nw * per_warp;
     double *tinv = tvp + nz + 1;
     double *tdrw = tinv + nz;
-    const int tab = (3 * nz + 1 + 1) & ~1;
-    const int per_warp = nz * 32 + TM_R * TM_ROW;
-    double *gbuf = tsm + tab + (size_t)warp * per_warp;
-    double *ring = gbuf + nz * 32;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(tsm + tab + (size_t)nw * per_warp) + warp * TM_R;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tdrw + nz + ((3 * nz + 1) & 1)) + warp * R;
     for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
         tvp[t] = L.vprof[t];
         if (t < nz) {
@@ -842,7 +807,7 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         }
     }
     if (lane == 0)
-        for (int r = 0; r < TM_R; ++r) mbar_init(&bars[r], 1);
+        for (int r = 0; r < R; ++r) mbar_init(&bars[r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
@@ -850,65 +815,80 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     const double cv = L.csub0, wx0 = L.wx0, wy0 = L.wy0;
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
-    // issue stream: (tile q, level k) in order over this warp's tiles
-    int iq = warp, ik = 0;             // next level to issue
-    uint32_t iseq = 0, cseq = 0;       // issued / consumed level counters
+    const uint32_t txb = (uint32_t)(nbr_zero ? KC * 32 * 8 : SL::SIZE * 8);
+    // issue stream over (tile of this warp, chunk)
+    int iq = warp, ic = 0;
+    uint32_t iseq = 0, cseq = 0;
     auto issue_next = [&]() {
         const int t = blockIdx.x + iq * gridDim.x;
         if (t >= ntiles) return;
-        const TmaTile T = tma_tile(L, t, htiles, c);
-        const int slot = iseq % TM_R;
         if (lane == 0) {
+            const int j = t / htiles, h0 = (t - j * htiles) * 32;
+            double *sl = ring + (iseq % R) * SL::SIZE;
+            uint64_t *bar = &bars[iseq % R];
             fence_proxy_async();
-            tma_issue(L, u, f, c, nbr_zero, T, ik, ring + slot * TM_ROW, &bars[slot]);
+            mbar_expect_tx(bar, txb);
+            const int k0 = ic * KC;
+            tma_box3(sl + SL::F, &mF, OFF + h0, k0, j + 1, bar);
+            if (!nbr_zero) {
+                tma_box3(sl + SL::W, &mW, OFF + h0 - 2, k0, j + 1, bar);
+                tma_box3(sl + SL::S, &mSN, OFF + h0, k0, j, bar);
+                tma_box3(sl + SL::N, &mSN, OFF + h0, k0, j + 2, bar);
+            }
         }
         ++iseq;
-        if (++ik == nz) {
-            ik = 0;
+        if (++ic == nch) {
+            ic = 0;
             iq += nw;
         }
     };
-    for (int r = 0; r < TM_R; ++r) issue_next();
+    for (int r = 0; r < R; ++r) issue_next();
 
     for (int q = warp;; q += nw) {
         const int t = blockIdx.x + q * gridDim.x;
         if (t >= ntiles) break;
-        const TmaTile T = tma_tile(L, t, htiles, c);
-        const bool act = lane < T.nact;
-        const int dW = (OFF + T.h0 + T.s0 - 1) - ((OFF + T.h0 + T.s0 - 1) & ~1);
-        // ---- forward: RHS assembly + elimination ----
+        const int j = t / htiles, h0 = (t - j * htiles) * 32;
+        const int s0 = (j + L.par + c) & 1;
+        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
+        const bool act = lane < nact;
+        // ---- forward: RHS assembly + elimination, chunk by chunk ----
         double g = 0.0;
-        for (int k = 0; k < nz; ++k) {
-            const int slot = cseq % TM_R;
-            mbar_wait(&bars[slot], (cseq / TM_R) & 1);
-            const double *sl = ring + slot * TM_ROW;
-            double rhs;
-            if (nbr_zero) {
-                rhs = sl[100 + lane];
-            } else {
-                rhs = wx0 * sl[dW + lane];
-                rhs = rhs + wx0 * sl[dW + lane + 1];
-                rhs = rhs + wy0 * sl[36 + lane];
-                rhs = rhs + wy0 * sl[68 + lane];
-                rhs = rhs * tdrw[k];
-                rhs = rhs + sl[100 + lane];
+        for (int ch = 0; ch < nch; ++ch) {
+            const int slot = cseq % R;
+            mbar_wait(&bars[slot], (cseq / R) & 1);
+            const double *sl = ring + slot * SL::SIZE;
+#pragma unroll 4
+            for (int e = 0; e < KC; ++e) {
+                const int k = ch * KC + e;
+                double rhs;
+                if (nbr_zero) {
+                    rhs = sl[SL::F + e * 32 + lane];
+                } else {
+                    const double *wrow = sl + SL::W + e * 36;
+                    rhs = wx0 * wrow[lane + 1 + s0];
+                    rhs = rhs + wx0 * wrow[lane + 2 + s0];
+                    rhs = rhs + wy0 * sl[SL::S + e * 32 + lane];
+                    rhs = rhs + wy0 * sl[SL::N + e * 32 + lane];
+                    rhs = rhs * tdrw[k];
+                    rhs = rhs + sl[SL::F + e * 32 + lane];
+                }
+                if (k == 0) {
+                    g = rhs * tinv[0];
+                } else {
+                    double tt = g * cv;
+                    tt = tt * tvp[k];
+                    g = rhs + tt;
+                    g = g * tinv[k];
+                }
+                gbuf[k * 32 + lane] = g;
             }
-            if (k == 0) {
-                g = rhs * tinv[0];
-            } else {
-                double tt = g * cv;
-                tt = tt * tvp[k];
-                g = rhs + tt;
-                g = g * tinv[k];
-            }
-            gbuf[k * 32 + lane] = g;
             ++cseq;
             __syncwarp();
             issue_next();
         }
         // ---- backward + relaxation + store ----
         if (act) {
-            const long long pc = at(L, c, 0, T.j, T.h0 + lane);
+            const long long pc = at(L, c, 0, j, h0 + lane);
             double x = g;
             const int top = ((nz - 1) / 8) * 8;
             for (int kb = top; kb >= 0; kb -= 8) {
@@ -958,7 +938,7 @@ k_half_sweep_tma(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // full L1 available -- no serial chain, no large shared buffers.  Same
 // operator and RHS as smoother.py:137-170; reassociated elimination
 // (agrees with the sequential solve to ~1e-15 relative; the exact mode is
-// k_half_sweep_tma / k_half_sweep).
+// k_half_sweep / k_half_sweep_tx).
 // ---------------------------------------------------------------------------
 // Column solve of one tile of the k-segmented smoother, given r[e] =
 // iota_k * rhs_k for this warp's levels: local forward, segment scan,
@@ -2158,8 +2138,8 @@ static int hs_variant() {
     if (v < 0) {
         const char *e = getenv("PMG_HS_VARIANT");
         // exact mode: 1 shared-memory RHS + lane-sequential Thomas (default),
-        // 3: TMA-fed solver warps
-        v = (e && e[0] == 't') ? 3 : 1;
+        // 4: tensor-map TMA solver warps (opt-in: measured slower)
+        v = (e && e[0] == 'x') ? 4 : 1;
     }
     return v;
 }
@@ -2294,6 +2274,71 @@ static bool cp_eligible(const Lvl &L) {
            L.nx % 32 == 0 && L.pitch >= OFF + L.nx / 2 + 4;
 }
 
+// tensor maps for k_half_sweep_tx: 3-D views (pitch, nz, ny + 2) of one
+// colour array with a box of boxw columns x kc levels x 1 row
+static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+static bool make_tmap(CUtensorMap *m, const double *base, const Lvl &L, int boxw, int kc) {
+    auto enc = tmap_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)L.plane, (cuuint64_t)L.nz, (cuuint64_t)L.ny + 2};
+    const cuuint64_t strides[2] = {(cuuint64_t)L.plane * 8, (cuuint64_t)L.jstride * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)boxw, (cuuint32_t)kc, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double *>(base), dims, strides,
+               box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// k_half_sweep_tx launch (exact arithmetic); false if not applicable here
+static bool launch_half_sweep_tx(const Lvl &L, double *u, const double *f, int color, double rho,
+                                 int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
+    static int cfg = -1;
+    if (cfg < 0) {
+        const char *e = getenv("PMG_TX");          // tuning: 8 (KC 8, 3 warps) / 16 (KC 16, 2 warps)
+        cfg = e ? atoi(e) : 16;
+    }
+    const int kc = (cfg == 8) ? 8 : 16;
+    if (!L.uniform || L.nz % kc != 0 || L.nz > 256 || (L.hflags & 1)) return false;
+    const int o = color ^ 1;
+    CUtensorMap mF, mW, mSN;
+    if (!make_tmap(&mF, f + (long long)color * L.cstride, L, 32, kc) ||
+        !make_tmap(&mW, u + (long long)o * L.cstride, L, 36, kc) ||
+        !make_tmap(&mSN, u + (long long)o * L.cstride, L, 32, kc))
+        return false;
+    const int hx = ((L.nx + 1) / 2 + 31) / 32;
+    const int ntiles = hx * L.ny;
+    auto run = [&](auto kern, int nw, int R) {
+        const size_t slot = (size_t)kc * 132;
+        const size_t per_warp = R * slot + (size_t)L.nz * 32;
+        const size_t sm = 8 * (nw * per_warp + 3 * (size_t)L.nz + 2) + 8 * (size_t)nw * R + 128;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        int grid = (ntiles + nw - 1) / nw;
+        if (grid > sm_count()) grid = sm_count();
+        kern<<<grid, 32 * nw, sm, st>>>(L, u, color, rho, zero_start, nbr_zero, post_scale,
+                                        ntiles, hx, mF, mW, mSN);
+    };
+    if (kc == 8) run(k_half_sweep_tx<8, 4>, 3, 4);
+    else run(k_half_sweep_tx<16, 3>, 2, 3);
+    return true;
+}
+
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
                                        double post_scale, cudaStream_t st, bool *fused) {
@@ -2396,28 +2441,9 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             return cudaGetLastError();
         }
     }
-    if (hs_variant() == 3 && L.uniform) {
-        const int tab = (3 * L.nz + 1 + 1) & ~1;
-        const size_t per_warp = (size_t)L.nz * 32 + TM_R * TM_ROW;
-        const size_t budget = 225 * 1024;
-        int nw = (int)((budget / 8 - tab) / (per_warp + TM_R));
-        if (nw > 4) nw = 4;
-        if (nw >= 1) {
-            const size_t sm = 8 * (tab + nw * per_warp) + 8 * (size_t)nw * TM_R;
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(k_half_sweep_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024);
-                attr = true;
-            }
-            const int ntiles = hx * L.ny;
-            int grid = (ntiles + nw - 1) / nw;
-            if (grid > 148) grid = 148;
-            k_half_sweep_tma<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero,
-                                                        post_scale, ntiles, hx);
-            return cudaGetLastError();
-        }
-    }
+    if (hs_variant() == 4 && L.uniform &&
+        launch_half_sweep_tx(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st))
+        return cudaGetLastError();
     const bool need_old = !zero_start && rho != 1.0;
     const size_t sm = half_sweep_smem(L, need_old);
     const dim3 b(HS_THREADS);
