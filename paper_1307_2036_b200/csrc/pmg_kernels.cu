@@ -2409,17 +2409,17 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             const int plc = (L.seg == 16 && full && !(L.hflags & 1)) ? (int)L.plane : 0;
 #define PMG_SEGP(S, P)                                                                \
     do {                                                                              \
-        if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true, false, P>);             \
-        else run(k_half_sweep_seg<S, 4, 2, 0, true, false, P>);                      \
+        if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, false, P>);             \
+        else run(k_half_sweep_seg<S, 4, 3, 0, true, false, P>);                      \
     } while (0)
 #define PMG_SEGF(S)                                                                   \
     do {                                                                              \
         if (full && (L.hflags & 1)) {                                                 \
-            if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true, true>);              \
-            else run(k_half_sweep_seg<S, 4, 2, 0, true, true>);                       \
+            if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, true>);              \
+            else run(k_half_sweep_seg<S, 4, 3, 0, true, true>);                       \
         } else if (full) {                                                            \
-            if (nbr_zero) run(k_half_sweep_seg<S, 4, 2, 1, true>);                    \
-            else run(k_half_sweep_seg<S, 4, 2, 0, true>);                             \
+            if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true>);                    \
+            else run(k_half_sweep_seg<S, 4, 3, 0, true>);                             \
         } else if (L.hflags & 1) {                                                    \
             run(k_half_sweep_seg<S, 4, 2, -1, false, true>);                          \
         } else {                                                                      \
