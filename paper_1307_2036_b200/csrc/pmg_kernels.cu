@@ -340,6 +340,108 @@ k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
     }
 }
 
+// Convergence norm ||f - A u||^2 (uniform coefficients, nz a multiple of
+// KB): k_apply_v's column-pair tiles with a lean inner loop -- the k-plane
+// stride a compile-time constant (PLC, 0 = runtime), per-level tables read
+// once for both cells, the vertical couplings as zero-padded tables
+// (bm[k] = band[k] for k >= 1 else 0, bp[k] = band[k+1] for k < nz-1 else 0)
+// so no per-cell predicates.  Same operation order as cell_res (the padded
+// terms subtract an exact zero).  Partial sums per CTA in a fixed order.
+template <int KB, int PLC, int MINB>
+__global__ void __launch_bounds__(32 * 2 * AP_TY, MINB)
+k_norm_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
+         double *__restrict__ partials, int hx, int jy, int ntiles, int kcs) {
+    __shared__ double s_drw[256], s_dg[256], s_bm[256], s_bp[256];
+    const int nz = L.nz;
+    for (int t = threadIdx.x + blockDim.x * threadIdx.y; t < nz; t += blockDim.x * blockDim.y) {
+        s_drw[t] = L.drw[t];
+        s_dg[t] = L.diag1[t];
+        s_bm[t] = (t >= 1) ? L.band1[t] : 0.0;
+        s_bp[t] = (t + 1 < nz) ? L.band1[t + 1] : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x;
+    const int c = threadIdx.y & 1;
+    const int o = c ^ 1;
+    const long long pl = PLC ? (long long)PLC : L.plane;
+    const int nkc = nz / kcs;
+    const double wx = L.wx0, wy = L.wy0;
+    double acc2 = 0.0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int kcI = tile % nkc;
+        const int t2 = tile / nkc;
+        const int jb = t2 / hx;
+        const int hb = t2 - jb * hx;
+        const int j = jb * AP_TY + (threadIdx.y >> 1);
+        if (j >= L.ny) continue;
+        const int s = (j + L.par + c) & 1;
+        const int ncol = ((L.nx - s) + 1) / 2;
+        const int m = hb * 32 + lane;
+        const bool act = 2 * m < ncol;
+        const int mm = act ? m : (ncol - 1) / 2;
+        const int h = 2 * mm;
+        const bool two = act && (h + 1 < ncol);
+        const int kbeg = kcI * kcs, kend = kbeg + kcs;
+        const double *pc = u + at(L, c, kbeg, j, h);
+        const double *pf = f + at(L, c, kbeg, j, h);
+        const double *po = u + at(L, o, kbeg, j, h);
+        const double *pS = u + at(L, o, kbeg, j - 1, h);
+        const double *pN = u + at(L, o, kbeg, j + 1, h);
+        const double *px = u + at(L, o, kbeg, j, s ? h + 2 : h - 1);
+        D2 um = ld2(pc - ((kbeg > 0) ? pl : 0));
+        for (int k0 = kbeg; k0 < kend; k0 += KB) {
+            D2 uc[KB + 1], vo[KB], vs[KB], vn[KB], vf[KB];
+            double vx[KB];
+#pragma unroll
+            for (int t = 0; t < KB; ++t) {
+                uc[t] = ld2(pc + t * pl);
+                vo[t] = ld2(po + t * pl);
+                vx[t] = px[t * pl];
+                vs[t] = ld2(pS + t * pl);
+                vn[t] = ld2(pN + t * pl);
+                vf[t] = ld2(pf + t * pl);
+            }
+            uc[KB] = ld2(pc + ((k0 + KB < nz) ? KB * pl : (KB - 1) * pl));
+#pragma unroll
+            for (int t = 0; t < KB; ++t) {
+                const int k = k0 + t;
+                const double drw = s_drw[k], dg = s_dg[k], bm = s_bm[k], bp = s_bp[k];
+                const D2 ul = t ? uc[t - 1] : um;
+                const double wa = s ? vo[t].x : vx[t];
+                const double ea = s ? vo[t].y : vo[t].x;
+                const double eb = s ? vx[t] : vo[t].y;
+                double a0 = wx * wa;
+                a0 = a0 + wx * ea;
+                a0 = a0 + wy * vs[t].x;
+                a0 = a0 + wy * vn[t].x;
+                a0 = a0 * drw;
+                double r0 = dg * uc[t].x - a0;
+                r0 = r0 - bm * ul.x;
+                r0 = r0 - bp * uc[t + 1].x;
+                r0 = vf[t].x - r0;
+                double a1 = wx * ea;
+                a1 = a1 + wx * eb;
+                a1 = a1 + wy * vs[t].y;
+                a1 = a1 + wy * vn[t].y;
+                a1 = a1 * drw;
+                double r1 = dg * uc[t].y - a1;
+                r1 = r1 - bm * ul.y;
+                r1 = r1 - bp * uc[t + 1].y;
+                r1 = vf[t].y - r1;
+                if (act) {
+                    acc2 += r0 * r0;
+                    if (two) acc2 += r1 * r1;
+                }
+            }
+            um = uc[KB - 1];
+            pc += KB * pl; pf += KB * pl; po += KB * pl; pS += KB * pl; pN += KB * pl;
+            px += KB * pl;
+        }
+    }
+    const double s2 = block_sum(acc2);
+    if (threadIdx.x == 0 && threadIdx.y == 0) partials[blockIdx.x] = s2;
+}
+
 // Vectorised residual + children-sum restriction (uniform): tile = 64
 // coarse columns I (= fine h) of coarse row J; warp (row rr, colour c)
 // computes the residual of fine columns h = 2m, 2m+1 in fine row 2J + rr;
@@ -2026,6 +2128,32 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
         return cudaGetLastError();
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (mode == 1 && partials && !out && L.uniform && L.nz % 4 == 0 && L.nz <= 256 &&
+        !getenv("PMG_NORM_NOV")) {
+        constexpr int KB = 4;
+        const int hx = ((L.nx + 1) / 2 + 63) / 64, jy = (L.ny + AP_TY - 1) / AP_TY;
+        static int mb = -1;
+        if (mb < 0) { const char *e = getenv("PMG_NORM_MB"); mb = e ? atoi(e) : 2; }
+        auto go = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * 2 * AP_TY, 0);
+            const int cap = sm_count() * (occ > 0 ? occ : 1);
+            int kcs = L.nz;
+            while (kcs > 2 * KB && kcs % (2 * KB) == 0 &&
+                   (long long)hx * jy * (L.nz / kcs) < 2LL * cap)
+                kcs >>= 1;
+            const int ntiles = hx * jy * (L.nz / kcs);
+            const int grid = ntiles < cap ? ntiles : cap;
+            *nparts = grid;
+            kern<<<grid, dim3(32, 2 * AP_TY), 0, st>>>(L, u, f, partials, hx, jy, ntiles, kcs);
+        };
+        if (L.plane == 520) {
+            if (mb == 3) go(k_norm_v<KB, 520, 3>); else go(k_norm_v<KB, 520, 2>);
+        } else {
+            if (mb == 3) go(k_norm_v<KB, 0, 3>); else go(k_norm_v<KB, 0, 2>);
+        }
+        return cudaGetLastError();
+    }
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
     if (apply_variant() == 0 && L.nz <= 256 && getenv("PMG_APPLY_V0") == nullptr) {
