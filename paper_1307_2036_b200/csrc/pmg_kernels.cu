@@ -347,10 +347,13 @@ k_apply_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
 // (bm[k] = band[k] for k >= 1 else 0, bp[k] = band[k+1] for k < nz-1 else 0)
 // so no per-cell predicates.  Same operation order as cell_res (the padded
 // terms subtract an exact zero).  Partial sums per CTA in a fixed order.
-template <int KB, int PLC, int MINB>
+// MODE 1: ||f - A u||^2 only; MODE 2: out = A u and u . (A u) (CG's
+// q = A p with <p, q>, krylov.py:139-140).
+template <int KB, int PLC, int MINB, int MODE = 1>
 __global__ void __launch_bounds__(32 * 2 * AP_TY, MINB)
 k_norm_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
-         double *__restrict__ partials, int hx, int jy, int ntiles, int kcs) {
+         double *__restrict__ partials, int hx, int jy, int ntiles, int kcs,
+         double *__restrict__ out) {
     __shared__ double s_drw[256], s_dg[256], s_bm[256], s_bp[256];
     const int nz = L.nz;
     for (int t = threadIdx.x + blockDim.x * threadIdx.y; t < nz; t += blockDim.x * blockDim.y) {
@@ -399,7 +402,7 @@ k_norm_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
                 vx[t] = px[t * pl];
                 vs[t] = ld2(pS + t * pl);
                 vn[t] = ld2(pN + t * pl);
-                vf[t] = ld2(pf + t * pl);
+                if (MODE == 1) vf[t] = ld2(pf + t * pl);
             }
             uc[KB] = ld2(pc + ((k0 + KB < nz) ? KB * pl : (KB - 1) * pl));
 #pragma unroll
@@ -418,7 +421,7 @@ k_norm_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
                 double r0 = dg * uc[t].x - a0;
                 r0 = r0 - bm * ul.x;
                 r0 = r0 - bp * uc[t + 1].x;
-                r0 = vf[t].x - r0;
+                if (MODE == 1) r0 = vf[t].x - r0;
                 double a1 = wx * ea;
                 a1 = a1 + wx * eb;
                 a1 = a1 + wy * vs[t].y;
@@ -427,10 +430,18 @@ k_norm_v(Lvl L, const double *__restrict__ u, const double *__restrict__ f,
                 double r1 = dg * uc[t].y - a1;
                 r1 = r1 - bm * ul.y;
                 r1 = r1 - bp * uc[t + 1].y;
-                r1 = vf[t].y - r1;
+                if (MODE == 1) r1 = vf[t].y - r1;
                 if (act) {
-                    acc2 += r0 * r0;
-                    if (two) acc2 += r1 * r1;
+                    if (MODE == 1) {
+                        acc2 += r0 * r0;
+                        if (two) acc2 += r1 * r1;
+                    } else {
+                        const long long q = (pc - u) + t * pl;
+                        if (two) *reinterpret_cast<double2 *>(out + q) = make_double2(r0, r1);
+                        else out[q] = r0;
+                        acc2 += uc[t].x * r0;
+                        if (two) acc2 += uc[t].y * r1;
+                    }
                 }
             }
             um = uc[KB - 1];
@@ -2128,8 +2139,8 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
         return cudaGetLastError();
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (mode == 1 && partials && !out && L.uniform && L.nz % 4 == 0 && L.nz <= 256 &&
-        !getenv("PMG_NORM_NOV")) {
+    if (((mode == 1 && !out) || mode == 2) && partials && L.uniform && L.nz % 4 == 0 &&
+        L.nz <= 256 && !getenv("PMG_NORM_NOV")) {
         constexpr int KB = 4;
         const int hx = ((L.nx + 1) / 2 + 63) / 64, jy = (L.ny + AP_TY - 1) / AP_TY;
         static int mb = -1;
@@ -2145,9 +2156,13 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
             const int ntiles = hx * jy * (L.nz / kcs);
             const int grid = ntiles < cap ? ntiles : cap;
             *nparts = grid;
-            kern<<<grid, dim3(32, 2 * AP_TY), 0, st>>>(L, u, f, partials, hx, jy, ntiles, kcs);
+            kern<<<grid, dim3(32, 2 * AP_TY), 0, st>>>(L, u, f, partials, hx, jy, ntiles, kcs,
+                                                       out);
         };
-        if (L.plane == 520) {
+        if (mode == 2) {
+            if (L.plane == 520) go(k_norm_v<KB, 520, 2, 2>);
+            else go(k_norm_v<KB, 0, 2, 2>);
+        } else if (L.plane == 520) {
             if (mb == 3) go(k_norm_v<KB, 520, 3>); else go(k_norm_v<KB, 520, 2>);
         } else {
             if (mb == 3) go(k_norm_v<KB, 0, 3>); else go(k_norm_v<KB, 0, 2>);
