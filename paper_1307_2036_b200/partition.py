@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import torch
@@ -384,10 +385,9 @@ def self_halo_flags(lay: "LevelLayout") -> int:
     return 0
 
 
-import os as _os
 # fused halos measured slower on B200 for configs[1] (boundary-tile epilogue
 # imbalances the persistent smoother grid): opt-in
-_FUSED_HALO = bool(_os.environ.get("PMG_FUSED_HALO"))
+_FUSED_HALO = bool(os.environ.get("PMG_FUSED_HALO"))
 
 
 def set_fused_halo(on: bool) -> bool:
