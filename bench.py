@@ -268,6 +268,9 @@ def main():
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = lib.pmg_launch_count()
+    from paper_1307_2036_b200 import multigrid as mgm
+    native = lay.px == 1 and lay.py == 1 and mgm.USE_NATIVE
+    r0_graph = hier.native(cfg).replayed_launches() if native else 0
     sampler = ClockSampler(local)
     iters = []
     with sampler:
@@ -283,15 +286,10 @@ def main():
     t = max_over_ranks(t_local, world)
     launches_lib = lib.pmg_launch_count() - l0
     # kernels replayed from the captured V-cycle graphs (first cycle + the rest)
-    from paper_1307_2036_b200 import multigrid as mgm
     gpu_launches = launches_lib
-    if lay.px == 1 and lay.py == 1 and mgm.USE_NATIVE:
-        # single part: the C++ driver's graphs (pmg_mg_solve)
-        nh = hier.native(cfg)
-        fp, up = f.parts[w].ptr, u.parts[w].ptr
-        l_first, l_rest = nh.graph_launches(fp, up, True), nh.graph_launches(fp, up, False)
-        for n_it in iters:
-            gpu_launches += (l_first + (n_it - 1) * l_rest) if l_first >= 0 else n_it * l_rest
+    if native:
+        # single part: the C++ driver counts the kernels of its graph replays
+        gpu_launches += hier.native(cfg).replayed_launches() - r0_graph
     else:
         gkey = (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
                 mgm._ptrs(f), mgm._ptrs(u))

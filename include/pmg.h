@@ -147,6 +147,19 @@ int pmg_get_smoother_mode(void);
 int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
                    double rho, int zero_start, int neighbors_zero, double post_scale,
                    void *stream);
+/* red half sweep (rho = 1) fused with the convergence residual of the
+ * iterate it relaxes: reads u, writes the relaxed red values into the red
+ * array of u_new (u_new's black array is not touched; u_new != u), and
+ * norm2_dev[0] = sum over u's RED owned cells of (f - A u)^2 (fixed order,
+ * scratch: pmg_partials_size() doubles).  After a V-cycle whose last
+ * half-sweep relaxed black lines exactly (rho = 1) the black residual is
+ * zero, so this is the next cycle's first half-sweep and the previous
+ * cycle's ||f - A u||^2 in one pass (multigrid.py:322-324 + smoother.py:
+ * 184-186).  Fast mode, uniform coefficients, nz a multiple of 16
+ * (<= 128); PMG_ERR_VALUE otherwise. */
+int pmg_half_sweep_res(const pmg_level *lvl, const double *u, double *u_new, const double *f,
+                       double *scratch, double *norm2_dev, void *stream);
+int pmg_half_sweep_res_ok(const pmg_level *lvl);
 
 /* z = M^-1 r, symmetric red-black block SSOR from zero for a part that is
  * its own neighbour (LineSmoother.ssor_apply, smoother.py:224-244): red
@@ -249,6 +262,14 @@ typedef struct pmg_mg_desc {
     int coarse_sweeps;         /* red-black sweeps on the coarsest level             */
     double rho;                /* overrelaxation weight, (0, 2)                      */
     int periodic_x, periodic_y;
+    /* 1: lagged convergence norm -- each cycle's ||f - A u|| is summed by
+     * the next cycle's first red half-sweep (pmg_half_sweep_res; the new
+     * red values go to a second red array, so the converged iterate is
+     * never touched).  Needs rho = 1, nu_pre, nu_post >= 1, two levels and
+     * pmg_half_sweep_res_ok(levels[0]); ignored otherwise.  Same iterates
+     * bit for bit; the history omits the black cells' rounding-level
+     * residual. */
+    int lagged_norm;
 } pmg_mg_desc;
 /* levels[0] finest ... levels[nlev-1] coarsest, each halving nx and ny */
 int pmg_hier_create(const pmg_level *const *levels, int nlev, const pmg_mg_desc *desc,
@@ -267,6 +288,8 @@ int pmg_mg_solve(pmg_hier *hier, const double *f, double *u, double eps, int max
  * none (launch accounting: graph replays issue no host-side launches) */
 long long pmg_hier_graph_launches(const pmg_hier *hier, const double *f, const double *u,
                                   int first);
+/* cumulative kernels issued by this hierarchy's graph replays */
+long long pmg_hier_replayed_launches(const pmg_hier *hier);
 /* preconditioned CG from u = 0 (krylov.py:88-167): precond 1 = SSOR(rho),
  * 0 = identity; tau as the reference (tiny-residual cut-off).  work: device
  * buffer of pmg_pcg_work_doubles() doubles; hist as pmg_mg_solve.

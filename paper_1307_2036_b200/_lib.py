@@ -24,6 +24,7 @@ class MGDesc(C.Structure):
     _fields_ = [
         ("nu_pre", C.c_int), ("nu_post", C.c_int), ("coarse_sweeps", C.c_int),
         ("rho", C.c_double), ("periodic_x", C.c_int), ("periodic_y", C.c_int),
+        ("lagged_norm", C.c_int),
     ]
 
 
@@ -67,6 +68,7 @@ SIGNATURES = {
     "pmg_hier_create": (_I, [C.POINTER(_P), _I, C.POINTER(MGDesc), C.POINTER(_P)]),
     "pmg_hier_destroy": (_I, [_P]),
     "pmg_hier_graph_launches": (_LL, [_P, _P, _P, _I]),
+    "pmg_hier_replayed_launches": (_LL, [_P]),
     "pmg_vcycle": (_I, [_P, _P, _P, _I, _P]),
     "pmg_mg_solve": (_I, [_P, _P, _P, _D, _I, _P, C.POINTER(_I), C.POINTER(_I), _P]),
     "pmg_pcg_work_doubles": (_LL, [_P]),
@@ -79,6 +81,8 @@ SIGNATURES = {
     "pmg_apply_dot": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_residual_restrict": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_half_sweep": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _P]),
+    "pmg_half_sweep_res": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "pmg_half_sweep_res_ok": (_I, [_P]),
     "pmg_set_smoother_mode": (_I, [_I]),
     "pmg_get_smoother_mode": (_I, []),
     "pmg_restrict": (_I, [_P, _P, _P, _P, _D, _P]),

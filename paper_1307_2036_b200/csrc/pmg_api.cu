@@ -29,6 +29,9 @@ cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, 
                             cudaStream_t);
 bool half_sweep_pro_ok(const Lvl &F);
 bool half_sweep_dot_ok(const Lvl &L);
+bool half_sweep_res_ok(const Lvl &L);
+cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
+                                  double *partials, int *np, cudaStream_t st);
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
                                   int zero_start, int nbr_zero, double post_scale,
                                   double *partials, int *np, cudaStream_t st);
@@ -79,6 +82,16 @@ static int fail(int code, const std::string &msg) {
 namespace pmg {
 // error reporting for the other translation units of the library
 int set_error(int code, const char *msg) { return fail(code, msg); }
+// driver-internal view of a level whose black array lies `cstride` doubles
+// from the red one (a red array in another allocation); shares the level's
+// device tables, owns nothing
+pmg_level *level_view(const pmg_level *lv, long long cstride) {
+    pmg_level *v = new pmg_level(*lv);
+    v->owned.clear();
+    v->L.cstride = cstride;
+    return v;
+}
+void level_view_free(pmg_level *v) { delete v; }
 }
 
 static int cuda_fail(cudaError_t e, const char *where) {
@@ -155,6 +168,7 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
     L.plane = L.pitch;
     L.jstride = (long long)nz * L.pitch;
     L.cstride = (long long)(ny + 2) * L.jstride;
+    L.fcs = L.cstride;
     L.par = (d->i0 + d->j0) & 1;
     L.omega2 = d->omega2;
     L.vcoef = d->vcoef;
@@ -380,6 +394,23 @@ int pmg_half_sweep(const pmg_level *lv, double *u, const double *f, int color, d
     PMG_CUDA(launch_half_sweep(lv->L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
                                (cudaStream_t)st),
              "half_sweep");
+    return PMG_OK;
+}
+
+int pmg_half_sweep_res_ok(const pmg_level *lv) { return lv && half_sweep_res_ok(lv->L) ? 1 : 0; }
+
+int pmg_half_sweep_res(const pmg_level *lv, const double *u, double *u_new, const double *f,
+                       double *scratch, double *norm2, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (!u || !u_new || !f || !scratch || !norm2) return fail(PMG_ERR_VALUE, "null argument");
+    if (u == u_new) return fail(PMG_ERR_VALUE, "u_new must be a different buffer from u");
+    if (!half_sweep_res_ok(lv->L))
+        return fail(PMG_ERR_VALUE, "fused sweep + residual needs fast mode, uniform "
+                                   "coefficients and nz a multiple of 16 (<= 128)");
+    int np = 0;
+    PMG_CUDA(launch_half_sweep_res(lv->L, u, u_new, f, scratch, &np, (cudaStream_t)st),
+             "half_sweep_res");
+    PMG_CUDA(launch_finalize(scratch, np, norm2, (cudaStream_t)st), "half_sweep_res norm");
     return PMG_OK;
 }
 

@@ -15,6 +15,9 @@ struct Lvl {
     long long plane;     // stride between vertical levels k (= pitch)
     long long jstride;   // stride between rows j (= nz * pitch)
     long long cstride;   // stride between the two colour arrays
+    long long fcs;       // the same for right-hand sides f (= cstride, except in
+                         // the lagged-norm driver's view of a red array held
+                         // in another allocation: pmg_driver.cu)
     double omega2, vcoef;
     // uniform coefficients (2-D factors constant)
     double wx0, wy0, csub0;

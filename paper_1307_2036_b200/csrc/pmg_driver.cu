@@ -9,6 +9,8 @@
 // Operation sequence = the Python drivers' fused path (multigrid.v_cycle
 // with cfg.fused, krylov.pcg_solve), so both give bit-identical results.
 #include <cmath>
+#include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +21,8 @@
 
 namespace pmg {
 int set_error(int code, const char *msg);
+pmg_level *level_view(const pmg_level *lv, long long cstride);
+void level_view_free(pmg_level *v);
 }
 
 namespace {
@@ -43,7 +47,7 @@ int cuda_err(cudaError_t e, const char *where) {
 struct Graph {
     const double *f;
     double *u;
-    int first;
+    int first;   // 0/1: cycle + norm (first = zero start); >= 2: lagged-norm kinds
     cudaStream_t st;
     cudaGraphExec_t exec;
     long long launches;   // library kernels recorded in the graph
@@ -60,6 +64,11 @@ struct pmg_hier {
     double *res_h = nullptr;         // host-mapped scalars [8]
     double *res_d = nullptr;
     std::vector<Graph> graphs;
+    long long replayed = 0;          // kernels issued by graph replays
+    // lagged norm: the second fine red array and the iteration count of the
+    // previous solve (chooses which red array the first cycle writes)
+    double *red1 = nullptr;
+    int last_iters = 4;
     // the legacy default stream cannot be captured: solves issued on it run
     // on this stream, ordered after / before the caller's work by events
     cudaStream_t own = nullptr;
@@ -75,6 +84,7 @@ void free_hier(pmg_hier *h) {
         cudaFree(h->f[c]);
     }
     if (h->scratch) cudaFree(h->scratch);
+    if (h->red1) cudaFree(h->red1);
     if (h->res_h) cudaFreeHost(h->res_h);
     if (h->own) cudaStreamDestroy(h->own);
     if (h->ev_in) cudaEventDestroy(h->ev_in);
@@ -82,46 +92,62 @@ void free_hier(pmg_hier *h) {
     delete h;
 }
 
-int halo(const pmg_hier *h, int c, double *x, cudaStream_t st) {
-    return pmg_halo_self(h->lv[c], x, h->d.periodic_x, h->d.periodic_y, st);
+// the fine level seen through `view` (lagged norm: red array elsewhere)
+// or the level itself
+struct Fine {
+    const pmg_level *view = nullptr;
+    bool red_done = false;   // the cycle's first red half-sweep already ran
+};
+
+const pmg_level *lvl(const pmg_hier *h, int c, const Fine &fv) {
+    return (c == 0 && fv.view) ? fv.view : h->lv[c];
+}
+
+int halo(const pmg_hier *h, const pmg_level *l, double *x, cudaStream_t st) {
+    return pmg_halo_self(l, x, h->d.periodic_x, h->d.periodic_y, st);
 }
 
 // red-black sweeps with a halo refresh after each half (smoother.py:184-191);
 // from_zero: the iterate is zero on entry but unfilled, the first red
-// half-sweep ignores it (neighbours zero; rhs = f exactly)
-int sweeps(const pmg_hier *h, int c, double *u, const double *f, int n, bool from_zero,
-           cudaStream_t st) {
+// half-sweep ignores it (neighbours zero; rhs = f exactly); red_done: the
+// first red half-sweep was run by pmg_half_sweep_res
+int sweeps(const pmg_hier *h, const pmg_level *l, double *u, const double *f, int n,
+           bool from_zero, bool red_done, cudaStream_t st) {
     for (int s = 0; s < n; ++s) {
-        TRY(pmg_half_sweep(h->lv[c], u, f, 0, h->d.rho, 0, (from_zero && s == 0) ? 1 : 0, 1.0, st));
-        TRY(halo(h, c, u, st));
-        TRY(pmg_half_sweep(h->lv[c], u, f, 1, h->d.rho, 0, 0, 1.0, st));
-        TRY(halo(h, c, u, st));
+        if (!(red_done && s == 0))
+            TRY(pmg_half_sweep(l, u, f, 0, h->d.rho, 0, (from_zero && s == 0) ? 1 : 0, 1.0, st));
+        TRY(halo(h, l, u, st));
+        TRY(pmg_half_sweep(l, u, f, 1, h->d.rho, 0, 0, 1.0, st));
+        TRY(halo(h, l, u, st));
     }
     return PMG_OK;
 }
 
 // Alg. 1 (multigrid.py:271-294); level 0 works on the caller's u0 / f0
-int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStream_t st) {
+int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStream_t st,
+           const Fine &fv = Fine()) {
     const int L = (int)h->lv.size();
     double *u = c ? h->u[c] : u0;
     const double *f = c ? h->f[c] : f0;
+    const pmg_level *lc = lvl(h, c, fv);
+    const bool red_done = c == 0 && fv.red_done;
     const bool lean = h->d.rho == 1.0;
     if (c + 1 < L) {
-        TRY(sweeps(h, c, u, f, h->d.nu_pre, lean && (c > 0 || first), st));
-        TRY(pmg_residual_restrict(h->lv[c], h->lv[c + 1], f, u, h->f[c + 1], st));
+        TRY(sweeps(h, lc, u, f, h->d.nu_pre, lean && (c > 0 || first), red_done, st));
+        TRY(pmg_residual_restrict(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
         // the coarse iterate starts from zero: skip the fill when its first
         // red half-sweep ignores it anyway
         const int first_sweeps = (c + 2 == L) ? h->d.coarse_sweeps : h->d.nu_pre;
         if (!(lean && first_sweeps >= 1))
             TRYC(cudaMemsetAsync(h->u[c + 1], 0, sizeof(double) * h->nd[c + 1], st), "coarse fill");
-        TRY(vcycle(h, c + 1, u0, f0, false, st));
+        TRY(vcycle(h, c + 1, u0, f0, false, st, fv));
         // u += P e (black cells only when the red half-sweep overwrites red)
-        TRY(pmg_prolong_colors(h->lv[c], h->lv[c + 1], h->u[c + 1], u, 1,
+        TRY(pmg_prolong_colors(lc, h->lv[c + 1], h->u[c + 1], u, 1,
                                (lean && h->d.nu_post >= 1) ? 2 : 3, st));
-        TRY(halo(h, c, u, st));
-        TRY(sweeps(h, c, u, f, h->d.nu_post, false, st));
+        TRY(halo(h, lc, u, st));
+        TRY(sweeps(h, lc, u, f, h->d.nu_post, false, false, st));
     } else {
-        TRY(sweeps(h, c, u, f, h->d.coarse_sweeps, lean && c > 0, st));
+        TRY(sweeps(h, lc, u, f, h->d.coarse_sweeps, lean && c > 0, false, st));
     }
     return PMG_OK;
 }
@@ -131,11 +157,32 @@ int cycle_and_norm(pmg_hier *h, double *u, const double *f, bool first, cudaStre
     return pmg_residual(h->lv[0], f, u, nullptr, h->scratch, h->res_d, st);
 }
 
-int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st) {
-    if (!st) return cycle_and_norm(h, u, f, first, st);   // legacy stream: no capture
+// lagged-norm cycle bodies.  Red array A = the caller's u (view: level 0),
+// B = h->red1 (view: black array at the caller's u + cstride).  kind 2 + X:
+// first cycle from zero relaxing into red array X; kind 4 + X: a cycle on
+// X whose first red half-sweep already ran.  Both end with the next
+// cycle's first red half-sweep from X into the other array, which also
+// sums ||f - A u||^2 of this cycle's result into res_d[0].
+struct Lag {
+    const pmg_level *view[2];
+    double *base[2];
+};
+
+int lagged_body(pmg_hier *h, const double *f, int kind, const Lag &g, cudaStream_t st) {
+    const int x = kind & 1;
+    Fine fv;
+    fv.view = g.view[x];
+    fv.red_done = kind >= 4;
+    TRY(vcycle(h, 0, g.base[x], f, kind < 4, st, fv));
+    return pmg_half_sweep_res(g.view[x], g.base[x], g.base[x ^ 1], f, h->scratch, h->res_d, st);
+}
+
+template <class Body>
+int replay_kind(pmg_hier *h, double *u, const double *f, int kind, cudaStream_t st, Body body) {
     for (auto &g : h->graphs)
-        if (g.f == f && g.u == u && g.first == (int)first && g.st == st) {
+        if (g.f == f && g.u == u && g.first == kind && g.st == st) {
             TRYC(cudaGraphLaunch(g.exec, st), "graph launch");
+            h->replayed += g.launches;
             return PMG_OK;
         }
     if (h->graphs.size() >= 8) {
@@ -145,20 +192,37 @@ int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st)
     cudaGraph_t graph;
     const long long l0 = pmg_launch_count();
     TRYC(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
-    int rc = cycle_and_norm(h, u, f, first, st);
+    int rc = body();
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (rc) {
         if (e == cudaSuccess) cudaGraphDestroy(graph);
         return rc;
     }
     TRYC(e, "capture end");
-    Graph g{f, u, (int)first, st, nullptr, pmg_launch_count() - l0};
+    Graph g{f, u, kind, st, nullptr, pmg_launch_count() - l0};
     e = cudaGraphInstantiate(&g.exec, graph, 0);
     cudaGraphDestroy(graph);
     TRYC(e, "graph instantiate");
     h->graphs.push_back(g);
     TRYC(cudaGraphLaunch(g.exec, st), "graph launch");
+    h->replayed += g.launches;
     return PMG_OK;
+}
+
+int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st) {
+    if (!st) return cycle_and_norm(h, u, f, first, st);   // legacy stream: no capture
+    return replay_kind(h, u, f, first ? 1 : 0, st,
+                       [&] { return cycle_and_norm(h, u, f, first, st); });
+}
+
+bool lagged_ok(const pmg_hier *h) {
+    int nx, ny, nz;
+    if (pmg_level_dims(h->lv[0], &nx, &ny, &nz)) return false;
+    // nx % 4: the fine residual-restriction is the column-quad kernel, the
+    // one that reads f through Lvl::fcs
+    return h->d.lagged_norm && h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->d.nu_post >= 1 &&
+           h->lv.size() > 1 && nx % 4 == 0 && !getenv("PMG_RR_NOQ") &&
+           pmg_half_sweep_res_ok(h->lv[0]);
 }
 
 }  // namespace
@@ -215,6 +279,8 @@ int pmg_hier_destroy(pmg_hier *h) {
     return PMG_OK;
 }
 
+long long pmg_hier_replayed_launches(const pmg_hier *h) { return h ? h->replayed : -1; }
+
 long long pmg_hier_graph_launches(const pmg_hier *h, const double *f, const double *u,
                                   int first) {
     if (!h) return -1;
@@ -228,6 +294,52 @@ int pmg_vcycle(pmg_hier *h, double *u, const double *f, int first, void *stream)
     if (first && !(h->d.rho == 1.0 && h->lv.size() > 1 && h->d.nu_pre >= 1))
         return err(PMG_ERR_VALUE, "first = 1 needs rho = 1, nu_pre >= 1 and two levels");
     return vcycle(h, 0, u, f, first != 0, (cudaStream_t)stream);
+}
+
+// mg_solve with the lagged norm (pmg_mg_desc.lagged_norm): cycle k's
+// residual norm is summed by the first red half-sweep of cycle k + 1, which
+// writes its red values into the other red array, so u_k stays intact
+// until the norm decides.  The first cycle relaxes into the red array that
+// makes the expected last iterate (the previous solve's count) land in the
+// caller's u; otherwise one red-array copy at the end.
+static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, int maxiter,
+                           double *hist, int *iters, int *converged, double r0,
+                           cudaStream_t st) {
+    const pmg_level *l0 = h->lv[0];
+    long long plane, cs;
+    int pitch, parity, uniform;
+    TRY(pmg_level_layout(l0, &pitch, &plane, &cs, &parity, &uniform));
+    if (!h->red1) TRYC(cudaMalloc(&h->red1, sizeof(double) * cs), "red array");
+    // black array of the caller's u, seen from red1
+    const long long csb =
+        (long long)(((intptr_t)(u + cs) - (intptr_t)h->red1) / (intptr_t)sizeof(double));
+    pmg_level *vb = pmg::level_view(l0, csb);
+    struct Free {
+        pmg_level *v;
+        ~Free() { pmg::level_view_free(v); }
+    } guard{vb};
+    Lag g{{l0, vb}, {u, h->red1}};
+    // iterate k lives in red array (x0 + k - 1) & 1; want the last one in A
+    int x = (h->last_iters & 1) ? 0 : 1;
+    int kind = 2 + x;
+    for (int it = 0; it < maxiter; ++it) {
+        TRY(replay_kind(h, u, f, kind, st, [&] { return lagged_body(h, f, kind, g, st); }));
+        TRYC(cudaStreamSynchronize(st), "sync");
+        const double rn = std::sqrt(h->res_h[0]);
+        hist[it + 1] = rn;
+        *iters = it + 1;
+        if (rn / r0 < eps) {
+            *converged = 1;
+            break;
+        }
+        x ^= 1;
+        kind = 4 + x;
+    }
+    h->last_iters = *iters;
+    if (x == 1)   // the result's red array is red1: copy it into u
+        TRYC(cudaMemcpyAsync(u, h->red1, sizeof(double) * cs, cudaMemcpyDeviceToDevice, st),
+             "red array copy");
+    return PMG_OK;
 }
 
 static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int maxiter,
@@ -245,6 +357,8 @@ static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int 
         *converged = 1;
         return PMG_OK;
     }
+    if (maxiter >= 1 && lagged_ok(h)) return mg_solve_lagged(h, f, u, eps, maxiter, hist, iters,
+                                                             converged, r0, st);
     // rho = 1: the first cycle starts from zero without filling u
     const bool lean_first = h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->lv.size() > 1;
     if (!lean_first) TRY(pmg_fill(l0, u, 0.0, st));

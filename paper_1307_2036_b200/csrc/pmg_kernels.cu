@@ -577,6 +577,10 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
         // row ja-1: even-i colour = cAb (parity flips with j); row jb+1: cAa
         const long long s_e = at(F, cAb, 0, ja - 1, 2 * m), s_o = at(F, cAa, 0, ja - 1, 2 * m);
         const long long n_e = at(F, cAa, 0, jb + 1, 2 * m), n_o = at(F, cAb, 0, jb + 1, 2 * m);
+        // f's colour arrays may lie fcs apart instead of cstride (Lvl::fcs)
+        const long long fd = F.fcs - F.cstride;
+        const double *fa_e = f + a_e + cAa * fd, *fa_o = f + a_o + (cAa ^ 1) * fd;
+        const double *fb_e = f + b_e + cAb * fd, *fb_o = f + b_o + (cAb ^ 1) * fd;
         const int cc0 = (2 * m + J + C.par) & 1;
         const long long q0 = at(C, cc0, 0, J, m), q1 = at(C, cc0 ^ 1, 0, J, m);
         // vertical window of the centre values: [0] k-1, [1] k, [2] k+1
@@ -596,8 +600,8 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
             const double xal = u[al + ko], xar = u[ar + ko], xbl = u[bl + ko], xbr = u[br + ko];
             const D2 se = ld2(u + s_e + ko), so = ld2(u + s_o + ko);
             const D2 ne = ld2(u + n_e + ko), no = ld2(u + n_o + ko);
-            const D2 fae = ld2(f + a_e + ko), fao = ld2(f + a_o + ko);
-            const D2 fbe = ld2(f + b_e + ko), fbo = ld2(f + b_o + ko);
+            const D2 fae = ld2(fa_e + ko), fao = ld2(fa_o + ko);
+            const D2 fbe = ld2(fb_e + ko), fbo = ld2(fb_o + ko);
             // row ja: cells 4m (ce.x), 4m+1 (co.x), 4m+2 (ce.y), 4m+3 (co.y)
             const double ra0 = cell_res<1, 1, true>(F, T, W, k, xal, co[1].x, se.x, de[1].x,
                                                     ce[0].x, ce[1].x, ce[2].x, fae.x);
@@ -1130,13 +1134,18 @@ __device__ __forceinline__ void seg_solve_store(
 }
 
 template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false,
-          int PLC = 0, bool DOT = false>
+          int PLC = 0, bool DOT = false, bool RES = false>
 __global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                  int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles,
-                 double *__restrict__ dotp) {
+                 double *__restrict__ dotp, double *__restrict__ uw) {
     // DOT: also dotp[blockIdx.x] = sum over this CTA's cells of f * (new u),
     // fixed order (CG's <r, z> fused into the SSOR half-sweeps)
+    // RES (rho = 1, FULL, NBZ = 0): u is only read; the relaxed colour-c
+    // values go to uw (same offsets, another buffer), and dotp[blockIdx.x]
+    // receives this CTA's sum of (f - A u)^2 over its colour-c cells of the
+    // INCOMING iterate, in cell_res's operation order (stencil.py:140-164):
+    // the lagged convergence norm of the previous V-cycle
     // NBZ = 0/1: neighbours-zero mode fixed at compile time; FULL: every warp
     // owns exactly SEG levels (nz % SEG == 0) -- no per-level predicates;
     // PLC: the k-plane stride as a compile-time constant (0: runtime), so
@@ -1155,6 +1164,9 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     // start the next tile while others still read the previous scan
     double *hend0 = tq + nz;            // [2][16][32]
     double *ybeg0 = hend0 + 2 * 16 * 32;  // [2][16][32]
+    // RES: (drw, diag) and zero-padded vertical couplings (bm, bp) as in k_norm_v
+    double2 *tr1 = reinterpret_cast<double2 *>(ybeg0 + 2 * 16 * 32);   // [nz]
+    double2 *tr2 = tr1 + nz;                                          // [nz]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int t = threadIdx.x; t < nz; t += blockDim.x) {
         const double io = L.invd1[t], dd = io * L.drw[t];
@@ -1162,6 +1174,10 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         ti[t] = make_double2(io, L.segtab[t]);
         tb[t] = make_double2(L.segtab[2 * nz + t], L.segtab[nz + t]);
         tq[t] = L.segtab[3 * nz + t];
+        if (RES) {
+            tr1[t] = make_double2(L.drw[t], L.diag1[t]);
+            tr2[t] = make_double2((t >= 1) ? L.band1[t] : 0.0, (t + 1 < nz) ? L.band1[t + 1] : 0.0);
+        }
     }
     __syncthreads();
     const int o = c ^ 1;
@@ -1171,6 +1187,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
     double dacc = 0.0;
+    const double wxr = L.wx0, wyr = L.wy0;
     int par = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
         double *hend = hend0 + par * 16 * 32;
@@ -1189,17 +1206,25 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         const long long pS = at(L, o, k0, j - 1, h);
         const long long pN = at(L, o, k0, j + 1, h);
         double r[SEG];
+        // RES: incoming colour-c values below / above this warp's levels
+        // (bm[0] = 0 and bp[nz-1] = 0 make the clamped loads inert)
+        double um = 0.0, un = 0.0, rpend = 0.0, fpend = 0.0, bpend = 0.0;
+        if (RES) {
+            um = u[pc - ((k0 > 0) ? pl : 0)];
+            un = u[pc + ((k0 + SEG < nz) ? SEG : SEG - 1) * pl];
+        }
         // ---- RHS assembly, batches of 8 levels ----
 #pragma unroll
         for (int b8 = 0; b8 < SEG; b8 += (SEG < PMG_SEG_B ? SEG : PMG_SEG_B)) {
             constexpr int B = SEG < PMG_SEG_B ? SEG : PMG_SEG_B;
-            double vf[B], vw[B], vs[B], vn[B], vx[B];
+            double vf[B], vw[B], vs[B], vn[B], vx[B], vo[B];
 #pragma unroll
             for (int e = 0; e < B; ++e) {
                 const int kk = b8 + e;
                 if (kk < kn) {
                     const long long ko = (long long)kk * pl;
                     vf[e] = f[pc + ko];
+                    if (RES) vo[e] = u[pc + ko];
                     if (!nbr_zero) {
                         vw[e] = u[pW + ko];
                         vs[e] = u[pS + ko];
@@ -1224,12 +1249,39 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                     }
                     r[b8 + e] = g;
                 }
+                if (RES) {
+                    // residual of level k - 1 completes with u_k; level k's
+                    // waits for u_{k+1} (stencil.py:140-156, then f - A u:
+                    // k_norm_v's operation order, no contraction)
+                    const double2 t1 = tr1[k0 + kk], t2 = tr2[k0 + kk];
+                    if (kk > 0) {
+                        double q = rpend - bpend * vo[e];
+                        q = fpend - q;
+                        if (lane < nact) dacc += q * q;
+                    }
+                    double a = wxr * vw[e];
+                    a = a + wxr * ve;
+                    a = a + wyr * vs[e];
+                    a = a + wyr * vn[e];
+                    a = a * t1.x;
+                    double q = t1.y * vo[e] - a;
+                    rpend = q - t2.x * um;
+                    fpend = vf[e];
+                    bpend = t2.y;
+                    um = vo[e];
+                }
             }
         }
-        seg_solve_store<SEG, HALO, DOT>(L, u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0, i, nact,
-                                        kn, pc, pl, zero_start, rho, scale, omr, f, &dacc);
+        if (RES) {
+            double q = rpend - bpend * un;
+            q = fpend - q;
+            if (lane < nact) dacc += q * q;
+        }
+        seg_solve_store<SEG, HALO, DOT>(L, RES ? uw : u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0,
+                                        i, nact, kn, pc, pl, zero_start, rho, scale, omr, f,
+                                        &dacc);
     }
-    if (DOT) {
+    if (DOT || RES) {
         const double s2 = block_sum(dacc);
         if (threadIdx.x == 0) dotp[blockIdx.x] = s2;
     }
@@ -2243,6 +2295,7 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
         runq(k_residual_restrict_q<2>);
         return cudaGetLastError();
     }
+    if (F.fcs != F.cstride) return cudaErrorInvalidValue;   // only the column-quad kernel reads fcs
     if (F.nz <= 256) {
         constexpr int KB = 4;
         const int hx = (C.nx + 63) / 64;
@@ -2296,6 +2349,9 @@ cudaError_t launch_halo_self(const Lvl &L, double *d, int px, int py, cudaStream
 cudaError_t launch_half_sweep(const Lvl &L0, double *u, const double *f, int color, double rho,
                               int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    // every half-sweep kernel reads f at the relaxed colour only: a view
+    // whose f colour stride differs shifts the f base instead
+    f += (long long)color * (L0.fcs - L0.cstride);
     bool fused = false;
     cudaError_t e = launch_half_sweep_k(L0, u, f, color, rho, zero_start, nbr_zero, post_scale,
                                         st, &fused);
@@ -2329,7 +2385,7 @@ cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int 
         const int grid = ntiles < cap ? ntiles : cap;
         *np = grid;
         kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                        ntiles, hx, partials);
+                                        ntiles, hx, partials, nullptr);
     };
     if (nbr_zero) {
         if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 1, true, false, 520, true>);
@@ -2338,6 +2394,41 @@ cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int 
         if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, true>);
         else run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, true>);
     }
+    return cudaGetLastError();
+}
+
+// red half-sweep (rho = 1) with the lagged convergence residual: reads the
+// iterate u, writes the relaxed red values into uw's red array and the
+// per-CTA sums of (f - A u)^2 over u's red cells into partials[0 .. *np).
+// Uniform levels in fast mode whose 16-level segments tile nz, no fused halo.
+bool half_sweep_res_ok(const Lvl &L) { return half_sweep_dot_ok(L); }
+
+cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
+                                  double *partials, int *np, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int hx = ((L.nx + 1) / 2 + 31) / 32;
+    const int nw = L.nz / 16;
+    const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
+    const int ntiles = hx * L.ny;
+    auto run = [&](auto kern) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        const int grid = ntiles < cap ? ntiles : cap;
+        *np = grid;
+        kern<<<grid, 32 * nw, sm, st>>>(L, const_cast<double *>(u), f, 0, 1.0, 0, 0, 1.0, ntiles,
+                                        hx, partials, uw);
+    };
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PMG_RES_V");
+        v = e ? atoi(e) : 0;
+    }
+    if (v == 1 && L.plane == 520) run(k_half_sweep_seg<16, 2, 3, 0, true, false, 520, false, true>);
+    else if (v == 2 && L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, true>);
+    else if (L.plane == 520) run(k_half_sweep_seg<16, 4, 3, 0, true, false, 520, false, true>);
+    else if (L.plane == 264) run(k_half_sweep_seg<16, 4, 3, 0, true, false, 264, false, true>);
+    else run(k_half_sweep_seg<16, 4, 3, 0, true, false, 0, false, true>);
     return cudaGetLastError();
 }
 
@@ -2525,7 +2616,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             const int cap = sm_count() * (occ > 0 ? occ : 1);
             const int grid = ntiles < cap ? ntiles : cap;
             kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                            ntiles, hx, nullptr);
+                                            ntiles, hx, nullptr, nullptr);
         };
         if (cp_eligible(L) && !(L.hflags & 1)) {
             const int ht = ((L.nx + 1) / 2) / CP_TW;

@@ -42,7 +42,12 @@ class MGConfig:
     """Cycle shape, level policy and stopping rule (multigrid.py:54-89).
 
     B200 extras (keyword, default on): ``fused`` residual+restriction,
-    ``graph`` CUDA-graph replay of the V-cycle.
+    ``graph`` CUDA-graph replay of the V-cycle, ``lagged_norm``: the
+    native driver sums each cycle's ||f - A u|| inside the next cycle's
+    first red half-sweep (the black residual is exactly zero after the
+    last black line solve with rho = 1), so the convergence check costs no
+    separate pass; same iterates bit for bit, the history omits the black
+    cells' rounding-level residual.
     """
 
     nu_pre: int = 1
@@ -57,6 +62,7 @@ class MGConfig:
     deterministic: bool = False
     fused: bool = True
     graph: bool = True
+    lagged_norm: bool = True
 
     def __post_init__(self):
         if self.nu_pre < 0 or self.nu_post < 0 or self.nu_pre + self.nu_post < 1:
@@ -149,7 +155,8 @@ class LevelHierarchy:
     def native(self, cfg: "MGConfig") -> "NativeHierarchy":
         """The device-resident driver (pmg_hier) of this single-part
         hierarchy for ``cfg``'s cycle shape (cached)."""
-        key = (cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), cfg.rho)
+        key = (cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), cfg.rho,
+               bool(cfg.lagged_norm))
         h = self._native.get(key)
         if h is None:
             h = NativeHierarchy(self, cfg)
@@ -170,19 +177,24 @@ class NativeHierarchy:
         arr = (C.c_void_p * len(self._levels))(*[h.h.value for h in self._levels])
         per = int(bool(lay.periodic))
         d = MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), float(cfg.rho), per,
-                   per)
+                   per, int(bool(cfg.lagged_norm)))
         h = C.c_void_p()
         call("pmg_hier_create", arr, len(self._levels), C.byref(d), C.byref(h))
         self.h = h
         self._lib = load()
 
     def __del__(self):
-        if getattr(self, "h", None) and self.h.value:
-            self._lib.pmg_hier_destroy(self.h)
-            self.h = C.c_void_p()
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self._lib.pmg_hier_destroy(h)
+            self.h = None
 
     def graph_launches(self, f_ptr: int, u_ptr: int, first: bool) -> int:
         return int(self._lib.pmg_hier_graph_launches(self.h, f_ptr, u_ptr, int(first)))
+
+    def replayed_launches(self) -> int:
+        """Cumulative kernels issued by this driver's graph replays."""
+        return int(self._lib.pmg_hier_replayed_launches(self.h))
 
 
 def _level_count(nx: int, pside: int, cfg: MGConfig) -> int:

@@ -577,7 +577,7 @@ def test_native_drivers_match_python(pmg, periodic):
     nx, nz = 32, 8
     grid = pmg.periodic_box(nx, nz, 0.01) if periodic else pmg.panel_grid(nx, nz, flat_mode=True)
     params = pmg.toy_parameters(nx, nz, 1e-3, 3.3e-2)
-    cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, eps=1e-9)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, eps=1e-9, lagged_norm=False)
     hier = pmg.build_hierarchy(grid, params, cfg)
     f = pmg.scatter_owned(uni((nx, nx, nz), 5), hier.fine.layout)
     res = {}
@@ -802,3 +802,102 @@ def test_shapes_vs_oracle(pmg, nx, nz):
         assert np.max(np.abs(ug - ou[1:-1, 1:-1, :])) <= tol * max(1.0, np.max(np.abs(ug)))
         assert abs(rc.iterations - crep.iterations) <= (0 if exact else 1)
         assert rc.converged
+
+
+def _red_mask(nx, ny, nz):
+    i, j = np.meshgrid(np.arange(nx), np.arange(ny), indexing="ij")
+    return np.broadcast_to((((i + j) % 2) == 0)[:, :, None], (nx, ny, nz))
+
+
+@pytest.mark.parametrize("nx,nz", [(32, 128), (128, 80), (64, 96)])
+def test_half_sweep_res(pmg, nx, nz):
+    """pmg_half_sweep_res: the relaxed red values equal pmg_half_sweep's bit
+    for bit (written into the other buffer, the input untouched), and the
+    fused sum equals ||f - A u||^2 over the red cells of the input."""
+    import ctypes as C
+    from paper_1307_2036_b200 import _lib
+    lib = _lib.load()
+    ny = nx
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=1)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    lay = hier.fine.layout
+    w = lay.local_workers[0]
+    h = hier.fine.op.handles[w].h
+    assert lib.pmg_half_sweep_res_ok(h) == 1
+    ua, fa = uni((nx, ny, nz), 1), uni((nx, ny, nz), 2)
+    u, f = field(pmg, ua, lay), field(pmg, fa, lay)
+    u_before = u.parts[w].data.clone()
+    un = pmg.DistField.zeros(lay, nz)
+    scratch = torch.empty(int(lib.pmg_partials_size()), dtype=torch.float64, device="cuda")
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.call("pmg_half_sweep_res", h, u.parts[w].ptr, un.parts[w].ptr, f.parts[w].ptr,
+              C.c_void_p(scratch.data_ptr()), C.c_void_p(nrm.data_ptr()),
+              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.equal(u.parts[w].data, u_before)          # input untouched
+    r = pmg.gather_owned(hier.fine.op.residual(f, u))
+    red = _red_mask(nx, ny, nz)
+    want = float(np.sum(r[red] ** 2))
+    assert abs(nrm.item() - want) <= 1e-12 * want
+    ref = u.copy()
+    hier.fine.smoother.half_sweep(ref, f, 0)
+    got = pmg.gather_owned(un)
+    assert np.array_equal(got[red], pmg.gather_owned(ref)[red])
+    assert not np.any(got[~red])                             # black array untouched
+    # ineligible levels are refused: nz = 32 (4-level segments), Neumann
+    # faces (2-D coefficients)
+    for g2 in (pmg.periodic_box(16, 32, 0.01), pmg.panel_grid(16, 128, flat_mode=True)):
+        h2 = pmg.build_hierarchy(g2, pmg.toy_parameters(16, g2.nz, 1e-3, 1.0),
+                                 pmg.MGConfig(policy="explicit", explicit_levels=1))
+        w2 = h2.fine.layout.local_workers[0]
+        assert lib.pmg_half_sweep_res_ok(h2.fine.op.handles[w2].h) == 0
+        z = pmg.DistField.zeros(h2.fine.layout, g2.nz)
+        z2 = pmg.DistField.zeros(h2.fine.layout, g2.nz)
+        with pytest.raises(ValueError):
+            _lib.call("pmg_half_sweep_res", h2.fine.op.handles[w2].h, z.parts[w2].ptr,
+                      z2.parts[w2].ptr, z.parts[w2].ptr, C.c_void_p(scratch.data_ptr()),
+                      C.c_void_p(nrm.data_ptr()), None)
+
+
+@pytest.mark.parametrize("case", ["box256", "box96", "box80", "box128"])
+def test_lagged_norm_solve(pmg, case):
+    """Native mg_solve with the lagged convergence norm against the plain
+    one: equal iteration counts and iterates BIT FOR BIT (same kernels, the
+    relaxed red values only land in the other red array), histories within
+    1e-12 (the black cells' residual after an exact black line solve is
+    rounding noise).  Odd and even cycle counts, repeated solves (the
+    red-array parity follows the previous count) and maxiter cut-offs."""
+    from paper_1307_2036_b200 import _lib
+    nx, nz, nlev = {"box256": (256, 128, 5), "box96": (64, 96, 3), "box80": (32, 80, 2),
+                    "box128": (128, 128, 3)}[case]
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    fa = uni((nx, nx, nz), 9)
+    for eps in (1e-5, 1e-7, 1e-9):
+        runs = {}
+        for lag in (False, True):
+            cfg = pmg.MGConfig(policy="explicit", explicit_levels=nlev, eps=eps, lagged_norm=lag)
+            hier = pmg.build_hierarchy(grid, params, cfg)
+            lay = hier.fine.layout
+            assert _lib.load().pmg_half_sweep_res_ok(
+                hier.fine.op.handles[lay.local_workers[0]].h) == 1
+            f = pmg.scatter_owned(fa, lay)
+            out = []
+            for _ in range(3):      # the parity guess changes after the first solve
+                u, rep = pmg.mg_solve(f, hier, cfg)
+                out.append((rep.iterations, rep.converged, np.array(rep.residual_history),
+                            pmg.gather_owned(u)))
+            for maxiter in (1, 2, 3):
+                c2 = pmg.MGConfig(policy="explicit", explicit_levels=nlev, eps=1e-14,
+                                  maxiter=maxiter, lagged_norm=lag)
+                u, rep = pmg.mg_solve(f, hier, c2)
+                out.append((rep.iterations, rep.converged, np.array(rep.residual_history),
+                            pmg.gather_owned(u)))
+            runs[lag] = out
+        for a, b in zip(runs[False], runs[True]):
+            assert a[0] == b[0] and a[1] == b[1]
+            assert a[2][0] == b[2][0]
+            assert hist_err(b[2], a[2]) <= 1e-12
+            assert np.array_equal(a[3], b[3])

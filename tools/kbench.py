@@ -70,6 +70,20 @@ for c, lev in enumerate(hier.levels):
         flip[0] += 1
     t = timeit(hs)
     row["half_sweep"] = (round(t * 1e3, 1), round(12 * n / t / 1e6))
+    lib = pmg._lib.load()
+    w = lev.layout.local_workers[0]
+    hh = lev.op.handles[w].h
+    if lib.pmg_half_sweep_res_ok(hh):
+        import ctypes as C
+        scr = torch.empty(int(lib.pmg_partials_size()), dtype=torch.float64, device="cuda")
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+        def hsr():
+            lib.pmg_half_sweep_res(hh, s.u.parts[w].ptr, s.r.parts[w].ptr, s.f.parts[w].ptr,
+                                   C.c_void_p(scr.data_ptr()), C.c_void_p(res.data_ptr()),
+                                   C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        t = timeit(hsr)
+        row["half_sweep_res"] = (round(t * 1e3, 1), round(16 * n / t / 1e6))
     t = timeit(lambda: lev.op.residual_norm2_dev(s.f, s.u, None, res))
     row["resid_norm"] = (round(t * 1e3, 1), round(16 * n / t / 1e6))
     if c + 1 < len(hier.levels):
@@ -86,9 +100,12 @@ for c, lev in enumerate(hier.levels):
     t = timeit(lambda: pmg.halo_exchange(s.u))
     row["halo"] = round(t * 1e3, 1)
     print(f"L{c} nx={lev.layout.nx}: " + json.dumps(row), flush=True)
-# full solve
-for _ in range(2):
-    u, rep = pmg.mg_solve(f, hier, cfg)
-t = timeit(lambda: pmg.mg_solve(f, hier, cfg, out=u), 5)
-print(json.dumps({"solve_ms": round(t, 3), "iters": rep.iterations,
-                  "hist": rep.residual_history}))
+# full solve (lagged convergence norm on / off)
+import dataclasses  # noqa: E402
+for lag in (True, False):
+    cfg = dataclasses.replace(cfg, lagged_norm=lag)
+    for _ in range(2):
+        u, rep = pmg.mg_solve(f, hier, cfg)
+    t = timeit(lambda: pmg.mg_solve(f, hier, cfg, out=u), 5)
+    print(json.dumps({"lagged_norm": lag, "solve_ms": round(t, 3), "iters": rep.iterations,
+                      "hist": rep.residual_history}))
