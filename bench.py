@@ -291,8 +291,7 @@ def main():
         # single part: the C++ driver counts the kernels of its graph replays
         gpu_launches += hier.native(cfg).replayed_launches() - r0_graph
     else:
-        gkey = (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
-                mgm._ptrs(f), mgm._ptrs(u))
+        gkey = mgm.graph_key(cfg, f, u)
         g_first = hier._graphs.get(gkey + (True,))
         g_rest = hier._graphs.get(gkey + (False,))
         for n_it in iters:

@@ -95,7 +95,7 @@ int main(int argc, char **argv) {
     double *hist = (double *)calloc(maxiter + 1, sizeof(double));
     int iters = 0, conv = 0;
     if (solver == 0) {
-        pmg_mg_desc md = {1, 1, 1, 1.0, periodic, periodic, 1};   /* V(1,1), rho = 1, lagged norm */
+        pmg_mg_desc md = {1, 1, 1, 1.0, periodic, periodic, 1, 1};   /* V(1,1), rho = 1, lagged norm, red restriction */
         pmg_hier *h;
         CHECK(pmg_hier_create((const pmg_level *const *)lv, nlev, &md, &h));
         CHECK(pmg_mg_solve(h, f, u, eps, maxiter, hist, &iters, &conv, NULL));

@@ -129,6 +129,16 @@ int pmg_apply_dot(const pmg_level *lvl, const double *p, double *q, double *scra
 int pmg_residual_restrict(const pmg_level *fine, const pmg_level *coarse,
                           const double *f, const double *u, double *coarse_f,
                           void *stream);
+/* the same right after a black half-sweep with exact line solves and
+ * rho = 1 (the V-cycle's pre-smoothing): the black residual is then zero,
+ * so only the red children are summed -- 14 N bytes instead of 18 N.
+ * Fast mode, uniform coefficients, nx a multiple of 4; PMG_ERR_VALUE
+ * otherwise.  Equal to pmg_residual_restrict up to the black cells'
+ * rounding-level residual. */
+int pmg_residual_restrict_red(const pmg_level *fine, const pmg_level *coarse,
+                              const double *f, const double *u, double *coarse_f,
+                              void *stream);
+int pmg_residual_restrict_red_ok(const pmg_level *fine);
 
 /* ---- line smoother: LineSmoother.half_sweep (smoother.py:122-182) ---- */
 /* mode 0 (default): fast k-segmented column solve (uniform levels; agrees
@@ -270,6 +280,10 @@ typedef struct pmg_mg_desc {
      * bit for bit; the history omits the black cells' rounding-level
      * residual. */
     int lagged_norm;
+    /* 1: the pre-smoothed residual is restricted from its red cells only
+     * (pmg_residual_restrict_red) where the level allows it; needs rho = 1
+     * and nu_pre >= 1, ignored otherwise. */
+    int red_restrict;
 } pmg_mg_desc;
 /* levels[0] finest ... levels[nlev-1] coarsest, each halving nx and ny */
 int pmg_hier_create(const pmg_level *const *levels, int nlev, const pmg_mg_desc *desc,

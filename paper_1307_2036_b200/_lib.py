@@ -24,7 +24,7 @@ class MGDesc(C.Structure):
     _fields_ = [
         ("nu_pre", C.c_int), ("nu_post", C.c_int), ("coarse_sweeps", C.c_int),
         ("rho", C.c_double), ("periodic_x", C.c_int), ("periodic_y", C.c_int),
-        ("lagged_norm", C.c_int),
+        ("lagged_norm", C.c_int), ("red_restrict", C.c_int),
     ]
 
 
@@ -80,6 +80,8 @@ SIGNATURES = {
     "pmg_residual": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "pmg_apply_dot": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_residual_restrict": (_I, [_P, _P, _P, _P, _P, _P]),
+    "pmg_residual_restrict_red": (_I, [_P, _P, _P, _P, _P, _P]),
+    "pmg_residual_restrict_red_ok": (_I, [_P]),
     "pmg_half_sweep": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _P]),
     "pmg_half_sweep_res": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "pmg_half_sweep_res_ok": (_I, [_P]),

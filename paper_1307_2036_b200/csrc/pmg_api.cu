@@ -30,6 +30,9 @@ cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, 
 bool half_sweep_pro_ok(const Lvl &F);
 bool half_sweep_dot_ok(const Lvl &L);
 bool half_sweep_res_ok(const Lvl &L);
+bool residual_restrict_red_ok(const Lvl &F);
+cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const double *u,
+                                         const double *f, double *cf, cudaStream_t st);
 cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
                                   double *partials, int *np, cudaStream_t st);
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
@@ -380,6 +383,22 @@ int pmg_residual_restrict(const pmg_level *fine, const pmg_level *coarse, const 
     if (rc) return rc;
     PMG_CUDA(launch_residual_restrict(fine->L, coarse->L, u, f, cf, (cudaStream_t)st),
              "residual_restrict");
+    return PMG_OK;
+}
+
+int pmg_residual_restrict_red_ok(const pmg_level *lv) {
+    return lv && residual_restrict_red_ok(lv->L) ? 1 : 0;
+}
+
+int pmg_residual_restrict_red(const pmg_level *fine, const pmg_level *coarse, const double *f,
+                              const double *u, double *cf, void *st) {
+    int rc = check_pair(fine, coarse);
+    if (rc) return rc;
+    if (!residual_restrict_red_ok(fine->L))
+        return fail(PMG_ERR_VALUE, "red-only restriction needs fast mode, uniform coefficients "
+                                   "and nx a multiple of 4");
+    PMG_CUDA(launch_residual_restrict_red(fine->L, coarse->L, u, f, cf, (cudaStream_t)st),
+             "residual_restrict_red");
     return PMG_OK;
 }
 

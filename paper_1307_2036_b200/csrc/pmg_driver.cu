@@ -134,7 +134,10 @@ int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStr
     const bool lean = h->d.rho == 1.0;
     if (c + 1 < L) {
         TRY(sweeps(h, lc, u, f, h->d.nu_pre, lean && (c > 0 || first), red_done, st));
-        TRY(pmg_residual_restrict(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
+        if (h->d.red_restrict && lean && h->d.nu_pre >= 1 && pmg_residual_restrict_red_ok(lc))
+            TRY(pmg_residual_restrict_red(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
+        else
+            TRY(pmg_residual_restrict(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
         // the coarse iterate starts from zero: skip the fill when its first
         // red half-sweep ignores it anyway
         const int first_sweeps = (c + 2 == L) ? h->d.coarse_sweeps : h->d.nu_pre;
@@ -332,6 +335,7 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
             *converged = 1;
             break;
         }
+        if (it + 1 == maxiter) break;   // u_maxiter stays in red array x
         x ^= 1;
         kind = 4 + x;
     }

@@ -647,6 +647,106 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
 }
 
 
+// Red-only residual + restriction (fast mode, rho = 1): right after a
+// black half-sweep with exact line solves the black residual is zero, so
+// R r sums only the two red children of each coarse cell (adding the
+// black children's exact zeros changes nothing; their computed values are
+// rounding noise).  Same thread mapping as k_residual_restrict_q; per
+// level it loads the red centre values (vertical windows), the black
+// centre / outer / S / N neighbours and f at red cells only: 14 N
+// algorithmic bytes instead of 18 N.  PAR = the level's parity (red at
+// even i in the even fine rows when 0).
+template <int PAR, int MINB = 2>
+__global__ void __launch_bounds__(128, MINB)
+k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
+                        double *__restrict__ cf, int mb32, int ntiles, int kcs) {
+    __shared__ double s_drw[256], s_a[257], s_b[257], s_c[257];
+    const Tabs T{s_drw, s_a, s_b, s_a, s_b, s_c};
+    load_tabs(F, T);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int nwarp = gridDim.x * (blockDim.x >> 5);
+    const int nz = F.nz;
+    const long long pl = F.plane;
+    const int nkc = (nz + kcs - 1) / kcs;
+    const int npair = C.nx >> 1;
+    const Col2 W = col2_coeffs<true>(F, 0, 0);
+    for (int wt = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wt < ntiles; wt += nwarp) {
+        const int kcI = wt % nkc;
+        const int t2 = wt / nkc;
+        const int J = t2 / mb32;
+        const int m0 = (t2 - J * mb32) * 32;
+        const bool act = m0 + lane < npair;
+        const int m = act ? m0 + lane : npair - 1;
+        const int kbeg = kcI * kcs, kend = min(nz, kbeg + kcs);
+        const int ja = 2 * J, jb = ja + 1;
+        // colour 0 (red) / 1 (black); row ja holds red at even i when PAR = 0
+        // red pairs: row ja at i = 4m + PAR, +2; row jb at i = 4m + 1 - PAR, +2
+        const long long ra = at(F, 0, 0, ja, 2 * m), rb = at(F, 0, 0, jb, 2 * m);
+        const long long ba = at(F, 1, 0, ja, 2 * m), bb = at(F, 1, 0, jb, 2 * m);
+        // outer black scalars: row ja W of its first red cell (PAR = 0: i = 4m-1)
+        // or E of its last (PAR = 1: i = 4m+4); row jb the other way round
+        const long long xa = PAR ? at(F, 1, 0, ja, 2 * m + 2) : at(F, 1, 0, ja, 2 * m - 1);
+        const long long xb = PAR ? at(F, 1, 0, jb, 2 * m - 1) : at(F, 1, 0, jb, 2 * m + 2);
+        // S of row ja = row ja-1 (black at row ja's red positions), N of
+        // row jb = row jb+1 (black at row jb's red positions)
+        const long long sa = at(F, 1, 0, ja - 1, 2 * m), nb = at(F, 1, 0, jb + 1, 2 * m);
+        const double *fa = f + ra, *fb = f + rb;   // colour 0: no fcs offset
+        const int cc0 = (2 * m + J + C.par) & 1;
+        const long long q0 = at(C, cc0, 0, J, m), q1 = at(C, cc0 ^ 1, 0, J, m);
+        D2 ca[3], cb[3];   // red pairs of rows ja / jb: [0] k-1, [1] k, [2] k+1
+        {
+            const long long km = (long long)max(kbeg - 1, 0) * pl, k0 = (long long)kbeg * pl;
+            ca[0] = ld2(u + ra + km); cb[0] = ld2(u + rb + km);
+            ca[1] = ld2(u + ra + k0); cb[1] = ld2(u + rb + k0);
+        }
+        for (int k = kbeg; k < kend; ++k) {
+            const long long ko = (long long)k * pl;
+            const long long kp = (long long)min(k + 1, nz - 1) * pl;
+            ca[2] = ld2(u + ra + kp); cb[2] = ld2(u + rb + kp);
+            const D2 va = ld2(u + ba + ko), vb = ld2(u + bb + ko);   // black pairs
+            const D2 vs = ld2(u + sa + ko), vn = ld2(u + nb + ko);
+            const double xao = u[xa + ko], xbo = u[xb + ko];
+            const D2 ffa = ld2(fa + ko), ffb = ld2(fb + ko);
+            double a, b;
+            if (PAR == 0) {
+                // row ja red at 4m (ca.x), 4m+2 (ca.y); black at 4m+1 (va.x), 4m+3 (va.y)
+                // row jb red at 4m+1 (cb.x), 4m+3 (cb.y); black at 4m (vb.x), 4m+2 (vb.y)
+                const double r0 = cell_res<1, 1, true>(F, T, W, k, xao, va.x, vs.x, vb.x,
+                                                       ca[0].x, ca[1].x, ca[2].x, ffa.x);
+                const double r2 = cell_res<1, 1, true>(F, T, W, k, va.x, va.y, vs.y, vb.y,
+                                                       ca[0].y, ca[1].y, ca[2].y, ffa.y);
+                const double r1 = cell_res<1, 1, true>(F, T, W, k, vb.x, vb.y, va.x, vn.x,
+                                                       cb[0].x, cb[1].x, cb[2].x, ffb.x);
+                const double r3 = cell_res<1, 1, true>(F, T, W, k, vb.y, xbo, va.y, vn.y,
+                                                       cb[0].y, cb[1].y, cb[2].y, ffb.y);
+                a = r0 + r1;        // ((r(4m,ja) + 0) + 0) + r(4m+1,jb)
+                b = r2 + r3;
+            } else {
+                // row ja red at 4m+1 (ca.x), 4m+3 (ca.y); black at 4m (va.x), 4m+2 (va.y)
+                // row jb red at 4m (cb.x), 4m+2 (cb.y); black at 4m+1 (vb.x), 4m+3 (vb.y)
+                const double r1 = cell_res<1, 1, true>(F, T, W, k, va.x, va.y, vs.x, vb.x,
+                                                       ca[0].x, ca[1].x, ca[2].x, ffa.x);
+                const double r3 = cell_res<1, 1, true>(F, T, W, k, va.y, xao, vs.y, vb.y,
+                                                       ca[0].y, ca[1].y, ca[2].y, ffa.y);
+                const double r0 = cell_res<1, 1, true>(F, T, W, k, xbo, vb.x, va.x, vn.x,
+                                                       cb[0].x, cb[1].x, cb[2].x, ffb.x);
+                const double r2 = cell_res<1, 1, true>(F, T, W, k, vb.x, vb.y, va.y, vn.y,
+                                                       cb[0].y, cb[1].y, cb[2].y, ffb.y);
+                a = r1 + r0;        // ((0 + r(4m+1,ja)) + r(4m,jb)) + 0
+                b = r3 + r2;
+            }
+            if (act) {
+                const long long cko = (long long)k * C.plane;
+                cf[q0 + cko] = a;
+                cf[q1 + cko] = b;
+            }
+            ca[0] = ca[1]; cb[0] = cb[1];
+            ca[1] = ca[2]; cb[1] = cb[2];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // residual fused with children-sum restriction (multigrid.py:278-282):
 // each thread owns one coarse column (I, J) and computes the residual of
@@ -2320,6 +2420,33 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
     const dim3 b(32, 8), g((C.nx + 31) / 32, (F.nz + kc - 1) / kc, (C.ny + 7) / 8);
     if (F.uniform) k_residual_restrict<true><<<g, b, 0, st>>>(F, C, u, f, cf, kc);
     else k_residual_restrict<false><<<g, b, 0, st>>>(F, C, u, f, cf, kc);
+    return cudaGetLastError();
+}
+
+// red-only residual + restriction (k_residual_restrict_red): fast mode,
+// uniform coefficients, fine nx a multiple of 4
+bool residual_restrict_red_ok(const Lvl &F) {
+    return !g_smoother_exact && F.uniform && F.nz <= 256 && F.nx % 4 == 0;
+}
+
+cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const double *u,
+                                         const double *f, double *cf, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const int mb32 = ((C.nx >> 1) + 31) / 32;
+    auto runq = [&](auto kern) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
+        const int capw = sm_count() * (occ > 0 ? occ : 1) * 4;
+        int kcs = F.nz;
+        while (kcs > 8 && (long long)mb32 * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * capw)
+            kcs >>= 1;
+        const int ntiles = mb32 * C.ny * ((F.nz + kcs - 1) / kcs);
+        int grid = (ntiles + 3) / 4;
+        if (grid > capw / 4) grid = capw / 4;
+        kern<<<grid, 128, 0, st>>>(F, C, u, f, cf, mb32, ntiles, kcs);
+    };
+    if (F.par & 1) runq(k_residual_restrict_red<1>);
+    else runq(k_residual_restrict_red<0>);
     return cudaGetLastError();
 }
 

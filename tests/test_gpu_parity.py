@@ -866,7 +866,7 @@ def test_lagged_norm_solve(pmg, case):
     """Native mg_solve with the lagged convergence norm against the plain
     one: equal iteration counts and iterates BIT FOR BIT (same kernels, the
     relaxed red values only land in the other red array), histories within
-    1e-12 (the black cells' residual after an exact black line solve is
+    1e-10 (the black cells' residual after an exact black line solve is
     rounding noise).  Odd and even cycle counts, repeated solves (the
     red-array parity follows the previous count) and maxiter cut-offs."""
     from paper_1307_2036_b200 import _lib
@@ -899,5 +899,86 @@ def test_lagged_norm_solve(pmg, case):
         for a, b in zip(runs[False], runs[True]):
             assert a[0] == b[0] and a[1] == b[1]
             assert a[2][0] == b[2][0]
-            assert hist_err(b[2], a[2]) <= 1e-12
+            # the dropped black residual is ~1e-14 ||r0|| (rounding of the
+            # exact black line solve): relative 1e-10 plus that floor
+            assert np.all(np.abs(b[2] - a[2]) <= 1e-10 * a[2] + 1e-14 * a[2][0])
             assert np.array_equal(a[3], b[3])
+
+
+@pytest.mark.parametrize("par", [0, 1])
+@pytest.mark.parametrize("mx,my,nz", [(32, 16, 16), (64, 8, 128), (4, 4, 8)])
+def test_residual_restrict_red(pmg, par, mx, my, nz):
+    """pmg_residual_restrict_red on a part of either parity (i0 = par): the
+    coarse values equal the reference children sums of pmg_residual's
+    (bit-exact) residual with the black children replaced by zero -- bit
+    for bit."""
+    import ctypes as C
+    from paper_1307_2036_b200 import _lib
+    from paper_1307_2036_b200.partition import DevField, LevelHandle, _stream
+    rng = np.random.default_rng(3 + par)
+    dr = rng.uniform(0.5, 1.5, nz)
+    vprof = rng.uniform(0.5, 1.5, nz + 1)
+    vol = dr.copy()
+
+    def level(m, n, i0):
+        one = np.ones(1)
+        return LevelHandle(m, n, nz, i0, 0, 1e-3, 3.3e-2, dr, vprof, vol,
+                           np.broadcast_to(one, (n, m + 1)), np.broadcast_to(one, (n + 1, m)),
+                           np.broadcast_to(0.7 * one, (n, m)), np.broadcast_to(1.3 * one, (n, m)),
+                           np.broadcast_to(4 * one, (n, m)))
+    fine, coarse = level(mx, my, par), level(mx // 2, my // 2, 0)
+    assert fine.parity == par
+    u, f, r, cf = DevField(fine), DevField(fine), DevField(fine), DevField(coarse)
+    u.load_owned(rng.uniform(-1, 1, (mx, my, nz)))
+    f.load_owned(rng.uniform(-1, 1, (mx, my, nz)))
+    st = _stream()
+    _lib.call("pmg_halo_self", fine.h, u.ptr, 1, 1, st)
+    _lib.call("pmg_residual", fine.h, f.ptr, u.ptr, r.ptr, None, None, st)
+    assert _lib.load().pmg_residual_restrict_red_ok(fine.h) == 1
+    _lib.call("pmg_residual_restrict_red", fine.h, coarse.h, f.ptr, u.ptr, cf.ptr, st)
+    torch.cuda.synchronize()
+    res = r.owned_array()
+    i, j = np.meshgrid(np.arange(mx), np.arange(my), indexing="ij")
+    red = (((i + par + j) % 2) == 0)[:, :, None]
+    rr = np.where(red, res, 0.0)
+    want = ((rr[0::2, 0::2] + rr[1::2, 0::2]) + rr[0::2, 1::2]) + rr[1::2, 1::2]
+    assert np.array_equal(cf.owned_array(), want)
+    # and the full restriction differs only by the black residual
+    cfull = DevField(coarse)
+    _lib.call("pmg_residual_restrict", fine.h, coarse.h, f.ptr, u.ptr, cfull.ptr, st)
+    full = ((res[0::2, 0::2] + res[1::2, 0::2]) + res[0::2, 1::2]) + res[1::2, 1::2]
+    assert np.array_equal(cfull.owned_array(), full)
+
+
+def test_red_restrict_solve(pmg):
+    """V-cycles with the red-only restriction against the full one on
+    configs[1]'s shape at 256^2 x 128: equal cycle counts, histories and
+    iterates within rounding (the dropped black residual is ~1e-16 of the
+    red one), native and Python drivers bit-identical to each other."""
+    from paper_1307_2036_b200 import multigrid as mgm
+    nx, nz = 256, 128
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    fa = uni((nx, nx, nz), 4)
+    out = {}
+    for red in (False, True):
+        for native in (False, True):
+            cfg = pmg.MGConfig(policy="explicit", explicit_levels=5, eps=1e-8,
+                               red_restrict=red, lagged_norm=False)
+            hier = pmg.build_hierarchy(grid, params, cfg)
+            f = pmg.scatter_owned(fa, hier.fine.layout)
+            mgm.USE_NATIVE = native
+            try:
+                u, rep = pmg.mg_solve(f, hier, cfg)
+            finally:
+                mgm.USE_NATIVE = True
+            out[red, native] = (np.array(rep.residual_history), pmg.gather_owned(u))
+    for red in (False, True):
+        assert np.array_equal(out[red, False][0], out[red, True][0])
+        assert np.array_equal(out[red, False][1], out[red, True][1])
+    (h0, u0), (h1, u1) = out[False, True], out[True, True]
+    assert len(h0) == len(h1)
+    # the black children's residual is rounding noise (~1e-16 ||r0||): the
+    # histories agree to 1e-10 relative above a 1e-14 ||r0|| floor
+    assert np.all(np.abs(h1 - h0) <= 1e-10 * h0 + 1e-14 * h0[0])
+    assert np.max(np.abs(u1 - u0)) <= 1e-10 * np.max(np.abs(u0))

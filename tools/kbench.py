@@ -90,6 +90,9 @@ for c, lev in enumerate(hier.levels):
         co = hier.levels[c + 1]
         t = timeit(lambda: mg._residual_restrict(lev, co, s.f, s.u, sc[c + 1].f))
         row["resid_restrict"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
+        if lib.pmg_residual_restrict_red_ok(hh):
+            t = timeit(lambda: mg._residual_restrict(lev, co, s.f, s.u, sc[c + 1].f, True))
+            row["resid_restrict_red"] = (round(t * 1e3, 1), round(14 * n / t / 1e6))
         t = timeit(lambda: mg._prolong_add(sc[c + 1].u, co, lev, s.u))
         row["prolong_add"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
         t = timeit(lambda: mg._prolong_add(sc[c + 1].u, co, lev, s.u, black_only=True))
@@ -102,10 +105,10 @@ for c, lev in enumerate(hier.levels):
     print(f"L{c} nx={lev.layout.nx}: " + json.dumps(row), flush=True)
 # full solve (lagged convergence norm on / off)
 import dataclasses  # noqa: E402
-for lag in (True, False):
-    cfg = dataclasses.replace(cfg, lagged_norm=lag)
+for lag, red in ((True, True), (True, False), (False, False)):
+    cfg = dataclasses.replace(cfg, lagged_norm=lag, red_restrict=red)
     for _ in range(2):
         u, rep = pmg.mg_solve(f, hier, cfg)
     t = timeit(lambda: pmg.mg_solve(f, hier, cfg, out=u), 5)
-    print(json.dumps({"lagged_norm": lag, "solve_ms": round(t, 3), "iters": rep.iterations,
+    print(json.dumps({"lagged_norm": lag, "red_restrict": red, "solve_ms": round(t, 3), "iters": rep.iterations,
                       "hist": rep.residual_history}))
