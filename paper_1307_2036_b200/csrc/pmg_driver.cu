@@ -107,6 +107,31 @@ int halo(const pmg_hier *h, const pmg_level *l, double *x, cudaStream_t st) {
     return pmg_halo_self(l, x, h->d.periodic_x, h->d.periodic_y, st);
 }
 
+// levels of at most this many columns per row refresh their halo inside the
+// half-sweep / prolongation kernels (launch-bound small levels)
+int fused_halo_nx() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PMG_FH_NX");
+        v = e ? atoi(e) : 0;
+    }
+    return v;
+}
+
+int halo_flags(const pmg_hier *h, const pmg_level *l) {
+    int nx, ny, nz;
+    if (pmg_level_dims(l, &nx, &ny, &nz) || nx > fused_halo_nx()) return 0;
+    return 1 | (h->d.periodic_x ? 2 : 0) | (h->d.periodic_y ? 4 : 0);
+}
+
+int half_sweep(const pmg_hier *h, const pmg_level *l, double *u, const double *f, int color,
+               int nbr_zero, cudaStream_t st) {
+    const int hf = halo_flags(h, l);
+    if (hf) return pmg_half_sweep_halo(l, u, f, color, h->d.rho, 0, nbr_zero, 1.0, hf, st);
+    TRY(pmg_half_sweep(l, u, f, color, h->d.rho, 0, nbr_zero, 1.0, st));
+    return halo(h, l, u, st);
+}
+
 // red-black sweeps with a halo refresh after each half (smoother.py:184-191);
 // from_zero: the iterate is zero on entry but unfilled, the first red
 // half-sweep ignores it (neighbours zero; rhs = f exactly); red_done: the
@@ -114,11 +139,11 @@ int halo(const pmg_hier *h, const pmg_level *l, double *x, cudaStream_t st) {
 int sweeps(const pmg_hier *h, const pmg_level *l, double *u, const double *f, int n,
            bool from_zero, bool red_done, cudaStream_t st) {
     for (int s = 0; s < n; ++s) {
-        if (!(red_done && s == 0))
-            TRY(pmg_half_sweep(l, u, f, 0, h->d.rho, 0, (from_zero && s == 0) ? 1 : 0, 1.0, st));
-        TRY(halo(h, l, u, st));
-        TRY(pmg_half_sweep(l, u, f, 1, h->d.rho, 0, 0, 1.0, st));
-        TRY(halo(h, l, u, st));
+        if (red_done && s == 0)
+            TRY(halo(h, l, u, st));
+        else
+            TRY(half_sweep(h, l, u, f, 0, (from_zero && s == 0) ? 1 : 0, st));
+        TRY(half_sweep(h, l, u, f, 1, 0, st));
     }
     return PMG_OK;
 }
@@ -145,9 +170,14 @@ int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStr
             TRYC(cudaMemsetAsync(h->u[c + 1], 0, sizeof(double) * h->nd[c + 1], st), "coarse fill");
         TRY(vcycle(h, c + 1, u0, f0, false, st, fv));
         // u += P e (black cells only when the red half-sweep overwrites red)
-        TRY(pmg_prolong_colors(lc, h->lv[c + 1], h->u[c + 1], u, 1,
-                               (lean && h->d.nu_post >= 1) ? 2 : 3, st));
-        TRY(halo(h, lc, u, st));
+        const int pmask = (lean && h->d.nu_post >= 1) ? 2 : 3;
+        const int hf = halo_flags(h, lc);
+        if (hf) {
+            TRY(pmg_prolong_colors_halo(lc, h->lv[c + 1], h->u[c + 1], u, 1, pmask, hf, st));
+        } else {
+            TRY(pmg_prolong_colors(lc, h->lv[c + 1], h->u[c + 1], u, 1, pmask, st));
+            TRY(halo(h, lc, u, st));
+        }
         TRY(sweeps(h, lc, u, f, h->d.nu_post, false, false, st));
     } else {
         TRY(sweeps(h, lc, u, f, h->d.coarse_sweeps, lean && c > 0, false, st));

@@ -14,8 +14,12 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "ncu launch rc=$?"
 # fine-level kernels: the first launches of each in a solve are the finest level
 python tools/kbench.py --levels 2 > gpurun_out/kb.log 2>&1
-for k in k_half_sweep_seg k_norm_v k_residual_restrict_q k_prolong_q; do
+for k in k_half_sweep_seg k_residual_restrict_red k_prolong_q; do
   ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
       -o gpurun_out/prof_$k python tools/kbench.py --levels 2 > gpurun_out/ncu_$k.log 2>&1
   echo "ncu full $k rc=$?"
 done
+# the red half-sweep with the fused lagged convergence residual
+ncu --set full --clock-control none --import-source on -k regex:k_half_sweep_seg -c 1 \
+    -o gpurun_out/prof_hs_res python tools/hs_res.py > gpurun_out/ncu_hs_res.log 2>&1
+echo "ncu full hs_res rc=$?"
