@@ -31,6 +31,8 @@ bool half_sweep_pro_ok(const Lvl &F);
 bool half_sweep_dot_ok(const Lvl &L);
 bool half_sweep_res_ok(const Lvl &L);
 bool residual_restrict_red_ok(const Lvl &F);
+cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int color,
+                                  int nbr_zero, double *partials, int *np, cudaStream_t st);
 cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const double *u,
                                          const double *f, double *cf, cudaStream_t st);
 cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
@@ -111,6 +113,21 @@ static int cuda_fail(cudaError_t e, const char *where) {
         cudaError_t e_ = (call);                                             \
         if (e_ != cudaSuccess) return cuda_fail(e_, where);                  \
     } while (0)
+
+namespace pmg {
+// rho = 1 half-sweep of a pmg_half_sweep_res_ok level that also sums f^2
+// over the relaxed colour: per-CTA partials into partials[0 .. *np)
+int half_sweep_fsq(const pmg_level *lv, double *u, const double *f, int color, int nbr_zero,
+                   double *partials, int *np, void *st) {
+    PMG_CUDA(launch_half_sweep_fsq(lv->L, u, f, color, nbr_zero, partials, np, (cudaStream_t)st),
+             "half_sweep_fsq");
+    return PMG_OK;
+}
+int finalize(const double *partials, int n, double *out, void *st) {
+    PMG_CUDA(launch_finalize(partials, n, out, (cudaStream_t)st), "finalize");
+    return PMG_OK;
+}
+}  // namespace pmg
 
 static cudaError_t upload(pmg_level *lv, const double *h, size_t n, const double **dst) {
     void *d = nullptr;

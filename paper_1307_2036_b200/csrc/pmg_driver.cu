@@ -23,6 +23,9 @@ namespace pmg {
 int set_error(int code, const char *msg);
 pmg_level *level_view(const pmg_level *lv, long long cstride);
 void level_view_free(pmg_level *v);
+int half_sweep_fsq(const pmg_level *lv, double *u, const double *f, int color, int nbr_zero,
+                   double *partials, int *np, void *st);
+int finalize(const double *partials, int n, double *out, void *st);
 }
 
 namespace {
@@ -97,6 +100,9 @@ void free_hier(pmg_hier *h) {
 struct Fine {
     const pmg_level *view = nullptr;
     bool red_done = false;   // the cycle's first red half-sweep already ran
+    // first cycle: ||f||^2 summed by its first red and black half-sweeps
+    // (partials at fsq_part, the total into fsq_out)
+    double *fsq_part = nullptr, *fsq_out = nullptr;
 };
 
 const pmg_level *lvl(const pmg_hier *h, int c, const Fine &fv) {
@@ -137,7 +143,18 @@ int half_sweep(const pmg_hier *h, const pmg_level *l, double *u, const double *f
 // half-sweep ignores it (neighbours zero; rhs = f exactly); red_done: the
 // first red half-sweep was run by pmg_half_sweep_res
 int sweeps(const pmg_hier *h, const pmg_level *l, double *u, const double *f, int n,
-           bool from_zero, bool red_done, cudaStream_t st) {
+           bool from_zero, bool red_done, cudaStream_t st, const Fine *fsq = nullptr) {
+    if (fsq && fsq->fsq_part && n >= 1 && !red_done) {
+        // first sweep with ||f||^2 folded in (no fused halo on such levels)
+        int n1 = 0, n2 = 0;
+        TRY(pmg::half_sweep_fsq(l, u, f, 0, from_zero ? 1 : 0, fsq->fsq_part, &n1, st));
+        TRY(halo(h, l, u, st));
+        TRY(pmg::half_sweep_fsq(l, u, f, 1, 0, fsq->fsq_part + n1, &n2, st));
+        TRY(halo(h, l, u, st));
+        TRY(pmg::finalize(fsq->fsq_part, n1 + n2, fsq->fsq_out, st));
+        from_zero = false;
+        n -= 1;
+    }
     for (int s = 0; s < n; ++s) {
         if (red_done && s == 0)
             TRY(halo(h, l, u, st));
@@ -158,7 +175,8 @@ int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStr
     const bool red_done = c == 0 && fv.red_done;
     const bool lean = h->d.rho == 1.0;
     if (c + 1 < L) {
-        TRY(sweeps(h, lc, u, f, h->d.nu_pre, lean && (c > 0 || first), red_done, st));
+        TRY(sweeps(h, lc, u, f, h->d.nu_pre, lean && (c > 0 || first), red_done, st,
+                   c == 0 ? &fv : nullptr));
         if (h->d.red_restrict && lean && h->d.nu_pre >= 1 && pmg_residual_restrict_red_ok(lc))
             TRY(pmg_residual_restrict_red(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
         else
@@ -206,6 +224,10 @@ int lagged_body(pmg_hier *h, const double *f, int kind, const Lag &g, cudaStream
     Fine fv;
     fv.view = g.view[x];
     fv.red_done = kind >= 4;
+    if (kind < 4) {   // first cycle: ||f||^2 into res_d[1]
+        fv.fsq_part = h->scratch + pmg_partials_size() / 2;
+        fv.fsq_out = h->res_d + 1;
+    }
     TRY(vcycle(h, 0, g.base[x], f, kind < 4, st, fv));
     return pmg_half_sweep_res(g.view[x], g.base[x], g.base[x ^ 1], f, h->scratch, h->res_d, st);
 }
@@ -336,8 +358,7 @@ int pmg_vcycle(pmg_hier *h, double *u, const double *f, int first, void *stream)
 // makes the expected last iterate (the previous solve's count) land in the
 // caller's u; otherwise one red-array copy at the end.
 static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, int maxiter,
-                           double *hist, int *iters, int *converged, double r0,
-                           cudaStream_t st) {
+                           double *hist, int *iters, int *converged, cudaStream_t st) {
     const pmg_level *l0 = h->lv[0];
     long long plane, cs;
     int pitch, parity, uniform;
@@ -355,9 +376,22 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     // iterate k lives in red array (x0 + k - 1) & 1; want the last one in A
     int x = (h->last_iters & 1) ? 0 : 1;
     int kind = 2 + x;
+    *iters = 0;
+    *converged = 0;
+    double r0 = 0.0;
     for (int it = 0; it < maxiter; ++it) {
         TRY(replay_kind(h, u, f, kind, st, [&] { return lagged_body(h, f, kind, g, st); }));
         TRYC(cudaStreamSynchronize(st), "sync");
+        if (it == 0) {
+            // r0 = ||f|| (multigrid.py:307-309), summed by the first cycle
+            r0 = std::sqrt(h->res_h[1]);
+            hist[0] = r0;
+            if (r0 == 0.0) {   // multigrid.py:317-318: u = 0, no iterations
+                TRY(pmg_fill(l0, u, 0.0, st));
+                *converged = 1;
+                return PMG_OK;
+            }
+        }
         const double rn = std::sqrt(h->res_h[0]);
         hist[it + 1] = rn;
         *iters = it + 1;
@@ -378,6 +412,8 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
 
 static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int maxiter,
                        double *hist, int *iters, int *converged, cudaStream_t st) {
+    if (maxiter >= 1 && lagged_ok(h))
+        return mg_solve_lagged(h, f, u, eps, maxiter, hist, iters, converged, st);
     const pmg_level *l0 = h->lv[0];
     // r0 = ||f|| (multigrid.py:307-309)
     TRY(pmg_dot(l0, f, f, h->scratch, h->res_d, st));
@@ -391,8 +427,7 @@ static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int 
         *converged = 1;
         return PMG_OK;
     }
-    if (maxiter >= 1 && lagged_ok(h)) return mg_solve_lagged(h, f, u, eps, maxiter, hist, iters,
-                                                             converged, r0, st);
+
     // rho = 1: the first cycle starts from zero without filling u
     const bool lean_first = h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->lv.size() > 1;
     if (!lean_first) TRY(pmg_fill(l0, u, 0.0, st));

@@ -1269,6 +1269,9 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     // - bp u_{k+1}): 5 fp64 operations per cell on top of the sweep.  The
     // incoming values come from registers (RES = 1) or are staged in
     // shared memory by cp.async (RES = 2).
+    // RES = 3: an ordinary in-place half-sweep that also sums f^2 over its
+    // colour-c cells into dotp[blockIdx.x] (||f||^2 of mg_solve's first
+    // cycle, multigrid.py:307-309, without a separate pass over f)
     // NBZ = 0/1: neighbours-zero mode fixed at compile time; FULL: every warp
     // owns exactly SEG levels (nz % SEG == 0) -- no per-level predicates;
     // PLC: the k-plane stride as a compile-time constant (0: runtime), so
@@ -1300,7 +1303,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         ti[t] = make_double2(io, L.segtab[t]);
         tb[t] = make_double2(L.segtab[2 * nz + t], L.segtab[nz + t]);
         tq[t] = L.segtab[3 * nz + t];
-        if (RES) {
+        if (RES == 1 || RES == 2) {
             tr1[t] = make_double2(1.0 / io, L.diag1[t]);
             tr2[t] = make_double2((t >= 1) ? L.band1[t] : 0.0, (t + 1 < nz) ? L.band1[t + 1] : 0.0);
         }
@@ -1339,7 +1342,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
             for (int e = 0; e < SEG; ++e) cp_async8(vos + e * 32, u + pc + (long long)e * pl);
             cp_async_commit();
         }
-        if (RES) {
+        if (RES == 1 || RES == 2) {
             um = u[pc - ((k0 > 0) ? pl : 0)];
             un = u[pc + ((k0 + SEG < nz) ? SEG : SEG - 1) * pl];
         }
@@ -1378,8 +1381,9 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                         g = __fma_rn(cw.x, vw[e] + ve, g);
                     }
                     r[b8 + e] = g;
+                    if (RES == 3 && lane < nact) dacc = __fma_rn(vf[e], vf[e], dacc);
                 }
-                if (RES) {
+                if (RES == 1 || RES == 2) {
                     // residual of level k - 1 completes with u_k; level k's
                     // waits for u_{k+1}
                     if (RES == 2) {
@@ -1398,11 +1402,11 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                 }
             }
         }
-        if (RES) {
+        if (RES == 1 || RES == 2) {
             const double q = __fma_rn(bpend, un, rpend);
             if (lane < nact) dacc = __fma_rn(q, q, dacc);
         }
-        seg_solve_store<SEG, HALO, DOT>(L, RES ? uw : u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0,
+        seg_solve_store<SEG, HALO, DOT>(L, (RES == 1 || RES == 2) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0,
                                         i, nact, kn, pc, pl, zero_start, rho, scale, omr, f,
                                         &dacc);
     }
@@ -2590,6 +2594,37 @@ cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, con
     } else {
         run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, false, 1>);
     }
+    return cudaGetLastError();
+}
+
+// half-sweep that also sums f^2 over the relaxed colour (mg_solve's ||f||
+// folded into the first cycle's two half-sweeps); half_sweep_res_ok levels
+cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int color,
+                                  int nbr_zero, double *partials, int *np, cudaStream_t st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    f += (long long)color * (L.fcs - L.cstride);   // see launch_half_sweep
+    const int hx = ((L.nx + 1) / 2 + 31) / 32;
+    const int nw = L.nz / 16;
+    const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
+    const int ntiles = hx * L.ny;
+    auto run = [&](auto kern) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        const int grid = ntiles < cap ? ntiles : cap;
+        *np = grid;
+        kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, 1.0, 0, nbr_zero, 1.0, ntiles, hx,
+                                        partials, nullptr);
+    };
+#define PMG_FSQ(P)                                                                   \
+    do {                                                                             \
+        if (nbr_zero) run(k_half_sweep_seg<16, 4, 3, 1, true, false, P, false, 3>); \
+        else run(k_half_sweep_seg<16, 4, 3, 0, true, false, P, false, 3>);         \
+    } while (0)
+    if (L.plane == 520) PMG_FSQ(520);
+    else if (L.plane == 264) PMG_FSQ(264);
+    else PMG_FSQ(0);
+#undef PMG_FSQ
     return cudaGetLastError();
 }
 

@@ -898,11 +898,21 @@ def test_lagged_norm_solve(pmg, case):
             runs[lag] = out
         for a, b in zip(runs[False], runs[True]):
             assert a[0] == b[0] and a[1] == b[1]
-            assert a[2][0] == b[2][0]
+            # ||f|| summed inside the first cycle's half-sweeps (other order)
+            assert abs(a[2][0] - b[2][0]) <= 1e-14 * a[2][0]
             # the dropped black residual is ~1e-14 ||r0|| (rounding of the
             # exact black line solve): relative 1e-10 plus that floor
             assert np.all(np.abs(b[2] - a[2]) <= 1e-10 * a[2] + 1e-14 * a[2][0])
             assert np.array_equal(a[3], b[3])
+    # f = 0: no cycles, u = 0, history [0] (multigrid.py:317-318), after a
+    # solve that left a non-zero iterate behind
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=nlev, eps=1e-5)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    f = pmg.scatter_owned(fa, hier.fine.layout)
+    pmg.mg_solve(f, hier, cfg)
+    u, rep = pmg.mg_solve(pmg.scatter_owned(np.zeros_like(fa), hier.fine.layout), hier, cfg)
+    assert rep.iterations == 0 and rep.converged and rep.residual_history == [0.0]
+    assert not np.any(pmg.gather_owned(u))
 
 
 @pytest.mark.parametrize("par", [0, 1])
