@@ -90,12 +90,14 @@ int set_error(int code, const char *msg) { return fail(code, msg); }
 // driver-internal view of a level whose black array lies `cstride` doubles
 // from the red one (a red array in another allocation); shares the level's
 // device tables, owns nothing
-pmg_level *level_view(const pmg_level *lv, long long cstride) {
+pmg_level *level_view(const pmg_level *lv, long long cstride, int hflags_or) {
     pmg_level *v = new pmg_level(*lv);
     v->owned.clear();
     v->L.cstride = cstride;
+    v->L.hflags |= hflags_or;
     return v;
 }
+int level_hflags(const pmg_level *lv) { return lv->L.hflags; }
 void level_view_free(pmg_level *v) { delete v; }
 }
 

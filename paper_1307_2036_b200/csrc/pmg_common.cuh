@@ -34,12 +34,26 @@ struct Lvl {
     int seg;
     const double *segtab;
     // fused self-halo for a part that is its own neighbour (set per call):
-    // bit0 enabled, bit1 periodic x, bit2 periodic y
+    // bit0 enabled, bit1 periodic x, bit2 periodic y; bit3 (HF_WRAP): the
+    // part is periodic in x and y and the neighbour reads of the half-sweep,
+    // residual-restriction and prolongation kernels wrap around instead of
+    // reading the halo ring (which is then not maintained: pmg_driver.cu)
     int hflags;
     // 2-D device factors (variable coefficients)
     const double *wx, *wy, *av, *vh, *sumw;
     const double *invd;     // variable: per-cell pivots, field layout
 };
+
+constexpr int HF_WRAP = 8;
+
+// neighbour coordinates: the periodic image when the level wraps, else the
+// coordinate itself (-1 and n address the halo ring)
+__host__ __device__ __forceinline__ int wrapx(const Lvl &L, int i) {
+    return (L.hflags & HF_WRAP) ? (i < 0 ? i + L.nx : (i >= L.nx ? i - L.nx : i)) : i;
+}
+__host__ __device__ __forceinline__ int wrapy(const Lvl &L, int j) {
+    return (L.hflags & HF_WRAP) ? (j < 0 ? j + L.ny : (j >= L.ny ? j - L.ny : j)) : j;
+}
 
 __host__ __device__ __forceinline__ long long at(const Lvl &L, int c, int k, int j, int h) {
     return (long long)c * L.cstride + (long long)(j + 1) * L.jstride + (long long)k * L.plane + OFF + h;

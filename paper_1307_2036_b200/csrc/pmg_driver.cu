@@ -21,8 +21,10 @@
 
 namespace pmg {
 int set_error(int code, const char *msg);
-pmg_level *level_view(const pmg_level *lv, long long cstride);
+pmg_level *level_view(const pmg_level *lv, long long cstride, int hflags_or = 0);
 void level_view_free(pmg_level *v);
+int level_hflags(const pmg_level *lv);
+constexpr int HF_WRAP = 8;   // pmg_common.cuh
 int half_sweep_fsq(const pmg_level *lv, double *u, const double *f, int color, int nbr_zero,
                    double *partials, int *np, void *st);
 int finalize(const double *partials, int n, double *out, void *st);
@@ -72,6 +74,10 @@ struct pmg_hier {
     // previous solve (chooses which red array the first cycle writes)
     double *red1 = nullptr;
     int last_iters = 4;
+    // wrap views of the levels (periodic neighbour reads, no halo ring
+    // upkeep) for the lagged driver; empty when not eligible
+    std::vector<pmg_level *> wv;
+    long long wv_cs = 0;
     // the legacy default stream cannot be captured: solves issued on it run
     // on this stream, ordered after / before the caller's work by events
     cudaStream_t own = nullptr;
@@ -88,6 +94,8 @@ void free_hier(pmg_hier *h) {
     }
     if (h->scratch) cudaFree(h->scratch);
     if (h->red1) cudaFree(h->red1);
+    for (auto *v : h->wv)
+        if (v) pmg::level_view_free(v);
     if (h->res_h) cudaFreeHost(h->res_h);
     if (h->own) cudaStreamDestroy(h->own);
     if (h->ev_in) cudaEventDestroy(h->ev_in);
@@ -106,10 +114,14 @@ struct Fine {
 };
 
 const pmg_level *lvl(const pmg_hier *h, int c, const Fine &fv) {
-    return (c == 0 && fv.view) ? fv.view : h->lv[c];
+    if (c == 0 && fv.view) return fv.view;
+    if (fv.view && c < (int)h->wv.size() && h->wv[c]) return h->wv[c];
+    return h->lv[c];
 }
 
+// halo ring refresh, skipped on wrap views (their readers wrap around)
 int halo(const pmg_hier *h, const pmg_level *l, double *x, cudaStream_t st) {
+    if (pmg::level_hflags(l) & pmg::HF_WRAP) return PMG_OK;
     return pmg_halo_self(l, x, h->d.periodic_x, h->d.periodic_y, st);
 }
 
@@ -126,6 +138,7 @@ int fused_halo_nx() {
 
 int halo_flags(const pmg_hier *h, const pmg_level *l) {
     int nx, ny, nz;
+    if (pmg::level_hflags(l) & pmg::HF_WRAP) return 0;
     if (pmg_level_dims(l, &nx, &ny, &nz) || nx > fused_halo_nx()) return 0;
     return 1 | (h->d.periodic_x ? 2 : 0) | (h->d.periodic_y ? 4 : 0);
 }
@@ -177,10 +190,11 @@ int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStr
     if (c + 1 < L) {
         TRY(sweeps(h, lc, u, f, h->d.nu_pre, lean && (c > 0 || first), red_done, st,
                    c == 0 ? &fv : nullptr));
+        const pmg_level *lcc = lvl(h, c + 1, fv);
         if (h->d.red_restrict && lean && h->d.nu_pre >= 1 && pmg_residual_restrict_red_ok(lc))
-            TRY(pmg_residual_restrict_red(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
+            TRY(pmg_residual_restrict_red(lc, lcc, f, u, h->f[c + 1], st));
         else
-            TRY(pmg_residual_restrict(lc, h->lv[c + 1], f, u, h->f[c + 1], st));
+            TRY(pmg_residual_restrict(lc, lcc, f, u, h->f[c + 1], st));
         // the coarse iterate starts from zero: skip the fill when its first
         // red half-sweep ignores it anyway
         const int first_sweeps = (c + 2 == L) ? h->d.coarse_sweeps : h->d.nu_pre;
@@ -191,9 +205,9 @@ int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStr
         const int pmask = (lean && h->d.nu_post >= 1) ? 2 : 3;
         const int hf = halo_flags(h, lc);
         if (hf) {
-            TRY(pmg_prolong_colors_halo(lc, h->lv[c + 1], h->u[c + 1], u, 1, pmask, hf, st));
+            TRY(pmg_prolong_colors_halo(lc, lcc, h->u[c + 1], u, 1, pmask, hf, st));
         } else {
-            TRY(pmg_prolong_colors(lc, h->lv[c + 1], h->u[c + 1], u, 1, pmask, st));
+            TRY(pmg_prolong_colors(lc, lcc, h->u[c + 1], u, 1, pmask, st));
             TRY(halo(h, lc, u, st));
         }
         TRY(sweeps(h, lc, u, f, h->d.nu_post, false, false, st));
@@ -268,6 +282,25 @@ int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st)
     if (!st) return cycle_and_norm(h, u, f, first, st);   // legacy stream: no capture
     return replay_kind(h, u, f, first ? 1 : 0, st,
                        [&] { return cycle_and_norm(h, u, f, first, st); });
+}
+
+// every level can be read through a wrap view: periodic in x and y,
+// uniform coefficients in fast mode (k_half_sweep_seg), nx % 4 == 0 with a
+// coarse level of >= 2 columns (column-quad restriction / prolongation)
+bool wrap_ok(const pmg_hier *h) {
+    if (!h->d.periodic_x || !h->d.periodic_y || getenv("PMG_NO_WRAP") || getenv("PMG_CP") ||
+        getenv("PMG_RR_NOQ") || getenv("PMG_PROLONG_NOQ") || pmg_get_smoother_mode() != 0)
+        return false;
+    for (size_t c = 0; c < h->lv.size(); ++c) {
+        int nx, ny, nz, pitch, par, uni;
+        long long plane, cs;
+        if (pmg_level_dims(h->lv[c], &nx, &ny, &nz) ||
+            pmg_level_layout(h->lv[c], &pitch, &plane, &cs, &par, &uni))
+            return false;
+        if (!uni || nz > 256 || nx % 2 || ny % 2) return false;
+        if (c + 1 < h->lv.size() && (nx % 4 || nx < 4)) return false;
+    }
+    return true;
 }
 
 bool lagged_ok(const pmg_hier *h) {
@@ -364,15 +397,29 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     int pitch, parity, uniform;
     TRY(pmg_level_layout(l0, &pitch, &plane, &cs, &parity, &uniform));
     if (!h->red1) TRYC(cudaMalloc(&h->red1, sizeof(double) * cs), "red array");
+    if (h->wv.empty()) {
+        // wrap views of every level when all of them qualify
+        const int wrap = wrap_ok(h) ? pmg::HF_WRAP : 0;
+        h->wv.assign(h->lv.size(), nullptr);
+        if (wrap) {
+            for (size_t c = 0; c < h->lv.size(); ++c) {
+                long long pc2, cs2;
+                int p2, par2, uni2;
+                TRY(pmg_level_layout(h->lv[c], &p2, &pc2, &cs2, &par2, &uni2));
+                h->wv[c] = pmg::level_view(h->lv[c], cs2, wrap);
+            }
+        }
+    }
+    const int wrap = h->wv[0] ? pmg::HF_WRAP : 0;
     // black array of the caller's u, seen from red1
     const long long csb =
         (long long)(((intptr_t)(u + cs) - (intptr_t)h->red1) / (intptr_t)sizeof(double));
-    pmg_level *vb = pmg::level_view(l0, csb);
+    pmg_level *vb = pmg::level_view(l0, csb, wrap);
     struct Free {
         pmg_level *v;
         ~Free() { pmg::level_view_free(v); }
     } guard{vb};
-    Lag g{{l0, vb}, {u, h->red1}};
+    Lag g{{wrap ? h->wv[0] : l0, vb}, {u, h->red1}};
     // iterate k lives in red array (x0 + k - 1) & 1; want the last one in A
     int x = (h->last_iters & 1) ? 0 : 1;
     int kind = 2 + x;
@@ -407,6 +454,8 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     if (x == 1)   // the result's red array is red1: copy it into u
         TRYC(cudaMemcpyAsync(u, h->red1, sizeof(double) * cs, cudaMemcpyDeviceToDevice, st),
              "red array copy");
+    // wrap views left the halo ring stale: refresh it for the caller
+    if (wrap) TRY(pmg_halo_self(l0, u, h->d.periodic_x, h->d.periodic_y, st));
     return PMG_OK;
 }
 

@@ -572,11 +572,14 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
         // row bases at level 0 (colour at even i first, then odd i)
         const long long a_e = at(F, cAa, 0, ja, 2 * m), a_o = at(F, cAa ^ 1, 0, ja, 2 * m);
         const long long b_e = at(F, cAb, 0, jb, 2 * m), b_o = at(F, cAb ^ 1, 0, jb, 2 * m);
-        const long long al = at(F, cAa ^ 1, 0, ja, 2 * m - 1), ar = at(F, cAa, 0, ja, 2 * m + 2);
-        const long long bl = at(F, cAb ^ 1, 0, jb, 2 * m - 1), br = at(F, cAb, 0, jb, 2 * m + 2);
+        // outer W / E neighbours: fine i = 4m - 1 / 4m + 4 (wrapped when the level wraps)
+        const int iw = wrapx(F, 4 * m - 1) >> 1, ie = wrapx(F, 4 * m + 4) >> 1;
+        const long long al = at(F, cAa ^ 1, 0, ja, iw), ar = at(F, cAa, 0, ja, ie);
+        const long long bl = at(F, cAb ^ 1, 0, jb, iw), br = at(F, cAb, 0, jb, ie);
         // row ja-1: even-i colour = cAb (parity flips with j); row jb+1: cAa
-        const long long s_e = at(F, cAb, 0, ja - 1, 2 * m), s_o = at(F, cAa, 0, ja - 1, 2 * m);
-        const long long n_e = at(F, cAa, 0, jb + 1, 2 * m), n_o = at(F, cAb, 0, jb + 1, 2 * m);
+        const int js = wrapy(F, ja - 1), jn = wrapy(F, jb + 1);
+        const long long s_e = at(F, cAb, 0, js, 2 * m), s_o = at(F, cAa, 0, js, 2 * m);
+        const long long n_e = at(F, cAa, 0, jn, 2 * m), n_o = at(F, cAb, 0, jn, 2 * m);
         // f's colour arrays may lie fcs apart instead of cstride (Lvl::fcs)
         const long long fd = F.fcs - F.cstride;
         const double *fa_e = f + a_e + cAa * fd, *fa_o = f + a_o + (cAa ^ 1) * fd;
@@ -686,11 +689,14 @@ k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double
         const long long ba = at(F, 1, 0, ja, 2 * m), bb = at(F, 1, 0, jb, 2 * m);
         // outer black scalars: row ja W of its first red cell (PAR = 0: i = 4m-1)
         // or E of its last (PAR = 1: i = 4m+4); row jb the other way round
-        const long long xa = PAR ? at(F, 1, 0, ja, 2 * m + 2) : at(F, 1, 0, ja, 2 * m - 1);
-        const long long xb = PAR ? at(F, 1, 0, jb, 2 * m - 1) : at(F, 1, 0, jb, 2 * m + 2);
+        // (fine i = 4m - 1 / 4m + 4, wrapped when the level wraps)
+        const int iw = wrapx(F, 4 * m - 1) >> 1, ie = wrapx(F, 4 * m + 4) >> 1;
+        const long long xa = PAR ? at(F, 1, 0, ja, ie) : at(F, 1, 0, ja, iw);
+        const long long xb = PAR ? at(F, 1, 0, jb, iw) : at(F, 1, 0, jb, ie);
         // S of row ja = row ja-1 (black at row ja's red positions), N of
         // row jb = row jb+1 (black at row jb's red positions)
-        const long long sa = at(F, 1, 0, ja - 1, 2 * m), nb = at(F, 1, 0, jb + 1, 2 * m);
+        const long long sa = at(F, 1, 0, wrapy(F, ja - 1), 2 * m);
+        const long long nb = at(F, 1, 0, wrapy(F, jb + 1), 2 * m);
         const double *fa = f + ra, *fb = f + rb;   // colour 0: no fcs offset
         const int cc0 = (2 * m + J + C.par) & 1;
         const long long q0 = at(C, cc0, 0, J, m), q1 = at(C, cc0 ^ 1, 0, J, m);
@@ -1329,10 +1335,10 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         const int h = h0 + ln;
         const int i = 2 * h + s0;
         const long long pc = at(L, c, k0, j, h);
-        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
-        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
-        const long long pS = at(L, o, k0, j - 1, h);
-        const long long pN = at(L, o, k0, j + 1, h);
+        const long long pW = at(L, o, k0, j, wrapx(L, i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, wrapx(L, i + 1) >> 1);
+        const long long pS = at(L, o, k0, wrapy(L, j - 1), h);
+        const long long pN = at(L, o, k0, wrapy(L, j + 1), h);
         double r[SEG];
         // RES: incoming colour-c values below / above this warp's levels
         // (bm[0] = 0 and bp[nz-1] = 0 make the clamped loads inert)
@@ -1936,11 +1942,11 @@ k_prolong_q(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu
     double e0[3], e1[3], el[3], er[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const int Y = J - 1 + d;
+        const int Y = wrapy(C, J - 1 + d);
         e0[d] = cu[cell(C, 2 * m, Y, k)];
         e1[d] = cu[cell(C, 2 * m + 1, Y, k)];
-        const double xl = first ? cu[cell(C, 2 * m - 1, Y, k)] : 0.0;
-        const double xr = last ? cu[cell(C, 2 * m + 2, Y, k)] : 0.0;
+        const double xl = first ? cu[cell(C, wrapx(C, 2 * m - 1), Y, k)] : 0.0;
+        const double xr = last ? cu[cell(C, wrapx(C, 2 * m + 2), Y, k)] : 0.0;
         el[d] = __shfl_up_sync(0xffffffffu, e1[d], 1);
         er[d] = __shfl_down_sync(0xffffffffu, e0[d], 1);
         if (first) el[d] = xl;

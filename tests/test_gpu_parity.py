@@ -889,6 +889,13 @@ def test_lagged_norm_solve(pmg, case):
                 u, rep = pmg.mg_solve(f, hier, cfg)
                 out.append((rep.iterations, rep.converged, np.array(rep.residual_history),
                             pmg.gather_owned(u)))
+                # the returned iterate's halo ring is current (the lagged
+                # driver reads neighbours by wrap-around and refreshes the
+                # ring once at the end)
+                v = u.copy()
+                pmg.halo_exchange(v)
+                for w in u.parts:
+                    assert torch.equal(u.parts[w].data, v.parts[w].data)
             for maxiter in (1, 2, 3):
                 c2 = pmg.MGConfig(policy="explicit", explicit_levels=nlev, eps=1e-14,
                                   maxiter=maxiter, lagged_norm=lag)
