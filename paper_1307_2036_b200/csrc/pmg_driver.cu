@@ -254,7 +254,7 @@ int replay_kind(pmg_hier *h, double *u, const double *f, int kind, cudaStream_t 
             h->replayed += g.launches;
             return PMG_OK;
         }
-    if (h->graphs.size() >= 8) {
+    if (h->graphs.size() >= 32) {   // 4 cycle kinds x a few (f, u) pairs
         cudaGraphExecDestroy(h->graphs.front().exec);
         h->graphs.erase(h->graphs.begin());
     }

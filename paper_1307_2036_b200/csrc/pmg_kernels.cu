@@ -1919,6 +1919,92 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
     cu[cell(C, I, J, k)] = a;
 }
 
+// k_prolong_q with JB coarse rows per thread: the coarse rows J0-1 ..
+// J0+JB form a sliding window (JB + 2 row loads instead of 3 JB), and all
+// loads of the thread's rows are issued before any arithmetic.  Same
+// arithmetic and order: bit-identical to k_prolong_q.
+template <int JB>
+__global__ void __launch_bounds__(128)
+k_prolong_w(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
+            int cmask) {
+    const int lane = threadIdx.x & 31;
+    const int npair = C.nx >> 1;
+    const int m0 = blockIdx.x * 128 + (threadIdx.x & ~31);
+    if (m0 >= npair) return;
+    const int k = blockIdx.y, J0 = blockIdx.z * JB;
+    const int nact = min(32, npair - m0);
+    const bool act = lane < nact;
+    const int m = m0 + (act ? lane : nact - 1);
+    const bool first = lane == 0, last = lane == nact - 1;
+    const int ix0 = wrapx(C, 2 * m - 1), ix3 = wrapx(C, 2 * m + 2);
+    double e0[JB + 2], e1[JB + 2], xl[JB + 2], xr[JB + 2];
+#pragma unroll
+    for (int d = 0; d < JB + 2; ++d) {
+        const int Y = wrapy(C, min(J0 - 1 + d, C.ny));   // rows past the part: halo / wrap
+        e0[d] = cu[cell(C, 2 * m, Y, k)];
+        e1[d] = cu[cell(C, 2 * m + 1, Y, k)];
+        xl[d] = first ? cu[cell(C, ix0, Y, k)] : 0.0;
+        xr[d] = last ? cu[cell(C, ix3, Y, k)] : 0.0;
+    }
+    const int nj = min(JB, C.ny - J0);
+    D2 old[JB][2][2];
+    if (add) {
+#pragma unroll
+        for (int jj = 0; jj < JB; ++jj)
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    if ((cmask >> c & 1) && jj < nj && act)
+                        old[jj][r][c] = ld2(fu + at(F, c, k, 2 * (J0 + jj) + r, 2 * m));
+    }
+#pragma unroll
+    for (int jj = 0; jj < JB; ++jj) {
+        if (jj >= nj) break;
+        double el[3], er[3], a0[3], a1[3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            a0[d] = e0[jj + d];
+            a1[d] = e1[jj + d];
+            el[d] = __shfl_up_sync(0xffffffffu, a1[d], 1);
+            er[d] = __shfl_down_sync(0xffffffffu, a0[d], 1);
+            if (first) el[d] = xl[jj + d];
+            if (last) er[d] = xr[jj + d];
+        }
+        const int J = J0 + jj;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int j = 2 * J + r;
+            const int yn = r ? 2 : 0;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                if (!(cmask >> c & 1)) continue;
+                const int sc = (j + F.par + c) & 1;
+                double v[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double cc1 = q ? a1[1] : a0[1], ccn = q ? a1[yn] : a0[yn];
+                    const double xc1 = sc ? (q ? er[1] : a1[1]) : (q ? a0[1] : el[1]);
+                    const double xcn = sc ? (q ? er[yn] : a1[yn]) : (q ? a0[yn] : el[yn]);
+                    double e = 9.0 * cc1;
+                    e = e + 3.0 * xc1;
+                    e = e + 3.0 * ccn;
+                    e = e + xcn;
+                    v[q] = e * 0.0625;
+                }
+                if (act) {
+                    const long long qf = at(F, c, k, j, 2 * m);
+                    if (add) {
+                        v[0] = old[jj][r][c].x + v[0];
+                        v[1] = old[jj][r][c].y + v[1];
+                    }
+                    *reinterpret_cast<double2 *>(fu + qf) = make_double2(v[0], v[1]);
+                }
+            }
+        }
+    }
+}
+
 // Prolongation + add, one thread per coarse column pair (fine nx a
 // multiple of 4): the fine 4 x 2 window of coarse cells (2m, J), (2m+1, J).
 // Per level and coarse row J-1 .. J+1 each lane loads e(2m) and e(2m+1)
@@ -2941,8 +3027,18 @@ cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!(F.hflags & 1) && F.nx % 4 == 0 && C.nx >= 2 && !getenv("PMG_PROLONG_NOQ")) {
         const int npair = C.nx >> 1;
-        k_prolong_q<<<dim3((npair + 127) / 128, F.nz, C.ny), 128, 0, st>>>(F, C, cu, fu, add,
-                                                                           cmask);
+        static int jb = -1;
+        if (jb < 0) {
+            // coarse rows per thread: 2 measured best on B200 (configs[1]
+            // fine level, black only: 1 -> 310 us, 2 -> 252, 4 -> 274, 8 -> 341)
+            const char *e = getenv("PMG_PROLONG_JB");
+            jb = e ? atoi(e) : 2;
+        }
+        const int gx = (npair + 127) / 128;
+        if (jb == 2) k_prolong_w<2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+        else if (jb == 4) k_prolong_w<4><<<dim3(gx, F.nz, (C.ny + 3) / 4), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+        else if (jb == 8) k_prolong_w<8><<<dim3(gx, F.nz, (C.ny + 7) / 8), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+        else k_prolong_q<<<dim3(gx, F.nz, C.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
         return cudaGetLastError();
     }
     const int n2 = (cmask == 3 ? 2 : 1) * ((F.nx + 1) / 2);
