@@ -2963,7 +2963,19 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             run(k_half_sweep_seg<S, 4, 2>);                                           \
         }                                                                             \
     } while (0)
-            if (plc == 520 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 520);
+            static int small = -1;
+            if (small < 0) {
+                // levels of <= 64 tiles (nx <= 64 at nz = 128): 5.5 -> 4.5 us per
+                // sweep; 256 tiles (nx = 128) is slower this way (6.6 -> 7.9)
+                const char *e = getenv("PMG_SMALL_TILES");
+                small = e ? atoi(e) : 64;
+            }
+            if (L.seg == 16 && full && !(L.hflags & 1) && ntiles <= small) {
+                // launch-latency-bound small level: all 16 levels' loads of a
+                // tile in one batch (one memory round trip per tile)
+                if (nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, false, 0>);
+                else run(k_half_sweep_seg<16, 16, 1, 0, true, false, 0>);
+            } else if (plc == 520 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 520);
             else if (plc == 264 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 264);
             else if (plc == 136 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 136);
             else switch (L.seg) {
