@@ -1145,24 +1145,6 @@ k_half_sweep_tx(Lvl L, double *__restrict__ u, int c, double rho, int zero_start
     }
 }
 
-// 8-byte asynchronous global -> shared copy (LDGSTS): the RES half-sweep
-// stages the incoming colour-c values there, off the register file
-__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                     (unsigned)__cvta_generic_to_shared(smem)),
-                 "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_wait() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
 // ---------------------------------------------------------------------------
 // Line smoother half-sweep, FAST mode (default, uniform coefficients):
 // k-segmented column solve.
@@ -1265,16 +1247,14 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                  double *__restrict__ dotp, double *__restrict__ uw) {
     // DOT: also dotp[blockIdx.x] = sum over this CTA's cells of f * (new u),
     // fixed order (CG's <r, z> fused into the SSOR half-sweeps)
-    // RES = 1, 2 (rho = 1, FULL, NBZ = 0): u is only read; the relaxed
+    // RES = 1 (rho = 1, FULL, NBZ = 0): u is only read; the relaxed
     // colour-c values go to uw (same offsets, another buffer), and
     // dotp[blockIdx.x] receives this CTA's sum of (f - A u)^2 over its
     // colour-c cells of the INCOMING iterate: the lagged convergence norm
     // of the previous V-cycle.  The line's right-hand side
     // f + drw (wx (u_W + u_E) + wy (u_S + u_N)) is the sweep's own
     // (g = iota rhs, so rhs = g / iota), and r = rhs - (d u_k - bm u_{k-1}
-    // - bp u_{k+1}): 5 fp64 operations per cell on top of the sweep.  The
-    // incoming values come from registers (RES = 1) or are staged in
-    // shared memory by cp.async (RES = 2).
+    // - bp u_{k+1}): 5 fp64 operations per cell on top of the sweep.
     // RES = 3: an ordinary in-place half-sweep that also sums f^2 over its
     // colour-c cells into dotp[blockIdx.x] (||f||^2 of mg_solve's first
     // cycle, multigrid.py:307-309, without a separate pass over f)
@@ -1299,9 +1279,6 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     // RES: (1 / iota, diag) and zero-padded vertical couplings (bm, bp) as in k_norm_v
     double2 *tr1 = reinterpret_cast<double2 *>(ybeg0 + 2 * 16 * 32);   // [nz]
     double2 *tr2 = tr1 + nz;                                          // [nz]
-    // RES: this thread's incoming colour-c values, [warp][level][lane]
-    double *vos = reinterpret_cast<double *>(tr2 + nz) + (threadIdx.x >> 5) * SEG * 32 +
-                  (threadIdx.x & 31);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int t = threadIdx.x; t < nz; t += blockDim.x) {
         const double io = L.invd1[t], dd = io * L.drw[t];
@@ -1309,7 +1286,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         ti[t] = make_double2(io, L.segtab[t]);
         tb[t] = make_double2(L.segtab[2 * nz + t], L.segtab[nz + t]);
         tq[t] = L.segtab[3 * nz + t];
-        if (RES == 1 || RES == 2) {
+        if (RES == 1) {
             tr1[t] = make_double2(1.0 / io, L.diag1[t]);
             tr2[t] = make_double2((t >= 1) ? L.band1[t] : 0.0, (t + 1 < nz) ? L.band1[t + 1] : 0.0);
         }
@@ -1343,12 +1320,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
         // RES: incoming colour-c values below / above this warp's levels
         // (bm[0] = 0 and bp[nz-1] = 0 make the clamped loads inert)
         double um = 0.0, un = 0.0, rpend = 0.0, bpend = 0.0;
-        if (RES == 2) {
-#pragma unroll
-            for (int e = 0; e < SEG; ++e) cp_async8(vos + e * 32, u + pc + (long long)e * pl);
-            cp_async_commit();
-        }
-        if (RES == 1 || RES == 2) {
+        if (RES == 1) {
             um = u[pc - ((k0 > 0) ? pl : 0)];
             un = u[pc + ((k0 + SEG < nz) ? SEG : SEG - 1) * pl];
         }
@@ -1389,13 +1361,9 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                     r[b8 + e] = g;
                     if (RES == 3 && lane < nact) dacc = __fma_rn(vf[e], vf[e], dacc);
                 }
-                if (RES == 1 || RES == 2) {
+                if (RES == 1) {
                     // residual of level k - 1 completes with u_k; level k's
                     // waits for u_{k+1}
-                    if (RES == 2) {
-                        if (kk == 0) cp_async_wait();   // own copies only: no barrier
-                        vo[e] = vos[kk * 32];
-                    }
                     const double2 t1 = tr1[k0 + kk], t2 = tr2[k0 + kk];
                     if (kk > 0) {
                         const double q = __fma_rn(bpend, vo[e], rpend);
@@ -1408,13 +1376,13 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
                 }
             }
         }
-        if (RES == 1 || RES == 2) {
+        if (RES == 1) {
             const double q = __fma_rn(bpend, un, rpend);
             if (lane < nact) dacc = __fma_rn(q, q, dacc);
         }
-        seg_solve_store<SEG, HALO, DOT>(L, (RES == 1 || RES == 2) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0,
-                                        i, nact, kn, pc, pl, zero_start, rho, scale, omr, f,
-                                        &dacc);
+        seg_solve_store<SEG, HALO, DOT>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
+                                        h0, s0, i, nact, kn, pc, pl, zero_start, rho, scale, omr,
+                                        f, &dacc);
     }
     if (DOT || RES) {
         const double s2 = block_sum(dacc);
@@ -2656,7 +2624,7 @@ cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, con
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
-    const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32 + 32 * (size_t)L.nz);
+    const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
     const int ntiles = hx * L.ny;
     auto run = [&](auto kern) {
         int occ = 1;
@@ -2667,25 +2635,13 @@ cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, con
         kern<<<grid, 32 * nw, sm, st>>>(L, const_cast<double *>(u), f, 0, 1.0, 0, 0, 1.0, ntiles,
                                         hx, partials, uw);
     };
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PMG_RES_V");
-        v = e ? atoi(e) : 0;
-    }
-    // v: 0 = register loads, 2 CTAs / SM (default, 128 registers, no spills:
-    // 413 us at configs[1]'s fine level); 1 = register loads, 3 CTAs (80
-    // registers, spills: 517 us); 2 = cp.async staging, 2 CTAs (413 us);
-    // 3 = cp.async, 3 CTAs (538 us) -- measured on B200, DESIGN.md section 3
-    if (L.plane == 520) {
-        if (v == 1) run(k_half_sweep_seg<16, 4, 3, 0, true, false, 520, false, 1>);
-        else if (v == 2) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, 2>);
-        else if (v == 3) run(k_half_sweep_seg<16, 4, 3, 0, true, false, 520, false, 2>);
-        else run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, 1>);
-    } else if (L.plane == 264) {
-        run(k_half_sweep_seg<16, 4, 2, 0, true, false, 264, false, 1>);
-    } else {
-        run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, false, 1>);
-    }
+    // register loads at 2 CTAs / SM (128 registers, no spills): 413 us at
+    // configs[1]'s fine level; at 3 CTAs / SM (80 registers, spills) 517 us,
+    // with the incoming values staged in shared memory by cp.async 413 /
+    // 538 us at 2 / 3 CTAs
+    if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, 1>);
+    else if (L.plane == 264) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 264, false, 1>);
+    else run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, false, 1>);
     return cudaGetLastError();
 }
 
@@ -2773,21 +2729,6 @@ void setup_kernel_attributes() {
     if (done) return;
     done = true;
     const int big = 227 * 1024;
-    // RES half-sweeps stage the incoming values in > 48 KB of shared memory
-    // (the limit counts their 256 B of static shared memory too)
-    const int res_big = big - 1024;
-    cudaFuncSetAttribute(k_half_sweep_seg<16, 4, 3, 0, true, false, 520, false, 2>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, res_big);
-    cudaFuncSetAttribute(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, 2>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, res_big);
-    cudaFuncSetAttribute(k_half_sweep_seg<16, 4, 3, 0, true, false, 520, false, 1>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, res_big);
-    cudaFuncSetAttribute(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, 1>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, res_big);
-    cudaFuncSetAttribute(k_half_sweep_seg<16, 4, 2, 0, true, false, 264, false, 1>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, res_big);
-    cudaFuncSetAttribute(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, false, 1>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, res_big);
     cudaFuncSetAttribute(k_half_sweep_cp<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
