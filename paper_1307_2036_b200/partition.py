@@ -154,10 +154,10 @@ class LevelLayout:
         if d is not None:
             if d.get_world_size() != decomp.workers:
                 raise ValueError("one worker per rank: world size must equal the worker count")
-            if len(self.workers) != decomp.workers:
-                raise ValueError("coarse-level folding across ranks is not supported "
-                                 "(use the shallow policy or fewer levels)")
-            self.local_workers = [d.get_rank()]
+            # one part per rank; on a folded level (fewer active workers)
+            # the ranks outside the active sub-grid hold no part
+            r = d.get_rank()
+            self.local_workers = [r] if r in self.workers else []
         else:
             self.local_workers = list(self.workers)
 
@@ -313,22 +313,27 @@ class DistField:
     """A field split over the parts of one layout (reference ``DistField``,
     partition.py:121-155).  ``parts`` holds the parts hosted here."""
 
-    __slots__ = ("layout", "parts")
+    __slots__ = ("layout", "parts", "_nz")
 
-    def __init__(self, layout: LevelLayout, parts: dict):
+    def __init__(self, layout: LevelLayout, parts: dict, nz: int | None = None):
         self.layout = layout
         self.parts = parts
+        self._nz = nz
 
     @classmethod
     def zeros(cls, layout: LevelLayout, nz: int) -> "DistField":
-        return cls(layout, {w: DevField(layout.geometry(w, nz)) for w in layout.local_workers})
+        return cls(layout, {w: DevField(layout.geometry(w, nz)) for w in layout.local_workers},
+                   nz)
 
     @property
     def nz(self) -> int:
-        return next(iter(self.parts.values())).nz
+        # a rank that is inactive on a folded level holds no part
+        if self._nz is None:
+            self._nz = next(iter(self.parts.values())).nz
+        return self._nz
 
     def copy(self) -> "DistField":
-        return DistField(self.layout, {w: f.copy() for w, f in self.parts.items()})
+        return DistField(self.layout, {w: f.copy() for w, f in self.parts.items()}, self._nz)
 
     def copy_from(self, other: "DistField") -> None:
         for w, f in self.parts.items():
@@ -404,6 +409,9 @@ def halo_exchange(df: DistField) -> None:
     boundaries.  Counted once per call on the layout."""
     lay = df.layout
     st = _stream()
+    if not df.parts:          # a rank outside a folded level's active grid
+        lay.halo_count += 1
+        return
     if lay.px == 1 and lay.py == 1:
         f = df.parts[lay.workers[0]]
         call("pmg_halo_self", f.geom.h, f.ptr, int(lay.periodic), int(lay.periodic), st)
@@ -511,6 +519,11 @@ def collect(df: DistField, to_layout: LevelLayout) -> DistField:
         raise ValueError("collect target must fold the active grid at the same level size")
     out = DistField.zeros(to_layout, df.nz)
     st = _stream()
+    d = _dist()
+    if d is not None:
+        _collect_dist(df, out, fx, fy, st, d)
+        lay.decomp.collect_calls += 1
+        return out
     for pw, big in out.parts.items():
         ai, aj = to_layout.coords(pw)
         for di in range(fx):
@@ -520,6 +533,63 @@ def collect(df: DistField, to_layout: LevelLayout) -> DistField:
                      di * lay.mx, dj * lay.my, lay.mx, lay.my, st)
     lay.decomp.collect_calls += 1
     return out
+
+
+def fold_root(lay: LevelLayout, to_layout: LevelLayout, w: int) -> int:
+    """The worker of ``to_layout`` (folded) whose part holds worker ``w``'s
+    block of ``lay`` (partition.py:194-218: the group's lowest index)."""
+    fx, fy = lay.px // to_layout.px, lay.py // to_layout.py
+    ai, aj = lay.coords(w)
+    return to_layout.worker_at(ai // fx, aj // fy)
+
+
+def _p2p(dist, sends, recvs) -> None:
+    """Post point-to-point transfers [(tensor, peer)] and wait: device
+    tensors under NCCL; under a CPU backend (gloo) device tensors are
+    staged through host memory."""
+    if not sends and not recvs:
+        return
+    staged = dist.get_backend() != "nccl"
+    if staged:
+        torch.cuda.current_stream().synchronize()
+        hs = [(t.cpu(), p) for t, p in sends]
+        hr = [(torch.empty(t.shape, dtype=t.dtype), p) for t, p in recvs]
+    else:
+        hs, hr = sends, recvs
+    ops = [dist.P2POp(dist.isend, t, p) for t, p in hs]
+    ops += [dist.P2POp(dist.irecv, t, p) for t, p in hr]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    if staged:
+        for (t, _), (h, _) in zip(recvs, hr):
+            t.copy_(h)
+
+
+def _collect_dist(df: DistField, out: DistField, fx: int, fy: int, st, dist) -> None:
+    """collect across ranks: a part whose group root is another rank sends
+    its whole part buffer there; the root places every block of its group
+    (received ones through a temporary part of the sender's geometry)."""
+    lay, to = df.layout, out.layout
+    sends, recvs, place = [], [], []
+    for w, f in df.parts.items():
+        root = fold_root(lay, to, w)
+        if root != w:
+            sends.append((f.data, root))
+    for pw, big in out.parts.items():
+        ai, aj = to.coords(pw)
+        for di in range(fx):
+            for dj in range(fy):
+                cw = lay.worker_at(fx * ai + di, fy * aj + dj)
+                if cw in df.parts:
+                    src = df.parts[cw]
+                else:
+                    src = DevField(lay.geometry(cw, df.nz))
+                    recvs.append((src.data, cw))
+                place.append((src, big, di, dj))
+    _p2p(dist, sends, recvs)
+    for src, big, di, dj in place:
+        call("pmg_copy_block", src.geom.h, src.ptr, big.geom.h, big.ptr, 0, 0,
+             di * lay.mx, dj * lay.my, lay.mx, lay.my, st)
 
 
 def distribute(df: DistField, to_layout: LevelLayout, out: DistField | None = None) -> DistField:
@@ -535,6 +605,29 @@ def distribute(df: DistField, to_layout: LevelLayout, out: DistField | None = No
         out = DistField.zeros(to_layout, df.nz)
     st = _stream()
     m, n = to_layout.mx, to_layout.my
+    d = _dist()
+    if d is not None:
+        # across ranks: the root cuts every child's block + ring into a
+        # part of the child's geometry and sends the whole part buffer
+        sends, recvs = [], []
+        for pw, big in df.parts.items():
+            pi, pj = lay.coords(pw)
+            for di in range(fx):
+                for dj in range(fy):
+                    cw = to_layout.worker_at(fx * pi + di, fy * pj + dj)
+                    ch = (out.parts[cw] if cw in out.parts
+                          else DevField(to_layout.geometry(cw, df.nz)))
+                    call("pmg_copy_block", big.geom.h, big.ptr, ch.geom.h, ch.ptr,
+                         di * m - 1, dj * n - 1, -1, -1, m + 2, n + 2, st)
+                    if cw not in out.parts:
+                        sends.append((ch.data, cw))
+        for cw, ch in out.parts.items():
+            root = fold_root(to_layout, lay, cw)
+            if root != cw:
+                recvs.append((ch.data, root))
+        _p2p(d, sends, recvs)
+        lay.decomp.distribute_calls += 1
+        return out
     for cw, ch in out.parts.items():
         ai, aj = to_layout.coords(cw)
         big = df.parts[lay.worker_at(ai // fx, aj // fy)]
@@ -630,11 +723,15 @@ def reduce_parts(vals: torch.Tensor) -> float:
     tot = vals.sum() if vals.numel() > 1 else vals[0]
     d = _dist()
     if d is not None:
+        # gather the per-rank sums and add them in rank (= worker) order on
+        # every rank: the same left-to-right order as the in-process sum over
+        # parts, independent of the backend's all-reduce algorithm
         t = tot.reshape(1).clone()
         if d.get_backend() != "nccl":
             t = t.cpu()
-        d.all_reduce(t)
-        return float(t.item())
+        allp = [torch.empty_like(t) for _ in range(d.get_world_size())]
+        d.all_gather(allp, t)
+        return float(sum(float(x.item()) for x in allp))
     return float(tot.item())
 
 

@@ -110,3 +110,25 @@ def test_worker_split():
         Decomposition(64, 3)
     with pytest.raises(ValueError):
         Decomposition(6, 16)
+
+
+@pytest.mark.parametrize("px,py,apx,apy", [(2, 2, 1, 1), (4, 2, 2, 1), (4, 4, 2, 2)])
+def test_fold_roots(px, py, apx, apy):
+    """Cross-rank folding plan (partition.collect / distribute under a
+    process group): every worker of the unfolded layout maps to the
+    lowest-indexed worker of its (px/apx) x (py/apy) group, which is active
+    on the folded layout and maps to itself."""
+    from paper_1307_2036_b200.partition import Decomposition, fold_root
+    dec = Decomposition(64, px * py, px=px, py=py, periodic=True)
+    lay, fol = dec.layout(64), dec.layout(64, active=(apx, apy))
+    gx, gy = px // apx, py // apy
+    roots = {}
+    for w in lay.workers:
+        wi, wj = divmod(w, py)
+        want = (wi // gx * gx) * py + (wj // gy * gy)
+        r = fold_root(lay, fol, w)
+        assert r == want and r in fol.workers
+        roots.setdefault(r, []).append(w)
+    assert sorted(roots) == sorted(fol.workers)
+    assert all(len(v) == gx * gy for v in roots.values())
+    assert all(fold_root(lay, fol, r) == r for r in fol.workers)

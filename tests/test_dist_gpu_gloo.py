@@ -22,7 +22,15 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, px, q):
+def _cfg(pmg, policy):
+    if policy == "explicit":
+        return pmg.MGConfig(policy="explicit", explicit_levels=3, eps=1e-8)
+    if policy == "standard":      # down to one global column: folds at nx = 1
+        return pmg.MGConfig(policy="standard", eps=1e-8)
+    return pmg.MGConfig(policy="standard", l_split=3, eps=1e-8)   # folds from l_split on
+
+
+def _worker(rank, world, port, px, q, policy="explicit"):
     trace = os.environ.get("PMG_TEST_TRACE")
     if trace:                       # debugging aid: dump stacks if stuck
         import faulthandler
@@ -41,7 +49,7 @@ def _worker(rank, world, port, px, q):
         grid = pmg.periodic_box(nx, nz, 0.01)
         params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
         dec = pmg.Decomposition(nx, world, px=px, py=py, periodic=True)
-        cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, eps=1e-8)
+        cfg = _cfg(pmg, policy)
         hier = pmg.build_hierarchy(grid, params, cfg, dec)
         lay = hier.fine.layout
         i0, j0 = lay.origin(rank)
@@ -54,22 +62,28 @@ def _worker(rank, world, port, px, q):
                                maxiter=200)
         ucg = pmg.gather_owned(uc)          # collective: every rank calls it
         q.put((rank, rep.residual_history, ug if rank == 0 else None, rc.residual_history,
-               ucg if rank == 0 else None))
+               ucg if rank == 0 else None, dec.collect_calls, dec.distribute_calls))
         dist.barrier()
         dist.destroy_process_group()
     except Exception as err:  # surfaced by the parent
         import traceback
-        q.put((rank, repr(err) + traceback.format_exc(), None, None, None))
+        q.put((rank, repr(err) + traceback.format_exc(), None, None, None, 0, 0))
 
 
-@pytest.mark.parametrize("world,px", [(2, 2), (4, 2)])
-def test_rank_path_matches_in_process(world, px):
+@pytest.mark.parametrize("world,px,policy", [(2, 2, "explicit"), (4, 2, "explicit"),
+                                             (4, 2, "standard"), (4, 2, "lsplit")])
+def test_rank_path_matches_in_process(world, px, policy):
+    """Rank path == in-process decomposition, bit for bit, also with
+    coarse-level folding across ranks (standard policy down to one global
+    column, and l_split): collect / distribute move whole part buffers
+    between a group's ranks and its root."""
     import torch.multiprocessing as mp
     import paper_1307_2036_b200 as pmg
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, px, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, px, q, policy))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -85,7 +99,7 @@ def test_rank_path_matches_in_process(world, px):
     grid = pmg.periodic_box(nx, nz, 0.01)
     params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
     dec = pmg.Decomposition(nx, world, px=px, py=world // px, periodic=True)
-    cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, eps=1e-8)
+    cfg = _cfg(pmg, policy)
     hier = pmg.build_hierarchy(grid, params, cfg, dec)
     fg = np.random.default_rng(3).uniform(-1, 1, (nx, nx, nz))
     f = pmg.scatter_owned(fg, hier.fine.layout)
@@ -98,3 +112,7 @@ def test_rank_path_matches_in_process(world, px):
         assert r[3] == rc.residual_history
     assert np.array_equal(res[0][2], pmg.gather_owned(u))
     assert np.array_equal(res[0][4], pmg.gather_owned(uc))
+    if policy != "explicit":      # one fold per V-cycle, on every rank
+        cycles = len(rep.residual_history) - 1
+        for r in res.values():
+            assert (r[5], r[6]) == (cycles, cycles)
