@@ -2284,6 +2284,89 @@ k_cg_update(Lvl L, const double *__restrict__ num, const double *__restrict__ de
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// Vectorised CG updates (double2, four independent iterations per thread in
+// flight): the element arithmetic of k_cg_up / k_cg_update unchanged.
+__global__ void __launch_bounds__(256)
+k_cg_up_v(long long n2, const double *__restrict__ an, const double *__restrict__ ad,
+          const double *__restrict__ bn, const double *__restrict__ bd,
+          const double2 *__restrict__ z, double2 *__restrict__ p, double2 *__restrict__ u) {
+    const double a = an[0] / ad[0];
+    const double b = z ? bn[0] / bd[0] : 0.0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (; e + 3 * stride < n2; e += 4 * stride) {
+        double2 pv[4], uv[4], zv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            pv[t] = p[e + t * stride];
+            uv[t] = u[e + t * stride];
+            if (z) zv[t] = z[e + t * stride];
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            double2 nu;
+            nu.x = uv[t].x + a * pv[t].x;
+            nu.y = uv[t].y + a * pv[t].y;
+            u[e + t * stride] = nu;
+            if (z) {
+                double2 np;
+                np.x = b * pv[t].x + zv[t].x;
+                np.y = b * pv[t].y + zv[t].y;
+                p[e + t * stride] = np;
+            }
+        }
+    }
+    for (; e < n2; e += stride) {
+        const double2 pv = p[e], uv = u[e];
+        u[e] = make_double2(uv.x + a * pv.x, uv.y + a * pv.y);
+        if (z) {
+            const double2 zv = z[e];
+            p[e] = make_double2(b * pv.x + zv.x, b * pv.y + zv.y);
+        }
+    }
+}
+
+// one warp per allocation row (c, jj, k): u += alpha p (if u), r -= alpha q
+// over the whole row, ||r||^2 over its owned cells; double2 accesses
+__global__ void __launch_bounds__(256)
+k_cg_update_v(Lvl L, const double *__restrict__ num, const double *__restrict__ den,
+              const double *__restrict__ p, const double *__restrict__ q,
+              double *__restrict__ u, double *__restrict__ r, double *__restrict__ partials) {
+    const double alpha = num[0] / den[0];
+    const double malpha = -alpha;
+    const int nrows = 2 * (L.ny + 2) * L.nz;
+    const int lane = threadIdx.x & 31;
+    const int np2 = L.pitch >> 1;
+    double s = 0.0;
+    for (int row = blockIdx.x * 8 + (threadIdx.x >> 5); row < nrows; row += gridDim.x * 8) {
+        const int jj = (row / L.nz) % (L.ny + 2);
+        const int c = row / ((L.ny + 2) * L.nz);
+        const int j = jj - 1;
+        const int s0 = (j + L.par + c) & 1;
+        const long long base = (long long)row * L.pitch;
+        const bool owned_row = (j >= 0 && j < L.ny);
+        const double2 *q2 = reinterpret_cast<const double2 *>(q + base);
+        double2 *r2 = reinterpret_cast<double2 *>(r + base);
+#pragma unroll 4
+        for (int t2 = lane; t2 < np2; t2 += 32) {
+            if (u != nullptr) {
+                const double2 pv = reinterpret_cast<const double2 *>(p + base)[t2];
+                double2 *u2 = reinterpret_cast<double2 *>(u + base);
+                const double2 uv = u2[t2];
+                u2[t2] = make_double2(uv.x + alpha * pv.x, uv.y + alpha * pv.y);
+            }
+            const double2 qv = q2[t2], rv0 = r2[t2];
+            const double2 rv = make_double2(rv0.x + malpha * qv.x, rv0.y + malpha * qv.y);
+            r2[t2] = rv;
+            const int h = 2 * t2 - OFF;
+            if (owned_row && h >= 0 && 2 * h + s0 < L.nx) s += rv.x * rv.x;
+            if (owned_row && h + 1 >= 0 && 2 * (h + 1) + s0 < L.nx) s += rv.y * rv.y;
+        }
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
 // ---------------------------------------------------------------------------
 // layout conversion: reference (nx, ny, nz) k-fastest <-> split layout.
 // 32x32 (i, k) tiles through shared memory so both sides are coalesced.
@@ -3089,6 +3172,17 @@ cudaError_t launch_cg_direction(long long n, const double *num, const double *de
 cudaError_t launch_cg_up(long long n, const double *an, const double *ad, const double *bn,
                          const double *bd, const double *z, double *p, double *u, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (n % 2 == 0 && !getenv("PMG_CG_SCALAR")) {
+        // whole allocations: even length, 16-byte aligned
+        const long long n2 = n / 2;
+        long long b = (n2 + 255) / 256;
+        if (b > 8LL * sm_count()) b = 8LL * sm_count();
+        k_cg_up_v<<<(int)b, 256, 0, st>>>(n2, an, ad, bn, bd,
+                                          reinterpret_cast<const double2 *>(z),
+                                          reinterpret_cast<double2 *>(p),
+                                          reinterpret_cast<double2 *>(u));
+        return cudaGetLastError();
+    }
     k_cg_up<<<stream_blocks(n), 256, 0, st>>>(n, an, ad, bn, bd, z, p, u);
     return cudaGetLastError();
 }
@@ -3098,6 +3192,14 @@ cudaError_t launch_cg_update(const Lvl &L, const double *num, const double *den,
                              double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const long long n = 2LL * L.cstride;
+    if (L.pitch % 2 == 0 && !getenv("PMG_CG_SCALAR")) {
+        const int rows = 2 * L.nz * (L.ny + 2);
+        int g = 8 * sm_count();
+        if (g > (rows + 7) / 8) g = (rows + 7) / 8;
+        *np = g;
+        k_cg_update_v<<<g, 256, 0, st>>>(L, num, den, p, q, u, r, partials);
+        return cudaGetLastError();
+    }
     int g = stream_blocks(n);
     if (g > 2 * L.nz * (L.ny + 2)) g = 2 * L.nz * (L.ny + 2);
     *np = g;
