@@ -121,6 +121,10 @@ namespace pmg {
 // over the relaxed colour: per-CTA partials into partials[0 .. *np)
 int half_sweep_fsq(const pmg_level *lv, double *u, const double *f, int color, int nbr_zero,
                    double *partials, int *np, void *st) {
+    if (!lv->L.uniform && !lv->prepared) {
+        int rc = pmg_level_prepare(const_cast<pmg_level *>(lv), st);
+        if (rc) return rc;
+    }
     PMG_CUDA(launch_half_sweep_fsq(lv->L, u, f, color, nbr_zero, partials, np, (cudaStream_t)st),
              "half_sweep_fsq");
     return PMG_OK;
@@ -443,8 +447,12 @@ int pmg_half_sweep_res(const pmg_level *lv, const double *u, double *u_new, cons
     if (!u || !u_new || !f || !scratch || !norm2) return fail(PMG_ERR_VALUE, "null argument");
     if (u == u_new) return fail(PMG_ERR_VALUE, "u_new must be a different buffer from u");
     if (!half_sweep_res_ok(lv->L))
-        return fail(PMG_ERR_VALUE, "fused sweep + residual needs fast mode, uniform "
-                                   "coefficients and nz a multiple of 16 (<= 128)");
+        return fail(PMG_ERR_VALUE, "fused sweep + residual needs fast mode and nz a multiple "
+                                   "of 16 (uniform: <= 128, variable: <= 256)");
+    if (!lv->L.uniform && !lv->prepared) {
+        int rc = pmg_level_prepare(const_cast<pmg_level *>(lv), st);
+        if (rc) return rc;
+    }
     int np = 0;
     PMG_CUDA(launch_half_sweep_res(lv->L, u, u_new, f, scratch, &np, (cudaStream_t)st),
              "half_sweep_res");

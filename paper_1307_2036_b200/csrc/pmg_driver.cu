@@ -284,9 +284,9 @@ int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st)
                        [&] { return cycle_and_norm(h, u, f, first, st); });
 }
 
-// every level can be read through a wrap view: periodic in x and y,
-// uniform coefficients in fast mode (k_half_sweep_seg), nx % 4 == 0 with a
-// coarse level of >= 2 columns (column-quad restriction / prolongation)
+// every level can be read through a wrap view: periodic in x and y, fast
+// mode (k_half_sweep_seg / k_half_sweep_segv), nx % 4 == 0 with a coarse
+// level of >= 2 columns (column-quad restriction / prolongation)
 bool wrap_ok(const pmg_hier *h) {
     if (!h->d.periodic_x || !h->d.periodic_y || getenv("PMG_NO_WRAP") || getenv("PMG_CP") ||
         getenv("PMG_RR_NOQ") || getenv("PMG_PROLONG_NOQ") || pmg_get_smoother_mode() != 0)
@@ -297,8 +297,17 @@ bool wrap_ok(const pmg_hier *h) {
         if (pmg_level_dims(h->lv[c], &nx, &ny, &nz) ||
             pmg_level_layout(h->lv[c], &pitch, &plane, &cs, &par, &uni))
             return false;
-        if (!uni || nz > 256 || nx % 2 || ny % 2) return false;
+        if (nz > 256 || nx % 2 || ny % 2) return false;
         if (c + 1 < h->lv.size() && (nx % 4 || nx < 4)) return false;
+        if (!uni) {
+            // variable levels: k_half_sweep_segv (16 warps) and, below the
+            // coarsest, the red-only restriction (the full one reads halos)
+            const int seg = nz / 16;
+            if (nz % 16 || !(seg == 1 || seg == 2 || seg == 4 || seg == 8 || seg == 16) ||
+                getenv("PMG_VAR_EXACT"))
+                return false;
+            if (c + 1 < h->lv.size() && !h->d.red_restrict) return false;
+        }
     }
     return true;
 }
@@ -308,6 +317,12 @@ bool lagged_ok(const pmg_hier *h) {
     if (pmg_level_dims(h->lv[0], &nx, &ny, &nz)) return false;
     // nx % 4: the fine residual-restriction is the column-quad kernel, the
     // one that reads f through Lvl::fcs
+    // a variable fine level restricts with the red-only kernel (the general
+    // variable restriction does not read Lvl::fcs)
+    long long plane, cs;
+    int pitch, par, uni;
+    if (pmg_level_layout(h->lv[0], &pitch, &plane, &cs, &par, &uni)) return false;
+    if (!uni && !(h->d.red_restrict && pmg_residual_restrict_red_ok(h->lv[0]))) return false;
     return h->d.lagged_norm && h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->d.nu_post >= 1 &&
            h->lv.size() > 1 && nx % 4 == 0 && !getenv("PMG_RR_NOQ") &&
            pmg_half_sweep_res_ok(h->lv[0]);
@@ -397,6 +412,10 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     int pitch, parity, uniform;
     TRY(pmg_level_layout(l0, &pitch, &plane, &cs, &parity, &uniform));
     if (!h->red1) TRYC(cudaMalloc(&h->red1, sizeof(double) * cs), "red array");
+    // variable levels compute their pivot field before any view of them is
+    // taken (a view shares the field; preparing through a view would index
+    // it with the view's colour stride) and outside any graph capture
+    for (auto *l : h->lv) TRY(pmg_level_prepare(const_cast<pmg_level *>(l), st));
     if (h->wv.empty()) {
         // wrap views of every level when all of them qualify
         const int wrap = wrap_ok(h) ? pmg::HF_WRAP : 0;

@@ -659,7 +659,7 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
 // centre / outer / S / N neighbours and f at red cells only: 14 N
 // algorithmic bytes instead of 18 N.  PAR = the level's parity (red at
 // even i in the even fine rows when 0).
-template <int PAR, int MINB = 2>
+template <int PAR, int MINB = 2, bool UNI = true>
 __global__ void __launch_bounds__(128, MINB)
 k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
                         double *__restrict__ cf, int mb32, int ntiles, int kcs) {
@@ -700,6 +700,12 @@ k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double
         const double *fa = f + ra, *fb = f + rb;   // colour 0: no fcs offset
         const int cc0 = (2 * m + J + C.par) & 1;
         const long long q0 = at(C, cc0, 0, J, m), q1 = at(C, cc0 ^ 1, 0, J, m);
+        // per-column coefficients of the four red cells (variable levels)
+        const int ia = 4 * m + PAR, ib = 4 * m + 1 - PAR;
+        const Col2 Wa0 = UNI ? W : col2_coeffs<UNI>(F, ia, ja);
+        const Col2 Wa2 = UNI ? W : col2_coeffs<UNI>(F, ia + 2, ja);
+        const Col2 Wb0 = UNI ? W : col2_coeffs<UNI>(F, ib, jb);
+        const Col2 Wb2 = UNI ? W : col2_coeffs<UNI>(F, ib + 2, jb);
         D2 ca[3], cb[3];   // red pairs of rows ja / jb: [0] k-1, [1] k, [2] k+1
         {
             const long long km = (long long)max(kbeg - 1, 0) * pl, k0 = (long long)kbeg * pl;
@@ -718,27 +724,27 @@ k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double
             if (PAR == 0) {
                 // row ja red at 4m (ca.x), 4m+2 (ca.y); black at 4m+1 (va.x), 4m+3 (va.y)
                 // row jb red at 4m+1 (cb.x), 4m+3 (cb.y); black at 4m (vb.x), 4m+2 (vb.y)
-                const double r0 = cell_res<1, 1, true>(F, T, W, k, xao, va.x, vs.x, vb.x,
-                                                       ca[0].x, ca[1].x, ca[2].x, ffa.x);
-                const double r2 = cell_res<1, 1, true>(F, T, W, k, va.x, va.y, vs.y, vb.y,
-                                                       ca[0].y, ca[1].y, ca[2].y, ffa.y);
-                const double r1 = cell_res<1, 1, true>(F, T, W, k, vb.x, vb.y, va.x, vn.x,
-                                                       cb[0].x, cb[1].x, cb[2].x, ffb.x);
-                const double r3 = cell_res<1, 1, true>(F, T, W, k, vb.y, xbo, va.y, vn.y,
-                                                       cb[0].y, cb[1].y, cb[2].y, ffb.y);
+                const double r0 = cell_res<1, 1, UNI>(F, T, Wa0, k, xao, va.x, vs.x, vb.x,
+                                                      ca[0].x, ca[1].x, ca[2].x, ffa.x);
+                const double r2 = cell_res<1, 1, UNI>(F, T, Wa2, k, va.x, va.y, vs.y, vb.y,
+                                                      ca[0].y, ca[1].y, ca[2].y, ffa.y);
+                const double r1 = cell_res<1, 1, UNI>(F, T, Wb0, k, vb.x, vb.y, va.x, vn.x,
+                                                      cb[0].x, cb[1].x, cb[2].x, ffb.x);
+                const double r3 = cell_res<1, 1, UNI>(F, T, Wb2, k, vb.y, xbo, va.y, vn.y,
+                                                      cb[0].y, cb[1].y, cb[2].y, ffb.y);
                 a = r0 + r1;        // ((r(4m,ja) + 0) + 0) + r(4m+1,jb)
                 b = r2 + r3;
             } else {
                 // row ja red at 4m+1 (ca.x), 4m+3 (ca.y); black at 4m (va.x), 4m+2 (va.y)
                 // row jb red at 4m (cb.x), 4m+2 (cb.y); black at 4m+1 (vb.x), 4m+3 (vb.y)
-                const double r1 = cell_res<1, 1, true>(F, T, W, k, va.x, va.y, vs.x, vb.x,
-                                                       ca[0].x, ca[1].x, ca[2].x, ffa.x);
-                const double r3 = cell_res<1, 1, true>(F, T, W, k, va.y, xao, vs.y, vb.y,
-                                                       ca[0].y, ca[1].y, ca[2].y, ffa.y);
-                const double r0 = cell_res<1, 1, true>(F, T, W, k, xbo, vb.x, va.x, vn.x,
-                                                       cb[0].x, cb[1].x, cb[2].x, ffb.x);
-                const double r2 = cell_res<1, 1, true>(F, T, W, k, vb.x, vb.y, va.y, vn.y,
-                                                       cb[0].y, cb[1].y, cb[2].y, ffb.y);
+                const double r1 = cell_res<1, 1, UNI>(F, T, Wa0, k, va.x, va.y, vs.x, vb.x,
+                                                      ca[0].x, ca[1].x, ca[2].x, ffa.x);
+                const double r3 = cell_res<1, 1, UNI>(F, T, Wa2, k, va.y, xao, vs.y, vb.y,
+                                                      ca[0].y, ca[1].y, ca[2].y, ffa.y);
+                const double r0 = cell_res<1, 1, UNI>(F, T, Wb0, k, xbo, vb.x, va.x, vn.x,
+                                                      cb[0].x, cb[1].x, cb[2].x, ffb.x);
+                const double r2 = cell_res<1, 1, UNI>(F, T, Wb2, k, vb.x, vb.y, va.y, vn.y,
+                                                      cb[0].y, cb[1].y, cb[2].y, ffb.y);
                 a = r1 + r0;        // ((0 + r(4m+1,ja)) + r(4m,jb)) + 0
                 b = r3 + r2;
             }
@@ -1713,11 +1719,17 @@ k_half_sweep_cp(Lvl L, double *__restrict__ u, const double *__restrict__ f, int
 // the RHS batch; the segment products (pf, q) are formed on the fly and
 // published with the boundary values.  nz must be a multiple of SEG.
 // ---------------------------------------------------------------------------
-template <int SEG, int NBZ>
+// RES = 1: as k_half_sweep_seg's RES mode (u read only, relaxed values into
+// uw, dotp[blockIdx.x] = sum over the colour's cells of (f - A u)^2 of the
+// incoming iterate); the line RHS g here is the reference's own
+// (smoother.py:137-145), so r_k = g_k - (d_k u_k - bm_k u_{k-1} - bp_k
+// u_{k+1}) with d_k of stencil.py:105-109 from the column's coefficients.
+// RES = 3: in-place sweep that also sums f^2 over the colour (first cycle).
+template <int SEG, int NBZ, int RES = 0>
 __global__ void __launch_bounds__(512, 1)
 k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                   int zero_start, int post_scale_unused, double post_scale, int ntiles,
-                  int htiles) {
+                  int htiles, double *__restrict__ dotp, double *__restrict__ uw) {
     extern __shared__ double vsm[];
     const int nz = L.nz;
     double *tdrw = vsm;                  // [nz]
@@ -1726,12 +1738,22 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
     double *xp = xh + 16 * 32;           // [16][32] segment product of alpha
     double *xy = xp + 16 * 32;           // [16][32] segment start y
     double *xq = xy + 16 * 32;           // [16][32] segment product of mu
+    double *tvol = xq + 16 * 32;         // RES: [nz] volprof
+    double *tdr = tvol + nz;             // RES: [nz] dr
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
         if (t < nz) tdrw[t] = L.drw[t];
         tvp[t] = L.vprof[t];
+        if (RES == 1 && t < nz) {
+            tvol[t] = L.volprof[t];
+            tdr[t] = L.dr[t];
+        }
     }
     __syncthreads();
+    double dacc = 0.0;
+    // the pivot field keeps the level's own colour stride (a lagged-norm
+    // view moves only the iterate's red array: Lvl::fcs)
+    const double *invdc = L.invd + (long long)c * (L.fcs - L.cstride);
     const int o = c ^ 1;
     const long long pl = L.plane;
     const int k0 = w * SEG;
@@ -1747,26 +1769,36 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
         const int h = h0 + ln;
         const int i = 2 * h + s0;
         const long long pc = at(L, c, k0, j, h);
-        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
-        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
-        const long long pS = at(L, o, k0, j - 1, h);
-        const long long pN = at(L, o, k0, j + 1, h);
+        const long long pW = at(L, o, k0, j, wrapx(L, i - 1) >> 1);
+        const long long pE = at(L, o, k0, j, wrapx(L, i + 1) >> 1);
+        const long long pS = at(L, o, k0, wrapy(L, j - 1), h);
+        const long long pN = at(L, o, k0, wrapy(L, j + 1), h);
         const long long q2 = (long long)j * L.nx + i;
         const double wxm = L.wx[(long long)j * (L.nx + 1) + i];
         const double wxp = L.wx[(long long)j * (L.nx + 1) + i + 1];
         const double wym = L.wy[q2];
         const double wyp = L.wy[(long long)(j + 1) * L.nx + i];
         const double cv = L.vcoef * L.av[q2];
+        // RES: the column's diagonal coefficients (stencil.py:105-109) and
+        // the incoming values next to this warp's levels
+        double vh = 0.0, osw = 0.0, um = 0.0, un = 0.0, rpend = 0.0, bpend = 0.0;
+        if (RES == 1) {
+            vh = L.vh[q2];
+            osw = L.omega2 * L.sumw[q2];
+            um = u[pc - ((k0 > 0) ? pl : 0)];
+            un = u[pc + ((k0 + SEG < nz) ? SEG : SEG - 1) * pl];
+        }
         double r[SEG], vi[SEG], pq[SEG];
-        constexpr int B = SEG < 4 ? SEG : 4;
+        constexpr int B = SEG < 4 ? SEG : (RES == 1 ? 2 : 4);
 #pragma unroll
         for (int b8 = 0; b8 < SEG; b8 += B) {
-            double vf[B], vw[B], vs[B], vn[B], vx[B], vv[B];
+            double vf[B], vw[B], vs[B], vn[B], vx[B], vv[B], vo[B];
 #pragma unroll
             for (int e = 0; e < B; ++e) {
                 const long long ko = (long long)(b8 + e) * pl;
                 vf[e] = f[pc + ko];
-                vv[e] = L.invd[pc + ko];
+                vv[e] = invdc[pc + ko];
+                if (RES == 1) vo[e] = u[pc + ko];
                 if (!NBZ) {
                     vw[e] = u[pW + ko];
                     vs[e] = u[pS + ko];
@@ -1791,7 +1823,28 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
                 }
                 r[b8 + e] = g;
                 vi[b8 + e] = vv[e];
+                if (RES == 3 && lane < nact) dacc = __fma_rn(vf[e], vf[e], dacc);
+                if (RES == 1) {
+                    const int k = k0 + b8 + e;
+                    const double bm = (k >= 1) ? cv * tvp[k] : 0.0;
+                    const double bp = (k + 1 < nz) ? cv * tvp[k + 1] : 0.0;
+                    if (b8 + e > 0) {
+                        const double q = __fma_rn(bpend, vo[e], rpend);
+                        if (lane < nact) dacc = __fma_rn(q, q, dacc);
+                    }
+                    double d = vh * tvol[k];
+                    d = d + osw * tdr[k];
+                    d = d + cv * (tvp[k] + tvp[k + 1]);
+                    const double tu = __fma_rn(-bm, um, d * vo[e]);   // d u_k - bm u_{k-1}
+                    rpend = g - tu;
+                    bpend = bp;
+                    um = vo[e];
+                }
             }
+        }
+        if (RES == 1) {
+            const double q = __fma_rn(bpend, un, rpend);
+            if (lane < nact) dacc = __fma_rn(q, q, dacc);
         }
         // local forward h_k = iota_k r_k + alpha_k h_{k-1}, alpha_k = (cv vp_k) iota_k
         double hp = 0.0, pf = 1.0;
@@ -1837,10 +1890,15 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
                     y = y * rho;
                     y = y + omr * u[q];
                 }
-                u[q] = y;
+                if (RES == 1) uw[q] = y;
+                else u[q] = y;
             }
         }
         __syncthreads();
+    }
+    if (RES) {
+        const double s2 = block_sum(dacc);
+        if (threadIdx.x == 0) dotp[blockIdx.x] = s2;
     }
 }
 
@@ -2598,7 +2656,7 @@ cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u
 // red-only residual + restriction (k_residual_restrict_red): fast mode,
 // uniform coefficients, fine nx a multiple of 4
 bool residual_restrict_red_ok(const Lvl &F) {
-    return !g_smoother_exact && F.uniform && F.nz <= 256 && F.nx % 4 == 0;
+    return !g_smoother_exact && F.nz <= 256 && F.nx % 4 == 0;
 }
 
 cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const double *u,
@@ -2617,8 +2675,13 @@ cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const doubl
         if (grid > capw / 4) grid = capw / 4;
         kern<<<grid, 128, 0, st>>>(F, C, u, f, cf, mb32, ntiles, kcs);
     };
-    if (F.par & 1) runq(k_residual_restrict_red<1>);
-    else runq(k_residual_restrict_red<0>);
+    if (F.uniform) {
+        if (F.par & 1) runq(k_residual_restrict_red<1>);
+        else runq(k_residual_restrict_red<0>);
+    } else {
+        if (F.par & 1) runq(k_residual_restrict_red<1, 2, false>);
+        else runq(k_residual_restrict_red<0, 2, false>);
+    }
     return cudaGetLastError();
 }
 
@@ -2696,15 +2759,66 @@ cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int 
     return cudaGetLastError();
 }
 
+// variable-coefficient levels the fast smoother handles with
+// k_half_sweep_segv (16 warps, SEG = nz / 16)
+static int segv_seg(const Lvl &L) {
+    if (g_smoother_exact || L.uniform || L.nz > 256 || L.nz % 16 || getenv("PMG_VAR_EXACT"))
+        return 0;
+    const int seg = L.nz / 16;
+    return (seg == 1 || seg == 2 || seg == 4 || seg == 8 || seg == 16) ? seg : 0;
+}
+
+// k_half_sweep_segv in mode RES (1: fused residual into uw, 3: f^2) with
+// per-CTA partial sums; grid as launch_half_sweep_k's variable branch
+template <int RES>
+static void launch_segv_mode(const Lvl &L, double *u, double *uw, const double *f, int color,
+                             int nbr_zero, double *partials, int *np, cudaStream_t st) {
+    const int hx = ((L.nx + 1) / 2 + 31) / 32;
+    const int seg = segv_seg(L);
+    const int nw = L.nz / seg;
+    const size_t sm =
+        sizeof(double) * (L.nz + ((L.nz + 2) & ~1) + 4 * 16 * 32 + (RES == 1 ? 2 * L.nz : 0));
+    const int ntiles = hx * L.ny;
+    auto runv = [&](auto kern) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
+        const int cap = sm_count() * (occ > 0 ? occ : 1);
+        const int grid = ntiles < cap ? ntiles : cap;
+        *np = grid;
+        kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, 1.0, 0, 0, 1.0, ntiles, hx, partials,
+                                        uw);
+    };
+#define PMG_SEGVM(S)                                                               \
+    do {                                                                           \
+        if (RES != 1 && nbr_zero) runv(k_half_sweep_segv<S, 1, RES>);              \
+        else runv(k_half_sweep_segv<S, 0, RES>);                                   \
+    } while (0)
+    switch (seg) {
+    case 1: PMG_SEGVM(1); break;
+    case 2: PMG_SEGVM(2); break;
+    case 4: PMG_SEGVM(4); break;
+    case 8: PMG_SEGVM(8); break;
+    default: PMG_SEGVM(16); break;
+    }
+#undef PMG_SEGVM
+}
+
 // red half-sweep (rho = 1) with the lagged convergence residual: reads the
 // iterate u, writes the relaxed red values into uw's red array and the
 // per-CTA sums of (f - A u)^2 over u's red cells into partials[0 .. *np).
-// Uniform levels in fast mode whose 16-level segments tile nz, no fused halo.
-bool half_sweep_res_ok(const Lvl &L) { return half_sweep_dot_ok(L); }
+// Fast mode, no fused halo: uniform levels whose 16-level segments tile nz
+// (k_half_sweep_seg) or variable levels of k_half_sweep_segv.
+bool half_sweep_res_ok(const Lvl &L) {
+    return half_sweep_dot_ok(L) || (segv_seg(L) && !(L.hflags & 1));
+}
 
 cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
                                   double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!L.uniform) {
+        launch_segv_mode<1>(L, const_cast<double *>(u), uw, f, 0, 0, partials, np, st);
+        return cudaGetLastError();
+    }
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
     const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
@@ -2734,6 +2848,10 @@ cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int 
                                   int nbr_zero, double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     f += (long long)color * (L.fcs - L.cstride);   // see launch_half_sweep
+    if (!L.uniform) {
+        launch_segv_mode<3>(L, u, nullptr, f, color, nbr_zero, partials, np, st);
+        return cudaGetLastError();
+    }
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
     const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
@@ -2919,7 +3037,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
                 const int cap = sm_count() * (occ > 0 ? occ : 1);
                 const int grid = ntiles < cap ? ntiles : cap;
                 kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, 0, post_scale,
-                                                ntiles, hx);
+                                                ntiles, hx, nullptr, nullptr);
             };
 #define PMG_SEGV(S) do { if (nbr_zero) runv(k_half_sweep_segv<S, 1>); else runv(k_half_sweep_segv<S, 0>); } while (0)
             switch (seg) {

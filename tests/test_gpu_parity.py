@@ -809,19 +809,26 @@ def _red_mask(nx, ny, nz):
     return np.broadcast_to((((i + j) % 2) == 0)[:, :, None], (nx, ny, nz))
 
 
-@pytest.mark.parametrize("nx,nz", [(32, 128), (128, 80), (64, 96)])
-def test_half_sweep_res(pmg, nx, nz):
+@pytest.mark.parametrize("nx,nz,variable", [(32, 128, False), (128, 80, False), (64, 96, False),
+                                            (64, 128, True), (32, 64, True)])
+def test_half_sweep_res(pmg, nx, nz, variable):
     """pmg_half_sweep_res: the relaxed red values equal pmg_half_sweep's bit
     for bit (written into the other buffer, the input untouched), and the
     fused sum equals ||f - A u||^2 over the red cells of the input."""
     import ctypes as C
     from paper_1307_2036_b200 import _lib
     lib = _lib.load()
+    from paper_1307_2036_b200 import configs
     ny = nx
-    grid = pmg.periodic_box(nx, nz, 0.01)
-    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    if variable:      # configs[4]'s graded levels and omega^2(x, y)
+        prob = configs.Problem(nx, nx, nz, 1e-3, 1.0, 1, stretch=1.05, variable_omega=True)
+        grid, params = prob.grid(), prob.params()
+    else:
+        grid = pmg.periodic_box(nx, nz, 0.01)
+        params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
     cfg = pmg.MGConfig(policy="explicit", explicit_levels=1)
     hier = pmg.build_hierarchy(grid, params, cfg)
+    assert hier.fine.op.uniform == (not variable)
     lay = hier.fine.layout
     w = lay.local_workers[0]
     h = hier.fine.op.handles[w].h
@@ -846,9 +853,9 @@ def test_half_sweep_res(pmg, nx, nz):
     got = pmg.gather_owned(un)
     assert np.array_equal(got[red], pmg.gather_owned(ref)[red])
     assert not np.any(got[~red])                             # black array untouched
-    # ineligible levels are refused: nz = 32 (4-level segments), Neumann
-    # faces (2-D coefficients)
-    for g2 in (pmg.periodic_box(16, 32, 0.01), pmg.panel_grid(16, 128, flat_mode=True)):
+    # ineligible levels are refused: uniform with nz = 32 (4-level
+    # segments), variable with nz = 8 (not a multiple of 16)
+    for g2 in (pmg.periodic_box(16, 32, 0.01), pmg.panel_grid(16, 8, flat_mode=True)):
         h2 = pmg.build_hierarchy(g2, pmg.toy_parameters(16, g2.nz, 1e-3, 1.0),
                                  pmg.MGConfig(policy="explicit", explicit_levels=1))
         w2 = h2.fine.layout.local_workers[0]
@@ -861,7 +868,7 @@ def test_half_sweep_res(pmg, nx, nz):
                       C.c_void_p(nrm.data_ptr()), None)
 
 
-@pytest.mark.parametrize("case", ["box256", "box96", "box80", "box128"])
+@pytest.mark.parametrize("case", ["box256", "box96", "box80", "box128", "var128", "var256"])
 def test_lagged_norm_solve(pmg, case):
     """Native mg_solve with the lagged convergence norm against the plain
     one: equal iteration counts and iterates BIT FOR BIT (same kernels, the
@@ -869,11 +876,16 @@ def test_lagged_norm_solve(pmg, case):
     1e-10 (the black cells' residual after an exact black line solve is
     rounding noise).  Odd and even cycle counts, repeated solves (the
     red-array parity follows the previous count) and maxiter cut-offs."""
-    from paper_1307_2036_b200 import _lib
+    from paper_1307_2036_b200 import _lib, configs
     nx, nz, nlev = {"box256": (256, 128, 5), "box96": (64, 96, 3), "box80": (32, 80, 2),
-                    "box128": (128, 128, 3)}[case]
-    grid = pmg.periodic_box(nx, nz, 0.01)
-    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+                    "box128": (128, 128, 3), "var128": (128, 128, 3),
+                    "var256": (256, 128, 5)}[case]
+    if case.startswith("var"):    # configs[4]-like: graded levels, omega^2(x, y)
+        prob = configs.Problem(nx, nx, nz, 1e-3, 1.0, nlev, stretch=1.05, variable_omega=True)
+        grid, params = prob.grid(), prob.params()
+    else:
+        grid = pmg.periodic_box(nx, nz, 0.01)
+        params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
     fa = uni((nx, nx, nz), 9)
     for eps in (1e-5, 1e-7, 1e-9):
         runs = {}
