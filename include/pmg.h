@@ -139,6 +139,11 @@ int pmg_residual_restrict_red(const pmg_level *fine, const pmg_level *coarse,
                               const double *f, const double *u, double *coarse_f,
                               void *stream);
 int pmg_residual_restrict_red_ok(const pmg_level *fine);
+/* norm2_dev[0] = sum over the RED owned cells of (f - A u)^2 (the
+ * convergence norm after an exact black half-sweep, rho = 1, whose black
+ * residual is zero); same eligibility as pmg_residual_restrict_red. */
+int pmg_red_residual_norm(const pmg_level *lvl, const double *f, const double *u,
+                          double *scratch, double *norm2_dev, void *stream);
 
 /* ---- line smoother: LineSmoother.half_sweep (smoother.py:122-182) ---- */
 /* mode 0 (default): fast k-segmented column solve (uniform levels; agrees

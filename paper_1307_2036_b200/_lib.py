@@ -82,6 +82,7 @@ SIGNATURES = {
     "pmg_residual_restrict": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_residual_restrict_red": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_residual_restrict_red_ok": (_I, [_P]),
+    "pmg_red_residual_norm": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_half_sweep": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _P]),
     "pmg_half_sweep_res": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "pmg_half_sweep_res_ok": (_I, [_P]),

@@ -34,7 +34,8 @@ bool residual_restrict_red_ok(const Lvl &F);
 cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int color,
                                   int nbr_zero, double *partials, int *np, cudaStream_t st);
 cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const double *u,
-                                         const double *f, double *cf, cudaStream_t st);
+                                         const double *f, double *cf, cudaStream_t st,
+                                         double *partials = nullptr, int *np = nullptr);
 cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
                                   double *partials, int *np, cudaStream_t st);
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
@@ -422,6 +423,24 @@ int pmg_residual_restrict_red(const pmg_level *fine, const pmg_level *coarse, co
                                    "and nx a multiple of 4");
     PMG_CUDA(launch_residual_restrict_red(fine->L, coarse->L, u, f, cf, (cudaStream_t)st),
              "residual_restrict_red");
+    return PMG_OK;
+}
+
+int pmg_red_residual_norm(const pmg_level *lv, const double *f, const double *u,
+                          double *scratch, double *norm2, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (!scratch || !norm2) return fail(PMG_ERR_VALUE, "norm needs scratch and output");
+    if (!residual_restrict_red_ok(lv->L) || lv->L.nx < 4)
+        return fail(PMG_ERR_VALUE, "red residual norm needs fast mode and nx a multiple of 4");
+    // the column-quad grid of the red restriction: nx / 2 x ny / 2
+    Lvl Cq = lv->L;
+    Cq.nx = lv->L.nx / 2;
+    Cq.ny = lv->L.ny / 2;
+    int np = 0;
+    PMG_CUDA(launch_residual_restrict_red(lv->L, Cq, u, f, nullptr, (cudaStream_t)st, scratch,
+                                          &np),
+             "red_residual_norm");
+    PMG_CUDA(launch_finalize(scratch, np, norm2, (cudaStream_t)st), "red residual norm");
     return PMG_OK;
 }
 

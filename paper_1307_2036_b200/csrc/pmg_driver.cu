@@ -233,17 +233,34 @@ struct Lag {
     double *base[2];
 };
 
+// kinds 6 + X (predicted last cycle): as 4 + X but ending with the
+// check-only red residual norm of the result (pmg_red_residual_norm: reads
+// f_r, u_r, u_b; writes nothing).  Kinds 8 + X: a full cycle on X from an
+// ordinary red half-sweep (after a check that did not converge), ending
+// with the fused next red half-sweep.
 int lagged_body(pmg_hier *h, const double *f, int kind, const Lag &g, cudaStream_t st) {
     const int x = kind & 1;
+    const bool first = kind < 4;
     Fine fv;
     fv.view = g.view[x];
-    fv.red_done = kind >= 4;
-    if (kind < 4) {   // first cycle: ||f||^2 into res_d[1]
+    fv.red_done = (kind >= 4 && kind < 8);
+    if (first) {   // first cycle: ||f||^2 into res_d[1]
         fv.fsq_part = h->scratch + pmg_partials_size() / 2;
         fv.fsq_out = h->res_d + 1;
     }
-    TRY(vcycle(h, 0, g.base[x], f, kind < 4, st, fv));
+    TRY(vcycle(h, 0, g.base[x], f, first, st, fv));
+    if (kind == 6 || kind == 7)
+        return pmg_red_residual_norm(g.view[x], f, g.base[x], h->scratch, h->res_d, st);
     return pmg_half_sweep_res(g.view[x], g.base[x], g.base[x ^ 1], f, h->scratch, h->res_d, st);
+}
+
+// the next cycle ends with the check-only norm when the last contraction
+// predicts convergence with a factor-2 margin (PMG_NO_PREDICT: never)
+bool predict_last(double rn, double prev, double r0, double eps) {
+    static int off = -1;
+    if (off < 0) off = getenv("PMG_NO_PREDICT") ? 1 : 0;
+    if (off || !(prev > 0.0)) return false;
+    return rn * (rn / prev) < 0.5 * eps * r0;
 }
 
 template <class Body>
@@ -444,7 +461,8 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     int kind = 2 + x;
     *iters = 0;
     *converged = 0;
-    double r0 = 0.0;
+    double r0 = 0.0, prev = 0.0;
+    bool predict = pmg_residual_restrict_red_ok(l0) != 0;
     for (int it = 0; it < maxiter; ++it) {
         TRY(replay_kind(h, u, f, kind, st, [&] { return lagged_body(h, f, kind, g, st); }));
         TRYC(cudaStreamSynchronize(st), "sync");
@@ -466,8 +484,16 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
             break;
         }
         if (it + 1 == maxiter) break;   // u_maxiter stays in red array x
-        x ^= 1;
-        kind = 4 + x;
+        if (kind == 6 || kind == 7) {
+            // predicted convergence missed: the next cycle starts with an
+            // ordinary red half-sweep on the same red array; no more guesses
+            kind = 8 + x;
+            predict = false;
+        } else {
+            x ^= 1;   // the fused sweep relaxed red into the other array
+            kind = (predict && predict_last(rn, prev, r0, eps)) ? 6 + x : 4 + x;
+        }
+        prev = rn;
     }
     h->last_iters = *iters;
     if (x == 1)   // the result's red array is red1: copy it into u

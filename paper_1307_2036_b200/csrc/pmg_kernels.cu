@@ -659,10 +659,15 @@ k_residual_restrict_q(Lvl F, Lvl C, const double *__restrict__ u, const double *
 // centre / outer / S / N neighbours and f at red cells only: 14 N
 // algorithmic bytes instead of 18 N.  PAR = the level's parity (red at
 // even i in the even fine rows when 0).
-template <int PAR, int MINB = 2, bool UNI = true>
+// NORM: instead of the restriction, partials[blockIdx.x] = this CTA's sum
+// of (f - A u)^2 over the red cells (the lagged driver's check-only
+// convergence norm; C then only describes the column-quad grid).
+template <int PAR, int MINB = 2, bool UNI = true, bool NORM = false>
 __global__ void __launch_bounds__(128, MINB)
 k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double *__restrict__ f,
-                        double *__restrict__ cf, int mb32, int ntiles, int kcs) {
+                        double *__restrict__ cf, int mb32, int ntiles, int kcs,
+                        double *__restrict__ partials) {
+    double acc2 = 0.0;
     __shared__ double s_drw[256], s_a[257], s_b[257], s_c[257];
     const Tabs T{s_drw, s_a, s_b, s_a, s_b, s_c};
     load_tabs(F, T);
@@ -734,6 +739,9 @@ k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double
                                                       cb[0].y, cb[1].y, cb[2].y, ffb.y);
                 a = r0 + r1;        // ((r(4m,ja) + 0) + 0) + r(4m+1,jb)
                 b = r2 + r3;
+                if (NORM && act) {
+                    acc2 += r0 * r0; acc2 += r1 * r1; acc2 += r2 * r2; acc2 += r3 * r3;
+                }
             } else {
                 // row ja red at 4m+1 (ca.x), 4m+3 (ca.y); black at 4m (va.x), 4m+2 (va.y)
                 // row jb red at 4m (cb.x), 4m+2 (cb.y); black at 4m+1 (vb.x), 4m+3 (vb.y)
@@ -747,8 +755,11 @@ k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double
                                                       cb[0].y, cb[1].y, cb[2].y, ffb.y);
                 a = r1 + r0;        // ((0 + r(4m+1,ja)) + r(4m,jb)) + 0
                 b = r3 + r2;
+                if (NORM && act) {
+                    acc2 += r1 * r1; acc2 += r0 * r0; acc2 += r3 * r3; acc2 += r2 * r2;
+                }
             }
-            if (act) {
+            if (!NORM && act) {
                 const long long cko = (long long)k * C.plane;
                 cf[q0 + cko] = a;
                 cf[q1 + cko] = b;
@@ -756,6 +767,10 @@ k_residual_restrict_red(Lvl F, Lvl C, const double *__restrict__ u, const double
             ca[0] = ca[1]; cb[0] = cb[1];
             ca[1] = ca[2]; cb[1] = cb[2];
         }
+    }
+    if (NORM) {
+        const double s2 = block_sum(acc2);
+        if (threadIdx.x == 0) partials[blockIdx.x] = s2;
     }
 }
 
@@ -2660,7 +2675,8 @@ bool residual_restrict_red_ok(const Lvl &F) {
 }
 
 cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const double *u,
-                                         const double *f, double *cf, cudaStream_t st) {
+                                         const double *f, double *cf, cudaStream_t st,
+                                         double *partials, int *np) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int mb32 = ((C.nx >> 1) + 31) / 32;
     auto runq = [&](auto kern) {
@@ -2673,14 +2689,26 @@ cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const doubl
         const int ntiles = mb32 * C.ny * ((F.nz + kcs - 1) / kcs);
         int grid = (ntiles + 3) / 4;
         if (grid > capw / 4) grid = capw / 4;
-        kern<<<grid, 128, 0, st>>>(F, C, u, f, cf, mb32, ntiles, kcs);
+        if (np) *np = grid;
+        kern<<<grid, 128, 0, st>>>(F, C, u, f, cf, mb32, ntiles, kcs, partials);
     };
+    const bool norm = partials != nullptr;
     if (F.uniform) {
-        if (F.par & 1) runq(k_residual_restrict_red<1>);
-        else runq(k_residual_restrict_red<0>);
+        if (norm) {
+            if (F.par & 1) runq(k_residual_restrict_red<1, 2, true, true>);
+            else runq(k_residual_restrict_red<0, 2, true, true>);
+        } else {
+            if (F.par & 1) runq(k_residual_restrict_red<1>);
+            else runq(k_residual_restrict_red<0>);
+        }
     } else {
-        if (F.par & 1) runq(k_residual_restrict_red<1, 2, false>);
-        else runq(k_residual_restrict_red<0, 2, false>);
+        if (norm) {
+            if (F.par & 1) runq(k_residual_restrict_red<1, 2, false, true>);
+            else runq(k_residual_restrict_red<0, 2, false, true>);
+        } else {
+            if (F.par & 1) runq(k_residual_restrict_red<1, 2, false>);
+            else runq(k_residual_restrict_red<0, 2, false>);
+        }
     }
     return cudaGetLastError();
 }

@@ -934,6 +934,71 @@ def test_lagged_norm_solve(pmg, case):
     assert not np.any(pmg.gather_owned(u))
 
 
+def test_red_residual_norm(pmg):
+    """pmg_red_residual_norm = the sum of squares of pmg_residual's (bit-exact)
+    residual over the red cells (the lagged driver's check-only norm)."""
+    import ctypes as C
+    from paper_1307_2036_b200 import _lib
+    lib = _lib.load()
+    nx, nz = 64, 128
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    hier = pmg.build_hierarchy(grid, pmg.toy_parameters(nx, nz, 1e-3, 1.0),
+                               pmg.MGConfig(policy="explicit", explicit_levels=1))
+    lay = hier.fine.layout
+    w = lay.local_workers[0]
+    u, f = field(pmg, uni((nx, nx, nz), 4), lay), field(pmg, uni((nx, nx, nz), 5), lay)
+    scratch = torch.empty(int(lib.pmg_partials_size()), dtype=torch.float64, device="cuda")
+    nrm = torch.zeros(1, dtype=torch.float64, device="cuda")
+    _lib.call("pmg_red_residual_norm", hier.fine.op.handles[w].h, f.parts[w].ptr,
+              u.parts[w].ptr, C.c_void_p(scratch.data_ptr()), C.c_void_p(nrm.data_ptr()),
+              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    r = pmg.gather_owned(hier.fine.op.residual(f, u))
+    want = float(np.sum(r[_red_mask(nx, nx, nz)] ** 2))
+    assert abs(nrm.item() - want) <= 1e-13 * want
+
+
+def test_predicted_check_matches(pmg, tmp_path):
+    """The lagged driver's predicted check-only last norm (default) against
+    PMG_NO_PREDICT=1, in a subprocess: same iterates bit for bit, same
+    cycle counts, histories within rounding."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_1307_2036_b200 as pmg\n"
+        "out = []\n"
+        "for nx, nz, nl in ((256, 128, 5), (128, 128, 3)):\n"
+        "    g = pmg.periodic_box(nx, nz, 0.01); p = pmg.toy_parameters(nx, nz, 1e-3, 1.0)\n"
+        "    fa = np.random.default_rng(7).uniform(-1, 1, (nx, nx, nz))\n"
+        "    for eps in (1e-5, 1e-8):\n"
+        "        cfg = pmg.MGConfig(policy='explicit', explicit_levels=nl, eps=eps)\n"
+        "        h = pmg.build_hierarchy(g, p, cfg)\n"
+        "        f = pmg.scatter_owned(fa, h.fine.layout)\n"
+        "        for _ in range(2):\n"
+        "            u, rep = pmg.mg_solve(f, h, cfg)\n"
+        "        np.save(%r + f'/u_{nx}_{eps}.npy', pmg.gather_owned(u))\n"
+        "        out.append(rep.residual_history)\n"
+        "print(json.dumps(out))\n") % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                        str(tmp_path))
+    res = {}
+    for tag, env in (("pred", {}), ("nopred", {"PMG_NO_PREDICT": "1"})):
+        d = tmp_path / tag
+        d.mkdir()
+        r = subprocess.run([sys.executable, "-c", code.replace(str(tmp_path), str(d))],
+                           capture_output=True, text=True, env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr[-2000:]
+        import json
+        res[tag] = (json.loads(r.stdout.strip().splitlines()[-1]), d)
+    (ha, da), (hb, db) = res["pred"], res["nopred"]
+    for a, b in zip(ha, hb):
+        a, b = np.array(a), np.array(b)
+        assert len(a) == len(b)
+        assert np.all(np.abs(a - b) <= 1e-10 * b + 1e-14 * b[0])
+    for fn in sorted(os.listdir(da)):
+        assert np.array_equal(np.load(da / fn), np.load(db / fn)), fn
+
+
 @pytest.mark.parametrize("par", [0, 1])
 @pytest.mark.parametrize("mx,my,nz", [(32, 16, 16), (64, 8, 128), (4, 4, 8)])
 def test_residual_restrict_red(pmg, par, mx, my, nz):
