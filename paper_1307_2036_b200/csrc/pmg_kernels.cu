@@ -1411,6 +1411,232 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     }
 }
 
+// ---------------------------------------------------------------------------
+// Row-marching TMA half-sweep (fast mode, uniform, nz = 128: 8 warps x 16
+// levels, the column solve of k_half_sweep_seg).  One persistent CTA per SM
+// walks units of (strip of 32 columns, band of rows).  Per row j it needs f
+// at row j and the other colour's rows j-1, j, j+1 (the W/E neighbours and
+// the S/N rows): each row of the other colour is streamed into shared
+// memory ONCE by a 3-D tensor-map box (34 columns x nz levels) and reused by
+// the three rows that read it -- the register kernel loads it three times
+// (L2 hits) and waits on every load batch.  Rings: 4 rows of the other
+// colour, 2 rows of f; the boxes for rows j+3 / j+2 are issued as soon as
+// step j's right-hand sides are assembled (after the first barrier of its
+// column solve), so the copies overlap the solves.  On a wrap view the
+// strip-edge neighbours (i = -1, nx) come from a 2-column box of the
+// periodic image.  Same arithmetic as k_half_sweep_seg: bit-identical.
+// ---------------------------------------------------------------------------
+constexpr int BAND_NZ = 128, BAND_W = 36;
+static size_t band_smem();
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bar_compute() {   // the 8 compute warps only
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+template <int PLC>
+__global__ void __launch_bounds__(288, 1)
+k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
+                  double post_scale, int nstrip, int nband, int band_rows,
+                  const __grid_constant__ CUtensorMap mF, const __grid_constant__ CUtensorMap mB,
+                  const __grid_constant__ CUtensorMap mE) {
+    constexpr int SEG = 16, NZ = BAND_NZ, B = 4;
+    extern __shared__ __align__(128) double bsm_raw[];
+    double *bsm = bsm_raw + (((128u - (smem_u32(bsm_raw) & 127u)) & 127u) >> 3);
+    // (TMA box starts must be 16-byte aligned: the other-colour box covers
+    // h0 - 2 .. h0 + 33, column 0 unused)
+    double *ring = bsm;                              // [4][NZ][36] other colour rows
+    double *fring = ring + 4 * NZ * BAND_W;          // [2][NZ][32] f rows
+    double *ering = fring + 2 * NZ * 32;             // [4][NZ][2]  wrapped edge columns
+    double2 *ti = reinterpret_cast<double2 *>(ering + 4 * NZ * 2);
+    double2 *tb = ti + NZ;
+    double *tq = reinterpret_cast<double *>(tb + NZ);
+    double *tdrw = tq + NZ;
+    double *hend = tdrw + NZ;                         // [8][32]
+    double *ybeg = hend + 8 * 32;                     // [8][32]
+    uint64_t *fullB = reinterpret_cast<uint64_t *>(ybeg + 8 * 32);   // [4]
+    uint64_t *fullF = fullB + 4;                                     // [2]
+    uint64_t *emptyB = fullF + 2;                                    // [4]
+    uint64_t *emptyF = emptyB + 4;                                   // [2]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t < NZ; t += blockDim.x) {
+        tdrw[t] = L.drw[t];
+        ti[t] = make_double2(L.invd1[t], L.segtab[t]);
+        tb[t] = make_double2(L.segtab[2 * NZ + t], L.segtab[NZ + t]);
+        tq[t] = L.segtab[3 * NZ + t];
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) {
+            mbar_init(fullB + q, 1);
+            mbar_init(emptyB + q, 8);
+        }
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(fullF + q, 1);
+            mbar_init(emptyF + q, 8);
+        }
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const bool wrap = (L.hflags & HF_WRAP) != 0;
+    const int hrow = L.nx / 2;                       // cells of one colour per row
+    const int nunits = nstrip * nband;
+    if (w == 8) {
+        // ---- producer warp: streams every row of this CTA's units in the
+        // consumers' order; a slot is refilled once all 8 compute warps have
+        // released its previous row (empty barriers) ----
+        if (lane != 0) return;
+        unsigned nb = 0, nf = 0;
+        for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+            const int strip = unit % nstrip, band = unit / nstrip;
+            const int h0 = strip * 32;
+            const int j0 = band * band_rows, j1 = min(L.ny, j0 + band_rows);
+            if (j0 >= j1) continue;
+            const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
+            const uint32_t bytesb = NZ * BAND_W * 8 + ((eleft || eright) ? NZ * 2 * 8 : 0);
+            // black rows j0 - 1 .. j1 and f rows j0 .. j1 - 1, interleaved as
+            // the consumers need them: black j0-1, j0, j0+1, f j0, then per
+            // step j: black j+2, f j+1
+            auto put_b = [&](int r) {
+                const int slot = nb & 3;
+                if (nb >= 4) mbar_wait(emptyB + slot, ((nb >> 2) + 1) & 1);
+                const int rr = wrap ? (r < 0 ? r + L.ny : (r >= L.ny ? r - L.ny : r)) : r;
+                fence_proxy_async();
+                mbar_expect_tx(fullB + slot, bytesb);
+                tma_box3(ring + slot * NZ * BAND_W, &mB, OFF + h0 - 2, 0, rr + 1, fullB + slot);
+                if (eleft)
+                    tma_box3(ering + slot * NZ * 2, &mE, OFF + hrow - 2, 0, rr + 1, fullB + slot);
+                else if (eright)
+                    tma_box3(ering + slot * NZ * 2, &mE, OFF, 0, rr + 1, fullB + slot);
+                ++nb;
+            };
+            auto put_f = [&](int r) {
+                const int slot = nf & 1;
+                if (nf >= 2) mbar_wait(emptyF + slot, ((nf >> 1) + 1) & 1);
+                fence_proxy_async();
+                mbar_expect_tx(fullF + slot, NZ * 32 * 8);
+                tma_box3(fring + slot * NZ * 32, &mF, OFF + h0, 0, r + 1, fullF + slot);
+                ++nf;
+            };
+            put_b(j0 - 1);
+            put_b(j0);
+            for (int j = j0; j < j1; ++j) {
+                put_b(j + 1);
+                put_f(j);
+            }
+        }
+        return;
+    }
+    // ---- 8 compute warps ----
+    const int o = c ^ 1;
+    (void)o;
+    constexpr long long pl = PLC;                    // plane stride (compile time)
+    const int k0 = w * SEG;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    unsigned seqb = 0, seqf = 0;                     // sequence of the unit's first rows
+    for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+        const int strip = unit % nstrip, band = unit / nstrip;
+        const int h0 = strip * 32;
+        const int j0 = band * band_rows, j1 = min(L.ny, j0 + band_rows);
+        if (j0 >= j1) continue;
+        const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
+        for (int j = j0; j < j1; ++j) {
+            // black row r of this unit = sequence seqb + r - (j0 - 1)
+            for (int r = (j == j0 ? j - 1 : j + 1); r <= j + 1; ++r) {
+                const unsigned q = seqb + (unsigned)(r - (j0 - 1));
+                mbar_wait(fullB + (q & 3), (q >> 2) & 1);
+            }
+            const unsigned qf = seqf + (unsigned)(j - j0);
+            mbar_wait(fullF + (qf & 1), (qf >> 1) & 1);
+            const unsigned qs = seqb + (unsigned)(j - 1 - (j0 - 1));
+            const double *Srow = ring + (qs & 3) * NZ * BAND_W;
+            const double *Crow = ring + ((qs + 1) & 3) * NZ * BAND_W;
+            const double *Nrow = ring + ((qs + 2) & 3) * NZ * BAND_W;
+            const double *Ce = ering + ((qs + 1) & 3) * NZ * 2;
+            const double *Frow = fring + (qf & 1) * NZ * 32;
+            const int s0 = (j + L.par + c) & 1;
+            // W / E box columns of this lane (box column 0 = h0 - 2)
+            const int iw = lane + 1 + s0, ie = lane + 2 + s0;
+            const bool wfix = eleft && s0 == 0 && lane == 0;     // W = h' = -1 -> hrow - 1
+            const bool efix = eright && s0 == 1 && lane == 31;   // E = h' = hrow -> 0
+            double r[SEG];
+#pragma unroll
+            for (int b8 = 0; b8 < SEG; b8 += B) {
+#pragma unroll
+                for (int e = 0; e < B; ++e) {
+                    const int k = k0 + b8 + e;
+                    const double *cr = Crow + k * BAND_W;
+                    double vw = cr[iw], ve = cr[ie];
+                    if (wfix) vw = Ce[k * 2 + 1];
+                    if (efix) ve = Ce[k * 2 + 0];
+                    const double vs = Srow[k * BAND_W + lane + 2];
+                    const double vn = Nrow[k * BAND_W + lane + 2];
+                    const double2 ia = ti[k];
+                    double g = ia.x * Frow[k * 32 + lane];
+                    // k_half_sweep_seg's tw table, formed on the fly
+                    const double dd = ia.x * tdrw[k];
+                    const double2 cw = make_double2(dd * L.wx0, dd * L.wy0);
+                    g = __fma_rn(cw.y, vs + vn, g);
+                    g = __fma_rn(cw.x, vw + ve, g);
+                    r[b8 + e] = g;
+                }
+            }
+            // this warp is done with the S row and f row j (and, at the
+            // unit's last row, with rows j and j + 1)
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(emptyB + (qs & 3));
+                mbar_arrive(emptyF + (qf & 1));
+                if (j == j1 - 1) {
+                    mbar_arrive(emptyB + ((qs + 1) & 3));
+                    mbar_arrive(emptyB + ((qs + 2) & 3));
+                }
+            }
+            // ---- column solve (seg_solve_store's sequence) ----
+            double hp = 0.0;
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                hp = __fma_rn(ti[k0 + e].y, hp, r[e]);
+                r[e] = hp;
+            }
+            hend[w * 32 + lane] = hp;
+            bar_compute();
+            double G = 0.0;
+            for (int sgm = 0; sgm < w; ++sgm)
+                G = __fma_rn(tb[(sgm + 1) * SEG - 1].x, G, hend[sgm * 32 + lane]);
+            double yp = 0.0;
+#pragma unroll
+            for (int e = SEG - 1; e >= 0; --e) {
+                const double2 pm = tb[k0 + e];
+                const double g = __fma_rn(pm.x, G, r[e]);
+                yp = __fma_rn(pm.y, yp, g);
+                r[e] = yp;
+            }
+            ybeg[w * 32 + lane] = yp;
+            bar_compute();
+            double X = 0.0;
+            for (int sgm = 7; sgm > w; --sgm) X = __fma_rn(tq[sgm * SEG], X, ybeg[sgm * 32 + lane]);
+            const long long pc = at(L, c, k0, j, h0 + lane);
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                double y = __fma_rn(tq[k0 + e], X, r[e]);
+                const long long q = pc + (long long)e * pl;
+                if (zero_start) {
+                    if (scale != 1.0) y = y * scale;
+                } else if (rho != 1.0) {
+                    y = y * rho;
+                    y = y + omr * u[q];
+                }
+                u[q] = y;
+            }
+        }
+        seqb += (unsigned)(j1 - j0 + 2);
+        seqf += (unsigned)(j1 - j0);
+    }
+}
+
 // Post-smoothing first half-sweep with the coarse-grid correction fused in
 // (fast mode, uniform, rho = 1).  The reference adds P e to the whole fine
 // iterate, exchanges halos and then relaxes colour c (multigrid.py:283-292,
@@ -2958,6 +3184,10 @@ void setup_kernel_attributes() {
     if (done) return;
     done = true;
     const int big = 227 * 1024;
+    cudaFuncSetAttribute(k_half_sweep_band<520>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<264>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_cp<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -3046,9 +3276,65 @@ static bool launch_half_sweep_tx(const Lvl &L, double *u, const double *f, int c
     return true;
 }
 
+// k_half_sweep_band: configs[1]'s fine level shape (nz = 128, plane 520),
+// neighbours read, no fused halo
+static size_t band_smem() {
+    return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 4 * BAND_NZ * 2 +
+                             6 * BAND_NZ + 2 * 8 * 32) + 12 * 8 + 128;
+}
+
+static bool band_on() {
+    static int v = -1;
+    if (v < 0) v = getenv("PMG_BAND") ? atoi(getenv("PMG_BAND")) : 1;
+    return v == 1;
+}
+
+static bool band_l1() {
+    static int v = -1;
+    if (v < 0) v = getenv("PMG_BAND_L1") ? atoi(getenv("PMG_BAND_L1")) : 0;
+    return v == 1;
+}
+
+static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
+                                   double rho, int zero_start, int nbr_zero, double post_scale,
+                                   cudaStream_t st) {
+    const int hrow = L.nx / 2;
+    if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
+        !(L.plane == 520 || (L.plane == 264 && band_l1())) ||
+        L.seg != 16 || nbr_zero || (L.hflags & 1) || L.nx % 2 || hrow % 32 || hrow < 64 ||
+        L.ny < 8)
+        return false;
+    const int o = color ^ 1;
+    CUtensorMap mF, mB, mE;
+    if (!make_tmap(&mF, f + (long long)color * L.cstride, L, 32, BAND_NZ) ||
+        !make_tmap(&mB, u + (long long)o * L.cstride, L, BAND_W, BAND_NZ) ||
+        !make_tmap(&mE, u + (long long)o * L.cstride, L, 2, BAND_NZ))
+        return false;
+    const int nstrip = hrow / 32;
+    int nband = (4 * sm_count() + nstrip - 1) / nstrip;
+    if (nband > L.ny) nband = L.ny;
+    const int band_rows = (L.ny + nband - 1) / nband;
+    nband = (L.ny + band_rows - 1) / band_rows;
+    const int nunits = nstrip * nband;
+    const int grid = nunits < sm_count() ? nunits : sm_count();
+    if (L.plane == 520)
+        k_half_sweep_band<520><<<grid, 288, band_smem(), st>>>(L, u, color, rho, zero_start,
+                                                               post_scale, nstrip, nband,
+                                                               band_rows, mF, mB, mE);
+    else
+        k_half_sweep_band<264><<<grid, 288, band_smem(), st>>>(L, u, color, rho, zero_start,
+                                                               post_scale, nstrip, nband,
+                                                               band_rows, mF, mB, mE);
+    return true;
+}
+
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
                                        double post_scale, cudaStream_t st, bool *fused) {
+    if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st)) {
+        *fused = false;
+        return cudaGetLastError();
+    }
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
     if (!g_smoother_exact && !L.uniform && L.nz <= 256 && getenv("PMG_VAR_EXACT") == nullptr) {
