@@ -209,13 +209,25 @@ def run_reference(args):
 
 
 def time_kernel(fn, reps, torch):
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    """Mean device time of one call of ``fn``: ``reps`` calls captured into a
+    CUDA graph (no host launch gaps between them) and replayed between two
+    CUDA events on the replaying stream."""
     fn()
     torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(reps):
+                fn()
+    torch.cuda.current_stream().wait_stream(side)
+    g.replay()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    for _ in range(reps):
-        fn()
+    g.replay()
     e1.record(st)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps * 1e-3
@@ -316,20 +328,31 @@ def main():
     kern = {}
     coarse = hier.levels[1]
     from paper_1307_2036_b200 import multigrid as mgmod
-    t_rr = time_kernel(lambda: mgmod._residual_restrict(fine, coarse, s0.f, s0.u,
-                                                        scratch[1].f), 10, torch)
-    t_pa = time_kernel(lambda: mgmod._prolong_add(scratch[1].u, coarse, fine, s0.u), 10, torch)
+    import ctypes as C
+    # the fine-level kernels of the solve: fused-residual red sweep, red-only
+    # residual restriction, black-only prolongation (DESIGN.md sections 3-4)
+    part = s0.u.parts[w]
+    hh = fine.op.handles[w].h
+    scr = torch.empty(int(lib.pmg_partials_size()), dtype=torch.float64, device="cuda")
     res = torch.zeros(1, dtype=torch.float64, device="cuda")
-    t_rn = time_kernel(lambda: fine.op.residual_norm2_dev(s0.f, s0.u, None, res), 10, torch)
-    for name, tt, b in (("half_sweep", t_hs, 12), ("residual_restrict", t_rr, 18),
-                        ("prolong_add", t_pa, 18), ("residual_norm", t_rn, 16)):
+    t_res = time_kernel(lambda: lib.pmg_half_sweep_res(
+        hh, part.ptr, s0.r.parts[w].ptr, s0.f.parts[w].ptr, C.c_void_p(scr.data_ptr()),
+        C.c_void_p(res.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+        10, torch)
+    t_rr = time_kernel(lambda: mgmod._residual_restrict(fine, coarse, s0.f, s0.u,
+                                                        scratch[1].f, True), 10, torch)
+    t_pa = time_kernel(lambda: mgmod._prolong_add(scratch[1].u, coarse, fine, s0.u,
+                                                  black_only=True), 10, torch)
+    for name, tt, b in (("half_sweep", t_hs, 12), ("half_sweep_res", t_res, 16),
+                        ("residual_restrict_red", t_rr, 14), ("prolong_black", t_pa, 10)):
         kern[name] = {"ms": tt * 1e3, "alg_bytes_per_cell": b,
                       "GB_s": b * n_fine / tt / 1e9}
     peak, peak_src = measured_peak()
     ach = 12 * n_fine / t_hs / 1e9
-    traffic = ncu_traffic("k_half_sweep_seg")
+    traffic = ncu_traffic("k_half_sweep_band")
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": traffic, "kernel": "k_half_sweep_seg (fine level, fast line solver)",
+                "frac": ach / peak, "traffic": traffic,
+                "kernel": "k_half_sweep_band (fine level, TMA-fed line relaxation)",
                 "alg_bytes_per_launch": 12 * n_fine, "launch_ms": t_hs * 1e3,
                 "peak_source": peak_src}
 

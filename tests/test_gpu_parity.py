@@ -1076,3 +1076,30 @@ def test_red_restrict_solve(pmg):
     # histories agree to 1e-10 relative above a 1e-14 ||r0|| floor
     assert np.all(np.abs(h1 - h0) <= 1e-10 * h0 + 1e-14 * h0[0])
     assert np.max(np.abs(u1 - u0)) <= 1e-10 * np.max(np.abs(u0))
+
+
+def test_band_half_sweep_matches_exact(pmg):
+    """The TMA band half-sweep (configs[1]'s fine level, halo-ring mode)
+    against the exact sequential-Thomas smoother (bit-identical to the
+    reference): within the fast mode's 1e-12 (tests/test_smoother.py:48)."""
+    from paper_1307_2036_b200 import configs
+    prob = configs.config(1)
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(),
+                               pmg.MGConfig(policy="explicit", explicit_levels=1))
+    lay = hier.fine.layout
+    f = pmg.scatter_owned(configs.rhs(prob.nx, prob.ny, prob.nz, 0), lay)
+    u0 = pmg.scatter_owned(uni((prob.nx, prob.ny, prob.nz), 11), lay)
+    pmg.halo_exchange(u0)
+    out = []
+    for exact in (False, True):
+        u = u0.copy()
+        if exact:
+            with pmg.exact_smoother():
+                hier.fine.smoother.half_sweep(u, f, 1)
+                hier.fine.smoother.half_sweep(u, f, 0)
+        else:
+            hier.fine.smoother.half_sweep(u, f, 1)
+            hier.fine.smoother.half_sweep(u, f, 0)
+        out.append(pmg.gather_owned(u))
+    fast, ex = out
+    assert np.max(np.abs(fast - ex)) <= 1e-12 * np.max(np.abs(ex))

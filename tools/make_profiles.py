@@ -54,7 +54,7 @@ if os.path.exists(p):
 # ---- full capture of fine-level kernels ----
 traffic = {}
 import glob
-CURRENT = ["k_half_sweep_seg", "hs_res", "k_residual_restrict_red", "k_prolong_w"]
+CURRENT = ["k_half_sweep_band", "hs_res", "k_residual_restrict_red", "k_prolong_w"]
 for p in [os.path.join(GO, f"prof_{k}.ncu-rep") for k in CURRENT]:
     if not os.path.exists(p):
         continue

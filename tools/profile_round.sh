@@ -14,7 +14,7 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
 echo "ncu launch rc=$?"
 # fine-level kernels: the first launches of each in a solve are the finest level
 python tools/kbench.py --levels 2 > gpurun_out/kb.log 2>&1
-for k in k_half_sweep_seg k_residual_restrict_red k_prolong_w; do
+for k in k_half_sweep_band k_residual_restrict_red k_prolong_w; do
   ncu --set full --clock-control none --import-source on -k regex:$k -c 1 \
       -o gpurun_out/prof_$k python tools/kbench.py --levels 2 > gpurun_out/ncu_$k.log 2>&1
   echo "ncu full $k rc=$?"
