@@ -1426,7 +1426,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // strip-edge neighbours (i = -1, nx) come from a 2-column box of the
 // periodic image.  Same arithmetic as k_half_sweep_seg: bit-identical.
 // ---------------------------------------------------------------------------
-constexpr int BAND_NZ = 128, BAND_W = 36;
+constexpr int BAND_NZ = 128, BAND_W = 32;
 static size_t band_smem();
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
@@ -1436,6 +1436,9 @@ __device__ __forceinline__ void bar_compute() {   // the 8 compute warps only
     asm volatile("bar.sync 1, 256;" ::: "memory");
 }
 
+// (A fused-residual mode -- the lagged norm's red sweep, with the incoming
+// red values loaded from HBM into registers at each step -- ran at 501 us
+// against 413 us for k_half_sweep_seg's: not kept.)
 template <int PLC>
 __global__ void __launch_bounds__(288, 1)
 k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
@@ -1445,12 +1448,14 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
     constexpr int SEG = 16, NZ = BAND_NZ, B = 4;
     extern __shared__ __align__(128) double bsm_raw[];
     double *bsm = bsm_raw + (((128u - (smem_u32(bsm_raw) & 127u)) & 127u) >> 3);
-    // (TMA box starts must be 16-byte aligned: the other-colour box covers
-    // h0 - 2 .. h0 + 33, column 0 unused)
-    double *ring = bsm;                              // [4][NZ][36] other colour rows
+    // (TMA box starts must be 16-byte aligned: the other colour's row is
+    // three boxes, columns h0 .. h0 + 31 and the 2-column edges h0 - 2,
+    // h0 - 1 and h0 + 32, h0 + 33 -- the periodic image's on a wrap view)
+    double *ring = bsm;                              // [4][NZ][32] other colour rows
     double *fring = ring + 4 * NZ * BAND_W;          // [2][NZ][32] f rows
-    double *ering = fring + 2 * NZ * 32;             // [4][NZ][2]  wrapped edge columns
-    double2 *ti = reinterpret_cast<double2 *>(ering + 4 * NZ * 2);
+    double *ewr = fring + 2 * NZ * 32;               // [4][NZ][2]  W edge columns
+    double *eer = ewr + 4 * NZ * 2;                  // [4][NZ][2]  E edge columns
+    double2 *ti = reinterpret_cast<double2 *>(eer + 4 * NZ * 2);
     double2 *tb = ti + NZ;
     double *tq = reinterpret_cast<double *>(tb + NZ);
     double *tdrw = tq + NZ;
@@ -1494,7 +1499,9 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             const int j0 = band * band_rows, j1 = min(L.ny, j0 + band_rows);
             if (j0 >= j1) continue;
             const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
-            const uint32_t bytesb = NZ * BAND_W * 8 + ((eleft || eright) ? NZ * 2 * 8 : 0);
+            const uint32_t bytesb = NZ * BAND_W * 8 + 2 * NZ * 2 * 8;
+            const int xw = eleft ? OFF + hrow - 2 : OFF + h0 - 2;
+            const int xe = eright ? OFF : OFF + h0 + 32;
             // black rows j0 - 1 .. j1 and f rows j0 .. j1 - 1, interleaved as
             // the consumers need them: black j0-1, j0, j0+1, f j0, then per
             // step j: black j+2, f j+1
@@ -1504,11 +1511,9 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                 const int rr = wrap ? (r < 0 ? r + L.ny : (r >= L.ny ? r - L.ny : r)) : r;
                 fence_proxy_async();
                 mbar_expect_tx(fullB + slot, bytesb);
-                tma_box3(ring + slot * NZ * BAND_W, &mB, OFF + h0 - 2, 0, rr + 1, fullB + slot);
-                if (eleft)
-                    tma_box3(ering + slot * NZ * 2, &mE, OFF + hrow - 2, 0, rr + 1, fullB + slot);
-                else if (eright)
-                    tma_box3(ering + slot * NZ * 2, &mE, OFF, 0, rr + 1, fullB + slot);
+                tma_box3(ring + slot * NZ * BAND_W, &mB, OFF + h0, 0, rr + 1, fullB + slot);
+                tma_box3(ewr + slot * NZ * 2, &mE, xw, 0, rr + 1, fullB + slot);
+                tma_box3(eer + slot * NZ * 2, &mE, xe, 0, rr + 1, fullB + slot);
                 ++nb;
             };
             auto put_f = [&](int r) {
@@ -1541,8 +1546,8 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
         const int h0 = strip * 32;
         const int j0 = band * band_rows, j1 = min(L.ny, j0 + band_rows);
         if (j0 >= j1) continue;
-        const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
         for (int j = j0; j < j1; ++j) {
+            const long long pc = at(L, c, k0, j, h0 + lane);
             // black row r of this unit = sequence seqb + r - (j0 - 1)
             for (int r = (j == j0 ? j - 1 : j + 1); r <= j + 1; ++r) {
                 const unsigned q = seqb + (unsigned)(r - (j0 - 1));
@@ -1554,13 +1559,15 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             const double *Srow = ring + (qs & 3) * NZ * BAND_W;
             const double *Crow = ring + ((qs + 1) & 3) * NZ * BAND_W;
             const double *Nrow = ring + ((qs + 2) & 3) * NZ * BAND_W;
-            const double *Ce = ering + ((qs + 1) & 3) * NZ * 2;
+            const double *Cw = ewr + ((qs + 1) & 3) * NZ * 2;
+            const double *Cx = eer + ((qs + 1) & 3) * NZ * 2;
             const double *Frow = fring + (qf & 1) * NZ * 32;
             const int s0 = (j + L.par + c) & 1;
-            // W / E box columns of this lane (box column 0 = h0 - 2)
-            const int iw = lane + 1 + s0, ie = lane + 2 + s0;
-            const bool wfix = eleft && s0 == 0 && lane == 0;     // W = h' = -1 -> hrow - 1
-            const bool efix = eright && s0 == 1 && lane == 31;   // E = h' = hrow -> 0
+            // W / E columns of this lane: h0 + lane - 1 + s0 and h0 + lane + s0
+            // (box column 0 = h0); lane 0's W (s0 = 0) and lane 31's E
+            // (s0 = 1) come from the edge boxes
+            const int iw = max(lane - 1 + s0, 0), ie = min(lane + s0, 31);
+            const bool wfix = s0 == 0 && lane == 0, efix = s0 == 1 && lane == 31;
             double r[SEG];
 #pragma unroll
             for (int b8 = 0; b8 < SEG; b8 += B) {
@@ -1569,10 +1576,10 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                     const int k = k0 + b8 + e;
                     const double *cr = Crow + k * BAND_W;
                     double vw = cr[iw], ve = cr[ie];
-                    if (wfix) vw = Ce[k * 2 + 1];
-                    if (efix) ve = Ce[k * 2 + 0];
-                    const double vs = Srow[k * BAND_W + lane + 2];
-                    const double vn = Nrow[k * BAND_W + lane + 2];
+                    if (wfix) vw = Cw[k * 2 + 1];
+                    if (efix) ve = Cx[k * 2 + 0];
+                    const double vs = Srow[k * BAND_W + lane];
+                    const double vn = Nrow[k * BAND_W + lane];
                     const double2 ia = ti[k];
                     double g = ia.x * Frow[k * 32 + lane];
                     // k_half_sweep_seg's tw table, formed on the fly
@@ -1618,7 +1625,6 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             bar_compute();
             double X = 0.0;
             for (int sgm = 7; sgm > w; --sgm) X = __fma_rn(tq[sgm * SEG], X, ybeg[sgm * 32 + lane]);
-            const long long pc = at(L, c, k0, j, h0 + lane);
 #pragma unroll
             for (int e = 0; e < SEG; ++e) {
                 double y = __fma_rn(tq[k0 + e], X, r[e]);
@@ -3279,7 +3285,7 @@ static bool launch_half_sweep_tx(const Lvl &L, double *u, const double *f, int c
 // k_half_sweep_band: configs[1]'s fine level shape (nz = 128, plane 520),
 // neighbours read, no fused halo
 static size_t band_smem() {
-    return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 4 * BAND_NZ * 2 +
+    return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 2 * 4 * BAND_NZ * 2 +
                              6 * BAND_NZ + 2 * 8 * 32) + 12 * 8 + 128;
 }
 
@@ -3318,13 +3324,11 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     const int nunits = nstrip * nband;
     const int grid = nunits < sm_count() ? nunits : sm_count();
     if (L.plane == 520)
-        k_half_sweep_band<520><<<grid, 288, band_smem(), st>>>(L, u, color, rho, zero_start,
-                                                               post_scale, nstrip, nband,
-                                                               band_rows, mF, mB, mE);
+        k_half_sweep_band<520><<<grid, 288, band_smem(), st>>>(
+            L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
     else
-        k_half_sweep_band<264><<<grid, 288, band_smem(), st>>>(L, u, color, rho, zero_start,
-                                                               post_scale, nstrip, nband,
-                                                               band_rows, mF, mB, mE);
+        k_half_sweep_band<264><<<grid, 288, band_smem(), st>>>(
+            L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
     return true;
 }
 
