@@ -3194,6 +3194,8 @@ void setup_kernel_attributes() {
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<264>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<136>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_cp<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -3295,9 +3297,9 @@ static bool band_on() {
     return v == 1;
 }
 
-static bool band_l1() {
+static bool band_l1() {   // level 2 (nx = 256) on the band kernel too
     static int v = -1;
-    if (v < 0) v = getenv("PMG_BAND_L1") ? atoi(getenv("PMG_BAND_L1")) : 0;
+    if (v < 0) v = getenv("PMG_BAND_L2") ? atoi(getenv("PMG_BAND_L2")) : 1;
     return v == 1;
 }
 
@@ -3306,7 +3308,7 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
                                    cudaStream_t st) {
     const int hrow = L.nx / 2;
     if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
-        !(L.plane == 520 || (L.plane == 264 && band_l1())) ||
+        !(L.plane == 520 || L.plane == 264 || (L.plane == 136 && band_l1())) ||
         L.seg != 16 || nbr_zero || (L.hflags & 1) || L.nx % 2 || hrow % 32 || hrow < 64 ||
         L.ny < 8)
         return false;
@@ -3317,7 +3319,13 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
         !make_tmap(&mE, u + (long long)o * L.cstride, L, 2, BAND_NZ))
         return false;
     const int nstrip = hrow / 32;
-    int nband = (4 * sm_count() + nstrip - 1) / nstrip;
+    // units per SM: a multiple of the SM count keeps the CTAs balanced;
+    // measured best 4 at 16 strips (nx = 1024: 269 us; 2 -> 373, 8 -> 278),
+    // 2 at 8 strips (nx = 512: 76.3 us; 4 -> 80.3), 1 below
+    static int ups_env = -1;
+    if (ups_env < 0) ups_env = getenv("PMG_BAND_UPS") ? atoi(getenv("PMG_BAND_UPS")) : 0;
+    const int ups = ups_env ? ups_env : (nstrip >= 16 ? 4 : (nstrip >= 8 ? 2 : 1));
+    int nband = (ups * sm_count() + nstrip - 1) / nstrip;
     if (nband > L.ny) nband = L.ny;
     const int band_rows = (L.ny + nband - 1) / nband;
     nband = (L.ny + band_rows - 1) / band_rows;
@@ -3326,8 +3334,11 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     if (L.plane == 520)
         k_half_sweep_band<520><<<grid, 288, band_smem(), st>>>(
             L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
-    else
+    else if (L.plane == 264)
         k_half_sweep_band<264><<<grid, 288, band_smem(), st>>>(
+            L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
+    else
+        k_half_sweep_band<136><<<grid, 288, band_smem(), st>>>(
             L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
     return true;
 }
