@@ -731,7 +731,7 @@ def reduce_parts(vals: torch.Tensor) -> float:
             t = t.cpu()
         allp = [torch.empty_like(t) for _ in range(d.get_world_size())]
         d.all_gather(allp, t)
-        return float(sum(float(x.item()) for x in allp))
+        return float(sum(torch.cat(allp).cpu().tolist()))   # one device -> host copy
     return float(tot.item())
 
 
