@@ -1439,12 +1439,15 @@ __device__ __forceinline__ void bar_compute() {   // the 8 compute warps only
 // (A fused-residual mode -- the lagged norm's red sweep, with the incoming
 // red values loaded from HBM into registers at each step -- ran at 501 us
 // against 413 us for k_half_sweep_seg's: not kept.)
-template <int PLC>
+// DOT: also partials[blockIdx.x] = this CTA's sum of f * (new value) over
+// its cells (CG's <r, z> fused into the SSOR half-sweeps, as
+// k_half_sweep_seg's DOT mode); the f row is then released after the store.
+template <int PLC, bool DOT = false>
 __global__ void __launch_bounds__(288, 1)
 k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
                   double post_scale, int nstrip, int nband, int band_rows,
                   const __grid_constant__ CUtensorMap mF, const __grid_constant__ CUtensorMap mB,
-                  const __grid_constant__ CUtensorMap mE) {
+                  const __grid_constant__ CUtensorMap mE, double *__restrict__ partials) {
     constexpr int SEG = 16, NZ = BAND_NZ, B = 4;
     extern __shared__ __align__(128) double bsm_raw[];
     double *bsm = bsm_raw + (((128u - (smem_u32(bsm_raw) & 127u)) & 127u) >> 3);
@@ -1465,6 +1468,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
     uint64_t *fullF = fullB + 4;                                     // [2]
     uint64_t *emptyB = fullF + 2;                                    // [4]
     uint64_t *emptyF = emptyB + 4;                                   // [2]
+    double *wsum = reinterpret_cast<double *>(emptyF + 2);           // DOT: [8]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < NZ; t += blockDim.x) {
         tdrw[t] = L.drw[t];
@@ -1540,6 +1544,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
     const int k0 = w * SEG;
     const double scale = rho * post_scale;
     const double omr = 1.0 - rho;
+    double dacc = 0.0;
     unsigned seqb = 0, seqf = 0;                     // sequence of the unit's first rows
     for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
         const int strip = unit % nstrip, band = unit / nstrip;
@@ -1595,7 +1600,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(emptyB + (qs & 3));
-                mbar_arrive(emptyF + (qf & 1));
+                if (!DOT) mbar_arrive(emptyF + (qf & 1));
                 if (j == j1 - 1) {
                     mbar_arrive(emptyB + ((qs + 1) & 3));
                     mbar_arrive(emptyB + ((qs + 2) & 3));
@@ -1636,10 +1641,25 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                     y = y + omr * u[q];
                 }
                 u[q] = y;
+                if (DOT) dacc += Frow[(k0 + e) * 32 + lane] * y;
+            }
+            if (DOT) {   // the f row is free only now
+                __syncwarp();
+                if (lane == 0) mbar_arrive(emptyF + (qf & 1));
             }
         }
         seqb += (unsigned)(j1 - j0 + 2);
         seqf += (unsigned)(j1 - j0);
+    }
+    if (DOT) {   // fixed-order reduction over the compute warps
+        const double ws = warp_sum(dacc);
+        if (lane == 0) wsum[w] = ws;
+        bar_compute();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q) t += wsum[q];
+            partials[blockIdx.x] = t;
+        }
     }
 }
 
@@ -2992,10 +3012,17 @@ bool half_sweep_dot_ok(const Lvl &L) {
            !(L.hflags & 1);
 }
 
+static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
+                                   double rho, int zero_start, int nbr_zero, double post_scale,
+                                   cudaStream_t st, double *partials, int *np);
+
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
                                   int zero_start, int nbr_zero, double post_scale,
                                   double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st,
+                               partials, np))
+        return cudaGetLastError();
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
     const size_t sm = sizeof(double) * (7 * (size_t)L.nz + 4 * 16 * 32);
@@ -3196,6 +3223,12 @@ void setup_kernel_attributes() {
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<136>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<520, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<264, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<136, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_cp<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaFuncSetAttribute(k_half_sweep_cp<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -3288,7 +3321,7 @@ static bool launch_half_sweep_tx(const Lvl &L, double *u, const double *f, int c
 // neighbours read, no fused halo
 static size_t band_smem() {
     return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 2 * 4 * BAND_NZ * 2 +
-                             6 * BAND_NZ + 2 * 8 * 32) + 12 * 8 + 128;
+                             6 * BAND_NZ + 2 * 8 * 32 + 8) + 12 * 8 + 128;
 }
 
 static bool band_on() {
@@ -3305,7 +3338,7 @@ static bool band_l1() {   // level 2 (nx = 256) on the band kernel too
 
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
                                    double rho, int zero_start, int nbr_zero, double post_scale,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, double *partials, int *np) {
     const int hrow = L.nx / 2;
     if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
         !(L.plane == 520 || L.plane == 264 || (L.plane == 136 && band_l1())) ||
@@ -3331,22 +3364,30 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     nband = (L.ny + band_rows - 1) / band_rows;
     const int nunits = nstrip * nband;
     const int grid = nunits < sm_count() ? nunits : sm_count();
-    if (L.plane == 520)
-        k_half_sweep_band<520><<<grid, 288, band_smem(), st>>>(
-            L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
-    else if (L.plane == 264)
-        k_half_sweep_band<264><<<grid, 288, band_smem(), st>>>(
-            L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
-    else
-        k_half_sweep_band<136><<<grid, 288, band_smem(), st>>>(
-            L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, mE);
+    if (np) *np = grid;
+#define PMG_BANDL(P)                                                                        \
+    do {                                                                                    \
+        if (partials)                                                                       \
+            k_half_sweep_band<P, true><<<grid, 288, band_smem(), st>>>(                     \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, partials);                                                              \
+        else                                                                                \
+            k_half_sweep_band<P><<<grid, 288, band_smem(), st>>>(                           \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, nullptr);                                                               \
+    } while (0)
+    if (L.plane == 520) PMG_BANDL(520);
+    else if (L.plane == 264) PMG_BANDL(264);
+    else PMG_BANDL(136);
+#undef PMG_BANDL
     return true;
 }
 
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
                                        double post_scale, cudaStream_t st, bool *fused) {
-    if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st)) {
+    if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st, nullptr,
+                               nullptr)) {
         *fused = false;
         return cudaGetLastError();
     }
