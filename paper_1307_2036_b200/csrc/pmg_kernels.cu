@@ -2935,7 +2935,10 @@ cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const doubl
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
         const int capw = sm_count() * (occ > 0 ? occ : 1) * 4;
-        int kcs = F.nz;
+        // k-chunks of at most 32 levels: more, shorter warp tasks balance the
+        // persistent warps (configs[1] fine level: 331 us at 64, 314 at 32,
+        // 317 at 16)
+        int kcs = F.nz < 32 ? F.nz : 32;
         while (kcs > 8 && (long long)mb32 * C.ny * ((F.nz + kcs - 1) / kcs) < 2LL * capw)
             kcs >>= 1;
         const int ntiles = mb32 * C.ny * ((F.nz + kcs - 1) / kcs);
