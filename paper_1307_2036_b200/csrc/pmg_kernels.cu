@@ -1442,7 +1442,9 @@ __device__ __forceinline__ void bar_compute() {   // the 8 compute warps only
 // DOT: also partials[blockIdx.x] = this CTA's sum of f * (new value) over
 // its cells (CG's <r, z> fused into the SSOR half-sweeps, as
 // k_half_sweep_seg's DOT mode); the f row is then released after the store.
-template <int PLC, bool DOT = false>
+// FSQ: partials[blockIdx.x] = this CTA's sum of f^2 (mg_solve's ||f|| in the
+// first cycle, k_half_sweep_seg's RES = 3 mode).
+template <int PLC, bool DOT = false, bool FSQ = false>
 __global__ void __launch_bounds__(288, 1)
 k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
                   double post_scale, int nstrip, int nband, int band_rows,
@@ -1586,7 +1588,9 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                     const double vs = Srow[k * BAND_W + lane];
                     const double vn = Nrow[k * BAND_W + lane];
                     const double2 ia = ti[k];
-                    double g = ia.x * Frow[k * 32 + lane];
+                    const double fv = Frow[k * 32 + lane];
+                    if (FSQ) dacc = __fma_rn(fv, fv, dacc);
+                    double g = ia.x * fv;
                     // k_half_sweep_seg's tw table, formed on the fly
                     const double dd = ia.x * tdrw[k];
                     const double2 cw = make_double2(dd * L.wx0, dd * L.wy0);
@@ -1651,7 +1655,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
         seqb += (unsigned)(j1 - j0 + 2);
         seqf += (unsigned)(j1 - j0);
     }
-    if (DOT) {   // fixed-order reduction over the compute warps
+    if (DOT || FSQ) {   // fixed-order reduction over the compute warps
         const double ws = warp_sum(dacc);
         if (lane == 0) wsum[w] = ws;
         bar_compute();
@@ -3017,14 +3021,14 @@ bool half_sweep_dot_ok(const Lvl &L) {
 
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
                                    double rho, int zero_start, int nbr_zero, double post_scale,
-                                   cudaStream_t st, double *partials, int *np);
+                                   cudaStream_t st, double *partials, int *np, bool fsq);
 
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
                                   int zero_start, int nbr_zero, double post_scale,
                                   double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st,
-                               partials, np))
+                               partials, np, false))
         return cudaGetLastError();
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
@@ -3142,6 +3146,8 @@ cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int 
         launch_segv_mode<3>(L, u, nullptr, f, color, nbr_zero, partials, np, st);
         return cudaGetLastError();
     }
+    if (launch_half_sweep_band(L, u, f, color, 1.0, 0, nbr_zero, 1.0, st, partials, np, true))
+        return cudaGetLastError();
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
     const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
@@ -3228,6 +3234,12 @@ void setup_kernel_attributes() {
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<520, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<520, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<264, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<136, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<264, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<136, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3341,7 +3353,8 @@ static bool band_l1() {   // level 2 (nx = 256) on the band kernel too
 
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
                                    double rho, int zero_start, int nbr_zero, double post_scale,
-                                   cudaStream_t st, double *partials, int *np) {
+                                   cudaStream_t st, double *partials, int *np,
+                                   bool fsq = false) {
     const int hrow = L.nx / 2;
     if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
         !(L.plane == 520 || L.plane == 264 || (L.plane == 136 && band_l1())) ||
@@ -3370,7 +3383,11 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     if (np) *np = grid;
 #define PMG_BANDL(P)                                                                        \
     do {                                                                                    \
-        if (partials)                                                                       \
+        if (partials && fsq)                                                                \
+            k_half_sweep_band<P, false, true><<<grid, 288, band_smem(), st>>>(              \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, partials);                                                              \
+        else if (partials)                                                                  \
             k_half_sweep_band<P, true><<<grid, 288, band_smem(), st>>>(                     \
                 L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
                 mE, partials);                                                              \
@@ -3390,7 +3407,7 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
                                        double rho, int zero_start, int nbr_zero,
                                        double post_scale, cudaStream_t st, bool *fused) {
     if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st, nullptr,
-                               nullptr)) {
+                               nullptr, false)) {
         *fused = false;
         return cudaGetLastError();
     }
