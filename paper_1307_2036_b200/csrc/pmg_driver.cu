@@ -9,6 +9,7 @@
 // Operation sequence = the Python drivers' fused path (multigrid.v_cycle
 // with cfg.fused, krylov.pcg_solve), so both give bit-identical results.
 #include <cmath>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -463,9 +464,31 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     *converged = 0;
     double r0 = 0.0, prev = 0.0;
     bool predict = pmg_residual_restrict_red_ok(l0) != 0;
+    // PMG_GRAPH_TIMING=1: device time of each cycle graph vs the solve's wall
+    // time (the difference is the host round trip per cycle), on stderr
+    static int timing = getenv("PMG_GRAPH_TIMING") ? 1 : 0;
+    cudaEvent_t tev[2] = {nullptr, nullptr};
+    double gsum = 0.0;
+    if (timing) {
+        cudaEventCreate(&tev[0]);
+        cudaEventCreate(&tev[1]);
+    }
+    cudaEvent_t t_all0 = nullptr, t_all1 = nullptr;
+    if (timing) {
+        cudaEventCreate(&t_all0);
+        cudaEventCreate(&t_all1);
+        cudaEventRecord(t_all0, st);
+    }
     for (int it = 0; it < maxiter; ++it) {
+        if (timing) cudaEventRecord(tev[0], st);
         TRY(replay_kind(h, u, f, kind, st, [&] { return lagged_body(h, f, kind, g, st); }));
+        if (timing) cudaEventRecord(tev[1], st);
         TRYC(cudaStreamSynchronize(st), "sync");
+        if (timing) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tev[0], tev[1]);
+            gsum += ms;
+        }
         if (it == 0) {
             // r0 = ||f|| (multigrid.py:307-309), summed by the first cycle
             r0 = std::sqrt(h->res_h[1]);
@@ -494,6 +517,18 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
             kind = (predict && predict_last(rn, prev, r0, eps)) ? 6 + x : 4 + x;
         }
         prev = rn;
+    }
+    if (timing) {
+        cudaEventRecord(t_all1, st);
+        cudaEventSynchronize(t_all1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, t_all0, t_all1);
+        fprintf(stderr, "pmg graph timing: %d cycles, graphs %.3f ms, solve %.3f ms\n", *iters,
+                gsum, ms);
+        cudaEventDestroy(tev[0]);
+        cudaEventDestroy(tev[1]);
+        cudaEventDestroy(t_all0);
+        cudaEventDestroy(t_all1);
     }
     h->last_iters = *iters;
     if (x == 1)   // the result's red array is red1: copy it into u
