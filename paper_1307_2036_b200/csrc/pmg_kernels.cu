@@ -3232,6 +3232,12 @@ void setup_kernel_attributes() {
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<136>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<1032>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<1032, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<1032, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<520, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<520, false, true>,
@@ -3357,7 +3363,8 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
                                    bool fsq = false) {
     const int hrow = L.nx / 2;
     if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
-        !(L.plane == 520 || L.plane == 264 || (L.plane == 136 && band_l1())) ||
+        !(L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
+          (L.plane == 136 && band_l1())) ||
         L.seg != 16 || nbr_zero || (L.hflags & 1) || L.nx % 2 || hrow % 32 || hrow < 64 ||
         L.ny < 8)
         return false;
@@ -3371,9 +3378,17 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     // units per SM: a multiple of the SM count keeps the CTAs balanced;
     // measured best 4 at 16 strips (nx = 1024: 269 us; 2 -> 373, 8 -> 278),
     // 2 at 8 strips (nx = 512: 76.3 us; 4 -> 80.3), 1 below
+    // (the smallest count that makes strips x bands a multiple of the SMs:
+    // nstrip / gcd(nstrip, SMs) -- 8 at 32 strips on 148 SMs)
     static int ups_env = -1;
     if (ups_env < 0) ups_env = getenv("PMG_BAND_UPS") ? atoi(getenv("PMG_BAND_UPS")) : 0;
-    const int ups = ups_env ? ups_env : (nstrip >= 16 ? 4 : (nstrip >= 8 ? 2 : 1));
+    int gcd = nstrip, bsm = sm_count();
+    while (bsm) {
+        const int t = gcd % bsm;
+        gcd = bsm;
+        bsm = t;
+    }
+    const int ups = ups_env ? ups_env : nstrip / gcd;
     int nband = (ups * sm_count() + nstrip - 1) / nstrip;
     if (nband > L.ny) nband = L.ny;
     const int band_rows = (L.ny + nband - 1) / nband;
@@ -3398,6 +3413,7 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     } while (0)
     if (L.plane == 520) PMG_BANDL(520);
     else if (L.plane == 264) PMG_BANDL(264);
+    else if (L.plane == 1032) PMG_BANDL(1032);
     else PMG_BANDL(136);
 #undef PMG_BANDL
     return true;
