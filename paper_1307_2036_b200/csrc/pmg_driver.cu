@@ -306,7 +306,7 @@ int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st)
 // mode (k_half_sweep_seg / k_half_sweep_segv), nx % 4 == 0 with a coarse
 // level of >= 2 columns (column-quad restriction / prolongation)
 bool wrap_ok(const pmg_hier *h) {
-    if (!h->d.periodic_x || !h->d.periodic_y || getenv("PMG_NO_WRAP") || getenv("PMG_CP") ||
+    if (!h->d.periodic_x || !h->d.periodic_y || getenv("PMG_NO_WRAP") ||
         getenv("PMG_RR_NOQ") || getenv("PMG_PROLONG_NOQ") || pmg_get_smoother_mode() != 0)
         return false;
     for (size_t c = 0; c < h->lv.size(); ++c) {

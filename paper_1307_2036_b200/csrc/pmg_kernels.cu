@@ -1801,189 +1801,6 @@ k_half_sweep_pro(Lvl L, Lvl C, double *__restrict__ u, const double *__restrict_
 }
 
 // ---------------------------------------------------------------------------
-// Line smoother half-sweep, FAST mode, software-pipelined through shared
-// memory (default for nz = 16 * SEG, nx a multiple of 32, uniform).
-//
-// k_half_sweep_seg is bound by per-tile latency: each tile's loads are
-// waited on before its recurrences run and nothing is in flight while they
-// do.  Here one persistent CTA per SM streams tiles of 16 columns x nz
-// levels through two shared-memory stages with cp.async: while tile t is
-// solved from stage t&1, tile t+1's rows (f, the other colour's W/E row,
-// the S and N rows: 68 x nz doubles) are already on their way into the
-// other stage, so HBM sees a continuous request stream.  Thread (sg, col):
-// column h0 + col, levels [sg*SEG, sg*SEG + SEG) of the 16 segments; the
-// segmented solve is k_half_sweep_seg's (same tables, same reassociation).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-constexpr int CP_TW = 16;                      // columns per tile
-constexpr int CP_ROW = 16 + 20 + 16 + 16;      // staged doubles per level: f | W/E | S | N
-
-template <int SEG, int NBZ, int NST = 3>
-__global__ void __launch_bounds__(256, 1)
-k_half_sweep_cp(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-                int zero_start, double post_scale, int ntiles, int htiles) {
-    constexpr int NZ = 16 * SEG;
-    extern __shared__ __align__(16) double csm[];
-    double *stage0 = csm;                                   // [NST][NZ][CP_ROW]
-    double2 *tw = reinterpret_cast<double2 *>(csm + NST * NZ * CP_ROW);
-    double2 *ti = tw + NZ;
-    double2 *tb = ti + NZ;
-    double *tq = reinterpret_cast<double *>(tb + NZ);
-    double *hend = tq + NZ;                                 // [16][16]
-    double *ybeg = hend + 16 * 16;                          // [16][16]
-    const int tid = threadIdx.x;
-    const int col = tid & 15, sg = tid >> 4;
-    for (int t = tid; t < NZ; t += blockDim.x) {
-        const double io = L.invd1[t], dd = io * L.drw[t];
-        tw[t] = make_double2(dd * L.wx0, dd * L.wy0);
-        ti[t] = make_double2(io, L.segtab[t]);          // (iota, alpha)
-        tb[t].y = L.segtab[NZ + t];                      // mu
-    }
-    __syncthreads();
-    // segment products for this kernel's 16 segments of SEG levels (the
-    // level's segtab pf / q are for L.seg-level segments)
-    if (tid < 16) {
-        const int a = tid * SEG;
-        double pp = 1.0;
-        for (int e = 0; e < SEG; ++e) {
-            pp *= ti[a + e].y;
-            tb[a + e].x = pp;
-        }
-        double qq = 1.0;
-        for (int e = SEG - 1; e >= 0; --e) {
-            qq *= tb[a + e].y;
-            tq[a + e] = qq;
-        }
-    }
-    const int o = c ^ 1;
-    const long long pl = L.plane;
-    const double scale = rho * post_scale;
-    const double omr = 1.0 - rho;
-    // issue the copies of tile t into stage st (all threads).  Uniform
-    // control flow: per array, thread tid copies 16-byte piece (tid & 7) of
-    // levels (tid >> 3) + 32 m; the W/E row's last two pieces per level
-    // are one extra copy per thread
-    const int pk = tid >> 3, pp = 2 * (tid & 7);
-    const int qk = tid >> 1, qp = 16 + 2 * (tid & 1);
-    auto prefetch = [&](int t, int st) {
-        const int j = t / htiles;
-        const int h0 = (t - j * htiles) * CP_TW;
-        double *S = stage0 + st * NZ * CP_ROW;
-        const double *gf = f + at(L, c, pk, j, h0) + pp;
-        const double *gw = u + at(L, o, pk, j, h0 - 2) + pp;
-        const double *gs = u + at(L, o, pk, j - 1, h0) + pp;
-        const double *gn = u + at(L, o, pk, j + 1, h0) + pp;
-        double *d = S + pk * CP_ROW + pp;
-#pragma unroll
-        for (int m = 0; m < NZ / 32; ++m) {
-            const long long go = (long long)m * 32 * pl;
-            double *dm = d + m * 32 * CP_ROW;
-            cp_async16(dm, gf + go);
-            if (!NBZ) {
-                cp_async16(dm + 16, gw + go);
-                cp_async16(dm + 36, gs + go);
-                cp_async16(dm + 52, gn + go);
-            }
-        }
-        if (!NBZ) {
-#pragma unroll
-            for (int m = 0; m < NZ / 128 + (NZ % 128 ? 1 : 0); ++m) {
-                const int k = qk + 128 * m;
-                if (k < NZ)
-                    cp_async16(S + k * CP_ROW + 16 + qp,
-                               u + at(L, o, k, j, h0 - 2) + qp);
-            }
-        }
-    };
-    // prologue: tiles of the first NST-1 iterations in flight
-#pragma unroll
-    for (int q = 0; q < NST - 1; ++q) {
-        const int tq0 = blockIdx.x + q * gridDim.x;
-        if (tq0 < ntiles) prefetch(tq0, q);
-        cp_commit();
-    }
-    int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        cp_wait<NST - 2>();                                 // tile t's group landed
-        __syncthreads();       // ... for every thread; tile t-1 fully consumed
-        {
-            const int tn = t + (NST - 1) * gridDim.x;      // refill the stage tile t-1 used
-            if (tn < ntiles) prefetch(tn, (it + NST - 1) % NST);
-            cp_commit();
-        }
-        const double *S = stage0 + (it % NST) * NZ * CP_ROW;
-        const int j = t / htiles;
-        const int h0 = (t - j * htiles) * CP_TW;
-        const int s0 = (j + L.par + c) & 1;
-        const int nact = min(CP_TW, ((L.nx - s0) + 1) / 2 - h0);
-        const int k0 = sg * SEG;
-        double r[SEG];
-#pragma unroll
-        for (int e = 0; e < SEG; ++e) {
-            const double *row = S + (k0 + e) * CP_ROW;
-            const double2 ia = ti[k0 + e];
-            double g = ia.x * row[col];
-            if (!NBZ) {
-                const double2 cw = tw[k0 + e];
-                const double w = row[16 + col + 1 + s0], ee = row[16 + col + 2 + s0];
-                g = __fma_rn(cw.y, row[36 + col] + row[52 + col], g);
-                g = __fma_rn(cw.x, w + ee, g);
-            }
-            r[e] = g;
-        }
-        // local forward, segment scan, local backward, segment scan
-        double hp = 0.0;
-#pragma unroll
-        for (int e = 0; e < SEG; ++e) {
-            hp = __fma_rn(ti[k0 + e].y, hp, r[e]);
-            r[e] = hp;
-        }
-        hend[sg * 16 + col] = hp;
-        __syncthreads();
-        double G = 0.0;
-        for (int q = 0; q < sg; ++q) G = __fma_rn(tb[(q + 1) * SEG - 1].x, G, hend[q * 16 + col]);
-        double yp = 0.0;
-#pragma unroll
-        for (int e = SEG - 1; e >= 0; --e) {
-            const double2 pm = tb[k0 + e];
-            const double g = __fma_rn(pm.x, G, r[e]);
-            yp = __fma_rn(pm.y, yp, g);
-            r[e] = yp;
-        }
-        ybeg[sg * 16 + col] = yp;
-        __syncthreads();
-        double X = 0.0;
-        for (int q = 15; q > sg; --q) X = __fma_rn(tq[q * SEG], X, ybeg[q * 16 + col]);
-        if (col < nact) {
-            const long long pc = at(L, c, k0, j, h0 + col);
-#pragma unroll
-            for (int e = 0; e < SEG; ++e) {
-                double y = __fma_rn(tq[k0 + e], X, r[e]);
-                const long long q = pc + (long long)e * pl;
-                if (zero_start) {
-                    if (scale != 1.0) y = y * scale;
-                } else if (rho != 1.0) {
-                    y = y * rho;
-                    y = y + omr * u[q];
-                }
-                u[q] = y;
-            }
-        }
-    }
-    cp_wait<0>();
-}
-
-
-// ---------------------------------------------------------------------------
 // FAST half-sweep for VARIABLE coefficients (configs[4]): the k-segmented
 // solve of k_half_sweep_seg with per-column weights / vertical coupling and
 // the per-cell pivots of the level (L.invd, smoother.py:93-99) loaded with
@@ -3225,7 +3042,6 @@ void setup_kernel_attributes() {
     static bool done = false;
     if (done) return;
     done = true;
-    const int big = 227 * 1024;
     cudaFuncSetAttribute(k_half_sweep_band<520>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<264>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3250,28 +3066,9 @@ void setup_kernel_attributes() {
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<136, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_cp<8, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_half_sweep_cp<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_half_sweep_cp<4, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_half_sweep_cp<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_half_sweep_cp<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    cudaFuncSetAttribute(k_half_sweep_cp<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     cudaGetLastError();
 }
 
-// k_half_sweep_cp: nz = 16 * {2, 4, 8}, whole 16-column tiles per row
-// (nx a multiple of 32), so every staged row lies inside the padded rows
-// Opt-in (PMG_CP=1): measured slower than k_half_sweep_seg on B200
-// (595 vs 320 us at configs[1]'s fine level): the cp.async requests of one
-// CTA per SM hit the L1 request queue (lg_throttle) and the 16-column tiles'
-// cross-warp scans serialise the compute.
-static bool cp_eligible(const Lvl &L) {
-    static int on = -1;
-    if (on < 0) on = getenv("PMG_CP") ? 1 : 0;
-    const int nz16 = L.nz / 16;
-    return on && L.uniform && L.nz % 16 == 0 && (nz16 == 2 || nz16 == 4 || nz16 == 8) &&
-           L.nx % 32 == 0 && L.pitch >= OFF + L.nx / 2 + 4;
-}
 
 // tensor maps for k_half_sweep_tx: 3-D views (pitch, nz, ny + 2) of one
 // colour array with a box of boxw columns x kc levels x 1 row
@@ -3469,22 +3266,6 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
                                             ntiles, hx, nullptr, nullptr);
         };
-        if (cp_eligible(L) && !(L.hflags & 1)) {
-            const int ht = ((L.nx + 1) / 2) / CP_TW;
-            const int nt = ht * L.ny;
-            const size_t smc = sizeof(double) * (3 * (size_t)L.nz * CP_ROW + 7 * (size_t)L.nz +
-                                                 2 * 16 * 16);
-            auto runc = [&](auto kern) {
-                const int grid = nt < sm_count() ? nt : sm_count();
-                kern<<<grid, 256, smc, st>>>(L, u, f, color, rho, zero_start, post_scale, nt, ht);
-            };
-            switch (L.nz / 16) {
-            case 8: if (nbr_zero) runc(k_half_sweep_cp<8, 1>); else runc(k_half_sweep_cp<8, 0>); break;
-            case 4: if (nbr_zero) runc(k_half_sweep_cp<4, 1>); else runc(k_half_sweep_cp<4, 0>); break;
-            default: if (nbr_zero) runc(k_half_sweep_cp<2, 1>); else runc(k_half_sweep_cp<2, 0>); break;
-            }
-            return cudaGetLastError();
-        }
         {
             // compile-time neighbour mode, predicate-free when the segments
             // tile nz exactly (all BASELINE configs)

@@ -741,8 +741,8 @@ def test_collect_distribute_round_trip(pmg):
                                            (128, 128, 4), (256, 32, 1)])
 def test_staged_smoother_vs_exact(pmg, nx, nz, workers):
     """The fast half-sweep at nz multiples of 16 and parts of >= 32 columns
-    (k_half_sweep_seg with compile-time plane strides; k_half_sweep_cp when
-    PMG_CP=1) against the exact sequential solver, every mode of
+    (k_half_sweep_seg with compile-time plane strides) against the exact
+    sequential solver, every mode of
     LineSmoother.half_sweep (rho, zero start, no neighbours, post scale) and
     ssor_apply: 1e-12 (tests/test_smoother.py:48)."""
     grid = pmg.periodic_box(nx, nz, 0.01)
