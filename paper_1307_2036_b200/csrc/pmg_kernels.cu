@@ -2037,10 +2037,13 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
 // J0+JB form a sliding window (JB + 2 row loads instead of 3 JB), and all
 // loads of the thread's rows are issued before any arithmetic.  Same
 // arithmetic and order: bit-identical to k_prolong_q.
-template <int JB>
+template <int JB, int CM = 0>
 __global__ void __launch_bounds__(128)
 k_prolong_w(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
-            int cmask) {
+            int cmask_rt) {
+    // CM: the colour mask at compile time (2 = black only, the V-cycle's
+    // case), 0 = runtime
+    const int cmask = CM ? CM : cmask_rt;
     const int lane = threadIdx.x & 31;
     const int npair = C.nx >> 1;
     const int m0 = blockIdx.x * 128 + (threadIdx.x & ~31);
@@ -3376,7 +3379,9 @@ cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double 
             jb = e ? atoi(e) : 2;
         }
         const int gx = (npair + 127) / 128;
-        if (jb == 2) k_prolong_w<2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+        if (jb == 2 && cmask == 2)
+            k_prolong_w<2, 2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+        else if (jb == 2) k_prolong_w<2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
         else if (jb == 4) k_prolong_w<4><<<dim3(gx, F.nz, (C.ny + 3) / 4), 128, 0, st>>>(F, C, cu, fu, add, cmask);
         else if (jb == 8) k_prolong_w<8><<<dim3(gx, F.nz, (C.ny + 7) / 8), 128, 0, st>>>(F, C, cu, fu, add, cmask);
         else k_prolong_q<<<dim3(gx, F.nz, C.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
