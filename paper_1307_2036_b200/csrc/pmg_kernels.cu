@@ -1188,7 +1188,7 @@ k_half_sweep_tx(Lvl L, double *__restrict__ u, int c, double rho, int zero_start
 // iota_k * rhs_k for this warp's levels: local forward, segment scan,
 // local backward, segment scan, fix-up, relaxation and store (+ halo
 // copies).  Shared by k_half_sweep_seg and k_half_sweep_pro.
-template <int SEG, bool HALO, bool DOT = false>
+template <int SEG, bool HALO, bool DOT = false, bool LEAN = false>
 __device__ __forceinline__ void seg_solve_store(
     const Lvl &L, double *__restrict__ u, double (&r)[SEG], const double2 *ti,
     const double2 *tb, const double *tq, double *hend, double *ybeg, int c, int j, int h0,
@@ -1238,9 +1238,10 @@ __device__ __forceinline__ void seg_solve_store(
                 const int k = k0 + e;
                 double y = __fma_rn(tq[k], X, r[e]);
                 const long long q = pc + (long long)e * pl;
-                if (zero_start) {
+                // LEAN: rho = 1 without zero start at compile time
+                if (!LEAN && zero_start) {
                     if (scale != 1.0) y = y * scale;
-                } else if (rho != 1.0) {
+                } else if (!LEAN && rho != 1.0) {
                     y = y * rho;
                     y = y + omr * u[q];
                 }
@@ -1401,7 +1402,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
             const double q = __fma_rn(bpend, un, rpend);
             if (lane < nact) dacc = __fma_rn(q, q, dacc);
         }
-        seg_solve_store<SEG, HALO, DOT>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
+        seg_solve_store<SEG, HALO, DOT, RES == 1>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
                                         h0, s0, i, nact, kn, pc, pl, zero_start, rho, scale, omr,
                                         f, &dacc);
     }
@@ -1444,7 +1445,7 @@ __device__ __forceinline__ void bar_compute() {   // the 8 compute warps only
 // k_half_sweep_seg's DOT mode); the f row is then released after the store.
 // FSQ: partials[blockIdx.x] = this CTA's sum of f^2 (mg_solve's ||f|| in the
 // first cycle, k_half_sweep_seg's RES = 3 mode).
-template <int PLC, bool DOT = false, bool FSQ = false>
+template <int PLC, bool DOT = false, bool FSQ = false, bool LEAN = false>
 __global__ void __launch_bounds__(288, 1)
 k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
                   double post_scale, int nstrip, int nband, int band_rows,
@@ -1638,9 +1639,10 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             for (int e = 0; e < SEG; ++e) {
                 double y = __fma_rn(tq[k0 + e], X, r[e]);
                 const long long q = pc + (long long)e * pl;
-                if (zero_start) {
+                // LEAN: rho = 1 without zero start at compile time
+                if (!LEAN && zero_start) {
                     if (scale != 1.0) y = y * scale;
-                } else if (rho != 1.0) {
+                } else if (!LEAN && rho != 1.0) {
                     y = y * rho;
                     y = y + omr * u[q];
                 }
@@ -3053,6 +3055,14 @@ void setup_kernel_attributes() {
                          (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<1032>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<1032, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<520, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<264, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+    cudaFuncSetAttribute(k_half_sweep_band<136, false, false, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<1032, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
     cudaFuncSetAttribute(k_half_sweep_band<1032, false, true>,
@@ -3196,9 +3206,14 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     const int nunits = nstrip * nband;
     const int grid = nunits < sm_count() ? nunits : sm_count();
     if (np) *np = grid;
+    const bool lean = rho == 1.0 && !zero_start;
 #define PMG_BANDL(P)                                                                        \
     do {                                                                                    \
-        if (partials && fsq)                                                                \
+        if (lean && !partials)                                                              \
+            k_half_sweep_band<P, false, false, true><<<grid, 288, band_smem(), st>>>(       \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, nullptr);                                                               \
+        else if (partials && fsq)                                                           \
             k_half_sweep_band<P, false, true><<<grid, 288, band_smem(), st>>>(              \
                 L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
                 mE, partials);                                                              \
