@@ -1262,7 +1262,7 @@ __device__ __forceinline__ void seg_solve_store(
 }
 
 template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false,
-          int PLC = 0, bool DOT = false, int RES = 0>
+          int PLC = 0, bool DOT = false, int RES = 0, bool LEAN = false>
 __global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                  int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles,
@@ -1402,7 +1402,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
             const double q = __fma_rn(bpend, un, rpend);
             if (lane < nact) dacc = __fma_rn(q, q, dacc);
         }
-        seg_solve_store<SEG, HALO, DOT, RES == 1>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
+        seg_solve_store<SEG, HALO, DOT, RES == 1 || LEAN>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
                                         h0, s0, i, nact, kn, pc, pl, zero_start, rho, scale, omr,
                                         f, &dacc);
     }
@@ -3288,12 +3288,15 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             // compile-time neighbour mode, predicate-free when the segments
             // tile nz exactly (all BASELINE configs)
             const bool full = (L.nz % L.seg) == 0;
+            const bool lean = rho == 1.0 && !zero_start;   // compile-time store path
             // compile-time plane stride for the large levels of nz = 128
             // (pitch of nx = 1024, 512, 256)
             const int plc = (L.seg == 16 && full && !(L.hflags & 1)) ? (int)L.plane : 0;
 #define PMG_SEGP(S, P)                                                                \
     do {                                                                              \
-        if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, false, P>);             \
+        if (lean && nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, false, P, false, 0, true>); \
+        else if (lean) run(k_half_sweep_seg<S, 4, 3, 0, true, false, P, false, 0, true>); \
+        else if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, false, P>);        \
         else run(k_half_sweep_seg<S, 4, 3, 0, true, false, P>);                      \
     } while (0)
 #define PMG_SEGF(S)                                                                   \
@@ -3320,7 +3323,9 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             if (L.seg == 16 && full && !(L.hflags & 1) && ntiles <= small) {
                 // launch-latency-bound small level: all 16 levels' loads of a
                 // tile in one batch (one memory round trip per tile)
-                if (nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, false, 0>);
+                if (lean && nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, false, 0, false, 0, true>);
+                else if (lean) run(k_half_sweep_seg<16, 16, 1, 0, true, false, 0, false, 0, true>);
+                else if (nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, false, 0>);
                 else run(k_half_sweep_seg<16, 16, 1, 0, true, false, 0>);
             } else if (plc == 520 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 520);
             else if (plc == 264 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 264);
