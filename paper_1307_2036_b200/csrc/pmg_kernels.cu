@@ -1815,7 +1815,7 @@ k_half_sweep_pro(Lvl L, Lvl C, double *__restrict__ u, const double *__restrict_
 // (smoother.py:137-145), so r_k = g_k - (d_k u_k - bm_k u_{k-1} - bp_k
 // u_{k+1}) with d_k of stencil.py:105-109 from the column's coefficients.
 // RES = 3: in-place sweep that also sums f^2 over the colour (first cycle).
-template <int SEG, int NBZ, int RES = 0>
+template <int SEG, int NBZ, int RES = 0, bool LEAN = false>
 __global__ void __launch_bounds__(512, 1)
 k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                   int zero_start, int post_scale_unused, double post_scale, int ntiles,
@@ -1974,9 +1974,10 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
             for (int e = 0; e < SEG; ++e) {
                 double y = __fma_rn(pq[e], X, r[e]);
                 const long long q = pc + (long long)e * pl;
-                if (zero_start) {
+                // LEAN (and RES = 1): rho = 1 without zero start at compile time
+                if (!LEAN && RES != 1 && zero_start) {
                     if (scale != 1.0) y = y * scale;
-                } else if (rho != 1.0) {
+                } else if (!LEAN && RES != 1 && rho != 1.0) {
                     y = y * rho;
                     y = y + omr * u[q];
                 }
@@ -2906,8 +2907,8 @@ static void launch_segv_mode(const Lvl &L, double *u, double *uw, const double *
     };
 #define PMG_SEGVM(S)                                                               \
     do {                                                                           \
-        if (RES != 1 && nbr_zero) runv(k_half_sweep_segv<S, 1, RES>);              \
-        else runv(k_half_sweep_segv<S, 0, RES>);                                   \
+        if (RES != 1 && nbr_zero) runv(k_half_sweep_segv<S, 1, RES, true>);        \
+        else runv(k_half_sweep_segv<S, 0, RES, true>);                             \
     } while (0)
     switch (seg) {
     case 1: PMG_SEGVM(1); break;
@@ -3260,7 +3261,14 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
                 kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, 0, post_scale,
                                                 ntiles, hx, nullptr, nullptr);
             };
-#define PMG_SEGV(S) do { if (nbr_zero) runv(k_half_sweep_segv<S, 1>); else runv(k_half_sweep_segv<S, 0>); } while (0)
+#define PMG_SEGV(S)                                                                   \
+    do {                                                                              \
+        const bool lean_ = rho == 1.0 && !zero_start;                                 \
+        if (lean_ && nbr_zero) runv(k_half_sweep_segv<S, 1, 0, true>);                \
+        else if (lean_) runv(k_half_sweep_segv<S, 0, 0, true>);                       \
+        else if (nbr_zero) runv(k_half_sweep_segv<S, 1>);                             \
+        else runv(k_half_sweep_segv<S, 0>);                                           \
+    } while (0)
             switch (seg) {
             case 1: PMG_SEGV(1); break;
             case 2: PMG_SEGV(2); break;
