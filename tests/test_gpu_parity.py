@@ -868,7 +868,8 @@ def test_half_sweep_res(pmg, nx, nz, variable):
                       C.c_void_p(nrm.data_ptr()), None)
 
 
-@pytest.mark.parametrize("case", ["box256", "box96", "box80", "box128", "var128", "var256"])
+@pytest.mark.parametrize("case", ["box256", "box96", "box80", "box128", "var128", "var256",
+                                  "box2048"])
 def test_lagged_norm_solve(pmg, case):
     """Native mg_solve with the lagged convergence norm against the plain
     one: equal iteration counts and iterates BIT FOR BIT (same kernels, the
@@ -879,7 +880,7 @@ def test_lagged_norm_solve(pmg, case):
     from paper_1307_2036_b200 import _lib, configs
     nx, nz, nlev = {"box256": (256, 128, 5), "box96": (64, 96, 3), "box80": (32, 80, 2),
                     "box128": (128, 128, 3), "var128": (128, 128, 3),
-                    "var256": (256, 128, 5)}[case]
+                    "var256": (256, 128, 5), "box2048": (2048, 128, 4)}[case]
     if case.startswith("var"):    # configs[4]-like: graded levels, omega^2(x, y)
         prob = configs.Problem(nx, nx, nz, 1e-3, 1.0, nlev, stretch=1.05, variable_omega=True)
         grid, params = prob.grid(), prob.params()
@@ -1078,12 +1079,13 @@ def test_red_restrict_solve(pmg):
     assert np.max(np.abs(u1 - u0)) <= 1e-10 * np.max(np.abs(u0))
 
 
-def test_band_half_sweep_matches_exact(pmg):
-    """The TMA band half-sweep (configs[1]'s fine level, halo-ring mode)
-    against the exact sequential-Thomas smoother (bit-identical to the
-    reference): within the fast mode's 1e-12 (tests/test_smoother.py:48)."""
+@pytest.mark.parametrize("nx", [256, 512, 1024, 2048])
+def test_band_half_sweep_matches_exact(pmg, nx):
+    """The TMA band half-sweep (nx = 256 ... 2048 at nz = 128, halo-ring
+    mode) against the exact sequential-Thomas smoother (bit-identical to
+    the reference): within the fast mode's 1e-12 (tests/test_smoother.py:48)."""
     from paper_1307_2036_b200 import configs
-    prob = configs.config(1)
+    prob = configs.Problem(nx, nx, 128, 1e-3, 1.0, 1)
     hier = pmg.build_hierarchy(prob.grid(), prob.params(),
                                pmg.MGConfig(policy="explicit", explicit_levels=1))
     lay = hier.fine.layout
