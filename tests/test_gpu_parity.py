@@ -888,7 +888,8 @@ def test_lagged_norm_solve(pmg, case):
         grid = pmg.periodic_box(nx, nz, 0.01)
         params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
     fa = uni((nx, nx, nz), 9)
-    for eps in (1e-5, 1e-7, 1e-9):
+    # (the 2048^2 case -- a 4 GB fine level -- checks one tolerance only)
+    for eps in ((1e-5,) if nx >= 2048 else (1e-5, 1e-7, 1e-9)):
         runs = {}
         for lag in (False, True):
             cfg = pmg.MGConfig(policy="explicit", explicit_levels=nlev, eps=eps, lagged_norm=lag)
