@@ -102,6 +102,12 @@ int pmg_field_upload(const pmg_level *lvl, const double *host, double *field,
                      double *staging_dev, void *stream);
 int pmg_field_download(const pmg_level *lvl, const double *field, double *host,
                        double *staging_dev, void *stream);
+/* Device field of a level (both colour arrays, halo ring and padding:
+ * pmg_level_field_doubles() doubles), zero-filled; pmg_field_free releases
+ * it (NULL is a no-op).  Callers may equally pass their own allocations
+ * (e.g. torch tensors) of that size to every entry point. */
+int pmg_field_alloc(const pmg_level *lvl, double **out);
+int pmg_field_free(double *field);
 /* whole allocation (halo included): fill with a value / copy
  * (DistField.fill / copy, partition.py:128-137) */
 int pmg_fill(const pmg_level *lvl, double *field, double value, void *stream);
@@ -193,6 +199,9 @@ int pmg_restrict(const pmg_level *fine, const pmg_level *coarse, const double *f
  * add = 0: overwrite owned cells, add = 1: u += P e (multigrid.py:287-290). */
 int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
                 double *fine_u, int add, void *stream);
+/* fine += P coarse: pmg_prolong with add = 1 (SURVEY 8b's pmg_prolong_add) */
+int pmg_prolong_add(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
+                    double *fine_u, void *stream);
 /* same, restricted to the colours in color_mask (1 red, 2 black, 3 both):
  * with rho = 1 the post-smoothing red half-sweep overwrites every red cell
  * without reading it, so the V-cycle prolongs into black cells only. */

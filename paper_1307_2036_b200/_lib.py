@@ -90,6 +90,9 @@ SIGNATURES = {
     "pmg_get_smoother_mode": (_I, []),
     "pmg_restrict": (_I, [_P, _P, _P, _P, _D, _P]),
     "pmg_prolong": (_I, [_P, _P, _P, _P, _I, _P]),
+    "pmg_prolong_add": (_I, [_P, _P, _P, _P, _P]),
+    "pmg_field_alloc": (_I, [_P, _P]),
+    "pmg_field_free": (_I, [_P]),
     "pmg_prolong_colors": (_I, [_P, _P, _P, _P, _I, _I, _P]),
     "pmg_prolong_colors_halo": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
     "pmg_half_sweep_halo": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _I, _P]),

@@ -531,6 +531,11 @@ int pmg_prolong(const pmg_level *fine, const pmg_level *coarse, const double *cu
     return PMG_OK;
 }
 
+int pmg_prolong_add(const pmg_level *fine, const pmg_level *coarse, const double *cu, double *fu,
+                    void *st) {
+    return pmg_prolong(fine, coarse, cu, fu, 1, st);
+}
+
 int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *cu, double *fu,
                        int add, int color_mask, void *st) {
     return pmg_prolong_colors_halo(fine, coarse, cu, fu, add, color_mask, 0, st);
@@ -587,6 +592,27 @@ int pmg_dot(const pmg_level *lv, const double *a, const double *b, double *scrat
 
 int pmg_norm2(const pmg_level *lv, const double *a, double *scratch, double *out, void *st) {
     return pmg_dot(lv, a, a, scratch, out, st);
+}
+
+int pmg_field_alloc(const pmg_level *lv, double **out) {
+    PMG_CHECK_LVL(lv);
+    if (!out) return fail(PMG_ERR_VALUE, "out must not be NULL");
+    *out = nullptr;
+    const size_t bytes = sizeof(double) * (size_t)pmg_level_field_doubles(lv);
+    void *d = nullptr;
+    PMG_CUDA(cudaMalloc(&d, bytes), "field_alloc");
+    cudaError_t e = cudaMemset(d, 0, bytes);
+    if (e != cudaSuccess) {
+        cudaFree(d);
+        PMG_CUDA(e, "field_alloc");
+    }
+    *out = (double *)d;
+    return PMG_OK;
+}
+
+int pmg_field_free(double *field) {
+    if (field) PMG_CUDA(cudaFree(field), "field_free");
+    return PMG_OK;
 }
 
 int pmg_fill(const pmg_level *lv, double *field, double value, void *st) {

@@ -1106,3 +1106,37 @@ def test_band_half_sweep_matches_exact(pmg, nx):
         out.append(pmg.gather_owned(u))
     fast, ex = out
     assert np.max(np.abs(fast - ex)) <= 1e-12 * np.max(np.abs(ex))
+
+
+def test_field_alloc_and_prolong_add(pmg):
+    """pmg_field_alloc: a zeroed field of pmg_level_field_doubles doubles,
+    released by pmg_field_free; pmg_prolong_add = pmg_prolong(add = 1)
+    bit for bit (SURVEY 8b's names)."""
+    import ctypes as C
+    from paper_1307_2036_b200 import _lib
+    lib = _lib.load()
+    nx, nz = 64, 16
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    hier = pmg.build_hierarchy(grid, pmg.toy_parameters(nx, nz, 1e-3, 1.0),
+                               pmg.MGConfig(policy="explicit", explicit_levels=2))
+    lay, cl = hier.fine.layout, hier.levels[1].layout
+    w = lay.local_workers[0]
+    fh, ch = hier.fine.op.handles[w].h, hier.levels[1].op.handles[w].h
+    n = int(lib.pmg_level_field_doubles(fh))
+    p = C.c_void_p()
+    _lib.call("pmg_field_alloc", fh, C.byref(p))
+    assert p.value
+    got = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.call("pmg_copy", fh, C.c_void_p(got.data_ptr()), p, st)
+    torch.cuda.synchronize()
+    assert got.abs().max().item() == 0.0
+    _lib.call("pmg_field_free", p)
+    _lib.call("pmg_field_free", C.c_void_p(None))
+    cu = field(pmg, uni((nx // 2, nx // 2, nz), 8), cl)
+    pmg.halo_exchange(cu)
+    a, b = field(pmg, uni((nx, nx, nz), 9), lay), field(pmg, uni((nx, nx, nz), 9), lay)
+    _lib.call("pmg_prolong", fh, ch, cu.parts[w].ptr, a.parts[w].ptr, 1, st)
+    _lib.call("pmg_prolong_add", fh, ch, cu.parts[w].ptr, b.parts[w].ptr, st)
+    torch.cuda.synchronize()
+    assert np.array_equal(pmg.gather_owned(a), pmg.gather_owned(b))
