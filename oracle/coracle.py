@@ -39,6 +39,13 @@ def lib():
                                   C.c_double, C.c_int, P, P, P, P]
         L.or_pcg_solve.argtypes = [P, P, P, C.c_double, C.c_int, C.c_double, C.c_int, P, P,
                                    P, P]
+        I, D = C.c_int, C.c_double
+        L.or_apply.argtypes = [P, I, P, P, P]
+        L.or_half_sweep.argtypes = [P, I, P, P, I, D, I, I, D]
+        L.or_sweep.argtypes = [P, I, P, P, I, D]
+        L.or_ssor.argtypes = [P, I, P, P, D]
+        L.or_restrict.argtypes = [P, I, P, P, D]
+        L.or_prolong.argtypes = [P, I, P, P]
         _lib = L
     return _lib
 
@@ -96,6 +103,56 @@ class Hierarchy:
             raise port.BreakdownError("CG breakdown")
         n = it.value
         return u, port.Report(n, list(hist[:n + 1]), bool(conv.value), wall.value)
+
+
+    # ---- per-operation entry points (owned (nx, ny, nz) arrays) ---------------
+
+    def _dims(self, c):
+        return (self.nx >> c, self.ny >> c, self.nz)
+
+    def apply(self, u, c=0):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.empty(self._dims(c))
+        lib().or_apply(self.h, c, u.ctypes.data, None, out.ctypes.data)
+        return out
+
+    def residual(self, f, u, c=0):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        out = np.empty(self._dims(c))
+        lib().or_apply(self.h, c, u.ctypes.data, f.ctypes.data, out.ctypes.data)
+        return out
+
+    def half_sweep(self, u, f, color, rho=1.0, zero_start=False, neighbors_zero=False,
+                   post_scale=1.0, c=0):
+        """In place on ``u`` (owned array)."""
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        assert u.flags.c_contiguous and u.dtype == np.float64
+        lib().or_half_sweep(self.h, c, u.ctypes.data, f.ctypes.data, color, rho,
+                            int(zero_start), int(neighbors_zero), post_scale)
+
+    def sweep(self, u, f, nsweeps=1, rho=1.0, c=0):
+        f = np.ascontiguousarray(f, dtype=np.float64)
+        assert u.flags.c_contiguous and u.dtype == np.float64
+        lib().or_sweep(self.h, c, u.ctypes.data, f.ctypes.data, nsweeps, rho)
+
+    def ssor(self, r, rho=1.0, c=0):
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        z = np.empty(self._dims(c))
+        lib().or_ssor(self.h, c, r.ctypes.data, z.ctypes.data, rho)
+        return z
+
+    def restrict(self, fine, weight=0.25, c=0):
+        fine = np.ascontiguousarray(fine, dtype=np.float64)
+        out = np.empty(self._dims(c + 1))
+        lib().or_restrict(self.h, c, fine.ctypes.data, out.ctypes.data, weight)
+        return out
+
+    def prolong(self, coarse, c=0):
+        coarse = np.ascontiguousarray(coarse, dtype=np.float64)
+        out = np.empty(self._dims(c))
+        lib().or_prolong(self.h, c, coarse.ctypes.data, out.ctypes.data)
+        return out
 
 
 def config_hierarchy(cfg: "port.Config", nlev=None):

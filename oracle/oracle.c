@@ -456,3 +456,98 @@ done:
     free(u); free(r); free(z); free(p); free(q);
     return rc;
 }
+
+/* ---- per-operation entry points (tests/test_oracle_c.py pins each one
+ * against the reference's own outputs, tests/golden/ops_*.npz).  Arrays are
+ * owned (nx, ny, nz) k fastest; level c's scratch fields carry the halo. */
+
+/* stencil.py:127-165: out = A u (f == NULL) or f - A u */
+int or_apply(void *h, int c, const double *u, const double *f, double *out) {
+    hier_t *H = (hier_t *)h;
+    level_t *L = &H->lv[c];
+    memset(L->u, 0, fsize(L) * sizeof(double));
+    load_owned(L, L->u, u);
+    halo(L, L->u, H->px, H->py);
+    if (f) {
+        memset(L->f, 0, fsize(L) * sizeof(double));
+        load_owned(L, L->f, f);
+    }
+    memset(L->r, 0, fsize(L) * sizeof(double));
+    apply_op(L, L->u, f ? L->f : NULL, L->r, 0);
+    store_owned(L, L->r, out);
+    return 0;
+}
+
+/* smoother.py:122-182: one colour of line relaxation of u (in / out) */
+int or_half_sweep(void *h, int c, double *u, const double *f, int color, double rho,
+                  int zero_start, int nbr_zero, double post_scale) {
+    hier_t *H = (hier_t *)h;
+    level_t *L = &H->lv[c];
+    memset(L->u, 0, fsize(L) * sizeof(double));
+    memset(L->f, 0, fsize(L) * sizeof(double));
+    load_owned(L, L->u, u);
+    load_owned(L, L->f, f);
+    halo(L, L->u, H->px, H->py);
+    half_sweep(L, L->u, L->f, color, rho, zero_start, nbr_zero, post_scale);
+    store_owned(L, L->u, u);
+    return 0;
+}
+
+/* smoother.py:184-191: nsweeps red-black sweeps of u (in / out) */
+int or_sweep(void *h, int c, double *u, const double *f, int nsweeps, double rho) {
+    hier_t *H = (hier_t *)h;
+    level_t *L = &H->lv[c];
+    memset(L->u, 0, fsize(L) * sizeof(double));
+    memset(L->f, 0, fsize(L) * sizeof(double));
+    load_owned(L, L->u, u);
+    load_owned(L, L->f, f);
+    halo(L, L->u, H->px, H->py);
+    sweep(L, L->u, L->f, nsweeps, rho, H->px, H->py);
+    store_owned(L, L->u, u);
+    return 0;
+}
+
+/* smoother.py:224-244: z = M^-1 r (symmetric line SOR from zero) */
+int or_ssor(void *h, int c, const double *r, double *z, double rho) {
+    hier_t *H = (hier_t *)h;
+    level_t *L = &H->lv[c];
+    memset(L->f, 0, fsize(L) * sizeof(double));
+    load_owned(L, L->f, r);
+    memset(L->u, 0, fsize(L) * sizeof(double));
+    half_sweep(L, L->u, L->f, 0, rho, 1, 1, 1.0);
+    halo(L, L->u, H->px, H->py);
+    half_sweep(L, L->u, L->f, 1, rho, 1, 0, 2.0 - rho);
+    halo(L, L->u, H->px, H->py);
+    half_sweep(L, L->u, L->f, 0, rho, 0, 0, 1.0);
+    store_owned(L, L->u, z);
+    return 0;
+}
+
+/* multigrid.py:209-230: coarse = weight x children sum of level c's fine */
+int or_restrict(void *h, int c, const double *fine, double *coarse, double weight) {
+    hier_t *H = (hier_t *)h;
+    level_t *L = &H->lv[c], *Cl = &H->lv[c + 1];
+    memset(L->r, 0, fsize(L) * sizeof(double));
+    load_owned(L, L->r, fine);
+    memset(Cl->f, 0, fsize(Cl) * sizeof(double));
+    restrict_sum(L, L->r, Cl, Cl->f);
+    if (weight != 1.0) {
+        const size_t n = fsize(Cl);
+        for (size_t e = 0; e < n; ++e) Cl->f[e] = Cl->f[e] * weight;
+    }
+    store_owned(Cl, Cl->f, coarse);
+    return 0;
+}
+
+/* multigrid.py:233-246: fine (level c) = P coarse (level c + 1) */
+int or_prolong(void *h, int c, const double *coarse, double *fine) {
+    hier_t *H = (hier_t *)h;
+    level_t *L = &H->lv[c], *Cl = &H->lv[c + 1];
+    memset(Cl->u, 0, fsize(Cl) * sizeof(double));
+    load_owned(Cl, Cl->u, coarse);
+    halo(Cl, Cl->u, H->px, H->py);
+    memset(L->r, 0, fsize(L) * sizeof(double));
+    prolong_add(L, L->r, Cl, Cl->u);
+    store_owned(L, L->r, fine);
+    return 0;
+}
