@@ -2,36 +2,52 @@
 achieved HBM GB/s vs peak, 1-8 GPU".
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload config3|config4|config1]
 
 A step is one complete MG solve (u = 0 -> ||r||/||r0|| < 1e-5, V(1,1),
-7 levels) of a 1024 x 1024 x 128 fp64 subdomain per GPU: at N = 1 exactly
-BASELINE configs[1]; at N > 1 the configs[3] weak-scaling decomposition
-(px x py parts, periodic global grid) with configs[1]'s per-GPU size, so
-the per-N values are comparable.  Inputs are synthetic: f ~ U[-1, 1] from
-default_rng(0) in global (i, j, k) order, generated per rank.
+rho = 1, coarse_sweeps = 1) of the workload:
 
-value   = global DOF x K / (max over ranks of the device time of K solves)
-e2e     = same metric through the public API with host buffers: pinned
-          host f -> scatter_block (H2D + layout kernel) -> mg_solve ->
-          owned_to (layout kernel + D2H of u), every step
-roofline= the dominant kernel (fine-level line-smoother half-sweep):
-          12 algorithmic bytes per fine cell / CUDA-event time
-cpu_baseline = oracle/oracle.c (C restatement of the reference, OpenMP)
-          running the full configs[1] solve on the host cores, rank 0, N = 1.
+  config3 (default)  BASELINE configs[3]: 2048 x 2048 x 128 fp64 PER GPU,
+                     8 levels, px x py horizontal decomposition (1x1, 2x1,
+                     2x2, 4x2) of the periodic global grid -- weak scaling;
+                     N = 1 is the single-GPU block
+  config4            BASELINE configs[4]: fixed 4096 x 4096 x 128 global grid,
+                     graded levels (1.05), omega2(x, y), 9 levels -- strong
+                     scaling
+  config1            BASELINE configs[1]: 1024 x 1024 x 128 per GPU, 7 levels
 
---impl reference: the reference algorithm's CPU implementation (the same
-C restatement; the Python reference cannot travel) on this host's cores,
-same config and metric; each step one V-cycle + convergence residual,
-solve time = mean step time x the cycle count of a full reference solve.
+Inputs are synthetic: f ~ U[-1, 1] from default_rng(0) in global (i, j, k)
+order, each rank generating only its own block (PCG64 advanced per row).
+
+value    = global DOF x K / (max over ranks of the device time of K solves)
+e2e      = same metric through the public API with host buffers, one solve
+           at a time (pinned host f -> H2D + layout kernel -> mg_solve ->
+           layout kernel + D2H -> pinned host u, nothing overlapped across
+           steps: a dependent time-step sequence); "pipelined" beside it =
+           SolvePipeline.run, next step's upload overlapping this solve
+roofline = the dominant kernel (fine-level line-smoother half-sweep, 12
+           algorithmic bytes per fine cell) / its CUDA-event time
+extra    = (N = 1) configs[1] MG, configs[2] CG + MG over the omega2 sweep,
+           configs[4] MG -- each timed the same way
+cpu_baseline = (rank 0, N = 1) the REAL reference package (baseline/_ref,
+           SURVEY App. B injection, one core) on a bounded sample, plus the
+           C restatement oracle/oracle.c on the workload (all host threads)
+           and on the sample (one core, taskset -c 0)
+
+--impl reference: rank 0 runs WHOLE solves of the reference algorithm's
+CPU implementation (oracle/oracle.c, pinned to the reference's outputs by
+tests/test_oracle_c.py; the Python reference itself needs ~35 s per V-cycle
+at 1024^2 and cannot run K solves at the workload size) on this host's
+cores, same config dict, metric and residual history.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -41,8 +57,38 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-NX_PER_GPU, NZ, LEVELS = 1024, 128, 7
 PX = {1: 1, 2: 2, 4: 2, 8: 4}
+METRIC = "MG solve DOF/s to 1e-5 residual"
+
+
+def workload(name: str, world: int):
+    """(Problem, description, scaling) of a workload at ``world`` GPUs."""
+    from paper_1307_2036_b200 import configs
+    px = PX[world]
+    py = world // px
+    if name == "config3":
+        prob = configs.config(3, gpus=world)
+        desc = (f"configs[3] MG solve, 2048x2048x128 fp64 per GPU ({prob.nx}x{prob.ny}x128 "
+                "global), 8 levels, V(1,1), rho 1, coarse_sweeps 1, eps 1e-5")
+        return prob, desc, "weak", (px, py)
+    if name == "config4":
+        prob = configs.config(4)
+        desc = ("configs[4] MG solve, 4096x4096x128 fp64 global (fixed), graded levels 1.05, "
+                "omega2(x,y)=1e-3(1+0.5 sin2pix sin2piy), 9 levels, V(1,1), eps 1e-5")
+        return prob, desc, "strong", (px, py)
+    if name == "config1":
+        prob = configs.Problem(1024 * px, 1024 * py, 128, 1e-3, 1.0, 7)
+        desc = (f"configs[1] MG solve, 1024x1024x128 fp64 per GPU ({prob.nx}x{prob.ny}x128 "
+                "global), 7 levels, V(1,1), eps 1e-5")
+        return prob, desc, "weak", (px, py)
+    raise SystemExit(f"unknown workload {name}")
+
+
+def config_dict(name, world):
+    prob, desc, scaling, (px, py) = workload(name, world)
+    return {"workload": desc, "global_grid": [prob.nx, prob.ny, prob.nz], "levels": prob.levels,
+            "parallelism": f"{px}x{py} horizontal domain decomposition (whole columns)",
+            "l2": "inputs larger than L2 (>= 1.09 GB per field)"}, prob, scaling
 
 
 def measured_peak():
@@ -53,12 +99,17 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str):
+def ncu_traffic(kernel: str, nx: int):
+    """DRAM bytes per launch of ``kernel`` at fine-level size ``nx`` from the
+    committed ncu --set full capture (profiles/ncu_traffic.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         with open(p) as fh:
-            return json.load(fh).get(kernel)
-    return None
+            d = json.load(fh)
+        v = d.get(f"{kernel}@{nx}")
+        if isinstance(v, dict):
+            return v.get("dram_bytes"), v.get("source")
+    return None, None
 
 
 class ClockSampler:
@@ -153,59 +204,143 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def cpu_baseline_sample():
-    """Full configs[1] MG solve with the C restatement on this host's cores."""
-    from oracle import coracle, port
-    cfg = port.CONFIGS[1]
-    f = port.rhs(cfg.nx, cfg.ny, cfg.nz, 0)
-    h = coracle.config_hierarchy(cfg)
-    _, rep = h.mg_solve(f, want_u=False)
-    dof = cfg.nx * cfg.ny * cfg.nz
-    return {"value": dof / rep.wall_time, "unit": "DOF/s", "cores": coracle.threads(),
-            "kind": "port",
-            "sample": (f"full configs[1] MG solve ({rep.iterations} V-cycles to 1e-5, "
-                       f"{rep.wall_time:.2f} s) by oracle/oracle.c (C restatement of the "
-                       "reference, OpenMP, reference op order)"),
-            "iterations": rep.iterations, "solve_s": rep.wall_time}
+# ---------------------------------------------------------------------------
+# CPU legs (oracle/ is the checker / CPU baseline only -- never the product)
+# ---------------------------------------------------------------------------
+
+SAMPLE_NX, SAMPLE_LEVELS = 512, 6
+
+
+def _ref_subprocess(code: str, one_core: bool, timeout: float = 600.0) -> dict:
+    """Run ``code`` (prints one JSON line) in a fresh interpreter, optionally
+    pinned to core 0 with one thread."""
+    env = dict(os.environ)
+    cmd = [sys.executable, "-c", code]
+    if one_core:
+        env.update(OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+        cmd = ["taskset", "-c", "0"] + cmd
+    out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True,
+                         timeout=timeout)
+    if out.returncode != 0:
+        raise RuntimeError(out.stderr.strip().splitlines()[-1] if out.stderr else "failed")
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+_REF_CODE = """
+import json, sys
+sys.path.insert(0, {root!r})
+from oracle import port, refharness
+cfg = port.Config({nx}, {nx}, 128, 0.01, 1e-3, 1.0, {lv})
+u, rep = refharness.mg_solve(cfg)
+print(json.dumps({{"wall": rep.wall_time, "iterations": rep.iterations,
+                   "history": [float(x) for x in rep.residual_history]}}))
+"""
+
+_PORT_CODE = """
+import json, sys
+sys.path.insert(0, {root!r})
+from oracle import coracle, port
+cfg = port.Config({nx}, {ny}, 128, 0.01, {w!r}, 1.0, {lv}, stretch={st!r}, variable_omega={var!r})
+h = coracle.config_hierarchy(cfg)
+f = port.rhs({nx}, {ny}, 128, 0)
+u, rep = h.mg_solve(f, want_u=False)
+print(json.dumps({{"wall": rep.wall_time, "iterations": rep.iterations, "threads": coracle.threads(),
+                   "history": [float(x) for x in rep.residual_history]}}))
+"""
+
+
+def port_solve(prob, one_core=False):
+    code = _PORT_CODE.format(root=ROOT, nx=prob.nx, ny=prob.ny, w=prob.omega2, lv=prob.levels,
+                             st=prob.stretch, var=prob.variable_omega)
+    return _ref_subprocess(code, one_core)
+
+
+def cpu_baseline(prob) -> dict:
+    """The real reference (one core) on a bounded sample; oracle.c on the
+    workload (all threads) and on the sample (one core)."""
+    from paper_1307_2036_b200 import configs
+    sample = configs.Problem(SAMPLE_NX, SAMPLE_NX, 128, 1e-3, 1.0, SAMPLE_LEVELS)
+    sdof = sample.dof
+    out = {"value": None, "unit": "DOF/s", "cores": 1, "kind": "reference",
+           "sample": (f"the reference package itself (panelmg mg_solve via oracle/refharness.py, "
+                      f"SURVEY App. B injection), full MG solve to 1e-5 at {SAMPLE_NX}x"
+                      f"{SAMPLE_NX}x128 ({SAMPLE_LEVELS} levels) -- a bounded sample of the "
+                      "workload (its 2048^2 block needs ~9 min per solve); numpy on one core "
+                      "(taskset -c 0, OPENBLAS_NUM_THREADS=1)")}
+    try:
+        r = _ref_subprocess(_REF_CODE.format(root=ROOT, nx=SAMPLE_NX, lv=SAMPLE_LEVELS), True)
+        out.update(value=sdof / r["wall"], solve_s=r["wall"], iterations=r["iterations"],
+                   residual_history=r["history"])
+    except Exception as err:   # reference not installed on this host
+        out["sample"] += f" -- unavailable: {err}"
+    try:
+        p1 = port_solve(sample, one_core=True)
+        out["port_one_core"] = {"value": sdof / p1["wall"], "solve_s": p1["wall"], "cores": 1,
+                                "iterations": p1["iterations"],
+                                "sample": "oracle/oracle.c, same sample, taskset -c 0, 1 thread"}
+        if out.get("residual_history"):
+            h, g = np.array(p1["history"]), np.array(out["residual_history"])
+            out["port_one_core"]["history_rel_vs_reference"] = (
+                float(np.max(np.abs(h - g) / g)) if h.shape == g.shape else None)
+        pw = port_solve(prob)
+        out["port_workload"] = {"value": prob.dof / pw["wall"], "solve_s": pw["wall"],
+                                "cores": pw["threads"], "iterations": pw["iterations"],
+                                "sample": (f"oracle/oracle.c (C/OpenMP restatement, pinned by "
+                                           f"tests/test_oracle_c.py), full solve of the workload "
+                                           f"{prob.nx}x{prob.ny}x128, all host threads")}
+    except Exception as err:
+        out["port_error"] = str(err)
+    return out
 
 
 def run_reference(args):
-    """--impl reference: rank 0 times the CPU implementation; others exit."""
+    """--impl reference: rank 0 times WHOLE oracle.c solves of the workload."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
+    cfgd, prob, scaling = config_dict(args.workload, world)
     from oracle import coracle, port
-    cfg = port.CONFIGS[1]
-    f = port.rhs(cfg.nx, cfg.ny, cfg.nz, 0)
-    h = coracle.config_hierarchy(cfg)
-    _, full = h.mg_solve(f, want_u=False)          # establishes the cycle count
-    cycles = full.iterations
-    for _ in range(args.warmup):
-        h.mg_solve(f, want_u=False, max_cycles=1)
-    times = []
+    pc = port.Config(prob.nx, prob.ny, prob.nz, prob.depth, prob.omega2, prob.lambda2,
+                     prob.levels, stretch=prob.stretch, variable_omega=prob.variable_omega)
+    h = coracle.config_hierarchy(pc)
+    f = port.rhs(prob.nx, prob.ny, prob.nz, 0)
+    for _ in range(min(args.warmup, 1)):          # page in / first touch
+        h.mg_solve(f, want_u=False)
+    walls, rep = [], None
+    t_all = time.perf_counter()
     for _ in range(args.steps):
-        _, rep = h.mg_solve(f, want_u=False, max_cycles=1)
-        times.append(rep.wall_time)
-    t_cycle = sum(times) / len(times)
-    dof = cfg.nx * cfg.ny * cfg.nz
-    value = dof / (t_cycle * cycles)
+        _, rep = h.mg_solve(f, want_u=False)
+        walls.append(rep.wall_time)
+    t_all = time.perf_counter() - t_all
+    t = sum(walls)
+    value = prob.dof * args.steps / t
+    cores = coracle.threads()
     out = {
-        "metric": "MG solve DOF/s to 1e-5 residual (configs[1] per GPU)", "value": value,
-        "unit": "DOF/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t_cycle * cycles,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: f ~ U[-1,1], default_rng(0)",
-        "config": {"workload": "configs[1] MG solve 1024x1024x128 fp64, 7 levels, V(1,1), "
-                               "eps 1e-5", "levels": LEVELS},
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": coracle.threads(),
-                         "kind": "port",
-                         "sample": (f"oracle/oracle.c, each step one V-cycle + residual at "
-                                    f"full configs[1] size; solve = {cycles} cycles "
-                                    f"(full reference solve {full.wall_time:.2f} s)")},
+        "metric": METRIC, "value": value, "unit": "DOF/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: f ~ U[-1,1] from default_rng(0), global (i,j,k) order",
+        "config": cfgd,
+        "iterations": rep.iterations,
+        "residual_history": [float(x) for x in rep.residual_history],
+        "timed_wall_s": t_all,
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
+                         "sample": (f"{args.steps} whole MG solves of the workload by "
+                                    "oracle/oracle.c (C/OpenMP restatement of the reference, "
+                                    "reference op order, pinned to the reference's outputs by "
+                                    "tests/test_oracle_c.py), all host threads; "
+                                    f"{min(args.warmup, 1)} untimed warm-up solve")},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
 
 
 def time_kernel(fn, reps, torch):
@@ -233,181 +368,270 @@ def time_kernel(fn, reps, torch):
     return e0.elapsed_time(e1) / reps * 1e-3
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=32)
-    args = ap.parse_args()
-    if args.impl == "reference":
-        return run_reference(args)
+class Setup:
+    """Hierarchy, decomposition and this rank's f block for a Problem."""
 
-    import torch
-    world, rank, local = dist_setup(args.gpus)
+    def __init__(self, prob, px, py, world):
+        import paper_1307_2036_b200 as pmg
+        from paper_1307_2036_b200 import configs
+        from paper_1307_2036_b200.partition import scatter_block
+        self.prob = prob
+        cfg = prob.mg_config()
+        self.cfg = cfg
+        dec = pmg.Decomposition(prob.nx, world, ny=prob.ny, px=px, py=py)
+        self.hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg, dec)
+        self.lay = lay = self.hier.fine.layout
+        (self.w,) = lay.local_workers
+        i0, j0 = lay.origin(self.w)
+        self.block = configs.rhs_block(prob.nx, prob.ny, prob.nz, i0, j0, lay.mx, lay.my, 0)
+        self.f = scatter_block(self.block, lay)
+        self.dof_local = lay.mx * lay.my * prob.nz
+        self.u = pmg.DistField.zeros(lay, prob.nz)
+
+
+def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
     import paper_1307_2036_b200 as pmg
-    from paper_1307_2036_b200 import _lib, configs
-    from paper_1307_2036_b200.partition import scatter_block
-
-    px = PX[world]
-    py = world // px
-    nxg, nyg = NX_PER_GPU * px, NX_PER_GPU * py
-    prob = configs.Problem(nxg, nyg, NZ, 1e-3, 1.0, LEVELS)
-    grid, params = prob.grid(), prob.params()
-    cfg = prob.mg_config()
-    dec = pmg.Decomposition(nxg, world, ny=nyg, px=px, py=py)
-    hier = pmg.build_hierarchy(grid, params, cfg, dec)
-    lay = hier.fine.layout
-    (w,) = lay.local_workers
-    i0, j0 = lay.origin(w)
-    mx, my = lay.mx, lay.my
-    block = configs.rhs_block(nxg, nyg, NZ, i0, j0, mx, my, 0)
-    f = scatter_block(block, lay)
-    dof_local = mx * my * NZ
-    dof = nxg * nyg * NZ
+    from paper_1307_2036_b200 import _lib
+    from paper_1307_2036_b200 import multigrid as mgm
     lib = _lib.load()
-
-    # ---- device-resident solves --------------------------------------------
     reps = []
-    u = pmg.DistField.zeros(lay, NZ)        # iterate buffer reused by every solve
-    for _ in range(max(1, args.warmup)):    # (graphs are captured for (f, u) here)
-        u, rep = pmg.mg_solve(f, hier, cfg, out=u)
+    for _ in range(max(1, warmup)):          # graphs are captured for (f, u) here
+        s.u, rep = pmg.mg_solve(s.f, s.hier, s.cfg, out=s.u)
         reps.append(rep)
     torch.cuda.synchronize()
     barrier(world)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    native = s.lay.px == 1 and s.lay.py == 1 and mgm.USE_NATIVE
+    r0_graph = s.hier.native(s.cfg).replayed_launches() if native else 0
     l0 = lib.pmg_launch_count()
-    from paper_1307_2036_b200 import multigrid as mgm
-    native = lay.px == 1 and lay.py == 1 and mgm.USE_NATIVE
-    r0_graph = hier.native(cfg).replayed_launches() if native else 0
-    sampler = ClockSampler(local)
     iters = []
-    with sampler:
+    ctx = sampler if sampler is not None else _Null()
+    with ctx:
         torch.cuda.synchronize()
         e0.record(st)
-        for _ in range(args.steps):
-            u, rep = pmg.mg_solve(f, hier, cfg, out=u)
+        for _ in range(steps):
+            s.u, rep = pmg.mg_solve(s.f, s.hier, s.cfg, out=s.u)
             iters.append(rep.iterations)
         e1.record(st)
         torch.cuda.synchronize()
     barrier(world)
-    t_local = e0.elapsed_time(e1) * 1e-3
-    t = max_over_ranks(t_local, world)
-    launches_lib = lib.pmg_launch_count() - l0
-    # kernels replayed from the captured V-cycle graphs (first cycle + the rest)
-    gpu_launches = launches_lib
+    t = max_over_ranks(e0.elapsed_time(e1) * 1e-3, world)
+    launches = lib.pmg_launch_count() - l0
     if native:
-        # single part: the C++ driver counts the kernels of its graph replays
-        gpu_launches += hier.native(cfg).replayed_launches() - r0_graph
+        launches += s.hier.native(s.cfg).replayed_launches() - r0_graph
     else:
-        gkey = mgm.graph_key(cfg, f, u)
-        g_first = hier._graphs.get(gkey + (True,))
-        g_rest = hier._graphs.get(gkey + (False,))
+        gkey = mgm.graph_key(s.cfg, s.f, s.u)
+        g_first = s.hier._graphs.get(gkey + (True,))
+        g_rest = s.hier._graphs.get(gkey + (False,))
         for n_it in iters:
             if g_first is not None:
-                gpu_launches += g_first.launches + (n_it - 1) * g_rest.launches
+                launches += g_first.launches + (n_it - 1) * g_rest.launches
             elif g_rest is not None:
-                gpu_launches += n_it * g_rest.launches
-    value = dof * args.steps / t
+                launches += n_it * g_rest.launches
+    return {"t": t, "solve_ms": t / steps * 1e3, "iterations": iters[-1],
+            "v_cycle_ms": t / sum(iters) * 1e3, "dof_s": s.prob.dof * steps / t,
+            "residual_history": [float(x) for x in reps[-1].residual_history],
+            "launches": int(launches)}
 
-    # ---- dominant kernel: fine-level half-sweep (12 B per fine cell) ---------
-    fine = hier.fine
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def fine_kernels(s: Setup, torch):
+    """CUDA-event times of the fine-level kernels of the solve:
+    band half-sweep (the dominant kernel), fused-residual red sweep, red-only
+    residual restriction, black-only prolongation."""
+    import ctypes as C
+    from paper_1307_2036_b200 import _lib
+    from paper_1307_2036_b200 import multigrid as mgmod
+    lib = _lib.load()
+    hier, w = s.hier, s.w
+    fine, coarse = hier.fine, hier.levels[1]
     scratch = hier.persistent_scratch()
     s0 = scratch[0]
-    n_fine = dof_local
     flip = [0]
 
     def hs():
         fine.smoother.half_sweep(s0.u, s0.f, flip[0] & 1, 1.0)
         flip[0] += 1
 
+    out = {}
     t_hs = time_kernel(hs, 20, torch)
-    kern = {}
-    coarse = hier.levels[1]
-    from paper_1307_2036_b200 import multigrid as mgmod
-    import ctypes as C
-    # the fine-level kernels of the solve: fused-residual red sweep, red-only
-    # residual restriction, black-only prolongation (DESIGN.md sections 3-4)
-    part = s0.u.parts[w]
     hh = fine.op.handles[w].h
+    part = s0.u.parts[w]
     scr = torch.empty(int(lib.pmg_partials_size()), dtype=torch.float64, device="cuda")
     res = torch.zeros(1, dtype=torch.float64, device="cuda")
-    t_res = time_kernel(lambda: lib.pmg_half_sweep_res(
-        hh, part.ptr, s0.r.parts[w].ptr, s0.f.parts[w].ptr, C.c_void_p(scr.data_ptr()),
-        C.c_void_p(res.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream)),
-        10, torch)
-    t_rr = time_kernel(lambda: mgmod._residual_restrict(fine, coarse, s0.f, s0.u,
-                                                        scratch[1].f, True), 10, torch)
-    t_pa = time_kernel(lambda: mgmod._prolong_add(scratch[1].u, coarse, fine, s0.u,
-                                                  black_only=True), 10, torch)
-    for name, tt, b in (("half_sweep", t_hs, 12), ("half_sweep_res", t_res, 16),
-                        ("residual_restrict_red", t_rr, 14), ("prolong_black", t_pa, 10)):
-        kern[name] = {"ms": tt * 1e3, "alg_bytes_per_cell": b,
-                      "GB_s": b * n_fine / tt / 1e9}
-    peak, peak_src = measured_peak()
-    ach = 12 * n_fine / t_hs / 1e9
-    traffic = ncu_traffic("k_half_sweep_band")
-    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": traffic,
-                "kernel": "k_half_sweep_band (fine level, TMA-fed line relaxation)",
-                "alg_bytes_per_launch": 12 * n_fine, "launch_ms": t_hs * 1e3,
-                "peak_source": peak_src}
+    times = {"half_sweep": (t_hs, 12)}
+    if s.lay.px == 1 and s.lay.py == 1 and lib.pmg_half_sweep_res_ok(hh):
+        times["half_sweep_res"] = (time_kernel(lambda: lib.pmg_half_sweep_res(
+            hh, part.ptr, s0.r.parts[w].ptr, s0.f.parts[w].ptr, C.c_void_p(scr.data_ptr()),
+            C.c_void_p(res.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream)),
+            10, torch), 16)
+    times["residual_restrict_red"] = (time_kernel(lambda: mgmod._residual_restrict(
+        fine, coarse, s0.f, s0.u, scratch[1].f, True), 10, torch), 14)
+    times["prolong_black"] = (time_kernel(lambda: mgmod._prolong_add(
+        scratch[1].u, coarse, fine, s0.u, black_only=True), 10, torch), 10)
+    for name, (tt, b) in times.items():
+        out[name] = {"ms": tt * 1e3, "alg_bytes_per_cell": b,
+                     "GB_s": b * s.dof_local / tt / 1e9}
+    return out
 
-    # ---- end to end through the public API with host buffers -----------------
-    # pinned host f in, pinned host u out, every step; SolvePipeline overlaps
-    # step i+1's upload and step i-1's download with step i's solve
+
+def e2e_legs(s: Setup, steps, world, torch):
+    """Serial host-to-host solves (the headline e2e) and the pipelined
+    stream of solves, both through SolvePipeline (the public API)."""
     from paper_1307_2036_b200.pipeline import SolvePipeline
-    ne = max(2, args.e2e_steps)
-    f_host = torch.from_numpy(block).pin_memory()
-    # two pinned result buffers, reused every other step (a D2H into a buffer
-    # is stream-ordered after the previous one out of it)
-    u_bufs = [torch.empty(dof_local, dtype=torch.float64).pin_memory() for _ in range(2)]
-    u_hosts = [u_bufs[i % 2] for i in range(ne)]
-    pipe = SolvePipeline(hier, cfg, NZ)
-    pipe.run([f_host] * 2, u_hosts[:2])                 # warm-up (graph capture)
+    ne = max(2, steps)
+    f_host = torch.from_numpy(s.block).pin_memory()
+    u_bufs = [torch.empty(s.dof_local, dtype=torch.float64).pin_memory() for _ in range(2)]
+    pipe = SolvePipeline(s.hier, s.cfg, s.prob.nz)
+    pipe.run([f_host] * 2, u_bufs)                      # warm-up (graph capture)
+    # serial: every step uploads, solves, downloads; nothing overlaps steps
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    reps_e = pipe.run([f_host] * ne, u_hosts)
+    reps_s = []
+    for i in range(ne):
+        reps_s += pipe.run([f_host], [u_bufs[i % 2]])
     torch.cuda.synchronize()
-    te = max_over_ranks(time.perf_counter() - t0, world)
-    ok = all(r.iterations == iters[-1] for r in reps_e)
-    e2e = {"value": dof * ne / te, "unit": "DOF/s", "h2d_bytes_per_step": 8 * dof_local,
-           "d2h_bytes_per_step": 8 * dof_local + 8 * (reps_e[-1].iterations + 1),
-           "ms_per_step": te / ne * 1e3, "steps": ne, "same_iterations": ok,
-           "path": "SolvePipeline.run: pinned host f -> H2D + layout kernel -> mg_solve -> "
-                   "layout kernel + D2H -> pinned host u, every step; transfers of "
-                   "neighbouring steps overlap the solve (double buffered)"}
+    ts = max_over_ranks(time.perf_counter() - t0, world)
+    # pipelined: step i+1's upload and step i-1's download overlap step i
+    barrier(world)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    reps_p = pipe.run([f_host] * ne, [u_bufs[i % 2] for i in range(ne)])
+    torch.cuda.synchronize()
+    tp = max_over_ranks(time.perf_counter() - t0, world)
+    dof = s.prob.dof
+    it = reps_s[-1].iterations
+    ok = all(r.iterations == it for r in reps_s + reps_p)
+    e2e = {"value": dof * ne / ts, "unit": "DOF/s", "h2d_bytes_per_step": 8 * s.dof_local,
+           "d2h_bytes_per_step": 8 * s.dof_local + 8 * (it + 1),
+           "ms_per_step": ts / ne * 1e3, "steps": ne, "same_iterations": ok,
+           "path": ("SolvePipeline.run with one step per call: pinned host f -> H2D + layout "
+                    "kernel -> mg_solve -> layout kernel + D2H -> pinned host u; no overlap "
+                    "between steps (a dependent time-step sequence)"),
+           "pipelined": {"value": dof * ne / tp, "ms_per_step": tp / ne * 1e3, "steps": ne,
+                         "path": ("SolvePipeline.run over all steps: step i+1's upload and "
+                                  "step i-1's download overlap step i's solve (independent "
+                                  "right-hand sides only)")}}
+    return e2e
+
+
+def extra_configs(torch):
+    """N = 1 companions: configs[1] MG, configs[2] omega2 sweep (CG and MG),
+    configs[4] MG -- device-resident f, CUDA events, same rules."""
+    import paper_1307_2036_b200 as pmg
+    from paper_1307_2036_b200 import configs
+    out = {}
+    s = Setup(configs.config(1), 1, 1, 1)
+    r = time_solves(s, 10, 3, 1, torch)
+    out["config1_mg"] = {k: r[k] for k in ("solve_ms", "v_cycle_ms", "iterations", "dof_s",
+                                           "residual_history")}
+    sweep = {}
+    st = torch.cuda.current_stream()
+    for w in (1e-4, 1e-3, 1e-2, 1e-1):
+        prob = configs.config(2, omega2=w)
+        ent = {}
+        s2 = Setup(prob, 1, 1, 1) if w != 1e-3 else s
+        r = time_solves(s2, 5, 2, 1, torch)
+        ent["mg"] = {"solve_ms": r["solve_ms"], "iterations": r["iterations"]}
+        op = s2.hier.fine.op
+        pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+        pmg.pcg_solve(s2.f, op, pre, eps=1e-5, maxiter=2000)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        n = 3
+        for _ in range(n):
+            _, rep = pmg.pcg_solve(s2.f, op, pre, eps=1e-5, maxiter=2000)
+        e1.record(st)
+        torch.cuda.synchronize()
+        tc = e0.elapsed_time(e1) / n
+        ent["cg"] = {"solve_ms": tc, "iterations": rep.iterations,
+                     "ms_per_iteration": tc / rep.iterations,
+                     "residual_history": [float(x) for x in rep.residual_history]}
+        sweep[f"{w:g}"] = ent
+        if s2 is not s:
+            del s2
+    out["config2_sweep"] = sweep
+    del s
+    torch.cuda.empty_cache()
+    s4 = Setup(configs.config(4), 1, 1, 1)
+    r = time_solves(s4, 3, 2, 1, torch)
+    out["config4_mg"] = {k: r[k] for k in ("solve_ms", "v_cycle_ms", "iterations", "dof_s",
+                                           "residual_history")}
+    del s4
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config3", choices=["config3", "config4", "config1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=12)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world, rank, local = dist_setup(args.gpus)
+    cfgd, prob, scaling = config_dict(args.workload, world)
+    px = PX[world]
+    s = Setup(prob, px, world // px, world)
+
+    sampler = ClockSampler(local)
+    r = time_solves(s, args.steps, args.warmup, world, torch, sampler)
+    cfgd["iterations"] = r["iterations"]
+
+    kern = fine_kernels(s, torch)
+    peak, peak_src = measured_peak()
+    t_hs = kern["half_sweep"]["ms"] * 1e-3
+    ach = 12 * s.dof_local / t_hs / 1e9
+    nxl = s.lay.mx
+    traffic, tsrc = ncu_traffic("k_half_sweep_band", nxl)
+    roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic,
+                "kernel": f"k_half_sweep_band (fine level {nxl}x{s.lay.my}x128, TMA-fed line "
+                          "relaxation)",
+                "alg_bytes_per_launch": 12 * s.dof_local, "launch_ms": t_hs * 1e3,
+                "peak_source": peak_src, "traffic_source": tsrc}
+
+    e2e = e2e_legs(s, args.e2e_steps, world, torch)
+    del s
+    torch.cuda.empty_cache()
+    extra = extra_configs(torch) if (world == 1 and not args.no_extra) else None
 
     if rank != 0:
         return
     out = {
-        "metric": "MG solve DOF/s to 1e-5 residual (configs[1] per GPU)",
-        "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: f ~ U[-1,1] from default_rng(0), global (i,j,k) order",
-        "config": {"workload": "configs[1] MG solve 1024x1024x128 fp64 per GPU, 7 levels, "
-                               "V(1,1), rho 1, coarse_sweeps 1, eps 1e-5",
-                   "global_grid": [nxg, nyg, NZ], "levels": LEVELS,
-                   "parallelism": f"{px}x{py} horizontal domain decomposition",
-                   "iterations": iters[-1], "l2": "inputs larger than L2 (1.09 GB/field)"},
-        "solve_ms": t / args.steps * 1e3,
-        "v_cycle_ms": t / sum(iters) * 1e3,
-        "residual_history": reps[-1].residual_history if reps else None,
+        "metric": METRIC, "value": r["dof_s"], "unit": "DOF/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["solve_ms"],
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: f ~ U[-1,1] from default_rng(0), global (i,j,k) order, per-rank block",
+        "config": cfgd,
+        "solve_ms": r["solve_ms"], "v_cycle_ms": r["v_cycle_ms"],
+        "residual_history": r["residual_history"],
         "roofline": roofline, "kernels": kern, "e2e": e2e,
-        "gpu_launches": int(gpu_launches),
+        "gpu_launches": r["launches"],
         "clocks": sampler.summary(),
     }
+    if extra is not None:
+        out["extra"] = extra
     if world == 1 and not args.no_cpu_baseline:
-        try:
-            out["cpu_baseline"] = cpu_baseline_sample()
-        except Exception as err:  # the oracle library may be missing
-            out["cpu_baseline"] = {"value": None, "unit": "DOF/s", "cores": 0, "kind": "port",
-                                   "sample": f"unavailable: {err}"}
+        out["cpu_baseline"] = cpu_baseline(prob)
     print(json.dumps(out), flush=True)
 
 

@@ -32,6 +32,9 @@ def lib():
         L = C.CDLL(LIB)
         L.or_hier_create.restype = C.c_void_p
         L.or_hier_create.argtypes = [C.c_int, C.POINTER(LevelDesc), C.c_int, C.c_int]
+        L.or_hier_create_lean.restype = C.c_void_p
+        L.or_hier_create_lean.argtypes = [C.c_int, C.POINTER(LevelDesc), C.c_int, C.c_int,
+                                          C.c_int]
         L.or_hier_destroy.argtypes = [C.c_void_p]
         L.or_threads.restype = C.c_int
         P = C.c_void_p
@@ -57,7 +60,8 @@ def threads() -> int:
 class Hierarchy:
     """C oracle hierarchy built from oracle.port factor functions."""
 
-    def __init__(self, nx, ny, nlev, factor_fn, omega2, lambda2, periodic=(True, True)):
+    def __init__(self, nx, ny, nlev, factor_fn, omega2, lambda2, periodic=(True, True),
+                 lean=False):
         self._keep = []
         descs = (LevelDesc * nlev)()
         self.nx, self.ny = nx, ny
@@ -72,7 +76,9 @@ class Hierarchy:
             self.nz = fac.nz
             nx //= 2
             ny //= 2
-        self.h = lib().or_hier_create(nlev, descs, int(periodic[0]), int(periodic[1]))
+        # lean: no N-sized coefficient caches (recomputed per column, same values)
+        self.h = lib().or_hier_create_lean(nlev, descs, int(periodic[0]), int(periodic[1]),
+                                           int(bool(lean)))
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -155,6 +161,6 @@ class Hierarchy:
         return out
 
 
-def config_hierarchy(cfg: "port.Config", nlev=None):
+def config_hierarchy(cfg: "port.Config", nlev=None, lean=False):
     return Hierarchy(cfg.nx, cfg.ny, cfg.levels if nlev is None else nlev, cfg.factor_fn(),
-                     cfg.omega2, cfg.lambda2)
+                     cfg.omega2, cfg.lambda2, lean=lean)

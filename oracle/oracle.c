@@ -34,9 +34,10 @@ typedef struct {
 typedef struct {
     int nx, ny, nz;
     double omega2, vcoef;
-    double *wx, *wy, *av, *sumw;
-    double *dr, *vprof, *drw;
-    double *diag3, *vband, *invd; /* (nx, ny, nz), (nx, ny, nz-1), (nx, ny, nz) */
+    double *wx, *wy, *av, *sumw, *vh;
+    double *dr, *vprof, *volprof, *drw;
+    double *diag3, *vband, *invd; /* (nx, ny, nz), (nx, ny, nz-1), (nx, ny, nz);
+                                     NULL in lean mode (recomputed per column) */
     double *u, *f, *r;            /* scratch fields with halo */
 } level_t;
 
@@ -44,6 +45,12 @@ typedef struct {
     int nlev, px, py;
     level_t *lv;
 } hier_t;
+
+#define OR_MAXT 512
+static int or_nthreads(void) {
+    const int n = omp_get_max_threads();
+    return n < OR_MAXT ? n : OR_MAXT;
+}
 
 #define IDX(L, i, j, k) ((((size_t)(i)) * ((L)->ny + 2) + (size_t)(j)) * (L)->nz + (size_t)(k))
 
@@ -55,7 +62,27 @@ static double *dup(const double *a, size_t n) {
     return b;
 }
 
-static void level_init(level_t *L, const or_level_desc *d) {
+/* diag3 / vband / invd of column q (stencil.py:105-109, stencil.py:79-81,
+ * smoother.py:93-99), in the reference's expression order */
+static void column_coefs(const level_t *L, size_t q, double *dg, double *vb, double *iv) {
+    const int nz = L->nz;
+    const double vh = L->vh[q], osw = L->omega2 * L->sumw[q], cv = L->vcoef * L->av[q];
+    for (int k = 0; k < nz; ++k) {
+        const double t1 = vh * L->volprof[k];
+        const double t2 = osw * L->dr[k];
+        const double t3 = cv * (L->vprof[k] + L->vprof[k + 1]);
+        dg[k] = (t1 + t2) + t3;
+    }
+    for (int k = 1; k < nz; ++k) vb[k - 1] = cv * L->vprof[k];
+    iv[0] = 1.0 / dg[0];
+    for (int k = 1; k < nz; ++k) {
+        const double sk = L->vprof[k] * cv;
+        const double m = (sk * sk) * iv[k - 1];
+        iv[k] = 1.0 / (dg[k] - m);
+    }
+}
+
+static void level_init(level_t *L, const or_level_desc *d, int lean) {
     const int nx = d->nx, ny = d->ny, nz = d->nz;
     L->nx = nx; L->ny = ny; L->nz = nz;
     L->omega2 = d->omega2; L->vcoef = d->vcoef;
@@ -65,32 +92,25 @@ static void level_init(level_t *L, const or_level_desc *d) {
     L->sumw = dup(d->sumw, (size_t)nx * ny);
     L->dr = dup(d->dr, nz);
     L->vprof = dup(d->vprof, nz + 1);
+    L->vh = dup(d->vh, (size_t)nx * ny);
+    L->volprof = dup(d->volprof, nz);
     L->drw = (double *)malloc(nz * sizeof(double));
     for (int k = 0; k < nz; ++k) L->drw[k] = d->omega2 * d->dr[k];
     const size_t N = (size_t)nx * ny * nz;
-    L->diag3 = (double *)malloc(N * sizeof(double));
-    L->vband = (double *)malloc((size_t)nx * ny * (nz > 1 ? nz - 1 : 1) * sizeof(double));
-    L->invd = (double *)malloc(N * sizeof(double));
+    L->diag3 = L->vband = L->invd = NULL;
+    if (!lean) {
+        /* the reference's N-sized caches (stencil.py:90-114, smoother.py:56-99) */
+        L->diag3 = (double *)malloc(N * sizeof(double));
+        L->vband = (double *)malloc((size_t)nx * ny * (nz > 1 ? nz - 1 : 1) * sizeof(double));
+        L->invd = (double *)malloc(N * sizeof(double));
 #pragma omp parallel for schedule(static)
-    for (int i = 0; i < nx; ++i)
-        for (int j = 0; j < ny; ++j) {
-            const size_t q = (size_t)i * ny + j;
-            const double vh = d->vh[q], osw = d->omega2 * d->sumw[q], cv = d->vcoef * d->av[q];
-            double *dg = L->diag3 + q * nz, *iv = L->invd + q * nz;
-            for (int k = 0; k < nz; ++k) {
-                const double t1 = vh * d->volprof[k];
-                const double t2 = osw * d->dr[k];
-                const double t3 = cv * (d->vprof[k] + d->vprof[k + 1]);
-                dg[k] = (t1 + t2) + t3;
+        for (int i = 0; i < nx; ++i)
+            for (int j = 0; j < ny; ++j) {
+                const size_t q = (size_t)i * ny + j;
+                column_coefs(L, q, L->diag3 + q * nz, L->vband + q * (nz > 1 ? nz - 1 : 1),
+                             L->invd + q * nz);
             }
-            for (int k = 1; k < nz; ++k) L->vband[q * (nz - 1) + (k - 1)] = cv * d->vprof[k];
-            iv[0] = 1.0 / dg[0];
-            for (int k = 1; k < nz; ++k) {
-                const double sk = d->vprof[k] * cv;
-                const double m = (sk * sk) * iv[k - 1];
-                iv[k] = 1.0 / (dg[k] - m);
-            }
-        }
+    }
     L->u = (double *)calloc(fsize(L), sizeof(double));
     L->f = (double *)calloc(fsize(L), sizeof(double));
     L->r = (double *)calloc(fsize(L), sizeof(double));
@@ -98,6 +118,7 @@ static void level_init(level_t *L, const or_level_desc *d) {
 
 static void level_free(level_t *L) {
     free(L->wx); free(L->wy); free(L->av); free(L->sumw); free(L->dr); free(L->vprof);
+    free(L->vh); free(L->volprof);
     free(L->drw); free(L->diag3); free(L->vband); free(L->invd);
     free(L->u); free(L->f); free(L->r);
 }
@@ -121,8 +142,15 @@ static void halo(const level_t *L, double *d, int px, int py) {
 static double apply_op(const level_t *L, const double *u, const double *f, double *out,
                        int norm) {
     const int nx = L->nx, ny = L->ny, nz = L->nz;
+    double part[OR_MAXT];
+    int nt = 1;
+#pragma omp parallel num_threads(or_nthreads())
+    {
+    const int t = omp_get_thread_num();
+    if (t == 0) nt = omp_get_num_threads();
     double s2 = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : s2)
+    double *cb = L->diag3 ? NULL : (double *)malloc(3 * (size_t)nz * sizeof(double));
+#pragma omp for schedule(static)
     for (int i = 0; i < nx; ++i)
         for (int j = 0; j < ny; ++j) {
             const size_t q = (size_t)i * ny + j;
@@ -131,7 +159,15 @@ static double apply_op(const level_t *L, const double *u, const double *f, doubl
             const double *uc = u + IDX(L, i + 1, j + 1, 0);
             const double *uw = u + IDX(L, i, j + 1, 0), *ue = u + IDX(L, i + 2, j + 1, 0);
             const double *us = u + IDX(L, i + 1, j, 0), *un = u + IDX(L, i + 1, j + 2, 0);
-            const double *dg = L->diag3 + q * nz, *vb = L->vband + q * (nz - 1);
+            const double *dg, *vb;
+            if (cb) {
+                column_coefs(L, q, cb, cb + nz, cb + 2 * nz);
+                dg = cb;
+                vb = cb + nz;
+            } else {
+                dg = L->diag3 + q * nz;
+                vb = L->vband + q * (nz - 1);
+            }
             double *o = out ? out + IDX(L, i + 1, j + 1, 0) : NULL;
             const double *fc = f ? f + IDX(L, i + 1, j + 1, 0) : NULL;
             for (int k = 0; k < nz; ++k) {
@@ -148,6 +184,11 @@ static double apply_op(const level_t *L, const double *u, const double *f, doubl
                 if (norm) s2 += res * res;
             }
         }
+    free(cb);
+    part[t] = s2;
+    }
+    double s2 = 0.0;
+    for (int t = 0; t < nt; ++t) s2 += part[t];
     return s2;
 }
 
@@ -159,13 +200,20 @@ static void half_sweep(const level_t *L, double *u, const double *f, int color, 
 #pragma omp parallel
     {
         double *g = (double *)malloc(nz * sizeof(double));
+        double *cb = L->invd ? NULL : (double *)malloc(3 * (size_t)nz * sizeof(double));
 #pragma omp for schedule(static)
         for (int i = 0; i < nx; ++i)
             for (int j = 0; j < ny; ++j) {
                 if (((i + j) & 1) != color) continue;
                 const size_t q = (size_t)i * ny + j;
                 const double cv = L->vcoef * L->av[q];
-                const double *iv = L->invd + q * nz;
+                const double *iv;
+                if (cb) {
+                    column_coefs(L, q, cb, cb + nz, cb + 2 * nz);
+                    iv = cb + 2 * nz;
+                } else {
+                    iv = L->invd + q * nz;
+                }
                 const double *fc = f + IDX(L, i + 1, j + 1, 0);
                 double *uc = u + IDX(L, i + 1, j + 1, 0);
                 if (nbr_zero) {
@@ -209,6 +257,7 @@ static void half_sweep(const level_t *L, double *u, const double *f, int color, 
                 memcpy(uc, g, nz * sizeof(double));
             }
         free(g);
+        free(cb);
     }
 }
 
@@ -281,16 +330,31 @@ static void v_cycle(hier_t *H, int c, int nu_pre, int nu_post, int ncs, double r
     }
 }
 
-static double norm2_owned(const level_t *L, const double *a) {
+/* owned-cell dot product: per-thread partials over static row blocks,
+ * added in thread order, so the sum does not depend on the OpenMP runtime's
+ * reduction order (bit-reproducible from run to run) */
+static double dot_owned(const level_t *L, const double *a, const double *b) {
+    double part[OR_MAXT];
+    int nt = 1;
+#pragma omp parallel num_threads(or_nthreads())
+    {
+        const int t = omp_get_thread_num();
+        if (t == 0) nt = omp_get_num_threads();
+        double s = 0.0;
+#pragma omp for schedule(static)
+        for (int i = 0; i < L->nx; ++i)
+            for (int j = 0; j < L->ny; ++j) {
+                const size_t o = IDX(L, i + 1, j + 1, 0);
+                for (int k = 0; k < L->nz; ++k) s += a[o + k] * b[o + k];
+            }
+        part[t] = s;
+    }
     double s = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : s)
-    for (int i = 0; i < L->nx; ++i)
-        for (int j = 0; j < L->ny; ++j) {
-            const double *p = a + IDX(L, i + 1, j + 1, 0);
-            for (int k = 0; k < L->nz; ++k) s += p[k] * p[k];
-        }
+    for (int t = 0; t < nt; ++t) s += part[t];
     return s;
 }
+
+static double norm2_owned(const level_t *L, const double *a) { return dot_owned(L, a, a); }
 
 static double now(void) {
     struct timespec ts;
@@ -316,14 +380,21 @@ static void store_owned(const level_t *L, const double *d, double *dst) {
 
 int or_threads(void) { return omp_get_max_threads(); }
 
-void *or_hier_create(int nlev, const or_level_desc *d, int px, int py) {
+/* lean != 0: no N-sized coefficient caches; diag3 / vband / invd are
+ * recomputed per column with the same expressions (identical values, about
+ * half the memory: the configs[4] parity check at 4096^2 x 128) */
+void *or_hier_create_lean(int nlev, const or_level_desc *d, int px, int py, int lean) {
     hier_t *H = (hier_t *)calloc(1, sizeof(hier_t));
     H->nlev = nlev;
     H->px = px;
     H->py = py;
     H->lv = (level_t *)calloc(nlev, sizeof(level_t));
-    for (int c = 0; c < nlev; ++c) level_init(&H->lv[c], &d[c]);
+    for (int c = 0; c < nlev; ++c) level_init(&H->lv[c], &d[c], lean);
     return H;
+}
+
+void *or_hier_create(int nlev, const or_level_desc *d, int px, int py) {
+    return or_hier_create_lean(nlev, d, px, py, 0);
 }
 
 void or_hier_destroy(void *h) {
@@ -404,12 +475,7 @@ int or_pcg_solve(void *h, const double *f, double *u_out, double eps, int maxite
         double kappa = 0.0;
         {
             double s = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : s)
-            for (int i = 0; i < L->nx; ++i)
-                for (int j = 0; j < L->ny; ++j) {
-                    const size_t o = IDX(L, i + 1, j + 1, 0);
-                    for (int k = 0; k < L->nz; ++k) s += r[o + k] * z[o + k];
-                }
+            s = dot_owned(L, r, z);
             kappa = s;
         }
         if (kappa <= 0.0) { rc = -3; goto done; }
@@ -417,12 +483,7 @@ int or_pcg_solve(void *h, const double *f, double *u_out, double eps, int maxite
         for (int it = 1; it <= nmax; ++it) {
             apply_op(L, p, NULL, q, 0);
             double pq = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : pq)
-            for (int i = 0; i < L->nx; ++i)
-                for (int j = 0; j < L->ny; ++j) {
-                    const size_t o = IDX(L, i + 1, j + 1, 0);
-                    for (int k = 0; k < L->nz; ++k) pq += p[o + k] * q[o + k];
-                }
+            pq = dot_owned(L, p, q);
             if (pq <= 0.0) { rc = -3; goto done; }
             const double alpha = kappa / pq, malpha = -alpha;
 #pragma omp parallel for schedule(static)
@@ -436,12 +497,7 @@ int or_pcg_solve(void *h, const double *f, double *u_out, double eps, int maxite
             if (rn / r0 < eps) { *converged = 1; break; }
             SSOR(z, r);
             double kn = 0.0;
-#pragma omp parallel for schedule(static) reduction(+ : kn)
-            for (int i = 0; i < L->nx; ++i)
-                for (int j = 0; j < L->ny; ++j) {
-                    const size_t o = IDX(L, i + 1, j + 1, 0);
-                    for (int k = 0; k < L->nz; ++k) kn += r[o + k] * z[o + k];
-                }
+            kn = dot_owned(L, r, z);
             if (kn <= 0.0) { rc = -3; goto done; }
             const double beta = kn / kappa;
 #pragma omp parallel for schedule(static)

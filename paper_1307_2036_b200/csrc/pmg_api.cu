@@ -17,6 +17,7 @@
 namespace pmg {
 extern std::atomic<long long> g_launches;
 extern int g_smoother_exact;
+extern int g_mode_gen;
 cudaError_t launch_apply(const Lvl &, const double *, const double *, double *, int, double *,
                          int *, cudaStream_t);
 cudaError_t launch_finalize(const double *, int, double *, cudaStream_t);
@@ -158,6 +159,7 @@ int pmg_version(void) { return 1; }
 
 int pmg_set_smoother_mode(int mode) {
     if (mode < 0 || mode > 1) return fail(PMG_ERR_VALUE, "smoother mode must be 0 (fast) or 1 (exact)");
+    if (pmg::g_smoother_exact != mode) ++pmg::g_mode_gen;   // cached graphs / views go stale
     pmg::g_smoother_exact = mode;
     return PMG_OK;
 }

@@ -21,6 +21,7 @@
 #include "../../include/pmg.h"
 
 namespace pmg {
+extern int g_mode_gen;
 int set_error(int code, const char *msg);
 pmg_level *level_view(const pmg_level *lv, long long cstride, int hflags_or = 0);
 void level_view_free(pmg_level *v);
@@ -83,6 +84,7 @@ struct pmg_hier {
     // on this stream, ordered after / before the caller's work by events
     cudaStream_t own = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    int mode_gen = 0;                // pmg::g_mode_gen the graphs / views were made under
 };
 
 namespace {
@@ -102,6 +104,18 @@ void free_hier(pmg_hier *h) {
     if (h->ev_in) cudaEventDestroy(h->ev_in);
     if (h->ev_out) cudaEventDestroy(h->ev_out);
     delete h;
+}
+
+// graphs and wrap views record the kernel variants of the smoother mode
+// they were made under: drop them when the mode has changed since
+void sync_mode(pmg_hier *h) {
+    if (h->mode_gen == pmg::g_mode_gen) return;
+    for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+    h->graphs.clear();
+    for (auto *v : h->wv)
+        if (v) pmg::level_view_free(v);
+    h->wv.clear();
+    h->mode_gen = pmg::g_mode_gen;
 }
 
 // the fine level seen through `view` (lagged norm: red array elsewhere)
@@ -412,6 +426,7 @@ long long pmg_hier_graph_launches(const pmg_hier *h, const double *f, const doub
 
 int pmg_vcycle(pmg_hier *h, double *u, const double *f, int first, void *stream) {
     if (!h || !u || !f) return err(PMG_ERR_VALUE, "null argument");
+    sync_mode(h);
     if (first && !(h->d.rho == 1.0 && h->lv.size() > 1 && h->d.nu_pre >= 1))
         return err(PMG_ERR_VALUE, "first = 1 needs rho = 1, nu_pre >= 1 and two levels");
     return vcycle(h, 0, u, f, first != 0, (cudaStream_t)stream);
@@ -544,6 +559,9 @@ static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int 
     if (maxiter >= 1 && lagged_ok(h))
         return mg_solve_lagged(h, f, u, eps, maxiter, hist, iters, converged, st);
     const pmg_level *l0 = h->lv[0];
+    // variable levels compute their pivot field here, outside the graph
+    // capture (a lazy prepare inside the capture would be replayed per cycle)
+    for (auto *l : h->lv) TRY(pmg_level_prepare(const_cast<pmg_level *>(l), st));
     // r0 = ||f|| (multigrid.py:307-309)
     TRY(pmg_dot(l0, f, f, h->scratch, h->res_d, st));
     TRYC(cudaStreamSynchronize(st), "sync");
@@ -579,6 +597,7 @@ int pmg_mg_solve(pmg_hier *h, const double *f, double *u, double eps, int maxite
     if (!h || !f || !u || !hist || !iters || !converged) return err(PMG_ERR_VALUE, "null argument");
     if (maxiter < 0 || !(eps > 0.0)) return err(PMG_ERR_VALUE, "need eps > 0 and maxiter >= 0");
     cudaStream_t st = (cudaStream_t)stream;
+    sync_mode(h);
     if (st) return mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, st);
     // legacy stream: run on the hierarchy's stream, ordered by events
     TRYC(cudaEventRecord(h->ev_in, 0), "event");

@@ -20,6 +20,10 @@ namespace pmg {
 // recorded into CUDA graphs)
 std::atomic<long long> g_launches{0};
 int g_smoother_exact = 0;
+// bumped whenever the smoother mode changes: kernel variants are chosen when a
+// driver graph is captured, so graphs and views cached under another mode are
+// discarded (pmg_driver.cu sync_mode)
+int g_mode_gen = 0;
 
 // ---------------------------------------------------------------------------
 // block reduction helpers (deterministic: fixed shuffle tree + fixed

@@ -491,9 +491,13 @@ def _ptrs(df: DistField):
 
 
 def graph_key(cfg: MGConfig, f: DistField, u: DistField) -> tuple:
-    """Cache key of the Python driver's captured cycle graphs (+ first)."""
+    """Cache key of the Python driver's captured cycle graphs (+ first):
+    cycle shape, buffers, and the process-wide kernel selection (smoother
+    mode, fused halos) the graph's kernels were chosen under."""
+    from . import partition
     return (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
-            cfg.red_restrict, _ptrs(f), _ptrs(u))
+            cfg.red_restrict, _ptrs(f), _ptrs(u), int(load().pmg_get_smoother_mode()),
+            partition._FUSED_HALO)
 
 
 def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField | None = None):

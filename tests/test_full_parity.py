@@ -1,0 +1,136 @@
+"""Whole-field parity at the BASELINE configs' full sizes (needs a B200).
+
+The GPU solve (the drop-in API: build_hierarchy + mg_solve, PanelOperator +
+SSORPreconditioner + pcg_solve) is compared with oracle/oracle.c -- the C
+restatement of the reference pinned by tests/test_oracle_c.py -- run on the
+GPU box's host cores on the same seeded f:
+
+* equal iteration counts;
+* residual histories within 1e-8 relative (north_star);
+* the WHOLE solution field within 1e-8 relative (max |u_gpu - u_cpu| over
+  max |u_cpu|), not samples.
+
+configs[4] (4096^2 x 128, 17 GB per field) runs the C oracle in its lean
+mode (no N-sized coefficient caches: ~4 fields of hierarchy + 3 host arrays
+here, ~125 GB); when the box has less RAM the largest graded / variable-
+omega^2 grid that fits is used (2048^2 x 128, 8 levels).  Sizes and errors
+are recorded in gpurun_out/full_parity.json.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+TOL = 1e-8
+
+
+@pytest.fixture(scope="module")
+def pmg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1307_2036_b200 as m
+    return m
+
+
+def record(name, **kw):
+    out = os.path.join(ROOT, "gpurun_out")
+    if not os.path.isdir(out):
+        return
+    p = os.path.join(out, "full_parity.json")
+    d = json.load(open(p)) if os.path.exists(p) else {}
+    d[name] = kw
+    with open(p, "w") as fh:
+        json.dump(d, fh, indent=1)
+
+
+def mem_available_bytes():
+    with open("/proc/meminfo") as fh:
+        for line in fh:
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    return 0
+
+
+def compare(name, u_gpu, rep_gpu, u_cpu, rep_cpu):
+    assert rep_gpu.iterations == rep_cpu.iterations, (rep_gpu.iterations, rep_cpu.iterations)
+    hg, hc = np.asarray(rep_gpu.residual_history), np.asarray(rep_cpu.residual_history)
+    assert hg.shape == hc.shape
+    herr = float(np.max(np.abs(hg - hc) / hc))
+    amax = float(np.max(np.abs(u_cpu)))
+    uerr = float(np.max(np.abs(u_gpu - u_cpu))) / amax
+    record(name, shape=list(u_cpu.shape), iterations=int(rep_gpu.iterations), hist_rel=herr,
+           field_rel=uerr, history=[float(x) for x in hg])
+    assert herr <= TOL, herr
+    assert uerr <= TOL, uerr
+
+
+def oracle_hier(prob):
+    from oracle import coracle, port
+    cfg = port.Config(prob.nx, prob.ny, prob.nz, prob.depth, prob.omega2, prob.lambda2,
+                      prob.levels, stretch=prob.stretch, variable_omega=prob.variable_omega)
+    # lean: coefficients recomputed per column (same bits, tests/test_oracle_c.py)
+    return coracle.config_hierarchy(cfg, lean=prob.dof > 600_000_000)
+
+
+def mg_case(pmg, name, prob):
+    from paper_1307_2036_b200 import configs
+    f = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
+    cfg = prob.mg_config()
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
+    u, rep = pmg.mg_solve(pmg.scatter_owned(f, hier.fine.layout), hier, cfg)
+    ug = pmg.gather_owned(u)
+    del u, hier
+    torch.cuda.empty_cache()
+    uc, rc = oracle_hier(prob).mg_solve(f)
+    del f
+    compare(name, ug, rep, uc, rc)
+
+
+def cg_case(pmg, name, prob):
+    from paper_1307_2036_b200 import configs
+    f = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
+    op = pmg.PanelOperator(prob.grid(), prob.params())
+    pre = pmg.SSORPreconditioner(pmg.LineSmoother(op))
+    u, rep = pmg.pcg_solve(pmg.scatter_owned(f, op.layout), op, pre, eps=1e-5, maxiter=2000)
+    ug = pmg.gather_owned(u)
+    del u, op, pre
+    torch.cuda.empty_cache()
+    uc, rc = oracle_hier(prob).pcg_solve(f, eps=1e-5, maxiter=2000)
+    compare(name, ug, rep, uc, rc)
+
+
+def test_config1_whole_field(pmg):
+    from paper_1307_2036_b200 import configs
+    mg_case(pmg, "config1_mg", configs.config(1))
+
+
+@pytest.mark.parametrize("w", [1e-4, 1e-3, 1e-2, 1e-1])
+@pytest.mark.parametrize("solver", ["mg", "cg"])
+def test_config2_whole_field(pmg, solver, w):
+    from paper_1307_2036_b200 import configs
+    prob = configs.config(2, omega2=w)
+    (mg_case if solver == "mg" else cg_case)(pmg, f"config2_{solver}_w{w:g}", prob)
+
+
+def test_config3_block_whole_field(pmg):
+    """configs[3]'s per-GPU block: 2048^2 x 128, 8 levels (one GPU's part of
+    the weak-scaling run; periodic on its own)."""
+    from paper_1307_2036_b200 import configs
+    mg_case(pmg, "config3_block_mg", configs.config(3, gpus=1))
+
+
+def test_config4_whole_field(pmg):
+    """configs[4]: graded levels (1.05), omega^2(x, y); 4096^2 x 128 with 9
+    levels when host RAM holds the C oracle, else 2048^2 x 128 with 8."""
+    from paper_1307_2036_b200 import configs
+    prob = configs.config(4)
+    need = 8 * prob.dof * 8
+    if mem_available_bytes() < need:
+        prob = configs.Problem(2048, 2048, 128, 1e-3, 1.0, 8, stretch=1.05, variable_omega=True)
+    mg_case(pmg, f"config4_{prob.nx}_mg", prob)

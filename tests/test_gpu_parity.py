@@ -1140,3 +1140,30 @@ def test_field_alloc_and_prolong_add(pmg):
     _lib.call("pmg_prolong_add", fh, ch, cu.parts[w].ptr, b.parts[w].ptr, st)
     torch.cuda.synchronize()
     assert np.array_equal(pmg.gather_owned(a), pmg.gather_owned(b))
+
+
+@pytest.mark.parametrize("name", ["ops_config", "ops_variable"])
+def test_mode_switch_recaptures_graphs(pmg, name):
+    """A fast-mode solve followed by an exact-mode solve on the SAME hierarchy
+    and buffers must run the exact kernels (graphs captured under the fast
+    mode are not replayed): bit-identical to an exact solve on a fresh
+    hierarchy, and the exact single V-cycle equals the reference's."""
+    g, grid, params, cfg, hier = setup(pmg, name)
+    nx, nz = grid.nx, grid.nz
+    fg = uni((nx, nx, nz), 2)
+    f = pmg.scatter_owned(fg, hier.fine.layout)
+    u = pmg.DistField.zeros(hier.fine.layout, nz)
+    for _ in range(2):
+        pmg.mg_solve(f, hier, cfg, out=u)          # fast mode, graphs cached
+    with pmg.exact_smoother():
+        u, rep = pmg.mg_solve(f, hier, cfg, out=u)
+        got = pmg.gather_owned(u)
+        _, _, _, _, hier2 = setup(pmg, name)
+        f2 = pmg.scatter_owned(fg, hier2.fine.layout)
+        u2, rep2 = pmg.mg_solve(f2, hier2, cfg)
+        want = pmg.gather_owned(u2)
+    assert rep.residual_history == rep2.residual_history
+    assert np.array_equal(got, want)
+    # and back: the fast mode is restored on the same buffers
+    u3, rep3 = pmg.mg_solve(f, hier, cfg, out=u)
+    assert rep3.iterations == rep.iterations

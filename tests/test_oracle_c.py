@@ -204,3 +204,36 @@ def test_c_oracle_config2_full_size(w, solver):
     tol = 1e-12 if solver == "mg" else CG_TOL
     assert hist_rel(rep.residual_history, g["history"]) <= tol
     check_samples(u, g, tol)
+
+
+def test_c_oracle_matches_live_reference():
+    """oracle.c against the reference package itself, run live on a
+    256^2 x 128 configs[1]-like problem (5 levels) through
+    oracle/refharness.py (baseline/_ref or $PANELMG_SRC; skipped when no
+    copy of the reference is present): same cycles, history <= 1e-12 and
+    the same solution to the last bit (measured: 0.0 difference)."""
+    from oracle import refharness
+    if not refharness.available():
+        pytest.skip("reference package not installed (baseline/_ref)")
+    cfg = port.Config(256, 256, 128, 0.01, 1e-3, 1.0, 5)
+    f = port.rhs(256, 256, 128, 0)
+    ur, rr = refharness.mg_solve(cfg, f)
+    uc, rc = coracle.config_hierarchy(cfg).mg_solve(f)
+    assert rc.iterations == rr.iterations
+    assert hist_rel(rc.residual_history, rr.residual_history) <= 1e-12
+    assert rel(uc, ur) <= 1e-15
+
+
+@pytest.mark.parametrize("variable", [False, True])
+def test_c_oracle_lean_mode_identical(variable):
+    """The lean hierarchy (coefficients recomputed per column instead of the
+    reference's N-sized caches; used for the 4096^2 configs[4] parity check)
+    gives the same bits as the cached one, MG and CG."""
+    cfg = port.Config(64, 64, 32, 0.01, 1e-3, 1.0, 4, stretch=1.05 if variable else None,
+                      variable_omega=variable)
+    f = port.rhs(64, 64, 32, 0)
+    for solve in ("mg_solve", "pcg_solve"):
+        ua, ra = getattr(coracle.config_hierarchy(cfg), solve)(f)
+        ub, rb = getattr(coracle.config_hierarchy(cfg, lean=True), solve)(f)
+        assert ra.residual_history == rb.residual_history
+        assert np.array_equal(ua, ub)
