@@ -168,6 +168,17 @@ int pmg_get_smoother_mode(void);
 int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
                    double rho, int zero_start, int neighbors_zero, double post_scale,
                    void *stream);
+/* the same half-sweep restricted to a tile region: the 32-cell strips
+ * rx0 + s * rxs (s < rxn) of the relaxed colour's rows and the rows
+ * ry0 + t * rys (t < ryn).  A boundary-first multi-part sweep relaxes the
+ * strips and rows that hold the part's boundary columns first, exchanges
+ * their halos while the interior region relaxes, with the
+ * same values as one whole-part call.  Fast smoother mode and uniform
+ * coefficients only (pmg_half_sweep_region_ok), else PMG_ERR_VALUE. */
+int pmg_half_sweep_region_ok(const pmg_level *lvl);
+int pmg_half_sweep_region(const pmg_level *lvl, double *u, const double *f, int color, double rho,
+                          int zero_start, int neighbors_zero, double post_scale, int rx0, int rxs,
+                          int rxn, int ry0, int rys, int ryn, void *stream);
 /* red half sweep (rho = 1) fused with the convergence residual of the
  * iterate it relaxes: reads u, writes the relaxed red values into the red
  * array of u_new (u_new's black array is not touched; u_new != u), and
@@ -273,6 +284,19 @@ int pmg_cg_step(long long n, const double *alpha_num, const double *alpha_den,
 /* p = z + (beta_num[0]/beta_den[0]) p over the full allocation. */
 int pmg_cg_direction(long long n, const double *beta_num, const double *beta_den,
                      const double *z, double *p, void *stream);
+
+/* ---- batched tridiagonal solves (paper Alg. 3; reference tridiag.py:59-100) --
+ * nsys independent systems of n unknowns, stored system-fastest (element k
+ * of system s at k * nsys + s; device pointers): diagonal a, superdiagonal
+ * b and subdiagonal c (n - 1 rows used; may be NULL when n = 1), right-hand
+ * side f, solution x.  work: pmg_thomas_work_doubles(n, nsys) device
+ * doubles.  One thread per system, the reference's operation order
+ * (bit-identical to its scalar solve).  PMG_ERR_PIVOT when a pivot falls
+ * below 1e-300 in magnitude (tridiag.py:79-90); *bad_row is the first such
+ * row over all systems, else -1.  Synchronises the stream. */
+int pmg_thomas_batch(int n, long long nsys, const double *a, const double *b, const double *c,
+                     const double *f, double *x, double *work, int *bad_row, void *stream);
+long long pmg_thomas_work_doubles(int n, long long nsys);
 
 /* ---- device-resident drivers (multigrid.py:271-330, krylov.py:88-167) --
  * For one part that is its own neighbour in both directions (one GPU per

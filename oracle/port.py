@@ -262,6 +262,41 @@ def dot(a: np.ndarray, b: np.ndarray) -> float:
 
 
 # ---------------------------------------------------------------------------
+# scalar Thomas algorithm (tridiag.py:59-100, paper Alg. 3)
+# ---------------------------------------------------------------------------
+
+
+def thomas_scalar(a, b, c, f) -> np.ndarray:
+    """One tridiagonal system by forward elimination and back substitution,
+    in the reference's operation order (tridiag.py:79-100): row 0 divides by
+    its pivot, later rows multiply by the reciprocal.  Raises
+    ``ArithmeticError`` at a pivot below 1e-300 in magnitude."""
+    n = len(a)
+    wp = np.empty(n)
+    yp = np.empty(n)
+    piv = a[0]
+    if abs(piv) < 1e-300:
+        raise ArithmeticError("zero pivot at row 0")
+    if n == 1:
+        return np.array([f[0] / piv])
+    wp[0] = b[0] / piv
+    yp[0] = f[0] / piv
+    for i in range(1, n):
+        piv = a[i] - wp[i - 1] * c[i - 1]
+        if abs(piv) < 1e-300:
+            raise ArithmeticError(f"zero pivot at row {i}")
+        inv = 1.0 / piv
+        if i + 1 < n:
+            wp[i] = b[i] * inv
+        yp[i] = (f[i] - yp[i - 1] * c[i - 1]) * inv
+    x = np.empty(n)
+    x[n - 1] = yp[n - 1]
+    for i in range(n - 2, -1, -1):
+        x[i] = yp[i] - wp[i] * x[i + 1]
+    return x
+
+
+# ---------------------------------------------------------------------------
 # line smoother (smoother.py:102-244)
 # ---------------------------------------------------------------------------
 

@@ -85,6 +85,8 @@ SIGNATURES = {
     "pmg_red_residual_norm": (_I, [_P, _P, _P, _P, _P, _P]),
     "pmg_half_sweep": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _P]),
     "pmg_half_sweep_res": (_I, [_P, _P, _P, _P, _P, _P, _P]),
+    "pmg_half_sweep_region_ok": (_I, [_P]),
+    "pmg_half_sweep_region": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _I, _I, _I, _I, _I, _I, _P]),
     "pmg_half_sweep_res_ok": (_I, [_P]),
     "pmg_set_smoother_mode": (_I, [_I]),
     "pmg_get_smoother_mode": (_I, []),
@@ -109,6 +111,8 @@ SIGNATURES = {
     "pmg_cg_update": (_I, [_P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pmg_cg_direction": (_I, [_LL, _P, _P, _P, _P, _P]),
     "pmg_cg_step": (_I, [_LL, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "pmg_thomas_batch": (_I, [_I, _LL, _P, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
+    "pmg_thomas_work_doubles": (_LL, [_I, _LL]),
 }
 
 

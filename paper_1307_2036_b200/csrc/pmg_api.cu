@@ -199,6 +199,8 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
     L.cstride = (long long)(ny + 2) * L.jstride;
     L.fcs = L.cstride;
     L.par = (d->i0 + d->j0) & 1;
+    L.rx0 = 0, L.rxs = 1, L.rxn = ((nx + 1) / 2 + 31) / 32;   // whole part
+    L.ry0 = 0, L.rys = 1, L.ryn = ny;
     L.omega2 = d->omega2;
     L.vcoef = d->vcoef;
     lv->i0 = d->i0;
@@ -457,6 +459,40 @@ int pmg_half_sweep(const pmg_level *lv, double *u, const double *f, int color, d
     PMG_CUDA(launch_half_sweep(lv->L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
                                (cudaStream_t)st),
              "half_sweep");
+    return PMG_OK;
+}
+
+int pmg_half_sweep_region_ok(const pmg_level *lv) {
+    if (!lv) return 0;
+    const Lvl &L = lv->L;
+    // the fast uniform column solvers (k_half_sweep_band / k_half_sweep_seg)
+    // walk tile regions; the exact, variable and fused-halo kernels do not
+    return (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8 &&
+            !(L.hflags & 1))
+               ? 1
+               : 0;
+}
+
+int pmg_half_sweep_region(const pmg_level *lv, double *u, const double *f, int color, double rho,
+                          int zero_start, int neighbors_zero, double post_scale, int rx0, int rxs,
+                          int rxn, int ry0, int rys, int ryn, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
+    if (!pmg_half_sweep_region_ok(lv))
+        return fail(PMG_ERR_VALUE, "tile regions need the fast smoother on a uniform level");
+    const Lvl &L0 = lv->L;
+    const int hx = ((L0.nx + 1) / 2 + 31) / 32;
+    if (rxn < 0 || ryn < 0 || rxs < 1 || rys < 1 || rx0 < 0 || ry0 < 0 ||
+        (rxn > 0 && rx0 + (long long)(rxn - 1) * rxs >= hx) ||
+        (ryn > 0 && ry0 + (long long)(ryn - 1) * rys >= L0.ny))
+        return fail(PMG_ERR_VALUE, "tile region outside the part");
+    if (rxn == 0 || ryn == 0) return PMG_OK;
+    Lvl L = L0;
+    L.rx0 = rx0, L.rxs = rxs, L.rxn = rxn;
+    L.ry0 = ry0, L.rys = rys, L.ryn = ryn;
+    PMG_CUDA(launch_half_sweep(L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
+                               (cudaStream_t)st),
+             "half_sweep_region");
     return PMG_OK;
 }
 

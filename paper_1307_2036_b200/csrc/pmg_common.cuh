@@ -39,6 +39,13 @@ struct Lvl {
     // residual-restriction and prolongation kernels wrap around instead of
     // reading the halo ring (which is then not maintained: pmg_driver.cu)
     int hflags;
+    // tile region of the fast uniform half-sweeps (k_half_sweep_seg,
+    // k_half_sweep_band): the 32-cell strips rx0 + s * rxs (s < rxn) of the
+    // colour arrays, and the rows ry0 + t * rys (t < ryn).  The level's own
+    // region is the whole part (0, 1, strips, 0, 1, ny); a boundary-first
+    // multi-part sweep relaxes the frame and the interior as separate
+    // regions (pmg_half_sweep_region, pmg_parts.cu)
+    int rx0, rxs, rxn, ry0, rys, ryn;
     // 2-D device factors (variable coefficients)
     const double *wx, *wy, *av, *vh, *sumw;
     const double *invd;     // variable: per-cell pivots, field layout

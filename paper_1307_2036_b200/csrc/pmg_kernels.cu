@@ -1329,8 +1329,11 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
         double *hend = hend0 + par * 16 * 32;
         double *ybeg = ybeg0 + par * 16 * 32;
-        const int j = t / htiles;
-        const int h0 = (t - j * htiles) * 32;
+        // tile t of the region: row ry0 + (t / htiles) rys, strip
+        // rx0 + (t % htiles) rxs (the whole part by default)
+        const int tj = t / htiles;
+        const int j = L.ry0 + tj * L.rys;
+        const int h0 = (L.rx0 + (t - tj * htiles) * L.rxs) * 32;
         const int s0 = (j + L.par + c) & 1;
         const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
         const int ln = min(lane, nact - 1);
@@ -1505,9 +1508,10 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
         if (lane != 0) return;
         unsigned nb = 0, nf = 0;
         for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-            const int strip = unit % nstrip, band = unit / nstrip;
+            // units tile the region: strips rx0 + s rxs, rows ry0 .. ry0 + ryn
+            const int strip = L.rx0 + (unit % nstrip) * L.rxs, band = unit / nstrip;
             const int h0 = strip * 32;
-            const int j0 = band * band_rows, j1 = min(L.ny, j0 + band_rows);
+            const int j0 = L.ry0 + band * band_rows, j1 = min(L.ry0 + L.ryn, j0 + band_rows);
             if (j0 >= j1) continue;
             const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
             const uint32_t bytesb = NZ * BAND_W * 8 + 2 * NZ * 2 * 8;
@@ -1554,9 +1558,9 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
     double dacc = 0.0;
     unsigned seqb = 0, seqf = 0;                     // sequence of the unit's first rows
     for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
-        const int strip = unit % nstrip, band = unit / nstrip;
+        const int strip = L.rx0 + (unit % nstrip) * L.rxs, band = unit / nstrip;
         const int h0 = strip * 32;
-        const int j0 = band * band_rows, j1 = min(L.ny, j0 + band_rows);
+        const int j0 = L.ry0 + band * band_rows, j1 = min(L.ry0 + L.ryn, j0 + band_rows);
         if (j0 >= j1) continue;
         for (int j = j0; j < j1; ++j) {
             const long long pc = at(L, c, k0, j, h0 + lane);
@@ -3181,7 +3185,7 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
         !(L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
           (L.plane == 136 && band_l1())) ||
         L.seg != 16 || nbr_zero || (L.hflags & 1) || L.nx % 2 || hrow % 32 || hrow < 64 ||
-        L.ny < 8)
+        L.ny < 8 || L.rys != 1 || L.rxn < 1 || L.ryn < 1)
         return false;
     const int o = color ^ 1;
     CUtensorMap mF, mB, mE;
@@ -3189,7 +3193,8 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
         !make_tmap(&mB, u + (long long)o * L.cstride, L, BAND_W, BAND_NZ) ||
         !make_tmap(&mE, u + (long long)o * L.cstride, L, 2, BAND_NZ))
         return false;
-    const int nstrip = hrow / 32;
+    // the tile region: L.rxn strips (stride L.rxs) x L.ryn consecutive rows
+    const int nstrip = L.rxn, nrows = L.ryn;
     // units per SM: a multiple of the SM count keeps the CTAs balanced;
     // measured best 4 at 16 strips (nx = 1024: 269 us; 2 -> 373, 8 -> 278),
     // 2 at 8 strips (nx = 512: 76.3 us; 4 -> 80.3), 1 below
@@ -3205,9 +3210,9 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     }
     const int ups = ups_env ? ups_env : nstrip / gcd;
     int nband = (ups * sm_count() + nstrip - 1) / nstrip;
-    if (nband > L.ny) nband = L.ny;
-    const int band_rows = (L.ny + nband - 1) / nband;
-    nband = (L.ny + band_rows - 1) / band_rows;
+    if (nband > nrows) nband = nrows;
+    const int band_rows = (nrows + nband - 1) / nband;
+    nband = (nrows + band_rows - 1) / band_rows;
     const int nunits = nstrip * nband;
     const int grid = nunits < sm_count() ? nunits : sm_count();
     if (np) *np = grid;
@@ -3287,14 +3292,17 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
     if (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) {
         const int nw = (L.nz + L.seg - 1) / L.seg;
         const size_t sm = sizeof(double) * (7 * (size_t)L.nz + 4 * 16 * 32);
-        const int ntiles = hx * L.ny;
+        // the level's tile region (the whole part unless a boundary-first
+        // sweep restricts it): L.rxn strips x L.ryn rows
+        const int ntiles = L.rxn * L.ryn;
+        if (ntiles <= 0) return cudaSuccess;
         auto run = [&](auto kern) {
             int occ = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
             const int cap = sm_count() * (occ > 0 ? occ : 1);
             const int grid = ntiles < cap ? ntiles : cap;
             kern<<<grid, 32 * nw, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                            ntiles, hx, nullptr, nullptr);
+                                            ntiles, L.rxn, nullptr, nullptr);
         };
         {
             // compile-time neighbour mode, predicate-free when the segments

@@ -224,7 +224,75 @@ def native_fixture(name, nx, nz, dt, flat, policy="standard"):
     print(name, "mg", rep.iterations, "cg", rc.iterations)
 
 
+def thomas_fixture(name):
+    """The reference's scalar Thomas solve (tridiag.py:59-100) on seeded
+    diagonally dominant systems of the sizes its own test uses
+    (tests/test_tridiag.py:33-47), plus a 1e-12-dominant near-singular case."""
+    from panelmg import TridiagonalSystem, thomas_solve
+    rng = np.random.default_rng(21)
+    out = {}
+    for n in (1, 2, 3, 64, 128, 257):
+        ns = 16
+        a = rng.uniform(2.5, 4.0, (ns, n))
+        b = rng.uniform(-1.0, 1.0, (ns, n - 1))
+        c = rng.uniform(-1.0, 1.0, (ns, n - 1))
+        f = rng.uniform(-1.0, 1.0, (ns, n))
+        x = np.stack([thomas_solve(TridiagonalSystem(a[s], b[s], c[s], f[s]))
+                      for s in range(ns)])
+        out.update({f"a{n}": a, f"b{n}": b, f"c{n}": c, f"f{n}": f, f"x{n}": x})
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(name)
+
+
+def orderings_fixture(name, nx, nz, omega2, lambda2, levels, periodic):
+    """The reference's alternative smoother orderings (smoother.py:193-222)
+    and its ``smooth`` dispatcher (smoother.py:247-256) on one grid."""
+    from panelmg.smoother import SmootherConfig, smooth
+    if periodic:
+        inject(False)
+    else:
+        uninject()
+    try:
+        grid = panel_grid(nx, nz, depth=levels[-1] - 1.0, flat_mode=True, levels=levels)
+        op = st.PanelOperator(grid, params(nx, nz, omega2, lambda2),
+                              Decomposition(nx, 1).layout(nx))
+        sm = LineSmoother(op)
+        ug, fg = uni((nx, nx, nz), 1), uni((nx, nx, nz), 2)
+
+        def field(a):
+            d = scatter_owned(a, op.layout)
+            halo_exchange(d)
+            return d
+
+        f = field(fg)
+        out = {"nx": nx, "nz": nz, "omega2": omega2, "lambda2": lambda2,
+               "levels": np.asarray(levels), "periodic": periodic, "variable": False,
+               "nlev": 1, "seed_u": 1, "seed_f": 2}
+        for rho in (1.0, 1.3):
+            u = field(ug)
+            sm.symmetric_sweep(u, f, nsweeps=2, rho=rho)
+            out[f"symmetric_rho{rho}"] = gather_owned(u)
+            u = field(ug)
+            sm.jacobi_sweep(u, f, nsweeps=2, rho=rho)
+            out[f"jacobi_rho{rho}"] = gather_owned(u)
+            for ordering in ("redblack", "symmetric", "jacobi"):
+                u = field(ug)
+                smooth(u, f, sm, SmootherConfig(ordering=ordering, sweeps=3, rho=rho))
+                out[f"smooth_{ordering}_rho{rho}"] = gather_owned(u)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+        print(name)
+    finally:
+        uninject()
+
+
 def main(which):
+    if which in ("orderings", "small", "all"):
+        orderings_fixture("orderings_periodic", 16, 8, 0.7, 1.3,
+                          port.uniform_levels(8, 1.0), periodic=True)
+        orderings_fixture("orderings_neumann", 16, 8, 0.7, 1.3,
+                          port.uniform_levels(8, 1.0), periodic=False)
+    if which in ("thomas", "small", "all"):
+        thomas_fixture("thomas")
     if which in ("small", "all"):
         # per-op fixtures: periodic config factors, the reference's own
         # Neumann flat factors, and configs[4]-style variable coefficients

@@ -172,3 +172,40 @@ def test_thomas_known_answers():
     port.half_sweep(lev, u, f, port.RED)
     # diagonal = vh * volprof = (1/2)^2 * (1/3)
     assert np.allclose(u[1, 1, :], 1.0 / (0.25 / 3.0), rtol=1e-15)
+
+
+def test_thomas_scalar_matches_reference():
+    """oracle thomas_scalar == the reference's thomas_solve (tridiag.py:59-100),
+    bit for bit, on the seeded systems of tests/golden/thomas.npz."""
+    g = load("thomas")
+    for n in (1, 2, 3, 64, 128, 257):
+        a, b, c, f, x = (g[f"{k}{n}"] for k in "abcfx")
+        for s in range(a.shape[0]):
+            assert np.array_equal(port.thomas_scalar(a[s], b[s], c[s], f[s]), x[s]), (n, s)
+    with pytest.raises(ArithmeticError):
+        port.thomas_scalar(np.array([1.0, 1.0]), np.array([1.0]), np.array([1.0]),
+                           np.array([1.0, 1.0]))
+
+
+@pytest.mark.parametrize("name", ["orderings_periodic", "orderings_neumann"])
+def test_oracle_orderings_match_reference(name):
+    """Symmetric and block-Jacobi orderings (smoother.py:193-222) and the
+    smooth() dispatcher (smoother.py:247-256) of the oracle vs the reference."""
+    g = load(name)
+    nx, nz = int(g["nx"]), int(g["nz"])
+    lev = fixture_level(g)
+    ug, fg = uni((nx, nx, nz), 1), uni((nx, nx, nz), 2)
+    f = lev.field(fg)
+    o = lambda d: d[1:-1, 1:-1, :]  # noqa: E731
+    for rho in (1.0, 1.3):
+        u = lev.field(ug)
+        port.symmetric_sweep(lev, u, f, 2, rho)
+        assert rel(o(u), g[f"symmetric_rho{rho}"]) <= 1e-15
+        u = lev.field(ug)
+        port.jacobi_sweep(lev, u, f, 2, rho)
+        assert rel(o(u), g[f"jacobi_rho{rho}"]) <= 1e-15
+        for ordering, fn in (("redblack", port.sweep), ("symmetric", port.symmetric_sweep),
+                             ("jacobi", port.jacobi_sweep)):
+            u = lev.field(ug)
+            fn(lev, u, f, 3, rho)
+            assert rel(o(u), g[f"smooth_{ordering}_rho{rho}"]) <= 1e-15
