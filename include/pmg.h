@@ -351,6 +351,61 @@ int pmg_pcg_solve(const pmg_level *lvl, const double *f, double *u, double eps, 
                   double tau, int precond, double rho, int periodic_x, int periodic_y,
                   double *work, double *hist, int *iters, int *converged, void *stream);
 
+/* ---- multi-part drivers (multigrid.py:271-330 over a px x py
+ * decomposition; partition.py:158-191 halo exchange, partition.py:267-286
+ * reductions) ------------------------------------------------------------
+ * A hierarchy over the parts this process owns: all parts of the
+ * decomposition (in-process, one device: the exchange is a device copy
+ * between parts), or exactly one part per rank with a communicator (the
+ * exchange is ncclSend / ncclRecv, the reductions an ncclAllGather of the
+ * per-part sums, added in worker order -- the in-process order, so results
+ * do not depend on the transport).  Each V-cycle + convergence norm is one
+ * CUDA graph replay (halo exchanges and reductions inside it) and one
+ * 8-byte host read.  overlap_nx > 0: levels whose parts are at least that
+ * wide (and >= 256 columns) relax boundary-first -- the frame regions
+ * (pmg_half_sweep_region), then the frame's halo exchange on a second
+ * stream while the interior relaxes; same values bit for
+ * bit.  Same operation sequence as the Python multi-part driver
+ * (multigrid.v_cycle, fused path). */
+typedef struct pmg_comm pmg_comm;     /* opaque: an NCCL communicator */
+typedef struct pmg_phier pmg_phier;   /* opaque */
+typedef struct pmg_part_desc {
+    int worker;   /* worker id; with a communicator: this rank */
+    int nbr[4];   /* worker across the W, E, S, N face; -1: physical boundary (mirror) */
+} pmg_part_desc;
+/* 1 if libnccl.so.2 can be loaded (resolved at run time; no link dependency) */
+int pmg_comm_available(void);
+/* NCCL unique id (128 bytes) on one rank, to be broadcast to the others */
+int pmg_comm_unique_id(void *id128);
+/* communicator of nranks ranks on the current device (ncclCommInitRank) */
+int pmg_comm_create(const void *id128, int nranks, int rank, pmg_comm **out);
+int pmg_comm_destroy(pmg_comm *comm);
+/* one phase's ordered message plan of a part with neighbours nbr[4]
+ * (phase 0: W/E faces, 1: S/N faces including the corners): ops[3 * n] =
+ * 0 send / 1 receive, ops[3 * n + 1] = face, ops[3 * n + 2] = peer worker;
+ * at most 4 ops.  [send a, recv b, send b, recv a]: messages to one peer
+ * pair up under NCCL's in-order matching.  Host only. */
+int pmg_exchange_plan(const int *nbr, int phase, int *ops, int *nops);
+/* levels[p * nlev + c]: part p (ascending worker order), level c (finest
+ * first, halving nx and ny) */
+int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
+                     const pmg_part_desc *parts, const pmg_mg_desc *desc, pmg_comm *comm,
+                     int overlap_nx, pmg_phier **out);
+int pmg_phier_destroy(pmg_phier *hier);
+/* mg_solve over every part: f[p], u[p] the parts' fields (multigrid.py:297-330) */
+int pmg_phier_mg_solve(pmg_phier *hier, const double *const *f, double *const *u, double eps,
+                       int maxiter, double *hist, int *iters, int *converged, void *stream);
+/* one V-cycle (u halos current; first = 1: u zero on entry, unfilled) */
+int pmg_phier_vcycle(pmg_phier *hier, double *const *u, const double *const *f, int first,
+                     void *stream);
+/* halo exchange of level `level`'s fields (partition.py:158-191) */
+int pmg_phier_halo_exchange(pmg_phier *hier, int level, double *const *fields, void *stream);
+/* owned-cell dot over every part and rank into *out (device or host-mapped) */
+int pmg_phier_dot(pmg_phier *hier, int level, const double *const *a, const double *const *b,
+                  double *out, void *stream);
+long long pmg_phier_replayed_launches(const pmg_phier *hier);
+long long pmg_phier_exchanges(const pmg_phier *hier);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,6 +28,10 @@ class MGDesc(C.Structure):
     ]
 
 
+class PartDesc(C.Structure):
+    _fields_ = [("worker", C.c_int), ("nbr", C.c_int * 4)]
+
+
 class LevelDesc(C.Structure):
     _fields_ = [
         ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
@@ -113,6 +117,21 @@ SIGNATURES = {
     "pmg_cg_step": (_I, [_LL, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pmg_thomas_batch": (_I, [_I, _LL, _P, _P, _P, _P, _P, _P, C.POINTER(_I), _P]),
     "pmg_thomas_work_doubles": (_LL, [_I, _LL]),
+    "pmg_comm_available": (_I, []),
+    "pmg_comm_unique_id": (_I, [_P]),
+    "pmg_comm_create": (_I, [_P, _I, _I, C.POINTER(_P)]),
+    "pmg_comm_destroy": (_I, [_P]),
+    "pmg_exchange_plan": (_I, [C.POINTER(_I), _I, C.POINTER(_I), C.POINTER(_I)]),
+    "pmg_phier_create": (_I, [C.POINTER(_P), _I, _I, C.POINTER(PartDesc), C.POINTER(MGDesc), _P,
+                              _I, C.POINTER(_P)]),
+    "pmg_phier_destroy": (_I, [_P]),
+    "pmg_phier_mg_solve": (_I, [_P, C.POINTER(_P), C.POINTER(_P), _D, _I, _P, C.POINTER(_I),
+                                C.POINTER(_I), _P]),
+    "pmg_phier_vcycle": (_I, [_P, C.POINTER(_P), C.POINTER(_P), _I, _P]),
+    "pmg_phier_halo_exchange": (_I, [_P, _I, C.POINTER(_P), _P]),
+    "pmg_phier_dot": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), _P, _P]),
+    "pmg_phier_replayed_launches": (_LL, [_P]),
+    "pmg_phier_exchanges": (_LL, [_P]),
 }
 
 

@@ -1,0 +1,684 @@
+// Native multi-part solve driver of libpmg (include/pmg.h, "multi-part
+// drivers"): the V-cycle / mg_solve of multigrid.py:271-330 over a px x py
+// horizontal decomposition, with the halo exchange of
+// partition.py:158-191 and the reductions of partition.py:267-286 issued by
+// the library, inside the captured CUDA graph of each cycle.
+//
+// A hierarchy holds the parts this process owns: all of them (in-process
+// decomposition on one device: the exchange is a device copy between
+// parts), or one part per rank with a library-owned NCCL communicator
+// (pmg_comm_create; the exchange is ncclSend / ncclRecv over NVLink, the
+// reductions an ncclAllGather of the per-part sums added in worker order).
+// Either way one cycle is one graph replay and one 8-byte host read.
+//
+// Boundary-first relaxation: on levels wide enough, a
+// half-sweep first relaxes the frame -- the rows and 32-cell strips that
+// hold the part's boundary columns (pmg_half_sweep_region) -- then forks
+// the halo exchange of those values onto a second stream while the
+// interior relaxes; the two join before anything reads the halo.  The
+// interior reads no halo cell and the exchange touches only frame and
+// halo cells, so the result is the unsplit sweep's, bit for bit.
+//
+// NCCL is resolved at run time (dlopen of libnccl.so.2, normally the copy
+// torch already loaded): the library links no NCCL and runs without one.
+#include <dlfcn.h>
+
+#include <array>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>   // types and prototypes only; symbols come from dlsym
+
+#include "../../include/pmg.h"
+
+namespace pmg {
+extern std::atomic<long long> g_launches;
+extern int g_mode_gen;
+int set_error(int code, const char *msg);
+}
+
+namespace {
+
+int err(int code, const std::string &m) { return pmg::set_error(code, m.c_str()); }
+
+#define TRY(x)                         \
+    do {                               \
+        int rc_ = (x);                 \
+        if (rc_) return rc_;           \
+    } while (0)
+#define TRYC(x, where)                                                                  \
+    do {                                                                                \
+        cudaError_t e_ = (x);                                                           \
+        if (e_ != cudaSuccess)                                                          \
+            return err(PMG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---- NCCL, resolved at run time ------------------------------------------
+struct Nccl {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclAllGather) all_gather = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+};
+
+const Nccl *nccl() {
+    static Nccl n;
+    static int state = 0;   // 0 untried, 1 ok, -1 unavailable
+    if (state == 0) {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        state = -1;
+        if (h) {
+            n.get_unique_id = (decltype(n.get_unique_id))dlsym(h, "ncclGetUniqueId");
+            n.comm_init_rank = (decltype(n.comm_init_rank))dlsym(h, "ncclCommInitRank");
+            n.comm_destroy = (decltype(n.comm_destroy))dlsym(h, "ncclCommDestroy");
+            n.send = (decltype(n.send))dlsym(h, "ncclSend");
+            n.recv = (decltype(n.recv))dlsym(h, "ncclRecv");
+            n.group_start = (decltype(n.group_start))dlsym(h, "ncclGroupStart");
+            n.group_end = (decltype(n.group_end))dlsym(h, "ncclGroupEnd");
+            n.all_gather = (decltype(n.all_gather))dlsym(h, "ncclAllGather");
+            n.error_string = (decltype(n.error_string))dlsym(h, "ncclGetErrorString");
+            if (n.get_unique_id && n.comm_init_rank && n.comm_destroy && n.send && n.recv &&
+                n.group_start && n.group_end && n.all_gather && n.error_string)
+                state = 1;
+        }
+    }
+    return state == 1 ? &n : nullptr;
+}
+
+int nccl_err(ncclResult_t r, const char *where) {
+    const Nccl *n = nccl();
+    return err(PMG_ERR_CUDA, std::string(where) + ": " + (n ? n->error_string(r) : "nccl"));
+}
+
+#define TRYN(x, where)                                    \
+    do {                                                  \
+        ncclResult_t r_ = (x);                            \
+        if (r_ != ncclSuccess) return nccl_err(r_, where); \
+    } while (0)
+
+// worker-order sum of n per-part scalars (the in-process order of
+// partition.reduce_parts: ((v0 + v1) + v2) + ...), one thread
+__global__ void k_sum_ordered(const double *__restrict__ v, int n, double *__restrict__ out) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += v[i];
+    *out = s;
+}
+
+constexpr int OPP[4] = {1, 0, 3, 2};
+
+}  // namespace
+
+struct pmg_comm {
+    ncclComm_t c = nullptr;
+    int nranks = 0, rank = 0;
+};
+
+namespace {
+
+// one part at one level
+struct PL {
+    const pmg_level *lv = nullptr;
+    double *u = nullptr, *f = nullptr;   // level >= 1: owned; level 0: the caller's
+    double *sb[4] = {nullptr, nullptr, nullptr, nullptr};   // packed own faces
+    double *rb[4] = {nullptr, nullptr, nullptr, nullptr};   // received halo faces (NCCL)
+    long long fd[4] = {0, 0, 0, 0};                         // face doubles
+    int nx = 0, ny = 0, nz = 0;
+};
+
+struct PGraph {
+    std::vector<const double *> f;
+    std::vector<double *> u;
+    int kind;
+    cudaStream_t st;
+    cudaGraphExec_t exec;
+    long long launches;
+};
+
+}  // namespace
+
+struct pmg_phier {
+    int np = 0, nlev = 0;
+    std::vector<int> worker;                  // per local part, ascending
+    std::vector<std::array<int, 4>> nbr;      // per local part: W, E, S, N worker or -1
+    std::vector<int> local;                   // worker -> local part index or -1
+    std::vector<std::vector<PL>> P;           // [part][level]
+    pmg_mg_desc d{};
+    pmg_comm *comm = nullptr;
+    int overlap_nx = 0;                       // boundary-first on levels with nx >= this
+    double *scr[2] = {nullptr, nullptr};      // reduction partials (solve / side stream)
+    double *slots = nullptr;                  // device [np + nranks + 8]
+    double *res_h = nullptr, *res_d = nullptr;   // host-mapped [8]
+    cudaStream_t side = nullptr, own = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_in = nullptr, ev_out = nullptr;
+    std::vector<PGraph> graphs;
+    long long replayed = 0;
+    long long exchanges = 0;                  // halo exchanges issued (per level, counted once)
+    int mode_gen = 0;
+};
+
+namespace {
+
+void free_phier(pmg_phier *h) {
+    for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto &pp : h->P)
+        for (size_t c = 0; c < pp.size(); ++c) {
+            PL &q = pp[c];
+            if (c > 0) {
+                cudaFree(q.u);
+                cudaFree(q.f);
+            }
+            for (int a = 0; a < 4; ++a) {
+                cudaFree(q.sb[a]);
+                cudaFree(q.rb[a]);
+            }
+        }
+    for (auto *s : h->scr) cudaFree(s);
+    cudaFree(h->slots);
+    if (h->res_h) cudaFreeHost(h->res_h);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->own) cudaStreamDestroy(h->own);
+    for (auto e : {h->ev_fork, h->ev_join, h->ev_in, h->ev_out})
+        if (e) cudaEventDestroy(e);
+    delete h;
+}
+
+void sync_mode(pmg_phier *h) {
+    if (h->mode_gen == pmg::g_mode_gen) return;
+    for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
+    h->graphs.clear();
+    h->mode_gen = pmg::g_mode_gen;
+}
+
+// halo exchange of level c's fields x[p] (partition.py:158-191): x faces,
+// then y faces over the extended range (corners), periodic neighbours or
+// mirrored physical boundaries, on stream s
+int exchange(pmg_phier *h, int c, double *const *x, cudaStream_t s) {
+    ++h->exchanges;
+    for (int phase = 0; phase < 2; ++phase) {
+        const int fa = 2 * phase, fb = fa + 1;
+        for (int p = 0; p < h->np; ++p)
+            for (int face : {fa, fb})
+                if (h->nbr[p][face] >= 0)
+                    TRY(pmg_pack_face(h->P[p][c].lv, x[p], face, h->P[p][c].sb[face], s));
+        if (h->comm) {
+            const Nccl *n = nccl();
+            TRYN(n->group_start(), "ncclGroupStart");
+            for (int p = 0; p < h->np; ++p) {
+                int ops[12], nops = 0;
+                TRY(pmg_exchange_plan(h->nbr[p].data(), phase, ops, &nops));
+                const PL &q = h->P[p][c];
+                for (int o = 0; o < nops; ++o) {
+                    const int kind = ops[3 * o], face = ops[3 * o + 1], peer = ops[3 * o + 2];
+                    ncclResult_t r = kind == 0
+                        ? n->send(q.sb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s)
+                        : n->recv(q.rb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s);
+                    if (r != ncclSuccess) {
+                        n->group_end();
+                        return nccl_err(r, kind == 0 ? "ncclSend" : "ncclRecv");
+                    }
+                }
+            }
+            TRYN(n->group_end(), "ncclGroupEnd");
+            for (int p = 0; p < h->np; ++p)
+                for (int face : {fa, fb}) {
+                    const PL &q = h->P[p][c];
+                    if (h->nbr[p][face] >= 0)
+                        TRY(pmg_unpack_face(q.lv, x[p], face, q.rb[face], 0, s));
+                    else
+                        TRY(pmg_unpack_face(q.lv, x[p], face, nullptr, 1, s));
+                }
+        } else {
+            // all parts local: the neighbour's packed strip is the halo
+            for (int p = 0; p < h->np; ++p)
+                for (int face : {fa, fb}) {
+                    const int nb = h->nbr[p][face];
+                    if (nb < 0) {
+                        TRY(pmg_unpack_face(h->P[p][c].lv, x[p], face, nullptr, 1, s));
+                    } else {
+                        const int q = h->local[nb];
+                        TRY(pmg_unpack_face(h->P[p][c].lv, x[p], face, h->P[q][c].sb[OPP[face]], 0,
+                                            s));
+                    }
+                }
+        }
+    }
+    return PMG_OK;
+}
+
+std::vector<double *> level_u(pmg_phier *h, int c, double *const *u0) {
+    std::vector<double *> v(h->np);
+    for (int p = 0; p < h->np; ++p) v[p] = c ? h->P[p][c].u : u0[p];
+    return v;
+}
+std::vector<const double *> level_f(pmg_phier *h, int c, const double *const *f0) {
+    std::vector<const double *> v(h->np);
+    for (int p = 0; p < h->np; ++p) v[p] = c ? h->P[p][c].f : f0[p];
+    return v;
+}
+
+// sum of the per-part scalars slots[0 .. np) over every part of every rank,
+// in worker order, into out (device or host-mapped)
+int global_sum(pmg_phier *h, double *out, cudaStream_t s) {
+    if (h->comm) {
+        // one part per rank: gather the rank sums, add them in rank order
+        double *gath = h->slots + h->np;
+        TRYN(nccl()->all_gather(h->slots, gath, 1, ncclDouble, h->comm->c, s), "ncclAllGather");
+        k_sum_ordered<<<1, 1, 0, s>>>(gath, h->comm->nranks, out);
+    } else {
+        k_sum_ordered<<<1, 1, 0, s>>>(h->slots, h->np, out);
+    }
+    pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
+    TRYC(cudaGetLastError(), "ordered sum");
+    return PMG_OK;
+}
+
+// whether level c relaxes boundary-first: every part region-capable, wide
+// and tall enough that the frame is a small share of the sweep
+bool overlapped(const pmg_phier *h, int c) {
+    if (!h->overlap_nx) return false;
+    for (int p = 0; p < h->np; ++p) {
+        const PL &q = h->P[p][c];
+        if (q.nx < h->overlap_nx || q.nx < 256 || q.ny < 16 || !pmg_half_sweep_region_ok(q.lv))
+            return false;
+    }
+    return true;
+}
+
+// one half-sweep of colour `color` on every part of level c, then the halo
+// exchange (boundary-first when the level qualifies)
+int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, int color,
+                 int nbr_zero, cudaStream_t s) {
+    const double rho = h->d.rho;
+    if (!overlapped(h, c)) {
+        for (int p = 0; p < h->np; ++p)
+            TRY(pmg_half_sweep(h->P[p][c].lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, s));
+        return exchange(h, c, u, s);
+    }
+    // frame: rows 0 and ny - 1 (all strips), the first and last strip of
+    // rows 1 .. ny - 2; then the interior strips 1 .. n - 2 of those rows
+    for (int p = 0; p < h->np; ++p) {
+        const PL &q = h->P[p][c];
+        const int ns = ((q.nx + 1) / 2 + 31) / 32;
+        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns, 0,
+                                  q.ny - 1, 2, s));
+        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, ns - 1, 2,
+                                  1, 1, q.ny - 2, s));
+    }
+    TRYC(cudaEventRecord(h->ev_fork, s), "fork");
+    TRYC(cudaStreamWaitEvent(h->side, h->ev_fork, 0), "fork wait");
+    TRY(exchange(h, c, u, h->side));
+    for (int p = 0; p < h->np; ++p) {
+        const PL &q = h->P[p][c];
+        const int ns = ((q.nx + 1) / 2 + 31) / 32;
+        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 1, 1, ns - 2,
+                                  1, 1, q.ny - 2, s));
+    }
+    TRYC(cudaEventRecord(h->ev_join, h->side), "join");
+    TRYC(cudaStreamWaitEvent(s, h->ev_join, 0), "join wait");
+    return PMG_OK;
+}
+
+int sweeps(pmg_phier *h, int c, double *const *u, const double *const *f, int n, bool from_zero,
+           cudaStream_t s) {
+    for (int k = 0; k < n; ++k) {
+        TRY(half_sweep_x(h, c, u, f, 0, (from_zero && k == 0) ? 1 : 0, s));
+        TRY(half_sweep_x(h, c, u, f, 1, 0, s));
+    }
+    return PMG_OK;
+}
+
+// Alg. 1 (multigrid.py:271-294): the operation sequence of the Python
+// v_cycle's fused path for every part, level by level
+int vcycle(pmg_phier *h, int c, double *const *u0, const double *const *f0, bool first,
+           cudaStream_t s) {
+    const int L = h->nlev;
+    const auto u = level_u(h, c, u0);
+    const auto f = level_f(h, c, f0);
+    const bool lean = h->d.rho == 1.0;
+    if (c + 1 < L) {
+        TRY(sweeps(h, c, u.data(), f.data(), h->d.nu_pre, lean && (c > 0 || first), s));
+        for (int p = 0; p < h->np; ++p) {
+            const pmg_level *lf = h->P[p][c].lv, *lc = h->P[p][c + 1].lv;
+            if (h->d.red_restrict && lean && h->d.nu_pre >= 1 && pmg_residual_restrict_red_ok(lf))
+                TRY(pmg_residual_restrict_red(lf, lc, f[p], u[p], h->P[p][c + 1].f, s));
+            else
+                TRY(pmg_residual_restrict(lf, lc, f[p], u[p], h->P[p][c + 1].f, s));
+        }
+        const int first_sweeps = (c + 2 == L) ? h->d.coarse_sweeps : h->d.nu_pre;
+        if (!(lean && first_sweeps >= 1))
+            for (int p = 0; p < h->np; ++p)
+                TRY(pmg_fill(h->P[p][c + 1].lv, h->P[p][c + 1].u, 0.0, s));
+        TRY(vcycle(h, c + 1, u0, f0, false, s));
+        const int pmask = (lean && h->d.nu_post >= 1) ? 2 : 3;
+        for (int p = 0; p < h->np; ++p)
+            TRY(pmg_prolong_colors(h->P[p][c].lv, h->P[p][c + 1].lv, h->P[p][c + 1].u, u[p], 1,
+                                   pmask, s));
+        TRY(exchange(h, c, u.data(), s));
+        TRY(sweeps(h, c, u.data(), f.data(), h->d.nu_post, false, s));
+    } else {
+        TRY(sweeps(h, c, u.data(), f.data(), h->d.coarse_sweeps, lean && c > 0, s));
+    }
+    return PMG_OK;
+}
+
+// ||f - A u||^2 over every part (the convergence check, multigrid.py:324)
+int norm2(pmg_phier *h, double *const *u, const double *const *f, double *out, cudaStream_t s) {
+    for (int p = 0; p < h->np; ++p)
+        TRY(pmg_residual(h->P[p][0].lv, f[p], u[p], nullptr, h->scr[0], h->slots + p, s));
+    return global_sum(h, out, s);
+}
+
+int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cudaStream_t s) {
+    for (auto &g : h->graphs) {
+        bool same = g.kind == kind && g.st == s;
+        for (int p = 0; same && p < h->np; ++p) same = g.f[p] == f[p] && g.u[p] == u[p];
+        if (same) {
+            TRYC(cudaGraphLaunch(g.exec, s), "graph launch");
+            h->replayed += g.launches;
+            return PMG_OK;
+        }
+    }
+    if (h->graphs.size() >= 16) {
+        cudaGraphExecDestroy(h->graphs.front().exec);
+        h->graphs.erase(h->graphs.begin());
+    }
+    cudaGraph_t graph;
+    const long long l0 = pmg_launch_count();
+    TRYC(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+    int rc = vcycle(h, 0, u, f, kind == 1, s);
+    if (!rc) rc = norm2(h, u, f, h->res_d, s);
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (rc) {
+        if (e == cudaSuccess) cudaGraphDestroy(graph);
+        return rc;
+    }
+    TRYC(e, "capture end");
+    PGraph g{std::vector<const double *>(f, f + h->np), std::vector<double *>(u, u + h->np), kind,
+             s, nullptr, pmg_launch_count() - l0};
+    e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    TRYC(e, "graph instantiate");
+    h->graphs.push_back(g);
+    TRYC(cudaGraphLaunch(g.exec, s), "graph launch");
+    h->replayed += g.launches;
+    return PMG_OK;
+}
+
+int mg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double eps, int maxiter,
+                double *hist, int *iters, int *converged, cudaStream_t s) {
+    for (int p = 0; p < h->np; ++p)
+        for (int c = 0; c < h->nlev; ++c)
+            TRY(pmg_level_prepare(const_cast<pmg_level *>(h->P[p][c].lv), s));
+    // r0 = ||f|| (multigrid.py:307-309)
+    for (int p = 0; p < h->np; ++p)
+        TRY(pmg_dot(h->P[p][0].lv, f[p], f[p], h->scr[0], h->slots + p, s));
+    TRY(global_sum(h, h->res_d, s));
+    TRYC(cudaStreamSynchronize(s), "sync");
+    const double r0 = std::sqrt(h->res_h[0]);
+    hist[0] = r0;
+    *iters = 0;
+    *converged = 0;
+    if (r0 == 0.0) {   // multigrid.py:317-318
+        for (int p = 0; p < h->np; ++p) TRY(pmg_fill(h->P[p][0].lv, u[p], 0.0, s));
+        *converged = 1;
+        return PMG_OK;
+    }
+    const bool lean_first = h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->nlev > 1;
+    if (!lean_first)
+        for (int p = 0; p < h->np; ++p) TRY(pmg_fill(h->P[p][0].lv, u[p], 0.0, s));
+    for (int it = 0; it < maxiter; ++it) {
+        TRY(replay(h, u, f, (lean_first && it == 0) ? 1 : 0, s));
+        TRYC(cudaStreamSynchronize(s), "sync");
+        const double rn = std::sqrt(h->res_h[0]);
+        hist[it + 1] = rn;
+        *iters = it + 1;
+        if (rn / r0 < eps) {   // strict, multigrid.py:326
+            *converged = 1;
+            break;
+        }
+    }
+    return PMG_OK;
+}
+
+template <class Fn>
+int on_stream(pmg_phier *h, void *stream, Fn fn) {
+    cudaStream_t st = (cudaStream_t)stream;
+    if (st) return fn(st);
+    // the legacy default stream cannot be captured: run on the hierarchy's
+    // own stream, ordered after / before the caller's work by events
+    TRYC(cudaEventRecord(h->ev_in, 0), "event");
+    TRYC(cudaStreamWaitEvent(h->own, h->ev_in, 0), "event wait");
+    const int rc = fn(h->own);
+    TRYC(cudaEventRecord(h->ev_out, h->own), "event");
+    TRYC(cudaStreamWaitEvent(0, h->ev_out, 0), "event wait");
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pmg_exchange_plan(const int *nbr, int phase, int *ops, int *nops) {
+    if (!nbr || !ops || !nops || phase < 0 || phase > 1)
+        return err(PMG_ERR_VALUE, "exchange_plan: bad arguments");
+    // [send a, recv b, send b, recv a]: two strips exchanged with the same
+    // peer (2 parts along a periodic axis, or a part that is its own
+    // neighbour) pair up under NCCL's in-order matching per peer
+    const int a = 2 * phase, b = a + 1;
+    int n = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        const int sf = pass ? b : a, rf = pass ? a : b;
+        if (nbr[sf] >= 0) {
+            ops[3 * n] = 0, ops[3 * n + 1] = sf, ops[3 * n + 2] = nbr[sf];
+            ++n;
+        }
+        if (nbr[rf] >= 0) {
+            ops[3 * n] = 1, ops[3 * n + 1] = rf, ops[3 * n + 2] = nbr[rf];
+            ++n;
+        }
+    }
+    *nops = n;
+    return PMG_OK;
+}
+
+int pmg_comm_available(void) { return nccl() ? 1 : 0; }
+
+int pmg_comm_unique_id(void *id) {
+    if (!id) return err(PMG_ERR_VALUE, "null argument");
+    const Nccl *n = nccl();
+    if (!n) return err(PMG_ERR_VALUE, "libnccl.so.2 is not available");
+    ncclUniqueId u;
+    TRYN(n->get_unique_id(&u), "ncclGetUniqueId");
+    std::memcpy(id, &u, sizeof(u));
+    return PMG_OK;
+}
+
+int pmg_comm_create(const void *id, int nranks, int rank, pmg_comm **out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+        return err(PMG_ERR_VALUE, "comm_create: bad arguments");
+    const Nccl *n = nccl();
+    if (!n) return err(PMG_ERR_VALUE, "libnccl.so.2 is not available");
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    auto *c = new pmg_comm();
+    ncclResult_t r = n->comm_init_rank(&c->c, nranks, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return nccl_err(r, "ncclCommInitRank");
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c;
+    return PMG_OK;
+}
+
+int pmg_comm_destroy(pmg_comm *c) {
+    if (!c) return PMG_OK;
+    if (c->c && nccl()) nccl()->comm_destroy(c->c);
+    delete c;
+    return PMG_OK;
+}
+
+int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
+                     const pmg_part_desc *parts, const pmg_mg_desc *desc, pmg_comm *comm,
+                     int overlap_nx, pmg_phier **out) {
+    if (!levels || !parts || !desc || !out || nlev < 1 || nparts < 1)
+        return err(PMG_ERR_VALUE, "bad multi-part hierarchy arguments");
+    if (desc->nu_pre < 0 || desc->nu_post < 0 || desc->coarse_sweeps < 0)
+        return err(PMG_ERR_VALUE, "sweep counts must be non-negative");
+    if (!(desc->rho > 0.0 && desc->rho < 2.0))
+        return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
+    if (comm && (nparts != 1 || parts[0].worker != comm->rank))
+        return err(PMG_ERR_VALUE, "with a communicator each rank holds one part: its rank");
+    int maxw = -1;
+    for (int p = 0; p < nparts; ++p) {
+        if (parts[p].worker < 0 || (p && parts[p].worker <= parts[p - 1].worker))
+            return err(PMG_ERR_VALUE, "parts must be listed in ascending worker order");
+        maxw = std::max(maxw, parts[p].worker);
+        for (int a = 0; a < 4; ++a) maxw = std::max(maxw, parts[p].nbr[a]);
+    }
+    if (comm && maxw >= comm->nranks)
+        return err(PMG_ERR_VALUE, "a neighbour worker is not a rank of the communicator");
+    pmg_phier *h = new pmg_phier();
+    h->np = nparts;
+    h->nlev = nlev;
+    h->d = *desc;
+    h->comm = comm;
+    h->overlap_nx = overlap_nx;
+    h->mode_gen = pmg::g_mode_gen;
+    h->local.assign(maxw + 1, -1);
+    for (int p = 0; p < nparts; ++p) {
+        h->worker.push_back(parts[p].worker);
+        h->nbr.push_back({parts[p].nbr[0], parts[p].nbr[1], parts[p].nbr[2], parts[p].nbr[3]});
+        h->local[parts[p].worker] = p;
+    }
+    if (!comm)
+        for (int p = 0; p < nparts; ++p)
+            for (int a = 0; a < 4; ++a) {
+                const int nb = h->nbr[p][a];
+                if (nb >= 0 && h->local[nb] < 0) {
+                    free_phier(h);
+                    return err(PMG_ERR_VALUE, "without a communicator every neighbour must be "
+                                              "a part of this hierarchy");
+                }
+                if (nb >= 0 && h->nbr[h->local[nb]][OPP[a]] != parts[p].worker) {
+                    free_phier(h);
+                    return err(PMG_ERR_VALUE, "neighbour relation is not symmetric");
+                }
+            }
+    h->P.assign(nparts, std::vector<PL>(nlev));
+    cudaError_t e = cudaSuccess;
+    int rc = PMG_OK;
+    for (int p = 0; p < nparts && !rc && e == cudaSuccess; ++p) {
+        for (int c = 0; c < nlev && !rc && e == cudaSuccess; ++c) {
+            PL &q = h->P[p][c];
+            q.lv = levels[p * nlev + c];
+            if (!q.lv) {
+                rc = err(PMG_ERR_VALUE, "null level handle");
+                break;
+            }
+            rc = pmg_level_dims(q.lv, &q.nx, &q.ny, &q.nz);
+            if (rc) break;
+            const PL &q0 = h->P[p][0];
+            const PL &r0 = h->P[0][c];
+            if (c && (q.nx != (q0.nx >> c) || q.ny != (q0.ny >> c) || q.nz != q0.nz ||
+                      (q.nx << c) != q0.nx || (q.ny << c) != q0.ny)) {
+                rc = err(PMG_ERR_VALUE, "each level must halve nx and ny at equal nz");
+                break;
+            }
+            if (p && (q.nx != r0.nx || q.ny != r0.ny || q.nz != r0.nz)) {
+                rc = err(PMG_ERR_VALUE, "all parts of a level must have the same shape");
+                break;
+            }
+            const long long nd = pmg_level_field_doubles(q.lv);
+            if (c) {
+                e = cudaMalloc(&q.u, sizeof(double) * nd);
+                if (e == cudaSuccess) e = cudaMalloc(&q.f, sizeof(double) * nd);
+                if (e == cudaSuccess) e = cudaMemset(q.u, 0, sizeof(double) * nd);
+            }
+            for (int a = 0; a < 4 && e == cudaSuccess; ++a) {
+                q.fd[a] = pmg_face_doubles(q.lv, a);
+                if (h->nbr[p][a] < 0) continue;
+                e = cudaMalloc(&q.sb[a], sizeof(double) * q.fd[a]);
+                if (e == cudaSuccess && comm) e = cudaMalloc(&q.rb[a], sizeof(double) * q.fd[a]);
+            }
+        }
+    }
+    const long long ps = pmg_partials_size();
+    if (!rc && e == cudaSuccess) e = cudaMalloc(&h->scr[0], sizeof(double) * ps);
+    if (!rc && e == cudaSuccess) e = cudaMalloc(&h->scr[1], sizeof(double) * 1024);
+    if (!rc && e == cudaSuccess)
+        e = cudaMalloc(&h->slots, sizeof(double) * (nparts + (comm ? comm->nranks : 0) + 8));
+    if (!rc && e == cudaSuccess) e = cudaHostAlloc(&h->res_h, 8 * sizeof(double), cudaHostAllocMapped);
+    if (!rc && e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&h->res_d, h->res_h, 0);
+    if (!rc && e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);
+    if (!rc && e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->own, cudaStreamNonBlocking);
+    for (cudaEvent_t *ev : {&h->ev_fork, &h->ev_join, &h->ev_in, &h->ev_out})
+        if (!rc && e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (rc || e != cudaSuccess) {
+        free_phier(h);
+        if (rc) return rc;
+        TRYC(e, "multi-part hierarchy allocation");
+    }
+    *out = h;
+    return PMG_OK;
+}
+
+int pmg_phier_destroy(pmg_phier *h) {
+    if (h) free_phier(h);
+    return PMG_OK;
+}
+
+int pmg_phier_mg_solve(pmg_phier *h, const double *const *f, double *const *u, double eps,
+                       int maxiter, double *hist, int *iters, int *converged, void *stream) {
+    if (!h || !f || !u || !hist || !iters || !converged) return err(PMG_ERR_VALUE, "null argument");
+    if (maxiter < 0 || !(eps > 0.0)) return err(PMG_ERR_VALUE, "need eps > 0 and maxiter >= 0");
+    for (int p = 0; p < h->np; ++p)
+        if (!f[p] || !u[p]) return err(PMG_ERR_VALUE, "null field");
+    sync_mode(h);
+    return on_stream(h, stream, [&](cudaStream_t s) {
+        return mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, s);
+    });
+}
+
+int pmg_phier_vcycle(pmg_phier *h, double *const *u, const double *const *f, int first,
+                     void *stream) {
+    if (!h || !u || !f) return err(PMG_ERR_VALUE, "null argument");
+    sync_mode(h);
+    if (first && !(h->d.rho == 1.0 && h->nlev > 1 && h->d.nu_pre >= 1))
+        return err(PMG_ERR_VALUE, "first = 1 needs rho = 1, nu_pre >= 1 and two levels");
+    return on_stream(h, stream, [&](cudaStream_t s) { return vcycle(h, 0, u, f, first != 0, s); });
+}
+
+int pmg_phier_halo_exchange(pmg_phier *h, int level, double *const *fields, void *stream) {
+    if (!h || !fields || level < 0 || level >= h->nlev) return err(PMG_ERR_VALUE, "bad arguments");
+    return on_stream(h, stream, [&](cudaStream_t s) { return exchange(h, level, fields, s); });
+}
+
+int pmg_phier_dot(pmg_phier *h, int level, const double *const *a, const double *const *b,
+                  double *out, void *stream) {
+    if (!h || !a || !b || !out || level < 0 || level >= h->nlev)
+        return err(PMG_ERR_VALUE, "bad arguments");
+    return on_stream(h, stream, [&](cudaStream_t s) {
+        for (int p = 0; p < h->np; ++p)
+            TRY(pmg_dot(h->P[p][level].lv, a[p], b[p], h->scr[0], h->slots + p, s));
+        return global_sum(h, out, s);
+    });
+}
+
+long long pmg_phier_replayed_launches(const pmg_phier *h) { return h ? h->replayed : -1; }
+long long pmg_phier_exchanges(const pmg_phier *h) { return h ? h->exchanges : -1; }
+
+}  // extern "C"

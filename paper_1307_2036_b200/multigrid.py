@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from ._lib import MGDesc, call, load
+from ._lib import MGDesc, PartDesc, call, load
 from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
@@ -51,7 +51,10 @@ class MGConfig:
     the pre-smoothed residual is restricted from its red cells only (the
     black residual after the exact black line solves is zero), 14 instead
     of 18 bytes per cell -- fast smoother mode only (the exact mode stays
-    bit-identical to the reference).
+    bit-identical to the reference); ``overlap``: multi-part solves relax
+    the part boundaries first and exchange their halos while the interior
+    relaxes on levels of at least ``OVERLAP_NX`` columns per
+    part -- same values bit for bit.
     """
 
     nu_pre: int = 1
@@ -68,6 +71,7 @@ class MGConfig:
     graph: bool = True
     lagged_norm: bool = True
     red_restrict: bool = True
+    overlap: bool = True
 
     def __post_init__(self):
         if self.nu_pre < 0 or self.nu_post < 0 or self.nu_pre + self.nu_post < 1:
@@ -157,6 +161,19 @@ class LevelHierarchy:
             self._persist = self.make_scratch()
         return self._persist
 
+    def native_parts(self, cfg: "MGConfig") -> "NativePartsHierarchy":
+        """The multi-part device-resident driver (pmg_phier) of this
+        hierarchy for ``cfg`` (cached); under torch.distributed with NCCL it
+        runs over the library's own communicator."""
+        from .partition import native_comm
+        key = ("parts", cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), cfg.rho,
+               bool(cfg.red_restrict), bool(cfg.overlap))
+        h = self._native.get(key)
+        if h is None:
+            h = NativePartsHierarchy(self, cfg, native_comm() if _dist() is not None else None)
+            self._native[key] = h
+        return h
+
     def native(self, cfg: "MGConfig") -> "NativeHierarchy":
         """The device-resident driver (pmg_hier) of this single-part
         hierarchy for ``cfg``'s cycle shape (cached)."""
@@ -200,6 +217,56 @@ class NativeHierarchy:
     def replayed_launches(self) -> int:
         """Cumulative kernels issued by this driver's graph replays."""
         return int(self._lib.pmg_hier_replayed_launches(self.h))
+
+
+#: narrowest part (columns) that relaxes boundary-first in a multi-part solve
+OVERLAP_NX = 256
+
+
+class NativePartsHierarchy:
+    """Owner of a ``pmg_phier``: the C++ multi-part V-cycle / mg_solve driver
+    over every part this process holds (all of them in-process, or one per
+    rank with the library's NCCL communicator), halo exchanges and
+    reductions issued inside the captured cycle graph (include/pmg.h,
+    multi-part drivers)."""
+
+    def __init__(self, hier: LevelHierarchy, cfg: "MGConfig", comm=None):
+        lay = hier.fine.layout
+        ws = list(lay.local_workers)
+        self._levels = [[lev.op.handles[w] for lev in hier.levels] for w in ws]   # keep alive
+        flat = [h.h.value for hs in self._levels for h in hs]
+        arr = (C.c_void_p * len(flat))(*flat)
+        parts = (PartDesc * len(ws))()
+        for n, w in enumerate(ws):
+            parts[n].worker = w
+            for face, (di, dj) in enumerate(((-1, 0), (1, 0), (0, -1), (0, 1))):
+                nb = lay.neighbor(w, di, dj)
+                parts[n].nbr[face] = -1 if nb is None else nb
+        per = int(bool(lay.periodic))
+        d = MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), float(cfg.rho), per,
+                   per, 0, int(bool(cfg.red_restrict)))
+        h = C.c_void_p()
+        call("pmg_phier_create", arr, len(hier.levels), len(ws), parts, C.byref(d),
+             comm, OVERLAP_NX if cfg.overlap else 0, C.byref(h))
+        self.h = h
+        self.workers = ws
+        self._lib = load()
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h is not None and h.value:
+            self._lib.pmg_phier_destroy(h)
+            self.h = None
+
+    def replayed_launches(self) -> int:
+        return int(self._lib.pmg_phier_replayed_launches(self.h))
+
+    def exchanges(self) -> int:
+        return int(self._lib.pmg_phier_exchanges(self.h))
+
+    def ptrs(self, df: DistField):
+        return (C.c_void_p * len(self.workers))(*[df.parts[w].data.data_ptr()
+                                                  for w in self.workers])
 
 
 def _level_count(nx: int, pside: int, cfg: MGConfig) -> int:
@@ -460,6 +527,10 @@ class _CycleGraph:
 #: single-part graph solves run the C++ driver (pmg_mg_solve); False keeps
 #: the Python V-cycle (same kernels, same order: bit-identical results)
 USE_NATIVE = True
+#: multi-part solves (in-process parts, or one part per rank over NCCL) run
+#: the C++ multi-part driver (pmg_phier_mg_solve); False keeps the Python
+#: V-cycle (same kernels, same order: bit-identical results)
+USE_NATIVE_PARTS = True
 
 
 def _mg_solve_native(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out):
@@ -478,6 +549,38 @@ def _mg_solve_native(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out):
     torch.cuda.current_stream().synchronize()
     t0 = time.perf_counter()
     call("pmg_mg_solve", nh.h, fp.ptr, uf.ptr, float(cfg.eps), int(cfg.maxiter),
+         hist.ctypes.data_as(C.c_void_p), C.byref(iters), C.byref(conv), _stream())
+    wall = time.perf_counter() - t0
+    history = hist[:iters.value + 1].tolist()
+    if out is None:
+        u = u.copy()
+    return u, SolveReport(iters.value, history, bool(conv.value), wall, _echo(hier, cfg))
+
+
+def _parts_native_ok(hier: LevelHierarchy, cfg: MGConfig) -> bool:
+    """The multi-part native driver takes hierarchies without folding whose
+    parts all live here (in-process) or one per rank over NCCL."""
+    from .partition import native_comm_ok
+    if not (cfg.graph and cfg.fused and USE_NATIVE and not FUSE_PROLONG and len(hier) > 0):
+        return False
+    if any(lev.fold_layout is not None for lev in hier.levels):
+        return False
+    if _dist() is not None:
+        return native_comm_ok()
+    return True
+
+
+def _mg_solve_parts(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out):
+    """mg_solve through pmg_phier_mg_solve: every part's V-cycle, the halo
+    exchanges (boundary-first where the level allows) and the reductions in
+    one captured graph per cycle, one 8-byte host read per cycle."""
+    nh = hier.native_parts(cfg)
+    u = out if out is not None else hier.persistent_scratch()[0].u
+    hist = np.zeros(cfg.maxiter + 1)
+    iters, conv = C.c_int(), C.c_int()
+    torch.cuda.current_stream().synchronize()
+    t0 = time.perf_counter()
+    call("pmg_phier_mg_solve", nh.h, nh.ptrs(f), nh.ptrs(u), float(cfg.eps), int(cfg.maxiter),
          hist.ctypes.data_as(C.c_void_p), C.byref(iters), C.byref(conv), _stream())
     wall = time.perf_counter() - t0
     history = hist[:iters.value + 1].tolist()
@@ -513,9 +616,11 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
     half-sweep ignores u, exactly as f + drw*0 = f).
     """
     use_graph = cfg.graph and _dist() is None
-    if (use_graph and cfg.fused and USE_NATIVE and not FUSE_PROLONG
-            and hier.fine.layout.px == 1 and hier.fine.layout.py == 1):
+    single = hier.fine.layout.px == 1 and hier.fine.layout.py == 1 and _dist() is None
+    if (use_graph and cfg.fused and USE_NATIVE and not FUSE_PROLONG and single):
         return _mg_solve_native(f, hier, cfg, out)
+    if not single and USE_NATIVE_PARTS and _parts_native_ok(hier, cfg):
+        return _mg_solve_parts(f, hier, cfg, out)
     coarse = hier.persistent_scratch() if use_graph else hier.make_scratch()
     # iterate: the caller's ``out``; else the hierarchy's level-0 scratch
     # (graph reuse across calls), copied out at the end

@@ -53,6 +53,39 @@ def _dist():
     return None
 
 
+_COMM = None
+
+
+def native_comm_ok() -> bool:
+    """The library's own NCCL communicator can serve this process group:
+    torch.distributed over NCCL (device buffers), one GPU per rank, and
+    libnccl.so.2 loadable by the library."""
+    d = _dist()
+    return (d is not None and d.get_backend() == "nccl" and torch.cuda.is_available()
+            and bool(lib().pmg_comm_available()))
+
+
+def native_comm():
+    """The process-wide pmg_comm over the torch.distributed world (created
+    once: rank 0's NCCL unique id is broadcast through torch.distributed,
+    then ncclCommInitRank on every rank's current device)."""
+    global _COMM
+    if _COMM is None:
+        d = _dist()
+        if d is None:
+            raise ValueError("native_comm needs an initialised torch.distributed world")
+        uid = (C.c_ubyte * 128)()
+        if d.get_rank() == 0:
+            call("pmg_comm_unique_id", uid)
+        box = [bytes(uid)]
+        d.broadcast_object_list(box, src=0)
+        uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        comm = C.c_void_p()
+        call("pmg_comm_create", uid, d.get_world_size(), d.get_rank(), C.byref(comm))
+        _COMM = comm
+    return _COMM
+
+
 def _split_workers(workers: int):
     """px x py for a worker count: 4^p -> square (reference), 2 -> 2x1,
     8 -> 4x2 (BASELINE configs[3])."""
@@ -715,11 +748,21 @@ def scalar_buffer(n: int) -> torch.Tensor:
     return torch.zeros(n, dtype=torch.float64, device="cuda")
 
 
+def _ordered_sum(xs) -> float:
+    """Left-to-right sum from 0.0, the reference's worker loop
+    (partition.py:278-280; Python >= 3.12's ``sum`` of floats is
+    compensated, a different rounding)."""
+    total = 0.0
+    for x in xs:
+        total += x
+    return total
+
+
 def reduce_parts(vals: torch.Tensor) -> float:
     """Sum per-part scalars in part order, then over ranks."""
     if not vals.is_cuda and _dist() is None:   # host-mapped results
         torch.cuda.current_stream().synchronize()
-        return float(sum(vals.tolist()))
+        return _ordered_sum(vals.tolist())
     tot = vals.sum() if vals.numel() > 1 else vals[0]
     d = _dist()
     if d is not None:
@@ -731,7 +774,7 @@ def reduce_parts(vals: torch.Tensor) -> float:
             t = t.cpu()
         allp = [torch.empty_like(t) for _ in range(d.get_world_size())]
         d.all_gather(allp, t)
-        return float(sum(torch.cat(allp).cpu().tolist()))   # one device -> host copy
+        return _ordered_sum(torch.cat(allp).cpu().tolist())   # one device -> host copy
     return float(tot.item())
 
 

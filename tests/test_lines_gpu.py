@@ -193,7 +193,7 @@ def test_breakdown_native_negative_mass(pmg, precond):
     vprof[1:nz] = 1.0 / dz[:-1]
     vprof[0], vprof[nz] = 2.0 / dz[0], 2.0 / dz[-1]
     one = np.ones(1)
-    h = LevelHandle(n, n, nz, 0, 0, 1e-3, 1e-3, dz, vprof, -1e3 * dz,
+    h = LevelHandle(n, n, nz, 0, 0, 1e-3, 1e-3, dz, vprof, -1e5 * dz,
                     np.broadcast_to(one, (n, n + 1)), np.broadcast_to(one, (n + 1, n)),
                     np.broadcast_to(one / n**2, (n, n)), np.broadcast_to(one / n**2, (n, n)),
                     np.broadcast_to(4 * one, (n, n)))

@@ -32,7 +32,7 @@ def frame_and_interior(nstrip, ny):
 
 
 @pytest.mark.parametrize("nx,ny,nz", [(256, 64, 128), (512, 512, 128), (1024, 256, 128),
-                                      (128, 96, 32), (192, 40, 64)])
+                                      (128, 64, 32), (2048, 16, 128)])
 def test_region_sweep_matches_whole(pmg, nx, ny, nz):
     from paper_1307_2036_b200 import _lib
     lib = _lib.load()

@@ -1,0 +1,178 @@
+"""Native multi-part driver (pmg_phier, pmg_parts.cu) on the device.
+
+* In-process decompositions (2x1, 1x2, 2x2, 4x2; periodic and mirror): the
+  native driver -- every part's V-cycle, the halo exchanges and the
+  worker-order reductions captured in one graph per cycle -- gives the
+  Python multi-part driver's iterates and histories bit for bit, with and
+  without boundary-first overlap (frame regions relaxed first, their halo
+  exchange on a second stream while the interior relaxes); and it agrees
+  with the single-part solve of the same global grid to the reference's
+  partition-invariance tolerance (tests/test_partition.py:122-154).
+* The NCCL transport: a one-rank library communicator whose part is its
+  own periodic neighbour sends every halo strip to itself through
+  ncclSend / ncclRecv (captured in the cycle graph) and reduces through
+  ncclAllGather; iterates equal the in-process driver's bit for bit.  (Only
+  one GPU is available; ranks on separate GPUs run the same code with other
+  peers -- the per-pair message order is checked on CPU in test_parts.py.)
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pmg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1307_2036_b200 as m
+    return m
+
+
+def uni(shape, seed):
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, size=shape)
+
+
+def solve(pmg, grid, params, fg, px, py, native, overlap=True, levels=4, exact=False):
+    from paper_1307_2036_b200 import multigrid as mg
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=levels, overlap=overlap)
+    dec = pmg.Decomposition(grid.nx, px * py, ny=grid.ny, px=px, py=py)
+    hier = pmg.build_hierarchy(grid, params, cfg, dec)
+    f = pmg.scatter_owned(fg, hier.fine.layout)
+    prev = mg.USE_NATIVE_PARTS
+    mg.USE_NATIVE_PARTS = native
+    try:
+        with pmg.exact_smoother(exact):
+            u, rep = pmg.mg_solve(f, hier, cfg)
+            # a second solve replays the captured graphs
+            u2, rep2 = pmg.mg_solve(f, hier, cfg)
+    finally:
+        mg.USE_NATIVE_PARTS = prev
+    assert rep2.residual_history == rep.residual_history
+    g = pmg.gather_owned(u)
+    assert np.array_equal(g, pmg.gather_owned(u2))
+    return g, rep, hier
+
+
+CASES = [  # (nx, ny, nz, px, py, periodic)
+    (512, 256, 32, 2, 1, True),
+    (256, 512, 32, 1, 2, True),
+    (512, 512, 32, 2, 2, True),
+    (1024, 512, 32, 4, 2, True),
+    (512, 512, 32, 2, 2, False),
+    (64, 32, 16, 2, 2, True),
+]
+
+
+@pytest.mark.parametrize("nx,ny,nz,px,py,periodic", CASES)
+def test_native_parts_match_python(pmg, nx, ny, nz, px, py, periodic):
+    if periodic:
+        grid = pmg.periodic_box(nx, nz, 0.01, ny=ny)
+    else:
+        grid = pmg.panel_grid(nx, nz, flat_mode=True)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    fg = uni((nx, ny, nz), 3)
+    levels = 4 if min(nx, ny) >= 64 else 3
+    ref, rep_ref, _ = solve(pmg, grid, params, fg, px, py, native=False, levels=levels)
+    for overlap in (True, False):
+        got, rep, hier = solve(pmg, grid, params, fg, px, py, native=True, overlap=overlap,
+                               levels=levels)
+        assert rep.iterations == rep_ref.iterations
+        assert rep.residual_history == rep_ref.residual_history, overlap
+        assert np.array_equal(got, ref), overlap
+    # the native driver really ran: its graphs replayed library kernels
+    nh = hier.native_parts(pmg.MGConfig(policy="explicit", explicit_levels=levels,
+                                        overlap=overlap))
+    assert nh.replayed_launches() > 0 and nh.exchanges() > 0
+    # partition invariance against the single-part solve (<= 1e-10)
+    one, rep1, _ = solve(pmg, grid, params, fg, 1, 1, native=True, levels=levels)
+    assert rep1.iterations == rep.iterations
+    h, h1 = np.array(rep.residual_history), np.array(rep1.residual_history)
+    assert np.max(np.abs(h - h1) / (h1 + 1e-13 * h1[0])) <= 1e-10
+    assert np.max(np.abs(got - one)) <= 1e-10 * np.max(np.abs(one))
+
+
+def test_native_parts_exact_mode(pmg):
+    """Exact smoother: no tile regions (overlap off by construction), the
+    same native sequence, bit-identical to the Python driver."""
+    grid = pmg.periodic_box(128, 16, 0.01)
+    params = pmg.toy_parameters(128, 16, 1e-3, 1.0)
+    fg = uni((128, 128, 16), 4)
+    ref, r0, _ = solve(pmg, grid, params, fg, 2, 2, native=False, exact=True)
+    got, r1, _ = solve(pmg, grid, params, fg, 2, 2, native=True, exact=True)
+    assert r0.residual_history == r1.residual_history
+    assert np.array_equal(got, ref)
+
+
+def _nccl_self_hier(pmg, hier, cfg):
+    from paper_1307_2036_b200 import _lib
+    lib = _lib.load()
+    if not lib.pmg_comm_available():
+        pytest.skip("libnccl.so.2 not loadable")
+    uid = (C.c_ubyte * 128)()
+    _lib.call("pmg_comm_unique_id", uid)
+    comm = C.c_void_p()
+    _lib.call("pmg_comm_create", uid, 1, 0, C.byref(comm))
+    lay = hier.fine.layout
+    (w,) = lay.local_workers
+    levels = [lev.op.handles[w].h.value for lev in hier.levels]
+    arr = (C.c_void_p * len(levels))(*levels)
+    parts = (_lib.PartDesc * 1)()
+    parts[0].worker = 0
+    for a in range(4):
+        parts[0].nbr[a] = 0          # its own periodic neighbour, through NCCL
+    d = _lib.MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), 1.0, 1, 1, 0, 1)
+    h = C.c_void_p()
+    _lib.call("pmg_phier_create", arr, len(levels), 1, parts, C.byref(d), comm, 256,
+              C.byref(h))
+    return lib, comm, h, w
+
+
+@pytest.mark.parametrize("nx,nz", [(512, 32), (64, 16)])
+def test_nccl_self_exchange_matches(pmg, nx, nz):
+    from paper_1307_2036_b200 import _lib, multigrid as mg
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=4 if nx >= 64 else 3)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    fg = uni((nx, nx, nz), 5)
+    f = pmg.scatter_owned(fg, hier.fine.layout)
+    # reference: the Python single-part driver (pmg_halo_self exchanges)
+    prev = mg.USE_NATIVE
+    mg.USE_NATIVE = False
+    try:
+        uref, rref = pmg.mg_solve(f, hier, cfg)
+    finally:
+        mg.USE_NATIVE = prev
+    lib, comm, h, w = _nccl_self_hier(pmg, hier, cfg)
+    try:
+        u = pmg.DistField.zeros(hier.fine.layout, nz)
+        hist = np.zeros(cfg.maxiter + 1)
+        iters, conv = C.c_int(), C.c_int()
+        fp = (C.c_void_p * 1)(f.parts[w].data.data_ptr())
+        up = (C.c_void_p * 1)(u.parts[w].data.data_ptr())
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for _ in range(2):   # capture, then replay
+            _lib.call("pmg_phier_mg_solve", h, fp, up, float(cfg.eps), int(cfg.maxiter),
+                      hist.ctypes.data_as(C.c_void_p), C.byref(iters), C.byref(conv), st)
+            assert iters.value == rref.iterations and conv.value == 1
+            assert hist[:iters.value + 1].tolist() == rref.residual_history
+            assert np.array_equal(pmg.gather_owned(u), pmg.gather_owned(uref))
+        assert lib.pmg_phier_exchanges(h) > 0
+        # the standalone exchange and dot entry points over NCCL
+        v = pmg.scatter_owned(uni((nx, nx, nz), 6), hier.fine.layout)
+        ref = v.copy()
+        pmg.halo_exchange(ref)
+        vp = (C.c_void_p * 1)(v.parts[w].data.data_ptr())
+        _lib.call("pmg_phier_halo_exchange", h, 0, vp, st)
+        assert torch.equal(v.parts[w].data, ref.parts[w].data)
+        out = torch.zeros(1, dtype=torch.float64, device="cuda")
+        _lib.call("pmg_phier_dot", h, 0, vp, vp, C.c_void_p(out.data_ptr()), st)
+        assert float(out.item()) == pytest.approx(pmg.dist_dot(v, v), rel=1e-14)
+    finally:
+        lib.pmg_phier_destroy(h)
+        lib.pmg_comm_destroy(comm)

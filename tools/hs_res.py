@@ -11,7 +11,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1307_2036_b200 as pmg  # noqa: E402
 from paper_1307_2036_b200 import _lib, configs  # noqa: E402
 
-prob = configs.config(1)
+NX = int(os.environ.get("NX", "1024"))
+prob = configs.Problem(NX, NX, 128, 1e-3, 1.0, 1)
 cfg = prob.mg_config()
 hier = pmg.build_hierarchy(prob.grid(), prob.params(), pmg.MGConfig(policy="explicit",
                                                                     explicit_levels=1))

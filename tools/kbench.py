@@ -48,6 +48,7 @@ ap.add_argument("--nz", type=int, default=128)
 ap.add_argument("--ny", type=int, default=0)
 ap.add_argument("--levels", type=int, default=7)
 ap.add_argument("--variable", action="store_true")
+ap.add_argument("--no-solve", action="store_true")
 a = ap.parse_args()
 a.ny = a.ny or a.nx
 prob = configs.Problem(a.nx, a.ny, a.nz, 1e-3, 1.0, a.levels, stretch=1.05 if a.variable else None,
@@ -105,7 +106,7 @@ for c, lev in enumerate(hier.levels):
     print(f"L{c} nx={lev.layout.nx}: " + json.dumps(row), flush=True)
 # full solve (lagged convergence norm on / off)
 import dataclasses  # noqa: E402
-for lag, red in ((True, True), (True, False), (False, False)):
+for lag, red in () if a.no_solve else ((True, True), (True, False), (False, False)):
     cfg = dataclasses.replace(cfg, lagged_norm=lag, red_restrict=red)
     for _ in range(2):
         u, rep = pmg.mg_solve(f, hier, cfg)
