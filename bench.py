@@ -402,8 +402,14 @@ def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
     barrier(world)
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    native = s.lay.px == 1 and s.lay.py == 1 and mgm.USE_NATIVE
-    r0_graph = s.hier.native(s.cfg).replayed_launches() if native else 0
+    native = s.lay.px == 1 and s.lay.py == 1 and mgm.USE_NATIVE and world == 1
+    parts = (not native and mgm.USE_NATIVE_PARTS and mgm._parts_native_ok(s.hier, s.cfg))
+    if native:
+        r0_graph = s.hier.native(s.cfg).replayed_launches()
+    elif parts:
+        r0_graph = s.hier.native_parts(s.cfg).replayed_launches()
+    else:
+        r0_graph = 0
     l0 = lib.pmg_launch_count()
     iters = []
     ctx = sampler if sampler is not None else _Null()
@@ -420,6 +426,8 @@ def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
     launches = lib.pmg_launch_count() - l0
     if native:
         launches += s.hier.native(s.cfg).replayed_launches() - r0_graph
+    elif parts:
+        launches += s.hier.native_parts(s.cfg).replayed_launches() - r0_graph
     else:
         gkey = mgm.graph_key(s.cfg, s.f, s.u)
         g_first = s.hier._graphs.get(gkey + (True,))
@@ -432,7 +440,10 @@ def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
     return {"t": t, "solve_ms": t / steps * 1e3, "iterations": iters[-1],
             "v_cycle_ms": t / sum(iters) * 1e3, "dof_s": s.prob.dof * steps / t,
             "residual_history": [float(x) for x in reps[-1].residual_history],
-            "launches": int(launches)}
+            "launches": int(launches),
+            "driver": ("pmg_mg_solve (single part, lagged norm, wrap views)" if native else
+                       "pmg_phier_mg_solve (multi-part: in-graph NCCL halos + reductions, "
+                       "boundary-first overlap)" if parts else "python multi-part V-cycle")}
 
 
 class _Null:
@@ -625,7 +636,7 @@ def main():
         "solve_ms": r["solve_ms"], "v_cycle_ms": r["v_cycle_ms"],
         "residual_history": r["residual_history"],
         "roofline": roofline, "kernels": kern, "e2e": e2e,
-        "gpu_launches": r["launches"],
+        "gpu_launches": r["launches"], "driver": r["driver"],
         "clocks": sampler.summary(),
     }
     if extra is not None:

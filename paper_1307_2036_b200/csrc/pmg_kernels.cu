@@ -1440,60 +1440,85 @@ static size_t band_smem();
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void bar_compute() {   // the 8 compute warps only
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+template <int NW>
+__device__ __forceinline__ void bar_compute() {   // the NW compute warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory");
 }
 
-// (A fused-residual mode -- the lagged norm's red sweep, with the incoming
-// red values loaded from HBM into registers at each step -- ran at 501 us
-// against 413 us for k_half_sweep_seg's: not kept.)
+// RES (rho = 1): the lagged norm's fused red sweep (k_half_sweep_seg's
+// RES = 1 mode): u is only read -- the relaxed values go to uw -- and
+// partials[blockIdx.x] receives this CTA's sum of (f - A u)^2 over its
+// cells of the incoming iterate, formed from the sweep's own line
+// right-hand side; each lane loads its column's incoming values (its
+// levels and one on either side) at the start of the row step.
 // DOT: also partials[blockIdx.x] = this CTA's sum of f * (new value) over
 // its cells (CG's <r, z> fused into the SSOR half-sweeps, as
 // k_half_sweep_seg's DOT mode); the f row is then released after the store.
 // FSQ: partials[blockIdx.x] = this CTA's sum of f^2 (mg_solve's ||f|| in the
 // first cycle, k_half_sweep_seg's RES = 3 mode).
-template <int PLC, bool DOT = false, bool FSQ = false, bool LEAN = false>
-__global__ void __launch_bounds__(288, 1)
+// NW: compute warps (8: 16 levels each, the level's own segment tables;
+// 16: 8 levels each, 8-level segment products formed in the prologue)
+template <int PLC, bool DOT = false, bool FSQ = false, bool LEAN = false, int NW = 8,
+          bool RES = false>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
 k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
                   double post_scale, int nstrip, int nband, int band_rows,
                   const __grid_constant__ CUtensorMap mF, const __grid_constant__ CUtensorMap mB,
-                  const __grid_constant__ CUtensorMap mE, double *__restrict__ partials) {
-    constexpr int SEG = 16, NZ = BAND_NZ, B = 4;
+                  const __grid_constant__ CUtensorMap mE, double *__restrict__ partials,
+                  double *__restrict__ uw) {
+    constexpr int NZ = BAND_NZ, SEG = NZ / NW, B = 4;
     extern __shared__ __align__(128) double bsm_raw[];
     double *bsm = bsm_raw + (((128u - (smem_u32(bsm_raw) & 127u)) & 127u) >> 3);
     // (TMA box starts must be 16-byte aligned: the other colour's row is
-    // three boxes, columns h0 .. h0 + 31 and the 2-column edges h0 - 2,
-    // h0 - 1 and h0 + 32, h0 + 33 -- the periodic image's on a wrap view)
+    // two boxes, columns h0 .. h0 + 31 and the 2-column edge the row's
+    // colour parity needs -- h0 - 2, h0 - 1 (W of lane 0) or h0 + 32,
+    // h0 + 33 (E of lane 31), the periodic image's on a wrap view)
     double *ring = bsm;                              // [4][NZ][32] other colour rows
     double *fring = ring + 4 * NZ * BAND_W;          // [2][NZ][32] f rows
-    double *ewr = fring + 2 * NZ * 32;               // [4][NZ][2]  W edge columns
-    double *eer = ewr + 4 * NZ * 2;                  // [4][NZ][2]  E edge columns
-    double2 *ti = reinterpret_cast<double2 *>(eer + 4 * NZ * 2);
+    double *edge = fring + 2 * NZ * 32;              // [4][NZ][2]  edge columns
+    double2 *ti = reinterpret_cast<double2 *>(edge + 4 * NZ * 2);
     double2 *tb = ti + NZ;
-    double *tq = reinterpret_cast<double *>(tb + NZ);
-    double *tdrw = tq + NZ;
-    double *hend = tdrw + NZ;                         // [8][32]
-    double *ybeg = hend + 8 * 32;                     // [8][32]
-    uint64_t *fullB = reinterpret_cast<uint64_t *>(ybeg + 8 * 32);   // [4]
+    double2 *tw = tb + NZ;                           // (iota drw wx0, iota drw wy0)
+    double2 *tr1 = tw + NZ;                          // RES: (1 / iota, diag)
+    double2 *tr2 = tr1 + NZ;                         // RES: (bm, bp), zero-padded
+    double *tq = reinterpret_cast<double *>(tr2 + NZ);
+    double *hend = tq + NZ;                           // [NW][32]
+    double *ybeg = hend + NW * 32;                    // [NW][32]
+    uint64_t *fullB = reinterpret_cast<uint64_t *>(ybeg + NW * 32);  // [4]
     uint64_t *fullF = fullB + 4;                                     // [2]
     uint64_t *emptyB = fullF + 2;                                    // [4]
     uint64_t *emptyF = emptyB + 4;                                   // [2]
-    double *wsum = reinterpret_cast<double *>(emptyF + 2);           // DOT: [8]
+    double *wsum = reinterpret_cast<double *>(emptyF + 2);           // DOT: [NW]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < NZ; t += blockDim.x) {
-        tdrw[t] = L.drw[t];
+        const double io = L.invd1[t], dd = io * L.drw[t];
+        tw[t] = make_double2(dd * L.wx0, dd * L.wy0);
+        if (RES) {
+            tr1[t] = make_double2(1.0 / io, L.diag1[t]);
+            tr2[t] = make_double2((t >= 1) ? L.band1[t] : 0.0, (t + 1 < NZ) ? L.band1[t + 1] : 0.0);
+        }
         ti[t] = make_double2(L.invd1[t], L.segtab[t]);
-        tb[t] = make_double2(L.segtab[2 * NZ + t], L.segtab[NZ + t]);
-        tq[t] = L.segtab[3 * NZ + t];
+        double pf = L.segtab[2 * NZ + t], qq = L.segtab[3 * NZ + t];
+        if (SEG != 16) {
+            // products of alpha from the segment start to t and of mu from
+            // the segment end down to t (the host's order, pmg_level_create)
+            const int a = t / SEG * SEG, b = a + SEG - 1;
+            pf = 1.0;
+            for (int k = a; k <= t; ++k) pf *= L.segtab[k];
+            qq = 1.0;
+            for (int k = b; k >= t; --k) qq *= L.segtab[NZ + k];
+        }
+        tb[t] = make_double2(pf, L.segtab[NZ + t]);
+        tq[t] = qq;
     }
     if (threadIdx.x == 0) {
         for (int q = 0; q < 4; ++q) {
             mbar_init(fullB + q, 1);
-            mbar_init(emptyB + q, 8);
+            mbar_init(emptyB + q, NW);
         }
         for (int q = 0; q < 2; ++q) {
             mbar_init(fullF + q, 1);
-            mbar_init(emptyF + q, 8);
+            mbar_init(emptyF + q, NW);
         }
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1501,7 +1526,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
     const bool wrap = (L.hflags & HF_WRAP) != 0;
     const int hrow = L.nx / 2;                       // cells of one colour per row
     const int nunits = nstrip * nband;
-    if (w == 8) {
+    if (w == NW) {
         // ---- producer warp: streams every row of this CTA's units in the
         // consumers' order; a slot is refilled once all 8 compute warps have
         // released its previous row (empty barriers) ----
@@ -1514,7 +1539,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             const int j0 = L.ry0 + band * band_rows, j1 = min(L.ry0 + L.ryn, j0 + band_rows);
             if (j0 >= j1) continue;
             const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
-            const uint32_t bytesb = NZ * BAND_W * 8 + 2 * NZ * 2 * 8;
+            const uint32_t bytesb = NZ * BAND_W * 8 + NZ * 2 * 8;
             const int xw = eleft ? OFF + hrow - 2 : OFF + h0 - 2;
             const int xe = eright ? OFF : OFF + h0 + 32;
             // black rows j0 - 1 .. j1 and f rows j0 .. j1 - 1, interleaved as
@@ -1527,8 +1552,10 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                 fence_proxy_async();
                 mbar_expect_tx(fullB + slot, bytesb);
                 tma_box3(ring + slot * NZ * BAND_W, &mB, OFF + h0, 0, rr + 1, fullB + slot);
-                tma_box3(ewr + slot * NZ * 2, &mE, xw, 0, rr + 1, fullB + slot);
-                tma_box3(eer + slot * NZ * 2, &mE, xe, 0, rr + 1, fullB + slot);
+                // as the centre row r, the W neighbour of lane 0 (colour
+                // parity 0) or the E neighbour of lane 31 (parity 1)
+                tma_box3(edge + slot * NZ * 2, &mE, ((r + L.par + c) & 1) ? xe : xw, 0, rr + 1,
+                         fullB + slot);
                 ++nb;
             };
             auto put_f = [&](int r) {
@@ -1548,7 +1575,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
         }
         return;
     }
-    // ---- 8 compute warps ----
+    // ---- NW compute warps ----
     const int o = c ^ 1;
     (void)o;
     constexpr long long pl = PLC;                    // plane stride (compile time)
@@ -1562,6 +1589,18 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
         const int h0 = strip * 32;
         const int j0 = L.ry0 + band * band_rows, j1 = min(L.ry0 + L.ryn, j0 + band_rows);
         if (j0 >= j1) continue;
+        // RES: the incoming values of this lane's column (levels k0 - 1 ..
+        // k0 + SEG; the clamped out-of-column loads meet zero couplings),
+        // loaded one row step ahead so the loads overlap a column solve
+        double vo[RES ? SEG : 1], um = 0.0, un = 0.0;
+        auto load_old = [&](int jj) {
+            const long long p0 = at(L, c, k0, jj, h0 + lane);
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) vo[e] = u[p0 + (long long)e * pl];
+            um = u[p0 - ((k0 > 0) ? pl : 0)];
+            un = u[p0 + (long long)((k0 + SEG < NZ) ? SEG : SEG - 1) * pl];
+        };
+        if (RES) load_old(j0);
         for (int j = j0; j < j1; ++j) {
             const long long pc = at(L, c, k0, j, h0 + lane);
             // black row r of this unit = sequence seqb + r - (j0 - 1)
@@ -1575,8 +1614,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             const double *Srow = ring + (qs & 3) * NZ * BAND_W;
             const double *Crow = ring + ((qs + 1) & 3) * NZ * BAND_W;
             const double *Nrow = ring + ((qs + 2) & 3) * NZ * BAND_W;
-            const double *Cw = ewr + ((qs + 1) & 3) * NZ * 2;
-            const double *Cx = eer + ((qs + 1) & 3) * NZ * 2;
+            const double *Ce = edge + ((qs + 1) & 3) * NZ * 2;
             const double *Frow = fring + (qf & 1) * NZ * 32;
             const int s0 = (j + L.par + c) & 1;
             // W / E columns of this lane: h0 + lane - 1 + s0 and h0 + lane + s0
@@ -1585,6 +1623,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
             const int iw = max(lane - 1 + s0, 0), ie = min(lane + s0, 31);
             const bool wfix = s0 == 0 && lane == 0, efix = s0 == 1 && lane == 31;
             double r[SEG];
+            double rpend = 0.0, bpend = 0.0;
 #pragma unroll
             for (int b8 = 0; b8 < SEG; b8 += B) {
 #pragma unroll
@@ -1592,21 +1631,37 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                     const int k = k0 + b8 + e;
                     const double *cr = Crow + k * BAND_W;
                     double vw = cr[iw], ve = cr[ie];
-                    if (wfix) vw = Cw[k * 2 + 1];
-                    if (efix) ve = Cx[k * 2 + 0];
+                    if (wfix) vw = Ce[k * 2 + 1];
+                    if (efix) ve = Ce[k * 2 + 0];
                     const double vs = Srow[k * BAND_W + lane];
                     const double vn = Nrow[k * BAND_W + lane];
-                    const double2 ia = ti[k];
                     const double fv = Frow[k * 32 + lane];
                     if (FSQ) dacc = __fma_rn(fv, fv, dacc);
-                    double g = ia.x * fv;
-                    // k_half_sweep_seg's tw table, formed on the fly
-                    const double dd = ia.x * tdrw[k];
-                    const double2 cw = make_double2(dd * L.wx0, dd * L.wy0);
+                    double g = ti[k].x * fv;
+                    const double2 cw = tw[k];
                     g = __fma_rn(cw.y, vs + vn, g);
                     g = __fma_rn(cw.x, vw + ve, g);
                     r[b8 + e] = g;
+                    if (RES) {
+                        // residual of level k - 1 completes with u_k; level
+                        // k's waits for u_{k+1} (k_half_sweep_seg's order)
+                        const double2 t1 = tr1[k], t2 = tr2[k];
+                        const double vk = vo[b8 + e];
+                        if (b8 + e > 0) {
+                            const double q = __fma_rn(bpend, vk, rpend);
+                            dacc = __fma_rn(q, q, dacc);
+                        }
+                        const double tu = __fma_rn(-t2.x, um, t1.y * vk);   // d u_k - bm u_{k-1}
+                        rpend = __fma_rn(g, t1.x, -tu);                   // rhs_k - that
+                        bpend = t2.y;
+                        um = vk;
+                    }
                 }
+            }
+            if (RES) {
+                const double q = __fma_rn(bpend, un, rpend);
+                dacc = __fma_rn(q, q, dacc);
+                if (j + 1 < j1) load_old(j + 1);
             }
             // this warp is done with the S row and f row j (and, at the
             // unit's last row, with rows j and j + 1)
@@ -1627,7 +1682,7 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                 r[e] = hp;
             }
             hend[w * 32 + lane] = hp;
-            bar_compute();
+            bar_compute<NW>();
             double G = 0.0;
             for (int sgm = 0; sgm < w; ++sgm)
                 G = __fma_rn(tb[(sgm + 1) * SEG - 1].x, G, hend[sgm * 32 + lane]);
@@ -1640,21 +1695,23 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
                 r[e] = yp;
             }
             ybeg[w * 32 + lane] = yp;
-            bar_compute();
+            bar_compute<NW>();
             double X = 0.0;
-            for (int sgm = 7; sgm > w; --sgm) X = __fma_rn(tq[sgm * SEG], X, ybeg[sgm * 32 + lane]);
+            for (int sgm = NW - 1; sgm > w; --sgm)
+                X = __fma_rn(tq[sgm * SEG], X, ybeg[sgm * 32 + lane]);
 #pragma unroll
             for (int e = 0; e < SEG; ++e) {
                 double y = __fma_rn(tq[k0 + e], X, r[e]);
                 const long long q = pc + (long long)e * pl;
-                // LEAN: rho = 1 without zero start at compile time
-                if (!LEAN && zero_start) {
+                // LEAN (and RES): rho = 1 without zero start at compile time
+                if (!LEAN && !RES && zero_start) {
                     if (scale != 1.0) y = y * scale;
-                } else if (!LEAN && rho != 1.0) {
+                } else if (!LEAN && !RES && rho != 1.0) {
                     y = y * rho;
                     y = y + omr * u[q];
                 }
-                u[q] = y;
+                if (RES) uw[q] = y;
+                else u[q] = y;
                 if (DOT) dacc += Frow[(k0 + e) * 32 + lane] * y;
             }
             if (DOT) {   // the f row is free only now
@@ -1665,13 +1722,13 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
         seqb += (unsigned)(j1 - j0 + 2);
         seqf += (unsigned)(j1 - j0);
     }
-    if (DOT || FSQ) {   // fixed-order reduction over the compute warps
+    if (DOT || FSQ || RES) {   // fixed-order reduction over the compute warps
         const double ws = warp_sum(dacc);
         if (lane == 0) wsum[w] = ws;
-        bar_compute();
+        bar_compute<NW>();
         if (threadIdx.x == 0) {
             double t = 0.0;
-            for (int q = 0; q < 8; ++q) t += wsum[q];
+            for (int q = 0; q < NW; ++q) t += wsum[q];
             partials[blockIdx.x] = t;
         }
     }
@@ -2852,7 +2909,8 @@ bool half_sweep_dot_ok(const Lvl &L) {
 
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
                                    double rho, int zero_start, int nbr_zero, double post_scale,
-                                   cudaStream_t st, double *partials, int *np, bool fsq);
+                                   cudaStream_t st, double *partials, int *np, bool fsq,
+                                   double *res_uw = nullptr);
 
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
                                   int zero_start, int nbr_zero, double post_scale,
@@ -2944,6 +3002,11 @@ cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, con
         launch_segv_mode<1>(L, const_cast<double *>(u), uw, f, 0, 0, partials, np, st);
         return cudaGetLastError();
     }
+    // the TMA band kernel (16 compute warps) where the level's half-sweeps
+    // run on it: same column solves as those sweeps
+    if (launch_half_sweep_band(L, const_cast<double *>(u), f, 0, 1.0, 0, 0, 1.0, st, partials, np,
+                               false, uw))
+        return cudaGetLastError();
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const int nw = L.nz / 16;
     const size_t sm = sizeof(double) * (11 * (size_t)L.nz + 4 * 16 * 32);
@@ -3050,44 +3113,36 @@ cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const d
     return e;
 }
 
+template <int P, int NW>
+static void band_attrs_nw() {
+    const int sm = (int)band_smem();
+    cudaFuncSetAttribute(k_half_sweep_band<P, false, false, false, NW>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_band<P, false, false, true, NW>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_band<P, true, false, false, NW>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_band<P, false, true, false, NW>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+template <int P>
+static void band_attrs() {
+    band_attrs_nw<P, 8>();
+    band_attrs_nw<P, 16>();
+    cudaFuncSetAttribute(k_half_sweep_band<P, false, false, true, 16, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
+}
+
 // one-time kernel attributes (outside any stream capture: called from
 // pmg_level_create)
 void setup_kernel_attributes() {
     static bool done = false;
     if (done) return;
     done = true;
-    cudaFuncSetAttribute(k_half_sweep_band<520>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<264>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<136>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<1032>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<1032, false, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<520, false, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<264, false, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<136, false, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<1032, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<1032, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<520, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<520, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<264, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<136, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<264, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
-    cudaFuncSetAttribute(k_half_sweep_band<136, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)band_smem());
+    band_attrs<1032>();
+    band_attrs<520>();
+    band_attrs<264>();
+    band_attrs<136>();
     cudaGetLastError();
 }
 
@@ -3159,9 +3214,11 @@ static bool launch_half_sweep_tx(const Lvl &L, double *u, const double *f, int c
 
 // k_half_sweep_band: configs[1]'s fine level shape (nz = 128, plane 520),
 // neighbours read, no fused halo
-static size_t band_smem() {
-    return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 2 * 4 * BAND_NZ * 2 +
-                             6 * BAND_NZ + 2 * 8 * 32 + 8) + 12 * 8 + 128;
+static size_t band_smem() {   // sized for up to 16 compute warps
+    // rings (4 other-colour rows, 2 f rows, 4 edge pairs), tables ti tb tw
+    // tr1 tr2 (double2) and tq, hend / ybeg, barriers, warp sums
+    return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 4 * BAND_NZ * 2 +
+                             11 * BAND_NZ + 2 * 16 * 32 + 16) + 12 * 8 + 128;
 }
 
 static bool band_on() {
@@ -3169,6 +3226,12 @@ static bool band_on() {
     if (v < 0) v = getenv("PMG_BAND") ? atoi(getenv("PMG_BAND")) : 1;
     return v == 1;
 }
+
+// compute warps of k_half_sweep_band: 16 (8 levels each) on rows of >= 512
+// cells per colour -- 2048^2: 1214 -> 1008 us, 1024^2: 284 -> 260 us per
+// half-sweep -- and 8 (16 levels each) below, where 16 warps measured slower
+// (512^2: 71.4 -> 75.5 us, 256^2: 20.9 -> 23.5 us)
+static int band_nw(const Lvl &L) { return (L.nx / 2 >= 512) ? 16 : 8; }
 
 static bool band_l1() {   // level 2 (nx = 256) on the band kernel too
     static int v = -1;
@@ -3179,7 +3242,7 @@ static bool band_l1() {   // level 2 (nx = 256) on the band kernel too
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
                                    double rho, int zero_start, int nbr_zero, double post_scale,
                                    cudaStream_t st, double *partials, int *np,
-                                   bool fsq = false) {
+                                   bool fsq, double *res_uw) {
     const int hrow = L.nx / 2;
     if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
         !(L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
@@ -3187,6 +3250,9 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
         L.seg != 16 || nbr_zero || (L.hflags & 1) || L.nx % 2 || hrow % 32 || hrow < 64 ||
         L.ny < 8 || L.rys != 1 || L.rxn < 1 || L.ryn < 1)
         return false;
+    // the fused-residual mode fits the registers of the 16-warp kernel only
+    // (the 8-warp levels keep k_half_sweep_seg's, bit-identical to theirs)
+    if (res_uw && band_nw(L) != 16) return false;
     const int o = color ^ 1;
     CUtensorMap mF, mB, mE;
     if (!make_tmap(&mF, f + (long long)color * L.cstride, L, 32, BAND_NZ) ||
@@ -3217,30 +3283,41 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     const int grid = nunits < sm_count() ? nunits : sm_count();
     if (np) *np = grid;
     const bool lean = rho == 1.0 && !zero_start;
+#define PMG_BANDK(P, NW)                                                                    \
+    do {                                                                                    \
+        const int nt = 32 * (NW + 1);                                                       \
+        if (res_uw)                                                                         \
+            k_half_sweep_band<P, false, false, true, 16, true><<<grid, nt, band_smem(), st>>>( \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, partials, res_uw);                                                  \
+        else if (lean && !partials)                                                              \
+            k_half_sweep_band<P, false, false, true, NW><<<grid, nt, band_smem(), st>>>(    \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, nullptr, nullptr);                                                           \
+        else if (partials && fsq)                                                           \
+            k_half_sweep_band<P, false, true, false, NW><<<grid, nt, band_smem(), st>>>(    \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, partials, nullptr);                                                          \
+        else if (partials)                                                                  \
+            k_half_sweep_band<P, true, false, false, NW><<<grid, nt, band_smem(), st>>>(    \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, partials, nullptr);                                                          \
+        else                                                                                \
+            k_half_sweep_band<P, false, false, false, NW><<<grid, nt, band_smem(), st>>>(   \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
+                mE, nullptr, nullptr);                                                           \
+    } while (0)
 #define PMG_BANDL(P)                                                                        \
     do {                                                                                    \
-        if (lean && !partials)                                                              \
-            k_half_sweep_band<P, false, false, true><<<grid, 288, band_smem(), st>>>(       \
-                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
-                mE, nullptr);                                                               \
-        else if (partials && fsq)                                                           \
-            k_half_sweep_band<P, false, true><<<grid, 288, band_smem(), st>>>(              \
-                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
-                mE, partials);                                                              \
-        else if (partials)                                                                  \
-            k_half_sweep_band<P, true><<<grid, 288, band_smem(), st>>>(                     \
-                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
-                mE, partials);                                                              \
-        else                                                                                \
-            k_half_sweep_band<P><<<grid, 288, band_smem(), st>>>(                           \
-                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB, \
-                mE, nullptr);                                                               \
+        if (band_nw(L) == 16) PMG_BANDK(P, 16);                                             \
+        else PMG_BANDK(P, 8);                                                               \
     } while (0)
     if (L.plane == 520) PMG_BANDL(520);
     else if (L.plane == 264) PMG_BANDL(264);
     else if (L.plane == 1032) PMG_BANDL(1032);
     else PMG_BANDL(136);
 #undef PMG_BANDL
+#undef PMG_BANDK
     return true;
 }
 

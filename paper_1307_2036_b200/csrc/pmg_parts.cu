@@ -307,12 +307,16 @@ int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, 
         return exchange(h, c, u, s);
     }
     // frame: rows 0 and ny - 1 (all strips), the first and last strip of
-    // rows 1 .. ny - 2; then the interior strips 1 .. n - 2 of those rows
+    // rows 1 .. ny - 2; then the interior strips 1 .. n - 2 of those rows.
+    // Every region is a run of whole rows, so each runs on the kernel the
+    // whole-part sweep would use (the same column solves, bit for bit)
     for (int p = 0; p < h->np; ++p) {
         const PL &q = h->P[p][c];
         const int ns = ((q.nx + 1) / 2 + 31) / 32;
-        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns, 0,
-                                  q.ny - 1, 2, s));
+        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns, 0, 1,
+                                  1, s));
+        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns,
+                                  q.ny - 1, 1, 1, s));
         TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, ns - 1, 2,
                                   1, 1, q.ny - 2, s));
     }

@@ -24,11 +24,35 @@ def pmg():
 
 
 def frame_and_interior(nstrip, ny):
-    """(rx0, rxs, rxn, ry0, rys, ryn) regions: rows 0 and ny-1 (all strips),
-    the first and last strip of rows 1 .. ny-2, then the interior."""
-    return [(0, 1, nstrip, 0, max(ny - 1, 1), 2 if ny > 1 else 1),
+    """(rx0, rxs, rxn, ry0, rys, ryn) regions as the multi-part driver
+    issues them: row 0 and row ny-1 (all strips), the first and last strip
+    of rows 1 .. ny-2, then the interior."""
+    return [(0, 1, nstrip, 0, 1, 1), (0, 1, nstrip, ny - 1, 1, 1),
             (0, max(nstrip - 1, 1), 2 if nstrip > 1 else 1, 1, 1, ny - 2),
             (1, 1, nstrip - 2, 1, 1, ny - 2)]
+
+
+def test_strided_rows_match_whole(pmg):
+    """Row strides (a region of non-adjacent rows) run on the register
+    kernel: same values as that kernel's whole-part sweep (a level below
+    the TMA band kernel's sizes)."""
+    from paper_1307_2036_b200 import _lib
+    nx, nz = 128, 32
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    op = pmg.PanelOperator(grid, pmg.toy_parameters(nx, nz, 1e-3, 1.0),
+                           pmg.Decomposition(nx, 1).layout(nx))
+    (w, h), = op.handles.items()
+    rng = np.random.default_rng(8)
+    u0 = pmg.scatter_owned(rng.uniform(-1, 1, (nx, nx, nz)), op.layout)
+    pmg.halo_exchange(u0)
+    f = pmg.scatter_owned(rng.uniform(-1, 1, (nx, nx, nz)), op.layout)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    a, b = u0.copy(), u0.copy()
+    _lib.call("pmg_half_sweep", h.h, a.parts[w].ptr, f.parts[w].ptr, 0, 1.0, 0, 0, 1.0, st)
+    for reg in ((0, 1, 2, 0, 2, nx // 2), (0, 1, 2, 1, 2, nx // 2)):   # even rows, odd rows
+        _lib.call("pmg_half_sweep_region", h.h, b.parts[w].ptr, f.parts[w].ptr, 0, 1.0, 0, 0,
+                  1.0, *reg, st)
+    assert torch.equal(a.parts[w].data, b.parts[w].data)
 
 
 @pytest.mark.parametrize("nx,ny,nz", [(256, 64, 128), (512, 512, 128), (1024, 256, 128),
