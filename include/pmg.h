@@ -157,13 +157,6 @@ int pmg_red_residual_norm(const pmg_level *lvl, const double *f, const double *u
  * sequential Thomas recurrence, bit-identical to the reference.  Levels
  * with variable coefficients always use the exact solver. */
 int pmg_set_smoother_mode(int mode);
-/* half sweep of a part that is its own neighbour in both directions, with
- * the halo ring refresh fused into the kernel (halo_flags: bit0 = on,
- * bit1 = periodic x, bit2 = periodic y; mirror otherwise): equivalent to
- * pmg_half_sweep + pmg_halo_self without the extra launch and pass. */
-int pmg_half_sweep_halo(const pmg_level *lvl, double *u, const double *f, int color,
-                        double rho, int zero_start, int neighbors_zero, double post_scale,
-                        int halo_flags, void *stream);
 int pmg_get_smoother_mode(void);
 int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
                    double rho, int zero_start, int neighbors_zero, double post_scale,
@@ -218,23 +211,7 @@ int pmg_prolong_add(const pmg_level *fine, const pmg_level *coarse, const double
  * without reading it, so the V-cycle prolongs into black cells only. */
 int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *coarse_u,
                        double *fine_u, int add, int color_mask, void *stream);
-/* ... with the fused self-halo refresh of pmg_half_sweep_halo */
-int pmg_prolong_colors_halo(const pmg_level *fine, const pmg_level *coarse,
-                            const double *coarse_u, double *fine_u, int add, int color_mask,
-                            int halo_flags, void *stream);
 
-/* Coarse-grid correction fused into the first post-smoothing half-sweep
- * (multigrid.py:283-292 then smoother.py:184-191 with rho = 1): relaxes
- * colour `color` of fine_u as if fine_u had first received u += P coarse_u
- * and a halo exchange.  The other colour is NOT updated in memory -- valid
- * only because the next half-sweep overwrites it without reading it (the
- * V-cycle's post-smoothing with rho = 1).  coarse_u's halo must be current.
- * halo_flags as pmg_half_sweep_halo.  Fast smoother, uniform levels only:
- * pmg_half_sweep_prolong_ok tells (else PMG_ERR_VALUE). */
-int pmg_half_sweep_prolong_ok(const pmg_level *fine);
-int pmg_half_sweep_prolong(const pmg_level *fine, const pmg_level *coarse, double *fine_u,
-                           const double *fine_f, const double *coarse_u, int color,
-                           int halo_flags, void *stream);
 
 /* ---- halos (partition.py:158-191) ----------------------------------- */
 /* Fill the whole halo ring of a part that is its own neighbour (one worker

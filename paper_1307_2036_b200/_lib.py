@@ -100,10 +100,6 @@ SIGNATURES = {
     "pmg_field_alloc": (_I, [_P, _P]),
     "pmg_field_free": (_I, [_P]),
     "pmg_prolong_colors": (_I, [_P, _P, _P, _P, _I, _I, _P]),
-    "pmg_prolong_colors_halo": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
-    "pmg_half_sweep_halo": (_I, [_P, _P, _P, _I, _D, _I, _I, _D, _I, _P]),
-    "pmg_half_sweep_prolong_ok": (_I, [_P]),
-    "pmg_half_sweep_prolong": (_I, [_P, _P, _P, _P, _P, _I, _I, _P]),
     "pmg_halo_self": (_I, [_P, _P, _I, _I, _P]),
     "pmg_face_doubles": (_LL, [_P, _I]),
     "pmg_pack_face": (_I, [_P, _P, _I, _P, _P]),

@@ -28,7 +28,6 @@ cudaError_t launch_half_sweep(const Lvl &, double *, const double *, int, double
 cudaError_t launch_invd(const Lvl &, double *, cudaStream_t);
 cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, double,
                             cudaStream_t);
-bool half_sweep_pro_ok(const Lvl &F);
 bool half_sweep_dot_ok(const Lvl &L);
 bool half_sweep_res_ok(const Lvl &L);
 bool residual_restrict_red_ok(const Lvl &F);
@@ -43,8 +42,6 @@ cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int 
                                   int zero_start, int nbr_zero, double post_scale,
                                   double *partials, int *np, cudaStream_t st);
 void setup_kernel_attributes();
-cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const double *f,
-                                  const double *cu, int color, cudaStream_t st);
 cudaError_t launch_prolong(const Lvl &, const Lvl &, const double *, double *, int, int,
                            cudaStream_t);
 cudaError_t launch_halo_self(const Lvl &, double *, int, int, cudaStream_t);
@@ -256,10 +253,6 @@ int pmg_level_create(const pmg_level_desc *d, pmg_level **out) {
         // segment from its start / to its end (segments of L.seg levels)
         int seg = 4;
         while (seg < 32 && (nz + seg - 1) / seg > 8) seg <<= 1;
-        if (const char *es = getenv("PMG_SEG")) {   // tuning override
-            const int v = atoi(es);
-            if (v == 4 || v == 8 || v == 16 || v == 32) seg = v;
-        }
         L.seg = ((nz + seg - 1) / seg <= 16) ? seg : 0;
         lv->h_seg.assign(5 * (size_t)nz, 0.0);
         double *al = lv->h_seg.data(), *mu = al + nz, *pf = mu + nz, *qq = pf + nz;
@@ -466,11 +459,8 @@ int pmg_half_sweep_region_ok(const pmg_level *lv) {
     if (!lv) return 0;
     const Lvl &L = lv->L;
     // the fast uniform column solvers (k_half_sweep_band / k_half_sweep_seg)
-    // walk tile regions; the exact, variable and fused-halo kernels do not
-    return (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8 &&
-            !(L.hflags & 1))
-               ? 1
-               : 0;
+    // walk tile regions; the exact and variable kernels do not
+    return (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) ? 1 : 0;
 }
 
 int pmg_half_sweep_region(const pmg_level *lv, double *u, const double *f, int color, double rho,
@@ -517,42 +507,6 @@ int pmg_half_sweep_res(const pmg_level *lv, const double *u, double *u_new, cons
     return PMG_OK;
 }
 
-int pmg_half_sweep_halo(const pmg_level *lv, double *u, const double *f, int color, double rho,
-                        int zero_start, int neighbors_zero, double post_scale, int halo_flags,
-                        void *st) {
-    PMG_CHECK_LVL(lv);
-    if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
-    if (!lv->L.uniform && !lv->prepared) {
-        int rc = pmg_level_prepare(const_cast<pmg_level *>(lv), st);
-        if (rc) return rc;
-    }
-    Lvl L = lv->L;
-    L.hflags = halo_flags & 7;
-    PMG_CUDA(launch_half_sweep(L, u, f, color, rho, zero_start, neighbors_zero, post_scale,
-                               (cudaStream_t)st),
-             "half_sweep_halo");
-    return PMG_OK;
-}
-
-int pmg_half_sweep_prolong_ok(const pmg_level *fine) {
-    return (fine && half_sweep_pro_ok(fine->L)) ? 1 : 0;
-}
-
-int pmg_half_sweep_prolong(const pmg_level *fine, const pmg_level *coarse, double *u,
-                           const double *f, const double *cu, int color, int halo_flags,
-                           void *st) {
-    int rc = check_pair(fine, coarse);
-    if (rc) return rc;
-    if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
-    if (!half_sweep_pro_ok(fine->L))
-        return fail(PMG_ERR_VALUE, "fused prolongation needs the fast smoother on a uniform level");
-    Lvl F = fine->L;
-    F.hflags = halo_flags & 7;
-    PMG_CUDA(launch_half_sweep_pro(F, coarse->L, u, f, cu, color, (cudaStream_t)st),
-             "half_sweep_prolong");
-    return PMG_OK;
-}
-
 int pmg_restrict(const pmg_level *fine, const pmg_level *coarse, const double *ff, double *cf,
                  double weight, void *st) {
     int rc = check_pair(fine, coarse);
@@ -576,17 +530,10 @@ int pmg_prolong_add(const pmg_level *fine, const pmg_level *coarse, const double
 
 int pmg_prolong_colors(const pmg_level *fine, const pmg_level *coarse, const double *cu, double *fu,
                        int add, int color_mask, void *st) {
-    return pmg_prolong_colors_halo(fine, coarse, cu, fu, add, color_mask, 0, st);
-}
-
-int pmg_prolong_colors_halo(const pmg_level *fine, const pmg_level *coarse, const double *cu,
-                            double *fu, int add, int color_mask, int halo_flags, void *st) {
     int rc = check_pair(fine, coarse);
     if (rc) return rc;
     if (color_mask < 1 || color_mask > 3) return fail(PMG_ERR_VALUE, "color_mask must be 1, 2 or 3");
-    Lvl F = fine->L;
-    F.hflags = halo_flags & 7;
-    PMG_CUDA(launch_prolong(F, coarse->L, cu, fu, add, color_mask, (cudaStream_t)st),
+    PMG_CUDA(launch_prolong(fine->L, coarse->L, cu, fu, add, color_mask, (cudaStream_t)st),
              "prolong_colors");
     return PMG_OK;
 }

@@ -33,11 +33,10 @@ struct Lvl {
     // tables alpha[nz] mu[nz] pf[nz] q[nz] (see k_half_sweep_seg)
     int seg;
     const double *segtab;
-    // fused self-halo for a part that is its own neighbour (set per call):
-    // bit0 enabled, bit1 periodic x, bit2 periodic y; bit3 (HF_WRAP): the
-    // part is periodic in x and y and the neighbour reads of the half-sweep,
-    // residual-restriction and prolongation kernels wrap around instead of
-    // reading the halo ring (which is then not maintained: pmg_driver.cu)
+    // bit3 (HF_WRAP): the part is periodic in x and y and the neighbour
+    // reads of the half-sweep, residual-restriction and prolongation
+    // kernels wrap around instead of reading the halo ring (which is then
+    // not maintained: pmg_driver.cu's wrap views)
     int hflags;
     // tile region of the fast uniform half-sweeps (k_half_sweep_seg,
     // k_half_sweep_band): the 32-cell strips rx0 + s * rxs (s < rxn) of the
@@ -73,26 +72,5 @@ __host__ __device__ __forceinline__ long long cell(const Lvl &L, int i, int j, i
     return at(L, colour(L, i, j), k, j, i >> 1);
 }
 
-// A kernel that stores owned cell (i, j, k) of a self-neighbour part also
-// writes every halo cell whose source it is (partition.py:158-191 with one
-// worker: periodic wrap or mirror, corners included).  Only the thread
-// owning the source reads such a halo slot within the same kernel, and it
-// loads before it stores, so the fused copy is race-free.
-__device__ __forceinline__ void halo_copies(const Lvl &L, double *u, int i, int j, int k,
-                                            double v) {
-    if (!(L.hflags & 1)) return;
-    const bool px = L.hflags & 2, py = L.hflags & 4;
-    int xs[2], ys[2];
-    int nxs = 0, nys = 0;
-    if (i == 0) xs[nxs++] = px ? L.nx : -1;
-    if (i == L.nx - 1) xs[nxs++] = px ? -1 : L.nx;
-    if (j == 0) ys[nys++] = py ? L.ny : -1;
-    if (j == L.ny - 1) ys[nys++] = py ? -1 : L.ny;
-    for (int a = 0; a < nxs; ++a) u[cell(L, xs[a], j, k)] = v;
-    for (int b = 0; b < nys; ++b) {
-        u[cell(L, i, ys[b], k)] = v;
-        for (int a = 0; a < nxs; ++a) u[cell(L, xs[a], ys[b], k)] = v;
-    }
-}
 
 }  // namespace pmg

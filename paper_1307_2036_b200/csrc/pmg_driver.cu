@@ -140,28 +140,8 @@ int halo(const pmg_hier *h, const pmg_level *l, double *x, cudaStream_t st) {
     return pmg_halo_self(l, x, h->d.periodic_x, h->d.periodic_y, st);
 }
 
-// levels of at most this many columns per row refresh their halo inside the
-// half-sweep / prolongation kernels (launch-bound small levels)
-int fused_halo_nx() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PMG_FH_NX");
-        v = e ? atoi(e) : 0;
-    }
-    return v;
-}
-
-int halo_flags(const pmg_hier *h, const pmg_level *l) {
-    int nx, ny, nz;
-    if (pmg::level_hflags(l) & pmg::HF_WRAP) return 0;
-    if (pmg_level_dims(l, &nx, &ny, &nz) || nx > fused_halo_nx()) return 0;
-    return 1 | (h->d.periodic_x ? 2 : 0) | (h->d.periodic_y ? 4 : 0);
-}
-
 int half_sweep(const pmg_hier *h, const pmg_level *l, double *u, const double *f, int color,
                int nbr_zero, cudaStream_t st) {
-    const int hf = halo_flags(h, l);
-    if (hf) return pmg_half_sweep_halo(l, u, f, color, h->d.rho, 0, nbr_zero, 1.0, hf, st);
     TRY(pmg_half_sweep(l, u, f, color, h->d.rho, 0, nbr_zero, 1.0, st));
     return halo(h, l, u, st);
 }
@@ -173,7 +153,7 @@ int half_sweep(const pmg_hier *h, const pmg_level *l, double *u, const double *f
 int sweeps(const pmg_hier *h, const pmg_level *l, double *u, const double *f, int n,
            bool from_zero, bool red_done, cudaStream_t st, const Fine *fsq = nullptr) {
     if (fsq && fsq->fsq_part && n >= 1 && !red_done) {
-        // first sweep with ||f||^2 folded in (no fused halo on such levels)
+        // first sweep with ||f||^2 folded in
         int n1 = 0, n2 = 0;
         TRY(pmg::half_sweep_fsq(l, u, f, 0, from_zero ? 1 : 0, fsq->fsq_part, &n1, st));
         TRY(halo(h, l, u, st));
@@ -218,13 +198,8 @@ int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStr
         TRY(vcycle(h, c + 1, u0, f0, false, st, fv));
         // u += P e (black cells only when the red half-sweep overwrites red)
         const int pmask = (lean && h->d.nu_post >= 1) ? 2 : 3;
-        const int hf = halo_flags(h, lc);
-        if (hf) {
-            TRY(pmg_prolong_colors_halo(lc, lcc, h->u[c + 1], u, 1, pmask, hf, st));
-        } else {
-            TRY(pmg_prolong_colors(lc, lcc, h->u[c + 1], u, 1, pmask, st));
-            TRY(halo(h, lc, u, st));
-        }
+        TRY(pmg_prolong_colors(lc, lcc, h->u[c + 1], u, 1, pmask, st));
+        TRY(halo(h, lc, u, st));
         TRY(sweeps(h, lc, u, f, h->d.nu_post, false, false, st));
     } else {
         TRY(sweeps(h, lc, u, f, h->d.coarse_sweeps, lean && c > 0, false, st));
@@ -270,11 +245,9 @@ int lagged_body(pmg_hier *h, const double *f, int kind, const Lag &g, cudaStream
 }
 
 // the next cycle ends with the check-only norm when the last contraction
-// predicts convergence with a factor-2 margin (PMG_NO_PREDICT: never)
+// predicts convergence with a factor-2 margin
 bool predict_last(double rn, double prev, double r0, double eps) {
-    static int off = -1;
-    if (off < 0) off = getenv("PMG_NO_PREDICT") ? 1 : 0;
-    if (off || !(prev > 0.0)) return false;
+    if (!(prev > 0.0)) return false;
     return rn * (rn / prev) < 0.5 * eps * r0;
 }
 
@@ -320,9 +293,7 @@ int replay(pmg_hier *h, double *u, const double *f, bool first, cudaStream_t st)
 // mode (k_half_sweep_seg / k_half_sweep_segv), nx % 4 == 0 with a coarse
 // level of >= 2 columns (column-quad restriction / prolongation)
 bool wrap_ok(const pmg_hier *h) {
-    if (!h->d.periodic_x || !h->d.periodic_y || getenv("PMG_NO_WRAP") ||
-        getenv("PMG_RR_NOQ") || getenv("PMG_PROLONG_NOQ") || pmg_get_smoother_mode() != 0)
-        return false;
+    if (!h->d.periodic_x || !h->d.periodic_y || pmg_get_smoother_mode() != 0) return false;
     for (size_t c = 0; c < h->lv.size(); ++c) {
         int nx, ny, nz, pitch, par, uni;
         long long plane, cs;
@@ -335,8 +306,7 @@ bool wrap_ok(const pmg_hier *h) {
             // variable levels: k_half_sweep_segv (16 warps) and, below the
             // coarsest, the red-only restriction (the full one reads halos)
             const int seg = nz / 16;
-            if (nz % 16 || !(seg == 1 || seg == 2 || seg == 4 || seg == 8 || seg == 16) ||
-                getenv("PMG_VAR_EXACT"))
+            if (nz % 16 || !(seg == 1 || seg == 2 || seg == 4 || seg == 8 || seg == 16))
                 return false;
             if (c + 1 < h->lv.size() && !h->d.red_restrict) return false;
         }
@@ -356,7 +326,7 @@ bool lagged_ok(const pmg_hier *h) {
     if (pmg_level_layout(h->lv[0], &pitch, &plane, &cs, &par, &uni)) return false;
     if (!uni && !(h->d.red_restrict && pmg_residual_restrict_red_ok(h->lv[0]))) return false;
     return h->d.lagged_norm && h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->d.nu_post >= 1 &&
-           h->lv.size() > 1 && nx % 4 == 0 && !getenv("PMG_RR_NOQ") &&
+           h->lv.size() > 1 && nx % 4 == 0 &&
            pmg_half_sweep_res_ok(h->lv[0]);
 }
 
@@ -479,31 +449,9 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     *converged = 0;
     double r0 = 0.0, prev = 0.0;
     bool predict = pmg_residual_restrict_red_ok(l0) != 0;
-    // PMG_GRAPH_TIMING=1: device time of each cycle graph vs the solve's wall
-    // time (the difference is the host round trip per cycle), on stderr
-    static int timing = getenv("PMG_GRAPH_TIMING") ? 1 : 0;
-    cudaEvent_t tev[2] = {nullptr, nullptr};
-    double gsum = 0.0;
-    if (timing) {
-        cudaEventCreate(&tev[0]);
-        cudaEventCreate(&tev[1]);
-    }
-    cudaEvent_t t_all0 = nullptr, t_all1 = nullptr;
-    if (timing) {
-        cudaEventCreate(&t_all0);
-        cudaEventCreate(&t_all1);
-        cudaEventRecord(t_all0, st);
-    }
     for (int it = 0; it < maxiter; ++it) {
-        if (timing) cudaEventRecord(tev[0], st);
         TRY(replay_kind(h, u, f, kind, st, [&] { return lagged_body(h, f, kind, g, st); }));
-        if (timing) cudaEventRecord(tev[1], st);
         TRYC(cudaStreamSynchronize(st), "sync");
-        if (timing) {
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, tev[0], tev[1]);
-            gsum += ms;
-        }
         if (it == 0) {
             // r0 = ||f|| (multigrid.py:307-309), summed by the first cycle
             r0 = std::sqrt(h->res_h[1]);
@@ -532,18 +480,6 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
             kind = (predict && predict_last(rn, prev, r0, eps)) ? 6 + x : 4 + x;
         }
         prev = rn;
-    }
-    if (timing) {
-        cudaEventRecord(t_all1, st);
-        cudaEventSynchronize(t_all1);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, t_all0, t_all1);
-        fprintf(stderr, "pmg graph timing: %d cycles, graphs %.3f ms, solve %.3f ms\n", *iters,
-                gsum, ms);
-        cudaEventDestroy(tev[0]);
-        cudaEventDestroy(tev[1]);
-        cudaEventDestroy(t_all0);
-        cudaEventDestroy(t_all1);
     }
     h->last_iters = *iters;
     if (x == 1)   // the result's red array is red1: copy it into u

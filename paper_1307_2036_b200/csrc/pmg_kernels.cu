@@ -964,7 +964,6 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
             y = y + omr * so[k * 32 + lane];
         }
         u[pc + (long long)k * pl] = y;
-        halo_copies(L, u, i, j, k, y);
     }
 }
 
@@ -1020,155 +1019,6 @@ __device__ __forceinline__ void tma_box3(void *dst, const CUtensorMap *map, int 
         : "memory");
 }
 
-template <int KC>
-struct TxSlot {                  // doubles per ring slot: W [KC][36] S [KC][32] N [KC][32] F [KC][32]
-    static constexpr int W = 0, S = KC * 36, N = S + KC * 32, F = N + KC * 32, SIZE = F + KC * 32;
-};
-
-template <int KC, int R>
-__global__ void __launch_bounds__(128, 1)
-k_half_sweep_tx(Lvl L, double *__restrict__ u, int c, double rho, int zero_start, int nbr_zero,
-                double post_scale, int ntiles, int htiles,
-                const __grid_constant__ CUtensorMap mF, const __grid_constant__ CUtensorMap mW,
-                const __grid_constant__ CUtensorMap mSN) {
-    extern __shared__ __align__(128) double xsm_raw[];
-    // TMA destinations must be 128-byte aligned
-    double *xsm = xsm_raw + (((128u - (smem_u32(xsm_raw) & 127u)) & 127u) >> 3);
-    using SL = TxSlot<KC>;
-    const int nz = L.nz;
-    const int nw = blockDim.x >> 5;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nch = nz / KC;                          // chunks per tile (KC divides nz)
-    // shared layout: per warp { ring [R][SL::SIZE] | gbuf [nz][32] } | tables | bars
-    const int per_warp = R * SL::SIZE + nz * 32;
-    double *ring = xsm + (size_t)warp * per_warp;
-    double *gbuf = ring + R * SL::SIZE;
-    double *tvp = xsm + (size_t)nw * per_warp;
-    double *tinv = tvp + nz + 1;
-    double *tdrw = tinv + nz;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(tdrw + nz + ((3 * nz + 1) & 1)) + warp * R;
-    for (int t = threadIdx.x; t <= nz; t += blockDim.x) {
-        tvp[t] = L.vprof[t];
-        if (t < nz) {
-            tinv[t] = L.invd1[t];
-            tdrw[t] = L.drw[t];
-        }
-    }
-    if (lane == 0)
-        for (int r = 0; r < R; ++r) mbar_init(&bars[r], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-
-    const long long pl = L.plane;
-    const double cv = L.csub0, wx0 = L.wx0, wy0 = L.wy0;
-    const double scale = rho * post_scale;
-    const double omr = 1.0 - rho;
-    const uint32_t txb = (uint32_t)(nbr_zero ? KC * 32 * 8 : SL::SIZE * 8);
-    // issue stream over (tile of this warp, chunk)
-    int iq = warp, ic = 0;
-    uint32_t iseq = 0, cseq = 0;
-    auto issue_next = [&]() {
-        const int t = blockIdx.x + iq * gridDim.x;
-        if (t >= ntiles) return;
-        if (lane == 0) {
-            const int j = t / htiles, h0 = (t - j * htiles) * 32;
-            double *sl = ring + (iseq % R) * SL::SIZE;
-            uint64_t *bar = &bars[iseq % R];
-            fence_proxy_async();
-            mbar_expect_tx(bar, txb);
-            const int k0 = ic * KC;
-            tma_box3(sl + SL::F, &mF, OFF + h0, k0, j + 1, bar);
-            if (!nbr_zero) {
-                tma_box3(sl + SL::W, &mW, OFF + h0 - 2, k0, j + 1, bar);
-                tma_box3(sl + SL::S, &mSN, OFF + h0, k0, j, bar);
-                tma_box3(sl + SL::N, &mSN, OFF + h0, k0, j + 2, bar);
-            }
-        }
-        ++iseq;
-        if (++ic == nch) {
-            ic = 0;
-            iq += nw;
-        }
-    };
-    for (int r = 0; r < R; ++r) issue_next();
-
-    for (int q = warp;; q += nw) {
-        const int t = blockIdx.x + q * gridDim.x;
-        if (t >= ntiles) break;
-        const int j = t / htiles, h0 = (t - j * htiles) * 32;
-        const int s0 = (j + L.par + c) & 1;
-        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
-        const bool act = lane < nact;
-        // ---- forward: RHS assembly + elimination, chunk by chunk ----
-        double g = 0.0;
-        for (int ch = 0; ch < nch; ++ch) {
-            const int slot = cseq % R;
-            mbar_wait(&bars[slot], (cseq / R) & 1);
-            const double *sl = ring + slot * SL::SIZE;
-#pragma unroll 4
-            for (int e = 0; e < KC; ++e) {
-                const int k = ch * KC + e;
-                double rhs;
-                if (nbr_zero) {
-                    rhs = sl[SL::F + e * 32 + lane];
-                } else {
-                    const double *wrow = sl + SL::W + e * 36;
-                    rhs = wx0 * wrow[lane + 1 + s0];
-                    rhs = rhs + wx0 * wrow[lane + 2 + s0];
-                    rhs = rhs + wy0 * sl[SL::S + e * 32 + lane];
-                    rhs = rhs + wy0 * sl[SL::N + e * 32 + lane];
-                    rhs = rhs * tdrw[k];
-                    rhs = rhs + sl[SL::F + e * 32 + lane];
-                }
-                if (k == 0) {
-                    g = rhs * tinv[0];
-                } else {
-                    double tt = g * cv;
-                    tt = tt * tvp[k];
-                    g = rhs + tt;
-                    g = g * tinv[k];
-                }
-                gbuf[k * 32 + lane] = g;
-            }
-            ++cseq;
-            __syncwarp();
-            issue_next();
-        }
-        // ---- backward + relaxation + store ----
-        if (act) {
-            const long long pc = at(L, c, 0, j, h0 + lane);
-            double x = g;
-            const int top = ((nz - 1) / 8) * 8;
-            for (int kb = top; kb >= 0; kb -= 8) {
-                double r[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (kb + e < nz - 1) r[e] = gbuf[(kb + e) * 32 + lane];
-#pragma unroll
-                for (int e = 7; e >= 0; --e) {
-                    const int k = kb + e;
-                    if (k < nz - 1) {
-                        double tt = x * cv;
-                        tt = tt * tvp[k + 1];
-                        tt = tt * tinv[k];
-                        x = r[e] + tt;
-                    }
-                    if (k < nz) {
-                        double y = x;
-                        if (zero_start) {
-                            if (scale != 1.0) y = y * scale;
-                        } else if (rho != 1.0) {
-                            y = y * rho;
-                            y = y + omr * u[pc + (long long)k * pl];
-                        }
-                        u[pc + (long long)k * pl] = y;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Line smoother half-sweep, FAST mode (default, uniform coefficients):
@@ -1186,13 +1036,13 @@ k_half_sweep_tx(Lvl L, double *__restrict__ u, int c, double rho, int zero_start
 // full L1 available -- no serial chain, no large shared buffers.  Same
 // operator and RHS as smoother.py:137-170; reassociated elimination
 // (agrees with the sequential solve to ~1e-15 relative; the exact mode is
-// k_half_sweep / k_half_sweep_tx).
+// k_half_sweep).
 // ---------------------------------------------------------------------------
 // Column solve of one tile of the k-segmented smoother, given r[e] =
 // iota_k * rhs_k for this warp's levels: local forward, segment scan,
 // local backward, segment scan, fix-up, relaxation and store (+ halo
-// copies).  Shared by k_half_sweep_seg and k_half_sweep_pro.
-template <int SEG, bool HALO, bool DOT = false, bool LEAN = false>
+// copies) of k_half_sweep_seg.
+template <int SEG, bool DOT = false, bool LEAN = false>
 __device__ __forceinline__ void seg_solve_store(
     const Lvl &L, double *__restrict__ u, double (&r)[SEG], const double2 *ti,
     const double2 *tb, const double *tq, double *hend, double *ybeg, int c, int j, int h0,
@@ -1250,23 +1100,14 @@ __device__ __forceinline__ void seg_solve_store(
                     y = y + omr * u[q];
                 }
                 u[q] = y;
-                if (HALO) r[e] = y;
                 if (DOT) *dacc += f[q] * y;       // <rhs, new value> (CG's <r, z>)
             }
         }
     }
-    // fused self-halo: only tiles touching the part boundary (warp-uniform)
-    if (HALO && (j == 0 || j == L.ny - 1 || h0 == 0 || h0 + 32 >= ((L.nx - s0) + 1) / 2)) {
-        if (lane < nact) {
-#pragma unroll
-            for (int e = 0; e < SEG; ++e)
-                if (e < kn) halo_copies(L, u, i, j, k0 + e, r[e]);
-        }
-    }
 }
 
-template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, bool HALO = false,
-          int PLC = 0, bool DOT = false, int RES = 0, bool LEAN = false>
+template <int SEG, int PMG_SEG_B, int MINB, int NBZ = -1, bool FULL = false, int PLC = 0,
+          bool DOT = false, int RES = 0, bool LEAN = false>
 __global__ void __launch_bounds__(256, MINB)
 k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
                  int zero_start, int nbr_zero_rt, double post_scale, int ntiles, int htiles,
@@ -1409,7 +1250,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
             const double q = __fma_rn(bpend, un, rpend);
             if (lane < nact) dacc = __fma_rn(q, q, dacc);
         }
-        seg_solve_store<SEG, HALO, DOT, RES == 1 || LEAN>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
+        seg_solve_store<SEG, DOT, RES == 1 || LEAN>(L, (RES == 1) ? uw : u, r, ti, tb, tq, hend, ybeg, c, j,
                                         h0, s0, i, nact, kn, pc, pl, zero_start, rho, scale, omr,
                                         f, &dacc);
     }
@@ -1734,138 +1575,6 @@ k_half_sweep_band(Lvl L, double *__restrict__ u, int c, double rho, int zero_sta
     }
 }
 
-// Post-smoothing first half-sweep with the coarse-grid correction fused in
-// (fast mode, uniform, rho = 1).  The reference adds P e to the whole fine
-// iterate, exchanges halos and then relaxes colour c (multigrid.py:283-292,
-// smoother.py:184-191).  With rho = 1 the colour-c values are overwritten
-// unread and the other colour is read only here (before the next
-// half-sweep overwrites it), so the correction is applied on the fly to
-// the four neighbours the line RHS reads: v + (P e)(x, y), with P the 9-3-3-1
-// bilinear interpolation written as two 3-1 passes,
-//   P e = (3 g(Y) + g(Y + dY)) / 16,  g(Y) = 3 e(X, Y) + e(X + dX, Y)
-// (X = x >> 1, dX = x odd ? +1 : -1, likewise Y).  Neighbours in the fine
-// halo ring take the interpolation at their virtual position, which reads
-// coarse cells -1 .. nxc only and equals the correction of the cell the
-// halo copies (periodic wrap, mirror, or the neighbour part's own cell),
-// so no exchange is needed between prolongation and relaxation.  Each lane
-// loads e(h-1 .. h+1, J-1 .. J+1) per level (L1/L2-resident rows).
-template <int SEG, int PLC, int CPLC, bool HALO, int PB = 2>
-__global__ void __launch_bounds__(256, 2)
-k_half_sweep_pro(Lvl L, Lvl C, double *__restrict__ u, const double *__restrict__ f,
-                 const double *__restrict__ cu, int c, int ntiles, int htiles) {
-    extern __shared__ double ssm[];
-    const int nz = L.nz;
-    double2 *tw = reinterpret_cast<double2 *>(ssm);
-    double2 *ti = tw + nz;
-    double2 *tb = ti + nz;
-    double *tq = reinterpret_cast<double *>(tb + nz);
-    double *hend0 = tq + nz;
-    double *ybeg0 = hend0 + 2 * 16 * 32;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int t = threadIdx.x; t < nz; t += blockDim.x) {
-        const double io = L.invd1[t], dd = io * L.drw[t];
-        tw[t] = make_double2(dd * L.wx0, dd * L.wy0);
-        ti[t] = make_double2(io, L.segtab[t]);
-        tb[t] = make_double2(L.segtab[2 * nz + t], L.segtab[nz + t]);
-        tq[t] = L.segtab[3 * nz + t];
-    }
-    __syncthreads();
-    const int o = c ^ 1;
-    const long long pl = PLC ? (long long)PLC : L.plane;
-    const long long cpl = CPLC ? (long long)CPLC : C.plane;
-    const int k0 = w * SEG;
-    int par = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
-        double *hend = hend0 + par * 16 * 32;
-        double *ybeg = ybeg0 + par * 16 * 32;
-        const int j = t / htiles;
-        const int h0 = (t - j * htiles) * 32;
-        const int s0 = (j + L.par + c) & 1;
-        const int nact = min(32, ((L.nx - s0) + 1) / 2 - h0);
-        const int ln = min(lane, nact - 1);
-        const bool lastlane = (ln == nact - 1);
-        const int h = h0 + ln;
-        const int i = 2 * h + s0;
-        const long long pc = at(L, c, k0, j, h);
-        const long long pW = at(L, o, k0, j, (i - 1) >> 1);
-        const long long pE = at(L, o, k0, j, (i + 1) >> 1);
-        const long long pS = at(L, o, k0, j - 1, h);
-        const long long pN = at(L, o, k0, j + 1, h);
-        // coarse e(h-1 .. h+1, J-1 .. J+1): per row, e(h-1) and e(h+1) are
-        // adjacent elements of one colour array, e(h) is in the other
-        const int J = j >> 1;
-        const long long qa0 = cell(C, h - 1, J - 1, k0), qb0 = cell(C, h, J - 1, k0);
-        const long long qa1 = cell(C, h - 1, J, k0), qb1 = cell(C, h, J, k0);
-        const long long qa2 = cell(C, h - 1, J + 1, k0), qb2 = cell(C, h, J + 1, k0);
-        const bool jo = j & 1;
-        double r[SEG];
-        // ---- pass 1 (coarse rows, L1/L2-resident): the correction's share
-        // of the line RHS, wy (PeS + PeN) + wx (PeW + PeE), times iota ----
-#pragma unroll
-        for (int b = 0; b < SEG; b += PB) {
-            double em[PB][3], e0[PB][3], ep[PB][3];
-#pragma unroll
-            for (int e = 0; e < PB; ++e) {
-                const long long co = (long long)(b + e) * cpl;
-                em[e][0] = cu[qa0 + co]; ep[e][0] = cu[qa0 + co + 1]; e0[e][0] = cu[qb0 + co];
-                em[e][1] = cu[qa1 + co]; ep[e][1] = cu[qa1 + co + 1]; e0[e][1] = cu[qb1 + co];
-                em[e][2] = cu[qa2 + co]; ep[e][2] = cu[qa2 + co + 1]; e0[e][2] = cu[qb2 + co];
-            }
-#pragma unroll
-            for (int e = 0; e < PB; ++e) {
-                // x passes: g at x = i (S/N columns), i-1 (W), i+1 (E)
-                double gi[3], gw[3], ge[3];
-#pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double c3 = 3.0 * e0[e][d];
-                    gi[d] = s0 ? c3 + ep[e][d] : c3 + em[e][d];
-                    gw[d] = s0 ? c3 + em[e][d] : __fma_rn(3.0, em[e][d], e0[e][d]);
-                    ge[d] = s0 ? __fma_rn(3.0, ep[e][d], e0[e][d]) : c3 + ep[e][d];
-                }
-                // y passes (rows J-1, J, J+1 = d 0, 1, 2)
-                const double gw2 = jo ? gw[2] : gw[0];       // W/E partner row
-                const double ge2 = jo ? ge[2] : ge[0];
-                const double pw = __fma_rn(3.0, gw[1], gw2) * 0.0625;
-                const double pe = __fma_rn(3.0, ge[1], ge2) * 0.0625;
-                const double ps = (jo ? __fma_rn(3.0, gi[1], gi[0])
-                                      : __fma_rn(3.0, gi[0], gi[1])) * 0.0625;
-                const double pn = (jo ? __fma_rn(3.0, gi[2], gi[1])
-                                      : __fma_rn(3.0, gi[1], gi[2])) * 0.0625;
-                double pev = __shfl_down_sync(0xffffffffu, pw, 1);
-                if (lastlane) pev = pe;
-                const double2 cw = tw[k0 + b + e];
-                r[b + e] = __fma_rn(cw.y, ps + pn, cw.x * (pw + pev));
-            }
-        }
-        // ---- pass 2: the line RHS from the fine fields, as k_half_sweep_seg ----
-#pragma unroll
-        for (int b = 0; b < SEG; b += 4) {
-            double vf[4], vw[4], vs[4], vn[4], vx[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const long long ko = (long long)(b + e) * pl;
-                vf[e] = f[pc + ko];
-                vw[e] = u[pW + ko];
-                vs[e] = u[pS + ko];
-                vn[e] = u[pN + ko];
-                vx[e] = lastlane ? u[pE + ko] : 0.0;
-            }
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                double ve = __shfl_down_sync(0xffffffffu, vw[e], 1);
-                if (lastlane) ve = vx[e];
-                const double2 ia = ti[k0 + b + e];
-                const double2 cw = tw[k0 + b + e];
-                double g = __fma_rn(ia.x, vf[e], r[b + e]);
-                g = __fma_rn(cw.y, vs[e] + vn[e], g);
-                g = __fma_rn(cw.x, vw[e] + ve, g);
-                r[b + e] = g;
-            }
-        }
-        seg_solve_store<SEG, HALO>(L, u, r, ti, tb, tq, hend, ybeg, c, j, h0, s0, i, nact, SEG,
-                                   pc, pl, 0, 1.0, 1.0, 0.0);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // FAST half-sweep for VARIABLE coefficients (configs[4]): the k-segmented
@@ -2101,10 +1810,10 @@ __global__ void k_restrict(Lvl F, Lvl C, const double *__restrict__ fu, double *
     cu[cell(C, I, J, k)] = a;
 }
 
-// k_prolong_q with JB coarse rows per thread: the coarse rows J0-1 ..
+// The column-pair prolongation with JB coarse rows per thread: the coarse rows J0-1 ..
 // J0+JB form a sliding window (JB + 2 row loads instead of 3 JB), and all
 // loads of the thread's rows are issued before any arithmetic.  Same
-// arithmetic and order: bit-identical to k_prolong_q.
+// arithmetic and order: bit-identical to k_prolong.
 template <int JB, int CM = 0>
 __global__ void __launch_bounds__(128)
 k_prolong_w(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
@@ -2190,74 +1899,7 @@ k_prolong_w(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu
     }
 }
 
-// Prolongation + add, one thread per coarse column pair (fine nx a
-// multiple of 4): the fine 4 x 2 window of coarse cells (2m, J), (2m+1, J).
-// Per level and coarse row J-1 .. J+1 each lane loads e(2m) and e(2m+1)
-// (one element of each colour array, coalesced across lanes) and takes
-// e(2m-1), e(2m+2) from its neighbour lanes; the fine cells of the colours
-// in cmask are read and written as double2.  Same 9-3-3-1 arithmetic and
-// order as k_prolong (multigrid.py:233-245): bit-identical.
-__global__ void __launch_bounds__(128)
-k_prolong_q(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu, int add,
-            int cmask) {
-    const int lane = threadIdx.x & 31;
-    const int npair = C.nx >> 1;
-    const int m0 = blockIdx.x * 128 + (threadIdx.x & ~31);   // first pair of this warp
-    if (m0 >= npair) return;
-    const int k = blockIdx.y, J = blockIdx.z;
-    const int nact = min(32, npair - m0);
-    const bool act = lane < nact;
-    const int m = m0 + (act ? lane : nact - 1);
-    const bool first = lane == 0, last = lane == nact - 1;
-    // coarse rows J-1, J, J+1: e(2m), e(2m+1) and the window edges e(2m-1), e(2m+2)
-    double e0[3], e1[3], el[3], er[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const int Y = wrapy(C, J - 1 + d);
-        e0[d] = cu[cell(C, 2 * m, Y, k)];
-        e1[d] = cu[cell(C, 2 * m + 1, Y, k)];
-        const double xl = first ? cu[cell(C, wrapx(C, 2 * m - 1), Y, k)] : 0.0;
-        const double xr = last ? cu[cell(C, wrapx(C, 2 * m + 2), Y, k)] : 0.0;
-        el[d] = __shfl_up_sync(0xffffffffu, e1[d], 1);
-        er[d] = __shfl_down_sync(0xffffffffu, e0[d], 1);
-        if (first) el[d] = xl;
-        if (last) er[d] = xr;
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {           // fine rows 2J (dJ = -1), 2J+1 (dJ = +1)
-        const int j = 2 * J + r;
-        const int yn = r ? 2 : 0;           // coarse row J + dJ (J itself is index 1)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            if (!(cmask >> c & 1)) continue;
-            const int sc = (j + F.par + c) & 1;   // colour c at i = 4m + sc, 4m + 2 + sc
-            double v[2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                // fine i - 4m = 2q + sc: I = 2m + q, I + dI by the parity sc
-                const double cc1 = q ? e1[1] : e0[1], ccn = q ? e1[yn] : e0[yn];
-                const double xc1 = sc ? (q ? er[1] : e1[1]) : (q ? e0[1] : el[1]);
-                const double xcn = sc ? (q ? er[yn] : e1[yn]) : (q ? e0[yn] : el[yn]);
-                double e = 9.0 * cc1;
-                e = e + 3.0 * xc1;
-                e = e + 3.0 * ccn;
-                e = e + xcn;
-                v[q] = e * 0.0625;
-            }
-            if (act) {
-                const long long qf = at(F, c, k, j, 2 * m);
-                if (add) {
-                    const D2 old = ld2(fu + qf);
-                    v[0] = old.x + v[0];
-                    v[1] = old.y + v[1];
-                }
-                *reinterpret_cast<double2 *>(fu + qf) = make_double2(v[0], v[1]);
-            }
-        }
-    }
-}
 
-template <bool HALO>
 __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *__restrict__ fu,
                           int add, int cmask) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2282,7 +1924,6 @@ __global__ void k_prolong(Lvl F, Lvl C, const double *__restrict__ cu, double *_
     const long long q = at(F, c, k, j, h);
     const double v = add ? fu[q] + e : e;
     fu[q] = v;
-    if (HALO) halo_copies(F, fu, i, j, k, v);
 }
 
 
@@ -2645,47 +2286,13 @@ static inline int k_chunk(const Lvl &L, long long columns, int want_blocks_per_s
 }
 
 
-static int apply_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PMG_APPLY_VARIANT");
-        v = (e && e[0] == 'l') ? 1 : 0;   // 0: batched (default), 1: k-loop
-    }
-    return v;
-}
-
 cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double *out, int mode,
                          double *partials, int *nparts, cudaStream_t st) {
-    if (mode == 1 && partials && !out && L.uniform && L.nz <= 256 && L.nx % 4 == 0 &&
-        L.ny % 2 == 0 && L.nx >= 4 && getenv("PMG_NORM_Q")) {
-        // norm-only residual with the column-quad kernel (k_residual_restrict_q):
-        // opt-in, measured 444 vs 428 us (k_apply_v) at configs[1]'s fine level
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        Lvl Cq = L;                         // the row-pair / quad grid: nx/2 x ny/2
-        Cq.nx = L.nx / 2;
-        Cq.ny = L.ny / 2;
-        Cq.par = 0;
-        const int mb32 = ((Cq.nx >> 1) + 31) / 32;
-        auto kern = k_residual_restrict_q<2, true>;
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 128, 0);
-        const int capw = sm_count() * (occ > 0 ? occ : 1) * 4;
-        int kcs = L.nz;
-        while (kcs > 8 && (long long)mb32 * Cq.ny * ((L.nz + kcs - 1) / kcs) < 2LL * capw) kcs >>= 1;
-        const int ntiles = mb32 * Cq.ny * ((L.nz + kcs - 1) / kcs);
-        int grid = (ntiles + 3) / 4;
-        if (grid > capw / 4) grid = capw / 4;
-        *nparts = grid;
-        kern<<<grid, 128, 0, st>>>(L, Cq, u, f, nullptr, mb32, ntiles, kcs, partials);
-        return cudaGetLastError();
-    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (((mode == 1 && !out) || mode == 2) && partials && L.uniform && L.nz % 4 == 0 &&
-        L.nz <= 256 && !getenv("PMG_NORM_NOV")) {
+        L.nz <= 256) {
         constexpr int KB = 4;
         const int hx = ((L.nx + 1) / 2 + 63) / 64, jy = (L.ny + AP_TY - 1) / AP_TY;
-        static int mb = -1;
-        if (mb < 0) { const char *e = getenv("PMG_NORM_MB"); mb = e ? atoi(e) : 2; }
         auto go = [&](auto kern) {
             int occ = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * 2 * AP_TY, 0);
@@ -2704,15 +2311,15 @@ cudaError_t launch_apply(const Lvl &L, const double *u, const double *f, double 
             if (L.plane == 520) go(k_norm_v<KB, 520, 2, 2>);
             else go(k_norm_v<KB, 0, 2, 2>);
         } else if (L.plane == 520) {
-            if (mb == 3) go(k_norm_v<KB, 520, 3>); else go(k_norm_v<KB, 520, 2>);
+            go(k_norm_v<KB, 520, 2>);
         } else {
-            if (mb == 3) go(k_norm_v<KB, 0, 3>); else go(k_norm_v<KB, 0, 2>);
+            go(k_norm_v<KB, 0, 2>);
         }
         return cudaGetLastError();
     }
     const dim3 g0 = apply_grid(L), b(32, 2 * AP_TY);
     const bool norm = partials != nullptr;
-    if (apply_variant() == 0 && L.nz <= 256 && getenv("PMG_APPLY_V0") == nullptr) {
+    if (L.nz <= 256) {
         // vectorised column pairs
         constexpr int KB = 4;
         const int hx = ((L.nx + 1) / 2 + 63) / 64, jy = (L.ny + AP_TY - 1) / AP_TY;
@@ -2767,7 +2374,7 @@ cudaError_t launch_finalize(const double *partials, int n, double *out, cudaStre
 cudaError_t launch_residual_restrict(const Lvl &F, const Lvl &C, const double *u, const double *f,
                                      double *cf, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (F.uniform && F.nz <= 256 && F.nx % 4 == 0 && C.nx >= 2 && !getenv("PMG_RR_NOQ")) {
+    if (F.uniform && F.nz <= 256 && F.nx % 4 == 0 && C.nx >= 2) {
         const int mb32 = ((C.nx >> 1) + 31) / 32;
         auto runq = [&](auto kern) {
             int occ = 1;
@@ -2866,20 +2473,10 @@ size_t half_sweep_smem(const Lvl &L, bool need_old) {
 }
 
 
-static int hs_variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PMG_HS_VARIANT");
-        // exact mode: 1 shared-memory RHS + lane-sequential Thomas (default),
-        // 4: tensor-map TMA solver warps (opt-in: measured slower)
-        v = (e && e[0] == 'x') ? 4 : 1;
-    }
-    return v;
-}
 
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
-                                       double post_scale, cudaStream_t st, bool *fused);
+                                       double post_scale, cudaStream_t st);
 
 cudaError_t launch_halo_self(const Lvl &L, double *d, int px, int py, cudaStream_t st);
 
@@ -2889,22 +2486,14 @@ cudaError_t launch_half_sweep(const Lvl &L0, double *u, const double *f, int col
     // every half-sweep kernel reads f at the relaxed colour only: a view
     // whose f colour stride differs shifts the f base instead
     f += (long long)color * (L0.fcs - L0.cstride);
-    bool fused = false;
-    cudaError_t e = launch_half_sweep_k(L0, u, f, color, rho, zero_start, nbr_zero, post_scale,
-                                        st, &fused);
-    if (e == cudaSuccess && (L0.hflags & 1) && !fused) {
-        // this variant does not write halo copies itself
-        e = launch_halo_self(L0, u, (L0.hflags >> 1) & 1, (L0.hflags >> 2) & 1, st);
-    }
-    return e;
+    return launch_half_sweep_k(L0, u, f, color, rho, zero_start, nbr_zero, post_scale, st);
 }
 
 // fast half-sweep with the fused <f, new u> partial sums (CG's <r, z>):
-// available for uniform levels whose 16-level segments tile nz (no fused
-// halo); partials[0 .. *np) receive per-CTA sums in a fixed order.
+// available for uniform levels whose 16-level segments tile nz;
+// partials[0 .. *np) receive per-CTA sums in a fixed order.
 bool half_sweep_dot_ok(const Lvl &L) {
-    return !g_smoother_exact && L.uniform && L.seg == 16 && L.nz % 16 == 0 && L.nz / 16 <= 8 &&
-           !(L.hflags & 1);
+    return !g_smoother_exact && L.uniform && L.seg == 16 && L.nz % 16 == 0 && L.nz / 16 <= 8;
 }
 
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
@@ -2933,11 +2522,11 @@ cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int 
                                         ntiles, hx, partials, nullptr);
     };
     if (nbr_zero) {
-        if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 1, true, false, 520, true>);
-        else run(k_half_sweep_seg<16, 4, 2, 1, true, false, 0, true>);
+        if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 1, true, 520, true>);
+        else run(k_half_sweep_seg<16, 4, 2, 1, true, 0, true>);
     } else {
-        if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, true>);
-        else run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, true>);
+        if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, 520, true>);
+        else run(k_half_sweep_seg<16, 4, 2, 0, true, 0, true>);
     }
     return cudaGetLastError();
 }
@@ -2945,7 +2534,7 @@ cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int 
 // variable-coefficient levels the fast smoother handles with
 // k_half_sweep_segv (16 warps, SEG = nz / 16)
 static int segv_seg(const Lvl &L) {
-    if (g_smoother_exact || L.uniform || L.nz > 256 || L.nz % 16 || getenv("PMG_VAR_EXACT"))
+    if (g_smoother_exact || L.uniform || L.nz > 256 || L.nz % 16)
         return 0;
     const int seg = L.nz / 16;
     return (seg == 1 || seg == 2 || seg == 4 || seg == 8 || seg == 16) ? seg : 0;
@@ -2992,7 +2581,7 @@ static void launch_segv_mode(const Lvl &L, double *u, double *uw, const double *
 // Fast mode, no fused halo: uniform levels whose 16-level segments tile nz
 // (k_half_sweep_seg) or variable levels of k_half_sweep_segv.
 bool half_sweep_res_ok(const Lvl &L) {
-    return half_sweep_dot_ok(L) || (segv_seg(L) && !(L.hflags & 1));
+    return half_sweep_dot_ok(L) || segv_seg(L);
 }
 
 cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, const double *f,
@@ -3024,9 +2613,9 @@ cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, con
     // configs[1]'s fine level; at 3 CTAs / SM (80 registers, spills) 517 us,
     // with the incoming values staged in shared memory by cp.async 413 /
     // 538 us at 2 / 3 CTAs
-    if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 520, false, 1>);
-    else if (L.plane == 264) run(k_half_sweep_seg<16, 4, 2, 0, true, false, 264, false, 1>);
-    else run(k_half_sweep_seg<16, 4, 2, 0, true, false, 0, false, 1>);
+    if (L.plane == 520) run(k_half_sweep_seg<16, 4, 2, 0, true, 520, false, 1>);
+    else if (L.plane == 264) run(k_half_sweep_seg<16, 4, 2, 0, true, 264, false, 1>);
+    else run(k_half_sweep_seg<16, 4, 2, 0, true, 0, false, 1>);
     return cudaGetLastError();
 }
 
@@ -3057,8 +2646,8 @@ cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int 
     };
 #define PMG_FSQ(P)                                                                   \
     do {                                                                             \
-        if (nbr_zero) run(k_half_sweep_seg<16, 4, 3, 1, true, false, P, false, 3>); \
-        else run(k_half_sweep_seg<16, 4, 3, 0, true, false, P, false, 3>);         \
+        if (nbr_zero) run(k_half_sweep_seg<16, 4, 3, 1, true, P, false, 3>); \
+        else run(k_half_sweep_seg<16, 4, 3, 0, true, P, false, 3>);         \
     } while (0)
     if (L.plane == 520) PMG_FSQ(520);
     else if (L.plane == 264) PMG_FSQ(264);
@@ -3067,51 +2656,6 @@ cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int 
     return cudaGetLastError();
 }
 
-// fused coarse-grid correction + half-sweep (k_half_sweep_pro): available
-// in fast mode on uniform levels whose segments tile nz
-bool half_sweep_pro_ok(const Lvl &F) {
-    return !g_smoother_exact && F.uniform && (F.seg == 4 || F.seg == 8 || F.seg == 16) &&
-           F.nz % F.seg == 0 && F.nz / F.seg <= 8;
-}
-
-cudaError_t launch_half_sweep_pro(const Lvl &F, const Lvl &C, double *u, const double *f,
-                                  const double *cu, int color, cudaStream_t st) {
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    const int hx = ((F.nx + 1) / 2 + 31) / 32;
-    const int ntiles = hx * F.ny;
-    const int nw = F.nz / F.seg;
-    const size_t sm = sizeof(double) * (7 * (size_t)F.nz + 4 * 16 * 32);
-    auto run = [&](auto kern) {
-        int occ = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * nw, sm);
-        const int cap = sm_count() * (occ > 0 ? occ : 1);
-        const int grid = ntiles < cap ? ntiles : cap;
-        kern<<<grid, 32 * nw, sm, st>>>(F, C, u, f, cu, color, ntiles, hx);
-    };
-    static int pb = -1;
-    if (pb < 0) {
-        const char *e = getenv("PMG_PRO_PB");
-        pb = e ? atoi(e) : 2;
-    }
-    if (F.seg == 16 && pb == 4 && F.plane == 520 && C.plane == 264) {
-        run(k_half_sweep_pro<16, 520, 264, false, 4>);
-    } else if (F.seg == 16 && pb == 1 && F.plane == 520 && C.plane == 264) {
-        run(k_half_sweep_pro<16, 520, 264, false, 1>);
-    } else if (F.seg == 16) {
-        if (F.plane == 520 && C.plane == 264) run(k_half_sweep_pro<16, 520, 264, false>);
-        else if (F.plane == 264 && C.plane == 136) run(k_half_sweep_pro<16, 264, 136, false>);
-        else if (F.plane == 136 && C.plane == 72) run(k_half_sweep_pro<16, 136, 72, false>);
-        else run(k_half_sweep_pro<16, 0, 0, false>);
-    } else if (F.seg == 8) {
-        run(k_half_sweep_pro<8, 0, 0, false>);
-    } else {
-        run(k_half_sweep_pro<4, 0, 0, false>);
-    }
-    cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess && (F.hflags & 1))
-        e = launch_halo_self(F, u, (F.hflags >> 1) & 1, (F.hflags >> 2) & 1, st);
-    return e;
-}
 
 template <int P, int NW>
 static void band_attrs_nw() {
@@ -3147,7 +2691,7 @@ void setup_kernel_attributes() {
 }
 
 
-// tensor maps for k_half_sweep_tx: 3-D views (pitch, nz, ny + 2) of one
+// tensor maps of the band kernel: 3-D views (pitch, nz, ny + 2) of one
 // colour array with a box of boxw columns x kc levels x 1 row
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -3175,42 +2719,6 @@ static bool make_tmap(CUtensorMap *m, const double *base, const Lvl &L, int boxw
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// k_half_sweep_tx launch (exact arithmetic); false if not applicable here
-static bool launch_half_sweep_tx(const Lvl &L, double *u, const double *f, int color, double rho,
-                                 int zero_start, int nbr_zero, double post_scale, cudaStream_t st) {
-    static int cfg = -1;
-    if (cfg < 0) {
-        const char *e = getenv("PMG_TX");          // tuning: 8 (KC 8, 3 warps) / 16 (KC 16, 2 warps)
-        cfg = e ? atoi(e) : 16;
-    }
-    const int kc = (cfg == 8) ? 8 : 16;
-    if (!L.uniform || L.nz % kc != 0 || L.nz > 256 || (L.hflags & 1)) return false;
-    const int o = color ^ 1;
-    CUtensorMap mF, mW, mSN;
-    if (!make_tmap(&mF, f + (long long)color * L.cstride, L, 32, kc) ||
-        !make_tmap(&mW, u + (long long)o * L.cstride, L, 36, kc) ||
-        !make_tmap(&mSN, u + (long long)o * L.cstride, L, 32, kc))
-        return false;
-    const int hx = ((L.nx + 1) / 2 + 31) / 32;
-    const int ntiles = hx * L.ny;
-    auto run = [&](auto kern, int nw, int R) {
-        const size_t slot = (size_t)kc * 132;
-        const size_t per_warp = R * slot + (size_t)L.nz * 32;
-        const size_t sm = 8 * (nw * per_warp + 3 * (size_t)L.nz + 2) + 8 * (size_t)nw * R + 128;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            attr = true;
-        }
-        int grid = (ntiles + nw - 1) / nw;
-        if (grid > sm_count()) grid = sm_count();
-        kern<<<grid, 32 * nw, sm, st>>>(L, u, color, rho, zero_start, nbr_zero, post_scale,
-                                        ntiles, hx, mF, mW, mSN);
-    };
-    if (kc == 8) run(k_half_sweep_tx<8, 4>, 3, 4);
-    else run(k_half_sweep_tx<16, 3>, 2, 3);
-    return true;
-}
 
 // k_half_sweep_band: configs[1]'s fine level shape (nz = 128, plane 520),
 // neighbours read, no fused halo
@@ -3221,11 +2729,6 @@ static size_t band_smem() {   // sized for up to 16 compute warps
                              11 * BAND_NZ + 2 * 16 * 32 + 16) + 12 * 8 + 128;
 }
 
-static bool band_on() {
-    static int v = -1;
-    if (v < 0) v = getenv("PMG_BAND") ? atoi(getenv("PMG_BAND")) : 1;
-    return v == 1;
-}
 
 // compute warps of k_half_sweep_band: 16 (8 levels each) on rows of >= 512
 // cells per colour -- 2048^2: 1214 -> 1008 us, 1024^2: 284 -> 260 us per
@@ -3233,21 +2736,15 @@ static bool band_on() {
 // (512^2: 71.4 -> 75.5 us, 256^2: 20.9 -> 23.5 us)
 static int band_nw(const Lvl &L) { return (L.nx / 2 >= 512) ? 16 : 8; }
 
-static bool band_l1() {   // level 2 (nx = 256) on the band kernel too
-    static int v = -1;
-    if (v < 0) v = getenv("PMG_BAND_L2") ? atoi(getenv("PMG_BAND_L2")) : 1;
-    return v == 1;
-}
 
 static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int color,
                                    double rho, int zero_start, int nbr_zero, double post_scale,
                                    cudaStream_t st, double *partials, int *np,
                                    bool fsq, double *res_uw) {
     const int hrow = L.nx / 2;
-    if (!band_on() || g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
-        !(L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
-          (L.plane == 136 && band_l1())) ||
-        L.seg != 16 || nbr_zero || (L.hflags & 1) || L.nx % 2 || hrow % 32 || hrow < 64 ||
+    if (g_smoother_exact || !L.uniform || L.nz != BAND_NZ ||
+        !(L.plane == 1032 || L.plane == 520 || L.plane == 264 || L.plane == 136) ||
+        L.seg != 16 || nbr_zero || L.nx % 2 || hrow % 32 || hrow < 64 ||
         L.ny < 8 || L.rys != 1 || L.rxn < 1 || L.ryn < 1)
         return false;
     // the fused-residual mode fits the registers of the 16-warp kernel only
@@ -3266,15 +2763,13 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     // 2 at 8 strips (nx = 512: 76.3 us; 4 -> 80.3), 1 below
     // (the smallest count that makes strips x bands a multiple of the SMs:
     // nstrip / gcd(nstrip, SMs) -- 8 at 32 strips on 148 SMs)
-    static int ups_env = -1;
-    if (ups_env < 0) ups_env = getenv("PMG_BAND_UPS") ? atoi(getenv("PMG_BAND_UPS")) : 0;
     int gcd = nstrip, bsm = sm_count();
     while (bsm) {
         const int t = gcd % bsm;
         gcd = bsm;
         bsm = t;
     }
-    const int ups = ups_env ? ups_env : nstrip / gcd;
+    const int ups = nstrip / gcd;
     int nband = (ups * sm_count() + nstrip - 1) / nstrip;
     if (nband > nrows) nband = nrows;
     const int band_rows = (nrows + nband - 1) / nband;
@@ -3323,15 +2818,14 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
 
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
-                                       double post_scale, cudaStream_t st, bool *fused) {
+                                       double post_scale, cudaStream_t st) {
     if (launch_half_sweep_band(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st, nullptr,
                                nullptr, false)) {
-        *fused = false;
         return cudaGetLastError();
     }
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
-    if (!g_smoother_exact && !L.uniform && L.nz <= 256 && getenv("PMG_VAR_EXACT") == nullptr) {
+    if (!g_smoother_exact && !L.uniform && L.nz <= 256) {
         // variable coefficients: 16 warps, SEG = nz / 16 (must divide)
         int seg = 0;
         if (L.nz % 16 == 0 && L.nz / 16 <= 16) seg = L.nz / 16;
@@ -3388,45 +2882,35 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             const bool lean = rho == 1.0 && !zero_start;   // compile-time store path
             // compile-time plane stride for the large levels of nz = 128
             // (pitch of nx = 1024, 512, 256)
-            const int plc = (L.seg == 16 && full && !(L.hflags & 1)) ? (int)L.plane : 0;
+            const int plc = (L.seg == 16 && full) ? (int)L.plane : 0;
 #define PMG_SEGP(S, P)                                                                \
     do {                                                                              \
-        if (lean && nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, false, P, false, 0, true>); \
-        else if (lean) run(k_half_sweep_seg<S, 4, 3, 0, true, false, P, false, 0, true>); \
-        else if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, false, P>);        \
-        else run(k_half_sweep_seg<S, 4, 3, 0, true, false, P>);                      \
+        if (lean && nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, P, false, 0, true>); \
+        else if (lean) run(k_half_sweep_seg<S, 4, 3, 0, true, P, false, 0, true>); \
+        else if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, P>);        \
+        else run(k_half_sweep_seg<S, 4, 3, 0, true, P>);                      \
     } while (0)
 #define PMG_SEGF(S)                                                                   \
     do {                                                                              \
-        if (full && (L.hflags & 1)) {                                                 \
-            if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true, true>);              \
-            else run(k_half_sweep_seg<S, 4, 3, 0, true, true>);                       \
-        } else if (full) {                                                            \
+        if (full) {                                                                   \
             if (nbr_zero) run(k_half_sweep_seg<S, 4, 3, 1, true>);                    \
             else run(k_half_sweep_seg<S, 4, 3, 0, true>);                             \
-        } else if (L.hflags & 1) {                                                    \
-            run(k_half_sweep_seg<S, 4, 2, -1, false, true>);                          \
         } else {                                                                      \
             run(k_half_sweep_seg<S, 4, 2>);                                           \
         }                                                                             \
     } while (0)
-            static int small = -1;
-            if (small < 0) {
-                // levels of <= 64 tiles (nx <= 64 at nz = 128): 5.5 -> 4.5 us per
-                // sweep; 256 tiles (nx = 128) is slower this way (6.6 -> 7.9)
-                const char *e = getenv("PMG_SMALL_TILES");
-                small = e ? atoi(e) : 64;
-            }
-            if (L.seg == 16 && full && !(L.hflags & 1) && ntiles <= small) {
+            // levels of <= 64 tiles (nx <= 64 at nz = 128): 5.5 -> 4.5 us per
+            // sweep; 256 tiles (nx = 128) is slower this way (6.6 -> 7.9)
+            if (L.seg == 16 && full && ntiles <= 64) {
                 // launch-latency-bound small level: all 16 levels' loads of a
                 // tile in one batch (one memory round trip per tile)
-                if (lean && nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, false, 0, false, 0, true>);
-                else if (lean) run(k_half_sweep_seg<16, 16, 1, 0, true, false, 0, false, 0, true>);
-                else if (nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, false, 0>);
-                else run(k_half_sweep_seg<16, 16, 1, 0, true, false, 0>);
-            } else if (plc == 520 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 520);
-            else if (plc == 264 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 264);
-            else if (plc == 136 && !getenv("PMG_NO_PLC")) PMG_SEGP(16, 136);
+                if (lean && nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, 0, false, 0, true>);
+                else if (lean) run(k_half_sweep_seg<16, 16, 1, 0, true, 0, false, 0, true>);
+                else if (nbr_zero) run(k_half_sweep_seg<16, 16, 1, 1, true, 0>);
+                else run(k_half_sweep_seg<16, 16, 1, 0, true, 0>);
+            } else if (plc == 520) PMG_SEGP(16, 520);
+            else if (plc == 264) PMG_SEGP(16, 264);
+            else if (plc == 136) PMG_SEGP(16, 136);
             else switch (L.seg) {
             case 4: PMG_SEGF(4); break;
             case 8: PMG_SEGF(8); break;
@@ -3435,13 +2919,9 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             }
 #undef PMG_SEGF
 #undef PMG_SEGP
-            *fused = true;
             return cudaGetLastError();
         }
     }
-    if (hs_variant() == 4 && L.uniform &&
-        launch_half_sweep_tx(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st))
-        return cudaGetLastError();
     const bool need_old = !zero_start && rho != 1.0;
     const size_t sm = half_sweep_smem(L, need_old);
     const dim3 b(HS_THREADS);
@@ -3455,7 +2935,6 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             attr_set[0] = true;
         }
         k_half_sweep<true><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
-        *fused = true;
     } else {
         if (!attr_set[1]) {
             cudaFuncSetAttribute(k_half_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -3465,7 +2944,6 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
             attr_set[1] = true;
         }
         k_half_sweep<false><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
-        *fused = true;
     }
     return cudaGetLastError();
 }
@@ -3486,29 +2964,19 @@ cudaError_t launch_restrict(const Lvl &F, const Lvl &C, const double *fu, double
 cudaError_t launch_prolong(const Lvl &F, const Lvl &C, const double *cu, double *fu, int add,
                            int cmask, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (!(F.hflags & 1) && F.nx % 4 == 0 && C.nx >= 2 && !getenv("PMG_PROLONG_NOQ")) {
+    if (F.nx % 4 == 0 && C.nx >= 2) {
         const int npair = C.nx >> 1;
-        static int jb = -1;
-        if (jb < 0) {
-            // coarse rows per thread: 2 measured best on B200 (configs[1]
-            // fine level, black only: 1 -> 310 us, 2 -> 252, 4 -> 274, 8 -> 341)
-            const char *e = getenv("PMG_PROLONG_JB");
-            jb = e ? atoi(e) : 2;
-        }
+        // two coarse rows per thread (measured on B200 at configs[1]'s fine
+        // level, black only: 1 row -> 310 us, 2 -> 252, 4 -> 274, 8 -> 341)
         const int gx = (npair + 127) / 128;
-        if (jb == 2 && cmask == 2)
+        if (cmask == 2)
             k_prolong_w<2, 2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
-        else if (jb == 2) k_prolong_w<2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
-        else if (jb == 4) k_prolong_w<4><<<dim3(gx, F.nz, (C.ny + 3) / 4), 128, 0, st>>>(F, C, cu, fu, add, cmask);
-        else if (jb == 8) k_prolong_w<8><<<dim3(gx, F.nz, (C.ny + 7) / 8), 128, 0, st>>>(F, C, cu, fu, add, cmask);
-        else k_prolong_q<<<dim3(gx, F.nz, C.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+        else
+            k_prolong_w<2><<<dim3(gx, F.nz, (C.ny + 1) / 2), 128, 0, st>>>(F, C, cu, fu, add, cmask);
         return cudaGetLastError();
     }
     const int n2 = (cmask == 3 ? 2 : 1) * ((F.nx + 1) / 2);
-    if (F.hflags & 1)
-        k_prolong<true><<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
-    else
-        k_prolong<false><<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
+    k_prolong<<<dim3((n2 + 127) / 128, F.nz, F.ny), 128, 0, st>>>(F, C, cu, fu, add, cmask);
     return cudaGetLastError();
 }
 
@@ -3599,7 +3067,7 @@ cudaError_t launch_cg_direction(long long n, const double *num, const double *de
 cudaError_t launch_cg_up(long long n, const double *an, const double *ad, const double *bn,
                          const double *bd, const double *z, double *p, double *u, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    if (n % 2 == 0 && !getenv("PMG_CG_SCALAR")) {
+    if (n % 2 == 0) {
         // whole allocations: even length, 16-byte aligned
         const long long n2 = n / 2;
         long long b = (n2 + 255) / 256;
@@ -3619,7 +3087,7 @@ cudaError_t launch_cg_update(const Lvl &L, const double *num, const double *den,
                              double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const long long n = 2LL * L.cstride;
-    if (L.pitch % 2 == 0 && !getenv("PMG_CG_SCALAR")) {
+    if (L.pitch % 2 == 0) {
         const int rows = 2 * L.nz * (L.ny + 2);
         int g = 8 * sm_count();
         if (g > (rows + 7) / 8) g = (rows + 7) / 8;

@@ -29,8 +29,7 @@ from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
 from .partition import (Decomposition, DistField, LevelLayout, _dist, _stream, collect,
-                        distribute, dist_norm, halo_exchange, reduce_parts, scalar_buffer,
-                        self_halo_flags)
+                        distribute, dist_norm, halo_exchange, reduce_parts, scalar_buffer)
 from .smoother import BLACK, RED, LineSmoother
 from .stencil import PanelOperator
 
@@ -363,44 +362,12 @@ def prolong(df: DistField, coarse: Level, fine: Level, out: DistField | None = N
 def _prolong_add(cu: DistField, coarse: Level, fine: Level, u: DistField,
                  black_only: bool = False, exchange: bool = False) -> None:
     """u += P e (into black cells only if ``black_only``); ``exchange``
-    also refreshes u's halo (fused into the kernel on a single part)."""
+    also refreshes u's halo."""
     st = _stream()
-    hf = self_halo_flags(u.layout) if exchange else 0
     for w, cf in cu.parts.items():
-        call("pmg_prolong_colors_halo", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
-             u.parts[w].ptr, 1, 2 if black_only else 3, hf, st)
+        call("pmg_prolong_colors", fine.op.handles[w].h, coarse.op.handles[w].h, cf.ptr,
+             u.parts[w].ptr, 1, 2 if black_only else 3, st)
     if exchange:
-        if hf:
-            u.layout.halo_count += 1
-        else:
-            halo_exchange(u)
-
-
-#: fuse the coarse-grid correction into the first post-smoothing half-sweep
-#: (k_half_sweep_pro: fast smoother, uniform levels, rho = 1).  Off by
-#: default: it saves the 10 N-byte prolongation pass but the fused kernel
-#: is latency-bound on its extra coarse loads and measured slower on B200
-#: (configs[1] fine level: 835-970 us vs 640 us for black-only
-#: prolongation + half-sweep, DESIGN.md section 3)
-FUSE_PROLONG = False
-
-
-def _pro_ok(lev: Level) -> bool:
-    return all(load().pmg_half_sweep_prolong_ok(h.h) == 1 for h in lev.op.handles.values())
-
-
-def _sweep_prolong(lev: Level, coarse: Level, cu: DistField, s) -> None:
-    """Red half-sweep of ``s.u`` as if ``s.u += P cu`` and a halo exchange
-    had come first (pmg_half_sweep_prolong), then the red halo exchange."""
-    u = s.u
-    hf = self_halo_flags(u.layout)
-    st = _stream()
-    for w, uf in u.parts.items():
-        call("pmg_half_sweep_prolong", lev.op.handles[w].h, coarse.op.handles[w].h, uf.ptr,
-             s.f.parts[w].ptr, cu.parts[w].ptr, RED, hf, st)
-    if hf:
-        u.layout.halo_count += 1
-    else:
         halo_exchange(u)
 
 
@@ -452,12 +419,6 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
             corr = prolong(scratch[c + 1].u, coarse, lev, out=s.r)
             _add_owned(s.u, corr)
             halo_exchange(s.u)
-        elif cfg.fused and lean and post >= 1 and FUSE_PROLONG and _pro_ok(lev):
-            # correction fused into the first red half-sweep (the black
-            # values it corrects are read only there, then overwritten)
-            _sweep_prolong(lev, coarse, scratch[c + 1].u, s)
-            lev.smoother.half_sweep_exchange(s.u, s.f, BLACK, cfg.rho)
-            post -= 1
         elif cfg.fused:
             _prolong_add(scratch[c + 1].u, coarse, lev, s.u, black_only=lean and post >= 1,
                          exchange=True)
@@ -561,7 +522,7 @@ def _parts_native_ok(hier: LevelHierarchy, cfg: MGConfig) -> bool:
     """The multi-part native driver takes hierarchies without folding whose
     parts all live here (in-process) or one per rank over NCCL."""
     from .partition import native_comm_ok
-    if not (cfg.graph and cfg.fused and USE_NATIVE and not FUSE_PROLONG and len(hier) > 0):
+    if not (cfg.graph and cfg.fused and USE_NATIVE and len(hier) > 0):
         return False
     if any(lev.fold_layout is not None for lev in hier.levels):
         return False
@@ -596,11 +557,9 @@ def _ptrs(df: DistField):
 def graph_key(cfg: MGConfig, f: DistField, u: DistField) -> tuple:
     """Cache key of the Python driver's captured cycle graphs (+ first):
     cycle shape, buffers, and the process-wide kernel selection (smoother
-    mode, fused halos) the graph's kernels were chosen under."""
-    from . import partition
+    mode) the graph's kernels were chosen under."""
     return (cfg.nu_pre, cfg.nu_post, cfg.rho, cfg.resolved_coarse_sweeps(), cfg.fused,
-            cfg.red_restrict, _ptrs(f), _ptrs(u), int(load().pmg_get_smoother_mode()),
-            partition._FUSED_HALO)
+            cfg.red_restrict, _ptrs(f), _ptrs(u), int(load().pmg_get_smoother_mode()))
 
 
 def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField | None = None):
@@ -617,7 +576,7 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
     """
     use_graph = cfg.graph and _dist() is None
     single = hier.fine.layout.px == 1 and hier.fine.layout.py == 1 and _dist() is None
-    if (use_graph and cfg.fused and USE_NATIVE and not FUSE_PROLONG and single):
+    if (use_graph and cfg.fused and USE_NATIVE and single):
         return _mg_solve_native(f, hier, cfg, out)
     if not single and USE_NATIVE_PARTS and _parts_native_ok(hier, cfg):
         return _mg_solve_parts(f, hier, cfg, out)

@@ -24,7 +24,6 @@ from __future__ import annotations
 
 import ctypes as C
 import math
-import os
 
 import numpy as np
 import torch
@@ -413,27 +412,6 @@ class _FaceBuffers:
 
 def _ptr(t: torch.Tensor):
     return C.c_void_p(t.data_ptr())
-
-
-def self_halo_flags(lay: "LevelLayout") -> int:
-    """halo_flags for kernels that refresh the halo ring themselves: nonzero
-    only for a single-part layout (its own neighbour in both directions)."""
-    if lay.px == 1 and lay.py == 1 and _FUSED_HALO:
-        return 1 | (2 if lay.periodic else 0) | (4 if lay.periodic else 0)
-    return 0
-
-
-# fused halos measured slower on B200 for configs[1] (boundary-tile epilogue
-# imbalances the persistent smoother grid): opt-in
-_FUSED_HALO = bool(os.environ.get("PMG_FUSED_HALO"))
-
-
-def set_fused_halo(on: bool) -> bool:
-    """Enable the in-kernel halo refresh for single-part layouts; returns the
-    previous setting."""
-    global _FUSED_HALO
-    prev, _FUSED_HALO = _FUSED_HALO, bool(on)
-    return prev
 
 
 def halo_exchange(df: DistField) -> None:

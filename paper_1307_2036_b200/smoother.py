@@ -15,7 +15,7 @@ from contextlib import contextmanager
 from dataclasses import dataclass
 
 from ._lib import call, load
-from .partition import DistField, _stream, halo_exchange, self_halo_flags
+from .partition import DistField, _stream, halo_exchange
 from .stencil import PanelOperator
 
 RED, BLACK = 0, 1
@@ -83,20 +83,9 @@ class LineSmoother:
     def half_sweep_exchange(self, u: DistField, f: DistField, color: int, rho: float = 1.0,
                             zero_start: bool = False, neighbors_zero: bool = False,
                             post_scale: float = 1.0) -> None:
-        """half_sweep followed by halo_exchange; on a single-part layout the
-        halo refresh is fused into the smoother kernel (same result, one
-        launch and one pass fewer).  Counts as one exchange."""
-        hf = self_halo_flags(u.layout)
-        if not hf:
-            self.half_sweep(u, f, color, rho, zero_start, neighbors_zero, post_scale)
-            halo_exchange(u)
-            return
-        st = _stream()
-        for w, uf in u.parts.items():
-            call("pmg_half_sweep_halo", self.op.handles[w].h, uf.ptr, f.parts[w].ptr, int(color),
-                 float(rho), int(bool(zero_start)), int(bool(neighbors_zero)),
-                 float(post_scale), hf, st)
-        u.layout.halo_count += 1
+        """half_sweep followed by halo_exchange (one exchange)."""
+        self.half_sweep(u, f, color, rho, zero_start, neighbors_zero, post_scale)
+        halo_exchange(u)
 
     def sweep(self, u: DistField, f: DistField, nsweeps: int = 1, rho: float = 1.0) -> None:
         """Red-black sweeps with a halo exchange after each half (smoother.py:184-191)."""

@@ -277,18 +277,10 @@ def test_exchange_counts(pmg):
     f = pmg.scatter_owned(uni((32, 32, 4), 0), hier.fine.layout)
     scratch = hier.make_scratch()
     scratch[0].f.copy_from(f)
-    from paper_1307_2036_b200 import multigrid as mgm
-    # reference sequence (separate prolongation + exchange), then the fused
-    # correction, which needs no exchange between prolongation and smoothing
-    for fuse, per_level in ((False, 5), (True, 4)):
-        mgm.FUSE_PROLONG = fuse
-        try:
-            hier.reset_counters()
-            pmg.v_cycle(hier, cfg, scratch)
-        finally:
-            mgm.FUSE_PROLONG = False
-        counts = [lev.layout.halo_count for lev in hier.levels]
-        assert counts[:-1] == [per_level] * 2 and counts[-1] == 2
+    hier.reset_counters()
+    pmg.v_cycle(hier, cfg, scratch)
+    counts = [lev.layout.halo_count for lev in hier.levels]
+    assert counts[:-1] == [5] * 2 and counts[-1] == 2
 
 
 def test_layout_round_trip(pmg):
@@ -401,28 +393,6 @@ def test_config2_mg_full_size(pmg, w):
     assert hist_err(rep.residual_history, g["history"]) <= 1e-8
 
 
-@pytest.mark.parametrize("name", OPS)
-def test_fused_halo_path(pmg, name):
-    """In-kernel halo refresh (opt-in) gives the same V-cycle and solve."""
-    from paper_1307_2036_b200 import partition
-    g, grid, params, cfg, hier = setup(pmg, name)
-    nx, nz = grid.nx, grid.nz
-    prev = partition.set_fused_halo(True)
-    try:
-        with pmg.exact_smoother():
-            scratch = hier.make_scratch()
-            scratch[0].f.copy_from(field(pmg, uni((nx, nx, nz), 2), hier.fine.layout))
-            pmg.v_cycle(hier, cfg, scratch)
-            assert np.array_equal(pmg.gather_owned(scratch[0].u), g["vcycle1"])
-        cfg2 = pmg.MGConfig(policy="explicit", explicit_levels=int(g["nlev"]), graph=False)
-        u, rep = pmg.mg_solve(pmg.scatter_owned(uni((nx, nx, nz), 2), hier.fine.layout), hier,
-                              cfg2)
-        assert rep.iterations == len(g["mg_history"]) - 1
-        assert hist_err(rep.residual_history, g["mg_history"]) <= 1e-10
-    finally:
-        partition.set_fused_halo(prev)
-
-
 @pytest.mark.parametrize("name", ["native_panel32", "native_flat32", "native_panel64_shallow"])
 def test_reference_native_problem(pmg, name):
     """The reference's own problem family run UNMODIFIED by the reference:
@@ -532,39 +502,6 @@ def test_rank_halo_path_on_device(pmg, px, py, periodic):
     assert not errors, errors
     for w in lay.workers:
         assert torch.equal(ranks[w].parts[w].data, ref.parts[w].data), w
-
-
-@pytest.mark.parametrize("workers", [1, 4])
-@pytest.mark.parametrize("periodic", [True, False])
-@pytest.mark.parametrize("graph", [False, True])
-def test_fused_prolongation(pmg, workers, periodic, graph):
-    """Coarse-grid correction fused into the first post-smoothing half-sweep
-    (pmg_half_sweep_prolong) against the separate prolongation + exchange:
-    same MG history and iterate to rounding, for periodic and mirror halos,
-    one part (self halo) and four parts (exchanged halos)."""
-    from paper_1307_2036_b200 import multigrid as mgm
-    nx, nz = 32, 8
-    grid = pmg.periodic_box(nx, nz, 0.01) if periodic else pmg.panel_grid(nx, nz, flat_mode=True)
-    params = pmg.toy_parameters(nx, nz, 1e-3, 3.3e-2)
-    fg = uni((nx, nx, nz), 11)
-    out = {}
-    for fuse in (False, True):
-        mgm.FUSE_PROLONG = fuse
-        try:
-            cfg = pmg.MGConfig(policy="explicit", explicit_levels=3, graph=graph, eps=1e-8)
-            hier = pmg.build_hierarchy(grid, params, cfg, pmg.Decomposition(nx, workers))
-            # uniform levels only: the flat box (Neumann) has variable
-            # boundary weights and keeps the separate prolongation
-            assert mgm._pro_ok(hier.fine) == periodic
-            f = pmg.scatter_owned(fg, hier.fine.layout)
-            u, rep = pmg.mg_solve(f, hier, cfg)
-            out[fuse] = (np.array(rep.residual_history), pmg.gather_owned(u))
-        finally:
-            mgm.FUSE_PROLONG = False
-    (h0, u0), (h1, u1) = out[False], out[True]
-    assert len(h0) == len(h1)
-    assert np.max(np.abs(h1 - h0) / h0) <= 1e-9
-    assert np.max(np.abs(u1 - u0)) <= 1e-11 * np.max(np.abs(u0))
 
 
 @pytest.mark.parametrize("periodic", [True, False])

@@ -98,9 +98,6 @@ for c, lev in enumerate(hier.levels):
         row["prolong_add"] = (round(t * 1e3, 1), round(18 * n / t / 1e6))
         t = timeit(lambda: mg._prolong_add(sc[c + 1].u, co, lev, s.u, black_only=True))
         row["prolong_black"] = (round(t * 1e3, 1), round(10 * n / t / 1e6))
-        if mg._pro_ok(lev):
-            t = timeit(lambda: mg._sweep_prolong(lev, co, sc[c + 1].u, s))
-            row["sweep_prolong"] = (round(t * 1e3, 1), round(14 * n / t / 1e6))
     t = timeit(lambda: pmg.halo_exchange(s.u))
     row["halo"] = round(t * 1e3, 1)
     print(f"L{c} nx={lev.layout.nx}: " + json.dumps(row), flush=True)
