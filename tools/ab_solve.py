@@ -1,6 +1,6 @@
 """A/B helper: one configs[1] MG solve (or --nx/--levels), prints the
 history, a hash of the iterate and the graph-replayed solve time; run it
-under different PMG_* switches and compare (bit-identical paths must print
+under different configurations and compare (bit-identical paths must print
 the same hash)."""
 import argparse
 import hashlib

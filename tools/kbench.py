@@ -58,7 +58,7 @@ hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
 sc = hier.persistent_scratch()
 f = pmg.scatter_owned(configs.rhs(a.nx, a.ny, a.nz, 0), hier.fine.layout)
 sc[0].f.copy_from(f)
-out = {"variant": os.environ.get("PMG_HS_VARIANT", "reg")}
+out = {}
 res = torch.zeros(1, dtype=torch.float64, device="cuda")
 for c, lev in enumerate(hier.levels):
     s = sc[c]
