@@ -1277,6 +1277,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
 // ---------------------------------------------------------------------------
 constexpr int BAND_NZ = 128, BAND_W = 32;
 static size_t band_smem();
+static size_t bandv_smem();
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -1764,6 +1765,279 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
     if (RES) {
         const double s2 = block_sum(dacc);
         if (threadIdx.x == 0) dotp[blockIdx.x] = s2;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row-marching TMA half-sweep for VARIABLE coefficients (configs[4]): the
+// producer / ring structure of k_half_sweep_band (f row j and the other
+// colour's row j+1 as tensor-map boxes, each other-colour row serving as N,
+// centre and S row) with k_half_sweep_segv's arithmetic: 16 compute warps of
+// 8 levels, the column's face weights and vertical coupling from the 2-D
+// factors (smoother.py:137-145 order), the per-cell pivots of the level
+// (L.invd), segment products formed on the fly -- bit-identical to
+// k_half_sweep_segv<8>.  Per lane, the next row's column coefficients are
+// loaded right after this row's RHS assembly and its pivots right after
+// this row's backward pass, so both loads overlap a column solve.
+// RES = 1 / 3: k_half_sweep_segv's fused-residual / f^2 modes.
+// ---------------------------------------------------------------------------
+template <int PLC, int RES = 0, bool LEAN = false>
+__global__ void __launch_bounds__(32 * 16, 1)
+k_half_sweep_bandv(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
+                   double post_scale, int nstrip, int nband, int band_rows,
+                   const __grid_constant__ CUtensorMap mF, const __grid_constant__ CUtensorMap mB,
+                   const __grid_constant__ CUtensorMap mE, double *__restrict__ partials,
+                   double *__restrict__ uw) {
+    constexpr int NW = 16, NZ = BAND_NZ, SEG = NZ / NW, B = 4;
+    extern __shared__ __align__(128) double bsm_raw[];
+    double *bsm = bsm_raw + (((128u - (smem_u32(bsm_raw) & 127u)) & 127u) >> 3);
+    double *ring = bsm;                              // [4][NZ][32] other colour rows
+    double *fring = ring + 4 * NZ * BAND_W;          // [2][NZ][32] f rows
+    double *edge = fring + 2 * NZ * 32;              // [4][NZ][2]  edge columns
+    double *tdrw = edge + 4 * NZ * 2;                // [NZ]   omega2 dr
+    double *tvp = tdrw + NZ;                         // [NZ+2] vprof (padded)
+    double *tvol = tvp + NZ + 2;                     // RES: [NZ] volprof
+    double *tdr = tvol + NZ;                         // RES: [NZ] dr
+    double *xh = tdr + NZ;                           // [NW][32] segment end h
+    double *xp = xh + NW * 32;                       // [NW][32] segment product of alpha
+    double *xy = xp + NW * 32;                       // [NW][32] segment start y
+    double *xq = xy + NW * 32;                       // [NW][32] segment product of mu
+    uint64_t *fullB = reinterpret_cast<uint64_t *>(xq + NW * 32);   // [4]
+    uint64_t *fullF = fullB + 4;                                     // [2]
+    double *wsum = reinterpret_cast<double *>(fullF + 2);            // [NW]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int t = threadIdx.x; t <= NZ; t += blockDim.x) {
+        if (t < NZ) {
+            tdrw[t] = L.drw[t];
+            if (RES == 1) {
+                tvol[t] = L.volprof[t];
+                tdr[t] = L.dr[t];
+            }
+        }
+        tvp[t] = L.vprof[t];
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q) mbar_init(fullB + q, 1);
+        for (int q = 0; q < 2; ++q) mbar_init(fullF + q, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const bool wrap = (L.hflags & HF_WRAP) != 0;
+    const int hrow = L.nx / 2;
+    const int nunits = nstrip * nband;
+    // ---- 16 compute warps; thread 0 also issues the rows' tensor-map
+    // boxes.  No warp of its own and no empty barriers: a ring slot is
+    // refilled only after the CTA barrier that follows the last right-hand
+    // side assembly reading it (the column solve reads registers and the
+    // segment arrays, never the rings), so slots are free by construction.
+    // At step j (after that barrier) it issues other-colour row j + 3 and f
+    // row j + 2; a unit's first step issues its first four rows and two f rows.
+    // 512 threads: 128 registers per thread ----
+    constexpr long long pl = PLC;
+    const int k0 = w * SEG;
+    const double scale = rho * post_scale;
+    const double omr = 1.0 - rho;
+    // the pivot field keeps the level's own colour stride (a lagged-norm
+    // view moves only the iterate's red array: Lvl::fcs)
+    const double *invdc = L.invd + (long long)c * (L.fcs - L.cstride);
+    double dacc = 0.0;
+    unsigned seqb = 0, seqf = 0;
+    for (int unit = blockIdx.x; unit < nunits; unit += gridDim.x) {
+        const int strip = L.rx0 + (unit % nstrip) * L.rxs, band = unit / nstrip;
+        const int h0 = strip * 32;
+        const int j0 = L.ry0 + band * band_rows, j1 = min(L.ry0 + L.ryn, j0 + band_rows);
+        if (j0 >= j1) continue;
+        const bool eleft = wrap && h0 == 0, eright = wrap && h0 + 32 == hrow;
+        const int xw = eleft ? OFF + hrow - 2 : OFF + h0 - 2;
+        const int xe = eright ? OFF : OFF + h0 + 32;
+        // tensor-map boxes of other-colour row r (sequence number sq) and f row r
+        auto put_b = [&](int r, unsigned sq) {
+            const int slot = sq & 3;
+            const int rr = wrap ? (r < 0 ? r + L.ny : (r >= L.ny ? r - L.ny : r)) : r;
+            fence_proxy_async();
+            mbar_expect_tx(fullB + slot, NZ * BAND_W * 8 + NZ * 2 * 8);
+            tma_box3(ring + slot * NZ * BAND_W, &mB, OFF + h0, 0, rr + 1, fullB + slot);
+            tma_box3(edge + slot * NZ * 2, &mE, ((r + L.par + c) & 1) ? xe : xw, 0, rr + 1,
+                     fullB + slot);
+        };
+        auto put_f = [&](int r, unsigned sq) {
+            const int slot = sq & 1;
+            fence_proxy_async();
+            mbar_expect_tx(fullF + slot, NZ * 32 * 8);
+            tma_box3(fring + slot * NZ * 32, &mF, OFF + h0, 0, r + 1, fullF + slot);
+        };
+        if (threadIdx.x == 0) {
+            put_b(j0 - 1, seqb);
+            put_b(j0, seqb + 1);
+            put_b(j0 + 1, seqb + 2);
+            if (j0 + 2 <= j1) put_b(j0 + 2, seqb + 3);
+            put_f(j0, seqf);
+            if (j0 + 1 < j1) put_f(j0 + 1, seqf + 1);
+        }
+        // the column coefficients and pivots of row jj (loaded a row ahead)
+        double wxm, wxp, wym, wyp, cvn, vhn = 0.0, oswn = 0.0;
+        double vi[SEG];
+        auto load_coef = [&](int jj) {
+            const int i = 2 * (h0 + lane) + ((jj + L.par + c) & 1);
+            const long long q2 = (long long)jj * L.nx + i;
+            wxm = L.wx[(long long)jj * (L.nx + 1) + i];
+            wxp = L.wx[(long long)jj * (L.nx + 1) + i + 1];
+            wym = L.wy[q2];
+            wyp = L.wy[(long long)(jj + 1) * L.nx + i];
+            cvn = L.vcoef * L.av[q2];
+            if (RES == 1) {
+                vhn = L.vh[q2];
+                oswn = L.omega2 * L.sumw[q2];
+            }
+        };
+        auto load_piv = [&](int jj) {
+            const long long p0 = at(L, c, k0, jj, h0 + lane);
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) vi[e] = invdc[p0 + (long long)e * pl];
+        };
+        // RES: the incoming values of this lane's column (as the band kernel)
+        double vo[RES == 1 ? SEG : 1], um = 0.0, un = 0.0;
+        auto load_old = [&](int jj) {
+            const long long p0 = at(L, c, k0, jj, h0 + lane);
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) vo[e] = u[p0 + (long long)e * pl];
+            um = u[p0 - ((k0 > 0) ? pl : 0)];
+            un = u[p0 + (long long)((k0 + SEG < NZ) ? SEG : SEG - 1) * pl];
+        };
+        load_coef(j0);
+        load_piv(j0);
+        if (RES == 1) load_old(j0);
+        for (int j = j0; j < j1; ++j) {
+            const long long pc = at(L, c, k0, j, h0 + lane);
+            for (int r = (j == j0 ? j - 1 : j + 1); r <= j + 1; ++r) {
+                const unsigned q = seqb + (unsigned)(r - (j0 - 1));
+                mbar_wait(fullB + (q & 3), (q >> 2) & 1);
+            }
+            const unsigned qf = seqf + (unsigned)(j - j0);
+            mbar_wait(fullF + (qf & 1), (qf >> 1) & 1);
+            const unsigned qs = seqb + (unsigned)(j - 1 - (j0 - 1));
+            const double *Srow = ring + (qs & 3) * NZ * BAND_W;
+            const double *Crow = ring + ((qs + 1) & 3) * NZ * BAND_W;
+            const double *Nrow = ring + ((qs + 2) & 3) * NZ * BAND_W;
+            const double *Ce = edge + ((qs + 1) & 3) * NZ * 2;
+            const double *Frow = fring + (qf & 1) * NZ * 32;
+            const int s0 = (j + L.par + c) & 1;
+            const int iw = max(lane - 1 + s0, 0), ie = min(lane + s0, 31);
+            const bool wfix = s0 == 0 && lane == 0, efix = s0 == 1 && lane == 31;
+            const double cv = cvn, vh = vhn, osw = oswn;
+            double r[SEG], pq[SEG];
+            double rpend = 0.0, bpend = 0.0;
+#pragma unroll
+            for (int b8 = 0; b8 < SEG; b8 += B) {
+#pragma unroll
+                for (int e = 0; e < B; ++e) {
+                    const int k = k0 + b8 + e;
+                    const double *cr = Crow + k * BAND_W;
+                    double vw = cr[iw], ve = cr[ie];
+                    if (wfix) vw = Ce[k * 2 + 1];
+                    if (efix) ve = Ce[k * 2 + 0];
+                    const double vs = Srow[k * BAND_W + lane];
+                    const double vn = Nrow[k * BAND_W + lane];
+                    const double fv = Frow[k * 32 + lane];
+                    if (RES == 3) dacc = __fma_rn(fv, fv, dacc);
+                    double g = wxm * vw;
+                    g = g + wxp * ve;
+                    g = g + wym * vs;
+                    g = g + wyp * vn;
+                    g = g * tdrw[k];
+                    g = g + fv;
+                    r[b8 + e] = g;
+                    if (RES == 1) {
+                        const double vk = vo[b8 + e];
+                        const double bm = (k >= 1) ? cv * tvp[k] : 0.0;
+                        const double bp = (k + 1 < NZ) ? cv * tvp[k + 1] : 0.0;
+                        if (b8 + e > 0) {
+                            const double q = __fma_rn(bpend, vk, rpend);
+                            dacc = __fma_rn(q, q, dacc);
+                        }
+                        double d = vh * tvol[k];
+                        d = d + osw * tdr[k];
+                        d = d + cv * (tvp[k] + tvp[k + 1]);
+                        const double tu = __fma_rn(-bm, um, d * vk);   // d u_k - bm u_{k-1}
+                        rpend = g - tu;
+                        bpend = bp;
+                        um = vk;
+                    }
+                }
+            }
+            if (RES == 1) {
+                const double q = __fma_rn(bpend, un, rpend);
+                dacc = __fma_rn(q, q, dacc);
+                if (j + 1 < j1) load_old(j + 1);
+            }
+            if (j + 1 < j1) load_coef(j + 1);
+            // local forward h_k = iota_k r_k + alpha_k h_{k-1}, alpha_k = (cv vp_k) iota_k
+            double hp = 0.0, pf = 1.0;
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                const int k = k0 + e;
+                const double al = (k == 0) ? 0.0 : (cv * tvp[k]) * vi[e];
+                pf *= al;
+                pq[e] = pf;
+                hp = __fma_rn(al, hp, vi[e] * r[e]);
+                r[e] = hp;
+            }
+            xh[w * 32 + lane] = hp;
+            xp[w * 32 + lane] = pf;
+            bar_compute<NW>();
+            // every warp has assembled step j: the slots of other-colour row
+            // j - 1 and f row j are free -- for rows j + 3 and j + 2 (two
+            // rows of look-ahead in both rings)
+            if (threadIdx.x == 0) {
+                if (j + 3 <= j1) put_b(j + 3, seqb + (unsigned)(j + 3 - (j0 - 1)));
+                if (j + 2 < j1) put_f(j + 2, seqf + (unsigned)(j + 2 - j0));
+            }
+            double G = 0.0;
+            for (int sg = 0; sg < w; ++sg) G = __fma_rn(xp[sg * 32 + lane], G, xh[sg * 32 + lane]);
+            double yp = 0.0, qq = 1.0;
+#pragma unroll
+            for (int e = SEG - 1; e >= 0; --e) {
+                const int k = k0 + e;
+                const double mu = (k + 1 < NZ) ? (cv * tvp[k + 1]) * vi[e] : 0.0;
+                const double g = __fma_rn(pq[e], G, r[e]);
+                qq *= mu;
+                pq[e] = qq;
+                yp = __fma_rn(mu, yp, g);
+                r[e] = yp;
+            }
+            if (j + 1 < j1) load_piv(j + 1);
+            xy[w * 32 + lane] = yp;
+            xq[w * 32 + lane] = qq;
+            bar_compute<NW>();
+            double X = 0.0;
+            for (int sg = NW - 1; sg > w; --sg)
+                X = __fma_rn(xq[sg * 32 + lane], X, xy[sg * 32 + lane]);
+#pragma unroll
+            for (int e = 0; e < SEG; ++e) {
+                double y = __fma_rn(pq[e], X, r[e]);
+                const long long q = pc + (long long)e * pl;
+                if (!LEAN && RES != 1 && zero_start) {
+                    if (scale != 1.0) y = y * scale;
+                } else if (!LEAN && RES != 1 && rho != 1.0) {
+                    y = y * rho;
+                    y = y + omr * u[q];
+                }
+                if (RES == 1) uw[q] = y;
+                else u[q] = y;
+            }
+        }
+        seqb += (unsigned)(j1 - j0 + 2);
+        seqf += (unsigned)(j1 - j0);
+    }
+    if (RES) {   // fixed-order reduction over the compute warps
+        const double ws = warp_sum(dacc);
+        if (lane == 0) wsum[w] = ws;
+        bar_compute<NW>();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < NW; ++q) t += wsum[q];
+            partials[blockIdx.x] = t;
+        }
     }
 }
 
@@ -2500,6 +2774,10 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
                                    double rho, int zero_start, int nbr_zero, double post_scale,
                                    cudaStream_t st, double *partials, int *np, bool fsq,
                                    double *res_uw = nullptr);
+static bool launch_half_sweep_bandv(const Lvl &L, double *u, const double *f, int color,
+                                    double rho, int zero_start, int nbr_zero, double post_scale,
+                                    cudaStream_t st, int mode, double *partials, int *np,
+                                    double *res_uw);
 
 cudaError_t launch_half_sweep_dot(const Lvl &L, double *u, const double *f, int color, double rho,
                                   int zero_start, int nbr_zero, double post_scale,
@@ -2588,7 +2866,9 @@ cudaError_t launch_half_sweep_res(const Lvl &L, const double *u, double *uw, con
                                   double *partials, int *np, cudaStream_t st) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     if (!L.uniform) {
-        launch_segv_mode<1>(L, const_cast<double *>(u), uw, f, 0, 0, partials, np, st);
+        if (!launch_half_sweep_bandv(L, const_cast<double *>(u), f, 0, 1.0, 0, 0, 1.0, st, 1,
+                                     partials, np, uw))
+            launch_segv_mode<1>(L, const_cast<double *>(u), uw, f, 0, 0, partials, np, st);
         return cudaGetLastError();
     }
     // the TMA band kernel (16 compute warps) where the level's half-sweeps
@@ -2626,7 +2906,9 @@ cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int 
     g_launches.fetch_add(1, std::memory_order_relaxed);
     f += (long long)color * (L.fcs - L.cstride);   // see launch_half_sweep
     if (!L.uniform) {
-        launch_segv_mode<3>(L, u, nullptr, f, color, nbr_zero, partials, np, st);
+        if (!launch_half_sweep_bandv(L, u, f, color, 1.0, 0, nbr_zero, 1.0, st, 3, partials, np,
+                                     nullptr))
+            launch_segv_mode<3>(L, u, nullptr, f, color, nbr_zero, partials, np, st);
         return cudaGetLastError();
     }
     if (launch_half_sweep_band(L, u, f, color, 1.0, 0, nbr_zero, 1.0, st, partials, np, true))
@@ -2670,7 +2952,20 @@ static void band_attrs_nw() {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 template <int P>
+static void bandv_attrs() {
+    const int sm = (int)bandv_smem();
+    cudaFuncSetAttribute(k_half_sweep_bandv<P, 0, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_bandv<P, 0, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_bandv<P, 1, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_bandv<P, 3, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+}
+template <int P>
 static void band_attrs() {
+    bandv_attrs<P>();
     band_attrs_nw<P, 8>();
     band_attrs_nw<P, 16>();
     cudaFuncSetAttribute(k_half_sweep_band<P, false, false, true, 16, true>,
@@ -2683,6 +2978,7 @@ void setup_kernel_attributes() {
     static bool done = false;
     if (done) return;
     done = true;
+    bandv_attrs<2056>();
     band_attrs<1032>();
     band_attrs<520>();
     band_attrs<264>();
@@ -2722,6 +3018,13 @@ static bool make_tmap(CUtensorMap *m, const double *base, const Lvl &L, int boxw
 
 // k_half_sweep_band: configs[1]'s fine level shape (nz = 128, plane 520),
 // neighbours read, no fused halo
+// k_half_sweep_bandv: the same rings, tables tdrw tvp(+2) tvol tdr, the four
+// [16][32] segment arrays, barriers and warp sums
+static size_t bandv_smem() {
+    return sizeof(double) * (4 * BAND_NZ * BAND_W + 2 * BAND_NZ * 32 + 4 * BAND_NZ * 2 +
+                             4 * BAND_NZ + 2 + 4 * 16 * 32 + 16) + 12 * 8 + 128;
+}
+
 static size_t band_smem() {   // sized for up to 16 compute warps
     // rings (4 other-colour rows, 2 f rows, 4 edge pairs), tables ti tb tw
     // tr1 tr2 (double2) and tq, hend / ybeg, barriers, warp sums
@@ -2816,6 +3119,69 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
     return true;
 }
 
+// k_half_sweep_bandv (variable coefficients, nz = 128): mode 0 plain, 1 the
+// fused residual into uw, 3 with the f^2 partial sums; false if the level
+// does not fit it (then k_half_sweep_segv runs)
+static bool launch_half_sweep_bandv(const Lvl &L, double *u, const double *f, int color,
+                                    double rho, int zero_start, int nbr_zero, double post_scale,
+                                    cudaStream_t st, int mode, double *partials, int *np,
+                                    double *res_uw) {
+    const int hrow = L.nx / 2;
+    if (g_smoother_exact || L.uniform || !L.invd || L.nz != BAND_NZ ||
+        !(L.plane == 2056 || L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
+          L.plane == 136) || nbr_zero ||
+        L.nx % 2 || hrow % 32 || hrow < 64 || L.ny < 8 || L.rys != 1 || L.rxn < 1 || L.ryn < 1)
+        return false;
+    const int o = color ^ 1;
+    CUtensorMap mF, mB, mE;
+    if (!make_tmap(&mF, f + (long long)color * L.cstride, L, 32, BAND_NZ) ||
+        !make_tmap(&mB, u + (long long)o * L.cstride, L, BAND_W, BAND_NZ) ||
+        !make_tmap(&mE, u + (long long)o * L.cstride, L, 2, BAND_NZ))
+        return false;
+    const int nstrip = L.rxn, nrows = L.ryn;
+    int gcd = nstrip, bsm = sm_count();
+    while (bsm) {
+        const int t = gcd % bsm;
+        gcd = bsm;
+        bsm = t;
+    }
+    const int ups = nstrip / gcd;
+    int nband = (ups * sm_count() + nstrip - 1) / nstrip;
+    if (nband > nrows) nband = nrows;
+    const int band_rows = (nrows + nband - 1) / nband;
+    nband = (nrows + band_rows - 1) / band_rows;
+    const int nunits = nstrip * nband;
+    const int grid = nunits < sm_count() ? nunits : sm_count();
+    if (np) *np = grid;
+    const bool lean = rho == 1.0 && !zero_start;
+#define PMG_BANDV(P)                                                                         \
+    do {                                                                                     \
+        if (mode == 1)                                                                       \
+            k_half_sweep_bandv<P, 1, true><<<grid, 512, bandv_smem(), st>>>(                  \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
+                mE, partials, res_uw);                                                       \
+        else if (mode == 3)                                                                  \
+            k_half_sweep_bandv<P, 3, true><<<grid, 512, bandv_smem(), st>>>(                  \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
+                mE, partials, nullptr);                                                      \
+        else if (lean)                                                                       \
+            k_half_sweep_bandv<P, 0, true><<<grid, 512, bandv_smem(), st>>>(                  \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
+                mE, nullptr, nullptr);                                                       \
+        else                                                                                 \
+            k_half_sweep_bandv<P, 0, false><<<grid, 512, bandv_smem(), st>>>(                 \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
+                mE, nullptr, nullptr);                                                       \
+    } while (0)
+    if (L.plane == 2056) PMG_BANDV(2056);   // configs[4]'s 4096^2 fine level
+    else if (L.plane == 1032) PMG_BANDV(1032);
+    else if (L.plane == 520) PMG_BANDV(520);
+    else if (L.plane == 264) PMG_BANDV(264);
+    else PMG_BANDV(136);
+#undef PMG_BANDV
+    return true;
+}
+
 static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f, int color,
                                        double rho, int zero_start, int nbr_zero,
                                        double post_scale, cudaStream_t st) {
@@ -2825,6 +3191,9 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
     }
     const int hx = ((L.nx + 1) / 2 + 31) / 32;
     const dim3 g(hx, L.ny);
+    if (launch_half_sweep_bandv(L, u, f, color, rho, zero_start, nbr_zero, post_scale, st, 0,
+                                nullptr, nullptr, nullptr))
+        return cudaGetLastError();
     if (!g_smoother_exact && !L.uniform && L.nz <= 256) {
         // variable coefficients: 16 warps, SEG = nz / 16 (must divide)
         int seg = 0;
