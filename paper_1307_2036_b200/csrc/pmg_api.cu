@@ -97,6 +97,8 @@ pmg_level *level_view(const pmg_level *lv, long long cstride, int hflags_or) {
     return v;
 }
 int level_hflags(const pmg_level *lv) { return lv->L.hflags; }
+// the kernel-side view of a level (multi-part exchange kernels, pmg_parts.cu)
+const Lvl &level_lvl(const pmg_level *lv) { return lv->L; }
 void level_view_free(pmg_level *v) { delete v; }
 }
 

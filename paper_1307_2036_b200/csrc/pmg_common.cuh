@@ -73,4 +73,17 @@ __host__ __device__ __forceinline__ long long cell(const Lvl &L, int i, int j, i
 }
 
 
+// cell (i, j) of position t along face `face` (0 W, 1 E: t = j; 2 S, 3 N:
+// t = i + 1 over the extended range -1 .. nx), on the halo ring or the
+// adjacent owned row / column (partition.py:158-191)
+__host__ __device__ __forceinline__ void face_pos(const Lvl &L, int face, int t, bool halo, int &i, int &j) {
+    if (face < 2) {
+        j = t;
+        i = (face == 0) ? (halo ? -1 : 0) : (halo ? L.nx : L.nx - 1);
+    } else {
+        i = t - 1;
+        j = (face == 2) ? (halo ? -1 : 0) : (halo ? L.ny : L.ny - 1);
+    }
+}
+
 }  // namespace pmg

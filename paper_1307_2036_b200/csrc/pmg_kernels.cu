@@ -1146,7 +1146,7 @@ k_half_sweep_seg(Lvl L, double *__restrict__ u, const double *__restrict__ f, in
     // RES: (1 / iota, diag) and zero-padded vertical couplings (bm, bp) as in k_norm_v
     double2 *tr1 = reinterpret_cast<double2 *>(ybeg0 + 2 * 16 * 32);   // [nz]
     double2 *tr2 = tr1 + nz;                                          // [nz]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int t = threadIdx.x; t < nz; t += blockDim.x) {
         const double io = L.invd1[t], dd = io * L.drw[t];
         tw[t] = make_double2(dd * L.wx0, dd * L.wy0);
@@ -2238,15 +2238,6 @@ __global__ void k_halo_self(Lvl L, double *__restrict__ d, int px, int py) {
     d[cell(L, i, j, k)] = d[cell(L, hmap(i, L.nx, px), hmap(j, L.ny, py), k)];
 }
 
-__device__ __forceinline__ void face_pos(const Lvl &L, int face, int t, bool halo, int &i, int &j) {
-    if (face < 2) {
-        j = t;
-        i = (face == 0) ? (halo ? -1 : 0) : (halo ? L.nx : L.nx - 1);
-    } else {
-        i = t - 1;
-        j = (face == 2) ? (halo ? -1 : 0) : (halo ? L.ny : L.ny - 1);
-    }
-}
 
 __global__ void k_pack_face(Lvl L, const double *__restrict__ d, int face, double *__restrict__ buf,
                             int len) {

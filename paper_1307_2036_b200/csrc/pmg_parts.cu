@@ -35,12 +35,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>   // types and prototypes only; symbols come from dlsym
 
-#include "../../include/pmg.h"
+#include "pmg_common.cuh"
 
 namespace pmg {
 extern std::atomic<long long> g_launches;
 extern int g_mode_gen;
 int set_error(int code, const char *msg);
+const Lvl &level_lvl(const pmg_level *lv);
 }
 
 namespace {
@@ -117,6 +118,87 @@ __global__ void k_sum_ordered(const double *__restrict__ v, int n, double *__res
 }
 
 constexpr int OPP[4] = {1, 0, 3, 2};
+
+// ---- exchange kernels: one launch per phase for both faces of every part
+constexpr int MAXP = 16;   // in-process parts per hierarchy
+
+// in-process: halo face of part p <- owned boundary strip of its neighbour
+// part (the opposite face, same position) or its own mirror; blockIdx.z =
+// 2 p + face of the phase.  Reads only owned cells (phase 0) or the rows
+// that phase 0 completed (phase 1: the y strips' corner cells), writes only
+// halo cells of this phase's faces: race-free within the launch.
+struct LocalX {
+    int np, phase, len;
+    pmg::Lvl L[MAXP];
+    double *u[MAXP];
+    int nbr[MAXP][4];   // local part index, -1 mirror
+};
+
+__global__ void k_halo_local(const __grid_constant__ LocalX x) {
+    const int p = blockIdx.z >> 1, face = 2 * x.phase + (blockIdx.z & 1);
+    const pmg::Lvl &L = x.L[p];
+    const int len = face < 2 ? L.ny : L.nx + 2;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+    if (t >= len) return;
+    int i, j, si, sj;
+    pmg::face_pos(L, face, t, true, i, j);
+    const int q = x.nbr[p][face];
+    double v;
+    if (q < 0) {
+        pmg::face_pos(L, face, t, false, si, sj);
+        v = x.u[p][pmg::cell(L, si, sj, k)];
+    } else {
+        const pmg::Lvl &Q = x.L[q];
+        pmg::face_pos(Q, face ^ 1, t, false, si, sj);   // the opposite face
+        v = x.u[q][pmg::cell(Q, si, sj, k)];
+    }
+    x.u[p][pmg::cell(L, i, j, k)] = v;
+}
+
+// one part's two faces of a phase into / out of its message buffers
+// (layout of pmg_pack_face: buf[k * len + t]); blockIdx.z = face of the phase
+struct FaceX {
+    pmg::Lvl L;
+    double *u;
+    double *buf[2];
+    int use[2];     // pack: face has a neighbour; unpack: 1 buffer, 2 mirror, 0 skip
+    int phase;
+};
+
+__global__ void k_pack_phase(const __grid_constant__ FaceX x) {
+    const int fs = blockIdx.z, face = 2 * x.phase + fs;
+    if (!x.use[fs]) return;
+    const int len = face < 2 ? x.L.ny : x.L.nx + 2;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+    if (t >= len) return;
+    int i, j;
+    pmg::face_pos(x.L, face, t, false, i, j);
+    x.buf[fs][(long long)k * len + t] = x.u[pmg::cell(x.L, i, j, k)];
+}
+
+__global__ void k_unpack_phase(const __grid_constant__ FaceX x) {
+    const int fs = blockIdx.z, face = 2 * x.phase + fs;
+    if (!x.use[fs]) return;
+    const int len = face < 2 ? x.L.ny : x.L.nx + 2;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+    if (t >= len) return;
+    int i, j;
+    pmg::face_pos(x.L, face, t, true, i, j);
+    double v;
+    if (x.use[fs] == 2) {
+        int si, sj;
+        pmg::face_pos(x.L, face, t, false, si, sj);
+        v = x.u[pmg::cell(x.L, si, sj, k)];
+    } else {
+        v = x.buf[fs][(long long)k * len + t];
+    }
+    x.u[pmg::cell(x.L, i, j, k)] = v;
+}
+
+dim3 face_grid(const pmg::Lvl &L, int nz, int z) {
+    const int len = (L.nx + 2 > L.ny) ? L.nx + 2 : L.ny;
+    return dim3((unsigned)((len + 127) / 128), (unsigned)nz, (unsigned)z);
+}
 
 }  // namespace
 
@@ -203,56 +285,67 @@ void sync_mode(pmg_phier *h) {
 
 // halo exchange of level c's fields x[p] (partition.py:158-191): x faces,
 // then y faces over the extended range (corners), periodic neighbours or
-// mirrored physical boundaries, on stream s
+// mirrored physical boundaries, on stream s.  Per phase: in-process, one
+// launch for every part's two faces; with a communicator, one pack launch,
+// one NCCL group, one unpack launch.
 int exchange(pmg_phier *h, int c, double *const *x, cudaStream_t s) {
     ++h->exchanges;
+    const PL &q0 = h->P[0][c];
     for (int phase = 0; phase < 2; ++phase) {
-        const int fa = 2 * phase, fb = fa + 1;
-        for (int p = 0; p < h->np; ++p)
-            for (int face : {fa, fb})
-                if (h->nbr[p][face] >= 0)
-                    TRY(pmg_pack_face(h->P[p][c].lv, x[p], face, h->P[p][c].sb[face], s));
-        if (h->comm) {
-            const Nccl *n = nccl();
-            TRYN(n->group_start(), "ncclGroupStart");
+        const int fa = 2 * phase;
+        if (!h->comm) {
+            LocalX lx;
+            lx.np = h->np;
+            lx.phase = phase;
+            lx.len = 0;
             for (int p = 0; p < h->np; ++p) {
-                int ops[12], nops = 0;
-                TRY(pmg_exchange_plan(h->nbr[p].data(), phase, ops, &nops));
-                const PL &q = h->P[p][c];
-                for (int o = 0; o < nops; ++o) {
-                    const int kind = ops[3 * o], face = ops[3 * o + 1], peer = ops[3 * o + 2];
-                    ncclResult_t r = kind == 0
-                        ? n->send(q.sb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s)
-                        : n->recv(q.rb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s);
-                    if (r != ncclSuccess) {
-                        n->group_end();
-                        return nccl_err(r, kind == 0 ? "ncclSend" : "ncclRecv");
-                    }
+                lx.L[p] = pmg::level_lvl(h->P[p][c].lv);
+                lx.u[p] = x[p];
+                for (int a = 0; a < 4; ++a) {
+                    const int nb = h->nbr[p][a];
+                    lx.nbr[p][a] = nb < 0 ? -1 : h->local[nb];
                 }
             }
-            TRYN(n->group_end(), "ncclGroupEnd");
-            for (int p = 0; p < h->np; ++p)
-                for (int face : {fa, fb}) {
-                    const PL &q = h->P[p][c];
-                    if (h->nbr[p][face] >= 0)
-                        TRY(pmg_unpack_face(q.lv, x[p], face, q.rb[face], 0, s));
-                    else
-                        TRY(pmg_unpack_face(q.lv, x[p], face, nullptr, 1, s));
-                }
-        } else {
-            // all parts local: the neighbour's packed strip is the halo
-            for (int p = 0; p < h->np; ++p)
-                for (int face : {fa, fb}) {
-                    const int nb = h->nbr[p][face];
-                    if (nb < 0) {
-                        TRY(pmg_unpack_face(h->P[p][c].lv, x[p], face, nullptr, 1, s));
-                    } else {
-                        const int q = h->local[nb];
-                        TRY(pmg_unpack_face(h->P[p][c].lv, x[p], face, h->P[q][c].sb[OPP[face]], 0,
-                                            s));
-                    }
-                }
+            k_halo_local<<<face_grid(lx.L[0], q0.nz, 2 * h->np), 128, 0, s>>>(lx);
+            pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
+            TRYC(cudaGetLastError(), "halo exchange");
+            continue;
         }
+        // one part (this rank's)
+        const PL &q = h->P[0][c];
+        FaceX fx;
+        fx.L = pmg::level_lvl(q.lv);
+        fx.u = x[0];
+        fx.phase = phase;
+        for (int fs = 0; fs < 2; ++fs) {
+            fx.buf[fs] = q.sb[fa + fs];
+            fx.use[fs] = h->nbr[0][fa + fs] >= 0;
+        }
+        k_pack_phase<<<face_grid(fx.L, q.nz, 2), 128, 0, s>>>(fx);
+        pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
+        TRYC(cudaGetLastError(), "pack");
+        const Nccl *n = nccl();
+        TRYN(n->group_start(), "ncclGroupStart");
+        int ops[12], nops = 0;
+        TRY(pmg_exchange_plan(h->nbr[0].data(), phase, ops, &nops));
+        for (int o = 0; o < nops; ++o) {
+            const int kind = ops[3 * o], face = ops[3 * o + 1], peer = ops[3 * o + 2];
+            ncclResult_t r = kind == 0
+                ? n->send(q.sb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s)
+                : n->recv(q.rb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s);
+            if (r != ncclSuccess) {
+                n->group_end();
+                return nccl_err(r, kind == 0 ? "ncclSend" : "ncclRecv");
+            }
+        }
+        TRYN(n->group_end(), "ncclGroupEnd");
+        for (int fs = 0; fs < 2; ++fs) {
+            fx.buf[fs] = q.rb[fa + fs];
+            fx.use[fs] = h->nbr[0][fa + fs] >= 0 ? 1 : 2;
+        }
+        k_unpack_phase<<<face_grid(fx.L, q.nz, 2), 128, 0, s>>>(fx);
+        pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
+        TRYC(cudaGetLastError(), "unpack");
     }
     return PMG_OK;
 }
@@ -546,6 +639,8 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
         return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
     if (comm && (nparts != 1 || parts[0].worker != comm->rank))
         return err(PMG_ERR_VALUE, "with a communicator each rank holds one part: its rank");
+    if (nparts > MAXP)
+        return err(PMG_ERR_VALUE, "at most 16 in-process parts per hierarchy");
     int maxw = -1;
     for (int p = 0; p < nparts; ++p) {
         if (parts[p].worker < 0 || (p && parts[p].worker <= parts[p - 1].worker))
@@ -614,9 +709,9 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
             }
             for (int a = 0; a < 4 && e == cudaSuccess; ++a) {
                 q.fd[a] = pmg_face_doubles(q.lv, a);
-                if (h->nbr[p][a] < 0) continue;
+                if (h->nbr[p][a] < 0 || !comm) continue;
                 e = cudaMalloc(&q.sb[a], sizeof(double) * q.fd[a]);
-                if (e == cudaSuccess && comm) e = cudaMalloc(&q.rb[a], sizeof(double) * q.fd[a]);
+                if (e == cudaSuccess) e = cudaMalloc(&q.rb[a], sizeof(double) * q.fd[a]);
             }
         }
     }

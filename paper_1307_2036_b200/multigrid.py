@@ -219,7 +219,7 @@ class NativeHierarchy:
 
 
 #: narrowest part (columns) that relaxes boundary-first in a multi-part solve
-OVERLAP_NX = 256
+OVERLAP_NX = 1024
 
 
 class NativePartsHierarchy:
