@@ -42,6 +42,11 @@ extern std::atomic<long long> g_launches;
 extern int g_mode_gen;
 int set_error(int code, const char *msg);
 const Lvl &level_lvl(const pmg_level *lv);
+pmg_level *level_view(const pmg_level *lv, long long cstride, int hflags_or = 0);
+void level_view_free(pmg_level *v);
+int half_sweep_fsq(const pmg_level *lv, double *u, const double *f, int color, int nbr_zero,
+                   double *partials, int *np, void *st);
+int finalize(const double *partials, int n, double *out, void *st);
 }
 
 namespace {
@@ -248,6 +253,12 @@ struct pmg_phier {
     long long replayed = 0;
     long long exchanges = 0;                  // halo exchanges issued (per level, counted once)
     int mode_gen = 0;
+    // lagged norm (pmg_driver.cu's identities per part): each part's second
+    // red array, the level-0 view the cycle being issued works through (its
+    // red array elsewhere), and the previous solve's cycle count
+    std::vector<double *> red1;
+    std::vector<const pmg_level *> fine_view;
+    int last_iters = 4;
 };
 
 namespace {
@@ -267,6 +278,7 @@ void free_phier(pmg_phier *h) {
             }
         }
     for (auto *s : h->scr) cudaFree(s);
+    for (auto *r : h->red1) cudaFree(r);
     cudaFree(h->slots);
     if (h->res_h) cudaFreeHost(h->res_h);
     if (h->side) cudaStreamDestroy(h->side);
@@ -281,6 +293,13 @@ void sync_mode(pmg_phier *h) {
     for (auto &g : h->graphs) cudaGraphExecDestroy(g.exec);
     h->graphs.clear();
     h->mode_gen = pmg::g_mode_gen;
+}
+
+// level c of part p as the cycle being issued sees it: the lagged norm's
+// level-0 view (red array in the other allocation) while one is set
+const pmg_level *LV(const pmg_phier *h, int p, int c) {
+    if (c == 0 && !h->fine_view.empty() && h->fine_view[p]) return h->fine_view[p];
+    return h->P[p][c].lv;
 }
 
 // halo exchange of level c's fields x[p] (partition.py:158-191): x faces,
@@ -299,7 +318,7 @@ int exchange(pmg_phier *h, int c, double *const *x, cudaStream_t s) {
             lx.phase = phase;
             lx.len = 0;
             for (int p = 0; p < h->np; ++p) {
-                lx.L[p] = pmg::level_lvl(h->P[p][c].lv);
+                lx.L[p] = pmg::level_lvl(LV(h, p, c));
                 lx.u[p] = x[p];
                 for (int a = 0; a < 4; ++a) {
                     const int nb = h->nbr[p][a];
@@ -314,7 +333,7 @@ int exchange(pmg_phier *h, int c, double *const *x, cudaStream_t s) {
         // one part (this rank's)
         const PL &q = h->P[0][c];
         FaceX fx;
-        fx.L = pmg::level_lvl(q.lv);
+        fx.L = pmg::level_lvl(LV(h, 0, c));
         fx.u = x[0];
         fx.phase = phase;
         for (int fs = 0; fs < 2; ++fs) {
@@ -363,14 +382,15 @@ std::vector<const double *> level_f(pmg_phier *h, int c, const double *const *f0
 
 // sum of the per-part scalars slots[0 .. np) over every part of every rank,
 // in worker order, into out (device or host-mapped)
-int global_sum(pmg_phier *h, double *out, cudaStream_t s) {
+int global_sum(pmg_phier *h, double *out, cudaStream_t s, const double *vals = nullptr) {
+    if (!vals) vals = h->slots;
     if (h->comm) {
         // one part per rank: gather the rank sums, add them in rank order
-        double *gath = h->slots + h->np;
-        TRYN(nccl()->all_gather(h->slots, gath, 1, ncclDouble, h->comm->c, s), "ncclAllGather");
+        double *gath = h->slots + 2 * h->np;
+        TRYN(nccl()->all_gather(vals, gath, 1, ncclDouble, h->comm->c, s), "ncclAllGather");
         k_sum_ordered<<<1, 1, 0, s>>>(gath, h->comm->nranks, out);
     } else {
-        k_sum_ordered<<<1, 1, 0, s>>>(h->slots, h->np, out);
+        k_sum_ordered<<<1, 1, 0, s>>>(vals, h->np, out);
     }
     pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
     TRYC(cudaGetLastError(), "ordered sum");
@@ -383,7 +403,8 @@ bool overlapped(const pmg_phier *h, int c) {
     if (!h->overlap_nx) return false;
     for (int p = 0; p < h->np; ++p) {
         const PL &q = h->P[p][c];
-        if (q.nx < h->overlap_nx || q.nx < 256 || q.ny < 16 || !pmg_half_sweep_region_ok(q.lv))
+        if (q.nx < h->overlap_nx || q.nx < 256 || q.ny < 16 ||
+            !pmg_half_sweep_region_ok(LV(h, p, c)))
             return false;
     }
     return true;
@@ -396,7 +417,7 @@ int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, 
     const double rho = h->d.rho;
     if (!overlapped(h, c)) {
         for (int p = 0; p < h->np; ++p)
-            TRY(pmg_half_sweep(h->P[p][c].lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, s));
+            TRY(pmg_half_sweep(LV(h, p, c), u[p], f[p], color, rho, 0, nbr_zero, 1.0, s));
         return exchange(h, c, u, s);
     }
     // frame: rows 0 and ny - 1 (all strips), the first and last strip of
@@ -406,11 +427,11 @@ int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, 
     for (int p = 0; p < h->np; ++p) {
         const PL &q = h->P[p][c];
         const int ns = ((q.nx + 1) / 2 + 31) / 32;
-        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns, 0, 1,
+        TRY(pmg_half_sweep_region(LV(h, p, c), u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns, 0, 1,
                                   1, s));
-        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns,
+        TRY(pmg_half_sweep_region(LV(h, p, c), u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, 1, ns,
                                   q.ny - 1, 1, 1, s));
-        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, ns - 1, 2,
+        TRY(pmg_half_sweep_region(LV(h, p, c), u[p], f[p], color, rho, 0, nbr_zero, 1.0, 0, ns - 1, 2,
                                   1, 1, q.ny - 2, s));
     }
     TRYC(cudaEventRecord(h->ev_fork, s), "fork");
@@ -419,7 +440,7 @@ int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, 
     for (int p = 0; p < h->np; ++p) {
         const PL &q = h->P[p][c];
         const int ns = ((q.nx + 1) / 2 + 31) / 32;
-        TRY(pmg_half_sweep_region(q.lv, u[p], f[p], color, rho, 0, nbr_zero, 1.0, 1, 1, ns - 2,
+        TRY(pmg_half_sweep_region(LV(h, p, c), u[p], f[p], color, rho, 0, nbr_zero, 1.0, 1, 1, ns - 2,
                                   1, 1, q.ny - 2, s));
     }
     TRYC(cudaEventRecord(h->ev_join, h->side), "join");
@@ -427,27 +448,66 @@ int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, 
     return PMG_OK;
 }
 
+// fine-level state of a lagged-norm cycle (pmg_driver.cu's Fine): the first
+// red half-sweep already ran (the previous cycle's fused-residual sweep), or
+// the first two half-sweeps sum f^2 (the first cycle's ||f||)
+struct Fine {
+    bool red_done = false;
+    bool fsq = false;
+};
+
+// first cycle: red and black half-sweeps with per-part f^2 partials (part
+// p's at scr[0] + p * 1024), ||f||^2 over all parts into res_d[1]
+int fsq_sweeps(pmg_phier *h, double *const *u, const double *const *f, bool from_zero,
+               cudaStream_t s) {
+    double *fs = h->slots + h->np;
+    int n1[MAXP];
+    for (int p = 0; p < h->np; ++p)
+        TRY(pmg::half_sweep_fsq(LV(h, p, 0), u[p], f[p], 0, from_zero ? 1 : 0,
+                                h->scr[0] + p * 1024, &n1[p], s));
+    TRY(exchange(h, 0, u, s));
+    for (int p = 0; p < h->np; ++p) {
+        int n2 = 0;
+        TRY(pmg::half_sweep_fsq(LV(h, p, 0), u[p], f[p], 1, 0, h->scr[0] + p * 1024 + n1[p], &n2,
+                                s));
+        TRY(pmg::finalize(h->scr[0] + p * 1024, n1[p] + n2, fs + p, s));
+    }
+    TRY(exchange(h, 0, u, s));
+    return global_sum(h, h->res_d + 1, s, fs);
+}
+
 int sweeps(pmg_phier *h, int c, double *const *u, const double *const *f, int n, bool from_zero,
-           cudaStream_t s) {
+           cudaStream_t s, const Fine *fv = nullptr) {
+    const bool red_done = fv && fv->red_done;
+    if (fv && fv->fsq && n >= 1 && !red_done) {
+        TRY(fsq_sweeps(h, u, f, from_zero, s));
+        from_zero = false;
+        n -= 1;
+    }
     for (int k = 0; k < n; ++k) {
-        TRY(half_sweep_x(h, c, u, f, 0, (from_zero && k == 0) ? 1 : 0, s));
+        if (red_done && k == 0)
+            TRY(exchange(h, c, u, s));   // the red values the fused sweep wrote
+        else
+            TRY(half_sweep_x(h, c, u, f, 0, (from_zero && k == 0) ? 1 : 0, s));
         TRY(half_sweep_x(h, c, u, f, 1, 0, s));
     }
     return PMG_OK;
 }
 
 // Alg. 1 (multigrid.py:271-294): the operation sequence of the Python
-// v_cycle's fused path for every part, level by level
+// v_cycle's fused path for every part, level by level (level 0 through
+// LV's view under the lagged norm)
 int vcycle(pmg_phier *h, int c, double *const *u0, const double *const *f0, bool first,
-           cudaStream_t s) {
+           cudaStream_t s, const Fine *fv = nullptr) {
     const int L = h->nlev;
     const auto u = level_u(h, c, u0);
     const auto f = level_f(h, c, f0);
     const bool lean = h->d.rho == 1.0;
     if (c + 1 < L) {
-        TRY(sweeps(h, c, u.data(), f.data(), h->d.nu_pre, lean && (c > 0 || first), s));
+        TRY(sweeps(h, c, u.data(), f.data(), h->d.nu_pre, lean && (c > 0 || first), s,
+                   c == 0 ? fv : nullptr));
         for (int p = 0; p < h->np; ++p) {
-            const pmg_level *lf = h->P[p][c].lv, *lc = h->P[p][c + 1].lv;
+            const pmg_level *lf = LV(h, p, c), *lc = h->P[p][c + 1].lv;
             if (h->d.red_restrict && lean && h->d.nu_pre >= 1 && pmg_residual_restrict_red_ok(lf))
                 TRY(pmg_residual_restrict_red(lf, lc, f[p], u[p], h->P[p][c + 1].f, s));
             else
@@ -460,7 +520,7 @@ int vcycle(pmg_phier *h, int c, double *const *u0, const double *const *f0, bool
         TRY(vcycle(h, c + 1, u0, f0, false, s));
         const int pmask = (lean && h->d.nu_post >= 1) ? 2 : 3;
         for (int p = 0; p < h->np; ++p)
-            TRY(pmg_prolong_colors(h->P[p][c].lv, h->P[p][c + 1].lv, h->P[p][c + 1].u, u[p], 1,
+            TRY(pmg_prolong_colors(LV(h, p, c), h->P[p][c + 1].lv, h->P[p][c + 1].u, u[p], 1,
                                    pmask, s));
         TRY(exchange(h, c, u.data(), s));
         TRY(sweeps(h, c, u.data(), f.data(), h->d.nu_post, false, s));
@@ -477,7 +537,9 @@ int norm2(pmg_phier *h, double *const *u, const double *const *f, double *out, c
     return global_sum(h, out, s);
 }
 
-int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cudaStream_t s) {
+template <class Body>
+int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cudaStream_t s,
+           Body body) {
     for (auto &g : h->graphs) {
         bool same = g.kind == kind && g.st == s;
         for (int p = 0; same && p < h->np; ++p) same = g.f[p] == f[p] && g.u[p] == u[p];
@@ -494,8 +556,7 @@ int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cud
     cudaGraph_t graph;
     const long long l0 = pmg_launch_count();
     TRYC(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
-    int rc = vcycle(h, 0, u, f, kind == 1, s);
-    if (!rc) rc = norm2(h, u, f, h->res_d, s);
+    int rc = body();
     cudaError_t e = cudaStreamEndCapture(s, &graph);
     if (rc) {
         if (e == cudaSuccess) cudaGraphDestroy(graph);
@@ -513,11 +574,123 @@ int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cud
     return PMG_OK;
 }
 
+// the single-part driver's lagged-norm conditions (pmg_driver.cu lagged_ok)
+// for every part
+bool lagged_ok(const pmg_phier *h) {
+    if (!h->d.lagged_norm || h->d.rho != 1.0 || h->d.nu_pre < 1 || h->d.nu_post < 1 ||
+        h->nlev < 2)
+        return false;
+    for (int p = 0; p < h->np; ++p) {
+        const pmg_level *l0 = h->P[p][0].lv;
+        int pitch, par, uni;
+        long long plane, cs;
+        if (pmg_level_layout(l0, &pitch, &plane, &cs, &par, &uni)) return false;
+        if (!uni && !(h->d.red_restrict && pmg_residual_restrict_red_ok(l0))) return false;
+        if (h->P[p][0].nx % 4 || !pmg_half_sweep_res_ok(l0)) return false;
+    }
+    return true;
+}
+
+// mg_solve with the lagged norm (pmg_driver.cu mg_solve_lagged, per part):
+// cycle k's ||f - A u|| is summed by the first red half-sweep of cycle k + 1
+// (pmg_half_sweep_res), which writes the relaxed red values into the other
+// red array of each part; the first cycle's red and black half-sweeps sum
+// ||f||^2.  Kinds: 2 + X first cycle relaxing into red array X, 4 + X a
+// later cycle on X; each ends with the next cycle's fused sweep from X.
+int mg_solve_lagged(pmg_phier *h, const double *const *f, double *const *u, double eps,
+                    int maxiter, double *hist, int *iters, int *converged, cudaStream_t s) {
+    const int np = h->np;
+    long long cs = 0;
+    {
+        int pitch, par, uni;
+        long long plane;
+        TRY(pmg_level_layout(h->P[0][0].lv, &pitch, &plane, &cs, &par, &uni));
+    }
+    if (h->red1.empty()) {
+        h->red1.assign(np, nullptr);
+        for (int p = 0; p < np; ++p)
+            TRYC(cudaMalloc(&h->red1[p], sizeof(double) * cs), "red array");
+    }
+    // per part: view 1 = the level seen from red1 (black array at u + cs)
+    std::vector<pmg_level *> vb(np, nullptr);
+    struct Free {
+        std::vector<pmg_level *> &v;
+        pmg_phier *h;
+        ~Free() {
+            for (auto *x : v)
+                if (x) pmg::level_view_free(x);
+            h->fine_view.clear();
+        }
+    } guard{vb, h};
+    for (int p = 0; p < np; ++p) {
+        const long long csb =
+            (long long)(((intptr_t)(u[p] + cs) - (intptr_t)h->red1[p]) / (intptr_t)sizeof(double));
+        vb[p] = pmg::level_view(h->P[p][0].lv, csb, 0);
+    }
+    std::vector<double *> base[2] = {std::vector<double *>(u, u + np), h->red1};
+    auto body = [&](int kind) -> int {
+        const int x = kind & 1;
+        h->fine_view.assign(np, nullptr);
+        if (x)
+            for (int p = 0; p < np; ++p) h->fine_view[p] = vb[p];
+        Fine fv;
+        fv.red_done = kind >= 4;
+        fv.fsq = kind < 4;
+        int rc = vcycle(h, 0, base[x].data(), f, kind < 4, s, &fv);
+        // the next cycle's first red half-sweep into the other array, with
+        // ||f - A u||^2 of this cycle's result
+        for (int p = 0; !rc && p < np; ++p)
+            rc = pmg_half_sweep_res(LV(h, p, 0), base[x][p], base[x ^ 1][p], f[p],
+                                    h->scr[0] + p * 1024, h->slots + p, s);
+        if (!rc) rc = global_sum(h, h->res_d, s);
+        h->fine_view.clear();
+        return rc;
+    };
+    int x = (h->last_iters & 1) ? 0 : 1;   // want the last iterate in the caller's array
+    int kind = 2 + x;
+    *iters = 0;
+    *converged = 0;
+    double r0 = 0.0;
+    for (int it = 0; it < maxiter; ++it) {
+        // graphs are keyed on the caller's arrays (the views depend on them)
+        TRY(replay(h, u, f, kind, s, [&] { return body(kind); }));
+        TRYC(cudaStreamSynchronize(s), "sync");
+        if (it == 0) {
+            r0 = std::sqrt(h->res_h[1]);
+            hist[0] = r0;
+            if (r0 == 0.0) {   // multigrid.py:317-318
+                for (int p = 0; p < np; ++p) TRY(pmg_fill(h->P[p][0].lv, u[p], 0.0, s));
+                *converged = 1;
+                return PMG_OK;
+            }
+        }
+        const double rn = std::sqrt(h->res_h[0]);
+        hist[it + 1] = rn;
+        *iters = it + 1;
+        if (rn / r0 < eps) {
+            *converged = 1;
+            break;
+        }
+        if (it + 1 == maxiter) break;   // u_maxiter stays in red array x
+        x ^= 1;                          // the fused sweep relaxed red into the other array
+        kind = 4 + x;
+    }
+    h->last_iters = *iters;
+    if (x == 1)   // the result's red array is red1: copy it (halo included) into u
+        for (int p = 0; p < np; ++p)
+            TRYC(cudaMemcpyAsync(u[p], h->red1[p], sizeof(double) * cs, cudaMemcpyDeviceToDevice,
+                                 s),
+                 "red array copy");
+    return PMG_OK;
+}
+
 int mg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double eps, int maxiter,
                 double *hist, int *iters, int *converged, cudaStream_t s) {
     for (int p = 0; p < h->np; ++p)
         for (int c = 0; c < h->nlev; ++c)
             TRY(pmg_level_prepare(const_cast<pmg_level *>(h->P[p][c].lv), s));
+    if (maxiter >= 1 && lagged_ok(h))
+        return mg_solve_lagged(h, f, u, eps, maxiter, hist, iters, converged, s);
     // r0 = ||f|| (multigrid.py:307-309)
     for (int p = 0; p < h->np; ++p)
         TRY(pmg_dot(h->P[p][0].lv, f[p], f[p], h->scr[0], h->slots + p, s));
@@ -536,7 +709,11 @@ int mg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double e
     if (!lean_first)
         for (int p = 0; p < h->np; ++p) TRY(pmg_fill(h->P[p][0].lv, u[p], 0.0, s));
     for (int it = 0; it < maxiter; ++it) {
-        TRY(replay(h, u, f, (lean_first && it == 0) ? 1 : 0, s));
+        const int kind = (lean_first && it == 0) ? 1 : 0;
+        TRY(replay(h, u, f, kind, s, [&] {
+            TRY(vcycle(h, 0, u, f, kind == 1, s));
+            return norm2(h, u, f, h->res_d, s);
+        }));
         TRYC(cudaStreamSynchronize(s), "sync");
         const double rn = std::sqrt(h->res_h[0]);
         hist[it + 1] = rn;
@@ -719,7 +896,7 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
     if (!rc && e == cudaSuccess) e = cudaMalloc(&h->scr[0], sizeof(double) * ps);
     if (!rc && e == cudaSuccess) e = cudaMalloc(&h->scr[1], sizeof(double) * 1024);
     if (!rc && e == cudaSuccess)
-        e = cudaMalloc(&h->slots, sizeof(double) * (nparts + (comm ? comm->nranks : 0) + 8));
+        e = cudaMalloc(&h->slots, sizeof(double) * (2 * nparts + (comm ? comm->nranks : 0) + 8));
     if (!rc && e == cudaSuccess) e = cudaHostAlloc(&h->res_h, 8 * sizeof(double), cudaHostAllocMapped);
     if (!rc && e == cudaSuccess) e = cudaHostGetDevicePointer((void **)&h->res_d, h->res_h, 0);
     if (!rc && e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking);

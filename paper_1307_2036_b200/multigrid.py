@@ -166,7 +166,7 @@ class LevelHierarchy:
         runs over the library's own communicator."""
         from .partition import native_comm
         key = ("parts", cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), cfg.rho,
-               bool(cfg.red_restrict), bool(cfg.overlap))
+               bool(cfg.red_restrict), bool(cfg.overlap), bool(cfg.lagged_norm))
         h = self._native.get(key)
         if h is None:
             h = NativePartsHierarchy(self, cfg, native_comm() if _dist() is not None else None)
@@ -243,7 +243,7 @@ class NativePartsHierarchy:
                 parts[n].nbr[face] = -1 if nb is None else nb
         per = int(bool(lay.periodic))
         d = MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), float(cfg.rho), per,
-                   per, 0, int(bool(cfg.red_restrict)))
+                   per, int(bool(cfg.lagged_norm)), int(bool(cfg.red_restrict)))
         h = C.c_void_p()
         call("pmg_phier_create", arr, len(hier.levels), len(ws), parts, C.byref(d),
              comm, OVERLAP_NX if cfg.overlap else 0, C.byref(h))
