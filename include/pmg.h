@@ -372,6 +372,14 @@ int pmg_phier_destroy(pmg_phier *hier);
 /* mg_solve over every part: f[p], u[p] the parts' fields (multigrid.py:297-330) */
 int pmg_phier_mg_solve(pmg_phier *hier, const double *const *f, double *const *u, double eps,
                        int maxiter, double *hist, int *iters, int *converged, void *stream);
+/* preconditioned CG from u = 0 over every part (krylov.py:88-167): precond
+ * 1 = line SSOR(rho) with the halo exchanges of smoother.py:224-244, 0 =
+ * identity; dots added in worker order across parts and ranks; one host
+ * read per iteration.  Uses level 0 of the hierarchy (a one-level
+ * hierarchy is enough).  PMG_ERR_BREAKDOWN on <p, A p> <= 0 or <r, z> <= 0. */
+int pmg_phier_pcg_solve(pmg_phier *hier, const double *const *f, double *const *u, double eps,
+                        int maxiter, double tau, int precond, double rho, double *hist, int *iters,
+                        int *converged, void *stream);
 /* one V-cycle (u halos current; first = 1: u zero on entry, unfilled) */
 int pmg_phier_vcycle(pmg_phier *hier, double *const *u, const double *const *f, int first,
                      void *stream);

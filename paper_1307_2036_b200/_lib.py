@@ -124,6 +124,8 @@ SIGNATURES = {
     "pmg_phier_mg_solve": (_I, [_P, C.POINTER(_P), C.POINTER(_P), _D, _I, _P, C.POINTER(_I),
                                 C.POINTER(_I), _P]),
     "pmg_phier_vcycle": (_I, [_P, C.POINTER(_P), C.POINTER(_P), _I, _P]),
+    "pmg_phier_pcg_solve": (_I, [_P, C.POINTER(_P), C.POINTER(_P), _D, _I, _D, _I, _D, _P,
+                                 C.POINTER(_I), C.POINTER(_I), _P]),
     "pmg_phier_halo_exchange": (_I, [_P, _I, C.POINTER(_P), _P]),
     "pmg_phier_dot": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), _P, _P]),
     "pmg_phier_replayed_launches": (_LL, [_P]),

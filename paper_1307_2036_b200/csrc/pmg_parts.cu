@@ -259,6 +259,8 @@ struct pmg_phier {
     std::vector<double *> red1;
     std::vector<const pmg_level *> fine_view;
     int last_iters = 4;
+    // CG work fields per part (r, z, p, q), allocated on first use
+    std::vector<double *> cgw;
 };
 
 namespace {
@@ -279,6 +281,7 @@ void free_phier(pmg_phier *h) {
         }
     for (auto *s : h->scr) cudaFree(s);
     for (auto *r : h->red1) cudaFree(r);
+    for (auto *w : h->cgw) cudaFree(w);
     cudaFree(h->slots);
     if (h->res_h) cudaFreeHost(h->res_h);
     if (h->side) cudaStreamDestroy(h->side);
@@ -474,6 +477,16 @@ int fsq_sweeps(pmg_phier *h, double *const *u, const double *const *f, bool from
     }
     TRY(exchange(h, 0, u, s));
     return global_sum(h, h->res_d + 1, s, fs);
+}
+
+// a level-0 half-sweep with the SSOR flags (smoother.py:224-244) on every
+// part, then the halo exchange
+int half_sweep_y(pmg_phier *h, double *const *u, const double *const *f, int color, double rho,
+                 int zero_start, int nbr_zero, double post_scale, cudaStream_t s) {
+    for (int p = 0; p < h->np; ++p)
+        TRY(pmg_half_sweep(h->P[p][0].lv, u[p], f[p], color, rho, zero_start, nbr_zero,
+                           post_scale, s));
+    return exchange(h, 0, u, s);
 }
 
 int sweeps(pmg_phier *h, int c, double *const *u, const double *const *f, int n, bool from_zero,
@@ -726,6 +739,120 @@ int mg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double e
     return PMG_OK;
 }
 
+// Preconditioned CG over every part (krylov.py:88-167; the Python driver's
+// sequence -- pcg_solve without a callback -- issued by the library): per
+// iteration q = A p with <p, q>, the fused update r -= alpha q with
+// ||r||^2, one host read of (kappa, <p,q>, ||r||^2) for the breakdown checks
+// and the stopping test, z = M r by the line SSOR (red, black, red
+// half-sweeps, each followed by the halo exchange; smoother.py:224-244) or
+// the identity (copy + exchange), <r, z>, and p = z + beta p with the
+// deferred u += alpha p.  Dots are per-part sums added in worker order
+// across parts and ranks (global_sum).
+int pcg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double eps,
+                 int maxiter, double tau, int precond, double rho, double *hist, int *iters,
+                 int *converged, cudaStream_t s) {
+    const int np = h->np;
+    std::vector<long long> nd(np);
+    for (int p = 0; p < np; ++p) nd[p] = pmg_level_field_doubles(h->P[p][0].lv);
+    if (h->cgw.empty()) {
+        h->cgw.assign(4 * np, nullptr);
+        for (int p = 0; p < np; ++p)
+            for (int v = 0; v < 4; ++v)
+                TRYC(cudaMalloc(&h->cgw[4 * p + v], sizeof(double) * nd[p]), "CG work");
+    }
+    std::vector<double *> r(np), z(np), pp(np), q(np);
+    for (int p = 0; p < np; ++p) {
+        r[p] = h->cgw[4 * p];
+        z[p] = h->cgw[4 * p + 1];
+        pp[p] = h->cgw[4 * p + 2];
+        q[p] = h->cgw[4 * p + 3];
+    }
+    // device scalars kappa, <p,q>, ||r||^2, kappa_new (every thread of the
+    // update kernels reads them: device memory, after the per-part and the
+    // gathered rank sums in slots); copied to the host-mapped res for reads
+    double *kap = h->slots + 2 * np + (h->comm ? h->comm->nranks : 0);
+    double *pq = kap + 1, *rr = kap + 2, *kapn = kap + 3;
+    const double *kap_h = h->res_h + 2, *pq_h = h->res_h + 3, *rr_h = h->res_h + 4;
+    auto read3 = [&]() -> int {   // (kappa, <p,q>, ||r||^2) to the host
+        TRYC(cudaMemcpyAsync(h->res_d + 2, kap, 3 * sizeof(double), cudaMemcpyDeviceToDevice, s),
+             "scalar read");
+        TRYC(cudaStreamSynchronize(s), "sync");
+        return PMG_OK;
+    };
+    auto dots = [&](const std::vector<double *> &a, const std::vector<double *> &b,
+                    double *out) -> int {
+        for (int p = 0; p < np; ++p)
+            TRY(pmg_dot(h->P[p][0].lv, a[p], b[p], h->scr[0], h->slots + p, s));
+        return global_sum(h, out, s);
+    };
+    auto precondition = [&](double *rz) -> int {
+        if (precond) {
+            TRY(half_sweep_y(h, z.data(), r.data(), 0, rho, 1, 1, 1.0, s));
+            TRY(half_sweep_y(h, z.data(), r.data(), 1, rho, 1, 0, 2.0 - rho, s));
+            TRY(half_sweep_y(h, z.data(), r.data(), 0, rho, 0, 0, 1.0, s));
+        } else {
+            for (int p = 0; p < np; ++p) TRY(pmg_copy(h->P[p][0].lv, z[p], r[p], s));
+            TRY(exchange(h, 0, z.data(), s));
+        }
+        return dots(r, z, rz);
+    };
+    for (int p = 0; p < np; ++p) {
+        TRY(pmg_fill(h->P[p][0].lv, u[p], 0.0, s));
+        TRY(pmg_copy(h->P[p][0].lv, r[p], f[p], s));
+    }
+    TRY(dots(r, r, h->res_d));
+    TRYC(cudaStreamSynchronize(s), "sync");
+    const double r0 = std::sqrt(h->res_h[0]);
+    hist[0] = r0;
+    *iters = 0;
+    *converged = 0;
+    if (r0 == 0.0 || r0 < tau) {
+        *converged = 1;
+        return PMG_OK;
+    }
+    TRY(precondition(kap));
+    for (int p = 0; p < np; ++p) TRY(pmg_copy(h->P[p][0].lv, pp[p], z[p], s));
+    TRY(read3());
+    if (!(*kap_h > 0.0))
+        return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
+    bool pending = false;
+    for (int it = 1; it <= maxiter; ++it) {
+        for (int p = 0; p < np; ++p)
+            TRY(pmg_apply_dot(h->P[p][0].lv, pp[p], q[p], h->scr[0], h->slots + p, s));
+        TRY(global_sum(h, pq, s));
+        for (int p = 0; p < np; ++p)
+            TRY(pmg_cg_update(h->P[p][0].lv, kap, pq, pp[p], q[p], nullptr, r[p], h->scr[0],
+                              h->slots + p, s));
+        TRY(global_sum(h, rr, s));
+        pending = true;
+        TRY(read3());   // kappa, <p,q>, ||r||^2
+        if (!(*kap_h > 0.0))
+            return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
+        if (!(*pq_h > 0.0))
+            return err(PMG_ERR_BREAKDOWN, "<p, A p> <= 0: operator is not positive definite");
+        const double rn = std::sqrt(*rr_h);
+        hist[it] = rn;
+        *iters = it;
+        if (rn / r0 < eps || rn < tau) {
+            *converged = 1;
+            break;
+        }
+        TRY(precondition(kapn));
+        // u += (kappa / pq) p ; p = z + (kappa_new / kappa) p
+        for (int p = 0; p < np; ++p)
+            TRY(pmg_cg_step(nd[p], kap, pq, kapn, kap, z[p], pp[p], u[p], s));
+        pending = false;
+        TRYC(cudaMemcpyAsync(kap, kapn, sizeof(double), cudaMemcpyDeviceToDevice, s), "kappa");
+    }
+    if (pending)
+        for (int p = 0; p < np; ++p)
+            TRY(pmg_cg_step(nd[p], kap, pq, kap, kap, nullptr, pp[p], u[p], s));
+    TRY(read3());
+    if (!*converged && !(*kap_h > 0.0))
+        return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
+    return PMG_OK;
+}
+
 template <class Fn>
 int on_stream(pmg_phier *h, void *stream, Fn fn) {
     cudaStream_t st = (cudaStream_t)stream;
@@ -926,6 +1053,19 @@ int pmg_phier_mg_solve(pmg_phier *h, const double *const *f, double *const *u, d
     sync_mode(h);
     return on_stream(h, stream, [&](cudaStream_t s) {
         return mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, s);
+    });
+}
+
+int pmg_phier_pcg_solve(pmg_phier *h, const double *const *f, double *const *u, double eps,
+                        int maxiter, double tau, int precond, double rho, double *hist, int *iters,
+                        int *converged, void *stream) {
+    if (!h || !f || !u || !hist || !iters || !converged) return err(PMG_ERR_VALUE, "null argument");
+    if (!(eps > 0.0 && eps < 1.0)) return err(PMG_ERR_VALUE, "relative tolerance must lie in (0, 1)");
+    if (precond && !(rho > 0.0 && rho < 2.0))
+        return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
+    sync_mode(h);
+    return on_stream(h, stream, [&](cudaStream_t s) {
+        return pcg_solve_on(h, f, u, eps, maxiter, tau, precond, rho, hist, iters, converged, s);
     });
 }
 

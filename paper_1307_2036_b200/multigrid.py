@@ -229,10 +229,13 @@ class NativePartsHierarchy:
     reductions issued inside the captured cycle graph (include/pmg.h,
     multi-part drivers)."""
 
-    def __init__(self, hier: LevelHierarchy, cfg: "MGConfig", comm=None):
-        lay = hier.fine.layout
+    def __init__(self, hier: LevelHierarchy | None, cfg: "MGConfig", comm=None, ops=None):
+        # ``ops``: operators of the levels, finest first (default: the
+        # hierarchy's); a one-level list serves the CG driver
+        ops = [lev.op for lev in hier.levels] if ops is None else ops
+        lay = ops[0].layout
         ws = list(lay.local_workers)
-        self._levels = [[lev.op.handles[w] for lev in hier.levels] for w in ws]   # keep alive
+        self._levels = [[op.handles[w] for op in ops] for w in ws]   # keep alive
         flat = [h.h.value for hs in self._levels for h in hs]
         arr = (C.c_void_p * len(flat))(*flat)
         parts = (PartDesc * len(ws))()
@@ -245,7 +248,7 @@ class NativePartsHierarchy:
         d = MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), float(cfg.rho), per,
                    per, int(bool(cfg.lagged_norm)), int(bool(cfg.red_restrict)))
         h = C.c_void_p()
-        call("pmg_phier_create", arr, len(hier.levels), len(ws), parts, C.byref(d),
+        call("pmg_phier_create", arr, len(ops), len(ws), parts, C.byref(d),
              comm, OVERLAP_NX if cfg.overlap else 0, C.byref(h))
         self.h = h
         self.workers = ws

@@ -214,3 +214,47 @@ def test_native_parts_variable_coefficients(pmg, px, py):
     one, rep1, _ = solve(pmg, grid, params, fg, 1, 1, native=True, levels=5)
     assert rep1.iterations == rep.iterations
     assert np.max(np.abs(got - one)) <= 1e-10 * np.max(np.abs(one))
+
+
+def _cg(pmg, f, op, pre, native):
+    from paper_1307_2036_b200 import krylov
+    prev = krylov.USE_NATIVE_PARTS
+    krylov.USE_NATIVE_PARTS = native
+    try:
+        return pmg.pcg_solve(f, op, pre, eps=1e-8, maxiter=2000)
+    finally:
+        krylov.USE_NATIVE_PARTS = prev
+
+
+@pytest.mark.parametrize("precond", ["ssor", "identity"])
+@pytest.mark.parametrize("nx,ny,px,py,periodic", [(128, 128, 2, 2, True), (256, 128, 4, 2, True),
+                                                  (128, 128, 2, 2, False)])
+def test_native_parts_pcg(pmg, nx, ny, px, py, periodic, precond):
+    """The multi-part CG driver (pmg_phier_pcg_solve): iterates and
+    histories bit-identical to the Python multi-part pcg_solve, and the
+    single-part solve's within the partition-invariance bar."""
+    nz = 16
+    grid = (pmg.periodic_box(nx, nz, 0.01, ny=ny) if periodic
+            else pmg.panel_grid(nx, nz, flat_mode=True))
+    ny = grid.ny
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    fg = uni((nx, ny, nz), 8)
+    out = {}
+    for parts in ((px, py), (1, 1)):
+        dec = pmg.Decomposition(nx, parts[0] * parts[1], ny=ny, px=parts[0], py=parts[1])
+        op = pmg.PanelOperator(grid, params, dec.layout(nx))
+        pre = (pmg.SSORPreconditioner(pmg.LineSmoother(op)) if precond == "ssor"
+               else pmg.IdentityPreconditioner())
+        f = pmg.scatter_owned(fg, op.layout)
+        for native in ((True, False) if parts != (1, 1) else (False,)):
+            u, rep = _cg(pmg, f, op, pre, native)
+            out[(parts, native)] = (rep, pmg.gather_owned(u))
+    (rn, un), (rp, up) = out[((px, py), True)], out[((px, py), False)]
+    assert rn.iterations == rp.iterations and rn.converged
+    assert rn.residual_history == rp.residual_history
+    assert np.array_equal(un, up)
+    r1, u1 = out[((1, 1), False)]
+    assert r1.iterations == rn.iterations
+    h, h1 = np.array(rn.residual_history), np.array(r1.residual_history)
+    assert np.max(np.abs(h - h1) / (h1 + 1e-13 * h1[0])) <= 1e-10
+    assert np.max(np.abs(un - u1)) <= 1e-10 * np.max(np.abs(u1))
