@@ -1,12 +1,17 @@
 """Block red-black vertical-line relaxation on the device (reference
 ``smoother.py``).
 
-One half-sweep updates every column of one colour with an exact Thomas
-solve of its vertical tridiagonal block (``smoother.py:122-170``); on the
-device this is ``pmg_half_sweep``: one CTA per 32 columns of a row, the
-right-hand side assembled with coalesced k-plane loads by all warps into
-shared memory, the recurrence run per lane in the reference's operation
-order (bit-identical results).
+One half-sweep updates every column of one colour with a Thomas solve of
+its vertical tridiagonal block (``smoother.py:122-170``), ``pmg_half_sweep``
+on the device.  The default (fast) column solver is k-segmented: the
+linear forward / backward recurrences are solved per segment of levels by
+separate warps and joined by short scans (~1e-15 relative from the
+sequential recurrence); on the large levels of nz = 128 it runs in the
+TMA-fed band kernel (rows streamed once through shared memory), below in
+the register kernel, and for variable coefficients in their
+per-column-coefficient variants.  ``exact_smoother()`` selects the
+sequential recurrence in the reference's operation order (bit-identical to
+the reference).  DESIGN.md section 3.
 """
 
 from __future__ import annotations
