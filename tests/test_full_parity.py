@@ -134,3 +134,26 @@ def test_config4_whole_field(pmg):
     if mem_available_bytes() < need:
         prob = configs.Problem(2048, 2048, 128, 1e-3, 1.0, 8, stretch=1.05, variable_omega=True)
     mg_case(pmg, f"config4_{prob.nx}_mg", prob)
+
+
+def test_config3_two_gpu_grid_whole_field(pmg):
+    """configs[3] at N = 2: the 4096 x 2048 x 128 global grid decomposed as
+    the two-GPU run does (2 x 1 parts of 2048^2), both parts in this process
+    on the native multi-part driver (pmg_phier: exchanges, worker-order
+    reductions, boundary-first overlap, lagged norm), against the C oracle
+    solving the whole global grid."""
+    from paper_1307_2036_b200 import configs
+    prob = configs.config(3, gpus=2)
+    assert (prob.nx, prob.ny) == (4096, 2048)
+    f = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
+    cfg = prob.mg_config()
+    dec = pmg.Decomposition(prob.nx, 2, ny=prob.ny, px=2, py=1)
+    hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg, dec)
+    u, rep = pmg.mg_solve(pmg.scatter_owned(f, hier.fine.layout), hier, cfg)
+    assert hier.native_parts(cfg).replayed_launches() > 0
+    ug = pmg.gather_owned(u)
+    del u, hier
+    torch.cuda.empty_cache()
+    uc, rc = oracle_hier(prob).mg_solve(f)
+    del f
+    compare("config3_2gpu_grid_mg", ug, rep, uc, rc)
