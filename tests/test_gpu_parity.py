@@ -570,11 +570,14 @@ def test_native_hierarchy_errors(pmg):
         _lib.check(_lib.PMG_ERR_BREAKDOWN, "pmg_pcg_solve")
 
 
-@pytest.mark.parametrize("solver", ["mg", "cg"])
+@pytest.mark.parametrize("solver", ["mg", "cg", "mg_parts", "cg_parts"])
 def test_c_host_program(pmg, tmp_path, solver):
     """examples/c_solve.c: a plain C program builds the levels, uploads f,
     solves and downloads u through include/pmg.h alone; its history and
-    solution equal the Python drop-in's bit for bit (same kernels)."""
+    solution equal the Python drop-in's bit for bit (same kernels).  The
+    *_parts solvers cut the grid into a 2 x 2 decomposition in C and run
+    the multi-part drivers (pmg_phier_mg_solve / pmg_phier_pcg_solve)
+    against the Python drop-in on the same decomposition."""
     import shutil
     import subprocess
     from paper_1307_2036_b200 import _lib, configs
@@ -595,9 +598,10 @@ def test_c_host_program(pmg, tmp_path, solver):
     hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg)
     fg = configs.rhs(prob.nx, prob.ny, prob.nz, 0)
     maxiter = 50
+    code = {"mg": 0, "cg": 1, "mg_parts": 2, "cg_parts": 3}[solver]
     with open(tmp_path / "in.bin", "wb") as fp:
-        np.array([prob.nx, prob.ny, prob.nz, len(hier.levels), 1, maxiter,
-                  0 if solver == "mg" else 1], dtype=np.int32).tofile(fp)
+        np.array([prob.nx, prob.ny, prob.nz, len(hier.levels), 1, maxiter, code],
+                 dtype=np.int32).tofile(fp)
         op0 = hier.fine.op
         np.array([1e-5, op0.omega2, op0.vcoef]).tofile(fp)
         for lev in hier.levels:
@@ -613,8 +617,11 @@ def test_c_host_program(pmg, tmp_path, solver):
     iters, conv = np.frombuffer(raw[:8], dtype=np.int32)
     hist = np.frombuffer(raw[8:8 + 8 * (iters + 1)])
     u_c = np.frombuffer(raw[8 + 8 * (iters + 1):]).reshape(prob.nx, prob.ny, prob.nz)
+    if solver.endswith("_parts"):
+        hier = pmg.build_hierarchy(prob.grid(), prob.params(), cfg,
+                                   pmg.Decomposition(prob.nx, 4, px=2, py=2))
     f = pmg.scatter_owned(fg, hier.fine.layout)
-    if solver == "mg":
+    if solver.startswith("mg"):
         u, rep = pmg.mg_solve(f, hier, cfg)
     else:
         op = hier.fine.op
@@ -623,7 +630,7 @@ def test_c_host_program(pmg, tmp_path, solver):
     assert conv == 1 and iters == rep.iterations
     assert list(hist) == rep.residual_history
     assert np.array_equal(u_c, pmg.gather_owned(u))
-    if solver == "mg":                    # and the reference's own history
+    if solver.startswith("mg"):          # and the reference's own history
         g = load("config0_mg")
         ref = np.asarray(g["history"])
         assert len(ref) == len(hist)
