@@ -1781,7 +1781,9 @@ k_half_sweep_segv(Lvl L, double *__restrict__ u, const double *__restrict__ f, i
 // this row's backward pass, so both loads overlap a column solve.
 // RES = 1 / 3: k_half_sweep_segv's fused-residual / f^2 modes.
 // ---------------------------------------------------------------------------
-template <int PLC, int RES = 0, bool LEAN = false>
+// NBZ: neighbours zero (the first red half-sweep from a zero iterate): no
+// other-colour rows are streamed, the line right-hand side is f itself
+template <int PLC, int RES = 0, bool LEAN = false, bool NBZ = false>
 __global__ void __launch_bounds__(32 * 16, 1)
 k_half_sweep_bandv(Lvl L, double *__restrict__ u, int c, double rho, int zero_start,
                    double post_scale, int nstrip, int nband, int band_rows,
@@ -1867,10 +1869,12 @@ k_half_sweep_bandv(Lvl L, double *__restrict__ u, int c, double rho, int zero_st
             tma_box3(fring + slot * NZ * 32, &mF, OFF + h0, 0, r + 1, fullF + slot);
         };
         if (threadIdx.x == 0) {
-            put_b(j0 - 1, seqb);
-            put_b(j0, seqb + 1);
-            put_b(j0 + 1, seqb + 2);
-            if (j0 + 2 <= j1) put_b(j0 + 2, seqb + 3);
+            if (!NBZ) {
+                put_b(j0 - 1, seqb);
+                put_b(j0, seqb + 1);
+                put_b(j0 + 1, seqb + 2);
+                if (j0 + 2 <= j1) put_b(j0 + 2, seqb + 3);
+            }
             put_f(j0, seqf);
             if (j0 + 1 < j1) put_f(j0 + 1, seqf + 1);
         }
@@ -1909,7 +1913,7 @@ k_half_sweep_bandv(Lvl L, double *__restrict__ u, int c, double rho, int zero_st
         if (RES == 1) load_old(j0);
         for (int j = j0; j < j1; ++j) {
             const long long pc = at(L, c, k0, j, h0 + lane);
-            for (int r = (j == j0 ? j - 1 : j + 1); r <= j + 1; ++r) {
+            for (int r = (j == j0 ? j - 1 : j + 1); !NBZ && r <= j + 1; ++r) {
                 const unsigned q = seqb + (unsigned)(r - (j0 - 1));
                 mbar_wait(fullB + (q & 3), (q >> 2) & 1);
             }
@@ -1940,12 +1944,17 @@ k_half_sweep_bandv(Lvl L, double *__restrict__ u, int c, double rho, int zero_st
                     const double vn = Nrow[k * BAND_W + lane];
                     const double fv = Frow[k * 32 + lane];
                     if (RES == 3) dacc = __fma_rn(fv, fv, dacc);
-                    double g = wxm * vw;
-                    g = g + wxp * ve;
-                    g = g + wym * vs;
-                    g = g + wyp * vn;
-                    g = g * tdrw[k];
-                    g = g + fv;
+                    double g;
+                    if (NBZ) {
+                        g = fv;   // smoother.py:137-145 with neighbours_zero
+                    } else {
+                        g = wxm * vw;
+                        g = g + wxp * ve;
+                        g = g + wym * vs;
+                        g = g + wyp * vn;
+                        g = g * tdrw[k];
+                        g = g + fv;
+                    }
                     r[b8 + e] = g;
                     if (RES == 1) {
                         const double vk = vo[b8 + e];
@@ -1989,7 +1998,7 @@ k_half_sweep_bandv(Lvl L, double *__restrict__ u, int c, double rho, int zero_st
             // j - 1 and f row j are free -- for rows j + 3 and j + 2 (two
             // rows of look-ahead in both rings)
             if (threadIdx.x == 0) {
-                if (j + 3 <= j1) put_b(j + 3, seqb + (unsigned)(j + 3 - (j0 - 1)));
+                if (!NBZ && j + 3 <= j1) put_b(j + 3, seqb + (unsigned)(j + 3 - (j0 - 1)));
                 if (j + 2 < j1) put_f(j + 2, seqf + (unsigned)(j + 2 - j0));
             }
             double G = 0.0;
@@ -2721,12 +2730,15 @@ cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const doubl
             else runq(k_residual_restrict_red<0>);
         }
     } else {
+        // variable coefficients: 3 CTAs / SM (166 registers; the per-column
+        // coefficients of four cells): 1024^2 491.7 -> 433.4 us against 2
+        // CTAs / SM, 530.2 us at 4 (spills)
         if (norm) {
-            if (F.par & 1) runq(k_residual_restrict_red<1, 2, false, true>);
-            else runq(k_residual_restrict_red<0, 2, false, true>);
+            if (F.par & 1) runq(k_residual_restrict_red<1, 3, false, true>);
+            else runq(k_residual_restrict_red<0, 3, false, true>);
         } else {
-            if (F.par & 1) runq(k_residual_restrict_red<1, 2, false>);
-            else runq(k_residual_restrict_red<0, 2, false>);
+            if (F.par & 1) runq(k_residual_restrict_red<1, 3, false>);
+            else runq(k_residual_restrict_red<0, 3, false>);
         }
     }
     return cudaGetLastError();
@@ -2953,6 +2965,10 @@ static void bandv_attrs() {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_half_sweep_bandv<P, 3, true>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_bandv<P, 0, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_half_sweep_bandv<P, 3, true, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 template <int P>
 static void band_attrs() {
@@ -3120,7 +3136,7 @@ static bool launch_half_sweep_bandv(const Lvl &L, double *u, const double *f, in
     const int hrow = L.nx / 2;
     if (g_smoother_exact || L.uniform || !L.invd || L.nz != BAND_NZ ||
         !(L.plane == 2056 || L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
-          L.plane == 136) || nbr_zero ||
+          L.plane == 136) || (nbr_zero && !(rho == 1.0 && !zero_start && mode != 1)) ||
         L.nx % 2 || hrow % 32 || hrow < 64 || L.ny < 8 || L.rys != 1 || L.rxn < 1 || L.ryn < 1)
         return false;
     const int o = color ^ 1;
@@ -3147,7 +3163,15 @@ static bool launch_half_sweep_bandv(const Lvl &L, double *u, const double *f, in
     const bool lean = rho == 1.0 && !zero_start;
 #define PMG_BANDV(P)                                                                         \
     do {                                                                                     \
-        if (mode == 1)                                                                       \
+        if (nbr_zero && mode == 3)                                                           \
+            k_half_sweep_bandv<P, 3, true, true><<<grid, 512, bandv_smem(), st>>>(           \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
+                mE, partials, nullptr);                                                      \
+        else if (nbr_zero)                                                                   \
+            k_half_sweep_bandv<P, 0, true, true><<<grid, 512, bandv_smem(), st>>>(           \
+                L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
+                mE, nullptr, nullptr);                                                       \
+        else if (mode == 1)                                                                       \
             k_half_sweep_bandv<P, 1, true><<<grid, 512, bandv_smem(), st>>>(                  \
                 L, u, color, rho, zero_start, post_scale, nstrip, nband, band_rows, mF, mB,  \
                 mE, partials, res_uw);                                                       \
