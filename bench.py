@@ -615,11 +615,19 @@ def main():
     traffic, tsrc = ncu_traffic("k_half_sweep_band", nxl)
     roofline = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": ach / peak, "traffic": traffic,
-                "kernel": f"k_half_sweep_band (fine level {nxl}x{s.lay.my}x128, TMA-fed line "
-                          "relaxation)",
+                "kernel": (f"k_half_sweep_band (fine level {nxl}x{s.lay.my}x128, TMA-fed line "
+                           "relaxation)" if s.hier.fine.op.handles[s.w].uniform else
+                           f"k_half_sweep_bandv (fine level {nxl}x{s.lay.my}x128, variable "
+                           "coefficients; its 4 B/cell pivot field is not algorithmic, SURVEY 8d)"),
                 "alg_bytes_per_launch": 12 * s.dof_local, "launch_ms": t_hs * 1e3,
                 "peak_source": peak_src, "traffic_source": tsrc}
 
+    # the e2e legs allocate their own double-buffered fields: release the
+    # device-resident f / u and the kernel-timing scratch first (configs[4]
+    # needs ~17 GB per field)
+    s.hier._persist = None
+    s.f = s.u = None
+    torch.cuda.empty_cache()
     e2e = e2e_legs(s, args.e2e_steps, world, torch)
     del s
     torch.cuda.empty_cache()
