@@ -647,14 +647,17 @@ int mg_solve_lagged(pmg_phier *h, const double *const *f, double *const *u, doub
         if (x)
             for (int p = 0; p < np; ++p) h->fine_view[p] = vb[p];
         Fine fv;
-        fv.red_done = kind >= 4;
+        fv.red_done = kind >= 4 && kind < 8;
         fv.fsq = kind < 4;
         int rc = vcycle(h, 0, base[x].data(), f, kind < 4, s, &fv);
-        // the next cycle's first red half-sweep into the other array, with
-        // ||f - A u||^2 of this cycle's result
-        for (int p = 0; !rc && p < np; ++p)
-            rc = pmg_half_sweep_res(LV(h, p, 0), base[x][p], base[x ^ 1][p], f[p],
-                                    h->scr[0] + p * 1024, h->slots + p, s);
+        for (int p = 0; !rc && p < np; ++p) {
+            if (kind == 6 || kind == 7)   // predicted last cycle: the check-only norm
+                rc = pmg_red_residual_norm(LV(h, p, 0), f[p], base[x][p], h->scr[0] + p * 1024,
+                                           h->slots + p, s);
+            else   // the next cycle's first red half-sweep into the other array
+                rc = pmg_half_sweep_res(LV(h, p, 0), base[x][p], base[x ^ 1][p], f[p],
+                                        h->scr[0] + p * 1024, h->slots + p, s);
+        }
         if (!rc) rc = global_sum(h, h->res_d, s);
         h->fine_view.clear();
         return rc;
@@ -663,7 +666,13 @@ int mg_solve_lagged(pmg_phier *h, const double *const *f, double *const *u, doub
     int kind = 2 + x;
     *iters = 0;
     *converged = 0;
-    double r0 = 0.0;
+    double r0 = 0.0, prev = 0.0;
+    // kinds 6 + X (predicted last cycle, pmg_driver.cu): when the last
+    // contraction predicts convergence with a factor-2 margin the cycle ends
+    // with the check-only red residual norm; a miss continues with kind
+    // 8 + X (an ordinary first red half-sweep on the same array)
+    bool predict = true;
+    for (int p = 0; p < np; ++p) predict = predict && pmg_residual_restrict_red_ok(h->P[p][0].lv);
     for (int it = 0; it < maxiter; ++it) {
         // graphs are keyed on the caller's arrays (the views depend on them)
         TRY(replay(h, u, f, kind, s, [&] { return body(kind); }));
@@ -685,8 +694,14 @@ int mg_solve_lagged(pmg_phier *h, const double *const *f, double *const *u, doub
             break;
         }
         if (it + 1 == maxiter) break;   // u_maxiter stays in red array x
-        x ^= 1;                          // the fused sweep relaxed red into the other array
-        kind = 4 + x;
+        if (kind == 6 || kind == 7) {
+            kind = 8 + x;                // the guess missed: same array, no more guesses
+            predict = false;
+        } else {
+            x ^= 1;                      // the fused sweep relaxed red into the other array
+            kind = (predict && prev > 0.0 && rn * (rn / prev) < 0.5 * eps * r0) ? 6 + x : 4 + x;
+        }
+        prev = rn;
     }
     h->last_iters = *iters;
     if (x == 1)   // the result's red array is red1: copy it (halo included) into u
