@@ -605,7 +605,6 @@ def main():
 
     sampler = ClockSampler(local)
     r = time_solves(s, args.steps, args.warmup, world, torch, sampler)
-    cfgd["iterations"] = r["iterations"]
 
     kern = fine_kernels(s, torch)
     peak, peak_src = measured_peak()
@@ -641,7 +640,7 @@ def main():
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: f ~ U[-1,1] from default_rng(0), global (i,j,k) order, per-rank block",
         "config": cfgd,
-        "solve_ms": r["solve_ms"], "v_cycle_ms": r["v_cycle_ms"],
+        "solve_ms": r["solve_ms"], "v_cycle_ms": r["v_cycle_ms"], "iterations": r["iterations"],
         "residual_history": r["residual_history"],
         "roofline": roofline, "kernels": kern, "e2e": e2e,
         "gpu_launches": r["launches"], "driver": r["driver"],
