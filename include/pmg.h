@@ -166,8 +166,11 @@ int pmg_half_sweep(const pmg_level *lvl, double *u, const double *f, int color,
  * ry0 + t * rys (t < ryn).  A boundary-first multi-part sweep relaxes the
  * strips and rows that hold the part's boundary columns first, exchanges
  * their halos while the interior region relaxes, with the
- * same values as one whole-part call.  Fast smoother mode and uniform
- * coefficients only (pmg_half_sweep_region_ok), else PMG_ERR_VALUE. */
+ * same values as one whole-part call.  Fast smoother mode, on uniform
+ * levels or on variable levels the band kernel runs (nz = 128, rows of a
+ * multiple of 64 cells, eight rows or more; rows must then be consecutive,
+ * rys = 1, and neighbors_zero needs rho = 1 without zero_start) --
+ * pmg_half_sweep_region_ok -- else PMG_ERR_VALUE. */
 int pmg_half_sweep_region_ok(const pmg_level *lvl);
 int pmg_half_sweep_region(const pmg_level *lvl, double *u, const double *f, int color, double rho,
                           int zero_start, int neighbors_zero, double post_scale, int rx0, int rxs,

@@ -30,6 +30,7 @@ cudaError_t launch_restrict(const Lvl &, const Lvl &, const double *, double *, 
                             cudaStream_t);
 bool half_sweep_dot_ok(const Lvl &L);
 bool half_sweep_res_ok(const Lvl &L);
+bool half_sweep_bandv_ok(const Lvl &L);
 bool residual_restrict_red_ok(const Lvl &F);
 cudaError_t launch_half_sweep_fsq(const Lvl &L, double *u, const double *f, int color,
                                   int nbr_zero, double *partials, int *np, cudaStream_t st);
@@ -461,8 +462,11 @@ int pmg_half_sweep_region_ok(const pmg_level *lv) {
     if (!lv) return 0;
     const Lvl &L = lv->L;
     // the fast uniform column solvers (k_half_sweep_band / k_half_sweep_seg)
-    // walk tile regions; the exact and variable kernels do not
-    return (!g_smoother_exact && L.uniform && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) ? 1 : 0;
+    // and the variable-coefficient band kernel walk tile regions; the exact
+    // solver and the variable register kernel do not
+    if (L.uniform)
+        return (!g_smoother_exact && L.seg && (L.nz + L.seg - 1) / L.seg <= 8) ? 1 : 0;
+    return half_sweep_bandv_ok(L) ? 1 : 0;
 }
 
 int pmg_half_sweep_region(const pmg_level *lv, double *u, const double *f, int color, double rho,
@@ -471,7 +475,15 @@ int pmg_half_sweep_region(const pmg_level *lv, double *u, const double *f, int c
     PMG_CHECK_LVL(lv);
     if (color != 0 && color != 1) return fail(PMG_ERR_VALUE, "colour must be 0 (red) or 1 (black)");
     if (!pmg_half_sweep_region_ok(lv))
-        return fail(PMG_ERR_VALUE, "tile regions need the fast smoother on a uniform level");
+        return fail(PMG_ERR_VALUE, "tile regions need the fast smoother on a uniform level "
+                                   "or a band-kernel variable level");
+    if (!lv->L.uniform && neighbors_zero && !(rho == 1.0 && !zero_start))
+        return fail(PMG_ERR_VALUE, "variable-level regions with zero neighbours need rho = 1 "
+                                   "and no zero start");
+    if (!lv->L.uniform && !lv->prepared) {
+        int rc = pmg_level_prepare(const_cast<pmg_level *>(lv), st);
+        if (rc) return rc;
+    }
     const Lvl &L0 = lv->L;
     const int hx = ((L0.nx + 1) / 2 + 31) / 32;
     if (rxn < 0 || ryn < 0 || rxs < 1 || rys < 1 || rx0 < 0 || ry0 < 0 ||
@@ -479,6 +491,10 @@ int pmg_half_sweep_region(const pmg_level *lv, double *u, const double *f, int c
         (ryn > 0 && ry0 + (long long)(ryn - 1) * rys >= L0.ny))
         return fail(PMG_ERR_VALUE, "tile region outside the part");
     if (rxn == 0 || ryn == 0) return PMG_OK;
+    if (ryn == 1) rys = 1;
+    if (rxn == 1) rxs = 1;
+    if (!L0.uniform && rys != 1)
+        return fail(PMG_ERR_VALUE, "variable-level regions take consecutive rows (rys = 1)");
     Lvl L = L0;
     L.rx0 = rx0, L.rxs = rxs, L.rxn = rxn;
     L.ry0 = ry0, L.rys = rys, L.ryn = ryn;

@@ -2777,6 +2777,18 @@ static bool launch_half_sweep_band(const Lvl &L, double *u, const double *f, int
                                    double rho, int zero_start, int nbr_zero, double post_scale,
                                    cudaStream_t st, double *partials, int *np, bool fsq,
                                    double *res_uw = nullptr);
+
+// variable-coefficient levels the TMA band kernel (k_half_sweep_bandv) runs:
+// nz = 128, a planned plane pitch, whole 32-column strips of at least two
+// per colour row, eight rows or more.  Its units walk tile regions (rows in
+// consecutive runs), so these levels also relax boundary-first.
+bool half_sweep_bandv_ok(const Lvl &L) {
+    const int hrow = L.nx / 2;
+    return !g_smoother_exact && !L.uniform && L.nz == BAND_NZ &&
+           (L.plane == 2056 || L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
+            L.plane == 136) &&
+           L.nx % 2 == 0 && hrow % 32 == 0 && hrow >= 64 && L.ny >= 8;
+}
 static bool launch_half_sweep_bandv(const Lvl &L, double *u, const double *f, int color,
                                     double rho, int zero_start, int nbr_zero, double post_scale,
                                     cudaStream_t st, int mode, double *partials, int *np,
@@ -3133,11 +3145,9 @@ static bool launch_half_sweep_bandv(const Lvl &L, double *u, const double *f, in
                                     double rho, int zero_start, int nbr_zero, double post_scale,
                                     cudaStream_t st, int mode, double *partials, int *np,
                                     double *res_uw) {
-    const int hrow = L.nx / 2;
-    if (g_smoother_exact || L.uniform || !L.invd || L.nz != BAND_NZ ||
-        !(L.plane == 2056 || L.plane == 1032 || L.plane == 520 || L.plane == 264 ||
-          L.plane == 136) || (nbr_zero && !(rho == 1.0 && !zero_start && mode != 1)) ||
-        L.nx % 2 || hrow % 32 || hrow < 64 || L.ny < 8 || L.rys != 1 || L.rxn < 1 || L.ryn < 1)
+    if (!L.invd || !half_sweep_bandv_ok(L) ||
+        (nbr_zero && !(rho == 1.0 && !zero_start && mode != 1)) || L.rys != 1 || L.rxn < 1 ||
+        L.ryn < 1)
         return false;
     const int o = color ^ 1;
     CUtensorMap mF, mB, mE;

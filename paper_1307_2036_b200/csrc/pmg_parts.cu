@@ -418,7 +418,10 @@ bool overlapped(const pmg_phier *h, int c) {
 int half_sweep_x(pmg_phier *h, int c, double *const *u, const double *const *f, int color,
                  int nbr_zero, cudaStream_t s) {
     const double rho = h->d.rho;
-    if (!overlapped(h, c)) {
+    // variable-level regions run the band kernel, which relaxes against zero
+    // neighbours only as a plain rho = 1 sweep
+    const bool var_nz = nbr_zero && rho != 1.0 && !pmg::level_lvl(LV(h, 0, c)).uniform;
+    if (var_nz || !overlapped(h, c)) {
         for (int p = 0; p < h->np; ++p)
             TRY(pmg_half_sweep(LV(h, p, c), u[p], f[p], color, rho, 0, nbr_zero, 1.0, s));
         return exchange(h, c, u, s);

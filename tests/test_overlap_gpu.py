@@ -84,3 +84,49 @@ def test_region_sweep_matches_whole(pmg, nx, ny, nz):
     with pytest.raises(ValueError):
         _lib.call("pmg_half_sweep_region", h.h, u0.parts[w].ptr, f.parts[w].ptr, 0, 1.0, 0, 0,
                   1.0, 0, 1, nstrip + 1, 0, 1, ny, st)
+
+
+@pytest.mark.parametrize("nx,ny", [(256, 64), (512, 512), (1024, 256), (2048, 16)])
+def test_variable_region_sweep_matches_whole(pmg, nx, ny):
+    """configs[4]'s level family (graded dz, omega^2(x, y)): the variable
+    band kernel walks the same regions, bit for bit the whole-part sweep;
+    strided rows and zero neighbours with rho != 1 are refused (the band
+    kernel does not run them)."""
+    from paper_1307_2036_b200 import _lib, configs
+    lib = _lib.load()
+    nz = 128
+    prob = configs.Problem(nx, ny, nz, 1e-3, 1.0, 4, stretch=1.05, variable_omega=True)
+    op = pmg.PanelOperator(prob.grid(), prob.params(),
+                           pmg.Decomposition(nx, 1, ny=ny).layout(nx))
+    (w, h), = op.handles.items()
+    assert lib.pmg_half_sweep_region_ok(h.h) == 1
+    rng = np.random.default_rng(11)
+    u0 = pmg.scatter_owned(rng.uniform(-1, 1, (nx, ny, nz)), op.layout)
+    pmg.halo_exchange(u0)
+    f = pmg.scatter_owned(rng.uniform(-1, 1, (nx, ny, nz)), op.layout)
+    nstrip = ((nx + 1) // 2 + 31) // 32
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for color in (0, 1):
+        for rho, zs, nbz in ((1.0, 0, 0), (1.3, 0, 0), (1.0, 0, 1), (1.2, 1, 0)):
+            a, b = u0.copy(), u0.copy()
+            _lib.call("pmg_half_sweep", h.h, a.parts[w].ptr, f.parts[w].ptr, color, rho, zs,
+                      nbz, 1.0, st)
+            for reg in frame_and_interior(nstrip, ny):
+                _lib.call("pmg_half_sweep_region", h.h, b.parts[w].ptr, f.parts[w].ptr, color,
+                          rho, zs, nbz, 1.0, *reg, st)
+            assert torch.equal(a.parts[w].data, b.parts[w].data), (color, rho, zs, nbz)
+    with pytest.raises(ValueError):
+        _lib.call("pmg_half_sweep_region", h.h, u0.parts[w].ptr, f.parts[w].ptr, 0, 1.0, 0, 0,
+                  1.0, 0, 1, nstrip, 0, 2, ny // 2, st)
+    with pytest.raises(ValueError):
+        _lib.call("pmg_half_sweep_region", h.h, u0.parts[w].ptr, f.parts[w].ptr, 0, 1.3, 0, 1,
+                  1.0, 0, 1, nstrip, 0, 1, ny, st)
+
+
+def test_variable_region_refused_below_band(pmg):
+    """Variable levels below the band kernel's sizes have no regions."""
+    from paper_1307_2036_b200 import _lib, configs
+    prob = configs.Problem(64, 64, 128, 1e-3, 1.0, 3, stretch=1.05, variable_omega=True)
+    op = pmg.PanelOperator(prob.grid(), prob.params(), pmg.Decomposition(64, 1).layout(64))
+    (w, h), = op.handles.items()
+    assert _lib.load().pmg_half_sweep_region_ok(h.h) == 0

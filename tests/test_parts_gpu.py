@@ -196,12 +196,15 @@ def test_nccl_self_exchange_matches(pmg, nx, nz, lagged):
 
 
 @pytest.mark.parametrize("px,py", [(2, 2), (2, 1)])
-def test_native_parts_variable_coefficients(pmg, px, py):
+def test_native_parts_variable_coefficients(pmg, px, py, monkeypatch):
     """configs[4]'s problem family (graded levels, omega^2(x, y)) on the
-    native multi-part driver: iterates bit-identical to the Python
-    multi-part driver, histories within the lagged-norm bar, and the
-    single-part solve within the partition-invariance bar."""
-    from paper_1307_2036_b200 import configs
+    native multi-part driver, with boundary-first overlap on the fine
+    level (threshold lowered to the 256-column parts: the variable band
+    kernel walks the frame and interior regions): iterates bit-identical
+    to the Python multi-part driver, histories within the lagged-norm
+    bar, and the single-part solve within the partition-invariance bar."""
+    from paper_1307_2036_b200 import configs, multigrid as mg
+    monkeypatch.setattr(mg, "OVERLAP_NX", 256)
     prob = configs.Problem(512, 512, 128, 1e-3, 1.0, 5, stretch=1.05, variable_omega=True)
     grid, params = prob.grid(), prob.params()
     fg = configs.rhs(512, 512, 128, 0)
