@@ -437,7 +437,13 @@ def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
                 launches += g_first.launches + (n_it - 1) * g_rest.launches
             elif g_rest is not None:
                 launches += n_it * g_rest.launches
+    # one traced solve after the timed region: the device time of every
+    # V-cycle (CUDA event pair per graph replay, tracing.py)
+    with pmg.tracing():
+        s.u, trep = pmg.mg_solve(s.f, s.hier, s.cfg, out=s.u)
+    cyc = [round(max_over_ranks(x * 1e-3, world) * 1e3, 4) for x in trep.cycle_times_ms]
     return {"t": t, "solve_ms": t / steps * 1e3, "iterations": iters[-1],
+            "cycle_ms": cyc,
             "v_cycle_ms": t / sum(iters) * 1e3, "dof_s": s.prob.dof * steps / t,
             "residual_history": [float(x) for x in reps[-1].residual_history],
             "launches": int(launches),
@@ -641,7 +647,7 @@ def main():
         "data": "synthetic: f ~ U[-1,1] from default_rng(0), global (i,j,k) order, per-rank block",
         "config": cfgd,
         "solve_ms": r["solve_ms"], "v_cycle_ms": r["v_cycle_ms"], "iterations": r["iterations"],
-        "residual_history": r["residual_history"],
+        "cycle_ms": r["cycle_ms"], "residual_history": r["residual_history"],
         "roofline": roofline, "kernels": kern, "e2e": e2e,
         "gpu_launches": r["launches"], "driver": r["driver"],
         "clocks": sampler.summary(),

@@ -69,6 +69,14 @@ int pmg_version(void);
 /* number of kernel launches this library has issued (or recorded into a
  * CUDA graph) since load; launchers with a reduction count two. */
 long long pmg_launch_count(void);
+/* tracing mode (the reference times the iteration
+ * loop with wall time only, multigrid.py:321,329): while on (1), the
+ * drivers push NVTX ranges -- solve, cycle / CG iteration, level, halo
+ * exchange (level ranges mark the cycle graph's capture) -- and time every
+ * cycle's graph replay on the device with a CUDA event pair
+ * (pmg_hier_cycle_times / pmg_phier_cycle_times).  Off (0) by default. */
+int pmg_set_tracing(int on);
+int pmg_get_tracing(void);
 const char *pmg_last_error(void);
 int pmg_device_sm_count(int device, int *out);
 
@@ -322,6 +330,10 @@ long long pmg_hier_graph_launches(const pmg_hier *hier, const double *f, const d
                                   int first);
 /* cumulative kernels issued by this hierarchy's graph replays */
 long long pmg_hier_replayed_launches(const pmg_hier *hier);
+/* device milliseconds of each V-cycle of the last pmg_mg_solve run with
+ * tracing on: copies min(count, cap) values to ms, returns the count (0 when
+ * that solve ran untraced), -1 on a null handle */
+int pmg_hier_cycle_times(const pmg_hier *hier, double *ms, int cap);
 /* preconditioned CG from u = 0 (krylov.py:88-167): precond 1 = SSOR(rho),
  * 0 = identity; tau as the reference (tiny-residual cut-off).  work: device
  * buffer of pmg_pcg_work_doubles() doubles; hist as pmg_mg_solve.
@@ -392,6 +404,8 @@ int pmg_phier_halo_exchange(pmg_phier *hier, int level, double *const *fields, v
 int pmg_phier_dot(pmg_phier *hier, int level, const double *const *a, const double *const *b,
                   double *out, void *stream);
 long long pmg_phier_replayed_launches(const pmg_phier *hier);
+/* as pmg_hier_cycle_times, for the last pmg_phier_mg_solve */
+int pmg_phier_cycle_times(const pmg_phier *hier, double *ms, int cap);
 long long pmg_phier_exchanges(const pmg_phier *hier);
 
 #ifdef __cplusplus

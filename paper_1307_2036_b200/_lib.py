@@ -52,6 +52,8 @@ _LL = C.c_longlong
 SIGNATURES = {
     "pmg_version": (_I, []),
     "pmg_launch_count": (_LL, []),
+    "pmg_set_tracing": (_I, [_I]),
+    "pmg_get_tracing": (_I, []),
     "pmg_last_error": (C.c_char_p, []),
     "pmg_device_sm_count": (_I, [_I, C.POINTER(_I)]),
     "pmg_level_create": (_I, [C.POINTER(LevelDesc), C.POINTER(_P)]),
@@ -73,6 +75,7 @@ SIGNATURES = {
     "pmg_hier_destroy": (_I, [_P]),
     "pmg_hier_graph_launches": (_LL, [_P, _P, _P, _I]),
     "pmg_hier_replayed_launches": (_LL, [_P]),
+    "pmg_hier_cycle_times": (_I, [_P, _P, _I]),
     "pmg_vcycle": (_I, [_P, _P, _P, _I, _P]),
     "pmg_mg_solve": (_I, [_P, _P, _P, _D, _I, _P, C.POINTER(_I), C.POINTER(_I), _P]),
     "pmg_pcg_work_doubles": (_LL, [_P]),
@@ -129,6 +132,7 @@ SIGNATURES = {
     "pmg_phier_halo_exchange": (_I, [_P, _I, C.POINTER(_P), _P]),
     "pmg_phier_dot": (_I, [_P, _I, C.POINTER(_P), C.POINTER(_P), _P, _P]),
     "pmg_phier_replayed_launches": (_LL, [_P]),
+    "pmg_phier_cycle_times": (_I, [_P, _P, _I]),
     "pmg_phier_exchanges": (_LL, [_P]),
 }
 

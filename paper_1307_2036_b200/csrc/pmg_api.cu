@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "pmg_common.cuh"
+#include "pmg_trace.h"
 
 namespace pmg {
 extern std::atomic<long long> g_launches;
@@ -167,6 +168,14 @@ int pmg_set_smoother_mode(int mode) {
 int pmg_get_smoother_mode(void) { return pmg::g_smoother_exact; }
 
 long long pmg_launch_count(void) { return g_launches.load(); }
+
+int pmg_set_tracing(int on) {
+    if (on < 0 || on > 1) return fail(PMG_ERR_VALUE, "tracing must be 0 (off) or 1 (on)");
+    pmg::g_trace.store(on);
+    return PMG_OK;
+}
+
+int pmg_get_tracing(void) { return pmg::g_trace.load(); }
 
 const char *pmg_last_error(void) { return g_err.c_str(); }
 

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/pmg.h"
+#include "pmg_trace.h"
 
 namespace pmg {
 extern int g_mode_gen;
@@ -85,6 +86,7 @@ struct pmg_hier {
     cudaStream_t own = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     int mode_gen = 0;                // pmg::g_mode_gen the graphs / views were made under
+    pmg::CycleClock clock;           // per-cycle device times of the last traced solve
 };
 
 namespace {
@@ -136,6 +138,7 @@ const pmg_level *lvl(const pmg_hier *h, int c, const Fine &fv) {
 
 // halo ring refresh, skipped on wrap views (their readers wrap around)
 int halo(const pmg_hier *h, const pmg_level *l, double *x, cudaStream_t st) {
+    pmg::Trace tr("halo exchange");
     if (pmg::level_hflags(l) & pmg::HF_WRAP) return PMG_OK;
     return pmg_halo_self(l, x, h->d.periodic_x, h->d.periodic_y, st);
 }
@@ -176,6 +179,7 @@ int sweeps(const pmg_hier *h, const pmg_level *l, double *u, const double *f, in
 // Alg. 1 (multigrid.py:271-294); level 0 works on the caller's u0 / f0
 int vcycle(pmg_hier *h, int c, double *u0, const double *f0, bool first, cudaStream_t st,
            const Fine &fv = Fine()) {
+    pmg::Trace tr("level %d", c);
     const int L = (int)h->lv.size();
     double *u = c ? h->u[c] : u0;
     const double *f = c ? h->f[c] : f0;
@@ -263,6 +267,7 @@ int replay_kind(pmg_hier *h, double *u, const double *f, int kind, cudaStream_t 
         cudaGraphExecDestroy(h->graphs.front().exec);
         h->graphs.erase(h->graphs.begin());
     }
+    pmg::Trace tr("capture cycle graph");
     cudaGraph_t graph;
     const long long l0 = pmg_launch_count();
     TRYC(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "capture");
@@ -386,6 +391,11 @@ int pmg_hier_destroy(pmg_hier *h) {
 
 long long pmg_hier_replayed_launches(const pmg_hier *h) { return h ? h->replayed : -1; }
 
+int pmg_hier_cycle_times(const pmg_hier *h, double *ms, int cap) {
+    if (!h || (cap > 0 && !ms)) return -1;
+    return h->clock.copy_out(ms, cap);
+}
+
 long long pmg_hier_graph_launches(const pmg_hier *h, const double *f, const double *u,
                                   int first) {
     if (!h) return -1;
@@ -450,7 +460,10 @@ static int mg_solve_lagged(pmg_hier *h, const double *f, double *u, double eps, 
     double r0 = 0.0, prev = 0.0;
     bool predict = pmg_residual_restrict_red_ok(l0) != 0;
     for (int it = 0; it < maxiter; ++it) {
+        pmg::Trace tr("cycle %d", it + 1);
+        TRYC(h->clock.start(st), "cycle clock");
         TRY(replay_kind(h, u, f, kind, st, [&] { return lagged_body(h, f, kind, g, st); }));
+        TRYC(h->clock.stop(st), "cycle clock");
         TRYC(cudaStreamSynchronize(st), "sync");
         if (it == 0) {
             // r0 = ||f|| (multigrid.py:307-309), summed by the first cycle
@@ -515,7 +528,10 @@ static int mg_solve_on(pmg_hier *h, const double *f, double *u, double eps, int 
     const bool lean_first = h->d.rho == 1.0 && h->d.nu_pre >= 1 && h->lv.size() > 1;
     if (!lean_first) TRY(pmg_fill(l0, u, 0.0, st));
     for (int it = 0; it < maxiter; ++it) {
+        pmg::Trace tr("cycle %d", it + 1);
+        TRYC(h->clock.start(st), "cycle clock");
         TRY(replay(h, u, f, lean_first && it == 0, st));
+        TRYC(h->clock.stop(st), "cycle clock");
         TRYC(cudaStreamSynchronize(st), "sync");
         const double rn = std::sqrt(h->res_h[0]);
         hist[it + 1] = rn;
@@ -534,6 +550,8 @@ int pmg_mg_solve(pmg_hier *h, const double *f, double *u, double eps, int maxite
     if (maxiter < 0 || !(eps > 0.0)) return err(PMG_ERR_VALUE, "need eps > 0 and maxiter >= 0");
     cudaStream_t st = (cudaStream_t)stream;
     sync_mode(h);
+    pmg::Trace tr("pmg_mg_solve");
+    h->clock.reset();
     if (st) return mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, st);
     // legacy stream: run on the hierarchy's stream, ordered by events
     TRYC(cudaEventRecord(h->ev_in, 0), "event");
@@ -559,6 +577,7 @@ int pmg_pcg_solve(const pmg_level *lv, const double *f, double *u, double eps, i
     if (!(eps > 0.0 && eps < 1.0)) return err(PMG_ERR_VALUE, "relative tolerance must lie in (0, 1)");
     if (precond && !(rho > 0.0 && rho < 2.0))
         return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
+    pmg::Trace tr("pmg_pcg_solve");
     cudaStream_t st = (cudaStream_t)stream;
     const long long n = pmg_level_field_doubles(lv);
     double *r = work, *z = work + n, *p = work + 2 * n, *q = work + 3 * n;
@@ -605,6 +624,7 @@ int pmg_pcg_solve(const pmg_level *lv, const double *f, double *u, double eps, i
     if (!(res_h[0] > 0.0)) return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
     bool pending = false;
     for (int it = 1; it <= maxiter; ++it) {
+        pmg::Trace ti("iteration %d", it);
         TRY(pmg_apply_dot(lv, p, q, scratch, pq, stream));
         TRY(pmg_cg_update(lv, kap, pq, p, q, nullptr, r, scratch, rr, stream));
         pending = true;

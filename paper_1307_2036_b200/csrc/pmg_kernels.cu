@@ -19,6 +19,8 @@ namespace pmg {
 // kernel launches issued by this library (host-side count, incl. launches
 // recorded into CUDA graphs)
 std::atomic<long long> g_launches{0};
+// tracing mode (pmg_set_tracing, pmg_trace.h)
+std::atomic<int> g_trace{0};
 int g_smoother_exact = 0;
 // bumped whenever the smoother mode changes: kernel variants are chosen when a
 // driver graph is captured, so graphs and views cached under another mode are

@@ -36,6 +36,7 @@
 #include <nccl.h>   // types and prototypes only; symbols come from dlsym
 
 #include "pmg_common.cuh"
+#include "pmg_trace.h"
 
 namespace pmg {
 extern std::atomic<long long> g_launches;
@@ -261,6 +262,7 @@ struct pmg_phier {
     int last_iters = 4;
     // CG work fields per part (r, z, p, q), allocated on first use
     std::vector<double *> cgw;
+    pmg::CycleClock clock;                    // per-cycle device times of the last traced solve
 };
 
 namespace {
@@ -311,6 +313,7 @@ const pmg_level *LV(const pmg_phier *h, int p, int c) {
 // launch for every part's two faces; with a communicator, one pack launch,
 // one NCCL group, one unpack launch.
 int exchange(pmg_phier *h, int c, double *const *x, cudaStream_t s) {
+    pmg::Trace tr("halo exchange level %d", c);
     ++h->exchanges;
     const PL &q0 = h->P[0][c];
     for (int phase = 0; phase < 2; ++phase) {
@@ -515,6 +518,7 @@ int sweeps(pmg_phier *h, int c, double *const *u, const double *const *f, int n,
 // LV's view under the lagged norm)
 int vcycle(pmg_phier *h, int c, double *const *u0, const double *const *f0, bool first,
            cudaStream_t s, const Fine *fv = nullptr) {
+    pmg::Trace tr("level %d", c);
     const int L = h->nlev;
     const auto u = level_u(h, c, u0);
     const auto f = level_f(h, c, f0);
@@ -569,6 +573,7 @@ int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cud
         cudaGraphExecDestroy(h->graphs.front().exec);
         h->graphs.erase(h->graphs.begin());
     }
+    pmg::Trace tr("capture cycle graph");
     cudaGraph_t graph;
     const long long l0 = pmg_launch_count();
     TRYC(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
@@ -678,7 +683,10 @@ int mg_solve_lagged(pmg_phier *h, const double *const *f, double *const *u, doub
     for (int p = 0; p < np; ++p) predict = predict && pmg_residual_restrict_red_ok(h->P[p][0].lv);
     for (int it = 0; it < maxiter; ++it) {
         // graphs are keyed on the caller's arrays (the views depend on them)
+        pmg::Trace tr("cycle %d", it + 1);
+        TRYC(h->clock.start(s), "cycle clock");
         TRY(replay(h, u, f, kind, s, [&] { return body(kind); }));
+        TRYC(h->clock.stop(s), "cycle clock");
         TRYC(cudaStreamSynchronize(s), "sync");
         if (it == 0) {
             r0 = std::sqrt(h->res_h[1]);
@@ -741,10 +749,13 @@ int mg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double e
         for (int p = 0; p < h->np; ++p) TRY(pmg_fill(h->P[p][0].lv, u[p], 0.0, s));
     for (int it = 0; it < maxiter; ++it) {
         const int kind = (lean_first && it == 0) ? 1 : 0;
+        pmg::Trace tr("cycle %d", it + 1);
+        TRYC(h->clock.start(s), "cycle clock");
         TRY(replay(h, u, f, kind, s, [&] {
             TRY(vcycle(h, 0, u, f, kind == 1, s));
             return norm2(h, u, f, h->res_d, s);
         }));
+        TRYC(h->clock.stop(s), "cycle clock");
         TRYC(cudaStreamSynchronize(s), "sync");
         const double rn = std::sqrt(h->res_h[0]);
         hist[it + 1] = rn;
@@ -835,6 +846,7 @@ int pcg_solve_on(pmg_phier *h, const double *const *f, double *const *u, double 
         return err(PMG_ERR_BREAKDOWN, "<r, z> <= 0: preconditioner is not positive definite");
     bool pending = false;
     for (int it = 1; it <= maxiter; ++it) {
+        pmg::Trace ti("iteration %d", it);
         for (int p = 0; p < np; ++p)
             TRY(pmg_apply_dot(h->P[p][0].lv, pp[p], q[p], h->scr[0], h->slots + p, s));
         TRY(global_sum(h, pq, s));
@@ -1069,6 +1081,8 @@ int pmg_phier_mg_solve(pmg_phier *h, const double *const *f, double *const *u, d
     for (int p = 0; p < h->np; ++p)
         if (!f[p] || !u[p]) return err(PMG_ERR_VALUE, "null field");
     sync_mode(h);
+    pmg::Trace tr("pmg_phier_mg_solve");
+    h->clock.reset();
     return on_stream(h, stream, [&](cudaStream_t s) {
         return mg_solve_on(h, f, u, eps, maxiter, hist, iters, converged, s);
     });
@@ -1082,6 +1096,7 @@ int pmg_phier_pcg_solve(pmg_phier *h, const double *const *f, double *const *u, 
     if (precond && !(rho > 0.0 && rho < 2.0))
         return err(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
     sync_mode(h);
+    pmg::Trace tr("pmg_phier_pcg_solve");
     return on_stream(h, stream, [&](cudaStream_t s) {
         return pcg_solve_on(h, f, u, eps, maxiter, tau, precond, rho, hist, iters, converged, s);
     });
@@ -1113,6 +1128,11 @@ int pmg_phier_dot(pmg_phier *h, int level, const double *const *a, const double 
 }
 
 long long pmg_phier_replayed_launches(const pmg_phier *h) { return h ? h->replayed : -1; }
+
+int pmg_phier_cycle_times(const pmg_phier *h, double *ms, int cap) {
+    if (!h || (cap > 0 && !ms)) return -1;
+    return h->clock.copy_out(ms, cap);
+}
 long long pmg_phier_exchanges(const pmg_phier *h) { return h ? h->exchanges : -1; }
 
 }  // extern "C"

@@ -32,6 +32,7 @@ from .partition import (Decomposition, DistField, LevelLayout, _dist, _stream, c
                         distribute, dist_norm, halo_exchange, reduce_parts, scalar_buffer)
 from .smoother import BLACK, RED, LineSmoother
 from .stencil import PanelOperator
+from .tracing import nvtx_range, tracing_enabled
 
 POLICIES = ("standard", "shallow", "very_shallow", "explicit")
 
@@ -400,6 +401,11 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
     prolongation into red cells (the post-smoothing red half-sweep overwrites
     them without reading them).
     """
+    with nvtx_range(f"level {c}"):
+        _v_cycle_level(hier, cfg, scratch, c, first)
+
+
+def _v_cycle_level(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int, first: bool) -> None:
     lev = hier.levels[c]
     s = scratch[c]
     lean = cfg.fused and cfg.rho == 1.0
@@ -483,8 +489,17 @@ class _CycleGraph:
             fine.op.residual_norm2_dev(s0.f, s0.u, None, self.res)
         self.launches = lib().pmg_launch_count() - l0   # library kernels per replay
 
-    def replay(self) -> torch.Tensor:
+    def replay(self, clock: list | None = None) -> torch.Tensor:
+        """One cycle; ``clock`` (tracing): append its device milliseconds."""
+        if clock is None:
+            self.graph.replay()
+            return self.res
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
         self.graph.replay()
+        b.record()
+        b.synchronize()
+        clock.append(a.elapsed_time(b))
         return self.res
 
 
@@ -518,7 +533,18 @@ def _mg_solve_native(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out):
     history = hist[:iters.value + 1].tolist()
     if out is None:
         u = u.copy()
-    return u, SolveReport(iters.value, history, bool(conv.value), wall, _echo(hier, cfg))
+    return u, SolveReport(iters.value, history, bool(conv.value), wall, _echo(hier, cfg),
+                          cycle_times_ms=_cycle_times(nh._lib.pmg_hier_cycle_times, nh.h))
+
+
+def _cycle_times(fn, h) -> list:
+    """Per-cycle device times of a driver's last solve (empty when untraced)."""
+    n = int(fn(h, None, 0))
+    if n <= 0:
+        return []
+    buf = np.zeros(n)
+    fn(h, buf.ctypes.data_as(C.c_void_p), n)
+    return buf.tolist()
 
 
 def _parts_native_ok(hier: LevelHierarchy, cfg: MGConfig) -> bool:
@@ -550,7 +576,8 @@ def _mg_solve_parts(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out):
     history = hist[:iters.value + 1].tolist()
     if out is None:
         u = u.copy()
-    return u, SolveReport(iters.value, history, bool(conv.value), wall, _echo(hier, cfg))
+    return u, SolveReport(iters.value, history, bool(conv.value), wall, _echo(hier, cfg),
+                          cycle_times_ms=_cycle_times(nh._lib.pmg_phier_cycle_times, nh.h))
 
 
 def _ptrs(df: DistField):
@@ -611,16 +638,18 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
         u.fill(0.0)
     res = scalar_buffer(len(u.parts))
     converged = False
+    clock = [] if tracing_enabled() else None
     torch.cuda.current_stream().synchronize()
     t0 = time.perf_counter()
     for it in range(cfg.maxiter):
         first = lean_first and it == 0
-        if use_graph:
-            rr = graphs[first].replay()
-        else:
-            v_cycle(hier, cfg, scratch, first=first)
-            hier.fine.op.residual_norm2_dev(f, u, None, res)
-            rr = res
+        with nvtx_range(f"cycle {it + 1}"):
+            if use_graph:
+                rr = graphs[first].replay(clock)
+            else:
+                v_cycle(hier, cfg, scratch, first=first)
+                hier.fine.op.residual_norm2_dev(f, u, None, res)
+                rr = res
         rnorm = math.sqrt(reduce_parts(rr))
         history.append(rnorm)
         if rnorm / r0 < cfg.eps:
@@ -629,4 +658,5 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
     wall = time.perf_counter() - t0
     if out is None:
         u = u.copy()
-    return u, SolveReport(len(history) - 1, history, converged, wall, echo)
+    return u, SolveReport(len(history) - 1, history, converged, wall, echo,
+                          cycle_times_ms=clock or [])

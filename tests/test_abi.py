@@ -61,3 +61,20 @@ def test_sm100a_cubin():
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_tracing_switch_without_gpu():
+    """The tracing mode is host state: set, read back, refused out of range,
+    and a null driver handle reports -1 cycle times."""
+    import paper_1307_2036_b200 as pmg
+    from paper_1307_2036_b200 import _lib
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libpmg.so not built")
+    lib = _lib.load()
+    assert not pmg.tracing_enabled()
+    with pmg.tracing():
+        assert pmg.tracing_enabled() and lib.pmg_get_tracing() == 1
+    assert not pmg.tracing_enabled()
+    assert lib.pmg_set_tracing(2) == _lib.PMG_ERR_VALUE
+    assert lib.pmg_hier_cycle_times(None, None, 0) == -1
+    assert lib.pmg_phier_cycle_times(None, None, 0) == -1

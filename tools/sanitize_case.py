@@ -1,7 +1,8 @@
 """Small workloads of the hand-rolled synchronisation kernels for
 compute-sanitizer (tests/test_sanitizers.py): the TMA band half-sweep (8 and
 16 compute warps: mbarrier rings, named barriers), its fused-residual and
-<f, u> modes, tile regions, and a configs[0] MG + CG solve.
+<f, u> modes, tile regions, the variable-coefficient band kernel, and a
+configs[0] MG + CG solve.
 
     python tools/sanitize_case.py band|solve
 """
@@ -43,6 +44,24 @@ def band():
                       C.c_void_p(scr.data_ptr()), C.c_void_p(res.data_ptr()), st)
         z = pmg.DistField.zeros(op.layout, 128)
         _lib.call("pmg_ssor_apply", h.h, f.parts[w].ptr, z.parts[w].ptr, 1.0, 1, 1,
+                  C.c_void_p(scr.data_ptr()), C.c_void_p(res.data_ptr()), st)
+    # the variable-coefficient band kernel (thread-0 TMA issue after the CTA
+    # barrier): plain, zero-neighbour, fused-residual modes and a region
+    prob = configs.Problem(256, 16, 128, 1e-3, 1.0, 3, stretch=1.05, variable_omega=True)
+    op = pmg.PanelOperator(prob.grid(), prob.params(), pmg.Decomposition(256, 1, ny=16).layout(256))
+    (w, h), = op.handles.items()
+    rng = np.random.default_rng(2)
+    u = pmg.scatter_owned(rng.uniform(-1, 1, (256, 16, 128)), op.layout)
+    pmg.halo_exchange(u)
+    f = pmg.scatter_owned(rng.uniform(-1, 1, (256, 16, 128)), op.layout)
+    un = u.copy()
+    for color in (0, 1):
+        _lib.call("pmg_half_sweep", h.h, u.parts[w].ptr, f.parts[w].ptr, color, 1.0, 0, 0, 1.0, st)
+    _lib.call("pmg_half_sweep", h.h, u.parts[w].ptr, f.parts[w].ptr, 0, 1.0, 0, 1, 1.0, st)
+    _lib.call("pmg_half_sweep_region", h.h, u.parts[w].ptr, f.parts[w].ptr, 1, 1.0, 0, 0, 1.0,
+              1, 1, 2, 1, 1, 14, st)
+    if lib.pmg_half_sweep_res_ok(h.h):
+        _lib.call("pmg_half_sweep_res", h.h, u.parts[w].ptr, un.parts[w].ptr, f.parts[w].ptr,
                   C.c_void_p(scr.data_ptr()), C.c_void_p(res.data_ptr()), st)
     torch.cuda.synchronize()
     print("band ok")
