@@ -137,6 +137,14 @@ static int solve_parts(FILE *in, const int *hdr, const double *par, const char *
             }
             parts[w].nbr[a] = (ni < 0 || ni >= PX || nj < 0 || nj >= PY) ? -1 : ni * PY + nj;
         }
+        for (int a = 0; a < 4; ++a) {         /* SW, SE, NW, NE */
+            int ni = wi + (a & 1 ? 1 : -1), nj = wj + (a & 2 ? 1 : -1);
+            if (periodic) {
+                ni = (ni + PX) % PX;
+                nj = (nj + PY) % PY;
+            }
+            parts[w].diag[a] = (ni < 0 || ni >= PX || nj < 0 || nj >= PY) ? -1 : ni * PY + nj;
+        }
     }
     pmg_mg_desc md = {1, 1, 1, 1.0, periodic, periodic, 1, 1};
     pmg_phier *h;

@@ -364,6 +364,8 @@ typedef struct pmg_phier pmg_phier;   /* opaque */
 typedef struct pmg_part_desc {
     int worker;   /* worker id; with a communicator: this rank */
     int nbr[4];   /* worker across the W, E, S, N face; -1: physical boundary (mirror) */
+    int diag[4];  /* worker across the SW, SE, NW, NE corner; >= 0 exactly where both
+                   * adjacent faces have a neighbour (the y neighbour of the x neighbour) */
 } pmg_part_desc;
 /* 1 if libnccl.so.2 can be loaded (resolved at run time; no link dependency) */
 int pmg_comm_available(void);
@@ -372,11 +374,22 @@ int pmg_comm_unique_id(void *id128);
 /* communicator of nranks ranks on the current device (ncclCommInitRank) */
 int pmg_comm_create(const void *id128, int nranks, int rank, pmg_comm **out);
 int pmg_comm_destroy(pmg_comm *comm);
-/* one phase's ordered message plan of a part with neighbours nbr[4]
- * (phase 0: W/E faces, 1: S/N faces including the corners): ops[3 * n] =
- * 0 send / 1 receive, ops[3 * n + 1] = face, ops[3 * n + 2] = peer worker;
- * at most 4 ops.  [send a, recv b, send b, recv a]: messages to one peer
- * pair up under NCCL's in-order matching.  Host only. */
+/* The multi-part drivers' halo exchange is ONE phase: the four face strips
+ * (the y strips over the extended range, whose end columns carry the
+ * sender's mirrored boundary column at a physical x boundary) and the four
+ * corner columns from the diagonal parts travel in one NCCL group, between
+ * one pack and one unpack launch; the ring then holds what the two-phase
+ * exchange of partition.py:158-191 leaves there, bit for bit.
+ * pmg_exchange_plan8: its ordered message plan for a part with neighbours
+ * nbr8[8] = W, E, S, N, SW, SE, NW, NE (-1 none): ops[3 * n] = 0 send /
+ * 1 receive, ops[3 * n + 1] = direction (side of the part), ops[3 * n + 2] =
+ * peer worker; at most 16 ops.  Per direction d [send d, recv opposite(d)]:
+ * the messages two parts exchange pair up under NCCL's in-order matching per
+ * peer for every grid.  Host only.
+ * pmg_exchange_plan: one phase of the two-phase plan the Python multi-rank
+ * path posts (phase 0: W/E faces, 1: S/N faces including the corners; at
+ * most 4 ops, [send a, recv b, send b, recv a]).  Host only. */
+int pmg_exchange_plan8(const int *nbr8, int *ops, int *nops);
 int pmg_exchange_plan(const int *nbr, int phase, int *ops, int *nops);
 /* levels[p * nlev + c]: part p (ascending worker order), level c (finest
  * first, halving nx and ny) */

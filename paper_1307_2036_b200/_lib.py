@@ -29,7 +29,7 @@ class MGDesc(C.Structure):
 
 
 class PartDesc(C.Structure):
-    _fields_ = [("worker", C.c_int), ("nbr", C.c_int * 4)]
+    _fields_ = [("worker", C.c_int), ("nbr", C.c_int * 4), ("diag", C.c_int * 4)]
 
 
 class LevelDesc(C.Structure):
@@ -121,6 +121,7 @@ SIGNATURES = {
     "pmg_comm_create": (_I, [_P, _I, _I, C.POINTER(_P)]),
     "pmg_comm_destroy": (_I, [_P]),
     "pmg_exchange_plan": (_I, [C.POINTER(_I), _I, C.POINTER(_I), C.POINTER(_I)]),
+    "pmg_exchange_plan8": (_I, [C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "pmg_phier_create": (_I, [C.POINTER(_P), _I, _I, C.POINTER(PartDesc), C.POINTER(MGDesc), _P,
                               _I, C.POINTER(_P)]),
     "pmg_phier_destroy": (_I, [_P]),

@@ -124,81 +124,127 @@ __global__ void k_sum_ordered(const double *__restrict__ v, int n, double *__res
 }
 
 constexpr int OPP[4] = {1, 0, 3, 2};
+// directions of the single-phase exchange: W, E, S, N, SW, SE, NW, NE; a
+// strip sent towards d lands in the receiver's halo on side OPP8[d]
+constexpr int OPP8[8] = {1, 0, 3, 2, 7, 6, 5, 4};
 
-// ---- exchange kernels: one launch per phase for both faces of every part
+// ---- exchange kernels: ONE launch fills the whole halo ring of every part
+// (x faces, y faces and the four corner columns).  The two-phase exchange of
+// partition.py:158-191 -- x faces, then y faces over the extended range --
+// gives corner (a, b) the value found by resolving x first (the a-side
+// neighbour's column, or the mirrored own column at a physical boundary) and
+// then y on the part reached; both kernels below read that cell directly, so
+// the ring holds the two-phase exchange's values bit for bit.
 constexpr int MAXP = 16;   // in-process parts per hierarchy
 
-// in-process: halo face of part p <- owned boundary strip of its neighbour
-// part (the opposite face, same position) or its own mirror; blockIdx.z =
-// 2 p + face of the phase.  Reads only owned cells (phase 0) or the rows
-// that phase 0 completed (phase 1: the y strips' corner cells), writes only
-// halo cells of this phase's faces: race-free within the launch.
+// in-process: halo cell of part p <- the owned cell it images; blockIdx.z =
+// 4 p + face (faces 2, 3 cover the extended range -1 .. nx: the corners).
+// Reads only owned cells, writes only halo cells: race-free within the launch.
 struct LocalX {
-    int np, phase, len;
+    int np;
     pmg::Lvl L[MAXP];
     double *u[MAXP];
     int nbr[MAXP][4];   // local part index, -1 mirror
 };
 
 __global__ void k_halo_local(const __grid_constant__ LocalX x) {
-    const int p = blockIdx.z >> 1, face = 2 * x.phase + (blockIdx.z & 1);
+    const int p = blockIdx.z >> 2, face = blockIdx.z & 3;
     const pmg::Lvl &L = x.L[p];
     const int len = face < 2 ? L.ny : L.nx + 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
     if (t >= len) return;
-    int i, j, si, sj;
+    int i, j;
     pmg::face_pos(L, face, t, true, i, j);
-    const int q = x.nbr[p][face];
-    double v;
-    if (q < 0) {
-        pmg::face_pos(L, face, t, false, si, sj);
-        v = x.u[p][pmg::cell(L, si, sj, k)];
-    } else {
-        const pmg::Lvl &Q = x.L[q];
-        pmg::face_pos(Q, face ^ 1, t, false, si, sj);   // the opposite face
-        v = x.u[q][pmg::cell(Q, si, sj, k)];
+    int sp = p, si = i, sj = j;
+    if (i < 0) {
+        const int q = x.nbr[sp][0];
+        si = q >= 0 ? L.nx - 1 : 0;
+        if (q >= 0) sp = q;
+    } else if (i >= L.nx) {
+        const int q = x.nbr[sp][1];
+        si = q >= 0 ? 0 : L.nx - 1;
+        if (q >= 0) sp = q;
     }
-    x.u[p][pmg::cell(L, i, j, k)] = v;
+    if (j < 0) {
+        const int q = x.nbr[sp][2];
+        sj = q >= 0 ? L.ny - 1 : 0;
+        if (q >= 0) sp = q;
+    } else if (j >= L.ny) {
+        const int q = x.nbr[sp][3];
+        sj = q >= 0 ? 0 : L.ny - 1;
+        if (q >= 0) sp = q;
+    }
+    x.u[p][pmg::cell(L, i, j, k)] = x.u[sp][pmg::cell(x.L[sp], si, sj, k)];
 }
 
-// one part's two faces of a phase into / out of its message buffers
-// (layout of pmg_pack_face: buf[k * len + t]); blockIdx.z = face of the phase
+// one part's boundary strips into / out of its eight message buffers:
+// faces W, E (ny x nz, buf[k * ny + j]), S, N ((nx + 2) x nz over the
+// extended range, buf[k * (nx + 2) + i + 1]) and corners SW, SE, NW, NE (nz).
+// blockIdx.z = face.  An extended position of a y strip carries the sender's
+// mirrored boundary column where its x side is a physical boundary (what
+// the two-phase exchange's y strips carry there); next to an x neighbour it
+// is unused -- that corner travels as its own message from the diagonal part.
 struct FaceX {
     pmg::Lvl L;
     double *u;
-    double *buf[2];
-    int use[2];     // pack: face has a neighbour; unpack: 1 buffer, 2 mirror, 0 skip
-    int phase;
+    double *buf[8];
+    int nbr[8];     // peer worker per direction, -1 none
 };
 
-__global__ void k_pack_phase(const __grid_constant__ FaceX x) {
-    const int fs = blockIdx.z, face = 2 * x.phase + fs;
-    if (!x.use[fs]) return;
-    const int len = face < 2 ? x.L.ny : x.L.nx + 2;
+__global__ void k_pack_all(const __grid_constant__ FaceX x) {
+    const int face = blockIdx.z;
+    if (x.nbr[face] < 0) return;
+    const pmg::Lvl &L = x.L;
+    const int len = face < 2 ? L.ny : L.nx + 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
     if (t >= len) return;
     int i, j;
-    pmg::face_pos(x.L, face, t, false, i, j);
-    x.buf[fs][(long long)k * len + t] = x.u[pmg::cell(x.L, i, j, k)];
+    pmg::face_pos(L, face, t, false, i, j);
+    if (face >= 2 && (i < 0 || i >= L.nx)) {
+        const int a = i < 0 ? 0 : 1;
+        if (x.nbr[a] >= 0) return;             // the diagonal part's message
+        i = i < 0 ? 0 : L.nx - 1;              // mirrored own column
+    }
+    const double v = x.u[pmg::cell(L, i, j, k)];
+    x.buf[face][(long long)k * len + t] = v;
+    if (face >= 2 && (i == 0 || i == L.nx - 1) && t >= 1 && t <= L.nx) {
+        // the owned corner column also travels to the diagonal neighbour
+        if (i == 0) {
+            const int d = 4 + 2 * (face - 2);
+            if (x.nbr[d] >= 0) x.buf[d][k] = v;
+        }
+        if (i == L.nx - 1) {
+            const int d = 5 + 2 * (face - 2);
+            if (x.nbr[d] >= 0) x.buf[d][k] = v;
+        }
+    }
 }
 
-__global__ void k_unpack_phase(const __grid_constant__ FaceX x) {
-    const int fs = blockIdx.z, face = 2 * x.phase + fs;
-    if (!x.use[fs]) return;
-    const int len = face < 2 ? x.L.ny : x.L.nx + 2;
+__global__ void k_unpack_all(const __grid_constant__ FaceX x) {
+    const int face = blockIdx.z;
+    const pmg::Lvl &L = x.L;
+    const int len = face < 2 ? L.ny : L.nx + 2;
     const int t = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
     if (t >= len) return;
     int i, j;
-    pmg::face_pos(x.L, face, t, true, i, j);
+    pmg::face_pos(L, face, t, true, i, j);
     double v;
-    if (x.use[fs] == 2) {
-        int si, sj;
-        pmg::face_pos(x.L, face, t, false, si, sj);
-        v = x.u[pmg::cell(x.L, si, sj, k)];
+    if (face < 2) {
+        v = x.nbr[face] >= 0 ? x.buf[face][(long long)k * L.ny + j]
+                             : x.u[pmg::cell(L, face == 0 ? 0 : L.nx - 1, j, k)];
+    } else if (i >= 0 && i < L.nx) {
+        v = x.nbr[face] >= 0 ? x.buf[face][(long long)k * (L.nx + 2) + t]
+                             : x.u[pmg::cell(L, i, face == 2 ? 0 : L.ny - 1, k)];
     } else {
-        v = x.buf[fs][(long long)k * len + t];
+        // corner (a, face): x first, then y on the part reached
+        const int a = i < 0 ? 0 : 1, d = 4 + 2 * (face - 2) + a;
+        const int jb = face == 2 ? 0 : L.ny - 1;
+        if (x.nbr[a] >= 0 && x.nbr[face] >= 0) v = x.buf[d][k];
+        else if (x.nbr[face] >= 0) v = x.buf[face][(long long)k * (L.nx + 2) + t];
+        else if (x.nbr[a] >= 0) v = x.buf[a][(long long)k * L.ny + jb];
+        else v = x.u[pmg::cell(L, a == 0 ? 0 : L.nx - 1, jb, k)];
     }
-    x.u[pmg::cell(x.L, i, j, k)] = v;
+    x.u[pmg::cell(L, i, j, k)] = v;
 }
 
 dim3 face_grid(const pmg::Lvl &L, int nz, int z) {
@@ -219,9 +265,10 @@ namespace {
 struct PL {
     const pmg_level *lv = nullptr;
     double *u = nullptr, *f = nullptr;   // level >= 1: owned; level 0: the caller's
-    double *sb[4] = {nullptr, nullptr, nullptr, nullptr};   // packed own faces
-    double *rb[4] = {nullptr, nullptr, nullptr, nullptr};   // received halo faces (NCCL)
-    long long fd[4] = {0, 0, 0, 0};                         // face doubles
+    // NCCL message buffers per direction (W, E, S, N, SW, SE, NW, NE): the
+    // packed own strips, the received halo strips, and their doubles
+    double *sb[8] = {}, *rb[8] = {};
+    long long fd[8] = {};
     int nx = 0, ny = 0, nz = 0;
 };
 
@@ -240,6 +287,7 @@ struct pmg_phier {
     int np = 0, nlev = 0;
     std::vector<int> worker;                  // per local part, ascending
     std::vector<std::array<int, 4>> nbr;      // per local part: W, E, S, N worker or -1
+    std::vector<std::array<int, 4>> diag;     // per local part: SW, SE, NW, NE worker or -1
     std::vector<int> local;                   // worker -> local part index or -1
     std::vector<std::vector<PL>> P;           // [part][level]
     pmg_mg_desc d{};
@@ -276,7 +324,7 @@ void free_phier(pmg_phier *h) {
                 cudaFree(q.u);
                 cudaFree(q.f);
             }
-            for (int a = 0; a < 4; ++a) {
+            for (int a = 0; a < 8; ++a) {
                 cudaFree(q.sb[a]);
                 cudaFree(q.rb[a]);
             }
@@ -307,71 +355,69 @@ const pmg_level *LV(const pmg_phier *h, int p, int c) {
     return h->P[p][c].lv;
 }
 
-// halo exchange of level c's fields x[p] (partition.py:158-191): x faces,
-// then y faces over the extended range (corners), periodic neighbours or
-// mirrored physical boundaries, on stream s.  Per phase: in-process, one
-// launch for every part's two faces; with a communicator, one pack launch,
-// one NCCL group, one unpack launch.
+// halo exchange of level c's fields x[p] (partition.py:158-191: x faces,
+// then y faces over the extended range, periodic neighbours or mirrored
+// physical boundaries) as ONE phase on stream s: in-process, one launch
+// fills every part's halo ring; with a communicator, one pack launch, one
+// NCCL group carrying the four faces and the four corner columns (the plan
+// of pmg_exchange_plan8), one unpack launch.
 int exchange(pmg_phier *h, int c, double *const *x, cudaStream_t s) {
     pmg::Trace tr("halo exchange level %d", c);
     ++h->exchanges;
-    const PL &q0 = h->P[0][c];
-    for (int phase = 0; phase < 2; ++phase) {
-        const int fa = 2 * phase;
-        if (!h->comm) {
-            LocalX lx;
-            lx.np = h->np;
-            lx.phase = phase;
-            lx.len = 0;
-            for (int p = 0; p < h->np; ++p) {
-                lx.L[p] = pmg::level_lvl(LV(h, p, c));
-                lx.u[p] = x[p];
-                for (int a = 0; a < 4; ++a) {
-                    const int nb = h->nbr[p][a];
-                    lx.nbr[p][a] = nb < 0 ? -1 : h->local[nb];
-                }
+    const PL &q = h->P[0][c];
+    if (!h->comm) {
+        LocalX lx;
+        lx.np = h->np;
+        for (int p = 0; p < h->np; ++p) {
+            lx.L[p] = pmg::level_lvl(LV(h, p, c));
+            lx.u[p] = x[p];
+            for (int a = 0; a < 4; ++a) {
+                const int nb = h->nbr[p][a];
+                lx.nbr[p][a] = nb < 0 ? -1 : h->local[nb];
             }
-            k_halo_local<<<face_grid(lx.L[0], q0.nz, 2 * h->np), 128, 0, s>>>(lx);
-            pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
-            TRYC(cudaGetLastError(), "halo exchange");
-            continue;
         }
-        // one part (this rank's)
-        const PL &q = h->P[0][c];
-        FaceX fx;
-        fx.L = pmg::level_lvl(LV(h, 0, c));
-        fx.u = x[0];
-        fx.phase = phase;
-        for (int fs = 0; fs < 2; ++fs) {
-            fx.buf[fs] = q.sb[fa + fs];
-            fx.use[fs] = h->nbr[0][fa + fs] >= 0;
-        }
-        k_pack_phase<<<face_grid(fx.L, q.nz, 2), 128, 0, s>>>(fx);
+        k_halo_local<<<face_grid(lx.L[0], q.nz, 4 * h->np), 128, 0, s>>>(lx);
         pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
-        TRYC(cudaGetLastError(), "pack");
-        const Nccl *n = nccl();
+        TRYC(cudaGetLastError(), "halo exchange");
+        return PMG_OK;
+    }
+    // one part (this rank's)
+    FaceX fx;
+    fx.L = pmg::level_lvl(LV(h, 0, c));
+    fx.u = x[0];
+    int nbr8[8];
+    for (int a = 0; a < 4; ++a) {
+        nbr8[a] = h->nbr[0][a];
+        nbr8[4 + a] = h->diag[0][a];
+    }
+    for (int a = 0; a < 8; ++a) {
+        fx.buf[a] = q.sb[a];
+        fx.nbr[a] = nbr8[a];
+    }
+    k_pack_all<<<face_grid(fx.L, q.nz, 4), 128, 0, s>>>(fx);
+    pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
+    TRYC(cudaGetLastError(), "pack");
+    const Nccl *n = nccl();
+    int ops[48], nops = 0;
+    TRY(pmg_exchange_plan8(nbr8, ops, &nops));
+    if (nops) {
         TRYN(n->group_start(), "ncclGroupStart");
-        int ops[12], nops = 0;
-        TRY(pmg_exchange_plan(h->nbr[0].data(), phase, ops, &nops));
         for (int o = 0; o < nops; ++o) {
-            const int kind = ops[3 * o], face = ops[3 * o + 1], peer = ops[3 * o + 2];
+            const int kind = ops[3 * o], dir = ops[3 * o + 1], peer = ops[3 * o + 2];
             ncclResult_t r = kind == 0
-                ? n->send(q.sb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s)
-                : n->recv(q.rb[face], (size_t)q.fd[face], ncclDouble, peer, h->comm->c, s);
+                ? n->send(q.sb[dir], (size_t)q.fd[dir], ncclDouble, peer, h->comm->c, s)
+                : n->recv(q.rb[dir], (size_t)q.fd[dir], ncclDouble, peer, h->comm->c, s);
             if (r != ncclSuccess) {
                 n->group_end();
                 return nccl_err(r, kind == 0 ? "ncclSend" : "ncclRecv");
             }
         }
         TRYN(n->group_end(), "ncclGroupEnd");
-        for (int fs = 0; fs < 2; ++fs) {
-            fx.buf[fs] = q.rb[fa + fs];
-            fx.use[fs] = h->nbr[0][fa + fs] >= 0 ? 1 : 2;
-        }
-        k_unpack_phase<<<face_grid(fx.L, q.nz, 2), 128, 0, s>>>(fx);
-        pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
-        TRYC(cudaGetLastError(), "unpack");
     }
+    for (int a = 0; a < 8; ++a) fx.buf[a] = q.rb[a];
+    k_unpack_all<<<face_grid(fx.L, q.nz, 4), 128, 0, s>>>(fx);
+    pmg::g_launches.fetch_add(1, std::memory_order_relaxed);
+    TRYC(cudaGetLastError(), "unpack");
     return PMG_OK;
 }
 
@@ -924,6 +970,31 @@ int pmg_exchange_plan(const int *nbr, int phase, int *ops, int *nops) {
     return PMG_OK;
 }
 
+int pmg_exchange_plan8(const int *nbr8, int *ops, int *nops) {
+    if (!nbr8 || !ops || !nops) return err(PMG_ERR_VALUE, "exchange_plan8: bad arguments");
+    // per direction d (W, E, S, N, SW, SE, NW, NE): send the strip of side d
+    // to the part there, receive the halo of the opposite side from the part
+    // there.  Part A's sends to B, in this order, are the directions d with
+    // A + d = B; B's receives from A are the sides OPP8[d] of the same d's in
+    // the same order -- they pair up under NCCL's in-order matching per peer
+    // whatever the grid (2 parts along a periodic axis, a part that is its
+    // own neighbour, diagonal neighbours that coincide with face neighbours)
+    int n = 0;
+    for (int d = 0; d < 8; ++d) {
+        if (nbr8[d] >= 0) {
+            ops[3 * n] = 0, ops[3 * n + 1] = d, ops[3 * n + 2] = nbr8[d];
+            ++n;
+        }
+        const int r = OPP8[d];
+        if (nbr8[r] >= 0) {
+            ops[3 * n] = 1, ops[3 * n + 1] = r, ops[3 * n + 2] = nbr8[r];
+            ++n;
+        }
+    }
+    *nops = n;
+    return PMG_OK;
+}
+
 int pmg_comm_available(void) { return nccl() ? 1 : 0; }
 
 int pmg_comm_unique_id(void *id) {
@@ -981,6 +1052,14 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
             return err(PMG_ERR_VALUE, "parts must be listed in ascending worker order");
         maxw = std::max(maxw, parts[p].worker);
         for (int a = 0; a < 4; ++a) maxw = std::max(maxw, parts[p].nbr[a]);
+        for (int a = 0; a < 4; ++a) {
+            // diagonal a = SW, SE, NW, NE lies across x side (a & 1) and y side 2 + (a >> 1)
+            maxw = std::max(maxw, parts[p].diag[a]);
+            const bool both = parts[p].nbr[a & 1] >= 0 && parts[p].nbr[2 + (a >> 1)] >= 0;
+            if (both != (parts[p].diag[a] >= 0))
+                return err(PMG_ERR_VALUE, "a part has a diagonal neighbour exactly where it has "
+                                          "both face neighbours (pmg_part_desc.diag)");
+        }
     }
     if (comm && maxw >= comm->nranks)
         return err(PMG_ERR_VALUE, "a neighbour worker is not a rank of the communicator");
@@ -995,6 +1074,7 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
     for (int p = 0; p < nparts; ++p) {
         h->worker.push_back(parts[p].worker);
         h->nbr.push_back({parts[p].nbr[0], parts[p].nbr[1], parts[p].nbr[2], parts[p].nbr[3]});
+        h->diag.push_back({parts[p].diag[0], parts[p].diag[1], parts[p].diag[2], parts[p].diag[3]});
         h->local[parts[p].worker] = p;
     }
     if (!comm)
@@ -1009,6 +1089,17 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
                 if (nb >= 0 && h->nbr[h->local[nb]][OPP[a]] != parts[p].worker) {
                     free_phier(h);
                     return err(PMG_ERR_VALUE, "neighbour relation is not symmetric");
+                }
+            }
+    if (!comm)   // the in-process exchange walks x then y: the diagonals must agree
+        for (int p = 0; p < nparts; ++p)
+            for (int a = 0; a < 4; ++a) {
+                const int nx_ = h->nbr[p][a & 1];
+                if (h->diag[p][a] >= 0 &&
+                    h->nbr[h->local[nx_]][2 + (a >> 1)] != h->diag[p][a]) {
+                    free_phier(h);
+                    return err(PMG_ERR_VALUE, "diagonal neighbour is not the y neighbour of the "
+                                              "x neighbour");
                 }
             }
     h->P.assign(nparts, std::vector<PL>(nlev));
@@ -1041,9 +1132,9 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
                 if (e == cudaSuccess) e = cudaMalloc(&q.f, sizeof(double) * nd);
                 if (e == cudaSuccess) e = cudaMemset(q.u, 0, sizeof(double) * nd);
             }
-            for (int a = 0; a < 4 && e == cudaSuccess; ++a) {
-                q.fd[a] = pmg_face_doubles(q.lv, a);
-                if (h->nbr[p][a] < 0 || !comm) continue;
+            for (int a = 0; a < 8 && e == cudaSuccess; ++a) {
+                q.fd[a] = a < 4 ? pmg_face_doubles(q.lv, a) : q.nz;
+                if ((a < 4 ? h->nbr[p][a] : h->diag[p][a - 4]) < 0 || !comm) continue;
                 e = cudaMalloc(&q.sb[a], sizeof(double) * q.fd[a]);
                 if (e == cudaSuccess) e = cudaMalloc(&q.rb[a], sizeof(double) * q.fd[a]);
             }

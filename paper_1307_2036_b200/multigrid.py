@@ -245,6 +245,9 @@ class NativePartsHierarchy:
             for face, (di, dj) in enumerate(((-1, 0), (1, 0), (0, -1), (0, 1))):
                 nb = lay.neighbor(w, di, dj)
                 parts[n].nbr[face] = -1 if nb is None else nb
+            for corner, (di, dj) in enumerate(((-1, -1), (1, -1), (-1, 1), (1, 1))):
+                nb = lay.neighbor(w, di, dj)
+                parts[n].diag[corner] = -1 if nb is None else nb
         per = int(bool(lay.periodic))
         d = MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), float(cfg.rho), per,
                    per, int(bool(cfg.lagged_norm)), int(bool(cfg.red_restrict)))

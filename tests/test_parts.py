@@ -1,16 +1,19 @@
 """Host logic of the native multi-part driver (pmg_parts.cu), on CPU:
 
-* ``pmg_exchange_plan`` -- the ordered NCCL message plan each rank posts
-  inside one ncclGroupStart/End per exchange phase -- is consistent across
-  ranks for every process grid the configs use (1x1, 2x1, 1x2, 2x2, 4x2,
-  4x4; periodic and mirror): for every ordered pair of ranks, the strips A
-  sends to B, in order, are exactly the strips B expects from A, in order,
-  face for face (NCCL matches point-to-point messages between two ranks in
-  posting order), and it equals the Python driver's plan
-  (partition.exchange_plan);
-* the same plans executed by world-size-2 and -4 gloo process groups with a
+* ``pmg_exchange_plan8`` -- the ordered NCCL message plan each rank posts
+  inside the one ncclGroupStart/End of a (single-phase) halo exchange: four
+  face strips and four corner columns -- is consistent across ranks for
+  every process grid the configs use (1x1, 2x1, 1x2, 2x2, 4x2, 4x4;
+  periodic and mirror): for every ordered pair of ranks, the strips A sends
+  to B, in order, are exactly the strips B expects from A, in order, side
+  for opposite side (NCCL matches point-to-point messages between two ranks
+  in posting order);
+* ``pmg_exchange_plan`` -- one phase of the two-phase plan the Python
+  multi-rank path posts -- has the same property and equals
+  partition.exchange_plan;
+* both plans executed by world-size-2 and -4 gloo process groups with a
   single tag (so messages match in posting order, as under NCCL) deliver
-  every halo strip from the right neighbour face.
+  every halo strip from the right neighbour side.
 """
 
 import ctypes as C
@@ -23,8 +26,9 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 GRIDS = [(1, 1), (2, 1), (1, 2), (2, 2), (4, 2), (4, 4)]
-OPP = {0: 1, 1: 0, 2: 3, 3: 2}
+OPP = {0: 1, 1: 0, 2: 3, 3: 2, 4: 7, 5: 6, 6: 5, 7: 4}
 DIRS = ((-1, 0), (1, 0), (0, -1), (0, 1))
+DIRS8 = DIRS + ((-1, -1), (1, -1), (-1, 1), (1, 1))     # W E S N SW SE NW NE
 
 
 def _lib():
@@ -43,6 +47,45 @@ def neighbours(px, py, periodic):
         nb = [lay.neighbor(w, *d) for d in DIRS]
         out[w] = [-1 if n is None else n for n in nb]
     return lay, out
+
+
+def neighbours8(px, py, periodic):
+    lay, _ = neighbours(px, py, periodic)
+    out = {}
+    for w in lay.workers:
+        nb = [lay.neighbor(w, *d) for d in DIRS8]
+        out[w] = [-1 if n is None else n for n in nb]
+    return lay, out
+
+
+def c_plan8(L, nbr8):
+    ops = (C.c_int * 48)()
+    n = C.c_int()
+    L.call("pmg_exchange_plan8", (C.c_int * 8)(*nbr8), ops, C.byref(n))
+    return [tuple(ops[3 * i:3 * i + 3]) for i in range(n.value)]
+
+
+@pytest.mark.parametrize("periodic", [True, False])
+@pytest.mark.parametrize("px,py", GRIDS)
+def test_plan8_pairs_up_in_order(px, py, periodic):
+    L = _lib()
+    _, nbrs = neighbours8(px, py, periodic)
+    plans = {w: c_plan8(L, nbrs[w]) for w in nbrs}
+    for a in nbrs:
+        for b in nbrs:
+            sends = [d for kind, d, peer in plans[a] if kind == 0 and peer == b]
+            recvs = [d for kind, d, peer in plans[b] if kind == 1 and peer == a]
+            # the k-th strip A sends to B lands in B's k-th receive from A, in
+            # the halo side opposite to the strip's side
+            assert [OPP[d] for d in sends] == recvs, (a, b, sends, recvs)
+    for w, pl in plans.items():
+        # every side with a neighbour sends once and receives once
+        want = sorted(d for d in range(8) if nbrs[w][d] >= 0)
+        assert sorted(d for kind, d, _ in pl if kind == 1) == want
+        assert sorted(d for kind, d, _ in pl if kind == 0) == want
+        # a diagonal neighbour exists exactly where both faces have one
+        for c, (a, b) in enumerate(((0, 2), (1, 2), (0, 3), (1, 3))):
+            assert (nbrs[w][4 + c] >= 0) == (nbrs[w][a] >= 0 and nbrs[w][b] >= 0)
 
 
 def c_plan(L, nbr, phase):
@@ -89,6 +132,7 @@ def test_plan_rejects_bad_arguments():
     lib = L.load()
     assert lib.pmg_exchange_plan((C.c_int * 4)(0, 0, 0, 0), 2, ops, C.byref(n)) == L.PMG_ERR_VALUE
     assert lib.pmg_exchange_plan(None, 0, ops, C.byref(n)) == L.PMG_ERR_VALUE
+    assert lib.pmg_exchange_plan8(None, ops, C.byref(n)) == L.PMG_ERR_VALUE
 
 
 def _free_port():
@@ -106,10 +150,11 @@ def _worker(rank, world, port, px, py, periodic, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         dist.barrier()      # connect every pair before the point-to-point phase
         from paper_1307_2036_b200 import _lib as L
-        _, nbrs = neighbours(px, py, periodic)
+        _, nbrs = neighbours8(px, py, periodic)
         got = {}
-        for phase in (0, 1):
-            plan = c_plan(L, nbrs[rank], phase)
+        # the native driver's single-phase plan, then the Python path's two phases
+        for phase in (8, 0, 1):
+            plan = c_plan8(L, nbrs[rank]) if phase == 8 else c_plan(L, nbrs[rank][:4], phase)
             # strip content identifies (sender, face)
             bufs = {}
             ops = []
@@ -132,7 +177,7 @@ def _worker(rank, world, port, px, py, periodic, q):
                 for r in dist.batch_isend_irecv(ops):
                     r.wait()
             for face, t in bufs.items():
-                got[face] = float(t[0])
+                got[(phase == 8, face)] = float(t[0])
         q.put((rank, got, nbrs[rank]))
         dist.barrier()
         dist.destroy_process_group()
@@ -160,7 +205,8 @@ def test_plan_over_gloo_in_order(px, py, periodic):
     for p in procs:
         p.join(timeout=60)
     for rank, (got, nbr) in res.items():
-        for face, v in got.items():
-            # halo face `face` holds the neighbour's strip from the opposite face
-            assert v == 10.0 * nbr[face] + OPP[face], (rank, face, v)
-        assert sorted(got) == sorted(f for f in range(4) if nbr[f] >= 0)
+        for (single, face), v in got.items():
+            # halo side `face` holds the neighbour's strip from the opposite side
+            assert v == 10.0 * nbr[face] + OPP[face], (rank, single, face, v)
+        assert sorted(f for s1, f in got if not s1) == sorted(f for f in range(4) if nbr[f] >= 0)
+        assert sorted(f for s1, f in got if s1) == sorted(f for f in range(8) if nbr[f] >= 0)

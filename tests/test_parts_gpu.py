@@ -119,7 +119,7 @@ def test_native_parts_exact_mode(pmg):
     assert np.array_equal(got, ref)
 
 
-def _nccl_self_hier(pmg, hier, cfg, lagged=0):
+def _nccl_self_hier(pmg, hier, cfg, lagged=0, nbr=(0, 0, 0, 0)):
     from paper_1307_2036_b200 import _lib
     lib = _lib.load()
     if not lib.pmg_comm_available():
@@ -135,7 +135,8 @@ def _nccl_self_hier(pmg, hier, cfg, lagged=0):
     parts = (_lib.PartDesc * 1)()
     parts[0].worker = 0
     for a in range(4):
-        parts[0].nbr[a] = 0          # its own periodic neighbour, through NCCL
+        parts[0].nbr[a] = nbr[a]     # 0: its own periodic neighbour, through NCCL; -1: mirror
+        parts[0].diag[a] = 0 if nbr[a & 1] >= 0 and nbr[2 + (a >> 1)] >= 0 else -1
     d = _lib.MGDesc(cfg.nu_pre, cfg.nu_post, cfg.resolved_coarse_sweeps(), 1.0, 1, 1, lagged, 1)
     h = C.c_void_p()
     _lib.call("pmg_phier_create", arr, len(levels), 1, parts, C.byref(d), comm, 256,
@@ -261,3 +262,83 @@ def test_native_parts_pcg(pmg, nx, ny, px, py, periodic, precond):
     h, h1 = np.array(rn.residual_history), np.array(r1.residual_history)
     assert np.max(np.abs(h - h1) / (h1 + 1e-13 * h1[0])) <= 1e-10
     assert np.max(np.abs(un - u1)) <= 1e-10 * np.max(np.abs(u1))
+
+
+def _random_ring(pmg, lay, nz, seed):
+    """A field whose every double -- owned cells, halo ring, padding -- is random."""
+    v = pmg.DistField.zeros(lay, nz)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    for part in v.parts.values():
+        part.data.copy_(torch.rand(part.data.shape, dtype=torch.float64, device="cuda",
+                                   generator=g))
+    return v
+
+
+@pytest.mark.parametrize("nx,ny,nz,px,py,periodic", [
+    (64, 64, 8, 2, 2, True), (64, 64, 8, 2, 2, False), (64, 32, 8, 2, 1, True),
+    (64, 64, 8, 2, 1, False), (64, 64, 8, 1, 2, False), (128, 64, 8, 4, 2, True),
+    (128, 128, 8, 4, 2, False)])
+def test_single_phase_exchange_in_process(pmg, nx, ny, nz, px, py, periodic):
+    """The native driver's one-launch exchange (faces and corner columns
+    resolved x first, then y) leaves the whole halo ring as the two-phase
+    exchange of partition.py:158-191 (pack / unpack entry points, x faces
+    then y faces over the extended range) does, bit for bit."""
+    from paper_1307_2036_b200 import _lib
+    grid = (pmg.periodic_box(nx, nz, 0.01, ny=ny) if periodic
+            else pmg.panel_grid(nx, nz, flat_mode=True))
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=2)
+    dec = pmg.Decomposition(nx, px * py, ny=ny, px=px, py=py)
+    hier = pmg.build_hierarchy(grid, params, cfg, dec)
+    nh = hier.native_parts(cfg)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for level in (0, 1):
+        lay = hier.levels[level].layout
+        v = _random_ring(pmg, lay, nz, 11 + level)
+        ref = v.copy()
+        pmg.halo_exchange(ref)
+        _lib.call("pmg_phier_halo_exchange", nh.h, level, nh.ptrs(v), st)
+        for w in lay.local_workers:
+            assert torch.equal(v.parts[w].data, ref.parts[w].data), (level, w)
+
+
+@pytest.mark.parametrize("nbr", [(0, 0, 0, 0), (-1, -1, 0, 0), (0, 0, -1, -1), (-1, -1, -1, -1)])
+def test_single_phase_exchange_nccl_self(pmg, nbr):
+    """The NCCL form of the exchange (one pack, one group of up to 8 sends
+    and 8 receives, one unpack) with a one-rank communicator: the part is
+    its own neighbour across the sides marked 0 and mirrored across the
+    others -- every corner rule (diagonal message, the y strip's extended
+    position, the x strip's end, own cell) against the two-phase exchange
+    built from the pack / unpack entry points."""
+    from paper_1307_2036_b200 import _lib
+    nx, nz = 64, 8
+    grid = pmg.periodic_box(nx, nz, 0.01)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=2)
+    hier = pmg.build_hierarchy(grid, params, cfg)
+    lib, comm, h, w = _nccl_self_hier(pmg, hier, cfg, 0, nbr)
+    opp = (1, 0, 3, 2)
+    try:
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        for level in (0, 1):
+            lay = hier.levels[level].layout
+            v = _random_ring(pmg, lay, nz, 21 + level)
+            ref = v.copy()
+            part = ref.parts[w]
+            for faces in ((0, 1), (2, 3)):
+                for face in faces:
+                    if nbr[face] < 0:
+                        _lib.call("pmg_unpack_face", part.geom.h, part.ptr, face, None, 1, st)
+                        continue
+                    n = int(lib.pmg_face_doubles(part.geom.h, face))
+                    buf = torch.empty(n, dtype=torch.float64, device="cuda")
+                    _lib.call("pmg_pack_face", part.geom.h, part.ptr, opp[face],
+                              C.c_void_p(buf.data_ptr()), st)
+                    _lib.call("pmg_unpack_face", part.geom.h, part.ptr, face,
+                              C.c_void_p(buf.data_ptr()), 0, st)
+            vp = (C.c_void_p * 1)(v.parts[w].data.data_ptr())
+            _lib.call("pmg_phier_halo_exchange", h, level, vp, st)
+            assert torch.equal(v.parts[w].data, part.data), (level, nbr)
+    finally:
+        lib.pmg_phier_destroy(h)
+        lib.pmg_comm_destroy(comm)

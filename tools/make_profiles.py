@@ -85,7 +85,11 @@ for p in [os.path.join(GO, f"prof_{k}.ncu-rep") for k in CURRENT]:
         base = name.split("<")[0]
         if base not in traffic:
             traffic[base] = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
-    json.dump(traffic, open(os.path.join(PR, "ncu_traffic.json"), "w"), indent=1)
+    # merge: bench.py reads the "<kernel>@<nx>" entries of earlier captures
+    tp = os.path.join(PR, "ncu_traffic.json")
+    merged = json.load(open(tp)) if os.path.exists(tp) else {}
+    merged.update(traffic)
+    json.dump(merged, open(tp, "w"), indent=1)
 
 p = os.path.join(GO, "bench.json")
 if os.path.exists(p):
