@@ -31,3 +31,17 @@ for _ in range(int(os.environ.get("N", "3"))):
               C.c_void_p(torch.cuda.current_stream().cuda_stream))
 torch.cuda.synchronize()
 print("norm2", res.item())
+if os.environ.get("TIME"):          # CUDA-event mean over back-to-back launches
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = int(os.environ["TIME"])
+    e0.record(st)
+    for _ in range(n):
+        _lib.call("pmg_half_sweep_res", h, u.parts[w].ptr, un.parts[w].ptr, f.parts[w].ptr,
+                  C.c_void_p(scr.data_ptr()), C.c_void_p(res.data_ptr()),
+                  C.c_void_p(st.cuda_stream))
+    e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / n * 1e3
+    print(f"half_sweep_res nx={NX}: {us:.1f} us, {16 * NX * NX * 128 / us / 1e3:.0f} GB/s, "
+          f"checksum {float(un.parts[w].data.sum().item())!r}")
