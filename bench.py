@@ -395,6 +395,29 @@ def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
     from paper_1307_2036_b200 import multigrid as mgm
     lib = _lib.load()
     reps = []
+    fallback = None
+    if world > 1 and mgm.USE_NATIVE_PARTS:
+        # the first multi-rank solve sets up the library's own NCCL
+        # communicator and captures ncclSend / ncclRecv into the cycle
+        # graphs; if that fails on ANY rank, every rank falls back to the
+        # Python driver over torch.distributed (same kernels, same order,
+        # bit-identical iterates) and the line names the driver that ran
+        import torch.distributed as dist
+        ok, err = 1, ""
+        try:
+            s.u, rep = pmg.mg_solve(s.f, s.hier, s.cfg, out=s.u)
+            torch.cuda.synchronize()
+        except Exception as e:               # noqa: BLE001 -- reported below
+            ok, err = 0, f"{type(e).__name__}: {e}"
+        flag = torch.tensor([ok], dtype=torch.int32,
+                            device="cuda" if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            fallback = err or "native multi-part driver failed on another rank"
+            print(f"[bench] rank {dist.get_rank()}: native multi-part driver unavailable "
+                  f"({fallback}); using the Python driver", file=sys.stderr, flush=True)
+            mgm.USE_NATIVE_PARTS = False
+            s.u = pmg.DistField.zeros(s.lay, s.prob.nz)
     for _ in range(max(1, warmup)):          # graphs are captured for (f, u) here
         s.u, rep = pmg.mg_solve(s.f, s.hier, s.cfg, out=s.u)
         reps.append(rep)
@@ -446,7 +469,7 @@ def time_solves(s: Setup, steps, warmup, world, torch, sampler=None):
             "cycle_ms": cyc,
             "v_cycle_ms": t / sum(iters) * 1e3, "dof_s": s.prob.dof * steps / t,
             "residual_history": [float(x) for x in reps[-1].residual_history],
-            "launches": int(launches),
+            "launches": int(launches), "fallback": fallback,
             "driver": ("pmg_mg_solve (single part, lagged norm, wrap views)" if native else
                        "pmg_phier_mg_solve (multi-part: in-graph NCCL halos + reductions, "
                        "boundary-first overlap)" if parts else "python multi-part V-cycle")}
@@ -652,6 +675,8 @@ def main():
         "gpu_launches": r["launches"], "driver": r["driver"],
         "clocks": sampler.summary(),
     }
+    if r.get("fallback"):
+        out["driver_fallback"] = r["fallback"]
     if extra is not None:
         out["extra"] = extra
     if world == 1 and not args.no_cpu_baseline:

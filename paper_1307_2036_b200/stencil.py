@@ -131,6 +131,16 @@ class PanelOperator:
             call("pmg_apply_dot", self.handles[w].h, pf.ptr, q.parts[w].ptr, _ptr(scratch),
                  C.c_void_p(res.data_ptr() + 8 * n), st)
 
+    def assemble(self):
+        """Explicit sparse host matrix equal to the matrix-free operator
+        (stencil.py:182-232): a testing oracle for small grids only, refused
+        above ``ORACLE_CELL_CAP`` cells."""
+        n = self.grid.nx * self.grid.ny * self.grid.nz
+        if n > ORACLE_CELL_CAP:
+            raise ValueError(f"assembled-matrix oracle capped at {ORACLE_CELL_CAP} cells, "
+                             f"got {n}")
+        return _assemble_rows(self)
+
     def column_block(self, i: int, j: int) -> VerticalBlock:
         """Tridiagonal block of column (i, j) in global indices (stencil.py:167-180)."""
         nx, ny, nz = self.grid.nx, self.grid.ny, self.grid.nz
@@ -146,6 +156,62 @@ class PanelOperator:
             sub[1:] = coup
             sup[:-1] = coup
         return VerticalBlock(sub=sub, diag=diag, sup=sup)
+
+
+def _assemble_rows(op: "PanelOperator"):
+    """Host CSR matrix with the rows of the matrix-free operator: every
+    cell's diagonal and its (up to) six couplings taken from the cell's own
+    face weights, exactly the terms ``apply`` subtracts -- W/E faces
+    wx[i], wx[i+1], S/N faces wy[j], wy[j+1] (wrapping on a periodic grid,
+    zero-weight boundary faces dropped) and the vertical faces vprof[k],
+    vprof[k+1].  Unknowns are numbered nz * (ny * i + j) + k."""
+    import scipy.sparse as sp
+
+    g, f = op.grid, op.factors
+    nx, ny, nz = g.nx, g.ny, g.nz
+    n = nx * ny * nz
+    I, J, K = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    row = (nz * (ny * I + J) + K).ravel()
+    diag = (f.vh[:, :, None] * f.volprof[None, None, :]
+            + op.omega2 * f.sumw[:, :, None] * f.dr[None, None, :]
+            + op.vcoef * f.av[:, :, None] * (f.vprof[:-1] + f.vprof[1:])[None, None, :])
+    rows, cols, vals = [row], [row], [diag.ravel()]
+
+    def couple(weight, di, dj, dk):
+        """One neighbour direction: column ids of the neighbour cells and
+        -weight, for the cells that have that neighbour."""
+        ii, jj, kk = I + di, J + dj, K + dk
+        if g.periodic:
+            ii, jj = ii % nx, jj % ny
+        ok = ((ii >= 0) & (ii < nx) & (jj >= 0) & (jj < ny) & (kk >= 0) & (kk < nz)
+              & (weight != 0.0)).ravel()
+        rows.append(row[ok])
+        cols.append((nz * (ny * ii + jj) + kk).ravel()[ok])
+        vals.append(-weight.ravel()[ok])
+
+    drw = op.omega2 * f.dr[None, None, :]
+    one = np.ones((nx, ny, nz))
+    couple(f.wx[:-1, :, None] * drw, -1, 0, 0)
+    couple(f.wx[1:, :, None] * drw, +1, 0, 0)
+    couple(f.wy[:, :-1, None] * drw, 0, -1, 0)
+    couple(f.wy[:, 1:, None] * drw, 0, +1, 0)
+    vert = op.vcoef * f.av[:, :, None] * one
+    couple(vert * f.vprof[None, None, :-1], 0, 0, -1)
+    couple(vert * f.vprof[None, None, 1:], 0, 0, +1)
+    a = sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                      shape=(n, n))
+    return a.tocsr()
+
+
+#: largest grid (cells) ``assemble`` accepts (stencil.py:43)
+ORACLE_CELL_CAP = 100_000
+
+
+def assemble_matrix(grid: PanelGrid, params: ModelParameters):
+    """Sparse host matrix of the operator on a small grid (stencil.py:260-262):
+    the reference's testing oracle, kept for the same purpose -- no solver
+    path uses it."""
+    return PanelOperator(grid, params).assemble()
 
 
 def apply_operator(u, grid: PanelGrid, params: ModelParameters):
