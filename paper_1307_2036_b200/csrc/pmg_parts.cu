@@ -1156,6 +1156,25 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
         if (rc) return rc;
         TRYC(e, "multi-part hierarchy allocation");
     }
+    if (comm) {
+        // one exchange of the coarsest level (its iterate is zero: the ring
+        // stays zero) and one all-gather OUTSIDE any stream capture: NCCL
+        // sets up its connection to every neighbour rank on first use, and
+        // the first use would otherwise be inside the first cycle's capture
+        rc = PMG_OK;
+        if (nlev > 1) {
+            double *x[1] = {h->P[0][nlev - 1].u};
+            rc = exchange(h, nlev - 1, x, h->own);
+        }
+        if (!rc) rc = global_sum(h, h->slots + 1, h->own);
+        if (!rc && cudaStreamSynchronize(h->own) != cudaSuccess)
+            rc = err(PMG_ERR_CUDA, "communicator warm-up");
+        h->exchanges = 0;
+        if (rc) {
+            free_phier(h);
+            return rc;
+        }
+    }
     *out = h;
     return PMG_OK;
 }
