@@ -101,6 +101,15 @@ int pmg_from_ref_layout(const pmg_level *lvl, const double *src_dev, double *fie
                         void *stream);
 int pmg_to_ref_layout(const pmg_level *lvl, const double *field, double *dst_dev,
                       void *stream);
+/* the same for the columns i0 <= i < i1 only: i is the slowest index of the
+ * reference block, so the slab is the contiguous range [i0 ny nz, i1 ny nz)
+ * of src_dev / dst_dev (which still point at the whole block) -- a host
+ * transfer can be converted slab by slab while the next slab is in flight
+ * (pipeline.py). */
+int pmg_from_ref_layout_slab(const pmg_level *lvl, const double *src_dev, double *field, int i0,
+                             int i1, void *stream);
+int pmg_to_ref_layout_slab(const pmg_level *lvl, const double *field, double *dst_dev, int i0,
+                           int i1, void *stream);
 
 /* host (nx, ny, nz) reference-layout block <-> device field through a
  * device staging buffer of nx*ny*nz doubles (Field upload / download of

@@ -83,6 +83,8 @@ SIGNATURES = {
                            C.POINTER(_I), _P]),
     "pmg_from_ref_layout": (_I, [_P, _P, _P, _P]),
     "pmg_to_ref_layout": (_I, [_P, _P, _P, _P]),
+    "pmg_from_ref_layout_slab": (_I, [_P, _P, _P, C.c_int, C.c_int, _P]),
+    "pmg_to_ref_layout_slab": (_I, [_P, _P, _P, C.c_int, C.c_int, _P]),
     "pmg_apply": (_I, [_P, _P, _P, _P]),
     "pmg_residual": (_I, [_P, _P, _P, _P, _P, _P, _P]),
     "pmg_apply_dot": (_I, [_P, _P, _P, _P, _P, _P]),

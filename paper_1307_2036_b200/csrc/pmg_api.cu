@@ -60,10 +60,10 @@ cudaError_t launch_cg_direction(long long, const double *, const double *, const
                                 double *, cudaStream_t);
 cudaError_t launch_cg_update(const Lvl &, const double *, const double *, const double *,
                              const double *, double *, double *, double *, int *, cudaStream_t);
-cudaError_t launch_from_ref(const Lvl &, const double *, double *, cudaStream_t);
+cudaError_t launch_from_ref(const Lvl &, const double *, double *, int, int, cudaStream_t);
 cudaError_t launch_cg_up(long long, const double *, const double *, const double *, const double *,
                          const double *, double *, double *, cudaStream_t);
-cudaError_t launch_to_ref(const Lvl &, const double *, double *, cudaStream_t);
+cudaError_t launch_to_ref(const Lvl &, const double *, double *, int, int, cudaStream_t);
 }  // namespace pmg
 
 using namespace pmg;
@@ -365,13 +365,30 @@ int pmg_level_prepare(pmg_level *lv, void *stream) {
 
 int pmg_from_ref_layout(const pmg_level *lv, const double *src, double *field, void *st) {
     PMG_CHECK_LVL(lv);
-    PMG_CUDA(launch_from_ref(lv->L, src, field, (cudaStream_t)st), "from_ref_layout");
+    PMG_CUDA(launch_from_ref(lv->L, src, field, 0, lv->L.nx, (cudaStream_t)st),
+             "from_ref_layout");
     return PMG_OK;
 }
 
 int pmg_to_ref_layout(const pmg_level *lv, const double *field, double *dst, void *st) {
     PMG_CHECK_LVL(lv);
-    PMG_CUDA(launch_to_ref(lv->L, field, dst, (cudaStream_t)st), "to_ref_layout");
+    PMG_CUDA(launch_to_ref(lv->L, field, dst, 0, lv->L.nx, (cudaStream_t)st), "to_ref_layout");
+    return PMG_OK;
+}
+
+int pmg_from_ref_layout_slab(const pmg_level *lv, const double *src, double *field, int i0,
+                             int i1, void *st) {
+    PMG_CHECK_LVL(lv);
+    if (i0 < 0 || i1 > lv->L.nx || i0 > i1) return fail(PMG_ERR_VALUE, "slab out of range");
+    PMG_CUDA(launch_from_ref(lv->L, src, field, i0, i1, (cudaStream_t)st), "from_ref_layout");
+    return PMG_OK;
+}
+
+int pmg_to_ref_layout_slab(const pmg_level *lv, const double *field, double *dst, int i0, int i1,
+                           void *st) {
+    PMG_CHECK_LVL(lv);
+    if (i0 < 0 || i1 > lv->L.nx || i0 > i1) return fail(PMG_ERR_VALUE, "slab out of range");
+    PMG_CUDA(launch_to_ref(lv->L, field, dst, i0, i1, (cudaStream_t)st), "to_ref_layout");
     return PMG_OK;
 }
 
@@ -665,7 +682,8 @@ int pmg_field_upload(const pmg_level *lv, const double *host, double *field, dou
     const size_t n = (size_t)lv->L.nx * lv->L.ny * lv->L.nz;
     PMG_CUDA(cudaMemcpyAsync(staging, host, n * sizeof(double), cudaMemcpyHostToDevice,
                              (cudaStream_t)st), "field upload");
-    PMG_CUDA(launch_from_ref(lv->L, staging, field, (cudaStream_t)st), "field upload layout");
+    PMG_CUDA(launch_from_ref(lv->L, staging, field, 0, lv->L.nx, (cudaStream_t)st),
+             "field upload layout");
     return PMG_OK;
 }
 
@@ -674,7 +692,8 @@ int pmg_field_download(const pmg_level *lv, const double *field, double *host, d
     PMG_CHECK_LVL(lv);
     if (!host || !field || !staging) return fail(PMG_ERR_VALUE, "null buffer");
     const size_t n = (size_t)lv->L.nx * lv->L.ny * lv->L.nz;
-    PMG_CUDA(launch_to_ref(lv->L, field, staging, (cudaStream_t)st), "field download layout");
+    PMG_CUDA(launch_to_ref(lv->L, field, staging, 0, lv->L.nx, (cudaStream_t)st),
+             "field download layout");
     PMG_CUDA(cudaMemcpyAsync(host, staging, n * sizeof(double), cudaMemcpyDeviceToHost,
                              (cudaStream_t)st), "field download");
     return PMG_OK;

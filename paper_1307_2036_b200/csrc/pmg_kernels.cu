@@ -2505,33 +2505,37 @@ k_cg_update_v(Lvl L, const double *__restrict__ num, const double *__restrict__ 
 // layout conversion: reference (nx, ny, nz) k-fastest <-> split layout.
 // 32x32 (i, k) tiles through shared memory so both sides are coalesced.
 // ---------------------------------------------------------------------------
-__global__ void k_from_ref(Lvl L, const double *__restrict__ src, double *__restrict__ d) {
+// Columns ib <= i < ie only (a contiguous slab of the reference block: i is
+// its slowest index), so a host transfer can be converted slab by slab.
+__global__ void k_from_ref(Lvl L, const double *__restrict__ src, double *__restrict__ d, int ib,
+                           int ie) {
     __shared__ double tile[32][33];
-    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
+    const int i0 = ib + blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     for (int r = ty; r < 32; r += 8) {
         const int i = i0 + r, k = k0 + tx;
-        if (i < L.nx && k < L.nz) tile[r][tx] = src[((long long)i * L.ny + j) * L.nz + k];
+        if (i < ie && k < L.nz) tile[r][tx] = src[((long long)i * L.ny + j) * L.nz + k];
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
         const int i = i0 + tx, k = k0 + r;
-        if (i < L.nx && k < L.nz) d[cell(L, i, j, k)] = tile[tx][r];
+        if (i < ie && k < L.nz) d[cell(L, i, j, k)] = tile[tx][r];
     }
 }
 
-__global__ void k_to_ref(Lvl L, const double *__restrict__ d, double *__restrict__ dst) {
+__global__ void k_to_ref(Lvl L, const double *__restrict__ d, double *__restrict__ dst, int ib,
+                         int ie) {
     __shared__ double tile[32][33];
-    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
+    const int i0 = ib + blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
     const int tx = threadIdx.x, ty = threadIdx.y;
     for (int r = ty; r < 32; r += 8) {
         const int i = i0 + tx, k = k0 + r;
-        if (i < L.nx && k < L.nz) tile[tx][r] = d[cell(L, i, j, k)];
+        if (i < ie && k < L.nz) tile[tx][r] = d[cell(L, i, j, k)];
     }
     __syncthreads();
     for (int r = ty; r < 32; r += 8) {
         const int i = i0 + r, k = k0 + tx;
-        if (i < L.nx && k < L.nz) dst[((long long)i * L.ny + j) * L.nz + k] = tile[r][tx];
+        if (i < ie && k < L.nz) dst[((long long)i * L.ny + j) * L.nz + k] = tile[r][tx];
     }
 }
 
@@ -3498,15 +3502,21 @@ cudaError_t launch_cg_update(const Lvl &L, const double *num, const double *den,
     return cudaGetLastError();
 }
 
-cudaError_t launch_from_ref(const Lvl &L, const double *src, double *d, cudaStream_t st) {
+cudaError_t launch_from_ref(const Lvl &L, const double *src, double *d, int ib, int ie,
+                            cudaStream_t st) {
+    if (ie <= ib) return cudaSuccess;
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    k_from_ref<<<dim3((L.nx + 31) / 32, (L.nz + 31) / 32, L.ny), dim3(32, 8), 0, st>>>(L, src, d);
+    k_from_ref<<<dim3((ie - ib + 31) / 32, (L.nz + 31) / 32, L.ny), dim3(32, 8), 0, st>>>(
+        L, src, d, ib, ie);
     return cudaGetLastError();
 }
 
-cudaError_t launch_to_ref(const Lvl &L, const double *d, double *dst, cudaStream_t st) {
+cudaError_t launch_to_ref(const Lvl &L, const double *d, double *dst, int ib, int ie,
+                          cudaStream_t st) {
+    if (ie <= ib) return cudaSuccess;
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    k_to_ref<<<dim3((L.nx + 31) / 32, (L.nz + 31) / 32, L.ny), dim3(32, 8), 0, st>>>(L, d, dst);
+    k_to_ref<<<dim3((ie - ib + 31) / 32, (L.nz + 31) / 32, L.ny), dim3(32, 8), 0, st>>>(
+        L, d, dst, ib, ie);
     return cudaGetLastError();
 }
 

@@ -1111,3 +1111,57 @@ def test_mode_switch_recaptures_graphs(pmg, name):
     # and back: the fast mode is restored on the same buffers
     u3, rep3 = pmg.mg_solve(f, hier, cfg, out=u)
     assert rep3.iterations == rep.iterations
+
+
+@pytest.mark.parametrize("nx,ny,nz,slabs", [(64, 64, 32, 1), (128, 64, 32, 4), (256, 256, 128, 8)])
+def test_solve_pipeline_matches_direct(pmg, nx, ny, nz, slabs):
+    """SolvePipeline.run (pinned host blocks in, host solutions out, the
+    block converted slab by slab while the next slab is on the bus) returns
+    exactly what scatter_owned -> mg_solve -> gather_owned returns, for one
+    step per call and for a stream of steps; the slab entry points equal the
+    whole-block layout conversion."""
+    import ctypes as C
+    from paper_1307_2036_b200 import _lib
+    from paper_1307_2036_b200.pipeline import SolvePipeline
+    grid = pmg.periodic_box(nx, nz, 0.01, ny=ny)
+    params = pmg.toy_parameters(nx, nz, 1e-3, 1.0)
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=4, eps=1e-5)
+    hier = pmg.build_hierarchy(grid, params, cfg, pmg.Decomposition(nx, 1, ny=ny))
+    fs = [uni((nx, ny, nz), 40 + s) for s in range(3)]
+    direct = []
+    for fg in fs:
+        u, rep = pmg.mg_solve(field(pmg, fg, hier.fine.layout), hier, cfg)
+        direct.append((pmg.gather_owned(u), rep))
+    pipe = SolvePipeline(hier, cfg, nz, slabs=slabs, min_slab_bytes=1)
+    assert len(pipe.slabs) == slabs and pipe.slabs[0][0] == 0 and pipe.slabs[-1][1] == nx
+    fh = [torch.from_numpy(f).pin_memory() for f in fs]
+    uh = [torch.empty((nx, ny, nz), dtype=torch.float64).pin_memory() for _ in fs]
+    reps = pipe.run(fh, uh)                       # a stream of steps
+    for (ud, rd), u, r in zip(direct, uh, reps):
+        assert r.iterations == rd.iterations and r.residual_history == rd.residual_history
+        assert np.array_equal(u.numpy(), ud)
+    for k in range(3):                            # one step per call
+        uh[k].zero_()
+        (r,) = pipe.run([fh[k]], [uh[k]])
+        assert r.residual_history == direct[k][1].residual_history
+        assert np.array_equal(uh[k].numpy(), direct[k][0])
+    # slab entry points against the whole-block conversion
+    lay = hier.fine.layout
+    (w,) = lay.local_workers
+    a, b = pmg.DistField.zeros(lay, nz), pmg.DistField.zeros(lay, nz)
+    src = torch.from_numpy(fs[0]).cuda()
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    h = a.parts[w].geom.h
+    _lib.call("pmg_from_ref_layout", h, C.c_void_p(src.data_ptr()), a.parts[w].ptr, st)
+    for i0, i1 in ((0, 32), (32, 40), (40, nx)):
+        _lib.call("pmg_from_ref_layout_slab", h, C.c_void_p(src.data_ptr()), b.parts[w].ptr,
+                  i0, i1, st)
+    assert torch.equal(a.parts[w].data, b.parts[w].data)
+    back = torch.zeros_like(src)
+    for i0, i1 in ((0, 7), (7, 64), (64, nx)):
+        _lib.call("pmg_to_ref_layout_slab", h, a.parts[w].ptr, C.c_void_p(back.data_ptr()),
+                  i0, i1, st)
+    assert torch.equal(back, src)
+    with pytest.raises(ValueError):
+        _lib.call("pmg_to_ref_layout_slab", h, a.parts[w].ptr, C.c_void_p(back.data_ptr()),
+                  0, nx + 1, st)
