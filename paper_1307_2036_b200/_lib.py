@@ -185,3 +185,32 @@ def call(name: str, *args):
     rc = getattr(load(), name)(*args)
     check(rc, name)
     return rc
+
+
+# Library objects whose destruction was requested while the current stream
+# was being captured (a garbage-collected hierarchy or level inside a
+# ``torch.cuda.graph`` block): their cudaFree would invalidate the capture,
+# so they wait here until a destructor runs outside one.
+_PENDING: list = []
+
+
+def _capturing() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available() and torch.cuda.is_current_stream_capturing()
+    except Exception:                                   # interpreter shutdown
+        return False
+
+
+def destroy(name: str, handle) -> None:
+    """Call the destructor ``name`` on ``handle`` -- now, or once no stream
+    capture is under way."""
+    if _lib is None:
+        return
+    if _capturing():
+        _PENDING.append((name, handle))
+        return
+    while _PENDING:
+        n, h = _PENDING.pop()
+        getattr(_lib, n)(h)
+    getattr(_lib, name)(handle)

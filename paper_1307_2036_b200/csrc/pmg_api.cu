@@ -705,6 +705,13 @@ int pmg_ssor_apply(const pmg_level *lv, const double *r, double *z, double rho, 
     if (!(rho > 0.0 && rho < 2.0)) return fail(PMG_ERR_VALUE, "overrelaxation weight must lie in (0, 2)");
     if (rz_dev && !scratch) return fail(PMG_ERR_VALUE, "the <r, z> product needs a scratch buffer");
     int rc;
+    // the reference zero-fills z first (smoother.py:235-238).  That fill is
+    // dead work -- the first red half-sweep ignores z, the black one reads
+    // only the fresh red values -- unless a periodic level is one column
+    // wide: every cell is then its own neighbour through the wrap and the
+    // black half-sweep does read (copies of) black values
+    if ((periodic_x && lv->L.nx == 1) || (periodic_y && lv->L.ny == 1))
+        if ((rc = pmg_fill(lv, z, 0.0, st))) return rc;
     if (rz_dev && half_sweep_dot_ok(lv->L)) {
         // <r, z> fused into the two half-sweeps that produce final values:
         // black (final after the black sweep) and the last red sweep

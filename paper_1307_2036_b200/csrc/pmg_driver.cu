@@ -274,7 +274,11 @@ int replay_kind(pmg_hier *h, double *u, const double *f, int kind, cudaStream_t 
     int rc = body();
     cudaError_t e = cudaStreamEndCapture(st, &graph);
     if (rc) {
+        // a launch that failed inside the capture invalidates it: drop the
+        // graph and clear the error state, so the caller's next call starts
+        // clean (the failure itself is reported through rc)
         if (e == cudaSuccess) cudaGraphDestroy(graph);
+        cudaGetLastError();
         return rc;
     }
     TRYC(e, "capture end");
@@ -356,6 +360,13 @@ int pmg_hier_create(const pmg_level *const *levels, int nlev, const pmg_mg_desc 
                    (ny << c) != ny0) {
             return err(PMG_ERR_VALUE, "each level must halve nx and ny at equal nz");
         }
+        // a periodic level one column wide is its own neighbour: the fused
+        // cycle's identities (the black half-sweep reads no black value, the
+        // black residual after it is zero) fail there
+        if ((desc->periodic_x && nx == 1) || (desc->periodic_y && ny == 1))
+            return err(PMG_ERR_VALUE,
+                       "a periodic level one column wide is its own neighbour: use fewer "
+                       "levels (the Python driver runs the plain cycle on such hierarchies)");
     }
     pmg_hier *h = new pmg_hier();
     h->d = *desc;

@@ -878,14 +878,18 @@ constexpr int HS_THREADS = 128;
 template <bool UNI>
 __global__ void __launch_bounds__(HS_THREADS, 6)
 k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c, double rho,
-             int zero_start, int nbr_zero, double post_scale) {
+             int zero_start, int nbr_zero, double post_scale, int stage) {
+    // stage: bit 0 -- the old values (rho != 1) are staged in shared memory,
+    // bit 1 -- the pivots of a variable level are; tall columns that do not
+    // fit read them from HBM in the serial phase instead (half_sweep_stage)
     extern __shared__ double smem[];
     const int nz = L.nz;
     const bool need_old = !zero_start && rho != 1.0;
+    const bool st_old = need_old && (stage & 1), st_inv = !UNI && (stage & 2);
     double *s = smem;                                    // [nz][32]  rhs -> g
     double *so = s + nz * 32;                            // [nz][32]  u_old (rho != 1)
-    double *sinv = so + (need_old ? nz * 32 : 0);        // [nz][32]  pivots (variable)
-    double *tvp = sinv + (UNI ? 0 : nz * 32);            // [nz+1]    vprof
+    double *sinv = so + (st_old ? nz * 32 : 0);          // [nz][32]  pivots (variable)
+    double *tvp = sinv + (st_inv ? nz * 32 : 0);         // [nz+1]    vprof
     double *tinv = tvp + nz + 1;                         // [nz]      pivots (uniform)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int j = blockIdx.y;
@@ -927,8 +931,8 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
                 g = g + f[pc + ko];
             }
             s[k * 32 + lane] = g;
-            if (need_old) so[k * 32 + lane] = u[pc + ko];
-            if (!UNI) sinv[k * 32 + lane] = L.invd[pc + ko];
+            if (st_old) so[k * 32 + lane] = u[pc + ko];
+            if (st_inv) sinv[k * 32 + lane] = L.invd[pc + ko];
         }
     }
     __syncthreads();
@@ -936,14 +940,17 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
     double cv = L.csub0;
     if (!UNI) cv = L.vcoef * L.av[(long long)j * L.nx + i];
     // forward elimination (smoother.py:151-156)
-    double g = s[lane] * (UNI ? tinv[0] : sinv[lane]);
+    auto piv = [&](int k) {
+        return UNI ? tinv[k] : (st_inv ? sinv[k * 32 + lane] : L.invd[pc + (long long)k * pl]);
+    };
+    double g = s[lane] * piv(0);
     s[lane] = g;
 #pragma unroll 8
     for (int k = 1; k < nz; ++k) {
         double t = g * cv;
         t = t * tvp[k];
         g = s[k * 32 + lane] + t;
-        g = g * (UNI ? tinv[k] : sinv[k * 32 + lane]);
+        g = g * piv(k);
         s[k * 32 + lane] = g;
     }
     // back substitution (smoother.py:157-161) + relaxation (163-170)
@@ -955,7 +962,7 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
         if (k < nz - 1) {
             double t = x * cv;
             t = t * tvp[k + 1];
-            t = t * (UNI ? tinv[k] : sinv[k * 32 + lane]);
+            t = t * piv(k);
             x = s[k * 32 + lane] + t;
         }
         double y = x;
@@ -963,7 +970,7 @@ k_half_sweep(Lvl L, double *__restrict__ u, const double *__restrict__ f, int c,
             if (scale != 1.0) y = y * scale;
         } else if (rho != 1.0) {
             y = y * rho;
-            y = y + omr * so[k * 32 + lane];
+            y = y + omr * (st_old ? so[k * 32 + lane] : u[pc + (long long)k * pl]);
         }
         u[pc + (long long)k * pl] = y;
     }
@@ -2750,9 +2757,19 @@ cudaError_t launch_residual_restrict_red(const Lvl &F, const Lvl &C, const doubl
     return cudaGetLastError();
 }
 
-size_t half_sweep_smem(const Lvl &L, bool need_old) {
+constexpr size_t HS_SMEM_MAX = 200 * 1024;
+size_t half_sweep_smem(const Lvl &L, bool need_old, int stage = 3) {
     size_t n = (size_t)L.nz * 32;
-    return sizeof(double) * (n + (need_old ? n : 0) + (L.uniform ? 0 : n) + 2 * L.nz + 1);
+    return sizeof(double) * (n + ((need_old && (stage & 1)) ? n : 0) +
+                             ((!L.uniform && (stage & 2)) ? n : 0) + 2 * L.nz + 1);
+}
+// what the exact half-sweep stages in shared memory beside the right-hand
+// sides: everything when it fits (bits 0, 1), else the pivots stay in HBM,
+// then the old values too (columns of up to ~790 levels)
+int half_sweep_stage(const Lvl &L, bool need_old) {
+    for (int stage : {3, 1, 0})
+        if (half_sweep_smem(L, need_old, stage) <= HS_SMEM_MAX) return stage;
+    return 0;
 }
 
 
@@ -3003,6 +3020,12 @@ void setup_kernel_attributes() {
     static bool done = false;
     if (done) return;
     done = true;
+    // the exact half-sweep's opt-in shared memory (tall columns); set here so
+    // that its first launch may sit inside a stream capture
+    cudaFuncSetAttribute(k_half_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)HS_SMEM_MAX);
+    cudaFuncSetAttribute(k_half_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)HS_SMEM_MAX);
     bandv_attrs<2056>();
     band_attrs<1032>();
     band_attrs<520>();
@@ -3323,27 +3346,30 @@ static cudaError_t launch_half_sweep_k(const Lvl &L, double *u, const double *f,
         }
     }
     const bool need_old = !zero_start && rho != 1.0;
-    const size_t sm = half_sweep_smem(L, need_old);
+    const int stage = half_sweep_stage(L, need_old);
+    const size_t sm = half_sweep_smem(L, need_old, stage);
     const dim3 b(HS_THREADS);
     static bool attr_set[2] = {false, false};
     if (L.uniform) {
         if (!attr_set[0]) {
             cudaFuncSetAttribute(k_half_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024);
+                                 (int)HS_SMEM_MAX);
             cudaFuncSetAttribute(k_half_sweep<true>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             attr_set[0] = true;
         }
-        k_half_sweep<true><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
+        k_half_sweep<true><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale,
+                                             stage);
     } else {
         if (!attr_set[1]) {
             cudaFuncSetAttribute(k_half_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 200 * 1024);
+                                 (int)HS_SMEM_MAX);
             cudaFuncSetAttribute(k_half_sweep<false>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
             attr_set[1] = true;
         }
-        k_half_sweep<false><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero, post_scale);
+        k_half_sweep<false><<<g, b, sm, st>>>(L, u, f, color, rho, zero_start, nbr_zero,
+                                              post_scale, stage);
     }
     return cudaGetLastError();
 }

@@ -626,7 +626,11 @@ int replay(pmg_phier *h, double *const *u, const double *const *f, int kind, cud
     int rc = body();
     cudaError_t e = cudaStreamEndCapture(s, &graph);
     if (rc) {
+        // a launch that failed inside the capture invalidates it: drop the
+        // graph and clear the error state, so the caller's next call starts
+        // clean (the failure itself is reported through rc)
         if (e == cudaSuccess) cudaGraphDestroy(graph);
+        cudaGetLastError();
         return rc;
     }
     TRYC(e, "capture end");
@@ -1124,6 +1128,14 @@ int pmg_phier_create(const pmg_level *const *levels, int nlev, int nparts,
             }
             if (p && (q.nx != r0.nx || q.ny != r0.ny || q.nz != r0.nz)) {
                 rc = err(PMG_ERR_VALUE, "all parts of a level must have the same shape");
+                break;
+            }
+            // a part that is its own neighbour across a side one column
+            // wide couples every cell to itself (see pmg_hier_create)
+            if ((q.nx == 1 && (h->nbr[p][0] == h->worker[p] || h->nbr[p][1] == h->worker[p])) ||
+                (q.ny == 1 && (h->nbr[p][2] == h->worker[p] || h->nbr[p][3] == h->worker[p]))) {
+                rc = err(PMG_ERR_VALUE, "a periodic level one column wide is its own neighbour: "
+                                        "use fewer levels");
                 break;
             }
             const long long nd = pmg_level_field_doubles(q.lv);

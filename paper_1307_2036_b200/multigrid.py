@@ -19,12 +19,12 @@ from __future__ import annotations
 import ctypes as C
 import math
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, replace
 
 import numpy as np
 import torch
 
-from ._lib import MGDesc, PartDesc, call, load
+from ._lib import MGDesc, PartDesc, call, destroy, load
 from .geometry import PanelGrid
 from .krylov import SolveReport
 from .params import ModelParameters, is_power_of_two
@@ -208,7 +208,7 @@ class NativeHierarchy:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            self._lib.pmg_hier_destroy(h)
+            destroy("pmg_hier_destroy", h)
             self.h = None
 
     def graph_launches(self, f_ptr: int, u_ptr: int, first: bool) -> int:
@@ -261,7 +261,7 @@ class NativePartsHierarchy:
     def __del__(self):
         h = getattr(self, "h", None)
         if h is not None and h.value:
-            self._lib.pmg_phier_destroy(h)
+            destroy("pmg_phier_destroy", h)
             self.h = None
 
     def replayed_launches(self) -> int:
@@ -393,6 +393,26 @@ def _residual_restrict(lev: Level, coarse: Level, f: DistField, u: DistField,
         call(name, h, coarse.op.handles[w].h, f.parts[w].ptr, uf.ptr, cf.parts[w].ptr, st)
 
 
+def self_coupled(hier: LevelHierarchy) -> bool:
+    """A periodic level one column wide (nx = 1 or ny = 1 of a rectangular
+    periodic grid coarsened far enough) makes every cell its own neighbour
+    through the wrap.  The identities the fused cycle rests on -- the black
+    half-sweep never reads black values, the black residual after an exact
+    black line solve is zero -- do not hold there."""
+    return any(lev.grid.periodic and (lev.grid.nx == 1 or lev.grid.ny == 1)
+               for lev in hier.levels)
+
+
+def plain_if_self_coupled(hier: LevelHierarchy, cfg: MGConfig) -> MGConfig:
+    """The cycle configuration the drivers run: ``cfg``, or -- on a
+    hierarchy with a self-coupled level -- the reference's plain op sequence
+    (zero fills, full prolongation, full residual and restriction, the
+    separate convergence norm), which needs none of those identities."""
+    if (cfg.fused or cfg.lagged_norm or cfg.red_restrict) and self_coupled(hier):
+        return replace(cfg, fused=False, lagged_norm=False, red_restrict=False)
+    return cfg
+
+
 def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
             first: bool = False) -> None:
     """One V-cycle on ``scratch[c].u`` (halo-consistent on entry), Alg. 1.
@@ -404,6 +424,8 @@ def v_cycle(hier: LevelHierarchy, cfg: MGConfig, scratch, c: int = 0,
     prolongation into red cells (the post-smoothing red half-sweep overwrites
     them without reading them).
     """
+    if c == 0:
+        cfg = plain_if_self_coupled(hier, cfg)
     with nvtx_range(f"level {c}"):
         _v_cycle_level(hier, cfg, scratch, c, first)
 
@@ -607,6 +629,7 @@ def mg_solve(f: DistField, hier: LevelHierarchy, cfg: MGConfig, out: DistField |
     the first cycle starts from zero without a fill (its first red
     half-sweep ignores u, exactly as f + drw*0 = f).
     """
+    cfg = plain_if_self_coupled(hier, cfg)
     use_graph = cfg.graph and _dist() is None
     single = hier.fine.layout.px == 1 and hier.fine.layout.py == 1 and _dist() is None
     if (use_graph and cfg.fused and USE_NATIVE and single):

@@ -271,7 +271,8 @@ class LevelHandle:
     def __del__(self):
         try:
             if self.h:
-                lib().pmg_level_destroy(self.h)
+                from ._lib import destroy
+                destroy("pmg_level_destroy", self.h)
                 self.h = None
         except Exception:
             pass

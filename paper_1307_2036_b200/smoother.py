@@ -134,6 +134,8 @@ class LineSmoother:
         # dead work here: the first red half-sweep ignores z (neighbours zero,
         # zero start), the black one reads only the fresh red values
         z = DistField.zeros(self.op.layout, self.op.nz) if out is None else out
+        if out is not None and getattr(self.op, "self_coupled", False):
+            z.fill(0.0)      # not dead there: the black half-sweep reads copies of black
         self.half_sweep_exchange(z, r, RED, rho, zero_start=True, neighbors_zero=True)
         self.half_sweep_exchange(z, r, BLACK, rho, zero_start=True, post_scale=2.0 - rho)
         self.half_sweep_exchange(z, r, RED, rho)

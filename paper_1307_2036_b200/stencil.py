@@ -73,6 +73,13 @@ class PanelOperator:
         return self.grid.nz
 
     @property
+    def self_coupled(self) -> bool:
+        """A periodic grid one column wide: every cell is its own neighbour
+        through the wrap, so the red-black identities the fused paths rest
+        on (a half-sweep never reads its own colour) do not hold."""
+        return bool(self.grid.periodic) and (self.grid.nx == 1 or self.grid.ny == 1)
+
+    @property
     def uniform(self) -> bool:
         return all(h.uniform for h in self.handles.values())
 

@@ -1,0 +1,148 @@
+"""Randomised parity sweep of the device path against the numpy oracle
+(oracle/port.py): random grid shapes (nx, ny powers of two, any nz; periodic boxes and the
+reference's flat zero-flux box), level counts, coefficients (omega^2, lambda^2, graded levels, omega^2(x, y)),
+cycle shapes (nu_pre, nu_post, coarse sweeps, rho), in-process
+decompositions (px x py parts), driver switches (lagged norm, red-only
+restriction, overlap, graphs, exact / fast smoother) -- MG and SSOR-CG
+solves must give the oracle's iteration count, history (1e-8) and field
+(1e-8).  A measurement tool (like the other files here), not part of the
+package or the test suite:
+
+    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--max-cells 3e6]
+"""
+import argparse
+import os
+import sys
+import time
+import traceback
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def draw(rng, max_cells):
+    while True:
+        nx = int(2 ** rng.integers(0 if rng.random() < 0.15 else 2, 10))
+        ny = int(2 ** rng.integers(0 if rng.random() < 0.3 else 2, 10)) \
+            if rng.random() < 0.35 else nx
+        nz = int(rng.choice([1, 2, 3, 8, 16, 17, 32, 33, 48, 64, 80, 96, 100, 127, 128, 128, 128,
+                             129, 160, 255, 256, 257, 300]))
+        if nx * ny * nz <= max_cells:
+            break
+    maxlev = int(np.log2(min(nx, ny))) + 1
+    nlev = int(rng.integers(1, maxlev + 1))
+    c = dict(nx=nx, ny=ny, nz=nz, nlev=nlev,
+             omega2=float(10 ** rng.uniform(-4, -1)), lambda2=float(rng.choice([0.1, 1.0, 10.0])),
+             variable=bool(rng.random() < 0.3), stretch=bool(rng.random() < 0.3),
+             nu_pre=int(rng.choice([1, 1, 2])), nu_post=int(rng.choice([1, 1, 2])),
+             coarse=int(rng.choice([1, 1, 2, 3])), rho=float(rng.choice([1.0, 1.0, 1.0, 0.8, 1.3])),
+             lagged=bool(rng.random() < 0.7), red=bool(rng.random() < 0.7),
+             overlap=bool(rng.random() < 0.5), graph=bool(rng.random() < 0.8),
+             exact=bool(rng.random() < 0.25), seed=int(rng.integers(1, 1 << 30)))
+    # in-process parts: px x py with >= 2 columns per part side on the coarsest level
+    opts = [(1, 1)]
+    for px, py in ((2, 1), (1, 2), (2, 2), (4, 2), (4, 4)):
+        if nx % px == 0 and ny % py == 0 and (nx // px) >> (nlev - 1) >= 2 \
+                and (ny // py) >> (nlev - 1) >= 2:
+            opts.append((px, py))
+    c["px"], c["py"] = opts[int(rng.integers(0, len(opts)))] if rng.random() < 0.5 else (1, 1)
+    # the reference's own boundary: flat zero-flux box (square, mirror halos)
+    c["mirror"] = bool(nx == ny and not c["variable"] and rng.random() < 0.25)
+    return c
+
+
+def run_case(pmg, port, c):
+    nx, ny, nz = c["nx"], c["ny"], c["nz"]
+    lv = (port.graded_levels(nz, 0.01, 1.05) if c["stretch"] and nz > 1
+          else port.uniform_levels(nz, 0.01))
+    shape = port.omega_profile_config4 if c["variable"] else None
+    fg = np.random.default_rng(c["seed"]).uniform(-1.0, 1.0, (nx, ny, nz))
+    mirror = c.get("mirror", False)
+    if mirror:
+        h = port.Hierarchy(nx, ny, c["nlev"], lambda a, b: port.flat_neumann_factors(a, lv),
+                           c["omega2"], c["lambda2"], periodic=(False, False))
+    else:
+        h = port.Hierarchy(nx, ny, c["nlev"], lambda a, b: port.config_factors(a, b, lv, shape),
+                           c["omega2"], c["lambda2"])
+    ou, orep = port.mg_solve(h, fg, eps=1e-6, maxiter=60, nu_pre=c["nu_pre"],
+                             nu_post=c["nu_post"], coarse_sweeps=c["coarse"], rho=c["rho"])
+    if mirror:
+        grid = pmg.panel_grid(nx, nz, depth=0.01, flat_mode=True, levels=lv)
+    else:
+        grid = pmg.periodic_box(nx, nz, 0.01, lv, ny=ny,
+                                omega_shape=pmg.geometry.omega_shape_config4 if c["variable"]
+                                else None)
+    params = pmg.toy_parameters(nx, nz, c["omega2"], c["lambda2"])
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=c["nlev"], eps=1e-6, maxiter=60,
+                       nu_pre=c["nu_pre"], nu_post=c["nu_post"], coarse_sweeps=c["coarse"],
+                       rho=c["rho"], lagged_norm=c["lagged"], red_restrict=c["red"],
+                       overlap=c["overlap"], graph=c["graph"])
+    dec = pmg.Decomposition(nx, c["px"] * c["py"], ny=ny, px=c["px"], py=c["py"],
+                            periodic=not mirror)
+    hier = pmg.build_hierarchy(grid, params, cfg, dec)
+    f = pmg.scatter_owned(fg, hier.fine.layout)
+    tol = 1e-10 if c["exact"] else 1e-8
+    with pmg.exact_smoother(c["exact"]):
+        u, rep = pmg.mg_solve(f, hier, cfg)
+        u2, rep2 = pmg.mg_solve(f, hier, cfg)          # cached graphs / red-array parity
+    assert rep.iterations == orep.iterations, ("mg iterations", rep.iterations, orep.iterations)
+    assert rep.converged == orep.converged
+    hh, ref = np.array(rep.residual_history), np.array(orep.residual_history)
+    assert np.all(np.abs(hh - ref) <= tol * ref + 1e-13 * ref[0]), ("mg history", hh, ref)
+    assert rep2.residual_history == rep.residual_history, "second solve differs"
+    ug = pmg.gather_owned(u)
+    assert np.array_equal(ug, pmg.gather_owned(u2)), "second solve's field differs"
+    scale = max(1e-300, float(np.max(np.abs(ou))))
+    err = float(np.max(np.abs(ug - ou[1:-1, 1:-1, :]))) / scale
+    assert err <= tol, ("mg field", err)
+    # SSOR-CG on the fine level (single part or parts)
+    if c["rho"] == 1.0:
+        oc, crep = port.pcg_solve(h.levels[0], fg, eps=1e-6, maxiter=400)
+        op = hier.fine.op
+        with pmg.exact_smoother(c["exact"]):
+            uc, rc = pmg.pcg_solve(f, op, pmg.SSORPreconditioner(pmg.LineSmoother(op)),
+                                   eps=1e-6, maxiter=400)
+        assert rc.converged == crep.converged
+        assert abs(rc.iterations - crep.iterations) <= (0 if c["exact"] else 1), \
+            ("cg iterations", rc.iterations, crep.iterations)
+        n = min(len(rc.residual_history), len(crep.residual_history))
+        hh, ref = np.array(rc.residual_history[:n]), np.array(crep.residual_history[:n])
+        assert np.all(np.abs(hh - ref) <= 1e-6 * ref + 1e-12 * ref[0]), ("cg history", hh, ref)
+    return err
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cases", type=int, default=200)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--max-cells", type=float, default=3e6)
+    ap.add_argument("--budget-s", type=float, default=1e9)
+    args = ap.parse_args()
+    import paper_1307_2036_b200 as pmg
+    from oracle import port
+    rng = np.random.default_rng(args.seed)
+    bad, t0, worst, done = [], time.time(), 0.0, 0
+    for n in range(args.cases):
+        if time.time() - t0 > args.budget_s:
+            break
+        c = draw(rng, args.max_cells)
+        try:
+            worst = max(worst, run_case(pmg, port, c))
+        except Exception as e:                      # noqa: BLE001 -- reported
+            bad.append((c, repr(e)[:400]))
+            print("FAIL", c, "\n   ", repr(e)[:400], flush=True)
+            if not isinstance(e, AssertionError):
+                traceback.print_exc()
+        done += 1
+        if (n + 1) % 20 == 0:
+            print(f"{n + 1} cases, {len(bad)} failures, worst field error {worst:.2e}, "
+                  f"{time.time() - t0:.0f} s", flush=True)
+    print(f"fuzz: {done} cases, {len(bad)} failures, worst relative field error {worst:.2e}, "
+          f"seed {args.seed}")
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
