@@ -8,7 +8,7 @@ solves must give the oracle's iteration count, history (1e-8) and field
 (1e-8).  A measurement tool (like the other files here), not part of the
 package or the test suite:
 
-    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--max-cells 3e6]
+    python tools/fuzz_parity.py [--cases 200] [--seed 1] [--max-cells 3e6] [--min-cells 0]
 """
 import argparse
 import os
@@ -22,21 +22,21 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def draw(rng, max_cells):
+def draw(rng, max_cells, min_cells=0):
     while True:
         nx = int(2 ** rng.integers(0 if rng.random() < 0.15 else 2, 10))
         ny = int(2 ** rng.integers(0 if rng.random() < 0.3 else 2, 10)) \
             if rng.random() < 0.35 else nx
         nz = int(rng.choice([1, 2, 3, 8, 16, 17, 32, 33, 48, 64, 80, 96, 100, 127, 128, 128, 128,
                              129, 160, 255, 256, 257, 300]))
-        if nx * ny * nz <= max_cells:
+        if min_cells <= nx * ny * nz <= max_cells:
             break
     maxlev = int(np.log2(min(nx, ny))) + 1
     nlev = int(rng.integers(1, maxlev + 1))
     c = dict(nx=nx, ny=ny, nz=nz, nlev=nlev,
              omega2=float(10 ** rng.uniform(-4, -1)), lambda2=float(rng.choice([0.1, 1.0, 10.0])),
              variable=bool(rng.random() < 0.3), stretch=bool(rng.random() < 0.3),
-             nu_pre=int(rng.choice([1, 1, 2])), nu_post=int(rng.choice([1, 1, 2])),
+             nu_pre=int(rng.choice([1, 1, 1, 2, 0])), nu_post=int(rng.choice([1, 1, 2])),
              coarse=int(rng.choice([1, 1, 2, 3])), rho=float(rng.choice([1.0, 1.0, 1.0, 0.8, 1.3])),
              lagged=bool(rng.random() < 0.7), red=bool(rng.random() < 0.7),
              overlap=bool(rng.random() < 0.5), graph=bool(rng.random() < 0.8),
@@ -50,6 +50,9 @@ def draw(rng, max_cells):
     c["px"], c["py"] = opts[int(rng.integers(0, len(opts)))] if rng.random() < 0.5 else (1, 1)
     # the reference's own boundary: flat zero-flux box (square, mirror halos)
     c["mirror"] = bool(nx == ny and not c["variable"] and rng.random() < 0.25)
+    # stopping rule: the usual 1e-6 in 60 cycles, a loose one, or a cycle cap
+    c["eps"], c["maxiter"] = [(1e-6, 60), (1e-6, 60), (1e-3, 60), (1e-6, 1), (1e-6, 2),
+                              (1e-6, 3)][int(rng.integers(0, 6))]
     return c
 
 
@@ -66,8 +69,10 @@ def run_case(pmg, port, c):
     else:
         h = port.Hierarchy(nx, ny, c["nlev"], lambda a, b: port.config_factors(a, b, lv, shape),
                            c["omega2"], c["lambda2"])
-    ou, orep = port.mg_solve(h, fg, eps=1e-6, maxiter=60, nu_pre=c["nu_pre"],
+    eps, maxiter = c.get("eps", 1e-6), c.get("maxiter", 60)
+    ou, orep = port.mg_solve(h, fg, eps=eps, maxiter=maxiter, nu_pre=c["nu_pre"],
                              nu_post=c["nu_post"], coarse_sweeps=c["coarse"], rho=c["rho"])
+    ou = ou.copy()
     if mirror:
         grid = pmg.panel_grid(nx, nz, depth=0.01, flat_mode=True, levels=lv)
     else:
@@ -75,7 +80,7 @@ def run_case(pmg, port, c):
                                 omega_shape=pmg.geometry.omega_shape_config4 if c["variable"]
                                 else None)
     params = pmg.toy_parameters(nx, nz, c["omega2"], c["lambda2"])
-    cfg = pmg.MGConfig(policy="explicit", explicit_levels=c["nlev"], eps=1e-6, maxiter=60,
+    cfg = pmg.MGConfig(policy="explicit", explicit_levels=c["nlev"], eps=eps, maxiter=maxiter,
                        nu_pre=c["nu_pre"], nu_post=c["nu_post"], coarse_sweeps=c["coarse"],
                        rho=c["rho"], lagged_norm=c["lagged"], red_restrict=c["red"],
                        overlap=c["overlap"], graph=c["graph"])
@@ -98,6 +103,22 @@ def run_case(pmg, port, c):
     with pmg.exact_smoother(c["exact"]):
         u, rep = pmg.mg_solve(f, hier, cfg)
         u2, rep2 = pmg.mg_solve(f, hier, cfg)          # cached graphs / red-array parity
+        # another right-hand side through the same buffers and graphs
+        fg3 = np.random.default_rng(c["seed"] + 1).uniform(-1.0, 1.0, (nx, ny, nz))
+        f3 = pmg.scatter_owned(fg3, hier.fine.layout)
+        for w in f.parts:
+            f.parts[w].data.copy_(f3.parts[w].data)
+        ubuf = pmg.DistField.zeros(hier.fine.layout, nz)
+        _, rep3a = pmg.mg_solve(f, hier, cfg, out=ubuf)
+        f4 = pmg.scatter_owned(fg, hier.fine.layout)
+        for w in f.parts:
+            f.parts[w].data.copy_(f4.parts[w].data)
+        _, rep3b = pmg.mg_solve(f, hier, cfg, out=ubuf)
+    o3, orep3 = port.mg_solve(h, fg3, eps=eps, maxiter=maxiter, nu_pre=c["nu_pre"],
+                              nu_post=c["nu_post"], coarse_sweeps=c["coarse"], rho=c["rho"])
+    assert rep3a.iterations == orep3.iterations, ("second rhs", rep3a.iterations, orep3.iterations)
+    assert rep3b.residual_history == rep.residual_history, "solve into out= differs"
+    assert np.array_equal(pmg.gather_owned(ubuf), pmg.gather_owned(u)), "out= field differs"
     assert rep.iterations == orep.iterations, ("mg iterations", rep.iterations, orep.iterations)
     assert rep.converged == orep.converged
     assert rep2.residual_history == rep.residual_history, "second solve differs"
@@ -147,6 +168,7 @@ def main():
     ap.add_argument("--cases", type=int, default=200)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-cells", type=float, default=3e6)
+    ap.add_argument("--min-cells", type=float, default=0)
     ap.add_argument("--budget-s", type=float, default=1e9)
     args = ap.parse_args()
     import paper_1307_2036_b200 as pmg
@@ -156,7 +178,7 @@ def main():
     for n in range(args.cases):
         if time.time() - t0 > args.budget_s:
             break
-        c = draw(rng, args.max_cells)
+        c = draw(rng, args.max_cells, args.min_cells)
         try:
             worst = max(worst, run_case(pmg, port, c))
         except Exception as e:                      # noqa: BLE001 -- reported
