@@ -320,7 +320,14 @@ typedef struct pmg_mg_desc {
      * and nu_pre >= 1, ignored otherwise. */
     int red_restrict;
 } pmg_mg_desc;
-/* levels[0] finest ... levels[nlev-1] coarsest, each halving nx and ny */
+/* levels[0] finest ... levels[nlev-1] coarsest, each halving nx and ny.
+ * PMG_ERR_VALUE for a periodic axis along which some level is one column
+ * wide: every cell is then its own neighbour through the wrap, and the
+ * red-black identities this driver's cycle rests on (no zero fill of the
+ * coarse iterates, black-only prolongation, red-only restriction, the lagged
+ * norm) do not hold -- use fewer levels, or the Python driver, which runs
+ * the reference's plain op sequence on such hierarchies.  The multi-part
+ * pmg_phier_create refuses them likewise. */
 int pmg_hier_create(const pmg_level *const *levels, int nlev, const pmg_mg_desc *desc,
                     pmg_hier **out);
 int pmg_hier_destroy(pmg_hier *hier);
