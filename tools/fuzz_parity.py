@@ -53,6 +53,13 @@ def draw(rng, max_cells, min_cells=0):
     # stopping rule: the usual 1e-6 in 60 cycles, a loose one, or a cycle cap
     c["eps"], c["maxiter"] = [(1e-6, 60), (1e-6, 60), (1e-3, 60), (1e-6, 1), (1e-6, 2),
                               (1e-6, 3)][int(rng.integers(0, 6))]
+    # the reference's level policies on square worker grids, with folding
+    # (collect / distribute) below l_split where the policy goes deep enough
+    c["policy"] = None
+    if nx == ny and nx >= 8 and rng.random() < 0.2:
+        c["policy"] = str(rng.choice(["standard", "shallow", "very_shallow"]))
+        side = int(rng.choice([s for s in (1, 2, 4) if nx // s >= 2]))
+        c["px"] = c["py"] = side
     return c
 
 
@@ -63,6 +70,17 @@ def run_case(pmg, port, c):
     shape = port.omega_profile_config4 if c["variable"] else None
     fg = np.random.default_rng(c["seed"]).uniform(-1.0, 1.0, (nx, ny, nz))
     mirror = c.get("mirror", False)
+    policy = c.get("policy")
+    if policy:
+        # level count and coarse sweeps as the policy resolves them
+        probe = pmg.MGConfig(policy=policy)
+        grid0 = (pmg.panel_grid(nx, nz, depth=0.01, flat_mode=True, levels=lv) if mirror
+                 else pmg.periodic_box(nx, nz, 0.01, lv))
+        hp = pmg.build_hierarchy(grid0, pmg.toy_parameters(nx, nz, c["omega2"], c["lambda2"]),
+                                 probe, pmg.Decomposition(nx, c["px"] * c["py"], ny=ny, px=c["px"],
+                                                          py=c["py"], periodic=not mirror))
+        c = dict(c, nlev=len(hp.levels), coarse=probe.resolved_coarse_sweeps())
+        del hp
     if mirror:
         h = port.Hierarchy(nx, ny, c["nlev"], lambda a, b: port.flat_neumann_factors(a, lv),
                            c["omega2"], c["lambda2"], periodic=(False, False))
@@ -80,8 +98,10 @@ def run_case(pmg, port, c):
                                 omega_shape=pmg.geometry.omega_shape_config4 if c["variable"]
                                 else None)
     params = pmg.toy_parameters(nx, nz, c["omega2"], c["lambda2"])
-    cfg = pmg.MGConfig(policy="explicit", explicit_levels=c["nlev"], eps=eps, maxiter=maxiter,
-                       nu_pre=c["nu_pre"], nu_post=c["nu_post"], coarse_sweeps=c["coarse"],
+    cfg = pmg.MGConfig(policy=policy or "explicit",
+                       explicit_levels=None if policy else c["nlev"], eps=eps, maxiter=maxiter,
+                       nu_pre=c["nu_pre"], nu_post=c["nu_post"],
+                       coarse_sweeps=None if policy else c["coarse"],
                        rho=c["rho"], lagged_norm=c["lagged"], red_restrict=c["red"],
                        overlap=c["overlap"], graph=c["graph"])
     dec = pmg.Decomposition(nx, c["px"] * c["py"], ny=ny, px=c["px"], py=c["py"],
