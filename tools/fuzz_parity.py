@@ -147,6 +147,7 @@ def run_case(pmg, port, c):
     scale = max(1e-300, float(np.max(np.abs(ou))))
     err = float(np.max(np.abs(ug - ou[1:-1, 1:-1, :]))) / scale
     assert err <= tol, ("mg field", err, cond)
+    c["_cond"] = cond
 
     def noise(dev_field, ref_field):
         """||A (u_dev - u_ref)||: what a field difference of rounding size
@@ -190,6 +191,8 @@ def main():
     ap.add_argument("--max-cells", type=float, default=3e6)
     ap.add_argument("--min-cells", type=float, default=0)
     ap.add_argument("--budget-s", type=float, default=1e9)
+    ap.add_argument("--report", type=float, default=1e-9,
+                    help="print cases whose field error exceeds this")
     args = ap.parse_args()
     import paper_1307_2036_b200 as pmg
     from oracle import port
@@ -200,7 +203,12 @@ def main():
             break
         c = draw(rng, args.max_cells, args.min_cells)
         try:
-            worst = max(worst, run_case(pmg, port, c))
+            e = run_case(pmg, port, c)
+            if e > args.report:
+                print(f"outlier: field error {e:.2e}, column-block condition "
+                      f"{c.get('_cond', 0):.1e}, exact {c['exact']}, mirror {c['mirror']}, "
+                      f"nz {c['nz']}, lambda2 {c['lambda2']}, stretch {c['stretch']}", flush=True)
+            worst = max(worst, e)
         except Exception as e:                      # noqa: BLE001 -- reported
             bad.append((c, repr(e)[:400]))
             print("FAIL", c, "\n   ", repr(e)[:400], flush=True)
